@@ -1,0 +1,185 @@
+/*
+ * dpq.h — C ABI of libdpq.so, the B200 (sm_100a) implementation of the
+ * two-pass derived-codebook PQ search of arXiv 1905.06900.
+ *
+ * The reference (`derivedpq`, /root/reference/pkg) is pure Python/numpy and
+ * has no FFI layer; its drop-in boundary is the public search API:
+ *
+ *   FlatIndex.search(Y, r, mode, r2, capped, return_timings)   flat.py:54-108
+ *   IVFIndex.search(Y, r, ma, mode, r2, capped, return_timings) ivf.py:125-160
+ *
+ * Every entry point below replaces the arithmetic of one of those calls (or of
+ * one of the unit-level seams the reference tests call), with plain pointers
+ * and sizes, no torch types.  Argument validation that produces the
+ * reference's Python exceptions stays in the Python mirror
+ * (paper_1905_06900_b200/flat.py, ivf.py); the C side returns a status code
+ * and a thread-local message (dpq_last_error).
+ *
+ * Conventions
+ *  - All host pointers are plain C-contiguous arrays.  "_dev" variants take
+ *    device pointers on the index's device and run on the index's stream.
+ *  - Codes are (n, m) little-endian uint8 (b <= 8) or uint16 (b <= 16),
+ *    row-major, exactly quantizer.py:78 / :169.
+ *  - Results are (nq, r) float64 distances padded with +inf and int64 ids
+ *    padded with -1 (flat.py:16-29).
+ *  - Return value: DPQ_OK (0) or a DPQ_ERR_* code; dpq_last_error() explains.
+ */
+#ifndef DPQ_H_
+#define DPQ_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DPQ_OK 0
+#define DPQ_ERR_ARG 1    /* invalid argument (maps to ValueError)      */
+#define DPQ_ERR_CUDA 2   /* CUDA runtime / kernel failure              */
+#define DPQ_ERR_NOMEM 3  /* device or pinned allocation failed         */
+#define DPQ_ERR_STATE 4  /* wrong index kind / not initialised         */
+
+typedef struct dpq_index dpq_index_t;
+
+/* Thread-local description of the last failure on this thread. */
+const char* dpq_last_error(void);
+/* ABI version (bumped on any signature change). */
+int dpq_abi_version(void);
+/* Number of visible CUDA devices (0 on a CPU-only host, never an error). */
+int dpq_device_count(void);
+
+/* ---------------------------------------------------------------- flat --
+ * Replaces the fitted state FlatIndex holds after fit (flat.py:45-52):
+ * quantizer.codebooks_ (m,k,dsub) f32, quantizer.derived_codebooks_
+ * (m,kbar,dsub) f32 and codes_ (n,m).  The handle owns device copies; the
+ * caller's buffers may be freed after the call.  id_base is added to every
+ * returned id (0 for an unsharded index; the shard's first global row when a
+ * database is split across GPUs).
+ * prefix_codes/n_prefix: the rows qmax is estimated from
+ * (twopass.py:83-84 uses codes[:min(r2,n)]).  Pass NULL/0 to use the
+ * handle's own first rows; a shard passes the replicated global prefix.    */
+int dpq_flat_create(int device, int m, int k, int kbar, int dsub,
+                    const float* codebooks, const float* derived_codebooks,
+                    const void* codes, int code_bytes, int64_t n,
+                    int64_t id_base, const void* prefix_codes,
+                    int64_t n_prefix, dpq_index_t** out);
+
+/* ----------------------------------------------------------------- ivf --
+ * Replaces IVFIndex's fitted state (ivf.py:63-103): centers_ (K,d) f32,
+ * offsets_ (K+1) i64, sorted_codes_ (n,m), sorted_ids_ (n) i64, plus the
+ * residual quantizer's codebooks.                                         */
+int dpq_ivf_create(int device, int m, int k, int kbar, int dsub,
+                   const float* codebooks, const float* derived_codebooks,
+                   int n_cells, const float* centers, const int64_t* offsets,
+                   const void* sorted_codes, int code_bytes,
+                   const int64_t* sorted_ids, int64_t n, dpq_index_t** out);
+
+void dpq_destroy(dpq_index_t* index);
+
+/* Use an external CUDA stream (cudaStream_t as void*); NULL = own stream. */
+int dpq_set_stream(dpq_index_t* index, void* stream);
+/* Query batch size used internally (default 1024). */
+int dpq_set_batch(dpq_index_t* index, int batch);
+/* Enable per-phase CUDA-event timing (dpq_last_phase_ms). */
+int dpq_set_timing(dpq_index_t* index, int enabled);
+
+/* ------------------------------------------------------ flat searches --
+ * dpq_flat_search_derived: FlatIndex.search(..., mode="derived", r2)
+ * (flat.py:94-104 -> nns_derived, twopass.py:311-353) for nq queries.
+ *   yr        (nq, d) f32 host, queries AFTER quantizer.rotate in the
+ *             reference's call shape (identity for plain PQ).
+ *   phase_us  optional (nq, 4) f64 host: index/tables/scan/refine µs per
+ *             query (batched phases amortised per query), or NULL.
+ * `capped` is accepted for signature parity; the retained candidate set is
+ * identical either way (SURVEY Appendix A rule 8).                        */
+int dpq_flat_search_derived(dpq_index_t* index, const float* yr, int64_t nq,
+                            int r, int r2, int capped, double* dists,
+                            int64_t* ids, double* phase_us);
+/* Device-pointer twin: yr/dists/ids on the index's device. */
+int dpq_flat_search_derived_dev(dpq_index_t* index, const float* yr,
+                                int64_t nq, int r, int r2, double* dists,
+                                int64_t* ids);
+
+/* FlatIndex.search(..., mode="conventional") (flat.py:82-93): full
+ * (m,k) tables, adc over all n codes, exact top-r.                        */
+int dpq_flat_search_conventional(dpq_index_t* index, const float* yr,
+                                 int64_t nq, int r, double* dists,
+                                 int64_t* ids, double* phase_us);
+
+/* ------------------------------------------------------- ivf searches --
+ * IVFIndex.probe (ivf.py:107-120): the ma nearest cells (f64 distances,
+ * ties to the lower cell id).  cells (nq, ma) i64 host.                   */
+int dpq_ivf_probe(dpq_index_t* index, const float* y, int64_t nq, int ma,
+                  int64_t* cells);
+/* IVFIndex.search(..., mode="derived") (ivf.py:195-277).
+ *   y         (nq, d) raw queries (host).
+ *   res_rot   optional (nq, ma, d) rotated residuals computed by the caller
+ *             with quantizer.rotate in the (ma, d) call shape (OPQ); NULL
+ *             means identity rotation (residual y - center formed on
+ *             device in f32, exactly ivf.py:120).
+ *   cells     optional (nq, ma) probe result matching res_rot; NULL probes
+ *             on device.                                                  */
+int dpq_ivf_search_derived(dpq_index_t* index, const float* y, int64_t nq,
+                           int r, int ma, int r2, int capped,
+                           const float* res_rot, const int64_t* cells,
+                           double* dists, int64_t* ids, double* phase_us);
+int dpq_ivf_search_conventional(dpq_index_t* index, const float* y,
+                                int64_t nq, int r, int ma,
+                                const float* res_rot, const int64_t* cells,
+                                double* dists, int64_t* ids,
+                                double* phase_us);
+
+/* ----------------------------------------------------- sharded (flat) --
+ * Split form of dpq_flat_search_derived for a database sharded across
+ * GPUs.  The caller all-reduces between the phases:
+ *   1. dpq_shard_begin: small tables (global qmax from the replicated
+ *      prefix), sample histograms  -> hist_out (nq,256) i32 (sum these)
+ *   2. dpq_shard_guard: guards from the summed sample histograms and the
+ *      global row count; scan; local candidate histogram of scores <= guard
+ *                                    -> hist_out (nq,256) i32 (sum these)
+ *   3. dpq_shard_finish: global b* from the summed histogram; local refine
+ *      and top-r (ids include id_base)  -> dists/ids (nq,r), plus
+ *      need_exact (nq) u8 flags for queries whose guard proved too tight
+ *      (the caller then re-runs step 2 with exact=1 for all shards).
+ * All buffers are host memory.                                            */
+int dpq_shard_begin(dpq_index_t* index, const float* yr, int64_t nq, int r2,
+                    int32_t* sample_hist);
+int dpq_shard_scan(dpq_index_t* index, const int32_t* sample_hist_sum,
+                   int64_t n_global, int64_t sample_global, int r2,
+                   int exact, int32_t* cand_hist);
+int dpq_shard_finish(dpq_index_t* index, const int32_t* cand_hist_sum,
+                     int r, int r2, double* dists, int64_t* ids,
+                     uint8_t* need_exact);
+
+/* ------------------------------------------------ unit seams (debug) --
+ * Replace compute_tables(yr, derived_codebooks_) + quantize_tables
+ * (search.py:28-48, twopass.py:63-85) for nq queries: small (nq,m,kbar) f32,
+ * q (nq,m,kbar) u8, qmin/qmax (nq) f64.                                   */
+int dpq_debug_quantize_tables(dpq_index_t* index, const float* yr,
+                              int64_t nq, int r2, float* small, uint8_t* q,
+                              double* qmin, double* qmax);
+/* adc_low_batch (twopass.py:99-106) of every code for nq queries:
+ * scores (nq, n) u8.                                                      */
+int dpq_debug_low_scores(dpq_index_t* index, const float* yr, int64_t nq,
+                         int r2, uint8_t* scores);
+/* CappedBuckets bound + refine walk (twopass.py:171-201, 276-308):
+ * bstar (nq) i32 and ncand (nq) i64 = |{s <= b*, s < 255}|.               */
+int dpq_debug_candidates(dpq_index_t* index, const float* yr, int64_t nq,
+                         int r2, int32_t* bstar, int64_t* ncand);
+/* compute_tables(yr, codebooks_) (search.py:28-48), full (nq,m,k) f32.    */
+int dpq_debug_full_tables(dpq_index_t* index, const float* yr, int64_t nq,
+                          float* tables);
+
+/* ------------------------------------------------------- measurement --
+ * Milliseconds of the last batch's phases when timing is enabled:
+ * [0] tables (K1), [1] sample+guard, [2] scan (K2), [3] threshold (K3),
+ * [4] refine+top-r (K6), [5] fallback, [6] whole batch.                    */
+int dpq_last_phase_ms(dpq_index_t* index, float* ms7);
+/* Counters since creation: kernel launches, queries searched, code rows
+ * scanned (sum over queries), candidates refined, exact fallbacks.         */
+int dpq_counters(dpq_index_t* index, int64_t* out5);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DPQ_H_ */

@@ -1,0 +1,194 @@
+"""ctypes binding of libdpq.so (include/dpq.h).
+
+This is the reference-side binding a maintainer of `derivedpq` would add
+(INTEGRATION.md): the reference is Python, so its FFI is ctypes over the
+C ABI.  There is no CPU fallback: if the library is missing or no CUDA
+device is visible, every search raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from ctypes import POINTER, c_double, c_float, c_int, c_int32, c_int64, c_uint8, c_void_p
+from pathlib import Path
+
+import numpy as np
+
+_PATH = Path(__file__).with_name("libdpq.so")
+_lib = None
+
+DPQ_OK, DPQ_ERR_ARG, DPQ_ERR_CUDA, DPQ_ERR_NOMEM, DPQ_ERR_STATE = 0, 1, 2, 3, 4
+
+# name -> (restype, argtypes); mirrors include/dpq.h one-to-one
+SIGNATURES = {
+    "dpq_last_error": (ctypes.c_char_p, []),
+    "dpq_abi_version": (c_int, []),
+    "dpq_device_count": (c_int, []),
+    "dpq_flat_create": (c_int, [c_int, c_int, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p, c_int,
+                                c_int64, c_int64, c_void_p, c_int64, POINTER(c_void_p)]),
+    "dpq_ivf_create": (c_int, [c_int, c_int, c_int, c_int, c_int, c_void_p, c_void_p, c_int, c_void_p,
+                               c_void_p, c_void_p, c_int, c_void_p, c_int64, POINTER(c_void_p)]),
+    "dpq_destroy": (None, [c_void_p]),
+    "dpq_set_stream": (c_int, [c_void_p, c_void_p]),
+    "dpq_set_batch": (c_int, [c_void_p, c_int]),
+    "dpq_set_timing": (c_int, [c_void_p, c_int]),
+    "dpq_flat_search_derived": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_int, c_int, c_void_p,
+                                        c_void_p, c_void_p]),
+    "dpq_flat_search_derived_dev": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_int, c_void_p,
+                                            c_void_p]),
+    "dpq_flat_search_conventional": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_void_p, c_void_p,
+                                             c_void_p]),
+    "dpq_ivf_probe": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_void_p]),
+    "dpq_ivf_search_derived": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_int, c_int, c_int,
+                                       c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "dpq_ivf_search_conventional": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_int, c_void_p,
+                                            c_void_p, c_void_p, c_void_p, c_void_p]),
+    "dpq_shard_begin": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_void_p]),
+    "dpq_shard_scan": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int, c_int, c_void_p]),
+    "dpq_shard_finish": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p]),
+    "dpq_debug_quantize_tables": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_void_p, c_void_p,
+                                          c_void_p, c_void_p]),
+    "dpq_debug_low_scores": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_void_p]),
+    "dpq_debug_candidates": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_void_p, c_void_p]),
+    "dpq_debug_full_tables": (c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
+    "dpq_last_phase_ms": (c_int, [c_void_p, c_void_p]),
+    "dpq_counters": (c_int, [c_void_p, c_void_p]),
+}
+
+
+def lib():
+    """Load libdpq.so once; raise if it is absent (no CPU fallback)."""
+    global _lib
+    if _lib is None:
+        if not _PATH.exists():
+            raise RuntimeError(
+                f"{_PATH} is missing: build it with `python -m paper_1905_06900_b200.build` "
+                "(or __graft_entry__.build()); there is no CPU fallback")
+        L = ctypes.CDLL(str(_PATH))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def last_error() -> str:
+    msg = lib().dpq_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc == DPQ_OK:
+        return
+    msg = f"{what}: {last_error()}" if what else last_error()
+    if rc == DPQ_ERR_ARG:
+        raise ValueError(msg)
+    if rc == DPQ_ERR_NOMEM:
+        raise MemoryError(msg)
+    raise RuntimeError(msg)
+
+
+def device_count() -> int:
+    return int(lib().dpq_device_count())
+
+
+def require_device(device: int) -> None:
+    n = device_count()
+    if n <= device:
+        raise RuntimeError(
+            f"libdpq: CUDA device {device} not available ({n} visible); the derived search "
+            "runs only on the GPU")
+
+
+def ptr(a) -> c_void_p:
+    """Data pointer of a numpy array or torch tensor (None -> NULL)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return c_void_p(a.ctypes.data)
+    return c_void_p(int(a.data_ptr()))
+
+
+class Handle:
+    """Owns one dpq_index_t*; destroyed with the Python object."""
+
+    def __init__(self, raw: c_void_p, device: int):
+        self.raw = raw
+        self.device = device
+
+    def __del__(self):
+        raw = getattr(self, "raw", None)
+        if raw and _lib is not None:
+            _lib.dpq_destroy(raw)
+            self.raw = None
+
+    def phase_ms(self) -> np.ndarray:
+        out = np.zeros(7, dtype=np.float32)
+        check(lib().dpq_last_phase_ms(self.raw, ptr(out)))
+        return out
+
+    def counters(self) -> dict:
+        out = np.zeros(5, dtype=np.int64)
+        check(lib().dpq_counters(self.raw, ptr(out)))
+        return dict(zip(("launches", "queries", "rows_scanned", "refined", "fallbacks"), out.tolist()))
+
+    def set_timing(self, on: bool) -> None:
+        check(lib().dpq_set_timing(self.raw, int(bool(on))))
+
+    def set_batch(self, batch: int) -> None:
+        check(lib().dpq_set_batch(self.raw, int(batch)))
+
+    def set_stream(self, stream_ptr: int | None) -> None:
+        check(lib().dpq_set_stream(self.raw, c_void_p(stream_ptr) if stream_ptr else None))
+
+
+def _c(a, dtype):
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+def code_bytes_of(codes: np.ndarray) -> int:
+    if codes.dtype == np.uint8:
+        return 1
+    if codes.dtype == np.uint16:
+        return 2
+    if codes.size and (codes.min() < 0 or codes.max() > 65535):
+        raise ValueError("codes must fit in uint16")
+    return 2 if (codes.size and codes.max() > 255) else 1
+
+
+def flat_create(codebooks, derived, codes, device=0, id_base=0, prefix_codes=None) -> Handle:
+    require_device(device)
+    codebooks = _c(codebooks, np.float32)
+    derived = _c(derived, np.float32)
+    cbytes = code_bytes_of(np.asarray(codes))
+    codes = _c(codes, np.uint8 if cbytes == 1 else np.uint16)
+    m, k, dsub = codebooks.shape
+    kbar = derived.shape[1]
+    if prefix_codes is not None:
+        prefix_codes = _c(prefix_codes, codes.dtype)
+    out = c_void_p()
+    rc = lib().dpq_flat_create(int(device), m, k, kbar, dsub, ptr(codebooks), ptr(derived), ptr(codes), cbytes,
+                               int(codes.shape[0]), int(id_base), ptr(prefix_codes),
+                               int(prefix_codes.shape[0]) if prefix_codes is not None else 0,
+                               ctypes.byref(out))
+    check(rc, "dpq_flat_create")
+    return Handle(out, device)
+
+
+def ivf_create(codebooks, derived, centers, offsets, sorted_codes, sorted_ids, device=0) -> Handle:
+    require_device(device)
+    codebooks = _c(codebooks, np.float32)
+    derived = _c(derived, np.float32)
+    centers = _c(centers, np.float32)
+    offsets = _c(offsets, np.int64)
+    cbytes = code_bytes_of(np.asarray(sorted_codes))
+    sorted_codes = _c(sorted_codes, np.uint8 if cbytes == 1 else np.uint16)
+    sorted_ids = _c(sorted_ids, np.int64)
+    m, k, dsub = codebooks.shape
+    out = c_void_p()
+    rc = lib().dpq_ivf_create(int(device), m, k, derived.shape[1], dsub, ptr(codebooks), ptr(derived),
+                              int(centers.shape[0]), ptr(centers), ptr(offsets), ptr(sorted_codes), cbytes,
+                              ptr(sorted_ids), int(sorted_ids.shape[0]), ctypes.byref(out))
+    check(rc, "dpq_ivf_create")
+    return Handle(out, device)

@@ -1,0 +1,806 @@
+// dpq_flat.cu — flat-index orchestration of the derived two-pass search and
+// the conventional single-pass search on one GPU, plus the C ABI for them.
+//
+// Batch pipeline (one stream, inputs already in HBM):
+//   K1 k_small_tables -> K2a k_scan_hist (row sample) -> k_guard
+//   -> K2b k_scan_emit -> K3 k_threshold -> [rare: exact redo] -> K6 refine
+// The only host synchronisation per batch is the 1-byte-per-query flag read
+// after K3 (guard too tight / emit overflow), which decides whether the
+// exact redo runs.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "../../include/dpq.h"
+#include "dpq_impl.h"
+#include "dpq_kernels.cuh"
+
+namespace dpq {
+
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+const char* last_error() { return g_last_error.c_str(); }
+
+#define DPQ_CUDA(call)                                                          \
+  do {                                                                          \
+    cudaError_t e_ = (call);                                                    \
+    if (e_ != cudaSuccess) {                                                    \
+      set_error(std::string(#call) + ": " + cudaGetErrorString(e_) + " (" +     \
+                __FILE__ + ":" + std::to_string(__LINE__) + ")");               \
+      return DPQ_ERR_CUDA;                                                      \
+    }                                                                           \
+  } while (0)
+
+#define DPQ_LAUNCHED(h)                                                         \
+  do {                                                                          \
+    cudaError_t e_ = cudaGetLastError();                                        \
+    if (e_ != cudaSuccess) {                                                    \
+      set_error(std::string("kernel launch: ") + cudaGetErrorString(e_) + " (" + \
+                __FILE__ + ":" + std::to_string(__LINE__) + ")");               \
+      return DPQ_ERR_CUDA;                                                      \
+    }                                                                           \
+    (h)->counters[0]++;                                                         \
+  } while (0)
+
+#define DPQ_TRY(expr)            \
+  do {                           \
+    int rc_ = (expr);            \
+    if (rc_ != DPQ_OK) return rc_; \
+  } while (0)
+
+static constexpr int kScanThreads = 512;
+static constexpr int kTopThreads = 256;
+
+template <class T>
+static int dmalloc(T** p, size_t count) {
+  if (*p) { cudaFree(*p); *p = nullptr; }
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc((void**)p, count * sizeof(T));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    set_error(std::string("cudaMalloc(") + std::to_string(count * sizeof(T)) + " B): " + cudaGetErrorString(e));
+    *p = nullptr;
+    return DPQ_ERR_NOMEM;
+  }
+  return DPQ_OK;
+}
+template <class T>
+static int hmalloc(T** p, size_t count) {
+  if (*p) { cudaFreeHost(*p); *p = nullptr; }
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMallocHost((void**)p, count * sizeof(T));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    set_error(std::string("cudaMallocHost: ") + cudaGetErrorString(e));
+    *p = nullptr;
+    return DPQ_ERR_NOMEM;
+  }
+  return DPQ_OK;
+}
+
+static inline int qt_of(int mpad) { return mpad == 4 ? ScanGeom<4>::QT : ScanGeom<8>::QT; }
+static inline int tiles_of(int nslot, int mpad) { return (nslot + qt_of(mpad) - 1) / qt_of(mpad); }
+
+int ensure_ws(Index* h, int nslot, int r, int ystride) {
+  Workspace& w = h->ws;
+  const int qt = qt_of(h->mpad);
+  if (nslot > w.qb || ystride > w.ystride) {
+    const int qb = std::max(nslot, w.qb);
+    const int ys = std::max(ystride, w.ystride);
+    const int tiles = (qb + qt - 1) / qt;
+    const size_t mk = (size_t)h->m * h->kbar;
+    DPQ_TRY(dmalloc(&w.y, (size_t)qb * ys));
+    DPQ_TRY(dmalloc(&w.small, (size_t)qb * mk));
+    DPQ_TRY(dmalloc(&w.q8, (size_t)qb * mk));
+    DPQ_TRY(dmalloc(&w.qmin, (size_t)qb));
+    DPQ_TRY(dmalloc(&w.qmax, (size_t)qb));
+    DPQ_TRY(dmalloc(&w.bounds, (size_t)qb * 2));
+    DPQ_TRY(dmalloc(&w.lut, (size_t)tiles * h->mpad * 256 * qt));
+    DPQ_TRY(dmalloc(&w.hist, (size_t)tiles * qt * 256));
+    DPQ_TRY(dmalloc(&w.hist_i, (size_t)qb * 256));
+    DPQ_TRY(dmalloc(&w.guard_b, (size_t)tiles * qt));
+    DPQ_TRY(dmalloc(&w.gword, (size_t)tiles * qt));
+    DPQ_TRY(dmalloc(&w.bstar, (size_t)qb));
+    DPQ_TRY(dmalloc(&w.ncand, (size_t)qb));
+    DPQ_TRY(dmalloc(&w.flags, (size_t)qb));
+    DPQ_TRY(dmalloc(&w.only, (size_t)tiles * qt));
+    DPQ_TRY(dmalloc(&w.tile_list, (size_t)tiles));
+    DPQ_TRY(dmalloc(&w.slot_query, (size_t)tiles * qt));
+    DPQ_TRY(dmalloc(&w.slot_probe, (size_t)tiles * qt));
+    DPQ_TRY(dmalloc(&w.slot_pre_off, (size_t)qb));
+    DPQ_TRY(dmalloc(&w.slot_pre_len, (size_t)qb));
+    DPQ_TRY(hmalloc(&w.h_y, (size_t)qb * ys));
+    DPQ_TRY(hmalloc(&w.h_flags, (size_t)qb));
+    DPQ_TRY(hmalloc(&w.h_cnt, (size_t)qb));
+    w.qb = qb;
+    w.ystride = ys;
+    w.qcap_emit = 0;  // emit buffers re-sized below
+  }
+  if (w.qcap_emit < nslot || w.emit == nullptr) {
+    const int qb = w.qb;
+    if (w.cap == 0 && h->cap0 > 0) w.cap = (uint32_t)h->cap0;
+    if (w.cap == 0) {
+      int64_t c = h->n / 64;
+      c = std::max<int64_t>(c, 16384);
+      c = std::min<int64_t>(c, std::max<int64_t>(h->n, 1));
+      int64_t p2 = 1;
+      while (p2 < c) p2 <<= 1;
+      w.cap = (uint32_t)std::min<int64_t>(p2, (int64_t)1 << 31);
+    }
+    DPQ_TRY(dmalloc(&w.emit_cnt, (size_t)qb));
+    DPQ_TRY(dmalloc(&w.emit, (size_t)qb * w.cap));
+    w.qcap_emit = qb;
+  }
+  if (r > w.rcap || nslot > (int)w.h_out_elems / std::max(w.rcap, 1)) {
+    const int rc = std::max(r, w.rcap);
+    DPQ_TRY(dmalloc(&w.out_d, (size_t)w.qb * rc));
+    DPQ_TRY(dmalloc(&w.out_i, (size_t)w.qb * rc));
+    DPQ_TRY(hmalloc(&w.h_d, (size_t)w.qb * rc));
+    DPQ_TRY(hmalloc(&w.h_i, (size_t)w.qb * rc));
+    w.rcap = rc;
+    w.h_out_elems = (size_t)w.qb * rc;
+  }
+  return DPQ_OK;
+}
+
+static int grow_emit(Index* h, uint32_t need) {
+  Workspace& w = h->ws;
+  uint64_t c = w.cap;
+  while (c < need) c <<= 1;
+  c = std::min<uint64_t>(c, (uint64_t)1 << 31);
+  w.cap = (uint32_t)c;
+  DPQ_TRY(dmalloc(&w.emit, (size_t)w.qcap_emit * w.cap));
+  return DPQ_OK;
+}
+
+static inline void ev_rec(Index* h, int i) {
+  if (h->timing) cudaEventRecord(h->ev[i], h->stream);
+}
+static inline float ev_ms(Index* h, int a, int b) {
+  float ms = 0.f;
+  if (h->timing) cudaEventElapsedTime(&ms, h->ev[a], h->ev[b]);
+  return ms;
+}
+
+// ---------------------------------------------------------------------------
+// Launch helpers (template dispatch on MPAD)
+// ---------------------------------------------------------------------------
+template <int MPAD>
+static int launch_hist_t(Index* h, int ntiles, const int* tile_list, int64_t stride,
+                         int64_t nsamp, const uint8_t* plane) {
+  using G = ScanGeom<MPAD>;
+  const size_t smem = G::LUT_BYTES + (size_t)G::QT * 256 * 4;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_scan_hist<MPAD, kScanThreads>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  int chunks = (int)std::max<int64_t>(1, std::min<int64_t>((148 * 2 + ntiles - 1) / ntiles,
+                                                          (nsamp + 4095) / 4096));
+  int64_t per = (nsamp + chunks - 1) / chunks;
+  per = (per + 31) / 32 * 32;
+  chunks = (int)((nsamp + per - 1) / per);
+  if (chunks < 1) chunks = 1;
+  dim3 grid(chunks, ntiles);
+  k_scan_hist<MPAD, kScanThreads><<<grid, kScanThreads, smem, h->stream>>>(
+      plane, stride, nsamp, per, h->ws.lut, tile_list, h->ws.hist);
+  DPQ_LAUNCHED(h);
+  return DPQ_OK;
+}
+
+static int launch_hist(Index* h, int ntiles, const int* tile_list, int64_t stride, int64_t nsamp,
+                       const uint8_t* plane) {
+  return h->mpad == 4 ? launch_hist_t<4>(h, ntiles, tile_list, stride, nsamp, plane)
+                      : launch_hist_t<8>(h, ntiles, tile_list, stride, nsamp, plane);
+}
+
+template <int MPAD>
+static int launch_emit_t(Index* h, EmitArgs ea, int ntiles, int64_t rows) {
+  using G = ScanGeom<MPAD>;
+  const size_t smem = G::LUT_BYTES + (size_t)(kScanThreads / 32) * 32 * 16;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_scan_emit<MPAD, kScanThreads>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  // ~2 waves of one 512-thread CTA per SM across all query tiles.
+  int64_t want = std::max<int64_t>(1, (148 * 2 + ntiles - 1) / ntiles);
+  int64_t per = (rows + want - 1) / want;
+  const int64_t minper = (int64_t)G::CHUNK_ROWS * (kScanThreads / 32) * 4;
+  per = std::max(per, minper);
+  per = (per + G::CHUNK_ROWS - 1) / G::CHUNK_ROWS * G::CHUNK_ROWS;
+  const int64_t ctas = (rows + per - 1) / per;
+  ea.rows_per_cta = per;
+  dim3 grid((unsigned)std::max<int64_t>(ctas, 1), ntiles);
+  k_scan_emit<MPAD, kScanThreads><<<grid, kScanThreads, smem, h->stream>>>(ea);
+  DPQ_LAUNCHED(h);
+  return DPQ_OK;
+}
+
+static int launch_emit(Index* h, EmitArgs ea, int ntiles, int64_t rows) {
+  return h->mpad == 4 ? launch_emit_t<4>(h, ea, ntiles, rows) : launch_emit_t<8>(h, ea, ntiles, rows);
+}
+
+template <int BUF, int MODE>
+static int launch_refine_buf(Index* h, const RefineArgs& ra, int nq) {
+  const size_t smem = (size_t)BUF * 16 + (size_t)ra.ystride * 4;
+  static int attr = 0;
+  auto set_attr = [&](auto kern) {
+    if ((int)smem > attr) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 49152));
+    }
+  };
+  if (MODE == MODE_EMIT && ra.dsub == 32 && (ra.dsub % 4) == 0) {
+    auto kern = k_refine_topk<BUF, kTopThreads, MODE, 32>;
+    set_attr(kern);
+    kern<<<nq, kTopThreads, smem, h->stream>>>(ra);
+  } else if (MODE == MODE_EMIT && ra.dsub == 120) {
+    auto kern = k_refine_topk<BUF, kTopThreads, MODE, 120>;
+    set_attr(kern);
+    kern<<<nq, kTopThreads, smem, h->stream>>>(ra);
+  } else {
+    auto kern = k_refine_topk<BUF, kTopThreads, MODE, 0>;
+    set_attr(kern);
+    kern<<<nq, kTopThreads, smem, h->stream>>>(ra);
+  }
+  if ((int)smem > attr) attr = (int)smem;
+  DPQ_LAUNCHED(h);
+  return DPQ_OK;
+}
+
+template <int MODE>
+static int launch_refine(Index* h, const RefineArgs& ra, int nq) {
+  const int need = ra.r + kTopThreads;
+  if (need <= 1024) return launch_refine_buf<1024, MODE>(h, ra, nq);
+  if (need <= 2048) return launch_refine_buf<2048, MODE>(h, ra, nq);
+  if (need <= 4096) return launch_refine_buf<4096, MODE>(h, ra, nq);
+  if (need <= 8192) return launch_refine_buf<8192, MODE>(h, ra, nq);
+  set_error("r=" + std::to_string(ra.r) + " exceeds the device top-r limit (7936)");
+  return DPQ_ERR_ARG;
+}
+
+// ---------------------------------------------------------------------------
+// K1 for nslot slots whose queries are already in ws.y.
+// ---------------------------------------------------------------------------
+int run_small_tables(Index* h, int nslot, const void* prefix, int64_t npre,
+                     const int64_t* pre_off, const int64_t* pre_len, const double* bounds_in,
+                     bool export_debug, int ystride_override) {
+  Workspace& w = h->ws;
+  TablesArgs ta;
+  ta.y = w.y;
+  ta.dcb = h->dcb;
+  ta.m = h->m; ta.kbar = h->kbar; ta.dsub = h->dsub; ta.mask = h->mask;
+  ta.prefix = prefix; ta.code_bytes = h->code_bytes; ta.npre = npre;
+  ta.prefix_off = pre_off; ta.prefix_len = pre_len; ta.bounds_in = bounds_in;
+  ta.nslot = nslot;
+  ta.small_out = export_debug ? w.small : nullptr;
+  ta.q8_out = export_debug ? w.q8 : nullptr;
+  ta.qmin_out = w.qmin; ta.qmax_out = w.qmax;
+  ta.lut = w.lut; ta.mpad = h->mpad; ta.qt = qt_of(h->mpad);
+  (void)ystride_override;
+  const size_t smem = (size_t)(h->d + h->m * h->kbar) * 4 + (size_t)h->m * h->kbar + 16;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_small_tables, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  k_small_tables<<<nslot, 256, smem, h->stream>>>(ta);
+  DPQ_LAUNCHED(h);
+  return DPQ_OK;
+}
+
+// ---------------------------------------------------------------------------
+// First pass for a flat batch (slots = queries): guard, scan, b*.  Handles
+// the rare exact redo and emit overflow.  On return ws.bstar / emit are
+// valid for every query of the batch.
+// ---------------------------------------------------------------------------
+static int flat_first_pass(Index* h, int nb, int r2) {
+  Workspace& w = h->ws;
+  const int qt = qt_of(h->mpad);
+  const int tiles = tiles_of(nb, h->mpad);
+  // guard words of padding slots never hit: 0x7F7F < 0x8000
+  DPQ_CUDA(cudaMemsetAsync(w.gword, 0x7F, (size_t)tiles * qt * 2, h->stream));
+  DPQ_CUDA(cudaMemsetAsync(w.hist, 0, (size_t)tiles * qt * 256 * 4, h->stream));
+  const int64_t n = h->n;
+  const bool exact = n <= h->exact_limit;
+  const int64_t nsamp = exact ? n : std::min<int64_t>(n, h->sample);
+  const int64_t stride = exact ? 1 : n / nsamp;
+  DPQ_TRY(launch_hist(h, tiles, nullptr, stride, nsamp, h->plane));
+  const double lambda = (double)r2 * (double)nsamp / (double)std::max<int64_t>(n, 1);
+  k_guard<<<(nb + 127) / 128, 128, 0, h->stream>>>(w.hist, nb, r2, lambda, exact ? 1 : 0, nullptr,
+                                                    w.guard_b, w.gword);
+  DPQ_LAUNCHED(h);
+  ev_rec(h, 2);
+  bool first = true;
+  for (int attempt = 0; attempt < 8; ++attempt) {
+    DPQ_CUDA(cudaMemsetAsync(w.emit_cnt, 0, (size_t)nb * 4, h->stream));
+    EmitArgs ea;
+    ea.plane = h->plane; ea.row_begin = 0; ea.row_end = n; ea.rows_per_cta = 0;
+    ea.lut = w.lut; ea.gword = w.gword; ea.tile_list = nullptr;
+    ea.slot_query = nullptr; ea.slot_probe = nullptr;
+    ea.emit_cnt = w.emit_cnt; ea.emit = w.emit; ea.cap = w.cap;
+    DPQ_TRY(launch_emit(h, ea, tiles, n));
+    h->counters[2] += (int64_t)nb * n;
+    if (first) ev_rec(h, 3);
+    k_threshold<256><<<nb, 256, 0, h->stream>>>(w.emit, w.emit_cnt, w.cap, w.guard_b, r2, nullptr,
+                                                w.bstar, w.ncand, w.flags, nullptr);
+    DPQ_LAUNCHED(h);
+    if (first) ev_rec(h, 4);
+    first = false;
+    DPQ_CUDA(cudaMemcpyAsync(w.h_flags, w.flags, nb, cudaMemcpyDeviceToHost, h->stream));
+    DPQ_CUDA(cudaStreamSynchronize(h->stream));
+    bool any_exact = false, any_over = false;
+    for (int q = 0; q < nb; ++q) {
+      any_exact |= w.h_flags[q] == 1;
+      any_over |= w.h_flags[q] == 2;
+    }
+    if (!any_exact && !any_over) return DPQ_OK;
+    h->counters[4]++;
+    if (any_over) {
+      DPQ_CUDA(cudaMemcpyAsync(w.h_cnt, w.emit_cnt, (size_t)nb * 4, cudaMemcpyDeviceToHost, h->stream));
+      DPQ_CUDA(cudaStreamSynchronize(h->stream));
+      uint32_t need = 0;
+      for (int q = 0; q < nb; ++q)
+        if (w.h_flags[q] == 2) need = std::max(need, w.h_cnt[q]);
+      if ((size_t)w.qcap_emit * need * 8 > h->emit_budget && nb > 1) return 100;  // split batch
+      DPQ_TRY(grow_emit(h, need));
+    }
+    if (any_exact) {
+      // exact histogram for every tile holding a flagged query
+      std::vector<int> tl;
+      for (int t = 0; t < tiles; ++t) {
+        bool f = false;
+        for (int q = t * qt; q < std::min(nb, (t + 1) * qt); ++q) f |= w.h_flags[q] == 1;
+        if (f) tl.push_back(t);
+      }
+      for (int q = 0; q < nb; ++q) w.h_flags[q] = w.h_flags[q] == 1;
+      DPQ_CUDA(cudaMemcpyAsync(w.only, w.h_flags, nb, cudaMemcpyHostToDevice, h->stream));
+      DPQ_CUDA(cudaMemcpyAsync(w.tile_list, tl.data(), tl.size() * sizeof(int), cudaMemcpyHostToDevice,
+                               h->stream));
+      DPQ_CUDA(cudaMemsetAsync(w.hist, 0, (size_t)tiles * qt * 256 * 4, h->stream));
+      DPQ_TRY(launch_hist(h, (int)tl.size(), w.tile_list, 1, n, h->plane));
+      k_guard<<<(nb + 127) / 128, 128, 0, h->stream>>>(w.hist, nb, r2, 0.0, 1, w.only, w.guard_b, w.gword);
+      DPQ_LAUNCHED(h);
+      DPQ_CUDA(cudaStreamSynchronize(h->stream));
+    }
+  }
+  set_error("first pass did not converge");
+  return DPQ_ERR_CUDA;
+}
+
+static RefineArgs make_refine_args(Index* h, int r) {
+  Workspace& w = h->ws;
+  RefineArgs ra;
+  ra.emit = w.emit; ra.emit_cnt = w.emit_cnt; ra.cap = w.cap; ra.bstar = w.bstar;
+  ra.n_rows = h->n;
+  ra.codes = h->codes; ra.code_bytes = h->code_bytes; ra.m = h->m; ra.k = h->k; ra.dsub = h->dsub;
+  ra.cb = h->cb; ra.tables = w.tables; ra.y = w.y; ra.ystride = h->d;
+  ra.row_ids = nullptr; ra.id_base = h->id_base; ra.r = r;
+  ra.out_d = w.out_d; ra.out_i = w.out_i; ra.n_refined = h->d_nref;
+  return ra;
+}
+
+// One flat derived batch: queries already in ws.y (nb rows), results into
+// ws.out_d / ws.out_i.  Returns 100 when the batch must be split.
+static int flat_derived_batch(Index* h, int nb, int r, int r2) {
+  ev_rec(h, 0);
+  const int64_t npre = std::min<int64_t>(r2, h->n_prefix);
+  DPQ_TRY(run_small_tables(h, nb, h->prefix, npre, nullptr, nullptr, nullptr, false, 0));
+  ev_rec(h, 1);
+  int rc = flat_first_pass(h, nb, r2);
+  if (rc != DPQ_OK) return rc;
+  ev_rec(h, 5);
+  RefineArgs ra = make_refine_args(h, r);
+  DPQ_TRY(launch_refine<MODE_EMIT>(h, ra, nb));
+  ev_rec(h, 6);
+  h->counters[1] += nb;
+  if (h->timing) {
+    DPQ_CUDA(cudaEventSynchronize(h->ev[6]));
+    h->phase_ms[PH_TABLES] = ev_ms(h, 0, 1);
+    h->phase_ms[PH_GUARD] = ev_ms(h, 1, 2);
+    h->phase_ms[PH_SCAN] = ev_ms(h, 2, 3);
+    h->phase_ms[PH_THRESH] = ev_ms(h, 3, 4);
+    h->phase_ms[PH_FALLBACK] = ev_ms(h, 4, 5);
+    h->phase_ms[PH_REFINE] = ev_ms(h, 5, 6);
+    h->phase_ms[PH_TOTAL] = ev_ms(h, 0, 6);
+  }
+  return DPQ_OK;
+}
+
+static int flat_conventional_batch(Index* h, int nb, int r) {
+  Workspace& w = h->ws;
+  ev_rec(h, 0);
+  const int64_t need = (int64_t)nb * h->m * h->k;
+  if (need > w.tables_elems) {
+    DPQ_TRY(dmalloc(&w.tables, (size_t)need));
+    w.tables_elems = need;
+  }
+  dim3 grid((h->k + 255) / 256, h->m, nb);
+  k_full_tables<<<grid, 256, h->dsub * 4, h->stream>>>(w.y, h->cb, h->m, h->k, h->dsub, w.tables);
+  DPQ_LAUNCHED(h);
+  ev_rec(h, 1);
+  RefineArgs ra = make_refine_args(h, r);
+  DPQ_TRY(launch_refine<MODE_ALL>(h, ra, nb));
+  ev_rec(h, 2);
+  h->counters[1] += nb;
+  if (h->timing) {
+    DPQ_CUDA(cudaEventSynchronize(h->ev[2]));
+    h->phase_ms[PH_TABLES] = ev_ms(h, 0, 1);
+    h->phase_ms[PH_SCAN] = ev_ms(h, 1, 2);
+    h->phase_ms[PH_REFINE] = 0.f;
+    h->phase_ms[PH_TOTAL] = ev_ms(h, 0, 2);
+  }
+  return DPQ_OK;
+}
+
+// Generic host-buffer driver: splits nq into batches, stages through pinned
+// memory, calls `batch(nb)` and copies results back.
+template <class F>
+static int host_driver(Index* h, const float* y, int64_t nq, int r, int batch_limit, double* dists,
+                       int64_t* ids, double* phase_us, F&& batch) {
+  int bsz = std::max(1, std::min<int>(h->batch, batch_limit));
+  int64_t q0 = 0;
+  while (q0 < nq) {
+    const int nb = (int)std::min<int64_t>(bsz, nq - q0);
+    DPQ_TRY(ensure_ws(h, nb, r, h->d));
+    Workspace& w = h->ws;
+    memcpy(w.h_y, y + q0 * h->d, (size_t)nb * h->d * 4);
+    DPQ_CUDA(cudaMemcpyAsync(w.y, w.h_y, (size_t)nb * h->d * 4, cudaMemcpyHostToDevice, h->stream));
+    const bool want_t = phase_us != nullptr;
+    const bool old_t = h->timing;
+    if (want_t) h->timing = true;
+    int rc = batch(nb);
+    h->timing = old_t;
+    if (rc == 100) {  // split
+      bsz = std::max(1, nb / 2);
+      continue;
+    }
+    if (rc != DPQ_OK) return rc;
+    if (r > 0) {
+      DPQ_CUDA(cudaMemcpyAsync(w.h_d, w.out_d, (size_t)nb * r * 8, cudaMemcpyDeviceToHost, h->stream));
+      DPQ_CUDA(cudaMemcpyAsync(w.h_i, w.out_i, (size_t)nb * r * 8, cudaMemcpyDeviceToHost, h->stream));
+    }
+    DPQ_CUDA(cudaStreamSynchronize(h->stream));
+    if (r > 0) {
+      memcpy(dists + q0 * r, w.h_d, (size_t)nb * r * 8);
+      memcpy(ids + q0 * r, w.h_i, (size_t)nb * r * 8);
+    }
+    if (want_t) {
+      const double per = 1000.0 / nb;  // ms per batch -> us per query
+      for (int i = 0; i < nb; ++i) {
+        double* t = phase_us + (q0 + i) * 4;
+        t[0] = 0.0;  // flat: nothing to probe (flat.py:75-80)
+        t[1] = h->phase_ms[PH_TABLES] * per;
+        t[2] = (h->phase_ms[PH_GUARD] + h->phase_ms[PH_SCAN] + h->phase_ms[PH_THRESH] +
+                h->phase_ms[PH_FALLBACK]) * per;
+        t[3] = h->phase_ms[PH_REFINE] * per;
+      }
+    }
+    q0 += nb;
+  }
+  return DPQ_OK;
+}
+
+static int make_plane(Index* h);
+
+}  // namespace dpq
+
+using namespace dpq;
+
+// ============================================================================
+// Plane construction and index lifetime
+// ============================================================================
+namespace dpq {
+
+__global__ void k_make_plane(const void* codes, int code_bytes, int64_t n, int m, int mask, int mpad,
+                             uint8_t* plane) {
+  const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= n) return;
+  uint8_t b[8];
+  for (int j = 0; j < mpad; ++j)
+    b[j] = j < m ? (uint8_t)(code_at(codes, code_bytes, row * m + j) & mask) : (uint8_t)0;
+  for (int j = 0; j < mpad; ++j) plane[row * mpad + j] = b[j];
+}
+
+static int make_plane(Index* h) {
+  const int64_t pad_rows = ((h->n + 127) / 128) * 128 + 128;
+  h->n_pad = pad_rows;
+  DPQ_TRY(dmalloc(&h->plane, (size_t)pad_rows * h->mpad));
+  DPQ_CUDA(cudaMemsetAsync(h->plane, 0, (size_t)pad_rows * h->mpad, h->stream));
+  if (h->n > 0) {
+    k_make_plane<<<(unsigned)((h->n + 255) / 256), 256, 0, h->stream>>>(h->codes, h->code_bytes, h->n, h->m,
+                                                                         h->mask, h->mpad, h->plane);
+    DPQ_LAUNCHED(h);
+  }
+  return DPQ_OK;
+}
+
+int index_common_init(Index* h, int device, int m, int k, int kbar, int dsub, const float* codebooks,
+                      const float* derived, int code_bytes) {
+  if (m < 1 || m > 8) { set_error("m must be in [1, 8] for the device path"); return DPQ_ERR_ARG; }
+  if (k < 1 || k > 65536) { set_error("k must be in [1, 65536]"); return DPQ_ERR_ARG; }
+  if (kbar < 1 || kbar > 256 || (kbar & (kbar - 1))) {
+    set_error("kbar must be a power of two <= 256 for the device path"); return DPQ_ERR_ARG;
+  }
+  if (dsub < 1) { set_error("dsub must be >= 1"); return DPQ_ERR_ARG; }
+  if (code_bytes != 1 && code_bytes != 2) { set_error("code_bytes must be 1 or 2"); return DPQ_ERR_ARG; }
+  h->device = device;
+  DPQ_CUDA(cudaSetDevice(device));
+  h->m = m; h->k = k; h->kbar = kbar; h->dsub = dsub; h->d = m * dsub; h->mask = kbar - 1;
+  h->mpad = m <= 4 ? 4 : 8;
+  h->code_bytes = code_bytes;
+  if (const char* e = getenv("DPQ_GUARD_SAMPLE")) h->sample = std::max<int64_t>(1, atoll(e));
+  if (const char* e = getenv("DPQ_EXACT_LIMIT")) h->exact_limit = std::max<int64_t>(0, atoll(e));
+  if (const char* e = getenv("DPQ_EMIT_CAP")) h->cap0 = std::max<int64_t>(1, atoll(e));
+  DPQ_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  h->own_stream = true;
+  for (int i = 0; i < 8; ++i) DPQ_CUDA(cudaEventCreate(&h->ev[i]));
+  DPQ_TRY(dmalloc(&h->cb, (size_t)m * k * dsub));
+  DPQ_TRY(dmalloc(&h->dcb, (size_t)m * kbar * dsub));
+  DPQ_TRY(dmalloc(&h->d_nref, 1));
+  DPQ_CUDA(cudaMemcpy(h->cb, codebooks, (size_t)m * k * dsub * 4, cudaMemcpyHostToDevice));
+  DPQ_CUDA(cudaMemcpy(h->dcb, derived, (size_t)m * kbar * dsub * 4, cudaMemcpyHostToDevice));
+  DPQ_CUDA(cudaMemset(h->d_nref, 0, 8));
+  return DPQ_OK;
+}
+
+void index_free(Index* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  Workspace& w = h->ws;
+  void* dev[] = {h->cb, h->dcb, h->codes, h->plane, h->own_prefix ? h->prefix : nullptr, h->centers,
+                 h->offsets, h->sorted_ids, h->d_nref, w.y, w.small, w.q8, w.qmin, w.qmax, w.bounds,
+                 w.lut, w.hist, w.hist_i, w.guard_b, w.gword, w.emit_cnt, w.emit, w.bstar, w.ncand,
+                 w.flags, w.only, w.tile_list, w.out_d, w.out_i, w.tables, w.slot_query, w.slot_probe,
+                 w.slot_pre_off, w.slot_pre_len};
+  for (void* p : dev)
+    if (p) cudaFree(p);
+  void* host[] = {w.h_y, w.h_d, w.h_i, w.h_flags, w.h_cnt};
+  for (void* p : host)
+    if (p) cudaFreeHost(p);
+  for (int i = 0; i < 8; ++i)
+    if (h->ev[i]) cudaEventDestroy(h->ev[i]);
+  if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+}  // namespace dpq
+
+// ============================================================================
+// C ABI
+// ============================================================================
+extern "C" {
+
+const char* dpq_last_error(void) { return dpq::last_error(); }
+int dpq_abi_version(void) { return 1; }
+int dpq_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int dpq_flat_create(int device, int m, int k, int kbar, int dsub, const float* codebooks,
+                    const float* derived_codebooks, const void* codes, int code_bytes, int64_t n,
+                    int64_t id_base, const void* prefix_codes, int64_t n_prefix, dpq_index_t** out) {
+  if (!out || !codebooks || !derived_codebooks || (n > 0 && !codes) || n < 0) {
+    set_error("null pointer or negative size");
+    return DPQ_ERR_ARG;
+  }
+  if (n >= ((int64_t)1 << kRowBits)) { set_error("too many rows for one index shard"); return DPQ_ERR_ARG; }
+  Index* h = new Index();
+  h->kind = KIND_FLAT;
+  int rc = index_common_init(h, device, m, k, kbar, dsub, codebooks, derived_codebooks, code_bytes);
+  if (rc != DPQ_OK) { index_free(h); return rc; }
+  h->n = n;
+  h->id_base = id_base;
+  const size_t cbytes = (size_t)n * m * code_bytes;
+  if ((rc = dmalloc((uint8_t**)&h->codes, cbytes + 16)) != DPQ_OK) { index_free(h); return rc; }
+  if (n > 0 && cudaMemcpy(h->codes, codes, cbytes, cudaMemcpyHostToDevice) != cudaSuccess) {
+    set_error("codes upload failed"); index_free(h); return DPQ_ERR_CUDA;
+  }
+  if (prefix_codes && n_prefix > 0) {
+    const size_t pb = (size_t)n_prefix * m * code_bytes;
+    if ((rc = dmalloc((uint8_t**)&h->prefix, pb)) != DPQ_OK) { index_free(h); return rc; }
+    if (cudaMemcpy(h->prefix, prefix_codes, pb, cudaMemcpyHostToDevice) != cudaSuccess) {
+      set_error("prefix upload failed"); index_free(h); return DPQ_ERR_CUDA;
+    }
+    h->own_prefix = true;
+    h->n_prefix = n_prefix;
+  } else {
+    h->prefix = h->codes;
+    h->n_prefix = n;
+  }
+  if ((rc = make_plane(h)) != DPQ_OK) { index_free(h); return rc; }
+  if (cudaStreamSynchronize(h->stream) != cudaSuccess) {
+    set_error("index build failed"); index_free(h); return DPQ_ERR_CUDA;
+  }
+  *out = reinterpret_cast<dpq_index_t*>(h);
+  return DPQ_OK;
+}
+
+void dpq_destroy(dpq_index_t* index) { index_free(reinterpret_cast<Index*>(index)); }
+
+int dpq_set_stream(dpq_index_t* index, void* stream) {
+  Index* h = reinterpret_cast<Index*>(index);
+  if (!h) { set_error("null index"); return DPQ_ERR_ARG; }
+  cudaSetDevice(h->device);
+  if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+  if (stream) {
+    h->stream = (cudaStream_t)stream;
+    h->own_stream = false;
+  } else {
+    DPQ_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    h->own_stream = true;
+  }
+  return DPQ_OK;
+}
+
+int dpq_set_batch(dpq_index_t* index, int batch) {
+  Index* h = reinterpret_cast<Index*>(index);
+  if (!h || batch < 1) { set_error("bad batch"); return DPQ_ERR_ARG; }
+  h->batch = batch;
+  return DPQ_OK;
+}
+
+int dpq_set_timing(dpq_index_t* index, int enabled) {
+  Index* h = reinterpret_cast<Index*>(index);
+  if (!h) { set_error("null index"); return DPQ_ERR_ARG; }
+  h->timing = enabled != 0;
+  return DPQ_OK;
+}
+
+static int check_search(Index* h, int64_t nq, int r, int r2, bool derived) {
+  if (!h) { set_error("null index"); return DPQ_ERR_ARG; }
+  if (nq < 0 || r < 1) { set_error("need nq >= 0 and r >= 1"); return DPQ_ERR_ARG; }
+  if (derived && (r2 < 1 || r > r2)) { set_error("need 1 <= r <= r2"); return DPQ_ERR_ARG; }
+  if (derived && h->n_prefix < 1 && h->kind == KIND_FLAT) {
+    set_error("need at least one code to estimate qmax"); return DPQ_ERR_ARG;
+  }
+  cudaSetDevice(h->device);
+  return DPQ_OK;
+}
+
+int dpq_flat_search_derived(dpq_index_t* index, const float* yr, int64_t nq, int r, int r2, int capped,
+                            double* dists, int64_t* ids, double* phase_us) {
+  (void)capped;
+  Index* h = reinterpret_cast<Index*>(index);
+  DPQ_TRY(check_search(h, nq, r, r2, true));
+  if (h->kind != KIND_FLAT) { set_error("not a flat index"); return DPQ_ERR_STATE; }
+  return host_driver(h, yr, nq, r, 1 << 30, dists, ids, phase_us,
+                     [&](int nb) { return flat_derived_batch(h, nb, r, r2); });
+}
+
+int dpq_flat_search_derived_dev(dpq_index_t* index, const float* yr, int64_t nq, int r, int r2, double* dists,
+                                int64_t* ids) {
+  Index* h = reinterpret_cast<Index*>(index);
+  DPQ_TRY(check_search(h, nq, r, r2, true));
+  if (h->kind != KIND_FLAT) { set_error("not a flat index"); return DPQ_ERR_STATE; }
+  int bsz = h->batch;
+  int64_t q0 = 0;
+  while (q0 < nq) {
+    const int nb = (int)std::min<int64_t>(bsz, nq - q0);
+    DPQ_TRY(ensure_ws(h, nb, r, h->d));
+    Workspace& w = h->ws;
+    DPQ_CUDA(cudaMemcpyAsync(w.y, yr + q0 * h->d, (size_t)nb * h->d * 4, cudaMemcpyDeviceToDevice, h->stream));
+    int rc = flat_derived_batch(h, nb, r, r2);
+    if (rc == 100) { bsz = std::max(1, nb / 2); continue; }
+    if (rc != DPQ_OK) return rc;
+    DPQ_CUDA(cudaMemcpyAsync(dists + q0 * r, w.out_d, (size_t)nb * r * 8, cudaMemcpyDeviceToDevice, h->stream));
+    DPQ_CUDA(cudaMemcpyAsync(ids + q0 * r, w.out_i, (size_t)nb * r * 8, cudaMemcpyDeviceToDevice, h->stream));
+    q0 += nb;
+  }
+  DPQ_CUDA(cudaStreamSynchronize(h->stream));
+  return DPQ_OK;
+}
+
+int dpq_flat_search_conventional(dpq_index_t* index, const float* yr, int64_t nq, int r, double* dists,
+                                 int64_t* ids, double* phase_us) {
+  Index* h = reinterpret_cast<Index*>(index);
+  DPQ_TRY(check_search(h, nq, r, r, false));
+  if (h->kind != KIND_FLAT) { set_error("not a flat index"); return DPQ_ERR_STATE; }
+  // full tables are m*k floats per query: keep the batch's tables <= 1 GB
+  const int lim = (int)std::max<int64_t>(1, ((int64_t)1 << 28) / ((int64_t)h->m * h->k));
+  return host_driver(h, yr, nq, r, lim, dists, ids, phase_us,
+                     [&](int nb) { return flat_conventional_batch(h, nb, r); });
+}
+
+int dpq_debug_quantize_tables(dpq_index_t* index, const float* yr, int64_t nq, int r2, float* small, uint8_t* q,
+                              double* qmin, double* qmax) {
+  Index* h = reinterpret_cast<Index*>(index);
+  DPQ_TRY(check_search(h, nq, 1, r2, true));
+  const int64_t mk = (int64_t)h->m * h->kbar;
+  for (int64_t q0 = 0; q0 < nq; q0 += h->batch) {
+    const int nb = (int)std::min<int64_t>(h->batch, nq - q0);
+    DPQ_TRY(ensure_ws(h, nb, 1, h->d));
+    Workspace& w = h->ws;
+    DPQ_CUDA(cudaMemcpyAsync(w.y, yr + q0 * h->d, (size_t)nb * h->d * 4, cudaMemcpyHostToDevice, h->stream));
+    DPQ_TRY(run_small_tables(h, nb, h->prefix, std::min<int64_t>(r2, h->n_prefix), nullptr, nullptr, nullptr,
+                             true, 0));
+    DPQ_CUDA(cudaMemcpyAsync(small + q0 * mk, w.small, (size_t)nb * mk * 4, cudaMemcpyDeviceToHost, h->stream));
+    DPQ_CUDA(cudaMemcpyAsync(q + q0 * mk, w.q8, (size_t)nb * mk, cudaMemcpyDeviceToHost, h->stream));
+    DPQ_CUDA(cudaMemcpyAsync(qmin + q0, w.qmin, (size_t)nb * 8, cudaMemcpyDeviceToHost, h->stream));
+    DPQ_CUDA(cudaMemcpyAsync(qmax + q0, w.qmax, (size_t)nb * 8, cudaMemcpyDeviceToHost, h->stream));
+    DPQ_CUDA(cudaStreamSynchronize(h->stream));
+  }
+  return DPQ_OK;
+}
+
+int dpq_debug_candidates(dpq_index_t* index, const float* yr, int64_t nq, int r2, int32_t* bstar,
+                         int64_t* ncand) {
+  Index* h = reinterpret_cast<Index*>(index);
+  DPQ_TRY(check_search(h, nq, 1, r2, true));
+  if (h->kind != KIND_FLAT) { set_error("not a flat index"); return DPQ_ERR_STATE; }
+  for (int64_t q0 = 0; q0 < nq; q0 += h->batch) {
+    const int nb = (int)std::min<int64_t>(h->batch, nq - q0);
+    DPQ_TRY(ensure_ws(h, nb, 1, h->d));
+    Workspace& w = h->ws;
+    DPQ_CUDA(cudaMemcpyAsync(w.y, yr + q0 * h->d, (size_t)nb * h->d * 4, cudaMemcpyHostToDevice, h->stream));
+    DPQ_TRY(run_small_tables(h, nb, h->prefix, std::min<int64_t>(r2, h->n_prefix), nullptr, nullptr, nullptr,
+                             false, 0));
+    int rc = flat_first_pass(h, nb, r2);
+    if (rc == 100) { set_error("debug_candidates: emit budget exceeded, use a smaller batch"); return DPQ_ERR_NOMEM; }
+    if (rc != DPQ_OK) return rc;
+    DPQ_CUDA(cudaMemcpyAsync(bstar + q0, w.bstar, (size_t)nb * 4, cudaMemcpyDeviceToHost, h->stream));
+    DPQ_CUDA(cudaMemcpyAsync(ncand + q0, w.ncand, (size_t)nb * 8, cudaMemcpyDeviceToHost, h->stream));
+    DPQ_CUDA(cudaStreamSynchronize(h->stream));
+  }
+  return DPQ_OK;
+}
+
+int dpq_debug_full_tables(dpq_index_t* index, const float* yr, int64_t nq, float* tables) {
+  Index* h = reinterpret_cast<Index*>(index);
+  DPQ_TRY(check_search(h, nq, 1, 1, false));
+  const int64_t per = (int64_t)h->m * h->k;
+  for (int64_t q0 = 0; q0 < nq; ++q0) {
+    DPQ_TRY(ensure_ws(h, 1, 1, h->d));
+    Workspace& w = h->ws;
+    if (per > w.tables_elems) {
+      DPQ_TRY(dmalloc(&w.tables, (size_t)per));
+      w.tables_elems = per;
+    }
+    DPQ_CUDA(cudaMemcpyAsync(w.y, yr + q0 * h->d, (size_t)h->d * 4, cudaMemcpyHostToDevice, h->stream));
+    dim3 grid((h->k + 255) / 256, h->m, 1);
+    k_full_tables<<<grid, 256, h->dsub * 4, h->stream>>>(w.y, h->cb, h->m, h->k, h->dsub, w.tables);
+    DPQ_LAUNCHED(h);
+    DPQ_CUDA(cudaMemcpyAsync(tables + q0 * per, w.tables, (size_t)per * 4, cudaMemcpyDeviceToHost, h->stream));
+    DPQ_CUDA(cudaStreamSynchronize(h->stream));
+  }
+  return DPQ_OK;
+}
+
+int dpq_debug_low_scores(dpq_index_t* index, const float* yr, int64_t nq, int r2, uint8_t* scores) {
+  (void)index; (void)yr; (void)nq; (void)r2; (void)scores;
+  set_error("dpq_debug_low_scores: use dpq_debug_quantize_tables + host gather");
+  return DPQ_ERR_STATE;
+}
+
+int dpq_last_phase_ms(dpq_index_t* index, float* ms7) {
+  Index* h = reinterpret_cast<Index*>(index);
+  if (!h || !ms7) { set_error("null argument"); return DPQ_ERR_ARG; }
+  for (int i = 0; i < PH_N; ++i) ms7[i] = h->phase_ms[i];
+  return DPQ_OK;
+}
+
+int dpq_counters(dpq_index_t* index, int64_t* out5) {
+  Index* h = reinterpret_cast<Index*>(index);
+  if (!h || !out5) { set_error("null argument"); return DPQ_ERR_ARG; }
+  unsigned long long nref = 0;
+  cudaSetDevice(h->device);
+  cudaMemcpy(&nref, h->d_nref, 8, cudaMemcpyDeviceToHost);
+  h->counters[3] = (int64_t)nref;
+  for (int i = 0; i < 5; ++i) out5[i] = h->counters[i];
+  return DPQ_OK;
+}
+
+}  // extern "C"

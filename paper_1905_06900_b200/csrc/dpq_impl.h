@@ -1,0 +1,100 @@
+// dpq_impl.h — host-side state of a libdpq index handle (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+namespace dpq {
+
+void set_error(const std::string& msg);
+
+enum Kind { KIND_FLAT = 0, KIND_IVF = 1 };
+
+// Phase slots of dpq_last_phase_ms.
+enum Phase { PH_TABLES = 0, PH_GUARD, PH_SCAN, PH_THRESH, PH_REFINE, PH_FALLBACK, PH_TOTAL, PH_N };
+
+// Per-batch device workspace, grown on demand.
+struct Workspace {
+  int qb = 0;             // query (slot) capacity
+  int rcap = 0;           // result columns capacity
+  uint32_t cap = 0;       // emit capacity per query
+  int qcap_emit = 0;      // queries the emit buffer is sized for
+  float* y = nullptr;     // [qb][ystride]
+  int ystride = 0;
+  float* small = nullptr;     // [qb][m][kbar]
+  uint8_t* q8 = nullptr;      // [qb][m][kbar]
+  double* qmin = nullptr;
+  double* qmax = nullptr;
+  double* bounds = nullptr;   // [qb][2]
+  uint16_t* lut = nullptr;    // [tiles][mpad][256][qt]
+  uint32_t* hist = nullptr;   // [tiles*qt][256]
+  int32_t* hist_i = nullptr;  // [qb][256] (sharded exchange)
+  uint16_t* guard_b = nullptr;
+  uint16_t* gword = nullptr;
+  uint32_t* emit_cnt = nullptr;
+  uint64_t* emit = nullptr;
+  int32_t* bstar = nullptr;
+  int64_t* ncand = nullptr;
+  uint8_t* flags = nullptr;
+  uint8_t* only = nullptr;
+  int* tile_list = nullptr;
+  double* out_d = nullptr;
+  int64_t* out_i = nullptr;
+  float* tables = nullptr;    // conventional full tables
+  int64_t tables_elems = 0;
+  // ivf slot maps
+  int* slot_query = nullptr;
+  int* slot_probe = nullptr;
+  int64_t* slot_pre_off = nullptr;
+  int64_t* slot_pre_len = nullptr;
+  // pinned host staging
+  float* h_y = nullptr;
+  double* h_d = nullptr;
+  int64_t* h_i = nullptr;
+  uint8_t* h_flags = nullptr;
+  uint32_t* h_cnt = nullptr;
+  size_t h_y_bytes = 0, h_out_elems = 0;
+};
+
+struct Index {
+  int device = 0;
+  int kind = KIND_FLAT;
+  int m = 0, k = 0, kbar = 0, dsub = 0, d = 0, mask = 0, mpad = 4, code_bytes = 2;
+  int64_t n = 0, n_pad = 0, id_base = 0;
+  float* cb = nullptr;      // [m][k][dsub]
+  float* dcb = nullptr;     // [m][kbar][dsub]
+  void* codes = nullptr;    // [n][m]
+  uint8_t* plane = nullptr; // [n_pad][mpad]
+  void* prefix = nullptr;   // flat qmax prefix rows
+  int64_t n_prefix = 0;
+  bool own_prefix = false;
+  // ivf
+  int n_cells = 0;
+  float* centers = nullptr;       // [K][d]
+  int64_t* offsets = nullptr;     // device [K+1]
+  std::vector<int64_t> h_offsets; // host copy
+  int64_t* sorted_ids = nullptr;  // [n]
+  // execution
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int batch = 1024;
+  bool timing = false;
+  cudaEvent_t ev[8] = {};
+  float phase_ms[PH_N] = {};
+  int64_t counters[5] = {};  // launches, queries, rows scanned, refined, fallbacks
+  unsigned long long* d_nref = nullptr;
+  size_t emit_budget = (size_t)16 << 30;  // bytes for emit buffers
+  // guard sampling (env DPQ_GUARD_SAMPLE / DPQ_EXACT_LIMIT / DPQ_EMIT_CAP
+  // override them so tests can force the exact-redo and overflow paths)
+  int64_t sample = 16384;
+  int64_t exact_limit = 65536;
+  int64_t cap0 = 0;
+  Workspace ws;
+  // sharded-search state between dpq_shard_* calls
+  int shard_nq = 0;
+  int64_t shard_samp = 0;
+};
+
+}  // namespace dpq

@@ -1,0 +1,590 @@
+// dpq_kernels.cuh — sm_100a kernels of the derived two-pass search.
+//
+//   K1 k_small_tables   compute_tables(yr, derived) + quantize_tables
+//                       (search.py:28-48, twopass.py:41-85)
+//   K2 k_scan_hist      score histogram over a row sample (or all rows):
+//                       picks a provisional per-query bound ("guard") so the
+//                       main scan can drop everything that cannot be a
+//                       candidate without a per-code histogram update
+//      k_scan_emit      adc_low_batch (twopass.py:99-106) over every code,
+//                       query-tiled, emitting (row, score) for score <= guard
+//   K3 k_threshold      CappedBuckets bound + refine bucket walk
+//                       (twopass.py:171-201, 276-308) in closed form:
+//                       b* = min{b : #(s <= b) >= r2}, else 254
+//   K5 k_full_tables    compute_tables(yr, codebooks_) (conventional path)
+//   K6 k_refine_topk    LazyTables + _refine_batch + adc_batch + top-r
+//                       (twopass.py:220-273, search.py:64-88): exact f64
+//                       distance of every candidate, exact (dist,id) top-r
+//
+// Data layout in HBM (per index):
+//   plane  (n_pad, MPAD) u8   low bbar bits of every sub-code, subspaces
+//                             padded to MPAD in {4, 8} with zero bytes; the
+//                             first pass reads only this (4 or 8 B/code).
+//   codes  (n, m) u8/u16      original codes, gathered per candidate.
+//   lut    (tiles, MPAD, 256, QT) u16  8-bit tables of QT queries
+//                             interleaved so lane l of a warp reads the
+//                             entries of queries 2l, 2l+1 for one table row
+//                             with one conflict-free 32-bit LDS.
+#pragma once
+#include "dpq_device.cuh"
+
+namespace dpq {
+
+// ---- emit record: row | probe << 40 | score << 56 -------------------------
+constexpr int kRowBits = 40;
+constexpr uint64_t kRowMask = (uint64_t(1) << kRowBits) - 1;
+__device__ __forceinline__ uint64_t pack_emit(int64_t row, uint32_t probe,
+                                              uint32_t score) {
+  return (uint64_t)row | ((uint64_t)(probe & 0xFFFF) << kRowBits) |
+         ((uint64_t)score << 56);
+}
+__device__ __forceinline__ int64_t emit_row(uint64_t v) { return (int64_t)(v & kRowMask); }
+__device__ __forceinline__ uint32_t emit_probe(uint64_t v) { return (uint32_t)((v >> kRowBits) & 0xFFFF); }
+__device__ __forceinline__ uint32_t emit_score(uint64_t v) { return (uint32_t)(v >> 56); }
+
+__device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint32_t lds32(const uint8_t* p) {
+  return *reinterpret_cast<const uint32_t*>(p);
+}
+
+template <int MPAD>
+struct ScanGeom {
+  static constexpr int QT = MPAD == 4 ? 64 : 32;  // queries per tile
+  static constexpr int LPC = QT / 2;              // lanes per code
+  static constexpr int CPW = 32 / LPC;            // codes per warp step
+  static constexpr int ROWB = QT * 2;             // bytes per table row
+  static constexpr int LUT_BYTES = MPAD * 256 * ROWB;  // 128 KB
+  static constexpr int CHUNK_ROWS = 512 / MPAD;   // rows per 512-B warp load
+};
+
+// ============================================================================
+// K1: small tables, qmin/qmax, 8-bit quantization, scan-layout LUT.
+// ============================================================================
+struct TablesArgs {
+  const float* y;          // [nslot][d] queries (flat) or residuals (ivf)
+  const float* dcb;        // [m][kbar][dsub] derived codebooks
+  int m, kbar, dsub, mask;
+  const void* prefix;      // first rows of the scanned list (qmax)
+  int code_bytes;
+  int64_t npre;            // min(r2, rows) rows used for qmax
+  const int64_t* prefix_off;  // optional per-slot prefix row offset (ivf)
+  const int64_t* prefix_len;  // optional per-slot prefix length (ivf)
+  const double* bounds_in; // optional [nslot][2] externally chosen bounds
+  int nslot;
+  float* small_out;        // optional [nslot][m][kbar]
+  uint8_t* q8_out;         // optional [nslot][m][kbar]
+  double* qmin_out;        // [nslot]
+  double* qmax_out;        // [nslot]
+  uint16_t* lut;           // [tiles][mpad][256][qt]
+  int mpad, qt;
+};
+
+__global__ void __launch_bounds__(256) k_small_tables(TablesArgs a) {
+  extern __shared__ __align__(16) float sm_f[];
+  __shared__ float red_f[8];
+  __shared__ double red_d[8];
+  const int s = blockIdx.x, tid = threadIdx.x;
+  const int d = a.m * a.dsub, ne = a.m * a.kbar;
+  float* ys = sm_f;
+  float* st = sm_f + d;
+  uint8_t* q8 = reinterpret_cast<uint8_t*>(st + ne);
+  for (int i = tid; i < d; i += 256) ys[i] = a.y[(int64_t)s * d + i];
+  __syncthreads();
+  // compute_tables: row_sq_dists per derived centroid (search.py:24-25,46-47)
+  float mn = INFINITY;
+  for (int e = tid; e < ne; e += 256) {
+    const int j = e / a.kbar;
+    float v = pw_sqdist(a.dcb + (int64_t)e * a.dsub, ys + j * a.dsub, a.dsub);
+    st[e] = v;
+    mn = fminf(mn, v);
+  }
+  mn = warp_min_f(mn);
+  if ((tid & 31) == 0) red_f[tid >> 5] = mn;
+  __syncthreads();
+  // qmax: max over prefix codes of the f64 masked table sum, j ascending
+  // (twopass.py:41-47, 83-84)
+  int64_t pre_off = a.prefix_off ? a.prefix_off[s] : 0;
+  int64_t npre = a.prefix_len ? a.prefix_len[s] : a.npre;
+  double mx = -INFINITY;
+  for (int64_t p = tid; p < npre; p += 256) {
+    double acc = 0.0;
+    for (int j = 0; j < a.m; ++j) {
+      uint32_t c = code_at(a.prefix, a.code_bytes, (pre_off + p) * a.m + j);
+      acc = __dadd_rn(acc, (double)st[j * a.kbar + (c & a.mask)]);
+    }
+    mx = fmax(mx, acc);
+  }
+  mx = warp_max_d(mx);
+  if ((tid & 31) == 0) red_d[tid >> 5] = mx;
+  __syncthreads();
+  double qmin = (double)red_f[0], qmax = red_d[0];
+  for (int w = 1; w < 8; ++w) {
+    qmin = fmin(qmin, (double)red_f[w]);
+    qmax = fmax(qmax, red_d[w]);
+  }
+  if (a.bounds_in) {
+    qmin = a.bounds_in[2 * s];
+    qmax = a.bounds_in[2 * s + 1];
+  }
+  // quantize_with_bounds (twopass.py:50-60)
+  const bool degenerate = !(qmax > qmin);
+  const double scale = degenerate ? 0.0 : __ddiv_rn(255.0, __dsub_rn(qmax, qmin));
+  const float qmaxf = __double2float_rn(qmax);
+  for (int e = tid; e < ne; e += 256) {
+    uint8_t q = degenerate ? (uint8_t)0 : quantize_entry(st[e], qmin, scale, qmaxf);
+    q8[e] = q;
+    if (a.small_out) a.small_out[(int64_t)s * ne + e] = st[e];
+    if (a.q8_out) a.q8_out[(int64_t)s * ne + e] = q;
+  }
+  if (tid == 0) {
+    a.qmin_out[s] = qmin;
+    a.qmax_out[s] = degenerate ? qmin : qmax;
+  }
+  __syncthreads();
+  // scan-layout LUT: [tile][j][i][qq]
+  const int tile = s / a.qt, qq = s % a.qt;
+  uint16_t* L = a.lut + (int64_t)tile * a.mpad * 256 * a.qt + qq;
+  for (int e = tid; e < a.mpad * 256; e += 256) {
+    const int j = e >> 8, i = e & 255;
+    uint16_t v = (j < a.m && i < a.kbar) ? (uint16_t)q8[j * a.kbar + i] : (uint16_t)0;
+    L[(int64_t)e * a.qt] = v;
+  }
+}
+
+// ============================================================================
+// K2a: score histogram over a strided sample of rows (exact when stride=1
+// and the sample is every row).  One CTA = (sample chunk, query tile);
+// per-tile histograms live in shared memory, flushed with global atomics.
+// ============================================================================
+template <int MPAD>
+__device__ __forceinline__ uint32_t lut_sum(const uint8_t* L, uint32_t w0, uint32_t w1) {
+  constexpr int ROWB = ScanGeom<MPAD>::ROWB;
+  uint32_t s = 0;
+#pragma unroll
+  for (int j = 0; j < MPAD; ++j) {
+    const uint32_t w = j < 4 ? w0 : w1;
+    const uint32_t idx = (w >> (8 * (j & 3))) & 0xFFu;
+    s += lds32(L + (j * 256 + idx) * ROWB);
+  }
+  return s;
+}
+
+template <int MPAD, int NT>
+__global__ void __launch_bounds__(NT, 1)
+    k_scan_hist(const uint8_t* __restrict__ plane, int64_t stride, int64_t n_samp,
+                int64_t samp_per_cta, const uint16_t* __restrict__ lut,
+                const int* __restrict__ tile_list, uint32_t* __restrict__ hist) {
+  using G = ScanGeom<MPAD>;
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint8_t* slut = smem;
+  uint32_t* sh = reinterpret_cast<uint32_t*>(smem + G::LUT_BYTES);  // [QT][256]
+  const int tile = tile_list ? tile_list[blockIdx.y] : blockIdx.y;
+  const uint4* src = reinterpret_cast<const uint4*>(lut + (int64_t)tile * G::LUT_BYTES / 2);
+  for (int i = threadIdx.x; i < G::LUT_BYTES / 16; i += NT) reinterpret_cast<uint4*>(slut)[i] = src[i];
+  for (int i = threadIdx.x; i < G::QT * 256; i += NT) sh[i] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lic = lane % G::LPC, half = lane / G::LPC;
+  const uint8_t* L = slut + lic * 4;
+  uint32_t* h0 = sh + (2 * lic) * 256;
+  uint32_t* h1 = h0 + 256;
+  const int64_t s0 = (int64_t)blockIdx.x * samp_per_cta;
+  const int64_t s1 = min(n_samp, s0 + samp_per_cta);
+  for (int64_t g = s0 + (int64_t)warp * 32; g < s1; g += (int64_t)NT) {
+    const int64_t my = g + lane;
+    uint32_t w0 = 0, w1 = 0;
+    const bool ok = my < s1;
+    if (ok) {
+      const uint8_t* p = plane + my * stride * MPAD;
+      w0 = *reinterpret_cast<const uint32_t*>(p);
+      if (MPAD == 8) w1 = *reinterpret_cast<const uint32_t*>(p + 4);
+    }
+    const int cnt = (int)min((int64_t)32, s1 - g);
+    for (int k = 0; k < 32; k += G::CPW) {
+      const int src_lane = k + half;
+      const uint32_t c0 = __shfl_sync(0xffffffffu, w0, src_lane);
+      const uint32_t c1 = __shfl_sync(0xffffffffu, w1, src_lane);
+      if (src_lane < cnt) {
+        const uint32_t sum = lut_sum<MPAD>(L, c0, c1);
+        const uint32_t lo = sum & 0xFFFFu, hi = sum >> 16;
+        if (lo < 255u) atomicAdd(h0 + lo, 1u);
+        if (hi < 255u) atomicAdd(h1 + hi, 1u);
+      }
+    }
+  }
+  __syncthreads();
+  uint32_t* gh = hist + (int64_t)tile * G::QT * 256;
+  for (int i = threadIdx.x; i < G::QT * 256; i += NT) {
+    const uint32_t v = sh[i];
+    if (v) atomicAdd(gh + i, v);
+  }
+}
+
+// ============================================================================
+// K2b: the first-pass scan.  One CTA holds the 8-bit tables of QT queries in
+// shared memory (128 KB) and streams a contiguous range of code rows:
+// each warp pulls 512-B chunks of the low-byte plane with 128-bit
+// non-allocating loads (double-buffered through registers), re-reads them as
+// warp-uniform 128-bit shared loads, and every lane sums the table entries of
+// its two queries for each row with four (MPAD=4) conflict-free 32-bit LDS:
+// two u16 lanes per register, no carries (sum <= MPAD*255 < 2^15).  A row is
+// emitted for a query iff its raw sum <= guard (so score = raw sum < 255),
+// tested with one subtract on the packed pair:
+//   G = (0x8000 + B0) | (0x8000 + B1) << 16;  hit_k = bit 15+16k of (G - s).
+// ============================================================================
+struct EmitArgs {
+  const uint8_t* plane;
+  int64_t row_begin, row_end;   // scanned rows [row_begin, row_end)
+  int64_t rows_per_cta;
+  const uint16_t* lut;
+  const uint16_t* gword;        // [tiles*QT] guard words (0x8000+B or 0x7FFF)
+  const int* tile_list;         // optional blockIdx.y -> tile
+  const int* slot_query;        // optional slot -> emit list (ivf); else slot
+  const int* slot_probe;        // optional slot -> probe index (ivf)
+  uint32_t* emit_cnt;
+  uint64_t* emit;
+  uint32_t cap;
+};
+
+template <int MPAD, int NT>
+__global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
+  using G = ScanGeom<MPAD>;
+  constexpr int NW = NT / 32;
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint8_t* slut = smem;
+  uint4* stage = reinterpret_cast<uint4*>(smem + G::LUT_BYTES);
+  const int tile = a.tile_list ? a.tile_list[blockIdx.y] : blockIdx.y;
+  const uint4* src = reinterpret_cast<const uint4*>(a.lut + (int64_t)tile * G::LUT_BYTES / 2);
+  for (int i = threadIdx.x; i < G::LUT_BYTES / 16; i += NT) reinterpret_cast<uint4*>(slut)[i] = src[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lic = lane % G::LPC, half = lane / G::LPC;
+  const int slot0 = tile * G::QT + 2 * lic;
+  const uint32_t gw = (uint32_t)a.gword[slot0] | ((uint32_t)a.gword[slot0 + 1] << 16);
+  const uint8_t* L = slut + lic * 4;
+  // Logical range [r0, r1); loads start at the 512-B aligned row r0a and
+  // rows outside the range are never emitted.
+  const int64_t r0 = a.row_begin + (int64_t)blockIdx.x * a.rows_per_cta;
+  const int64_t r1 = min(a.row_end, r0 + a.rows_per_cta);
+  if (r0 >= r1) return;
+  const int64_t r0a = r0 & ~(int64_t)(G::CHUNK_ROWS - 1);
+  const int64_t nchunks = (r1 - r0a + G::CHUNK_ROWS - 1) / G::CHUNK_ROWS;
+  int64_t c = warp;
+  if (c >= nchunks) return;
+  uint4* wst = stage + warp * 32;
+  auto chunk_ptr = [&](int64_t ci) {
+    return reinterpret_cast<const uint4*>(a.plane + (r0a + ci * G::CHUNK_ROWS) * MPAD) + lane;
+  };
+  auto emit_one = [&](int slot, int64_t row, uint32_t score) {
+    const int qe = a.slot_query ? a.slot_query[slot] : slot;
+    const uint32_t probe = a.slot_probe ? (uint32_t)a.slot_probe[slot] : 0u;
+    const uint32_t pos = atomicAdd(a.emit_cnt + qe, 1u);
+    if (pos < a.cap) a.emit[(int64_t)qe * a.cap + pos] = pack_emit(row, probe, score);
+  };
+  auto process = [&](uint32_t w0, uint32_t w1, int64_t row) {
+    const uint32_t sum = lut_sum<MPAD>(L, w0, w1);
+    const uint32_t x = gw - sum;
+    if (__builtin_expect((x & 0x80008000u) != 0u, 0)) {
+      if (row >= r0 && row < r1) {
+        if (x & 0x00008000u) emit_one(slot0, row, sum & 0xFFFFu);
+        if (x & 0x80000000u) emit_one(slot0 + 1, row, sum >> 16);
+      }
+    }
+  };
+  uint4 nxt = ldg_stream(chunk_ptr(c));
+  for (; c < nchunks; c += NW) {
+    __syncwarp();
+    wst[lane] = nxt;
+    __syncwarp();
+    if (c + NW < nchunks) nxt = ldg_stream(chunk_ptr(c + NW));
+    const int64_t rb = r0a + c * G::CHUNK_ROWS;
+#pragma unroll 4
+    for (int i = 0; i < 32; ++i) {
+      const uint4 v = wst[i];
+      if (MPAD == 4) {
+        process(v.x, 0, rb + 4 * i + 0);
+        process(v.y, 0, rb + 4 * i + 1);
+        process(v.z, 0, rb + 4 * i + 2);
+        process(v.w, 0, rb + 4 * i + 3);
+      } else {
+        const uint32_t w0 = half ? v.z : v.x;
+        const uint32_t w1 = half ? v.w : v.y;
+        process(w0, w1, rb + 2 * i + half);
+      }
+    }
+  }
+}
+
+// ============================================================================
+// Guard selection from (sample or exact) histograms.  One thread per slot.
+//   exact: B = min{b <= 254 : cum[b] >= r2}, else 254  (the true b*)
+//   sample of S rows out of N: lambda = r2*S/N expected sample hits below
+//   b*; B = min{b : cum_s[b] >= lambda + 3 sqrt(lambda) + 4}, else 254.
+// A guard that proves too tight is detected by K3 and redone exactly.
+// ============================================================================
+__global__ void k_guard(const uint32_t* __restrict__ hist, int nslot, int r2,
+                        double lambda, int exact, const uint8_t* __restrict__ only,
+                        uint16_t* __restrict__ guard_b, uint16_t* __restrict__ gword) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nslot) return;
+  if (only && !only[s]) return;
+  const uint32_t* h = hist + (int64_t)s * 256;
+  const double target = exact ? (double)r2 : lambda + 3.0 * sqrt(lambda) + 4.0;
+  uint64_t cum = 0;
+  int B = 254;
+  for (int b = 0; b < 255; ++b) {
+    cum += h[b];
+    if ((double)cum >= target) { B = b; break; }
+  }
+  guard_b[s] = (uint16_t)B;
+  gword[s] = (uint16_t)(0x8000 + B);
+}
+
+// ============================================================================
+// K3: b* per query from the emitted scores (every emitted score <= guard, so
+// the histogram below the guard is exact).  flags: 1 = guard too tight
+// (cum[guard] < r2 with guard < 254: redo with the exact histogram),
+// 2 = emit buffer overflow.  When hist_out is given (sharded search) the
+// local histogram is exported instead and b* is decided after the
+// all-reduce.
+// ============================================================================
+template <int NT>
+__global__ void __launch_bounds__(NT)
+    k_threshold(const uint64_t* __restrict__ emit, const uint32_t* __restrict__ emit_cnt,
+                uint32_t cap, const uint16_t* __restrict__ guard_b, int r2,
+                const uint8_t* __restrict__ only, int32_t* __restrict__ bstar,
+                int64_t* __restrict__ ncand, uint8_t* __restrict__ flags,
+                int32_t* __restrict__ hist_out) {
+  __shared__ uint32_t h[256];
+  const int q = blockIdx.x;
+  if (only && !only[q]) return;
+  const uint32_t n = emit_cnt[q];
+  if (n > cap) {
+    if (threadIdx.x == 0) flags[q] = 2;
+    return;
+  }
+  for (int i = threadIdx.x; i < 256; i += NT) h[i] = 0;
+  __syncthreads();
+  const uint64_t* e = emit + (int64_t)q * cap;
+  for (uint32_t i = threadIdx.x; i < n; i += NT) atomicAdd(h + emit_score(e[i]), 1u);
+  __syncthreads();
+  if (hist_out) {
+    for (int i = threadIdx.x; i < 256; i += NT) hist_out[(int64_t)q * 256 + i] = (int32_t)h[i];
+    if (threadIdx.x == 0) flags[q] = 0;
+    return;
+  }
+  if (threadIdx.x == 0) {
+    const int B = guard_b[q];
+    int64_t cum = 0;
+    int bs = -1;
+    for (int b = 0; b <= B; ++b) {
+      cum += h[b];
+      if (cum >= r2) { bs = b; break; }
+    }
+    if (bs >= 0) {
+      bstar[q] = bs; ncand[q] = cum; flags[q] = 0;
+    } else if (B >= 254) {
+      bstar[q] = 254; ncand[q] = cum; flags[q] = 0;
+    } else {
+      flags[q] = 1;
+    }
+  }
+}
+
+// b* from a (globally summed) candidate histogram; sharded search.
+__global__ void k_bstar_from_hist(const int32_t* __restrict__ hist, const uint16_t* __restrict__ guard_b,
+                                  int nq, int r2, int32_t* __restrict__ bstar,
+                                  int64_t* __restrict__ ncand, uint8_t* __restrict__ flags) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  const int32_t* h = hist + (int64_t)q * 256;
+  const int B = guard_b[q];
+  int64_t cum = 0;
+  int bs = -1;
+  for (int b = 0; b <= B; ++b) {
+    cum += h[b];
+    if (cum >= r2) { bs = b; break; }
+  }
+  if (bs >= 0) { bstar[q] = bs; ncand[q] = cum; flags[q] = 0; }
+  else if (B >= 254) { bstar[q] = 254; ncand[q] = cum; flags[q] = 0; }
+  else { flags[q] = 1; }
+}
+
+// ============================================================================
+// K5: full (m, k) tables, exact (conventional mode and the debug seam).
+// ============================================================================
+__global__ void __launch_bounds__(256)
+    k_full_tables(const float* __restrict__ y, const float* __restrict__ cb, int m, int k,
+                  int dsub, float* __restrict__ out) {
+  extern __shared__ float ysub[];
+  const int q = blockIdx.z, j = blockIdx.y;
+  for (int t = threadIdx.x; t < dsub; t += 256) ysub[t] = y[((int64_t)q * m + j) * dsub + t];
+  __syncthreads();
+  const int i = blockIdx.x * 256 + threadIdx.x;
+  if (i < k)
+    out[((int64_t)q * m + j) * k + i] = pw_sqdist(cb + ((int64_t)j * k + i) * dsub, ysub, dsub);
+}
+
+// ============================================================================
+// K6: refine + exact top-r.  One CTA per query.  Every candidate's distance
+// is the f64 sum, subspace order, of its m full-table entries, each entry
+// computed on the fly with the same pairwise kernel as compute_tables (so
+// it is bit-identical to the lazily filled table of twopass.py:220-251
+// without materialising the table).  Survivors of the running threshold
+// (strictly better (dist,id) than the current r-th best) are collected in a
+// shared-memory buffer that is bitonic-sorted and truncated to r whenever it
+// could overflow.
+// Source of candidates:
+//   MODE_EMIT: emit list entries with score <= b*  (derived search)
+//   MODE_ALL : every row of [0, n_rows)            (conventional, tables)
+// ============================================================================
+enum { MODE_EMIT = 0, MODE_ALL = 1 };
+
+struct RefineArgs {
+  const uint64_t* emit; const uint32_t* emit_cnt; uint32_t cap;
+  const int32_t* bstar;
+  int64_t n_rows;            // MODE_ALL
+  const void* codes; int code_bytes; int m; int k; int dsub;
+  const float* cb;           // [m][k][dsub]
+  const float* tables;       // MODE_ALL: [nq][m][k] full tables
+  const float* y;            // [nq][ystride] query / per-probe residuals
+  int ystride;               // floats per query in y (d, or ma*d for ivf)
+  const int64_t* row_ids;    // optional row -> id (ivf sorted_ids)
+  int64_t id_base;
+  int r;
+  double* out_d; int64_t* out_i;
+  unsigned long long* n_refined;
+};
+
+template <int BUF, int NT>
+__device__ void sort_pairs(uint64_t* keys, int64_t* ids) {
+  for (int size = 2; size <= BUF; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = threadIdx.x; t < BUF / 2; t += NT) {
+        const int i = 2 * t - (t & (stride - 1));
+        const int j = i + stride;
+        const bool asc = (i & size) == 0;
+        const uint64_t ki = keys[i], kj = keys[j];
+        const int64_t ii = ids[i], ij = ids[j];
+        const bool sw = asc ? pair_less(kj, ij, ki, ii) : pair_less(ki, ii, kj, ij);
+        if (sw) { keys[i] = kj; keys[j] = ki; ids[i] = ij; ids[j] = ii; }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+template <int DSUB>
+__device__ __forceinline__ float entry_dist(const float* cbrow, const float* ys, int dsub) {
+  if constexpr (DSUB > 0) return pw_sqdist_fixed<DSUB>(cbrow, ys);
+  else return pw_sqdist(cbrow, ys, dsub);
+}
+
+template <int BUF, int NT, int MODE, int DSUB>
+__global__ void __launch_bounds__(NT) k_refine_topk(RefineArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint64_t* keys = reinterpret_cast<uint64_t*>(smem);
+  int64_t* ids = reinterpret_cast<int64_t*>(keys + BUF);
+  float* ys = reinterpret_cast<float*>(ids + BUF);
+  __shared__ int fill;
+  __shared__ uint64_t thr_k;
+  __shared__ int64_t thr_i;
+  __shared__ unsigned long long nref;
+  const int q = blockIdx.x;
+  for (int i = threadIdx.x; i < a.ystride; i += NT) ys[i] = a.y[(int64_t)q * a.ystride + i];
+  if (threadIdx.x == 0) { fill = 0; thr_k = ~0ull; thr_i = INT64_MAX; nref = 0; }
+  __syncthreads();
+  const int d = a.m * a.dsub;
+  int64_t ntot;
+  int bs = 254;
+  const uint64_t* e = nullptr;
+  if (MODE == MODE_EMIT) {
+    ntot = min(a.emit_cnt[q], a.cap);
+    bs = a.bstar[q];
+    e = a.emit + (int64_t)q * a.cap;
+  } else {
+    ntot = a.n_rows;
+  }
+  unsigned long long my_ref = 0;
+  for (int64_t base = 0; base < ntot; base += NT) {
+    const int64_t idx = base + threadIdx.x;
+    bool keep = false;
+    uint64_t key = 0;
+    int64_t id = 0;
+    if (idx < ntot) {
+      int64_t row;
+      uint32_t probe = 0;
+      bool cand = true;
+      if (MODE == MODE_EMIT) {
+        const uint64_t v = e[idx];
+        cand = (int)emit_score(v) <= bs;
+        row = emit_row(v);
+        probe = emit_probe(v);
+      } else {
+        row = idx;
+      }
+      if (cand) {
+        ++my_ref;
+        double dist = 0.0;
+        const float* yq = ys + (int64_t)probe * d;
+        for (int j = 0; j < a.m; ++j) {
+          const uint32_t c = code_at(a.codes, a.code_bytes, row * a.m + j);
+          float t;
+          if (MODE == MODE_ALL) t = a.tables[((int64_t)q * a.m + j) * a.k + c];
+          else t = entry_dist<DSUB>(a.cb + ((int64_t)j * a.k + c) * a.dsub, yq + j * a.dsub, a.dsub);
+          dist = __dadd_rn(dist, (double)t);
+        }
+        key = (uint64_t)__double_as_longlong(dist);
+        id = a.row_ids ? a.row_ids[row] : a.id_base + row;
+        keep = pair_less(key, id, thr_k, thr_i);
+      }
+    }
+    if (keep) {
+      const int p = atomicAdd(&fill, 1);
+      keys[p] = key;
+      ids[p] = id;
+    }
+    __syncthreads();
+    const int f = fill;
+    __syncthreads();
+    if (f > BUF - NT) {
+      for (int i = f + threadIdx.x; i < BUF; i += NT) { keys[i] = ~0ull; ids[i] = INT64_MAX; }
+      __syncthreads();
+      sort_pairs<BUF, NT>(keys, ids);
+      if (threadIdx.x == 0) {
+        const int nf = min(f, a.r);
+        fill = nf;
+        if (nf == a.r) { thr_k = keys[nf - 1]; thr_i = ids[nf - 1]; }
+      }
+      __syncthreads();
+    }
+  }
+  const int f = fill;
+  for (int i = f + threadIdx.x; i < BUF; i += NT) { keys[i] = ~0ull; ids[i] = INT64_MAX; }
+  __syncthreads();
+  sort_pairs<BUF, NT>(keys, ids);
+  const int got = min(f, a.r);
+  for (int i = threadIdx.x; i < a.r; i += NT) {
+    const int64_t o = (int64_t)q * a.r + i;
+    if (i < got) {
+      a.out_d[o] = __longlong_as_double((long long)keys[i]);
+      a.out_i[o] = ids[i];
+    } else {
+      a.out_d[o] = INFINITY;
+      a.out_i[o] = -1;
+    }
+  }
+  if (a.n_refined) {
+    atomicAdd(&nref, my_ref);
+    __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(a.n_refined, nref);
+  }
+}
+
+}  // namespace dpq

@@ -1,0 +1,214 @@
+"""GPU drop-in for derivedpq.FlatIndex (reference flat.py:32-140).
+
+Same constructor, fit, search signature, argument checks, exception types
+and messages, result dtypes/padding and timing keys as the reference; the
+search itself runs in libdpq.so on a B200.  Training and encoding are the
+quantizer's own (the reference's ProductQuantizer / OPQ, or any fitted
+object exposing codebooks_, derived_codebooks_, rotation_ and rotate()),
+so "same encode/train outputs" holds by construction.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+from sklearn.base import BaseEstimator
+from sklearn.utils.validation import check_array, check_is_fitted
+
+from . import _lib
+
+
+class ArrayQuantizer:
+    """A fitted quantizer assembled from arrays (the attributes the search
+    reads from ProductQuantizer, quantizer.py:94-131, 235-239)."""
+
+    def __init__(self, codebooks, derived_codebooks, rotation=None):
+        self.codebooks_ = np.ascontiguousarray(codebooks, dtype=np.float32)
+        self.derived_codebooks_ = np.ascontiguousarray(derived_codebooks, dtype=np.float32)
+        self.rotation_ = None if rotation is None else np.ascontiguousarray(rotation, dtype=np.float32)
+        self.m, self.k_, self.dsub_ = self.codebooks_.shape
+        self.kbar_ = self.derived_codebooks_.shape[1]
+        self.bbar_ = int(self.kbar_).bit_length() - 1
+        self.b = int(self.k_ - 1).bit_length() if self.k_ > 1 else 1
+        self.d_ = self.m * self.dsub_
+        self.code_dtype_ = np.uint8 if self.k_ <= 256 else np.uint16
+
+    def rotate(self, X):
+        if self.rotation_ is None:
+            return X
+        return (X @ self.rotation_).astype(np.float32, copy=False)
+
+    def fit(self, X, y=None):  # pragma: no cover - arrays are already fitted
+        return self
+
+
+def rotated_queries(quantizer, Y: np.ndarray) -> np.ndarray:
+    """Queries after quantizer.rotate in the reference's per-query call
+    shape (1, d) (twopass.py:334): a batched (nq,d)@R differs bitwise
+    from the per-row product under OpenBLAS (SURVEY Appendix A rule 11)."""
+    if getattr(quantizer, "rotation_", None) is None:
+        return np.ascontiguousarray(Y, dtype=np.float32)
+    out = np.empty((Y.shape[0], quantizer.codebooks_.shape[0] * quantizer.codebooks_.shape[2]),
+                   dtype=np.float32)
+    for i in range(Y.shape[0]):
+        out[i] = np.asarray(quantizer.rotate(Y[i: i + 1]), dtype=np.float32).reshape(-1)
+    return out
+
+
+def _timings(nq: int, phase: np.ndarray | None) -> dict:
+    keys = ("index_us", "tables_us", "scan_us", "refine_us")
+    if phase is None:
+        return {k: np.zeros(nq) for k in keys}
+    return {k: np.ascontiguousarray(phase[:, i]) for i, k in enumerate(keys)}
+
+
+class FlatIndex(BaseEstimator):
+    """Encoded database searched on the GPU, one or two passes.
+
+    Parameters
+    ----------
+    quantizer : fitted or unfitted product quantizer (reference
+        ProductQuantizer / OptimizedProductQuantizer, or ArrayQuantizer).
+    device : CUDA device ordinal holding the index.
+    """
+
+    def __init__(self, quantizer, device: int = 0):
+        self.quantizer = quantizer
+        self.device = device
+
+    # -- build (reference flat.py:45-52, unchanged semantics) -------------
+    def fit(self, X, train=None):
+        X = check_array(X, dtype=np.float32, order="C")
+        if not hasattr(self.quantizer, "codebooks_"):
+            self.quantizer.fit(X if train is None else train)
+        self.codes_ = self.quantizer.encode(X)
+        self.n_ = X.shape[0]
+        self._dev = None
+        return self
+
+    @classmethod
+    def from_reference(cls, index, device: int = 0) -> "FlatIndex":
+        """Wrap a fitted derivedpq.FlatIndex (shares its quantizer/codes)."""
+        check_is_fitted(index, "codes_")
+        out = cls(index.quantizer, device=device)
+        out.codes_ = index.codes_
+        out.n_ = index.codes_.shape[0]
+        out._dev = None
+        return out
+
+    @classmethod
+    def from_arrays(cls, codebooks, derived_codebooks, codes, rotation=None, device: int = 0) -> "FlatIndex":
+        out = cls(ArrayQuantizer(codebooks, derived_codebooks, rotation), device=device)
+        out.codes_ = np.asarray(codes)
+        out.n_ = out.codes_.shape[0]
+        out._dev = None
+        return out
+
+    # -- device state -----------------------------------------------------
+    def _handle(self) -> _lib.Handle:
+        codes = self.codes_
+        key = (id(codes), codes.ctypes.data if isinstance(codes, np.ndarray) else 0, codes.shape,
+               id(self.quantizer.codebooks_))
+        dev = getattr(self, "_dev", None)
+        if dev is None or dev[0] != key:
+            h = _lib.flat_create(self.quantizer.codebooks_, self.quantizer.derived_codebooks_, codes,
+                                 device=self.device)
+            self._dev = (key, h)
+        return self._dev[1]
+
+    def __getstate__(self):
+        state = self.__dict__.copy()
+        state.pop("_dev", None)
+        return state
+
+    # -- search (reference flat.py:54-108) ----------------------------------
+    def search(self, Y, r: int, mode: str = "conventional", r2=None, capped: bool = True,
+               return_timings: bool = False):
+        """Top-r neighbours for each query row (see derivedpq.FlatIndex.search)."""
+        check_is_fitted(self, "codes_")
+        Y = check_array(Y, dtype=np.float32, order="C")
+        if mode not in ("conventional", "derived"):
+            raise ValueError(f"unknown mode {mode!r}")
+        nq = Y.shape[0]
+        if mode == "derived" and r2 is None:
+            raise ValueError("derived mode requires r2")
+        if nq == 0:
+            dists = np.full((0, r), np.inf)
+            ids = np.full((0, r), -1, dtype=np.int64)
+            return (dists, ids, _timings(0, None)) if return_timings else (dists, ids)
+        if mode == "derived":
+            if r > r2:  # twopass.py:330-331
+                raise ValueError(f"r={r} must not exceed r2={r2}")
+            if self.codes_.shape[0] == 0 or r2 < 1:  # twopass.py:76-77
+                raise ValueError("need at least one code to estimate qmax")
+        if r < 1:  # search.py:99-101 (ResultSet)
+            raise ValueError(f"result size must be >= 1, got {r}")
+        yr = rotated_queries(self.quantizer, Y)
+        h = self._handle()
+        dists = np.empty((nq, r), dtype=np.float64)
+        ids = np.empty((nq, r), dtype=np.int64)
+        phase = np.zeros((nq, 4), dtype=np.float64) if return_timings else None
+        L = _lib.lib()
+        if mode == "derived":
+            rc = L.dpq_flat_search_derived(h.raw, _lib.ptr(yr), nq, int(r), int(r2), int(bool(capped)),
+                                           _lib.ptr(dists), _lib.ptr(ids), _lib.ptr(phase))
+        else:
+            rc = L.dpq_flat_search_conventional(h.raw, _lib.ptr(yr), nq, int(r), _lib.ptr(dists),
+                                                _lib.ptr(ids), _lib.ptr(phase))
+        _lib.check(rc, f"FlatIndex.search(mode={mode!r})")
+        if return_timings:
+            t = _timings(nq, phase)
+            if mode == "conventional":
+                t["refine_us"][:] = 0.0
+            return dists, ids, t
+        return dists, ids
+
+    # -- unit seams (GPU twins of the reference functions the tests call) --
+    def quantized_tables(self, Y, r2: int):
+        """compute_tables(yr, derived) + quantize_tables(small, codes[:r2], r2)
+        per query (search.py:28, twopass.py:63): (small f32 (nq,m,kbar),
+        q u8 (nq,m,kbar), qmin f64 (nq,), qmax f64 (nq,))."""
+        Y = check_array(Y, dtype=np.float32, order="C")
+        yr = rotated_queries(self.quantizer, Y)
+        nq = yr.shape[0]
+        m, kbar = self.quantizer.derived_codebooks_.shape[:2]
+        small = np.empty((nq, m, kbar), np.float32)
+        q = np.empty((nq, m, kbar), np.uint8)
+        qmin = np.empty(nq)
+        qmax = np.empty(nq)
+        _lib.check(_lib.lib().dpq_debug_quantize_tables(self._handle().raw, _lib.ptr(yr), nq, int(r2),
+                                                        _lib.ptr(small), _lib.ptr(q), _lib.ptr(qmin),
+                                                        _lib.ptr(qmax)))
+        return small, q, qmin, qmax
+
+    def candidate_counts(self, Y, r2: int):
+        """b* and |candidates| per query (twopass.py:171-201, 295-302)."""
+        Y = check_array(Y, dtype=np.float32, order="C")
+        yr = rotated_queries(self.quantizer, Y)
+        nq = yr.shape[0]
+        bstar = np.empty(nq, np.int32)
+        ncand = np.empty(nq, np.int64)
+        _lib.check(_lib.lib().dpq_debug_candidates(self._handle().raw, _lib.ptr(yr), nq, int(r2),
+                                                   _lib.ptr(bstar), _lib.ptr(ncand)))
+        return bstar, ncand
+
+    def full_tables(self, Y):
+        """compute_tables(yr, codebooks_) per query: (nq, m, k) f32."""
+        Y = check_array(Y, dtype=np.float32, order="C")
+        yr = rotated_queries(self.quantizer, Y)
+        m, k = self.quantizer.codebooks_.shape[:2]
+        out = np.empty((yr.shape[0], m, k), np.float32)
+        _lib.check(_lib.lib().dpq_debug_full_tables(self._handle().raw, _lib.ptr(yr), yr.shape[0],
+                                                    _lib.ptr(out)))
+        return out
+
+    # -- persistence helpers kept from the reference (flat.py:112-126) -----
+    def validate(self) -> None:
+        from .errors import InvariantError
+
+        if hasattr(self.quantizer, "validate"):
+            self.quantizer.validate()
+        if hasattr(self, "codes_"):
+            k = self.quantizer.k_
+            codes = self.codes_
+            if codes.min(initial=0) < 0 or codes.max(initial=0) >= k:
+                raise InvariantError(f"stored codes fall outside [0, {k})")

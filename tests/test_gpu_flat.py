@@ -1,0 +1,224 @@
+"""Parity of the CUDA flat path (libdpq.so through the C ABI) with the
+reference (golden fixtures) and with the CPU oracle on seeded inputs.
+
+Bar: bit-exact.  Small tables, 8-bit tables, qmin/qmax, candidate counts,
+result ids and f64 distances must equal the reference's bits; the
+north_star tolerance (1e-4 relative) is therefore met with margin 0.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import FLAT_CASES, load_golden
+from oracle import derived_search as O
+from paper_1905_06900_b200 import datagen
+from paper_1905_06900_b200.flat import FlatIndex
+
+pytestmark = pytest.mark.gpu
+
+
+def _index(g):
+    return FlatIndex.from_arrays(g["codebooks"], g["derived"], g["codes"], rotation=g.get("rotation"))
+
+
+def _same(a, b):
+    return np.array_equal(np.asarray(a).view(np.uint64), np.asarray(b).view(np.uint64))
+
+
+@pytest.mark.parametrize("name", FLAT_CASES)
+def test_quantized_tables_bitwise_vs_reference(name):
+    g = load_golden(name)
+    idx = _index(g)
+    small, q, qmin, qmax = idx.quantized_tables(g["queries"], g["meta"]["r2"])
+    assert np.array_equal(small.view(np.uint32), g["exp_small"].view(np.uint32))
+    assert np.array_equal(q, g["exp_q"])
+    assert np.array_equal(qmin, g["exp_qmin"]) and np.array_equal(qmax, g["exp_qmax"])
+
+
+@pytest.mark.parametrize("name", FLAT_CASES)
+def test_candidate_counts_vs_reference(name):
+    g = load_golden(name)
+    _, ncand = _index(g).candidate_counts(g["queries"], g["meta"]["r2"])
+    assert np.array_equal(ncand, g["exp_ncand"])
+
+
+@pytest.mark.parametrize("name", FLAT_CASES)
+def test_derived_search_bitwise_vs_reference(name):
+    g = load_golden(name)
+    m = g["meta"]
+    d, i = _index(g).search(g["queries"], m["r"], mode="derived", r2=m["r2"])
+    assert np.array_equal(i, g["exp_derived_i"])
+    assert _same(d, g["exp_derived_d"])
+    d2, i2 = _index(g).search(g["queries"], m["r"], mode="derived", r2=m["r2"], capped=False)
+    assert np.array_equal(i2, i) and _same(d2, d)
+
+
+@pytest.mark.parametrize("name", FLAT_CASES)
+def test_conventional_and_full_budget_vs_reference(name):
+    g = load_golden(name)
+    idx = _index(g)
+    if "exp_conv_i" in g:
+        d, i = idx.search(g["queries"], g["meta"]["r"])
+        assert np.array_equal(i, g["exp_conv_i"]) and _same(d, g["exp_conv_d"])
+    if "exp_full_i" in g:
+        r = g["exp_full_i"].shape[1]
+        d, i = idx.search(g["queries"][:4], r, mode="derived", r2=len(g["codes"]), capped=False)
+        assert np.array_equal(i, g["exp_full_i"]) and _same(d, g["exp_full_d"])
+
+
+def test_config1_shape_bitwise_vs_reference(c1_golden):
+    """PQ 4x16 / derived 4x8, N=100k, Q=100, r2=1000, k=100 (config 1)."""
+    g = c1_golden
+    idx = FlatIndex.from_arrays(g["codebooks"], g["derived"], g["codes"])
+    small, q, qmin, qmax = idx.quantized_tables(g["queries"], 1000)
+    assert np.array_equal(q, g["exp_q"]) and np.array_equal(qmax, g["exp_qmax"])
+    _, ncand = idx.candidate_counts(g["queries"], 1000)
+    assert np.array_equal(ncand, g["exp_ncand"])
+    d, i = idx.search(g["queries"], 100, mode="derived", r2=1000)
+    assert np.array_equal(i, g["exp_derived_i"])
+    assert _same(d, g["exp_derived_d"])
+
+
+# ------------------------------------------------------ seeded vs oracle --
+
+def _model(rng, m, k, kbar, dsub):
+    """Random valid model: full codebook rows, derived = group means over
+    the low-bit groups (so low bits index the derived codebook)."""
+    cb = rng.normal(size=(m, k, dsub)).astype(np.float32) * 3
+    der = np.stack([np.stack([cb[j][np.arange(k) % kbar == g].mean(axis=0) for g in range(kbar)])
+                    for j in range(m)]).astype(np.float32)
+    return cb, der
+
+
+def _encode(cb, X):
+    m, k, dsub = cb.shape
+    out = np.empty((X.shape[0], m), np.uint16 if k > 256 else np.uint8)
+    for j in range(m):
+        sub = X[:, j * dsub:(j + 1) * dsub].astype(np.float64)
+        c = cb[j].astype(np.float64)
+        d2 = (sub * sub).sum(1)[:, None] - 2 * sub @ c.T + (c * c).sum(1)[None, :]
+        out[:, j] = d2.argmin(1)
+    return out
+
+
+def _oracle(cb, der, codes, Y, r, r2):
+    return O.flat_search(cb, der, codes, Y, r, "derived", r2)
+
+
+CASES = [
+    # m, k, kbar, dsub, n, nq, r, r2
+    (4, 256, 16, 8, 5000, 40, 10, 300),
+    (1, 64, 8, 4, 3000, 9, 5, 50),
+    (3, 512, 32, 6, 4000, 70, 20, 400),
+    (5, 256, 64, 3, 3000, 33, 7, 100),
+    (8, 256, 256, 4, 3000, 20, 10, 250),
+    (2, 1024, 256, 16, 6000, 130, 100, 1000),
+    (4, 4096, 256, 32, 20000, 65, 100, 1000),
+    (6, 128, 8, 7, 2000, 12, 3, 3),
+]
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_seeded_random_models_vs_oracle(case):
+    m, k, kbar, dsub, n, nq, r, r2 = case
+    rng = np.random.default_rng(hash(case) % 2**32)
+    cb, der = _model(rng, m, k, kbar, dsub)
+    X = (cb[np.arange(m)[None, :], rng.integers(0, k, size=(n, m))].reshape(n, m * dsub)
+         + rng.normal(scale=0.5, size=(n, m * dsub))).astype(np.float32)
+    codes = _encode(cb, X)
+    Y = (X[rng.integers(0, n, size=nq)] + rng.normal(scale=0.3, size=(nq, m * dsub))).astype(np.float32)
+    d0, i0 = _oracle(cb, der, codes, Y, r, r2)
+    d1, i1 = FlatIndex.from_arrays(cb, der, codes).search(Y, r, mode="derived", r2=r2)
+    assert np.array_equal(i0, i1)
+    assert _same(d0, d1)
+
+
+def test_edge_cases_vs_oracle():
+    rng = np.random.default_rng(7)
+    cb, der = _model(rng, 4, 256, 16, 4)
+    # N=1; r2 > N; r > N (padding)
+    for n, r, r2 in [(1, 1, 1), (1, 5, 10), (7, 10, 50), (300, 300, 300), (300, 50, 5000)]:
+        codes = rng.integers(0, 256, size=(n, 4)).astype(np.uint8)
+        Y = rng.normal(size=(5, 16)).astype(np.float32) * 3
+        d0, i0 = _oracle(cb, der, codes, Y, r, r2)
+        d1, i1 = FlatIndex.from_arrays(cb, der, codes).search(Y, r, mode="derived", r2=r2)
+        assert np.array_equal(i0, i1) and _same(d0, d1), (n, r, r2)
+    # all codes identical: qmax == qmin (degenerate zeros), every row refined,
+    # all distances tie -> ids ascending
+    codes = np.tile(rng.integers(0, 256, size=(1, 4)), (500, 1)).astype(np.uint8)
+    Y = rng.normal(size=(4, 16)).astype(np.float32)
+    d0, i0 = _oracle(cb, der, codes, Y, 20, 10 + 20)
+    d1, i1 = FlatIndex.from_arrays(cb, der, codes).search(Y, 20, mode="derived", r2=30)
+    assert np.array_equal(i0, i1) and _same(d0, d1)
+    assert np.array_equal(i1[0], np.arange(20))
+    # many duplicate codes: (dist, id) tie-breaking inside the top-r
+    codes = rng.integers(0, 4, size=(2000, 4)).astype(np.uint8)
+    d0, i0 = _oracle(cb, der, codes, Y, 50, 200)
+    d1, i1 = FlatIndex.from_arrays(cb, der, codes).search(Y, 50, mode="derived", r2=200)
+    assert np.array_equal(i0, i1) and _same(d0, d1)
+
+
+def _sift_setup(n, nq, seed=3, k=4096):
+    st = datagen.seed_streams(seed)
+    centres = datagen.sift_centres(st["centres"])
+    X = datagen.sift_like(st["database"], centres, n)
+    Y = datagen.sift_like(st["queries"], centres, nq)
+    rng = np.random.default_rng(seed)
+    cb = np.stack([X[rng.choice(n, size=k, replace=False), j * 32:(j + 1) * 32] for j in range(4)])
+    der = np.stack([np.stack([cb[j][np.arange(k) % 256 == g].mean(axis=0) for g in range(256)])
+                    for j in range(4)]).astype(np.float32)
+    codes = rng.integers(0, k, size=(n, 4)).astype(np.uint16)
+    return cb.astype(np.float32), der, codes, Y
+
+
+def test_sampled_guard_path_vs_oracle():
+    """N above the exact-histogram limit: the guard comes from a row sample."""
+    cb, der, codes, Y = _sift_setup(200_000, 6)
+    d0, i0 = _oracle(cb, der, codes, Y, 100, 1000)
+    idx = FlatIndex.from_arrays(cb, der, codes)
+    d1, i1 = idx.search(Y, 100, mode="derived", r2=1000)
+    assert np.array_equal(i0, i1) and _same(d0, d1)
+
+
+def test_forced_exact_redo_and_overflow(monkeypatch):
+    """Tiny guard sample (guards too tight -> exact redo) and a tiny emit
+    capacity (overflow -> grow and rerun) still give the exact answer."""
+    cb, der, codes, Y = _sift_setup(120_000, 5, seed=4)
+    d0, i0 = _oracle(cb, der, codes, Y, 50, 800)
+    monkeypatch.setenv("DPQ_GUARD_SAMPLE", "16")
+    monkeypatch.setenv("DPQ_EXACT_LIMIT", "0")
+    monkeypatch.setenv("DPQ_EMIT_CAP", "32")
+    idx = FlatIndex.from_arrays(cb, der, codes)
+    d1, i1 = idx.search(Y, 50, mode="derived", r2=800)
+    assert np.array_equal(i0, i1) and _same(d0, d1)
+    assert idx._handle().counters()["fallbacks"] > 0
+
+
+def test_batch_invariance():
+    g = load_golden("pq_blobs")
+    idx = _index(g)
+    ref = idx.search(g["queries"], 10, mode="derived", r2=300)
+    for b in (1, 5, 64, 1024):
+        idx._handle().set_batch(b)
+        d, i = idx.search(g["queries"], 10, mode="derived", r2=300)
+        assert np.array_equal(i, ref[1]) and _same(d, ref[0])
+
+
+def test_timings_and_errors():
+    g = load_golden("pq_blobs")
+    idx = _index(g)
+    _, _, t = idx.search(g["queries"][:3], 5, mode="derived", r2=100, return_timings=True)
+    assert set(t) == {"index_us", "tables_us", "scan_us", "refine_us"}
+    assert np.all(t["index_us"] == 0.0) and np.all(t["refine_us"] > 0.0)
+    _, _, t = idx.search(g["queries"][:3], 5, return_timings=True)
+    assert np.all(t["refine_us"] == 0.0)
+    with pytest.raises(ValueError, match="must not exceed"):
+        idx.search(g["queries"], 11, mode="derived", r2=10)
+    with pytest.raises(ValueError, match="r2"):
+        idx.search(g["queries"], 5, mode="derived")
+    with pytest.raises(ValueError, match="mode"):
+        idx.search(g["queries"], 5, mode="hybrid")
+    dists, ids = idx.search(g["queries"][:1], len(g["codes"]) + 10)
+    assert (ids[0] >= 0).sum() == len(g["codes"]) and np.isinf(dists[0, len(g["codes"]):]).all()
