@@ -320,6 +320,7 @@ def run_ours(args):
         "cpu_baseline": cpu, "parity_sample": parity,
         "e2e": e2e, "gpu_launches": int(launches),
         "candidates_per_query": round(refined / max(1, args.steps * Bq), 1),
+        "emitted_per_query": round((c1["emitted"] - c0["emitted"]) / max(1, args.steps * Bq), 1),
         "clocks": clocks, "setup_s": round(wl["setup_s"], 1),
     }
     print(json.dumps(result), flush=True)

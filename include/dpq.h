@@ -175,9 +175,10 @@ int dpq_debug_full_tables(dpq_index_t* index, const float* yr, int64_t nq,
  * [0] tables (K1), [1] sample+guard, [2] scan (K2), [3] threshold (K3),
  * [4] refine+top-r (K6), [5] fallback, [6] whole batch.                    */
 int dpq_last_phase_ms(dpq_index_t* index, float* ms7);
-/* Counters since creation: kernel launches, queries searched, code rows
- * scanned (sum over queries), candidates refined, exact fallbacks.         */
-int dpq_counters(dpq_index_t* index, int64_t* out5);
+/* Counters since creation (8 x i64): kernel launches, queries searched,
+ * code rows scanned (sum over queries), candidates refined, exact-redo
+ * rounds, first-pass rows emitted (score <= guard), 0, 0.                  */
+int dpq_counters(dpq_index_t* index, int64_t* out8);
 
 #ifdef __cplusplus
 }

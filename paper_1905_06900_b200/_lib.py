@@ -129,9 +129,10 @@ class Handle:
         return out
 
     def counters(self) -> dict:
-        out = np.zeros(5, dtype=np.int64)
+        out = np.zeros(8, dtype=np.int64)
         check(lib().dpq_counters(self.raw, ptr(out)))
-        return dict(zip(("launches", "queries", "rows_scanned", "refined", "fallbacks"), out.tolist()))
+        return dict(zip(("launches", "queries", "rows_scanned", "refined", "fallbacks", "emitted"),
+                        out.tolist()))
 
     def set_timing(self, on: bool) -> None:
         check(lib().dpq_set_timing(self.raw, int(bool(on))))

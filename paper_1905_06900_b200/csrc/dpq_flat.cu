@@ -53,7 +53,7 @@ const char* last_error() { return g_last_error.c_str(); }
     if (rc_ != DPQ_OK) return rc_; \
   } while (0)
 
-static constexpr int kScanThreads = 512;
+static constexpr int kScanThreads = 1024;
 static constexpr int kTopThreads = 256;
 
 template <class T>
@@ -110,6 +110,7 @@ int ensure_ws(Index* h, int nslot, int r, int ystride) {
     DPQ_TRY(dmalloc(&w.flags, (size_t)qb));
     DPQ_TRY(dmalloc(&w.only, (size_t)tiles * qt));
     DPQ_TRY(dmalloc(&w.tile_list, (size_t)tiles));
+    if (!w.counter) DPQ_TRY(dmalloc(&w.counter, 4));
     DPQ_TRY(dmalloc(&w.slot_query, (size_t)tiles * qt));
     DPQ_TRY(dmalloc(&w.slot_probe, (size_t)tiles * qt));
     DPQ_TRY(dmalloc(&w.slot_pre_off, (size_t)qb));
@@ -200,25 +201,39 @@ static int launch_hist(Index* h, int ntiles, const int* tile_list, int64_t strid
                       : launch_hist_t<8>(h, ntiles, tile_list, stride, nsamp, plane);
 }
 
+static int num_sms(Index* h) {
+  static int sms = 0;
+  if (!sms) {
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device) != cudaSuccess || sms < 1) sms = 148;
+  }
+  return sms;
+}
+
 template <int MPAD>
 static int launch_emit_t(Index* h, EmitArgs ea, int ntiles, int64_t rows) {
   using G = ScanGeom<MPAD>;
-  const size_t smem = G::LUT_BYTES + (size_t)(kScanThreads / 32) * 32 * 16;
+  constexpr int NW = kScanThreads / 32;
+  const size_t smem = G::LUT_BYTES + (size_t)NW * 32 * 16 + (size_t)NW * kWarpBuf * 8 + (size_t)NW * G::QT * 4;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_scan_emit<MPAD, kScanThreads>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  // ~2 waves of one 512-thread CTA per SM across all query tiles.
-  int64_t want = std::max<int64_t>(1, (148 * 2 + ntiles - 1) / ntiles);
-  int64_t per = (rows + want - 1) / want;
-  const int64_t minper = (int64_t)G::CHUNK_ROWS * (kScanThreads / 32) * 4;
-  per = std::max(per, minper);
+  // Persistent CTAs (one per SM) pulling ~32 units each from a counter.
+  const int sms = num_sms(h);
+  const int64_t min_rows = (int64_t)G::CHUNK_ROWS * NW;
+  int64_t upt = std::max<int64_t>(1, (32LL * sms + ntiles - 1) / ntiles);
+  int64_t per = (rows + upt - 1) / upt;
+  per = std::max(per, min_rows);
   per = (per + G::CHUNK_ROWS - 1) / G::CHUNK_ROWS * G::CHUNK_ROWS;
-  const int64_t ctas = (rows + per - 1) / per;
+  upt = std::max<int64_t>(1, (rows + per - 1) / per);
   ea.rows_per_cta = per;
-  dim3 grid((unsigned)std::max<int64_t>(ctas, 1), ntiles);
+  ea.units_per_tile = (int)upt;
+  ea.n_units = (int)(upt * ntiles);
+  ea.unit_counter = h->ws.counter;
+  DPQ_CUDA(cudaMemsetAsync(h->ws.counter, 0, sizeof(unsigned), h->stream));
+  const int grid = (int)std::min<int64_t>(sms, ea.n_units);
   k_scan_emit<MPAD, kScanThreads><<<grid, kScanThreads, smem, h->stream>>>(ea);
   DPQ_LAUNCHED(h);
   return DPQ_OK;
@@ -330,7 +345,7 @@ static int flat_first_pass(Index* h, int nb, int r2) {
     h->counters[2] += (int64_t)nb * n;
     if (first) ev_rec(h, 3);
     k_threshold<256><<<nb, 256, 0, h->stream>>>(w.emit, w.emit_cnt, w.cap, w.guard_b, r2, nullptr,
-                                                w.bstar, w.ncand, w.flags, nullptr);
+                                                w.bstar, w.ncand, w.flags, nullptr, h->d_nemit);
     DPQ_LAUNCHED(h);
     if (first) ev_rec(h, 4);
     first = false;
@@ -545,9 +560,11 @@ int index_common_init(Index* h, int device, int m, int k, int kbar, int dsub, co
   DPQ_TRY(dmalloc(&h->cb, (size_t)m * k * dsub));
   DPQ_TRY(dmalloc(&h->dcb, (size_t)m * kbar * dsub));
   DPQ_TRY(dmalloc(&h->d_nref, 1));
+  DPQ_TRY(dmalloc(&h->d_nemit, 1));
   DPQ_CUDA(cudaMemcpy(h->cb, codebooks, (size_t)m * k * dsub * 4, cudaMemcpyHostToDevice));
   DPQ_CUDA(cudaMemcpy(h->dcb, derived, (size_t)m * kbar * dsub * 4, cudaMemcpyHostToDevice));
   DPQ_CUDA(cudaMemset(h->d_nref, 0, 8));
+  DPQ_CUDA(cudaMemset(h->d_nemit, 0, 8));
   return DPQ_OK;
 }
 
@@ -557,10 +574,10 @@ void index_free(Index* h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   Workspace& w = h->ws;
   void* dev[] = {h->cb, h->dcb, h->codes, h->plane, h->own_prefix ? h->prefix : nullptr, h->centers,
-                 h->offsets, h->sorted_ids, h->d_nref, w.y, w.small, w.q8, w.qmin, w.qmax, w.bounds,
+                 h->offsets, h->sorted_ids, h->d_nref, h->d_nemit, w.y, w.small, w.q8, w.qmin, w.qmax, w.bounds,
                  w.lut, w.hist, w.hist_i, w.guard_b, w.gword, w.emit_cnt, w.emit, w.bstar, w.ncand,
                  w.flags, w.only, w.tile_list, w.out_d, w.out_i, w.tables, w.slot_query, w.slot_probe,
-                 w.slot_pre_off, w.slot_pre_len};
+                 w.slot_pre_off, w.slot_pre_len, w.counter};
   for (void* p : dev)
     if (p) cudaFree(p);
   void* host[] = {w.h_y, w.h_d, w.h_i, w.h_flags, w.h_cnt};
@@ -792,14 +809,16 @@ int dpq_last_phase_ms(dpq_index_t* index, float* ms7) {
   return DPQ_OK;
 }
 
-int dpq_counters(dpq_index_t* index, int64_t* out5) {
+int dpq_counters(dpq_index_t* index, int64_t* out8) {
   Index* h = reinterpret_cast<Index*>(index);
-  if (!h || !out5) { set_error("null argument"); return DPQ_ERR_ARG; }
-  unsigned long long nref = 0;
+  if (!h || !out8) { set_error("null argument"); return DPQ_ERR_ARG; }
+  unsigned long long nref = 0, nemit = 0;
   cudaSetDevice(h->device);
-  cudaMemcpy(&nref, h->d_nref, 8, cudaMemcpyDeviceToHost);
+  DPQ_CUDA(cudaMemcpy(&nref, h->d_nref, 8, cudaMemcpyDeviceToHost));
+  DPQ_CUDA(cudaMemcpy(&nemit, h->d_nemit, 8, cudaMemcpyDeviceToHost));
   h->counters[3] = (int64_t)nref;
-  for (int i = 0; i < 5; ++i) out5[i] = h->counters[i];
+  h->counters[5] = (int64_t)nemit;
+  for (int i = 0; i < 8; ++i) out8[i] = h->counters[i];
   return DPQ_OK;
 }
 

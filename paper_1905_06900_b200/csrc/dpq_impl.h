@@ -40,6 +40,7 @@ struct Workspace {
   uint8_t* flags = nullptr;
   uint8_t* only = nullptr;
   int* tile_list = nullptr;
+  unsigned* counter = nullptr;  // persistent-scan unit counter
   double* out_d = nullptr;
   int64_t* out_i = nullptr;
   float* tables = nullptr;    // conventional full tables
@@ -83,8 +84,9 @@ struct Index {
   bool timing = false;
   cudaEvent_t ev[8] = {};
   float phase_ms[PH_N] = {};
-  int64_t counters[5] = {};  // launches, queries, rows scanned, refined, fallbacks
+  int64_t counters[8] = {};  // launches, queries, rows scanned, refined, fallbacks, emitted
   unsigned long long* d_nref = nullptr;
+  unsigned long long* d_nemit = nullptr;
   size_t emit_budget = (size_t)16 << 30;  // bytes for emit buffers
   // guard sampling (env DPQ_GUARD_SAMPLE / DPQ_EXACT_LIMIT / DPQ_EMIT_CAP
   // override them so tests can force the exact-redo and overflow paths)

@@ -250,7 +250,23 @@ struct EmitArgs {
   uint32_t* emit_cnt;
   uint64_t* emit;
   uint32_t cap;
+  unsigned* unit_counter;       // zeroed before launch (persistent scheduling)
+  int n_units;                  // tiles * units_per_tile
+  int units_per_tile;
 };
+
+// Persistent scan.  Work unit = (query tile, contiguous row range); CTAs
+// (one per SM, 32 warps) pull units from a global counter, so the grid never
+// has a partial last wave.  Per unit the CTA loads the tile's 8-bit tables
+// (128 KB) into shared memory once and its warps stream the unit's rows.
+//
+// Hit staging: a warp appends the rows that pass a guard to a private
+// shared-memory buffer (positions from ballot/popc, no atomics) and flushes
+// it when it may overflow or at the end of the unit: per-query counts in
+// shared memory, ONE global atomicAdd per query present in the buffer to
+// reserve space in that query's emit list, then the stores.  The common path
+// is 4 LDS + ~11 ALU per code and one warp vote per 4 codes.
+constexpr int kWarpBuf = 256;  // staged hits per warp (2 KB)
 
 template <int MPAD, int NT>
 __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
@@ -259,65 +275,137 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   uint8_t* slut = smem;
   uint4* stage = reinterpret_cast<uint4*>(smem + G::LUT_BYTES);
-  const int tile = a.tile_list ? a.tile_list[blockIdx.y] : blockIdx.y;
-  const uint4* src = reinterpret_cast<const uint4*>(a.lut + (int64_t)tile * G::LUT_BYTES / 2);
-  for (int i = threadIdx.x; i < G::LUT_BYTES / 16; i += NT) reinterpret_cast<uint4*>(slut)[i] = src[i];
-  __syncthreads();
+  uint64_t* hbuf_all = reinterpret_cast<uint64_t*>(smem + G::LUT_BYTES + NW * 32 * 16);
+  uint32_t* hcnt_all = reinterpret_cast<uint32_t*>(hbuf_all + NW * kWarpBuf);
+  __shared__ int s_unit;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int lic = lane % G::LPC, half = lane / G::LPC;
-  const int slot0 = tile * G::QT + 2 * lic;
-  const uint32_t gw = (uint32_t)a.gword[slot0] | ((uint32_t)a.gword[slot0 + 1] << 16);
   const uint8_t* L = slut + lic * 4;
-  // Logical range [r0, r1); loads start at the 512-B aligned row r0a and
-  // rows outside the range are never emitted.
-  const int64_t r0 = a.row_begin + (int64_t)blockIdx.x * a.rows_per_cta;
-  const int64_t r1 = min(a.row_end, r0 + a.rows_per_cta);
-  if (r0 >= r1) return;
-  const int64_t r0a = r0 & ~(int64_t)(G::CHUNK_ROWS - 1);
-  const int64_t nchunks = (r1 - r0a + G::CHUNK_ROWS - 1) / G::CHUNK_ROWS;
-  int64_t c = warp;
-  if (c >= nchunks) return;
   uint4* wst = stage + warp * 32;
-  auto chunk_ptr = [&](int64_t ci) {
-    return reinterpret_cast<const uint4*>(a.plane + (r0a + ci * G::CHUNK_ROWS) * MPAD) + lane;
-  };
-  auto emit_one = [&](int slot, int64_t row, uint32_t score) {
-    const int qe = a.slot_query ? a.slot_query[slot] : slot;
-    const uint32_t probe = a.slot_probe ? (uint32_t)a.slot_probe[slot] : 0u;
-    const uint32_t pos = atomicAdd(a.emit_cnt + qe, 1u);
-    if (pos < a.cap) a.emit[(int64_t)qe * a.cap + pos] = pack_emit(row, probe, score);
-  };
-  auto process = [&](uint32_t w0, uint32_t w1, int64_t row) {
-    const uint32_t sum = lut_sum<MPAD>(L, w0, w1);
-    const uint32_t x = gw - sum;
-    if (__builtin_expect((x & 0x80008000u) != 0u, 0)) {
-      if (row >= r0 && row < r1) {
-        if (x & 0x00008000u) emit_one(slot0, row, sum & 0xFFFFu);
-        if (x & 0x80000000u) emit_one(slot0 + 1, row, sum >> 16);
+  uint64_t* hbuf = hbuf_all + warp * kWarpBuf;
+  uint32_t* hcnt = hcnt_all + warp * G::QT;
+  const uint32_t lt = (1u << lane) - 1u;
+  int cur_tile = -1;
+  for (;;) {
+    __syncthreads();  // previous unit finished by every warp
+    if (threadIdx.x == 0) s_unit = (int)atomicAdd(a.unit_counter, 1u);
+    __syncthreads();
+    const int u = s_unit;
+    if (u >= a.n_units) break;
+    const int tix = u / a.units_per_tile;
+    const int64_t chunk_u = u % a.units_per_tile;
+    const int tile = a.tile_list ? a.tile_list[tix] : tix;
+    if (tile != cur_tile) {
+      const uint4* src = reinterpret_cast<const uint4*>(a.lut + (int64_t)tile * G::LUT_BYTES / 2);
+      for (int i = threadIdx.x; i < G::LUT_BYTES / 16; i += NT) reinterpret_cast<uint4*>(slut)[i] = src[i];
+      cur_tile = tile;
+      __syncthreads();
+    }
+    const int slot0 = tile * G::QT + 2 * lic;
+    const uint32_t gw = (uint32_t)a.gword[slot0] | ((uint32_t)a.gword[slot0 + 1] << 16);
+    // Logical range [r0, r1); loads start at the 512-B aligned row r0a and
+    // rows outside the range are never emitted.
+    const int64_t r0 = a.row_begin + chunk_u * a.rows_per_cta;
+    const int64_t r1 = min(a.row_end, r0 + a.rows_per_cta);
+    if (r0 >= r1) continue;
+    const int64_t r0a = r0 & ~(int64_t)(G::CHUNK_ROWS - 1);
+    const int64_t nchunks = (r1 - r0a + G::CHUNK_ROWS - 1) / G::CHUNK_ROWS;
+    int64_t c = warp;
+    if (c >= nchunks) continue;
+    int wc = 0;  // staged hits (warp-uniform)
+    auto chunk_ptr = [&](int64_t ci) {
+      return reinterpret_cast<const uint4*>(a.plane + (r0a + ci * G::CHUNK_ROWS) * MPAD) + lane;
+    };
+    // entry: row offset from r0a (32 b) | local slot << 32 | score << 40
+    auto flush = [&]() {
+      for (int s = lane; s < G::QT; s += 32) hcnt[s] = 0;
+      __syncwarp();
+      for (int i = lane; i < wc; i += 32) atomicAdd(hcnt + ((hbuf[i] >> 32) & 0xFF), 1u);
+      __syncwarp();
+      for (int s = lane; s < G::QT; s += 32) {
+        const uint32_t n = hcnt[s];
+        if (n) {
+          const int slot = tile * G::QT + s;
+          const int qe = a.slot_query ? a.slot_query[slot] : slot;
+          hcnt[s] = atomicAdd(a.emit_cnt + qe, n);
+        }
+      }
+      __syncwarp();
+      for (int i = lane; i < wc; i += 32) {
+        const uint64_t e = hbuf[i];
+        const int s = (int)((e >> 32) & 0xFF);
+        const uint32_t pos = atomicAdd(hcnt + s, 1u);
+        const int slot = tile * G::QT + s;
+        const int qe = a.slot_query ? a.slot_query[slot] : slot;
+        const uint32_t probe = a.slot_probe ? (uint32_t)a.slot_probe[slot] : 0u;
+        if (pos < a.cap)
+          a.emit[(int64_t)qe * a.cap + pos] = pack_emit(r0a + (int64_t)(uint32_t)e, probe, (uint32_t)(e >> 40));
+      }
+      __syncwarp();
+      wc = 0;
+    };
+    // Stage the hits of NC consecutive codes (rows rowb + k*rstep): hm holds
+    // bit 2k (query 2*lic) and 2k+1 (query 2*lic+1) per code k.  One warp
+    // prefix sum of the per-lane hit counts gives every hit its slot.
+    auto stage_hits = [&](uint32_t hm, uint32_t sa, uint32_t sb, uint32_t sc2, uint32_t sd, int64_t rowb, int rstep) {
+      const int cnt = __popc(hm);
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      if (wc + total > kWarpBuf) flush();
+      int pos = wc + incl - cnt;
+      while (hm) {
+        const int b = __ffs(hm) - 1;
+        hm &= hm - 1;
+        const int k = b >> 1;
+        const uint32_t sk = k == 0 ? sa : (k == 1 ? sb : (k == 2 ? sc2 : sd));
+        const uint32_t sc = (b & 1) ? (sk >> 16) : (sk & 0xFFFFu);
+        const uint64_t roff = (uint64_t)(uint32_t)(rowb + (int64_t)k * rstep - r0a);
+        hbuf[pos++] = roff | ((uint64_t)(2 * lic + (b & 1)) << 32) | ((uint64_t)sc << 40);
+      }
+      wc += total;
+    };
+    auto hit_bits = [&](uint32_t x, int k, int64_t row) -> uint32_t {
+      const bool ok = row >= r0 && row < r1;
+      return ok ? (((x >> 15) & 1u) | ((x >> 30) & 2u)) << (2 * k) : 0u;
+    };
+    uint4 nxt = ldg_stream(chunk_ptr(c));
+    for (; c < nchunks; c += NW) {
+      __syncwarp();
+      wst[lane] = nxt;
+      __syncwarp();
+      if (c + NW < nchunks) nxt = ldg_stream(chunk_ptr(c + NW));
+      const int64_t rb = r0a + c * G::CHUNK_ROWS;
+#pragma unroll 2
+      for (int i = 0; i < 32; ++i) {
+        const uint4 v = wst[i];
+        if (MPAD == 4) {
+          const uint32_t s0 = lut_sum<MPAD>(L, v.x, 0), s1 = lut_sum<MPAD>(L, v.y, 0);
+          const uint32_t s2 = lut_sum<MPAD>(L, v.z, 0), s3 = lut_sum<MPAD>(L, v.w, 0);
+          const uint32_t x0 = gw - s0, x1 = gw - s1, x2 = gw - s2, x3 = gw - s3;
+          if (__any_sync(0xffffffffu, ((x0 | x1 | x2 | x3) & 0x80008000u) != 0u)) {
+            const int64_t rw = rb + 4 * i;
+            const uint32_t hm = hit_bits(x0, 0, rw) | hit_bits(x1, 1, rw + 1) | hit_bits(x2, 2, rw + 2) |
+                                hit_bits(x3, 3, rw + 3);
+            stage_hits(hm, s0, s1, s2, s3, rw, 1);
+          }
+        } else {
+          const uint32_t w0 = half ? v.z : v.x;
+          const uint32_t w1 = half ? v.w : v.y;
+          const uint32_t s0 = lut_sum<MPAD>(L, w0, w1);
+          const uint32_t x0 = gw - s0;
+          if (__any_sync(0xffffffffu, (x0 & 0x80008000u) != 0u)) {
+            const int64_t rw = rb + 2 * i + half;
+            stage_hits(hit_bits(x0, 0, rw), s0, 0u, 0u, 0u, rw, 1);
+          }
+        }
       }
     }
-  };
-  uint4 nxt = ldg_stream(chunk_ptr(c));
-  for (; c < nchunks; c += NW) {
-    __syncwarp();
-    wst[lane] = nxt;
-    __syncwarp();
-    if (c + NW < nchunks) nxt = ldg_stream(chunk_ptr(c + NW));
-    const int64_t rb = r0a + c * G::CHUNK_ROWS;
-#pragma unroll 4
-    for (int i = 0; i < 32; ++i) {
-      const uint4 v = wst[i];
-      if (MPAD == 4) {
-        process(v.x, 0, rb + 4 * i + 0);
-        process(v.y, 0, rb + 4 * i + 1);
-        process(v.z, 0, rb + 4 * i + 2);
-        process(v.w, 0, rb + 4 * i + 3);
-      } else {
-        const uint32_t w0 = half ? v.z : v.x;
-        const uint32_t w1 = half ? v.w : v.y;
-        process(w0, w1, rb + 2 * i + half);
-      }
-    }
+    if (wc > 0) flush();
   }
 }
 
@@ -360,7 +448,7 @@ __global__ void __launch_bounds__(NT)
                 uint32_t cap, const uint16_t* __restrict__ guard_b, int r2,
                 const uint8_t* __restrict__ only, int32_t* __restrict__ bstar,
                 int64_t* __restrict__ ncand, uint8_t* __restrict__ flags,
-                int32_t* __restrict__ hist_out) {
+                int32_t* __restrict__ hist_out, unsigned long long* __restrict__ n_emitted) {
   __shared__ uint32_t h[256];
   const int q = blockIdx.x;
   if (only && !only[q]) return;
@@ -370,6 +458,7 @@ __global__ void __launch_bounds__(NT)
     return;
   }
   for (int i = threadIdx.x; i < 256; i += NT) h[i] = 0;
+  if (n_emitted && threadIdx.x == 0) atomicAdd(n_emitted, (unsigned long long)n);
   __syncthreads();
   const uint64_t* e = emit + (int64_t)q * cap;
   for (uint32_t i = threadIdx.x; i < n; i += NT) atomicAdd(h + emit_score(e[i]), 1u);
