@@ -213,7 +213,7 @@ template <int MPAD>
 static int launch_emit_t(Index* h, EmitArgs ea, int ntiles, int64_t rows) {
   using G = ScanGeom<MPAD>;
   constexpr int NW = kScanThreads / 32;
-  const size_t smem = G::LUT_BYTES + (size_t)NW * 32 * 16 + (size_t)NW * kWarpBuf * 8 + (size_t)NW * G::QT * 4;
+  const size_t smem = emit_smem_bytes<MPAD>();
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_scan_emit<MPAD, kScanThreads>,

@@ -58,10 +58,23 @@ struct ScanGeom {
   static constexpr int QT = MPAD == 4 ? 64 : 32;  // queries per tile
   static constexpr int LPC = QT / 2;              // lanes per code
   static constexpr int CPW = 32 / LPC;            // codes per warp step
-  static constexpr int ROWB = QT * 2;             // bytes per table row
+  static constexpr int ROWB = QT * 2;             // bytes of one subspace row
+  static constexpr int SPR = 256 / ROWB;          // subspaces per 256-B row
   static constexpr int LUT_BYTES = MPAD * 256 * ROWB;  // 128 KB
   static constexpr int CHUNK_ROWS = 512 / MPAD;   // rows per 512-B warp load
 };
+
+// LUT layout of one query tile (u16 units):
+//   [MPAD/SPR tables of 64 KB][256 rows of 256 B][SPR subspaces][QT queries]
+// Subspace j, table row i, query qq ->
+//   ((j / SPR) * 256 + i) * (SPR * QT) + (j % SPR) * QT + qq
+// With the tile at a 64-KB aligned shared address, the byte address of
+// lane lic's word for row i of subspace j is
+//   base | i << 8 | (j % SPR) * ROWB | lic * 4   (+ (j / SPR) * 64 KB)
+// i.e. ONE byte-permute of the code word into the lane's base word.
+__host__ __device__ __forceinline__ int64_t lut_index(int j, int i, int qq, int spr, int qt) {
+  return ((int64_t)(j / spr) * 256 + i) * (spr * qt) + (int64_t)(j % spr) * qt + qq;
+}
 
 // ============================================================================
 // K1: small tables, qmin/qmax, 8-bit quantization, scan-layout LUT.
@@ -147,13 +160,14 @@ __global__ void __launch_bounds__(256) k_small_tables(TablesArgs a) {
     a.qmax_out[s] = degenerate ? qmin : qmax;
   }
   __syncthreads();
-  // scan-layout LUT: [tile][j][i][qq]
+  // scan-layout LUT (see lut_index)
   const int tile = s / a.qt, qq = s % a.qt;
-  uint16_t* L = a.lut + (int64_t)tile * a.mpad * 256 * a.qt + qq;
+  const int spr = 256 / (2 * a.qt);
+  uint16_t* L = a.lut + (int64_t)tile * a.mpad * 256 * a.qt;
   for (int e = tid; e < a.mpad * 256; e += 256) {
     const int j = e >> 8, i = e & 255;
     uint16_t v = (j < a.m && i < a.kbar) ? (uint16_t)q8[j * a.kbar + i] : (uint16_t)0;
-    L[(int64_t)e * a.qt] = v;
+    L[lut_index(j, i, qq, spr, a.qt)] = v;
   }
 }
 
@@ -164,13 +178,32 @@ __global__ void __launch_bounds__(256) k_small_tables(TablesArgs a) {
 // ============================================================================
 template <int MPAD>
 __device__ __forceinline__ uint32_t lut_sum(const uint8_t* L, uint32_t w0, uint32_t w1) {
-  constexpr int ROWB = ScanGeom<MPAD>::ROWB;
+  // L = tile base + lic * 4 (generic addressing; used off the hot path)
+  using G = ScanGeom<MPAD>;
   uint32_t s = 0;
 #pragma unroll
   for (int j = 0; j < MPAD; ++j) {
     const uint32_t w = j < 4 ? w0 : w1;
     const uint32_t idx = (w >> (8 * (j & 3))) & 0xFFu;
-    s += lds32(L + (j * 256 + idx) * ROWB);
+    s += lds32(L + (j / G::SPR) * 65536 + (idx << 8) + (j % G::SPR) * G::ROWB);
+  }
+  return s;
+}
+
+// Hot-path variant: base = 64-KB aligned shared address | lic * 4.
+template <int MPAD>
+__device__ __forceinline__ uint32_t lut_sum_fast(uint32_t base, uint32_t w0, uint32_t w1) {
+  using G = ScanGeom<MPAD>;
+  uint32_t s = 0;
+#pragma unroll
+  for (int j = 0; j < MPAD; ++j) {
+    const uint32_t w = j < 4 ? w0 : w1;
+    // result bytes: [base.b0 | (j%SPR)*ROWB, w.b(j&3), base.b2, base.b3]
+    const uint32_t a = __byte_perm(w, base + (j % G::SPR) * G::ROWB, 0x7604u | ((j & 3) << 4));
+    uint32_t v;
+    if (j / G::SPR == 0) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    else asm volatile("ld.shared.u32 %0, [%1+65536];" : "=r"(v) : "r"(a));
+    s += v;
   }
   return s;
 }
@@ -266,21 +299,36 @@ struct EmitArgs {
 // shared memory, ONE global atomicAdd per query present in the buffer to
 // reserve space in that query's emit list, then the stores.  The common path
 // is 4 LDS + ~11 ALU per code and one warp vote per 4 codes.
-constexpr int kWarpBuf = 256;  // staged hits per warp (2 KB)
+constexpr int kWarpBuf = 128;  // staged hits per warp (1 KB)
+constexpr uint32_t kLutShared = 0x10000;  // LUT at shared address 64 KB
+
+template <int MPAD, int NT>
+__host__ __device__ constexpr int emit_low_bytes() {
+  // stage + hit buffers + per-warp counters, all below the LUT
+  return (NT / 32) * (32 * 16 + kWarpBuf * 8 + ScanGeom<MPAD>::QT * 4);
+}
+// dynamic smem request: enough to reach the end of the LUT whatever the
+// (small) offset of the dynamic window inside the CTA's shared space
+template <int MPAD>
+__host__ __device__ constexpr int emit_smem_bytes() {
+  return (int)kLutShared + ScanGeom<MPAD>::LUT_BYTES;
+}
 
 template <int MPAD, int NT>
 __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
   using G = ScanGeom<MPAD>;
   constexpr int NW = NT / 32;
   extern __shared__ __align__(16) uint8_t smem[];
-  uint8_t* slut = smem;
-  uint4* stage = reinterpret_cast<uint4*>(smem + G::LUT_BYTES);
-  uint64_t* hbuf_all = reinterpret_cast<uint64_t*>(smem + G::LUT_BYTES + NW * 32 * 16);
-  uint32_t* hcnt_all = reinterpret_cast<uint32_t*>(hbuf_all + NW * kWarpBuf);
   __shared__ int s_unit;
+  const uint32_t dyn = (uint32_t)__cvta_generic_to_shared(smem);
+  if (dyn + emit_low_bytes<MPAD, NT>() > kLutShared) __trap();  // layout invariant
+  uint8_t* slut = smem + (kLutShared - dyn);
+  uint4* stage = reinterpret_cast<uint4*>(smem);
+  uint64_t* hbuf_all = reinterpret_cast<uint64_t*>(smem + NW * 32 * 16);
+  uint32_t* hcnt_all = reinterpret_cast<uint32_t*>(hbuf_all + NW * kWarpBuf);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int lic = lane % G::LPC, half = lane / G::LPC;
-  const uint8_t* L = slut + lic * 4;
+  const uint32_t lbase = kLutShared | (uint32_t)(lic * 4);
   uint4* wst = stage + warp * 32;
   uint64_t* hbuf = hbuf_all + warp * kWarpBuf;
   uint32_t* hcnt = hcnt_all + warp * G::QT;
@@ -344,34 +392,26 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
       __syncwarp();
       wc = 0;
     };
-    // Stage the hits of NC consecutive codes (rows rowb + k*rstep): hm holds
-    // bit 2k (query 2*lic) and 2k+1 (query 2*lic+1) per code k.  One warp
-    // prefix sum of the per-lane hit counts gives every hit its slot.
-    auto stage_hits = [&](uint32_t hm, uint32_t sa, uint32_t sb, uint32_t sc2, uint32_t sd, int64_t rowb, int rstep) {
-      const int cnt = __popc(hm);
-      int incl = cnt;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
+    // Stage hits.  hm bit k = hit of query 2*lic on code k, bit 16+k = hit of
+    // query 2*lic+1; code k is row rowb + k (offset roff0 + k from r0a).
+    // One ballot round per hit per lane (nearly always a single round).
+    auto stage_hits = [&](uint32_t hm, uint32_t sa, uint32_t sb, uint32_t sc2, uint32_t sd, uint32_t roff0) {
+      for (;;) {
+        const bool has = hm != 0u;
+        const uint32_t bal = __ballot_sync(0xffffffffu, has);
+        if (!bal) break;
+        if (wc + 32 > kWarpBuf) flush();
+        if (has) {
+          const int b = __ffs(hm) - 1;
+          hm &= hm - 1u;
+          const int k = b & 15, q = b >> 4;
+          const uint32_t sk = k == 0 ? sa : (k == 1 ? sb : (k == 2 ? sc2 : sd));
+          const uint32_t score = q ? (sk >> 16) : (sk & 0xFFFFu);
+          hbuf[wc + __popc(bal & lt)] = (uint64_t)(roff0 + k) | ((uint64_t)(2 * lic + q) << 32) |
+                                        ((uint64_t)score << 40);
+        }
+        wc += __popc(bal);
       }
-      const int total = __shfl_sync(0xffffffffu, incl, 31);
-      if (wc + total > kWarpBuf) flush();
-      int pos = wc + incl - cnt;
-      while (hm) {
-        const int b = __ffs(hm) - 1;
-        hm &= hm - 1;
-        const int k = b >> 1;
-        const uint32_t sk = k == 0 ? sa : (k == 1 ? sb : (k == 2 ? sc2 : sd));
-        const uint32_t sc = (b & 1) ? (sk >> 16) : (sk & 0xFFFFu);
-        const uint64_t roff = (uint64_t)(uint32_t)(rowb + (int64_t)k * rstep - r0a);
-        hbuf[pos++] = roff | ((uint64_t)(2 * lic + (b & 1)) << 32) | ((uint64_t)sc << 40);
-      }
-      wc += total;
-    };
-    auto hit_bits = [&](uint32_t x, int k, int64_t row) -> uint32_t {
-      const bool ok = row >= r0 && row < r1;
-      return ok ? (((x >> 15) & 1u) | ((x >> 30) & 2u)) << (2 * k) : 0u;
     };
     uint4 nxt = ldg_stream(chunk_ptr(c));
     for (; c < nchunks; c += NW) {
@@ -380,27 +420,42 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
       __syncwarp();
       if (c + NW < nchunks) nxt = ldg_stream(chunk_ptr(c + NW));
       const int64_t rb = r0a + c * G::CHUNK_ROWS;
+      // rows of this chunk outside [r0, r1) only at the unit's two ends
+      const bool edge = rb < r0 || rb + G::CHUNK_ROWS > r1;
+      const uint32_t lo = edge ? (uint32_t)max((int64_t)0, r0 - rb) : 0u;
+      const uint32_t hi = edge ? (uint32_t)min((int64_t)G::CHUNK_ROWS, r1 - rb) : (uint32_t)G::CHUNK_ROWS;
+      const uint32_t rboff = (uint32_t)(rb - r0a);
 #pragma unroll 2
       for (int i = 0; i < 32; ++i) {
         const uint4 v = wst[i];
         if (MPAD == 4) {
-          const uint32_t s0 = lut_sum<MPAD>(L, v.x, 0), s1 = lut_sum<MPAD>(L, v.y, 0);
-          const uint32_t s2 = lut_sum<MPAD>(L, v.z, 0), s3 = lut_sum<MPAD>(L, v.w, 0);
+          const uint32_t s0 = lut_sum_fast<MPAD>(lbase, v.x, 0), s1 = lut_sum_fast<MPAD>(lbase, v.y, 0);
+          const uint32_t s2 = lut_sum_fast<MPAD>(lbase, v.z, 0), s3 = lut_sum_fast<MPAD>(lbase, v.w, 0);
           const uint32_t x0 = gw - s0, x1 = gw - s1, x2 = gw - s2, x3 = gw - s3;
           if (__any_sync(0xffffffffu, ((x0 | x1 | x2 | x3) & 0x80008000u) != 0u)) {
-            const int64_t rw = rb + 4 * i;
-            const uint32_t hm = hit_bits(x0, 0, rw) | hit_bits(x1, 1, rw + 1) | hit_bits(x2, 2, rw + 2) |
-                                hit_bits(x3, 3, rw + 3);
-            stage_hits(hm, s0, s1, s2, s3, rw, 1);
+            // bit 15/31 of x = hit; gather them at bits k and 16+k
+            uint32_t hm = ((x0 >> 15) & 0x10001u) | ((x1 >> 14) & 0x20002u) | ((x2 >> 13) & 0x40004u) |
+                          ((x3 >> 12) & 0x80008u);
+            if (edge) {
+              uint32_t ok = 0;
+              for (int k = 0; k < 4; ++k) {
+                const uint32_t r = 4 * i + k;
+                if (r >= lo && r < hi) ok |= 0x10001u << k;
+              }
+              hm &= ok;
+            }
+            stage_hits(hm, s0, s1, s2, s3, rboff + 4 * i);
           }
         } else {
           const uint32_t w0 = half ? v.z : v.x;
           const uint32_t w1 = half ? v.w : v.y;
-          const uint32_t s0 = lut_sum<MPAD>(L, w0, w1);
+          const uint32_t s0 = lut_sum_fast<MPAD>(lbase, w0, w1);
           const uint32_t x0 = gw - s0;
-          if (__any_sync(0xffffffffu, (x0 & 0x80008000u) != 0u)) {
-            const int64_t rw = rb + 2 * i + half;
-            stage_hits(hit_bits(x0, 0, rw), s0, 0u, 0u, 0u, rw, 1);
+          uint32_t hm = (x0 >> 15) & 0x10001u;
+          if (__any_sync(0xffffffffu, hm != 0u)) {
+            const uint32_t r = 2 * i + half;
+            if (edge && !(r >= lo && r < hi)) hm = 0u;
+            stage_hits(hm, s0, 0u, 0u, 0u, rboff + r);
           }
         }
       }
