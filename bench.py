@@ -321,6 +321,7 @@ def run_ours(args):
         "e2e": e2e, "gpu_launches": int(launches),
         "candidates_per_query": round(refined / max(1, args.steps * Bq), 1),
         "emitted_per_query": round((c1["emitted"] - c0["emitted"]) / max(1, args.steps * Bq), 1),
+        "table_entries_per_query": round((c1["table_entries"] - c0["table_entries"]) / max(1, args.steps * Bq), 1),
         "clocks": clocks, "setup_s": round(wl["setup_s"], 1),
     }
     print(json.dumps(result), flush=True)

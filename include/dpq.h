@@ -177,7 +177,8 @@ int dpq_debug_full_tables(dpq_index_t* index, const float* yr, int64_t nq,
 int dpq_last_phase_ms(dpq_index_t* index, float* ms7);
 /* Counters since creation (8 x i64): kernel launches, queries searched,
  * code rows scanned (sum over queries), candidates refined, exact-redo
- * rounds, first-pass rows emitted (score <= guard), 0, 0.                  */
+ * rounds, first-pass rows emitted (score <= guard), full-table entries
+ * computed by the group-lazy table builder, 0.                            */
 int dpq_counters(dpq_index_t* index, int64_t* out8);
 
 #ifdef __cplusplus

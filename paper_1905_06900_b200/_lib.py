@@ -131,7 +131,8 @@ class Handle:
     def counters(self) -> dict:
         out = np.zeros(8, dtype=np.int64)
         check(lib().dpq_counters(self.raw, ptr(out)))
-        return dict(zip(("launches", "queries", "rows_scanned", "refined", "fallbacks", "emitted"),
+        return dict(zip(("launches", "queries", "rows_scanned", "refined", "fallbacks", "emitted",
+                             "table_entries"),
                         out.tolist()))
 
     def set_timing(self, on: bool) -> None:

@@ -252,11 +252,15 @@ static int launch_refine_buf(Index* h, const RefineArgs& ra, int nq) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 49152));
     }
   };
-  if (MODE == MODE_EMIT && ra.dsub == 32 && (ra.dsub % 4) == 0) {
+  if (MODE != MODE_EMIT) {
+    auto kern = k_refine_topk<BUF, kTopThreads, MODE, 0>;
+    set_attr(kern);
+    kern<<<nq, kTopThreads, smem, h->stream>>>(ra);
+  } else if (ra.dsub == 32) {
     auto kern = k_refine_topk<BUF, kTopThreads, MODE, 32>;
     set_attr(kern);
     kern<<<nq, kTopThreads, smem, h->stream>>>(ra);
-  } else if (MODE == MODE_EMIT && ra.dsub == 120) {
+  } else if (ra.dsub == 120) {
     auto kern = k_refine_topk<BUF, kTopThreads, MODE, 120>;
     set_attr(kern);
     kern<<<nq, kTopThreads, smem, h->stream>>>(ra);
@@ -296,7 +300,7 @@ int run_small_tables(Index* h, int nslot, const void* prefix, int64_t npre,
   ta.prefix_off = pre_off; ta.prefix_len = pre_len; ta.bounds_in = bounds_in;
   ta.nslot = nslot;
   ta.small_out = export_debug ? w.small : nullptr;
-  ta.q8_out = export_debug ? w.q8 : nullptr;
+  ta.q8_out = w.q8;  // read by k_group_tables
   ta.qmin_out = w.qmin; ta.qmax_out = w.qmax;
   ta.lut = w.lut; ta.mpad = h->mpad; ta.qt = qt_of(h->mpad);
   (void)ystride_override;
@@ -396,10 +400,50 @@ static RefineArgs make_refine_args(Index* h, int r) {
   ra.emit = w.emit; ra.emit_cnt = w.emit_cnt; ra.cap = w.cap; ra.bstar = w.bstar;
   ra.n_rows = h->n;
   ra.codes = h->codes; ra.code_bytes = h->code_bytes; ra.m = h->m; ra.k = h->k; ra.dsub = h->dsub;
+  ra.kbar = h->kbar; ra.bbar = h->bbar;
   ra.cb = h->cb; ra.tables = w.tables; ra.y = w.y; ra.ystride = h->d;
   ra.row_ids = nullptr; ra.id_base = h->id_base; ra.r = r;
   ra.out_d = w.out_d; ra.out_i = w.out_i; ra.n_refined = h->d_nref;
   return ra;
+}
+
+static int ensure_tables(Index* h, int nq) {
+  Workspace& w = h->ws;
+  const int64_t need = (int64_t)nq * h->m * h->k;
+  if (need > w.tables_elems) {
+    DPQ_TRY(dmalloc(&w.tables, (size_t)need));
+    w.tables_elems = need;
+  }
+  return DPQ_OK;
+}
+
+static bool group_tables_fit(Index* h, int nq) {
+  const size_t smem = (size_t)(h->k / h->kbar) * (h->dsub + 1) * 4 + (size_t)nq * 4;
+  return smem <= 200 * 1024;
+}
+
+// Group-lazy exact tables for the batch (after K3 set ws.bstar).
+int run_group_tables(Index* h, int nq, int ystride) {
+  Workspace& w = h->ws;
+  DPQ_TRY(ensure_tables(h, nq));
+  GroupTablesArgs ga;
+  ga.cb = h->cb; ga.y = w.y; ga.ystride = ystride; ga.q8 = w.q8; ga.bstar = w.bstar;
+  ga.nq = nq; ga.m = h->m; ga.k = h->k; ga.kbar = h->kbar; ga.bbar = h->bbar; ga.dsub = h->dsub;
+  ga.tables = w.tables; ga.n_entries = h->d_nent;
+  const int gsize = h->k / h->kbar;
+  const size_t smem = (size_t)gsize * (h->dsub + 1) * 4 + (size_t)nq * 4;
+  static size_t attr = 0;
+  dim3 grid(h->kbar, h->m);
+  if (h->dsub == 32) {
+    if (smem > attr) cudaFuncSetAttribute(k_group_tables<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 49152));
+    k_group_tables<32><<<grid, 256, smem, h->stream>>>(ga);
+  } else {
+    if (smem > attr) cudaFuncSetAttribute(k_group_tables<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 49152));
+    k_group_tables<0><<<grid, 256, smem, h->stream>>>(ga);
+  }
+  attr = std::max(attr, smem);
+  DPQ_LAUNCHED(h);
+  return DPQ_OK;
 }
 
 // One flat derived batch: queries already in ws.y (nb rows), results into
@@ -413,7 +457,13 @@ static int flat_derived_batch(Index* h, int nb, int r, int r2) {
   if (rc != DPQ_OK) return rc;
   ev_rec(h, 5);
   RefineArgs ra = make_refine_args(h, r);
-  DPQ_TRY(launch_refine<MODE_EMIT>(h, ra, nb));
+  if (group_tables_fit(h, nb)) {
+    DPQ_TRY(run_group_tables(h, nb, h->d));
+    ra.tables = h->ws.tables;  // (re)allocated by run_group_tables
+    DPQ_TRY(launch_refine<MODE_EMIT_TABLE>(h, ra, nb));
+  } else {
+    DPQ_TRY(launch_refine<MODE_EMIT>(h, ra, nb));  // entries computed per candidate
+  }
   ev_rec(h, 6);
   h->counters[1] += nb;
   if (h->timing) {
@@ -432,13 +482,10 @@ static int flat_derived_batch(Index* h, int nb, int r, int r2) {
 static int flat_conventional_batch(Index* h, int nb, int r) {
   Workspace& w = h->ws;
   ev_rec(h, 0);
-  const int64_t need = (int64_t)nb * h->m * h->k;
-  if (need > w.tables_elems) {
-    DPQ_TRY(dmalloc(&w.tables, (size_t)need));
-    w.tables_elems = need;
-  }
-  dim3 grid((h->k + 255) / 256, h->m, nb);
-  k_full_tables<<<grid, 256, h->dsub * 4, h->stream>>>(w.y, h->cb, h->m, h->k, h->dsub, w.tables);
+  DPQ_TRY(ensure_tables(h, nb));
+  dim3 grid((h->k + 255) / 256, h->m, nb);  // NB: make_refine_args below reads ws.tables
+  k_full_tables<<<grid, 256, h->dsub * 4, h->stream>>>(w.y, h->cb, h->m, h->k, h->kbar, h->bbar, h->dsub, 1,
+                                                       w.tables);
   DPQ_LAUNCHED(h);
   ev_rec(h, 1);
   RefineArgs ra = make_refine_args(h, r);
@@ -549,6 +596,9 @@ int index_common_init(Index* h, int device, int m, int k, int kbar, int dsub, co
   h->device = device;
   DPQ_CUDA(cudaSetDevice(device));
   h->m = m; h->k = k; h->kbar = kbar; h->dsub = dsub; h->d = m * dsub; h->mask = kbar - 1;
+  h->bbar = 0;
+  while ((1 << h->bbar) < kbar) ++h->bbar;
+  if (k % kbar) { set_error("k must be a multiple of kbar"); return DPQ_ERR_ARG; }
   h->mpad = m <= 4 ? 4 : 8;
   h->code_bytes = code_bytes;
   if (const char* e = getenv("DPQ_GUARD_SAMPLE")) h->sample = std::max<int64_t>(1, atoll(e));
@@ -561,6 +611,8 @@ int index_common_init(Index* h, int device, int m, int k, int kbar, int dsub, co
   DPQ_TRY(dmalloc(&h->dcb, (size_t)m * kbar * dsub));
   DPQ_TRY(dmalloc(&h->d_nref, 1));
   DPQ_TRY(dmalloc(&h->d_nemit, 1));
+  DPQ_TRY(dmalloc(&h->d_nent, 1));
+  DPQ_CUDA(cudaMemset(h->d_nent, 0, 8));
   DPQ_CUDA(cudaMemcpy(h->cb, codebooks, (size_t)m * k * dsub * 4, cudaMemcpyHostToDevice));
   DPQ_CUDA(cudaMemcpy(h->dcb, derived, (size_t)m * kbar * dsub * 4, cudaMemcpyHostToDevice));
   DPQ_CUDA(cudaMemset(h->d_nref, 0, 8));
@@ -574,7 +626,7 @@ void index_free(Index* h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   Workspace& w = h->ws;
   void* dev[] = {h->cb, h->dcb, h->codes, h->plane, h->own_prefix ? h->prefix : nullptr, h->centers,
-                 h->offsets, h->sorted_ids, h->d_nref, h->d_nemit, w.y, w.small, w.q8, w.qmin, w.qmax, w.bounds,
+                 h->offsets, h->sorted_ids, h->d_nref, h->d_nemit, h->d_nent, w.y, w.small, w.q8, w.qmin, w.qmax, w.bounds,
                  w.lut, w.hist, w.hist_i, w.guard_b, w.gword, w.emit_cnt, w.emit, w.bstar, w.ncand,
                  w.flags, w.only, w.tile_list, w.out_d, w.out_i, w.tables, w.slot_query, w.slot_probe,
                  w.slot_pre_off, w.slot_pre_len, w.counter};
@@ -788,7 +840,8 @@ int dpq_debug_full_tables(dpq_index_t* index, const float* yr, int64_t nq, float
     }
     DPQ_CUDA(cudaMemcpyAsync(w.y, yr + q0 * h->d, (size_t)h->d * 4, cudaMemcpyHostToDevice, h->stream));
     dim3 grid((h->k + 255) / 256, h->m, 1);
-    k_full_tables<<<grid, 256, h->dsub * 4, h->stream>>>(w.y, h->cb, h->m, h->k, h->dsub, w.tables);
+    k_full_tables<<<grid, 256, h->dsub * 4, h->stream>>>(w.y, h->cb, h->m, h->k, h->kbar, h->bbar, h->dsub, 0,
+                                                         w.tables);
     DPQ_LAUNCHED(h);
     DPQ_CUDA(cudaMemcpyAsync(tables + q0 * per, w.tables, (size_t)per * 4, cudaMemcpyDeviceToHost, h->stream));
     DPQ_CUDA(cudaStreamSynchronize(h->stream));
@@ -812,12 +865,14 @@ int dpq_last_phase_ms(dpq_index_t* index, float* ms7) {
 int dpq_counters(dpq_index_t* index, int64_t* out8) {
   Index* h = reinterpret_cast<Index*>(index);
   if (!h || !out8) { set_error("null argument"); return DPQ_ERR_ARG; }
-  unsigned long long nref = 0, nemit = 0;
+  unsigned long long nref = 0, nemit = 0, nent = 0;
   cudaSetDevice(h->device);
   DPQ_CUDA(cudaMemcpy(&nref, h->d_nref, 8, cudaMemcpyDeviceToHost));
   DPQ_CUDA(cudaMemcpy(&nemit, h->d_nemit, 8, cudaMemcpyDeviceToHost));
+  DPQ_CUDA(cudaMemcpy(&nent, h->d_nent, 8, cudaMemcpyDeviceToHost));
   h->counters[3] = (int64_t)nref;
   h->counters[5] = (int64_t)nemit;
+  h->counters[6] = (int64_t)nent;
   for (int i = 0; i < 8; ++i) out8[i] = h->counters[i];
   return DPQ_OK;
 }

@@ -62,7 +62,7 @@ struct Workspace {
 struct Index {
   int device = 0;
   int kind = KIND_FLAT;
-  int m = 0, k = 0, kbar = 0, dsub = 0, d = 0, mask = 0, mpad = 4, code_bytes = 2;
+  int m = 0, k = 0, kbar = 0, bbar = 0, dsub = 0, d = 0, mask = 0, mpad = 4, code_bytes = 2;
   int64_t n = 0, n_pad = 0, id_base = 0;
   float* cb = nullptr;      // [m][k][dsub]
   float* dcb = nullptr;     // [m][kbar][dsub]
@@ -87,6 +87,7 @@ struct Index {
   int64_t counters[8] = {};  // launches, queries, rows scanned, refined, fallbacks, emitted
   unsigned long long* d_nref = nullptr;
   unsigned long long* d_nemit = nullptr;
+  unsigned long long* d_nent = nullptr;   // lazily computed table entries
   size_t emit_budget = (size_t)16 << 30;  // bytes for emit buffers
   // guard sampling (env DPQ_GUARD_SAMPLE / DPQ_EXACT_LIMIT / DPQ_EMIT_CAP
   // override them so tests can force the exact-redo and overflow paths)

@@ -561,18 +561,92 @@ __global__ void k_bstar_from_hist(const int32_t* __restrict__ hist, const uint16
 }
 
 // ============================================================================
-// K5: full (m, k) tables, exact (conventional mode and the debug seam).
+// K5: full-codebook tables, exact (row_sq_dists, search.py:16-25).
+//
+// Tables are stored group-major: entry (q, j, c) with c = ibar * kbar + g
+// lives at ((q * m + j) * kbar + g) * gsize + ibar  (gsize = k / kbar), so
+// the members of one derived group are contiguous.
+//
+// k_group_tables (derived search) is the GPU form of LazyTables
+// (twopass.py:220-251): a candidate's score s <= b* <= 254 is a sum of
+// non-negative 8-bit entries, so every subspace entry satisfies
+// q8[j][c_j mod kbar] <= b*; only groups with q8 <= b* can ever be gathered.
+// One CTA per (group, subspace) stages the group's gsize codebook rows in
+// shared memory once and computes entries for exactly the queries of the
+// batch where that group is active.  Entries are bit-identical to eager
+// tables (same pairwise kernel), so distances are bitwise the reference's.
+//
+// k_full_tables (conventional search, debug seam) computes every entry.
 // ============================================================================
+__host__ __device__ __forceinline__ int64_t table_index(int q, int j, uint32_t c, int m, int kbar,
+                                                        int bbar, int gsize) {
+  return (((int64_t)q * m + j) * kbar + (c & (kbar - 1))) * gsize + (c >> bbar);
+}
+
+struct GroupTablesArgs {
+  const float* cb; const float* y; int ystride;
+  const uint8_t* q8; const int32_t* bstar;
+  int nq, m, k, kbar, bbar, dsub;
+  float* tables;
+  unsigned long long* n_entries;
+};
+
+template <int DSUB>
+__global__ void __launch_bounds__(256) k_group_tables(GroupTablesArgs a) {
+  extern __shared__ __align__(16) float tile[];  // [gsize][dsub+1]
+  __shared__ int nact;
+  const int g = blockIdx.x, j = blockIdx.y;
+  const int dsub = DSUB > 0 ? DSUB : a.dsub;
+  const int gsize = a.k / a.kbar, ld = dsub + 1;
+  int* act = reinterpret_cast<int*>(tile + gsize * ld);
+  if (threadIdx.x == 0) nact = 0;
+  for (int e = threadIdx.x; e < gsize * dsub; e += 256) {
+    const int ib = e / dsub, t = e - ib * dsub;
+    tile[ib * ld + t] = a.cb[(((int64_t)j * a.k) + (int64_t)ib * a.kbar + g) * dsub + t];
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < a.nq; q += 256)
+    if ((int)a.q8[((int64_t)q * a.m + j) * a.kbar + g] <= a.bstar[q]) act[atomicAdd(&nact, 1)] = q;
+  __syncthreads();
+  const int n = nact;
+  for (int p = threadIdx.x; p < n * gsize; p += 256) {
+    const int qi = act[p / gsize], ib = p % gsize;
+    const float* yq = a.y + (int64_t)qi * a.ystride + j * dsub;
+    const float* row = tile + ib * ld;
+    float v;
+    if constexpr (DSUB > 0) {
+      float r[8];
+#pragma unroll
+      for (int i = 0; i < DSUB / 8; ++i)
+#pragma unroll
+        for (int l = 0; l < 8; ++l) {
+          const float sq = sqdiff(row[8 * i + l], __ldg(yq + 8 * i + l));
+          r[l] = i == 0 ? sq : __fadd_rn(r[l], sq);
+        }
+      v = __fadd_rn(__fadd_rn(__fadd_rn(r[0], r[1]), __fadd_rn(r[2], r[3])),
+                    __fadd_rn(__fadd_rn(r[4], r[5]), __fadd_rn(r[6], r[7])));
+    } else {
+      v = pw_sqdist(row, yq, dsub);
+    }
+    a.tables[(((int64_t)qi * a.m + j) * a.kbar + g) * gsize + ib] = v;
+  }
+  if (a.n_entries && threadIdx.x == 0) atomicAdd(a.n_entries, (unsigned long long)n * gsize);
+}
+
 __global__ void __launch_bounds__(256)
-    k_full_tables(const float* __restrict__ y, const float* __restrict__ cb, int m, int k,
-                  int dsub, float* __restrict__ out) {
+    k_full_tables(const float* __restrict__ y, const float* __restrict__ cb, int m, int k, int kbar,
+                  int bbar, int dsub, int group_major, float* __restrict__ out) {
   extern __shared__ float ysub[];
   const int q = blockIdx.z, j = blockIdx.y;
   for (int t = threadIdx.x; t < dsub; t += 256) ysub[t] = y[((int64_t)q * m + j) * dsub + t];
   __syncthreads();
   const int i = blockIdx.x * 256 + threadIdx.x;
-  if (i < k)
-    out[((int64_t)q * m + j) * k + i] = pw_sqdist(cb + ((int64_t)j * k + i) * dsub, ysub, dsub);
+  if (i < k) {
+    const float v = pw_sqdist(cb + ((int64_t)j * k + i) * dsub, ysub, dsub);
+    const int64_t o = group_major ? table_index(q, j, (uint32_t)i, m, kbar, bbar, k / kbar)
+                                  : ((int64_t)q * m + j) * k + i;
+    out[o] = v;
+  }
 }
 
 // ============================================================================
@@ -588,15 +662,15 @@ __global__ void __launch_bounds__(256)
 //   MODE_EMIT: emit list entries with score <= b*  (derived search)
 //   MODE_ALL : every row of [0, n_rows)            (conventional, tables)
 // ============================================================================
-enum { MODE_EMIT = 0, MODE_ALL = 1 };
+enum { MODE_EMIT = 0, MODE_ALL = 1, MODE_EMIT_TABLE = 2 };
 
 struct RefineArgs {
   const uint64_t* emit; const uint32_t* emit_cnt; uint32_t cap;
   const int32_t* bstar;
   int64_t n_rows;            // MODE_ALL
-  const void* codes; int code_bytes; int m; int k; int dsub;
+  const void* codes; int code_bytes; int m; int k; int dsub; int kbar; int bbar;
   const float* cb;           // [m][k][dsub]
-  const float* tables;       // MODE_ALL: [nq][m][k] full tables
+  const float* tables;       // MODE_ALL / MODE_EMIT_TABLE: group-major tables
   const float* y;            // [nq][ystride] query / per-probe residuals
   int ystride;               // floats per query in y (d, or ma*d for ivf)
   const int64_t* row_ids;    // optional row -> id (ivf sorted_ids)
@@ -648,7 +722,7 @@ __global__ void __launch_bounds__(NT) k_refine_topk(RefineArgs a) {
   int64_t ntot;
   int bs = 254;
   const uint64_t* e = nullptr;
-  if (MODE == MODE_EMIT) {
+  if (MODE != MODE_ALL) {
     ntot = min(a.emit_cnt[q], a.cap);
     bs = a.bstar[q];
     e = a.emit + (int64_t)q * a.cap;
@@ -665,7 +739,7 @@ __global__ void __launch_bounds__(NT) k_refine_topk(RefineArgs a) {
       int64_t row;
       uint32_t probe = 0;
       bool cand = true;
-      if (MODE == MODE_EMIT) {
+      if (MODE != MODE_ALL) {
         const uint64_t v = e[idx];
         cand = (int)emit_score(v) <= bs;
         row = emit_row(v);
@@ -680,7 +754,7 @@ __global__ void __launch_bounds__(NT) k_refine_topk(RefineArgs a) {
         for (int j = 0; j < a.m; ++j) {
           const uint32_t c = code_at(a.codes, a.code_bytes, row * a.m + j);
           float t;
-          if (MODE == MODE_ALL) t = a.tables[((int64_t)q * a.m + j) * a.k + c];
+          if (MODE != MODE_EMIT) t = a.tables[table_index(q, j, c, a.m, a.kbar, a.bbar, a.k / a.kbar)];
           else t = entry_dist<DSUB>(a.cb + ((int64_t)j * a.k + c) * a.dsub, yq + j * a.dsub, a.dsub);
           dist = __dadd_rn(dist, (double)t);
         }
