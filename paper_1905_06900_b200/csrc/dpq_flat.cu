@@ -100,7 +100,7 @@ int ensure_ws(Index* h, int nslot, int r, int ystride) {
     DPQ_TRY(dmalloc(&w.qmin, (size_t)qb));
     DPQ_TRY(dmalloc(&w.qmax, (size_t)qb));
     DPQ_TRY(dmalloc(&w.bounds, (size_t)qb * 2));
-    DPQ_TRY(dmalloc(&w.lut, (size_t)tiles * h->mpad * 256 * qt));
+    DPQ_TRY(dmalloc(&w.lut, (size_t)tiles * h->mpad * 256 * qt));  // u8 entries
     DPQ_TRY(dmalloc(&w.hist, (size_t)tiles * qt * 256));
     DPQ_TRY(dmalloc(&w.hist_i, (size_t)qb * 256));
     DPQ_TRY(dmalloc(&w.guard_b, (size_t)tiles * qt));
@@ -175,7 +175,7 @@ template <int MPAD>
 static int launch_hist_t(Index* h, int ntiles, const int* tile_list, int64_t stride,
                          int64_t nsamp, const uint8_t* plane) {
   using G = ScanGeom<MPAD>;
-  const size_t smem = G::LUT_BYTES + (size_t)G::QT * 256 * 4;
+  const size_t smem = G::LUT_BYTES + (size_t)G::QT * 128 * 4;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_scan_hist<MPAD, kScanThreads>,
@@ -186,6 +186,7 @@ static int launch_hist_t(Index* h, int ntiles, const int* tile_list, int64_t str
                                                           (nsamp + 4095) / 4096));
   int64_t per = (nsamp + chunks - 1) / chunks;
   per = (per + 31) / 32 * 32;
+  per = std::min<int64_t>(per, kHistRowsPerCta / 32 * 32);  // u16 counters never wrap
   chunks = (int)((nsamp + per - 1) / per);
   if (chunks < 1) chunks = 1;
   dim3 grid(chunks, ntiles);
@@ -213,7 +214,7 @@ template <int MPAD>
 static int launch_emit_t(Index* h, EmitArgs ea, int ntiles, int64_t rows) {
   using G = ScanGeom<MPAD>;
   constexpr int NW = kScanThreads / 32;
-  const size_t smem = emit_smem_bytes<MPAD>();
+  const size_t smem = emit_smem_bytes<MPAD, kScanThreads>();
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_scan_emit<MPAD, kScanThreads>,

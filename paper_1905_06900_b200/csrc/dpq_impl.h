@@ -28,7 +28,7 @@ struct Workspace {
   double* qmin = nullptr;
   double* qmax = nullptr;
   double* bounds = nullptr;   // [qb][2]
-  uint16_t* lut = nullptr;    // [tiles][mpad][256][qt]
+  uint8_t* lut = nullptr;     // [tiles][mpad][256][qt] u8
   uint32_t* hist = nullptr;   // [tiles*qt][256]
   int32_t* hist_i = nullptr;  // [qb][256] (sharded exchange)
   uint16_t* guard_b = nullptr;

@@ -55,23 +55,26 @@ __device__ __forceinline__ uint32_t lds32(const uint8_t* p) {
 
 template <int MPAD>
 struct ScanGeom {
-  static constexpr int QT = MPAD == 4 ? 64 : 32;  // queries per tile
-  static constexpr int LPC = QT / 2;              // lanes per code
-  static constexpr int CPW = 32 / LPC;            // codes per warp step
-  static constexpr int ROWB = QT * 2;             // bytes of one subspace row
-  static constexpr int SPR = 256 / ROWB;          // subspaces per 256-B row
+  static constexpr int QT = MPAD == 4 ? 128 : 64;  // queries per tile
+  static constexpr int LPC = QT / 4;               // lanes per code (4 queries/lane)
+  static constexpr int CPW = 32 / LPC;             // codes per warp step
+  static constexpr int ROWB = QT;                  // bytes of one subspace row (u8)
+  static constexpr int SPR = 256 / ROWB;           // subspaces per 256-B row
   static constexpr int LUT_BYTES = MPAD * 256 * ROWB;  // 128 KB
-  static constexpr int CHUNK_ROWS = 512 / MPAD;   // rows per 512-B warp load
+  static constexpr int CHUNK_ROWS = 512 / MPAD;    // rows per 512-B warp load
 };
 
-// LUT layout of one query tile (u16 units):
+// LUT layout of one query tile (bytes, one u8 entry per query):
 //   [MPAD/SPR tables of 64 KB][256 rows of 256 B][SPR subspaces][QT queries]
 // Subspace j, table row i, query qq ->
 //   ((j / SPR) * 256 + i) * (SPR * QT) + (j % SPR) * QT + qq
-// With the tile at a 64-KB aligned shared address, the byte address of
-// lane lic's word for row i of subspace j is
+// Lane lic owns queries 4*lic .. 4*lic+3 (one 32-bit word per table row).
+// With the tile at a 64-KB aligned shared address, the byte address of that
+// word for row i of subspace j is
 //   base | i << 8 | (j % SPR) * ROWB | lic * 4   (+ (j / SPR) * 64 KB)
 // i.e. ONE byte-permute of the code word into the lane's base word.
+// The four u8 entries of a word are split into two u16x2 accumulators
+// (bytes 0,2 and 1,3); sums of MPAD entries never carry across halves.
 __host__ __device__ __forceinline__ int64_t lut_index(int j, int i, int qq, int spr, int qt) {
   return ((int64_t)(j / spr) * 256 + i) * (spr * qt) + (int64_t)(j % spr) * qt + qq;
 }
@@ -94,7 +97,7 @@ struct TablesArgs {
   uint8_t* q8_out;         // optional [nslot][m][kbar]
   double* qmin_out;        // [nslot]
   double* qmax_out;        // [nslot]
-  uint16_t* lut;           // [tiles][mpad][256][qt]
+  uint8_t* lut;            // [tiles][mpad][256][qt] (see lut_index)
   int mpad, qt;
 };
 
@@ -162,11 +165,11 @@ __global__ void __launch_bounds__(256) k_small_tables(TablesArgs a) {
   __syncthreads();
   // scan-layout LUT (see lut_index)
   const int tile = s / a.qt, qq = s % a.qt;
-  const int spr = 256 / (2 * a.qt);
-  uint16_t* L = a.lut + (int64_t)tile * a.mpad * 256 * a.qt;
+  const int spr = 256 / a.qt;
+  uint8_t* L = a.lut + (int64_t)tile * a.mpad * 256 * a.qt;
   for (int e = tid; e < a.mpad * 256; e += 256) {
     const int j = e >> 8, i = e & 255;
-    uint16_t v = (j < a.m && i < a.kbar) ? (uint16_t)q8[j * a.kbar + i] : (uint16_t)0;
+    uint8_t v = (j < a.m && i < a.kbar) ? q8[j * a.kbar + i] : (uint8_t)0;
     L[lut_index(j, i, qq, spr, a.qt)] = v;
   }
 }
@@ -176,25 +179,29 @@ __global__ void __launch_bounds__(256) k_small_tables(TablesArgs a) {
 // and the sample is every row).  One CTA = (sample chunk, query tile);
 // per-tile histograms live in shared memory, flushed with global atomics.
 // ============================================================================
+struct Sum4 { uint32_t lo, hi; };  // u16x2: queries (0,2) and (1,3) of a lane
+
 template <int MPAD>
-__device__ __forceinline__ uint32_t lut_sum(const uint8_t* L, uint32_t w0, uint32_t w1) {
+__device__ __forceinline__ Sum4 lut_sum(const uint8_t* L, uint32_t w0, uint32_t w1) {
   // L = tile base + lic * 4 (generic addressing; used off the hot path)
   using G = ScanGeom<MPAD>;
-  uint32_t s = 0;
+  Sum4 s{0u, 0u};
 #pragma unroll
   for (int j = 0; j < MPAD; ++j) {
     const uint32_t w = j < 4 ? w0 : w1;
     const uint32_t idx = (w >> (8 * (j & 3))) & 0xFFu;
-    s += lds32(L + (j / G::SPR) * 65536 + (idx << 8) + (j % G::SPR) * G::ROWB);
+    const uint32_t v = lds32(L + (j / G::SPR) * 65536 + (idx << 8) + (j % G::SPR) * G::ROWB);
+    s.lo += v & 0x00FF00FFu;
+    s.hi += __byte_perm(v, 0u, 0x4341u);
   }
   return s;
 }
 
 // Hot-path variant: base = 64-KB aligned shared address | lic * 4.
 template <int MPAD>
-__device__ __forceinline__ uint32_t lut_sum_fast(uint32_t base, uint32_t w0, uint32_t w1) {
+__device__ __forceinline__ Sum4 lut_sum_fast(uint32_t base, uint32_t w0, uint32_t w1) {
   using G = ScanGeom<MPAD>;
-  uint32_t s = 0;
+  Sum4 s{0u, 0u};
 #pragma unroll
   for (int j = 0; j < MPAD; ++j) {
     const uint32_t w = j < 4 ? w0 : w1;
@@ -203,37 +210,48 @@ __device__ __forceinline__ uint32_t lut_sum_fast(uint32_t base, uint32_t w0, uin
     uint32_t v;
     if (j / G::SPR == 0) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
     else asm volatile("ld.shared.u32 %0, [%1+65536];" : "=r"(v) : "r"(a));
-    s += v;
+    s.lo += v & 0x00FF00FFu;
+    s.hi += __byte_perm(v, 0u, 0x4341u);
   }
   return s;
 }
 
+// score of lane query qsel (0..3) from the packed sums
+__device__ __forceinline__ uint32_t sum_of(Sum4 s, int qsel) {
+  const uint32_t w = (qsel & 1) ? s.hi : s.lo;
+  return (qsel & 2) ? (w >> 16) : (w & 0xFFFFu);
+}
+
+// Histogram counters are u16 pairs inside u32 words; a CTA handles at most
+// kHistRowsPerCta rows so no counter can wrap.
+constexpr int64_t kHistRowsPerCta = 65535;
+
 template <int MPAD, int NT>
 __global__ void __launch_bounds__(NT, 1)
     k_scan_hist(const uint8_t* __restrict__ plane, int64_t stride, int64_t n_samp,
-                int64_t samp_per_cta, const uint16_t* __restrict__ lut,
+                int64_t samp_per_cta, const uint8_t* __restrict__ lut,
                 const int* __restrict__ tile_list, uint32_t* __restrict__ hist) {
   using G = ScanGeom<MPAD>;
   extern __shared__ __align__(16) uint8_t smem[];
   uint8_t* slut = smem;
-  uint32_t* sh = reinterpret_cast<uint32_t*>(smem + G::LUT_BYTES);  // [QT][256]
+  uint32_t* sh = reinterpret_cast<uint32_t*>(smem + G::LUT_BYTES);  // [QT][128] u16 pairs
   const int tile = tile_list ? tile_list[blockIdx.y] : blockIdx.y;
-  const uint4* src = reinterpret_cast<const uint4*>(lut + (int64_t)tile * G::LUT_BYTES / 2);
+  const uint4* src = reinterpret_cast<const uint4*>(lut + (int64_t)tile * G::LUT_BYTES);
   for (int i = threadIdx.x; i < G::LUT_BYTES / 16; i += NT) reinterpret_cast<uint4*>(slut)[i] = src[i];
-  for (int i = threadIdx.x; i < G::QT * 256; i += NT) sh[i] = 0;
+  for (int i = threadIdx.x; i < G::QT * 128; i += NT) sh[i] = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int lic = lane % G::LPC, half = lane / G::LPC;
   const uint8_t* L = slut + lic * 4;
-  uint32_t* h0 = sh + (2 * lic) * 256;
-  uint32_t* h1 = h0 + 256;
   const int64_t s0 = (int64_t)blockIdx.x * samp_per_cta;
   const int64_t s1 = min(n_samp, s0 + samp_per_cta);
+  auto bump = [&](int qq, uint32_t score) {
+    if (score < 255u) atomicAdd(sh + qq * 128 + (score >> 1), 1u << (16 * (score & 1)));
+  };
   for (int64_t g = s0 + (int64_t)warp * 32; g < s1; g += (int64_t)NT) {
     const int64_t my = g + lane;
     uint32_t w0 = 0, w1 = 0;
-    const bool ok = my < s1;
-    if (ok) {
+    if (my < s1) {
       const uint8_t* p = plane + my * stride * MPAD;
       w0 = *reinterpret_cast<const uint32_t*>(p);
       if (MPAD == 8) w1 = *reinterpret_cast<const uint32_t*>(p + 4);
@@ -244,18 +262,19 @@ __global__ void __launch_bounds__(NT, 1)
       const uint32_t c0 = __shfl_sync(0xffffffffu, w0, src_lane);
       const uint32_t c1 = __shfl_sync(0xffffffffu, w1, src_lane);
       if (src_lane < cnt) {
-        const uint32_t sum = lut_sum<MPAD>(L, c0, c1);
-        const uint32_t lo = sum & 0xFFFFu, hi = sum >> 16;
-        if (lo < 255u) atomicAdd(h0 + lo, 1u);
-        if (hi < 255u) atomicAdd(h1 + hi, 1u);
+        const Sum4 sm = lut_sum<MPAD>(L, c0, c1);
+#pragma unroll
+        for (int qs = 0; qs < 4; ++qs) bump(4 * lic + qs, sum_of(sm, qs));
       }
     }
   }
   __syncthreads();
   uint32_t* gh = hist + (int64_t)tile * G::QT * 256;
-  for (int i = threadIdx.x; i < G::QT * 256; i += NT) {
+  for (int i = threadIdx.x; i < G::QT * 128; i += NT) {
     const uint32_t v = sh[i];
-    if (v) atomicAdd(gh + i, v);
+    const int qq = i / 128, b = (i % 128) * 2;
+    if (v & 0xFFFFu) atomicAdd(gh + qq * 256 + b, v & 0xFFFFu);
+    if (v >> 16) atomicAdd(gh + qq * 256 + b + 1, v >> 16);
   }
 }
 
@@ -275,8 +294,8 @@ struct EmitArgs {
   const uint8_t* plane;
   int64_t row_begin, row_end;   // scanned rows [row_begin, row_end)
   int64_t rows_per_cta;
-  const uint16_t* lut;
-  const uint16_t* gword;        // [tiles*QT] guard words (0x8000+B or 0x7FFF)
+  const uint8_t* lut;
+  const uint16_t* gword;        // [tiles*QT] guard words (0x8000+B or 0x7F7F)
   const int* tile_list;         // optional blockIdx.y -> tile
   const int* slot_query;        // optional slot -> emit list (ivf); else slot
   const int* slot_probe;        // optional slot -> probe index (ivf)
@@ -302,16 +321,13 @@ struct EmitArgs {
 constexpr int kWarpBuf = 128;  // staged hits per warp (1 KB)
 constexpr uint32_t kLutShared = 0x10000;  // LUT at shared address 64 KB
 
+// Shared layout: [stage | hit buffers] below 64 KB, LUT in [64 KB, 192 KB),
+// per-warp hit counters above it.
 template <int MPAD, int NT>
-__host__ __device__ constexpr int emit_low_bytes() {
-  // stage + hit buffers + per-warp counters, all below the LUT
-  return (NT / 32) * (32 * 16 + kWarpBuf * 8 + ScanGeom<MPAD>::QT * 4);
-}
-// dynamic smem request: enough to reach the end of the LUT whatever the
-// (small) offset of the dynamic window inside the CTA's shared space
-template <int MPAD>
+__host__ __device__ constexpr int emit_low_bytes() { return (NT / 32) * (32 * 16 + kWarpBuf * 8); }
+template <int MPAD, int NT>
 __host__ __device__ constexpr int emit_smem_bytes() {
-  return (int)kLutShared + ScanGeom<MPAD>::LUT_BYTES;
+  return (int)kLutShared + ScanGeom<MPAD>::LUT_BYTES + (NT / 32) * ScanGeom<MPAD>::QT * 4;
 }
 
 template <int MPAD, int NT>
@@ -325,7 +341,7 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
   uint8_t* slut = smem + (kLutShared - dyn);
   uint4* stage = reinterpret_cast<uint4*>(smem);
   uint64_t* hbuf_all = reinterpret_cast<uint64_t*>(smem + NW * 32 * 16);
-  uint32_t* hcnt_all = reinterpret_cast<uint32_t*>(hbuf_all + NW * kWarpBuf);
+  uint32_t* hcnt_all = reinterpret_cast<uint32_t*>(slut + G::LUT_BYTES);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int lic = lane % G::LPC, half = lane / G::LPC;
   const uint32_t lbase = kLutShared | (uint32_t)(lic * 4);
@@ -344,13 +360,14 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
     const int64_t chunk_u = u % a.units_per_tile;
     const int tile = a.tile_list ? a.tile_list[tix] : tix;
     if (tile != cur_tile) {
-      const uint4* src = reinterpret_cast<const uint4*>(a.lut + (int64_t)tile * G::LUT_BYTES / 2);
+      const uint4* src = reinterpret_cast<const uint4*>(a.lut + (int64_t)tile * G::LUT_BYTES);
       for (int i = threadIdx.x; i < G::LUT_BYTES / 16; i += NT) reinterpret_cast<uint4*>(slut)[i] = src[i];
       cur_tile = tile;
       __syncthreads();
     }
-    const int slot0 = tile * G::QT + 2 * lic;
-    const uint32_t gw = (uint32_t)a.gword[slot0] | ((uint32_t)a.gword[slot0 + 1] << 16);
+    const int q0 = tile * G::QT + 4 * lic;
+    const uint32_t glo = (uint32_t)a.gword[q0] | ((uint32_t)a.gword[q0 + 2] << 16);
+    const uint32_t ghi = (uint32_t)a.gword[q0 + 1] | ((uint32_t)a.gword[q0 + 3] << 16);
     // Logical range [r0, r1); loads start at the 512-B aligned row r0a and
     // rows outside the range are never emitted.
     const int64_t r0 = a.row_begin + chunk_u * a.rows_per_cta;
@@ -392,10 +409,9 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
       __syncwarp();
       wc = 0;
     };
-    // Stage hits.  hm bit k = hit of query 2*lic on code k, bit 16+k = hit of
-    // query 2*lic+1; code k is row rowb + k (offset roff0 + k from r0a).
-    // One ballot round per hit per lane (nearly always a single round).
-    auto stage_hits = [&](uint32_t hm, uint32_t sa, uint32_t sb, uint32_t sc2, uint32_t sd, uint32_t roff0) {
+    // Stage hits.  hm bit 4k+qs = hit of lane query qs on code k (row
+    // offset roff0 + k from r0a).  One ballot round per hit per lane.
+    auto stage_hits = [&](uint32_t hm, Sum4 sa, Sum4 sb, Sum4 sc2, Sum4 sd, uint32_t roff0) {
       for (;;) {
         const bool has = hm != 0u;
         const uint32_t bal = __ballot_sync(0xffffffffu, has);
@@ -404,14 +420,19 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
         if (has) {
           const int b = __ffs(hm) - 1;
           hm &= hm - 1u;
-          const int k = b & 15, q = b >> 4;
-          const uint32_t sk = k == 0 ? sa : (k == 1 ? sb : (k == 2 ? sc2 : sd));
-          const uint32_t score = q ? (sk >> 16) : (sk & 0xFFFFu);
-          hbuf[wc + __popc(bal & lt)] = (uint64_t)(roff0 + k) | ((uint64_t)(2 * lic + q) << 32) |
-                                        ((uint64_t)score << 40);
+          const int k = b >> 2, qs = b & 3;
+          const Sum4 sk = k == 0 ? sa : (k == 1 ? sb : (k == 2 ? sc2 : sd));
+          hbuf[wc + __popc(bal & lt)] = (uint64_t)(roff0 + k) | ((uint64_t)(4 * lic + qs) << 32) |
+                                        ((uint64_t)sum_of(sk, qs) << 40);
         }
         wc += __popc(bal);
       }
+    };
+    // hit bits of one code: query qs hits iff bit 15 (lo half) / 31 (hi half)
+    // of (guard - sum) is set: qs0 = lo.15, qs1 = hi.15, qs2 = lo.31, qs3 = hi.31
+    auto code_bits = [&](Sum4 sm) -> uint32_t {
+      const uint32_t xl = glo - sm.lo, xh = ghi - sm.hi;
+      return ((xl >> 15) & 1u) | ((xh >> 14) & 2u) | ((xl >> 29) & 4u) | ((xh >> 28) & 8u);
     };
     uint4 nxt = ldg_stream(chunk_ptr(c));
     for (; c < nchunks; c += NW) {
@@ -429,18 +450,17 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
       for (int i = 0; i < 32; ++i) {
         const uint4 v = wst[i];
         if (MPAD == 4) {
-          const uint32_t s0 = lut_sum_fast<MPAD>(lbase, v.x, 0), s1 = lut_sum_fast<MPAD>(lbase, v.y, 0);
-          const uint32_t s2 = lut_sum_fast<MPAD>(lbase, v.z, 0), s3 = lut_sum_fast<MPAD>(lbase, v.w, 0);
-          const uint32_t x0 = gw - s0, x1 = gw - s1, x2 = gw - s2, x3 = gw - s3;
-          if (__any_sync(0xffffffffu, ((x0 | x1 | x2 | x3) & 0x80008000u) != 0u)) {
-            // bit 15/31 of x = hit; gather them at bits k and 16+k
-            uint32_t hm = ((x0 >> 15) & 0x10001u) | ((x1 >> 14) & 0x20002u) | ((x2 >> 13) & 0x40004u) |
-                          ((x3 >> 12) & 0x80008u);
+          const Sum4 s0 = lut_sum_fast<MPAD>(lbase, v.x, 0), s1 = lut_sum_fast<MPAD>(lbase, v.y, 0);
+          const Sum4 s2 = lut_sum_fast<MPAD>(lbase, v.z, 0), s3 = lut_sum_fast<MPAD>(lbase, v.w, 0);
+          const uint32_t any = ((glo - s0.lo) | (ghi - s0.hi) | (glo - s1.lo) | (ghi - s1.hi) |
+                                (glo - s2.lo) | (ghi - s2.hi) | (glo - s3.lo) | (ghi - s3.hi)) & 0x80008000u;
+          if (__any_sync(0xffffffffu, any != 0u)) {
+            uint32_t hm = code_bits(s0) | (code_bits(s1) << 4) | (code_bits(s2) << 8) | (code_bits(s3) << 12);
             if (edge) {
               uint32_t ok = 0;
               for (int k = 0; k < 4; ++k) {
                 const uint32_t r = 4 * i + k;
-                if (r >= lo && r < hi) ok |= 0x10001u << k;
+                if (r >= lo && r < hi) ok |= 0xFu << (4 * k);
               }
               hm &= ok;
             }
@@ -449,13 +469,13 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
         } else {
           const uint32_t w0 = half ? v.z : v.x;
           const uint32_t w1 = half ? v.w : v.y;
-          const uint32_t s0 = lut_sum_fast<MPAD>(lbase, w0, w1);
-          const uint32_t x0 = gw - s0;
-          uint32_t hm = (x0 >> 15) & 0x10001u;
-          if (__any_sync(0xffffffffu, hm != 0u)) {
+          const Sum4 s0 = lut_sum_fast<MPAD>(lbase, w0, w1);
+          const uint32_t any = ((glo - s0.lo) | (ghi - s0.hi)) & 0x80008000u;
+          if (__any_sync(0xffffffffu, any != 0u)) {
+            uint32_t hm = code_bits(s0);
             const uint32_t r = 2 * i + half;
             if (edge && !(r >= lo && r < hi)) hm = 0u;
-            stage_hits(hm, s0, 0u, 0u, 0u, rboff + r);
+            stage_hits(hm, s0, s0, s0, s0, rboff + r);
           }
         }
       }
