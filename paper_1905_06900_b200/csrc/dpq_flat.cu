@@ -224,7 +224,7 @@ static int launch_emit_t(Index* h, EmitArgs ea, int ntiles, int64_t rows) {
   // Persistent CTAs (one per SM) pulling ~32 units each from a counter.
   const int sms = num_sms(h);
   const int64_t min_rows = (int64_t)G::CHUNK_ROWS * NW;
-  int64_t upt = std::max<int64_t>(1, (32LL * sms + ntiles - 1) / ntiles);
+  int64_t upt = std::max<int64_t>(1, (8LL * sms + ntiles - 1) / ntiles);  // ~8 units per CTA
   int64_t per = (rows + upt - 1) / upt;
   per = std::max(per, min_rows);
   per = (per + G::CHUNK_ROWS - 1) / G::CHUNK_ROWS * G::CHUNK_ROWS;
@@ -233,6 +233,7 @@ static int launch_emit_t(Index* h, EmitArgs ea, int ntiles, int64_t rows) {
   ea.units_per_tile = (int)upt;
   ea.n_units = (int)(upt * ntiles);
   ea.unit_counter = h->ws.counter;
+  ea.one = 1u;
   DPQ_CUDA(cudaMemsetAsync(h->ws.counter, 0, sizeof(unsigned), h->stream));
   const int grid = (int)std::min<int64_t>(sms, ea.n_units);
   k_scan_emit<MPAD, kScanThreads><<<grid, kScanThreads, smem, h->stream>>>(ea);

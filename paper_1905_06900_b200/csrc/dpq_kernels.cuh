@@ -197,9 +197,17 @@ __device__ __forceinline__ Sum4 lut_sum(const uint8_t* L, uint32_t w0, uint32_t 
   return s;
 }
 
+// a * b + c as an integer multiply-add: with b an opaque runtime 1 the
+// add is issued on the FMA pipe (IMAD) instead of the saturated ALU pipe.
+__device__ __forceinline__ uint32_t fma_add(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
 // Hot-path variant: base = 64-KB aligned shared address | lic * 4.
 template <int MPAD>
-__device__ __forceinline__ Sum4 lut_sum_fast(uint32_t base, uint32_t w0, uint32_t w1) {
+__device__ __forceinline__ Sum4 lut_sum_fast(uint32_t base, uint32_t w0, uint32_t w1, uint32_t one) {
   using G = ScanGeom<MPAD>;
   Sum4 s{0u, 0u};
 #pragma unroll
@@ -210,8 +218,8 @@ __device__ __forceinline__ Sum4 lut_sum_fast(uint32_t base, uint32_t w0, uint32_
     uint32_t v;
     if (j / G::SPR == 0) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
     else asm volatile("ld.shared.u32 %0, [%1+65536];" : "=r"(v) : "r"(a));
-    s.lo += v & 0x00FF00FFu;
-    s.hi += __byte_perm(v, 0u, 0x4341u);
+    s.lo = fma_add(v & 0x00FF00FFu, one, s.lo);
+    s.hi = fma_add(__byte_perm(v, 0u, 0x4341u), one, s.hi);
   }
   return s;
 }
@@ -303,6 +311,7 @@ struct EmitArgs {
   uint64_t* emit;
   uint32_t cap;
   unsigned* unit_counter;       // zeroed before launch (persistent scheduling)
+  uint32_t one;                 // = 1 (opaque to the compiler, see fma_add)
   int n_units;                  // tiles * units_per_tile
   int units_per_tile;
 };
@@ -349,6 +358,7 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
   uint64_t* hbuf = hbuf_all + warp * kWarpBuf;
   uint32_t* hcnt = hcnt_all + warp * G::QT;
   const uint32_t lt = (1u << lane) - 1u;
+  const uint32_t one = a.one, mone = 0u - a.one;  // opaque 1 / -1 (see fma_add)
   int cur_tile = -1;
   for (;;) {
     __syncthreads();  // previous unit finished by every warp
@@ -450,10 +460,11 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
       for (int i = 0; i < 32; ++i) {
         const uint4 v = wst[i];
         if (MPAD == 4) {
-          const Sum4 s0 = lut_sum_fast<MPAD>(lbase, v.x, 0), s1 = lut_sum_fast<MPAD>(lbase, v.y, 0);
-          const Sum4 s2 = lut_sum_fast<MPAD>(lbase, v.z, 0), s3 = lut_sum_fast<MPAD>(lbase, v.w, 0);
-          const uint32_t any = ((glo - s0.lo) | (ghi - s0.hi) | (glo - s1.lo) | (ghi - s1.hi) |
-                                (glo - s2.lo) | (ghi - s2.hi) | (glo - s3.lo) | (ghi - s3.hi)) & 0x80008000u;
+          const Sum4 s0 = lut_sum_fast<MPAD>(lbase, v.x, 0, one), s1 = lut_sum_fast<MPAD>(lbase, v.y, 0, one);
+          const Sum4 s2 = lut_sum_fast<MPAD>(lbase, v.z, 0, one), s3 = lut_sum_fast<MPAD>(lbase, v.w, 0, one);
+          const uint32_t any = (fma_add(s0.lo, mone, glo) | fma_add(s0.hi, mone, ghi) | fma_add(s1.lo, mone, glo) |
+                                fma_add(s1.hi, mone, ghi) | fma_add(s2.lo, mone, glo) | fma_add(s2.hi, mone, ghi) |
+                                fma_add(s3.lo, mone, glo) | fma_add(s3.hi, mone, ghi)) & 0x80008000u;
           if (__any_sync(0xffffffffu, any != 0u)) {
             uint32_t hm = code_bits(s0) | (code_bits(s1) << 4) | (code_bits(s2) << 8) | (code_bits(s3) << 12);
             if (edge) {
@@ -469,7 +480,7 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
         } else {
           const uint32_t w0 = half ? v.z : v.x;
           const uint32_t w1 = half ? v.w : v.y;
-          const Sum4 s0 = lut_sum_fast<MPAD>(lbase, w0, w1);
+          const Sum4 s0 = lut_sum_fast<MPAD>(lbase, w0, w1, one);
           const uint32_t any = ((glo - s0.lo) | (ghi - s0.hi)) & 0x80008000u;
           if (__any_sync(0xffffffffu, any != 0u)) {
             uint32_t hm = code_bits(s0);
