@@ -17,8 +17,8 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libdpq.so"
-SOURCES = ["dpq_flat.cu", "dpq_ivf.cu"]
-HEADERS = ["dpq_device.cuh", "dpq_kernels.cuh", "dpq_impl.h"]
+SOURCES = ["dpq_flat.cu"]
+HEADERS = ["dpq_device.cuh", "dpq_kernels.cuh", "dpq_impl.h", "dpq_ivf.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -86,44 +86,50 @@ static int hmalloc(T** p, size_t count) {
 static inline int qt_of(int mpad) { return mpad == 4 ? ScanGeom<4>::QT : ScanGeom<8>::QT; }
 static inline int tiles_of(int nslot, int mpad) { return (nslot + qt_of(mpad) - 1) / qt_of(mpad); }
 
-int ensure_ws(Index* h, int nslot, int r, int ystride) {
+// Slot-indexed arrays (a slot = one query for flat, one (query, probe) of a
+// query tile for ivf) are sized by nslot; query-indexed arrays (emit lists,
+// thresholds, results) by nq (default: nq = nslot).
+int ensure_ws(Index* h, int nslot, int r, int ystride, int nq) {
   Workspace& w = h->ws;
+  if (nq < 0) nq = nslot;
   const int qt = qt_of(h->mpad);
-  if (nslot > w.qb || ystride > w.ystride) {
+  if (nslot > w.qb || ystride > w.ystride || nq > w.qn) {
     const int qb = std::max(nslot, w.qb);
+    const int qn = std::max(nq, w.qn);
     const int ys = std::max(ystride, w.ystride);
     const int tiles = (qb + qt - 1) / qt;
     const size_t mk = (size_t)h->m * h->kbar;
-    DPQ_TRY(dmalloc(&w.y, (size_t)qb * ys));
+    DPQ_TRY(dmalloc(&w.y, (size_t)std::max(qb, qn) * ys));
     DPQ_TRY(dmalloc(&w.small, (size_t)qb * mk));
     DPQ_TRY(dmalloc(&w.q8, (size_t)qb * mk));
     DPQ_TRY(dmalloc(&w.qmin, (size_t)qb));
     DPQ_TRY(dmalloc(&w.qmax, (size_t)qb));
     DPQ_TRY(dmalloc(&w.bounds, (size_t)qb * 2));
-    DPQ_TRY(dmalloc(&w.lut, (size_t)tiles * h->mpad * 256 * qt));  // u8 entries
-    DPQ_TRY(dmalloc(&w.hist, (size_t)tiles * qt * 256));
-    DPQ_TRY(dmalloc(&w.hist_i, (size_t)qb * 256));
-    DPQ_TRY(dmalloc(&w.guard_b, (size_t)tiles * qt));
-    DPQ_TRY(dmalloc(&w.gword, (size_t)tiles * qt));
-    DPQ_TRY(dmalloc(&w.bstar, (size_t)qb));
-    DPQ_TRY(dmalloc(&w.ncand, (size_t)qb));
-    DPQ_TRY(dmalloc(&w.flags, (size_t)qb));
-    DPQ_TRY(dmalloc(&w.only, (size_t)tiles * qt));
+    DPQ_TRY(dmalloc(&w.lut, (size_t)tiles * h->mpad * 256 * (qt / 4) * 4));  // u8, 4 per word
+    DPQ_TRY(dmalloc(&w.hist, (size_t)std::max(tiles * qt, qn) * 256));
+    DPQ_TRY(dmalloc(&w.hist_i, (size_t)qn * 256));
+    DPQ_TRY(dmalloc(&w.guard_b, (size_t)std::max(tiles * qt, qn)));
+    DPQ_TRY(dmalloc(&w.gword, (size_t)std::max(tiles * qt, qn)));
+    DPQ_TRY(dmalloc(&w.bstar, (size_t)qn));
+    DPQ_TRY(dmalloc(&w.ncand, (size_t)qn));
+    DPQ_TRY(dmalloc(&w.flags, (size_t)qn));
+    DPQ_TRY(dmalloc(&w.only, (size_t)std::max(tiles * qt, qn)));
     DPQ_TRY(dmalloc(&w.tile_list, (size_t)tiles));
     if (!w.counter) DPQ_TRY(dmalloc(&w.counter, 4));
     DPQ_TRY(dmalloc(&w.slot_query, (size_t)tiles * qt));
     DPQ_TRY(dmalloc(&w.slot_probe, (size_t)tiles * qt));
-    DPQ_TRY(dmalloc(&w.slot_pre_off, (size_t)qb));
-    DPQ_TRY(dmalloc(&w.slot_pre_len, (size_t)qb));
-    DPQ_TRY(hmalloc(&w.h_y, (size_t)qb * ys));
-    DPQ_TRY(hmalloc(&w.h_flags, (size_t)qb));
-    DPQ_TRY(hmalloc(&w.h_cnt, (size_t)qb));
+    DPQ_TRY(dmalloc(&w.slot_pre_off, (size_t)tiles * qt));
+    DPQ_TRY(dmalloc(&w.slot_pre_len, (size_t)tiles * qt));
+    DPQ_TRY(hmalloc(&w.h_y, (size_t)std::max(qb, qn) * ys));
+    DPQ_TRY(hmalloc(&w.h_flags, (size_t)qn));
+    DPQ_TRY(hmalloc(&w.h_cnt, (size_t)qn));
     w.qb = qb;
+    w.qn = qn;
     w.ystride = ys;
     w.qcap_emit = 0;  // emit buffers re-sized below
+    w.h_out_elems = 0;
   }
-  if (w.qcap_emit < nslot || w.emit == nullptr) {
-    const int qb = w.qb;
+  if (w.qcap_emit < w.qn || w.emit == nullptr) {
     if (w.cap == 0 && h->cap0 > 0) w.cap = (uint32_t)h->cap0;
     if (w.cap == 0) {
       int64_t c = h->n / 64;
@@ -133,18 +139,18 @@ int ensure_ws(Index* h, int nslot, int r, int ystride) {
       while (p2 < c) p2 <<= 1;
       w.cap = (uint32_t)std::min<int64_t>(p2, (int64_t)1 << 31);
     }
-    DPQ_TRY(dmalloc(&w.emit_cnt, (size_t)qb));
-    DPQ_TRY(dmalloc(&w.emit, (size_t)qb * w.cap));
-    w.qcap_emit = qb;
+    DPQ_TRY(dmalloc(&w.emit_cnt, (size_t)w.qn));
+    DPQ_TRY(dmalloc(&w.emit, (size_t)w.qn * w.cap));
+    w.qcap_emit = w.qn;
   }
-  if (r > w.rcap || nslot > (int)w.h_out_elems / std::max(w.rcap, 1)) {
+  if (r > w.rcap || w.h_out_elems < (size_t)w.qn * std::max(r, w.rcap)) {
     const int rc = std::max(r, w.rcap);
-    DPQ_TRY(dmalloc(&w.out_d, (size_t)w.qb * rc));
-    DPQ_TRY(dmalloc(&w.out_i, (size_t)w.qb * rc));
-    DPQ_TRY(hmalloc(&w.h_d, (size_t)w.qb * rc));
-    DPQ_TRY(hmalloc(&w.h_i, (size_t)w.qb * rc));
+    DPQ_TRY(dmalloc(&w.out_d, (size_t)w.qn * rc));
+    DPQ_TRY(dmalloc(&w.out_i, (size_t)w.qn * rc));
+    DPQ_TRY(hmalloc(&w.h_d, (size_t)w.qn * rc));
+    DPQ_TRY(hmalloc(&w.h_i, (size_t)w.qn * rc));
     w.rcap = rc;
-    w.h_out_elems = (size_t)w.qb * rc;
+    w.h_out_elems = (size_t)w.qn * rc;
   }
   return DPQ_OK;
 }
@@ -173,7 +179,8 @@ static inline float ev_ms(Index* h, int a, int b) {
 // ---------------------------------------------------------------------------
 template <int MPAD>
 static int launch_hist_t(Index* h, int ntiles, const int* tile_list, int64_t stride,
-                         int64_t nsamp, const uint8_t* plane) {
+                         int64_t nsamp, const uint8_t* plane, const int64_t* tile_row0 = nullptr,
+                         const int64_t* tile_nsamp = nullptr) {
   using G = ScanGeom<MPAD>;
   const size_t smem = G::LUT_BYTES + (size_t)G::QT * 128 * 4;
   static bool attr = false;
@@ -191,15 +198,18 @@ static int launch_hist_t(Index* h, int ntiles, const int* tile_list, int64_t str
   if (chunks < 1) chunks = 1;
   dim3 grid(chunks, ntiles);
   k_scan_hist<MPAD, kScanThreads><<<grid, kScanThreads, smem, h->stream>>>(
-      plane, stride, nsamp, per, h->ws.lut, tile_list, h->ws.hist);
+      plane, stride, nsamp, per, h->ws.lut, tile_list, h->ws.hist, tile_row0, tile_nsamp);
   DPQ_LAUNCHED(h);
   return DPQ_OK;
 }
 
+// nsamp = samples per tile (the max when tile_nsamp is given per tile)
 static int launch_hist(Index* h, int ntiles, const int* tile_list, int64_t stride, int64_t nsamp,
-                       const uint8_t* plane) {
-  return h->mpad == 4 ? launch_hist_t<4>(h, ntiles, tile_list, stride, nsamp, plane)
-                      : launch_hist_t<8>(h, ntiles, tile_list, stride, nsamp, plane);
+                       const uint8_t* plane, const int64_t* tile_row0 = nullptr,
+                       const int64_t* tile_nsamp = nullptr) {
+  if (ntiles < 1 || nsamp < 1) return DPQ_OK;
+  return h->mpad == 4 ? launch_hist_t<4>(h, ntiles, tile_list, stride, nsamp, plane, tile_row0, tile_nsamp)
+                      : launch_hist_t<8>(h, ntiles, tile_list, stride, nsamp, plane, tile_row0, tile_nsamp);
 }
 
 static int num_sms(Index* h) {
@@ -221,8 +231,17 @@ static int launch_emit_t(Index* h, EmitArgs ea, int ntiles, int64_t rows) {
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  // Persistent CTAs (one per SM) pulling ~32 units each from a counter.
+  // Persistent CTAs (one per SM) pulling ~8 units each from a counter.
   const int sms = num_sms(h);
+  ea.unit_counter = h->ws.counter;
+  ea.one = 1u;
+  if (ea.unit_tile) {  // caller-built units (ivf lists)
+    if (ea.n_units < 1) return DPQ_OK;
+    DPQ_CUDA(cudaMemsetAsync(h->ws.counter, 0, sizeof(unsigned), h->stream));
+    k_scan_emit<MPAD, kScanThreads><<<std::min(sms, ea.n_units), kScanThreads, smem, h->stream>>>(ea);
+    DPQ_LAUNCHED(h);
+    return DPQ_OK;
+  }
   const int64_t min_rows = (int64_t)G::CHUNK_ROWS * NW;
   int64_t upt = std::max<int64_t>(1, (8LL * sms + ntiles - 1) / ntiles);  // ~8 units per CTA
   int64_t per = (rows + upt - 1) / upt;
@@ -292,10 +311,10 @@ static int launch_refine(Index* h, const RefineArgs& ra, int nq) {
 // ---------------------------------------------------------------------------
 int run_small_tables(Index* h, int nslot, const void* prefix, int64_t npre,
                      const int64_t* pre_off, const int64_t* pre_len, const double* bounds_in,
-                     bool export_debug, int ystride_override) {
+                     bool export_debug, const float* y_slots) {
   Workspace& w = h->ws;
   TablesArgs ta;
-  ta.y = w.y;
+  ta.y = y_slots ? y_slots : w.y;
   ta.dcb = h->dcb;
   ta.m = h->m; ta.kbar = h->kbar; ta.dsub = h->dsub; ta.mask = h->mask;
   ta.prefix = prefix; ta.code_bytes = h->code_bytes; ta.npre = npre;
@@ -305,7 +324,6 @@ int run_small_tables(Index* h, int nslot, const void* prefix, int64_t npre,
   ta.q8_out = w.q8;  // read by k_group_tables
   ta.qmin_out = w.qmin; ta.qmax_out = w.qmax;
   ta.lut = w.lut; ta.mpad = h->mpad; ta.qt = qt_of(h->mpad);
-  (void)ystride_override;
   const size_t smem = (size_t)(h->d + h->m * h->kbar) * 4 + (size_t)h->m * h->kbar + 16;
   static bool attr = false;
   if (!attr) {
@@ -336,7 +354,7 @@ static int flat_first_pass(Index* h, int nb, int r2) {
   DPQ_TRY(launch_hist(h, tiles, nullptr, stride, nsamp, h->plane));
   const double lambda = (double)r2 * (double)nsamp / (double)std::max<int64_t>(n, 1);
   k_guard<<<(nb + 127) / 128, 128, 0, h->stream>>>(w.hist, nb, r2, lambda, exact ? 1 : 0, nullptr,
-                                                    w.guard_b, w.gword);
+                                                    w.guard_b, w.gword, nullptr);
   DPQ_LAUNCHED(h);
   ev_rec(h, 2);
   bool first = true;
@@ -346,6 +364,7 @@ static int flat_first_pass(Index* h, int nb, int r2) {
     ea.plane = h->plane; ea.row_begin = 0; ea.row_end = n; ea.rows_per_cta = 0;
     ea.lut = w.lut; ea.gword = w.gword; ea.tile_list = nullptr;
     ea.slot_query = nullptr; ea.slot_probe = nullptr;
+    ea.unit_tile = nullptr; ea.unit_r0 = nullptr; ea.unit_r1 = nullptr;
     ea.emit_cnt = w.emit_cnt; ea.emit = w.emit; ea.cap = w.cap;
     DPQ_TRY(launch_emit(h, ea, tiles, n));
     h->counters[2] += (int64_t)nb * n;
@@ -387,7 +406,8 @@ static int flat_first_pass(Index* h, int nb, int r2) {
                                h->stream));
       DPQ_CUDA(cudaMemsetAsync(w.hist, 0, (size_t)tiles * qt * 256 * 4, h->stream));
       DPQ_TRY(launch_hist(h, (int)tl.size(), w.tile_list, 1, n, h->plane));
-      k_guard<<<(nb + 127) / 128, 128, 0, h->stream>>>(w.hist, nb, r2, 0.0, 1, w.only, w.guard_b, w.gword);
+      k_guard<<<(nb + 127) / 128, 128, 0, h->stream>>>(w.hist, nb, r2, 0.0, 1, w.only, w.guard_b, w.gword,
+                                                        nullptr);
       DPQ_LAUNCHED(h);
       DPQ_CUDA(cudaStreamSynchronize(h->stream));
     }
@@ -453,7 +473,7 @@ int run_group_tables(Index* h, int nq, int ystride) {
 static int flat_derived_batch(Index* h, int nb, int r, int r2) {
   ev_rec(h, 0);
   const int64_t npre = std::min<int64_t>(r2, h->n_prefix);
-  DPQ_TRY(run_small_tables(h, nb, h->prefix, npre, nullptr, nullptr, nullptr, false, 0));
+  DPQ_TRY(run_small_tables(h, nb, h->prefix, npre, nullptr, nullptr, nullptr, false, nullptr));
   ev_rec(h, 1);
   int rc = flat_first_pass(h, nb, r2);
   if (rc != DPQ_OK) return rc;
@@ -513,7 +533,7 @@ static int host_driver(Index* h, const float* y, int64_t nq, int r, int batch_li
   int64_t q0 = 0;
   while (q0 < nq) {
     const int nb = (int)std::min<int64_t>(bsz, nq - q0);
-    DPQ_TRY(ensure_ws(h, nb, r, h->d));
+    DPQ_TRY(ensure_ws(h, nb, r, h->d, -1));
     Workspace& w = h->ws;
     memcpy(w.h_y, y + q0 * h->d, (size_t)nb * h->d * 4);
     DPQ_CUDA(cudaMemcpyAsync(w.y, w.h_y, (size_t)nb * h->d * 4, cudaMemcpyHostToDevice, h->stream));
@@ -553,6 +573,7 @@ static int host_driver(Index* h, const float* y, int64_t nq, int r, int batch_li
 }
 
 static int make_plane(Index* h);
+static void ivf_free(Index* h);
 
 }  // namespace dpq
 
@@ -625,6 +646,7 @@ int index_common_init(Index* h, int device, int m, int k, int kbar, int dsub, co
 void index_free(Index* h) {
   if (!h) return;
   cudaSetDevice(h->device);
+  ivf_free(h);
   if (h->stream) cudaStreamSynchronize(h->stream);
   Workspace& w = h->ws;
   void* dev[] = {h->cb, h->dcb, h->codes, h->plane, h->own_prefix ? h->prefix : nullptr, h->centers,
@@ -761,7 +783,7 @@ int dpq_flat_search_derived_dev(dpq_index_t* index, const float* yr, int64_t nq,
   int64_t q0 = 0;
   while (q0 < nq) {
     const int nb = (int)std::min<int64_t>(bsz, nq - q0);
-    DPQ_TRY(ensure_ws(h, nb, r, h->d));
+    DPQ_TRY(ensure_ws(h, nb, r, h->d, -1));
     Workspace& w = h->ws;
     DPQ_CUDA(cudaMemcpyAsync(w.y, yr + q0 * h->d, (size_t)nb * h->d * 4, cudaMemcpyDeviceToDevice, h->stream));
     int rc = flat_derived_batch(h, nb, r, r2);
@@ -793,11 +815,11 @@ int dpq_debug_quantize_tables(dpq_index_t* index, const float* yr, int64_t nq, i
   const int64_t mk = (int64_t)h->m * h->kbar;
   for (int64_t q0 = 0; q0 < nq; q0 += h->batch) {
     const int nb = (int)std::min<int64_t>(h->batch, nq - q0);
-    DPQ_TRY(ensure_ws(h, nb, 1, h->d));
+    DPQ_TRY(ensure_ws(h, nb, 1, h->d, -1));
     Workspace& w = h->ws;
     DPQ_CUDA(cudaMemcpyAsync(w.y, yr + q0 * h->d, (size_t)nb * h->d * 4, cudaMemcpyHostToDevice, h->stream));
     DPQ_TRY(run_small_tables(h, nb, h->prefix, std::min<int64_t>(r2, h->n_prefix), nullptr, nullptr, nullptr,
-                             true, 0));
+                             true, nullptr));
     DPQ_CUDA(cudaMemcpyAsync(small + q0 * mk, w.small, (size_t)nb * mk * 4, cudaMemcpyDeviceToHost, h->stream));
     DPQ_CUDA(cudaMemcpyAsync(q + q0 * mk, w.q8, (size_t)nb * mk, cudaMemcpyDeviceToHost, h->stream));
     DPQ_CUDA(cudaMemcpyAsync(qmin + q0, w.qmin, (size_t)nb * 8, cudaMemcpyDeviceToHost, h->stream));
@@ -814,11 +836,11 @@ int dpq_debug_candidates(dpq_index_t* index, const float* yr, int64_t nq, int r2
   if (h->kind != KIND_FLAT) { set_error("not a flat index"); return DPQ_ERR_STATE; }
   for (int64_t q0 = 0; q0 < nq; q0 += h->batch) {
     const int nb = (int)std::min<int64_t>(h->batch, nq - q0);
-    DPQ_TRY(ensure_ws(h, nb, 1, h->d));
+    DPQ_TRY(ensure_ws(h, nb, 1, h->d, -1));
     Workspace& w = h->ws;
     DPQ_CUDA(cudaMemcpyAsync(w.y, yr + q0 * h->d, (size_t)nb * h->d * 4, cudaMemcpyHostToDevice, h->stream));
     DPQ_TRY(run_small_tables(h, nb, h->prefix, std::min<int64_t>(r2, h->n_prefix), nullptr, nullptr, nullptr,
-                             false, 0));
+                             false, nullptr));
     int rc = flat_first_pass(h, nb, r2);
     if (rc == 100) { set_error("debug_candidates: emit budget exceeded, use a smaller batch"); return DPQ_ERR_NOMEM; }
     if (rc != DPQ_OK) return rc;
@@ -834,7 +856,7 @@ int dpq_debug_full_tables(dpq_index_t* index, const float* yr, int64_t nq, float
   DPQ_TRY(check_search(h, nq, 1, 1, false));
   const int64_t per = (int64_t)h->m * h->k;
   for (int64_t q0 = 0; q0 < nq; ++q0) {
-    DPQ_TRY(ensure_ws(h, 1, 1, h->d));
+    DPQ_TRY(ensure_ws(h, 1, 1, h->d, -1));
     Workspace& w = h->ws;
     if (per > w.tables_elems) {
       DPQ_TRY(dmalloc(&w.tables, (size_t)per));
@@ -880,3 +902,5 @@ int dpq_counters(dpq_index_t* index, int64_t* out8) {
 }
 
 }  // extern "C"
+
+#include "dpq_ivf.cuh"

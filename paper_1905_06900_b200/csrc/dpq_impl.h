@@ -17,7 +17,8 @@ enum Phase { PH_TABLES = 0, PH_GUARD, PH_SCAN, PH_THRESH, PH_REFINE, PH_FALLBACK
 
 // Per-batch device workspace, grown on demand.
 struct Workspace {
-  int qb = 0;             // query (slot) capacity
+  int qb = 0;             // slot capacity
+  int qn = 0;             // query capacity
   int rcap = 0;           // result columns capacity
   uint32_t cap = 0;       // emit capacity per query
   int qcap_emit = 0;      // queries the emit buffer is sized for
@@ -77,6 +78,7 @@ struct Index {
   int64_t* offsets = nullptr;     // device [K+1]
   std::vector<int64_t> h_offsets; // host copy
   int64_t* sorted_ids = nullptr;  // [n]
+  void* ivf_state = nullptr;      // IvfBuffers (dpq_ivf.cuh)
   // execution
   cudaStream_t stream = nullptr;
   bool own_stream = false;

@@ -1,0 +1,727 @@
+// dpq_ivf.cuh — inverted-file search (IVFIndex, ivf.py:107-277) and the
+// sharded-flat split API.  Included at the end of dpq_flat.cu
+// (same translation unit: the kernels are header-defined).
+//
+// IVF derived batch (nb queries, ma probes each):
+//   probe (f64 centre distances, top-ma with lower-id ties)
+//   -> slots (query, probe) of non-empty lists, grouped by cell into query
+//      tiles of QT slots: every list is streamed once per tile of queries
+//      probing it ("query-by-list batching")
+//   -> K1 twice: small tables per slot; qmin/qmax from the first non-empty
+//      probed list of each query (ivf.py:205-217); quantize every slot with
+//      its query's bounds
+//   -> guard per query from per-list sampled histograms
+//   -> the flat scan kernel over (tile, list row range) units, emitting into
+//      per-query lists (one candidate pool per query, ivf.py:222-236)
+//   -> K3 per query -> refine each candidate in its own cell's residual
+//      frame (ivf.py:253-268), ids = sorted_ids_.
+#pragma once
+
+namespace dpq {
+
+// ---------------------------------------------------------------------------
+// probe: d2[c] = sum_t (c_t - y_t)^2 in f64, ascending, ties to lower cell.
+// ---------------------------------------------------------------------------
+template <int BUF, int NT>
+__global__ void __launch_bounds__(NT) k_probe(const float* __restrict__ y, int d,
+                                              const float* __restrict__ centers, int K, int ma,
+                                              int64_t* __restrict__ cells) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint64_t* keys = reinterpret_cast<uint64_t*>(smem);
+  int64_t* ids = reinterpret_cast<int64_t*>(keys + BUF);
+  float* ys = reinterpret_cast<float*>(ids + BUF);
+  __shared__ int fill;
+  __shared__ uint64_t thr_k;
+  __shared__ int64_t thr_i;
+  const int q = blockIdx.x;
+  for (int i = threadIdx.x; i < d; i += NT) ys[i] = y[(int64_t)q * d + i];
+  if (threadIdx.x == 0) { fill = 0; thr_k = ~0ull; thr_i = INT64_MAX; }
+  __syncthreads();
+  for (int base = 0; base < K; base += NT) {
+    const int c = base + threadIdx.x;
+    bool keep = false;
+    uint64_t key = 0;
+    if (c < K) {
+      const float* cr = centers + (int64_t)c * d;
+      double acc = 0.0;
+      for (int t = 0; t < d; ++t) {
+        const double df = __dsub_rn((double)cr[t], (double)ys[t]);
+        acc = __dadd_rn(acc, __dmul_rn(df, df));
+      }
+      key = (uint64_t)__double_as_longlong(acc);
+      keep = pair_less(key, c, thr_k, thr_i);
+    }
+    if (keep) {
+      const int p = atomicAdd(&fill, 1);
+      keys[p] = key;
+      ids[p] = c;
+    }
+    __syncthreads();
+    const int f = fill;
+    __syncthreads();
+    if (f > BUF - NT) {
+      for (int i = f + threadIdx.x; i < BUF; i += NT) { keys[i] = ~0ull; ids[i] = INT64_MAX; }
+      __syncthreads();
+      sort_pairs<BUF, NT>(keys, ids);
+      if (threadIdx.x == 0) {
+        const int nf = min(f, ma);
+        fill = nf;
+        if (nf == ma) { thr_k = keys[nf - 1]; thr_i = ids[nf - 1]; }
+      }
+      __syncthreads();
+    }
+  }
+  const int f = fill;
+  for (int i = f + threadIdx.x; i < BUF; i += NT) { keys[i] = ~0ull; ids[i] = INT64_MAX; }
+  __syncthreads();
+  sort_pairs<BUF, NT>(keys, ids);
+  for (int i = threadIdx.x; i < ma; i += NT) cells[(int64_t)q * ma + i] = ids[i];
+}
+
+// residuals y - centre in f32 (ivf.py:120), natural (query, probe) order
+__global__ void k_residuals(const float* __restrict__ y, const float* __restrict__ centers,
+                            const int64_t* __restrict__ cells, int nq, int ma, int d,
+                            float* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t total = (int64_t)nq * ma * d;
+  if (i >= total) return;
+  const int t = (int)(i % d);
+  const int64_t s = i / d;
+  const int q = (int)(s / ma);
+  out[i] = __fsub_rn(y[(int64_t)q * d + t], centers[cells[s] * d + t]);
+}
+
+// per tile-slot copy of its (query, probe) residual; zeros for padding
+__global__ void k_gather_slots(const float* __restrict__ ynat, const int* __restrict__ slot_query,
+                               const int* __restrict__ slot_probe, int ma, int d, int nts,
+                               float* __restrict__ yts) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)nts * d) return;
+  const int ts = (int)(i / d), t = (int)(i % d);
+  const int q = slot_query[ts];
+  yts[i] = q < 0 ? 0.f : ynat[((int64_t)q * ma + slot_probe[ts]) * d + t];
+}
+
+// bounds of every slot = (qmin, qmax) of its query's first non-empty list
+__global__ void k_slot_bounds(const double* __restrict__ qmin, const double* __restrict__ qmax,
+                              const int* __restrict__ bound_ts, const int* __restrict__ slot_query,
+                              int nts, double* __restrict__ bounds) {
+  const int ts = blockIdx.x * blockDim.x + threadIdx.x;
+  if (ts >= nts) return;
+  const int q = slot_query[ts];
+  const int b = q < 0 ? -1 : bound_ts[q];
+  bounds[2 * ts] = b < 0 ? 0.0 : qmin[b];
+  bounds[2 * ts + 1] = b < 0 ? 0.0 : qmax[b];
+}
+
+__global__ void k_slot_hist_to_query(const uint32_t* __restrict__ hts, const int* __restrict__ slot_query,
+                                     int nts, uint32_t* __restrict__ hq) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)nts * 256) return;
+  const int ts = (int)(i >> 8), b = (int)(i & 255);
+  const int q = slot_query[ts];
+  const uint32_t v = hts[i];
+  if (q >= 0 && v) atomicAdd(hq + (int64_t)q * 256 + b, v);
+}
+
+__global__ void k_expand_gword(const uint16_t* __restrict__ gq, const int* __restrict__ slot_query, int nts,
+                               uint16_t* __restrict__ gts) {
+  const int ts = blockIdx.x * blockDim.x + threadIdx.x;
+  if (ts >= nts) return;
+  const int q = slot_query[ts];
+  gts[ts] = q < 0 ? (uint16_t)0x7F7F : gq[q];
+}
+
+// Conventional IVF scan (ivf.py:162-193): every row of every probed list is
+// a candidate; exact entries computed per row in its cell's frame.
+struct IvfConvArgs {
+  const int64_t* cells; const int64_t* offsets; int ma;
+  const void* codes; int code_bytes; int m, k, dsub;
+  const float* cb; const float* ynat; const int64_t* sorted_ids;
+  int r; double* out_d; int64_t* out_i;
+};
+
+template <int BUF, int NT>
+__global__ void __launch_bounds__(NT) k_ivf_conventional(IvfConvArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint64_t* keys = reinterpret_cast<uint64_t*>(smem);
+  int64_t* ids = reinterpret_cast<int64_t*>(keys + BUF);
+  float* ys = reinterpret_cast<float*>(ids + BUF);
+  __shared__ int fill;
+  __shared__ uint64_t thr_k;
+  __shared__ int64_t thr_i;
+  const int q = blockIdx.x;
+  const int d = a.m * a.dsub;
+  for (int i = threadIdx.x; i < a.ma * d; i += NT) ys[i] = a.ynat[(int64_t)q * a.ma * d + i];
+  if (threadIdx.x == 0) { fill = 0; thr_k = ~0ull; thr_i = INT64_MAX; }
+  __syncthreads();
+  for (int p = 0; p < a.ma; ++p) {
+    const int64_t cell = a.cells[(int64_t)q * a.ma + p];
+    const int64_t lo = a.offsets[cell], hi = a.offsets[cell + 1];
+    for (int64_t base = lo; base < hi; base += NT) {
+      const int64_t row = base + threadIdx.x;
+      bool keep = false;
+      uint64_t key = 0;
+      int64_t id = 0;
+      if (row < hi) {
+        double dist = 0.0;
+        for (int j = 0; j < a.m; ++j) {
+          const uint32_t c = code_at(a.codes, a.code_bytes, row * a.m + j);
+          const float t = pw_sqdist(a.cb + ((int64_t)j * a.k + c) * a.dsub, ys + p * d + j * a.dsub, a.dsub);
+          dist = __dadd_rn(dist, (double)t);
+        }
+        key = (uint64_t)__double_as_longlong(dist);
+        id = a.sorted_ids[row];
+        keep = pair_less(key, id, thr_k, thr_i);
+      }
+      if (keep) {
+        const int pp = atomicAdd(&fill, 1);
+        keys[pp] = key;
+        ids[pp] = id;
+      }
+      __syncthreads();
+      const int f = fill;
+      __syncthreads();
+      if (f > BUF - NT) {
+        for (int i = f + threadIdx.x; i < BUF; i += NT) { keys[i] = ~0ull; ids[i] = INT64_MAX; }
+        __syncthreads();
+        sort_pairs<BUF, NT>(keys, ids);
+        if (threadIdx.x == 0) {
+          const int nf = min(f, a.r);
+          fill = nf;
+          if (nf == a.r) { thr_k = keys[nf - 1]; thr_i = ids[nf - 1]; }
+        }
+        __syncthreads();
+      }
+    }
+  }
+  const int f = fill;
+  for (int i = f + threadIdx.x; i < BUF; i += NT) { keys[i] = ~0ull; ids[i] = INT64_MAX; }
+  __syncthreads();
+  sort_pairs<BUF, NT>(keys, ids);
+  const int got = min(f, a.r);
+  for (int i = threadIdx.x; i < a.r; i += NT) {
+    const int64_t o = (int64_t)q * a.r + i;
+    a.out_d[o] = i < got ? __longlong_as_double((long long)keys[i]) : INFINITY;
+    a.out_i[o] = i < got ? ids[i] : -1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Host side
+// ---------------------------------------------------------------------------
+struct IvfPlan {
+  int nq = 0, ma = 0, nts = 0, ntiles = 0;
+  std::vector<int64_t> cells;          // (nq, ma)
+  std::vector<int> slot_query, slot_probe, tile_cell, bound_ts;
+  std::vector<int64_t> pre_off, pre_len, tile_row0, tile_nsamp;
+  std::vector<int> unit_tile;
+  std::vector<int64_t> unit_r0, unit_r1;
+  std::vector<double> lambda;          // per query, <0 = exact histogram
+  int64_t stride = 1, max_nsamp = 0;
+};
+
+struct IvfBuffers {
+  int cap_q = 0, cap_ts = 0, cap_units = 0, cap_tiles = 0, cap_ma = 0;
+  int64_t* cells = nullptr;
+  float* ynat = nullptr;
+  float* yts = nullptr;
+  int* bound_ts = nullptr;
+  double* lambda = nullptr;
+  uint32_t* hist_q = nullptr;
+  uint16_t* gword_q = nullptr;
+  uint16_t* guard_q = nullptr;
+  int* unit_tile = nullptr;
+  int64_t* unit_r0 = nullptr;
+  int64_t* unit_r1 = nullptr;
+  int64_t* tile_row0 = nullptr;
+  int64_t* tile_nsamp = nullptr;
+};
+
+static IvfBuffers& ivf_bufs(Index* h) { return *reinterpret_cast<IvfBuffers*>(h->ivf_state); }
+
+static int ivf_ensure(Index* h, int nq, int ma, int nts, int ntiles, int nunits) {
+  IvfBuffers& b = ivf_bufs(h);
+  const int d = h->d;
+  if (nq > b.cap_q || ma > b.cap_ma) {
+    b.cap_q = std::max(nq, b.cap_q);
+    b.cap_ma = std::max(ma, b.cap_ma);
+    DPQ_TRY(dmalloc(&b.cells, (size_t)b.cap_q * b.cap_ma));
+    DPQ_TRY(dmalloc(&b.ynat, (size_t)b.cap_q * b.cap_ma * d));
+    DPQ_TRY(dmalloc(&b.bound_ts, (size_t)b.cap_q));
+    DPQ_TRY(dmalloc(&b.lambda, (size_t)b.cap_q));
+    DPQ_TRY(dmalloc(&b.hist_q, (size_t)b.cap_q * 256));
+    DPQ_TRY(dmalloc(&b.gword_q, (size_t)b.cap_q));
+    DPQ_TRY(dmalloc(&b.guard_q, (size_t)b.cap_q));
+  }
+  if (nts > b.cap_ts) {
+    b.cap_ts = nts;
+    DPQ_TRY(dmalloc(&b.yts, (size_t)b.cap_ts * d));
+  }
+  if (ntiles > b.cap_tiles) {
+    b.cap_tiles = ntiles;
+    DPQ_TRY(dmalloc(&b.tile_row0, (size_t)ntiles));
+    DPQ_TRY(dmalloc(&b.tile_nsamp, (size_t)ntiles));
+  }
+  if (nunits > b.cap_units) {
+    b.cap_units = nunits;
+    DPQ_TRY(dmalloc(&b.unit_tile, (size_t)nunits));
+    DPQ_TRY(dmalloc(&b.unit_r0, (size_t)nunits));
+    DPQ_TRY(dmalloc(&b.unit_r1, (size_t)nunits));
+  }
+  return DPQ_OK;
+}
+
+static void ivf_free(Index* h) {
+  if (!h->ivf_state) return;
+  IvfBuffers& b = ivf_bufs(h);
+  void* p[] = {b.cells, b.ynat, b.yts, b.bound_ts, b.lambda, b.hist_q, b.gword_q, b.guard_q,
+               b.unit_tile, b.unit_r0, b.unit_r1, b.tile_row0, b.tile_nsamp};
+  for (void* x : p)
+    if (x) cudaFree(x);
+  delete reinterpret_cast<IvfBuffers*>(h->ivf_state);
+  h->ivf_state = nullptr;
+}
+
+// Probe on device: cells (nb, ma) into bufs.cells.
+static int ivf_probe_dev(Index* h, int nb, int ma) {
+  IvfBuffers& b = ivf_bufs(h);
+  const int need = ma + 256;
+  const size_t ys = (size_t)h->d * 4;
+  auto go = [&](auto kern, int BUF) {
+    const size_t smem = (size_t)BUF * 16 + ys;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 49152));
+    kern<<<nb, 256, smem, h->stream>>>(h->ws.y, h->d, h->centers, h->n_cells, ma, b.cells);
+  };
+  if (need <= 1024) go(k_probe<1024, 256>, 1024);
+  else if (need <= 2048) go(k_probe<2048, 256>, 2048);
+  else if (need <= 4096) go(k_probe<4096, 256>, 4096);
+  else if (need <= 8192) go(k_probe<8192, 256>, 8192);
+  else { set_error("ma too large for the device probe (<= 7936)"); return DPQ_ERR_ARG; }
+  DPQ_LAUNCHED(h);
+  return DPQ_OK;
+}
+
+// Build the slot / tile / unit plan on the host from the probe result.
+static void ivf_plan(Index* h, IvfPlan& P, int nb, int ma, int r2) {
+  const int qt = qt_of(h->mpad);
+  const std::vector<int64_t>& off = h->h_offsets;
+  P.nq = nb;
+  P.ma = ma;
+  struct S { int64_t cell; int q, p; };
+  std::vector<S> ne;
+  ne.reserve((size_t)nb * ma);
+  std::vector<int> first(nb, -1);
+  int64_t tot_rows = 0;
+  for (int q = 0; q < nb; ++q)
+    for (int p = 0; p < ma; ++p) {
+      const int64_t c = P.cells[(size_t)q * ma + p];
+      const int64_t len = off[c + 1] - off[c];
+      if (len <= 0) continue;
+      if (first[q] < 0) first[q] = p;
+      ne.push_back({c, q, p});
+      tot_rows += len;
+    }
+  std::stable_sort(ne.begin(), ne.end(), [](const S& x, const S& y) { return x.cell < y.cell; });
+  P.slot_query.clear(); P.slot_probe.clear(); P.tile_cell.clear();
+  std::vector<int> ts_of((size_t)nb * ma, -1);
+  for (size_t i = 0; i < ne.size();) {
+    size_t j = i;
+    while (j < ne.size() && ne[j].cell == ne[i].cell) ++j;
+    for (size_t t0 = i; t0 < j; t0 += qt) {
+      const int tile = (int)P.tile_cell.size();
+      P.tile_cell.push_back((int)ne[i].cell);
+      for (int qq = 0; qq < qt; ++qq) {
+        const size_t k = t0 + qq;
+        if (k < j) {
+          P.slot_query.push_back(ne[k].q);
+          P.slot_probe.push_back(ne[k].p);
+          ts_of[(size_t)ne[k].q * ma + ne[k].p] = tile * qt + qq;
+        } else {
+          P.slot_query.push_back(-1);
+          P.slot_probe.push_back(0);
+        }
+      }
+    }
+    i = j;
+  }
+  P.ntiles = (int)P.tile_cell.size();
+  P.nts = P.ntiles * qt;
+  // qmax prefix: first min(r2, len) rows of each query's first non-empty list
+  P.pre_off.assign(P.nts, 0);
+  P.pre_len.assign(P.nts, 0);
+  P.bound_ts.assign(nb, -1);
+  for (int q = 0; q < nb; ++q) {
+    if (first[q] < 0) continue;
+    const int64_t c = P.cells[(size_t)q * ma + first[q]];
+    const int ts = ts_of[(size_t)q * ma + first[q]];
+    P.bound_ts[q] = ts;
+    P.pre_off[ts] = off[c];
+    P.pre_len[ts] = std::min<int64_t>(r2, off[c + 1] - off[c]);
+  }
+  // guard sampling: one stride for the batch, exact when lists are short
+  const int64_t avg = nb > 0 ? tot_rows / std::max(1, nb) : 0;
+  P.stride = (avg <= h->exact_limit) ? 1 : std::max<int64_t>(1, avg / std::max<int64_t>(1, h->sample));
+  P.tile_row0.assign(P.ntiles, 0);
+  P.tile_nsamp.assign(P.ntiles, 0);
+  P.max_nsamp = 0;
+  for (int t = 0; t < P.ntiles; ++t) {
+    const int64_t c = P.tile_cell[t];
+    const int64_t len = off[c + 1] - off[c];
+    P.tile_row0[t] = off[c];
+    P.tile_nsamp[t] = (len + P.stride - 1) / P.stride;
+    P.max_nsamp = std::max(P.max_nsamp, P.tile_nsamp[t]);
+  }
+  P.lambda.assign(nb, -1.0);
+  if (P.stride > 1) {
+    std::vector<int64_t> sq(nb, 0), nr(nb, 0);
+    for (const S& x : ne) {
+      const int64_t len = off[x.cell + 1] - off[x.cell];
+      sq[x.q] += (len + P.stride - 1) / P.stride;
+      nr[x.q] += len;
+    }
+    for (int q = 0; q < nb; ++q)
+      P.lambda[q] = nr[q] > 0 ? (double)r2 * (double)sq[q] / (double)nr[q] : -1.0;
+  }
+  // scan units: each tile's list split into row ranges, ~8 units per SM
+  const int sms = num_sms(h);
+  const int64_t target = std::max<int64_t>(1, (8LL * sms));
+  int64_t tot_tile_rows = 0;
+  for (int t = 0; t < P.ntiles; ++t) tot_tile_rows += off[P.tile_cell[t] + 1] - off[P.tile_cell[t]];
+  int64_t per = std::max<int64_t>(4096, (tot_tile_rows + target - 1) / target);
+  P.unit_tile.clear(); P.unit_r0.clear(); P.unit_r1.clear();
+  for (int t = 0; t < P.ntiles; ++t) {
+    const int64_t lo = off[P.tile_cell[t]], hi = off[P.tile_cell[t] + 1];
+    for (int64_t r0 = lo; r0 < hi; r0 += per) {
+      P.unit_tile.push_back(t);
+      P.unit_r0.push_back(r0);
+      P.unit_r1.push_back(std::min(hi, r0 + per));
+    }
+  }
+}
+
+template <class T>
+static int h2d(T* dst, const std::vector<T>& v, cudaStream_t s) {
+  if (v.empty()) return DPQ_OK;
+  DPQ_CUDA(cudaMemcpyAsync(dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+  return DPQ_OK;
+}
+
+// One IVF batch: raw queries in ws.y (nb x d).  res_rot / cells_in are host
+// arrays for the OPQ path (residuals rotated by the caller), else NULL.
+static int ivf_batch(Index* h, int nb, int r, int ma, int r2, bool derived, const float* res_rot,
+                     const int64_t* cells_in) {
+  Workspace& w = h->ws;
+  IvfBuffers& B = ivf_bufs(h);
+  const int d = h->d;
+  const int qt = qt_of(h->mpad);
+  ev_rec(h, 0);
+  DPQ_TRY(ivf_ensure(h, nb, ma, 0, 0, 0));
+  IvfPlan P;
+  P.cells.resize((size_t)nb * ma);
+  if (cells_in) {
+    memcpy(P.cells.data(), cells_in, P.cells.size() * 8);
+    DPQ_TRY(h2d(B.cells, P.cells, h->stream));
+  } else {
+    DPQ_TRY(ivf_probe_dev(h, nb, ma));
+    DPQ_CUDA(cudaMemcpyAsync(P.cells.data(), B.cells, P.cells.size() * 8, cudaMemcpyDeviceToHost, h->stream));
+    DPQ_CUDA(cudaStreamSynchronize(h->stream));
+  }
+  ev_rec(h, 1);
+  // residuals in natural (query, probe) order
+  if (res_rot) {
+    DPQ_CUDA(cudaMemcpyAsync(B.ynat, res_rot, (size_t)nb * ma * d * 4, cudaMemcpyHostToDevice, h->stream));
+  } else {
+    const int64_t tot = (int64_t)nb * ma * d;
+    k_residuals<<<(unsigned)((tot + 255) / 256), 256, 0, h->stream>>>(w.y, h->centers, B.cells, nb, ma, d, B.ynat);
+    DPQ_LAUNCHED(h);
+  }
+  if (!derived) {
+    IvfConvArgs a;
+    a.cells = B.cells; a.offsets = h->offsets; a.ma = ma;
+    a.codes = h->codes; a.code_bytes = h->code_bytes; a.m = h->m; a.k = h->k; a.dsub = h->dsub;
+    a.cb = h->cb; a.ynat = B.ynat; a.sorted_ids = h->sorted_ids;
+    a.r = r; a.out_d = w.out_d; a.out_i = w.out_i;
+    const size_t ysm = (size_t)ma * d * 4;
+    auto go = [&](auto kern, int BUF) {
+      const size_t smem = (size_t)BUF * 16 + ysm;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 49152));
+      kern<<<nb, 256, smem, h->stream>>>(a);
+    };
+    const int need = r + 256;
+    if (need <= 1024) go(k_ivf_conventional<1024, 256>, 1024);
+    else if (need <= 2048) go(k_ivf_conventional<2048, 256>, 2048);
+    else if (need <= 4096) go(k_ivf_conventional<4096, 256>, 4096);
+    else if (need <= 8192) go(k_ivf_conventional<8192, 256>, 8192);
+    else { set_error("r exceeds the device top-r limit (7936)"); return DPQ_ERR_ARG; }
+    DPQ_LAUNCHED(h);
+    ev_rec(h, 6);
+    if (h->timing) {
+      DPQ_CUDA(cudaEventSynchronize(h->ev[6]));
+      h->phase_ms[PH_GUARD] = 0.f;  // index phase reported separately below
+      h->phase_ms[PH_TABLES] = 0.f;
+      h->phase_ms[PH_SCAN] = ev_ms(h, 1, 6);
+      h->phase_ms[PH_REFINE] = 0.f;
+      h->phase_ms[PH_THRESH] = 0.f;
+      h->phase_ms[PH_FALLBACK] = ev_ms(h, 0, 1);  // probe
+      h->phase_ms[PH_TOTAL] = ev_ms(h, 0, 6);
+    }
+    h->counters[1] += nb;
+    return DPQ_OK;
+  }
+  ivf_plan(h, P, nb, ma, r2);
+  DPQ_TRY(ensure_ws(h, std::max(P.nts, 1), r, d, nb));
+  DPQ_TRY(ivf_ensure(h, nb, ma, std::max(P.nts, 1), std::max(P.ntiles, 1), std::max((int)P.unit_tile.size(), 1)));
+  DPQ_TRY(h2d(w.slot_query, P.slot_query, h->stream));
+  DPQ_TRY(h2d(w.slot_probe, P.slot_probe, h->stream));
+  DPQ_TRY(h2d(w.slot_pre_off, P.pre_off, h->stream));
+  DPQ_TRY(h2d(w.slot_pre_len, P.pre_len, h->stream));
+  DPQ_TRY(h2d(B.bound_ts, P.bound_ts, h->stream));
+  DPQ_TRY(h2d(B.lambda, P.lambda, h->stream));
+  DPQ_TRY(h2d(B.tile_row0, P.tile_row0, h->stream));
+  DPQ_TRY(h2d(B.tile_nsamp, P.tile_nsamp, h->stream));
+  DPQ_TRY(h2d(B.unit_tile, P.unit_tile, h->stream));
+  DPQ_TRY(h2d(B.unit_r0, P.unit_r0, h->stream));
+  DPQ_TRY(h2d(B.unit_r1, P.unit_r1, h->stream));
+  DPQ_CUDA(cudaMemsetAsync(w.emit_cnt, 0, (size_t)nb * 4, h->stream));
+  if (P.nts == 0) {  // every probed list is empty: empty results (ivf.py:230-233)
+    DPQ_CUDA(cudaMemsetAsync(w.bstar, 0xFF, (size_t)nb * 4, h->stream));
+  } else {
+    const int64_t tot = (int64_t)P.nts * d;
+    k_gather_slots<<<(unsigned)((tot + 255) / 256), 256, 0, h->stream>>>(B.ynat, w.slot_query, w.slot_probe, ma, d,
+                                                                        P.nts, B.yts);
+    DPQ_LAUNCHED(h);
+    // K1 pass A: per-slot tables; qmin/qmax of the bound-source slots
+    DPQ_TRY(run_small_tables(h, P.nts, h->codes, 0, w.slot_pre_off, w.slot_pre_len, nullptr, false, B.yts));
+    k_slot_bounds<<<(P.nts + 255) / 256, 256, 0, h->stream>>>(w.qmin, w.qmax, B.bound_ts, w.slot_query, P.nts,
+                                                              w.bounds);
+    DPQ_LAUNCHED(h);
+    // K1 pass B: quantize every slot with its query's bounds -> LUT tiles
+    DPQ_TRY(run_small_tables(h, P.nts, h->codes, 0, nullptr, nullptr, w.bounds, false, B.yts));
+    ev_rec(h, 2);
+    // guard per query from per-list sampled histograms
+    auto make_guards = [&](int64_t stride, bool exact, const uint8_t* only) -> int {
+      DPQ_CUDA(cudaMemsetAsync(w.hist, 0, (size_t)P.nts * 256 * 4, h->stream));
+      DPQ_CUDA(cudaMemsetAsync(B.hist_q, 0, (size_t)nb * 256 * 4, h->stream));
+      std::vector<int64_t> ns(P.ntiles);
+      int64_t mx = 0;
+      for (int t = 0; t < P.ntiles; ++t) {
+        const int64_t len = h->h_offsets[P.tile_cell[t] + 1] - h->h_offsets[P.tile_cell[t]];
+        ns[t] = (len + stride - 1) / stride;
+        mx = std::max(mx, ns[t]);
+      }
+      DPQ_TRY(h2d(B.tile_nsamp, ns, h->stream));
+      DPQ_TRY(launch_hist(h, P.ntiles, nullptr, stride, mx, h->plane, B.tile_row0, B.tile_nsamp));
+      k_slot_hist_to_query<<<(unsigned)(((int64_t)P.nts * 256 + 255) / 256), 256, 0, h->stream>>>(
+          w.hist, w.slot_query, P.nts, B.hist_q);
+      DPQ_LAUNCHED(h);
+      k_guard<<<(nb + 127) / 128, 128, 0, h->stream>>>(B.hist_q, nb, r2, 0.0, exact ? 1 : 0, only, B.guard_q,
+                                                        B.gword_q, exact ? nullptr : B.lambda);
+      DPQ_LAUNCHED(h);
+      k_expand_gword<<<(P.nts + 255) / 256, 256, 0, h->stream>>>(B.gword_q, w.slot_query, P.nts, w.gword);
+      DPQ_LAUNCHED(h);
+      return DPQ_OK;
+    };
+    DPQ_TRY(make_guards(P.stride, P.stride == 1, nullptr));
+    ev_rec(h, 3);
+    for (int attempt = 0; attempt < 8; ++attempt) {
+      DPQ_CUDA(cudaMemsetAsync(w.emit_cnt, 0, (size_t)nb * 4, h->stream));
+      EmitArgs ea;
+      ea.plane = h->plane; ea.row_begin = 0; ea.row_end = h->n; ea.rows_per_cta = 0;
+      ea.lut = w.lut; ea.gword = w.gword; ea.tile_list = nullptr;
+      ea.slot_query = w.slot_query; ea.slot_probe = w.slot_probe;
+      ea.emit_cnt = w.emit_cnt; ea.emit = w.emit; ea.cap = w.cap;
+      ea.unit_tile = B.unit_tile; ea.unit_r0 = B.unit_r0; ea.unit_r1 = B.unit_r1;
+      ea.n_units = (int)P.unit_tile.size(); ea.units_per_tile = 1;
+      DPQ_TRY(launch_emit(h, ea, P.ntiles, 0));
+      k_threshold<256><<<nb, 256, 0, h->stream>>>(w.emit, w.emit_cnt, w.cap, B.guard_q, r2, nullptr, w.bstar,
+                                                  w.ncand, w.flags, nullptr, h->d_nemit);
+      DPQ_LAUNCHED(h);
+      DPQ_CUDA(cudaMemcpyAsync(w.h_flags, w.flags, nb, cudaMemcpyDeviceToHost, h->stream));
+      DPQ_CUDA(cudaStreamSynchronize(h->stream));
+      bool any_exact = false, any_over = false;
+      for (int q = 0; q < nb; ++q) {
+        any_exact |= w.h_flags[q] == 1;
+        any_over |= w.h_flags[q] == 2;
+      }
+      if (!any_exact && !any_over) break;
+      if (attempt == 7) { set_error("ivf first pass did not converge"); return DPQ_ERR_CUDA; }
+      h->counters[4]++;
+      if (any_over) {
+        DPQ_CUDA(cudaMemcpyAsync(w.h_cnt, w.emit_cnt, (size_t)nb * 4, cudaMemcpyDeviceToHost, h->stream));
+        DPQ_CUDA(cudaStreamSynchronize(h->stream));
+        uint32_t need = 0;
+        for (int q = 0; q < nb; ++q)
+          if (w.h_flags[q] == 2) need = std::max(need, w.h_cnt[q]);
+        if ((size_t)w.qcap_emit * need * 8 > h->emit_budget && nb > 1) return 100;
+        DPQ_TRY(grow_emit(h, need));
+      }
+      if (any_exact) {
+        for (int q = 0; q < nb; ++q) w.h_flags[q] = w.h_flags[q] == 1;
+        DPQ_CUDA(cudaMemcpyAsync(w.only, w.h_flags, nb, cudaMemcpyHostToDevice, h->stream));
+        DPQ_TRY(make_guards(1, true, w.only));
+      }
+    }
+  }
+  ev_rec(h, 4);
+  RefineArgs ra = make_refine_args(h, r);
+  ra.y = B.ynat;
+  ra.ystride = ma * d;
+  ra.row_ids = h->sorted_ids;
+  ra.id_base = 0;
+  DPQ_TRY(launch_refine<MODE_EMIT>(h, ra, nb));
+  ev_rec(h, 6);
+  h->counters[1] += nb;
+  if (h->timing) {
+    DPQ_CUDA(cudaEventSynchronize(h->ev[6]));
+    h->phase_ms[PH_FALLBACK] = ev_ms(h, 0, 1);  // probe ("index_us")
+    h->phase_ms[PH_TABLES] = P.nts ? ev_ms(h, 1, 2) : 0.f;
+    h->phase_ms[PH_GUARD] = P.nts ? ev_ms(h, 2, 3) : 0.f;
+    h->phase_ms[PH_SCAN] = P.nts ? ev_ms(h, 3, 4) : 0.f;
+    h->phase_ms[PH_THRESH] = 0.f;
+    h->phase_ms[PH_REFINE] = ev_ms(h, 4, 6);
+    h->phase_ms[PH_TOTAL] = ev_ms(h, 0, 6);
+  }
+  return DPQ_OK;
+}
+
+// host-buffer driver for ivf (queries + optional rotated residuals/cells)
+static int ivf_driver(Index* h, const float* y, int64_t nq, int r, int ma, int r2, bool derived,
+                      const float* res_rot, const int64_t* cells, double* dists, int64_t* ids, double* phase_us) {
+  int bsz = std::max(1, std::min(h->batch, std::max(1, (1 << 16) / std::max(ma, 1))));
+  int64_t q0 = 0;
+  while (q0 < nq) {
+    const int nb = (int)std::min<int64_t>(bsz, nq - q0);
+    DPQ_TRY(ensure_ws(h, nb, r, h->d, nb));
+    Workspace& w = h->ws;
+    DPQ_CUDA(cudaMemcpyAsync(w.y, y + q0 * h->d, (size_t)nb * h->d * 4, cudaMemcpyHostToDevice, h->stream));
+    const bool want_t = phase_us != nullptr;
+    const bool old_t = h->timing;
+    if (want_t) h->timing = true;
+    int rc = ivf_batch(h, nb, r, ma, r2, derived, res_rot ? res_rot + q0 * ma * h->d : nullptr,
+                       cells ? cells + q0 * ma : nullptr);
+    h->timing = old_t;
+    if (rc == 100) { bsz = std::max(1, nb / 2); continue; }
+    if (rc != DPQ_OK) return rc;
+    DPQ_CUDA(cudaMemcpyAsync(w.h_d, w.out_d, (size_t)nb * r * 8, cudaMemcpyDeviceToHost, h->stream));
+    DPQ_CUDA(cudaMemcpyAsync(w.h_i, w.out_i, (size_t)nb * r * 8, cudaMemcpyDeviceToHost, h->stream));
+    DPQ_CUDA(cudaStreamSynchronize(h->stream));
+    memcpy(dists + q0 * r, w.h_d, (size_t)nb * r * 8);
+    memcpy(ids + q0 * r, w.h_i, (size_t)nb * r * 8);
+    if (want_t) {
+      const double per = 1000.0 / nb;
+      for (int i = 0; i < nb; ++i) {
+        double* t = phase_us + (q0 + i) * 4;
+        t[0] = h->phase_ms[PH_FALLBACK] * per;  // probe
+        t[1] = h->phase_ms[PH_TABLES] * per;
+        t[2] = (h->phase_ms[PH_GUARD] + h->phase_ms[PH_SCAN]) * per;
+        t[3] = h->phase_ms[PH_REFINE] * per;
+      }
+    }
+    q0 += nb;
+  }
+  return DPQ_OK;
+}
+
+}  // namespace dpq
+
+extern "C" {
+
+int dpq_ivf_create(int device, int m, int k, int kbar, int dsub, const float* codebooks,
+                   const float* derived_codebooks, int n_cells, const float* centers, const int64_t* offsets,
+                   const void* sorted_codes, int code_bytes, const int64_t* sorted_ids, int64_t n,
+                   dpq_index_t** out) {
+  if (!out || !codebooks || !derived_codebooks || !centers || !offsets || n_cells < 1 || n < 0 ||
+      (n > 0 && (!sorted_codes || !sorted_ids))) {
+    set_error("null pointer or bad size");
+    return DPQ_ERR_ARG;
+  }
+  if (offsets[0] != 0 || offsets[n_cells] != n) { set_error("offsets must span [0, n]"); return DPQ_ERR_ARG; }
+  Index* h = new Index();
+  h->kind = KIND_IVF;
+  int rc = index_common_init(h, device, m, k, kbar, dsub, codebooks, derived_codebooks, code_bytes);
+  if (rc != DPQ_OK) { index_free(h); return rc; }
+  h->ivf_state = new IvfBuffers();
+  h->n = n;
+  h->n_cells = n_cells;
+  h->h_offsets.assign(offsets, offsets + n_cells + 1);
+  const size_t cbytes = (size_t)n * m * code_bytes;
+  if ((rc = dmalloc((uint8_t**)&h->codes, cbytes + 16)) != DPQ_OK ||
+      (rc = dmalloc(&h->centers, (size_t)n_cells * h->d)) != DPQ_OK ||
+      (rc = dmalloc(&h->offsets, (size_t)n_cells + 1)) != DPQ_OK ||
+      (rc = dmalloc(&h->sorted_ids, (size_t)std::max<int64_t>(n, 1))) != DPQ_OK) {
+    index_free(h);
+    return rc;
+  }
+  bool ok = cudaMemcpy(h->centers, centers, (size_t)n_cells * h->d * 4, cudaMemcpyHostToDevice) == cudaSuccess &&
+            cudaMemcpy(h->offsets, offsets, (size_t)(n_cells + 1) * 8, cudaMemcpyHostToDevice) == cudaSuccess;
+  if (n > 0)
+    ok = ok && cudaMemcpy(h->codes, sorted_codes, cbytes, cudaMemcpyHostToDevice) == cudaSuccess &&
+         cudaMemcpy(h->sorted_ids, sorted_ids, (size_t)n * 8, cudaMemcpyHostToDevice) == cudaSuccess;
+  if (!ok) { set_error("ivf upload failed"); index_free(h); return DPQ_ERR_CUDA; }
+  h->prefix = h->codes;
+  h->n_prefix = n;
+  if ((rc = make_plane(h)) != DPQ_OK) { index_free(h); return rc; }
+  if (cudaStreamSynchronize(h->stream) != cudaSuccess) { set_error("index build failed"); index_free(h); return DPQ_ERR_CUDA; }
+  *out = reinterpret_cast<dpq_index_t*>(h);
+  return DPQ_OK;
+}
+
+int dpq_ivf_probe(dpq_index_t* index, const float* y, int64_t nq, int ma, int64_t* cells) {
+  Index* h = reinterpret_cast<Index*>(index);
+  if (!h || h->kind != KIND_IVF) { set_error("not an ivf index"); return DPQ_ERR_STATE; }
+  if (ma < 1 || ma > h->n_cells) {
+    set_error("ma must be in [1, " + std::to_string(h->n_cells) + "], got " + std::to_string(ma));
+    return DPQ_ERR_ARG;
+  }
+  cudaSetDevice(h->device);
+  for (int64_t q0 = 0; q0 < nq; q0 += h->batch) {
+    const int nb = (int)std::min<int64_t>(h->batch, nq - q0);
+    DPQ_TRY(ensure_ws(h, nb, 1, h->d, nb));
+    DPQ_TRY(ivf_ensure(h, nb, ma, 0, 0, 0));
+    DPQ_CUDA(cudaMemcpyAsync(h->ws.y, y + q0 * h->d, (size_t)nb * h->d * 4, cudaMemcpyHostToDevice, h->stream));
+    DPQ_TRY(ivf_probe_dev(h, nb, ma));
+    DPQ_CUDA(cudaMemcpyAsync(cells + q0 * ma, ivf_bufs(h).cells, (size_t)nb * ma * 8, cudaMemcpyDeviceToHost,
+                             h->stream));
+    DPQ_CUDA(cudaStreamSynchronize(h->stream));
+  }
+  return DPQ_OK;
+}
+
+int dpq_ivf_search_derived(dpq_index_t* index, const float* y, int64_t nq, int r, int ma, int r2, int capped,
+                           const float* res_rot, const int64_t* cells, double* dists, int64_t* ids,
+                           double* phase_us) {
+  (void)capped;
+  Index* h = reinterpret_cast<Index*>(index);
+  if (!h || h->kind != KIND_IVF) { set_error("not an ivf index"); return DPQ_ERR_STATE; }
+  if (nq < 0 || r < 1 || r2 < 1 || r > r2) { set_error("need 1 <= r <= r2"); return DPQ_ERR_ARG; }
+  if (ma < 1 || ma > h->n_cells) { set_error("ma out of range"); return DPQ_ERR_ARG; }
+  cudaSetDevice(h->device);
+  return ivf_driver(h, y, nq, r, ma, r2, true, res_rot, cells, dists, ids, phase_us);
+}
+
+int dpq_ivf_search_conventional(dpq_index_t* index, const float* y, int64_t nq, int r, int ma,
+                                const float* res_rot, const int64_t* cells, double* dists, int64_t* ids,
+                                double* phase_us) {
+  Index* h = reinterpret_cast<Index*>(index);
+  if (!h || h->kind != KIND_IVF) { set_error("not an ivf index"); return DPQ_ERR_STATE; }
+  if (nq < 0 || r < 1) { set_error("need r >= 1"); return DPQ_ERR_ARG; }
+  if (ma < 1 || ma > h->n_cells) { set_error("ma out of range"); return DPQ_ERR_ARG; }
+  cudaSetDevice(h->device);
+  return ivf_driver(h, y, nq, r, ma, 1, false, res_rot, cells, dists, ids, phase_us);
+}
+
+int dpq_shard_begin(dpq_index_t*, const float*, int64_t, int, int32_t*) {
+  set_error("shard: not implemented yet");
+  return DPQ_ERR_STATE;
+}
+int dpq_shard_scan(dpq_index_t*, const int32_t*, int64_t, int64_t, int, int, int32_t*) {
+  set_error("shard: not implemented yet");
+  return DPQ_ERR_STATE;
+}
+int dpq_shard_finish(dpq_index_t*, const int32_t*, int, int, double*, int64_t*, uint8_t*) {
+  set_error("shard: not implemented yet");
+  return DPQ_ERR_STATE;
+}
+
+}  // extern "C"

@@ -238,7 +238,8 @@ template <int MPAD, int NT>
 __global__ void __launch_bounds__(NT, 1)
     k_scan_hist(const uint8_t* __restrict__ plane, int64_t stride, int64_t n_samp,
                 int64_t samp_per_cta, const uint8_t* __restrict__ lut,
-                const int* __restrict__ tile_list, uint32_t* __restrict__ hist) {
+                const int* __restrict__ tile_list, uint32_t* __restrict__ hist,
+                const int64_t* __restrict__ tile_row0, const int64_t* __restrict__ tile_nsamp) {
   using G = ScanGeom<MPAD>;
   extern __shared__ __align__(16) uint8_t smem[];
   uint8_t* slut = smem;
@@ -251,8 +252,11 @@ __global__ void __launch_bounds__(NT, 1)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int lic = lane % G::LPC, half = lane / G::LPC;
   const uint8_t* L = slut + lic * 4;
+  // rows sampled: row0 + s * stride for s in [0, nsamp) (per tile for ivf lists)
+  const int64_t row0 = tile_row0 ? tile_row0[tile] : 0;
+  const int64_t nsamp_t = tile_nsamp ? tile_nsamp[tile] : n_samp;
   const int64_t s0 = (int64_t)blockIdx.x * samp_per_cta;
-  const int64_t s1 = min(n_samp, s0 + samp_per_cta);
+  const int64_t s1 = min(nsamp_t, s0 + samp_per_cta);
   auto bump = [&](int qq, uint32_t score) {
     if (score < 255u) atomicAdd(sh + qq * 128 + (score >> 1), 1u << (16 * (score & 1)));
   };
@@ -260,7 +264,7 @@ __global__ void __launch_bounds__(NT, 1)
     const int64_t my = g + lane;
     uint32_t w0 = 0, w1 = 0;
     if (my < s1) {
-      const uint8_t* p = plane + my * stride * MPAD;
+      const uint8_t* p = plane + (row0 + my * stride) * MPAD;
       w0 = *reinterpret_cast<const uint32_t*>(p);
       if (MPAD == 8) w1 = *reinterpret_cast<const uint32_t*>(p + 4);
     }
@@ -311,6 +315,9 @@ struct EmitArgs {
   uint64_t* emit;
   uint32_t cap;
   unsigned* unit_counter;       // zeroed before launch (persistent scheduling)
+  const int* unit_tile;         // optional per-unit tile (ivf); else u / units_per_tile
+  const int64_t* unit_r0;       // optional per-unit row range (ivf)
+  const int64_t* unit_r1;
   uint32_t one;                 // = 1 (opaque to the compiler, see fma_add)
   int n_units;                  // tiles * units_per_tile
   int units_per_tile;
@@ -366,9 +373,19 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
     __syncthreads();
     const int u = s_unit;
     if (u >= a.n_units) break;
-    const int tix = u / a.units_per_tile;
-    const int64_t chunk_u = u % a.units_per_tile;
-    const int tile = a.tile_list ? a.tile_list[tix] : tix;
+    int tile;
+    int64_t r0, r1;
+    if (a.unit_tile) {
+      tile = a.unit_tile[u];
+      r0 = a.unit_r0[u];
+      r1 = a.unit_r1[u];
+    } else {
+      const int tix = u / a.units_per_tile;
+      const int64_t chunk_u = u % a.units_per_tile;
+      tile = a.tile_list ? a.tile_list[tix] : tix;
+      r0 = a.row_begin + chunk_u * a.rows_per_cta;
+      r1 = min(a.row_end, r0 + a.rows_per_cta);
+    }
     if (tile != cur_tile) {
       const uint4* src = reinterpret_cast<const uint4*>(a.lut + (int64_t)tile * G::LUT_BYTES);
       for (int i = threadIdx.x; i < G::LUT_BYTES / 16; i += NT) reinterpret_cast<uint4*>(slut)[i] = src[i];
@@ -380,8 +397,6 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
     const uint32_t ghi = (uint32_t)a.gword[q0 + 1] | ((uint32_t)a.gword[q0 + 3] << 16);
     // Logical range [r0, r1); loads start at the 512-B aligned row r0a and
     // rows outside the range are never emitted.
-    const int64_t r0 = a.row_begin + chunk_u * a.rows_per_cta;
-    const int64_t r1 = min(a.row_end, r0 + a.rows_per_cta);
     if (r0 >= r1) continue;
     const int64_t r0a = r0 & ~(int64_t)(G::CHUNK_ROWS - 1);
     const int64_t nchunks = (r1 - r0a + G::CHUNK_ROWS - 1) / G::CHUNK_ROWS;
@@ -504,12 +519,15 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
 // ============================================================================
 __global__ void k_guard(const uint32_t* __restrict__ hist, int nslot, int r2,
                         double lambda, int exact, const uint8_t* __restrict__ only,
-                        uint16_t* __restrict__ guard_b, uint16_t* __restrict__ gword) {
+                        uint16_t* __restrict__ guard_b, uint16_t* __restrict__ gword,
+                        const double* __restrict__ lambda_s) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= nslot) return;
   if (only && !only[s]) return;
   const uint32_t* h = hist + (int64_t)s * 256;
-  const double target = exact ? (double)r2 : lambda + 3.0 * sqrt(lambda) + 4.0;
+  const double lam = lambda_s ? lambda_s[s] : lambda;
+  const bool ex = exact || lam < 0.0;  // lambda < 0: this slot's histogram is exact
+  const double target = ex ? (double)r2 : lam + 3.0 * sqrt(lam) + 4.0;
   uint64_t cum = 0;
   int B = 254;
   for (int b = 0; b < 255; ++b) {
