@@ -130,20 +130,28 @@ int dpq_ivf_search_conventional(dpq_index_t* index, const float* y,
                                 double* phase_us);
 
 /* ----------------------------------------------------- sharded (flat) --
- * Split form of dpq_flat_search_derived for a database sharded across
- * GPUs.  The caller all-reduces between the phases:
- *   1. dpq_shard_begin: small tables (global qmax from the replicated
- *      prefix), sample histograms  -> hist_out (nq,256) i32 (sum these)
- *   2. dpq_shard_guard: guards from the summed sample histograms and the
- *      global row count; scan; local candidate histogram of scores <= guard
- *                                    -> hist_out (nq,256) i32 (sum these)
- *   3. dpq_shard_finish: global b* from the summed histogram; local refine
- *      and top-r (ids include id_base)  -> dists/ids (nq,r), plus
- *      need_exact (nq) u8 flags for queries whose guard proved too tight
- *      (the caller then re-runs step 2 with exact=1 for all shards).
- * All buffers are host memory.                                            */
+ * Split form of dpq_flat_search_derived for a database split into
+ * contiguous row shards, one per GPU.  Each shard's handle is
+ * created with its rows, id_base = its first global row and the replicated
+ * global prefix (the first min(N, max r2) rows, twopass.py:83-84), so every
+ * shard quantizes with the same global qmin/qmax.  The caller exchanges
+ * two small histograms between the phases (sum over shards, e.g. an NCCL
+ * all-reduce) and merges the per-shard top-r by (dist, id):
+ *   1. dpq_shard_begin: small tables + a score histogram of a row sample of
+ *      this shard (all rows when exact != 0)
+ *        -> sample_hist (nq,256) i32 and *n_sampled      [sum over shards]
+ *   2. dpq_shard_scan: guard per query from the summed sample histogram
+ *      (identical on every shard), scan, local histogram of the emitted
+ *      scores (all <= guard)  -> cand_hist (nq,256) i32  [sum over shards]
+ *   3. dpq_shard_finish: b* per query from the summed candidate histogram;
+ *      refine local candidates (score <= b*), local top-r with global ids
+ *        -> dists/ids (nq,r), need_exact (nq) u8: 1 where the guard proved
+ *      too tight; the caller then repeats 1-3 with exact = 1.
+ * The union of the shards' candidates is the unsharded candidate set, so the
+ * merged top-r equals the unsharded result bit for bit.  Host buffers.     */
 int dpq_shard_begin(dpq_index_t* index, const float* yr, int64_t nq, int r2,
-                    int32_t* sample_hist);
+                    int64_t n_global, int exact, int32_t* sample_hist,
+                    int64_t* n_sampled);
 int dpq_shard_scan(dpq_index_t* index, const int32_t* sample_hist_sum,
                    int64_t n_global, int64_t sample_global, int r2,
                    int exact, int32_t* cand_hist);

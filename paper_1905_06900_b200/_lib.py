@@ -43,7 +43,7 @@ SIGNATURES = {
                                        c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "dpq_ivf_search_conventional": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_int, c_void_p,
                                             c_void_p, c_void_p, c_void_p, c_void_p]),
-    "dpq_shard_begin": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_void_p]),
+    "dpq_shard_begin": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_int64, c_int, c_void_p, c_void_p]),
     "dpq_shard_scan": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int, c_int, c_void_p]),
     "dpq_shard_finish": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p]),
     "dpq_debug_quantize_tables": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_void_p, c_void_p,

@@ -711,17 +711,115 @@ int dpq_ivf_search_conventional(dpq_index_t* index, const float* y, int64_t nq, 
   return ivf_driver(h, y, nq, r, ma, 1, false, res_rot, cells, dists, ids, phase_us);
 }
 
-int dpq_shard_begin(dpq_index_t*, const float*, int64_t, int, int32_t*) {
-  set_error("shard: not implemented yet");
-  return DPQ_ERR_STATE;
+int dpq_shard_begin(dpq_index_t* index, const float* yr, int64_t nq, int r2, int64_t n_global, int exact,
+                    int32_t* sample_hist, int64_t* n_sampled) {
+  Index* h = reinterpret_cast<Index*>(index);
+  if (!h || h->kind != KIND_FLAT) { set_error("not a flat index"); return DPQ_ERR_STATE; }
+  if (nq < 1 || nq > (1 << 20) || r2 < 1 || !yr || !sample_hist || !n_sampled) {
+    set_error("bad shard_begin arguments"); return DPQ_ERR_ARG;
+  }
+  const int64_t npre = std::min<int64_t>(r2, n_global);
+  if (h->n_prefix < npre) {
+    set_error("shard prefix holds " + std::to_string(h->n_prefix) + " rows, need min(r2, N) = " +
+              std::to_string(npre));
+    return DPQ_ERR_ARG;
+  }
+  cudaSetDevice(h->device);
+  const int nb = (int)nq;
+  DPQ_TRY(ensure_ws(h, nb, 1, h->d, -1));
+  Workspace& w = h->ws;
+  const int qt = qt_of(h->mpad);
+  const int tiles = tiles_of(nb, h->mpad);
+  DPQ_CUDA(cudaMemcpyAsync(w.y, yr, (size_t)nb * h->d * 4, cudaMemcpyHostToDevice, h->stream));
+  DPQ_TRY(run_small_tables(h, nb, h->prefix, npre, nullptr, nullptr, nullptr, false, nullptr));
+  DPQ_CUDA(cudaMemsetAsync(w.gword, 0x7F, (size_t)tiles * qt * 2, h->stream));
+  DPQ_CUDA(cudaMemsetAsync(w.hist, 0, (size_t)tiles * qt * 256 * 4, h->stream));
+  const bool ex = exact || n_global <= h->exact_limit;
+  const int64_t ns = h->n == 0 ? 0 : (ex ? h->n : std::min<int64_t>(h->n, h->sample));
+  const int64_t stride = ns ? h->n / ns : 1;
+  if (ns > 0) DPQ_TRY(launch_hist(h, tiles, nullptr, stride, ns, h->plane));
+  DPQ_CUDA(cudaMemcpyAsync(sample_hist, w.hist, (size_t)nb * 256 * 4, cudaMemcpyDeviceToHost, h->stream));
+  DPQ_CUDA(cudaStreamSynchronize(h->stream));
+  *n_sampled = ns;
+  h->shard_nq = nb;
+  return DPQ_OK;
 }
-int dpq_shard_scan(dpq_index_t*, const int32_t*, int64_t, int64_t, int, int, int32_t*) {
-  set_error("shard: not implemented yet");
-  return DPQ_ERR_STATE;
+
+int dpq_shard_scan(dpq_index_t* index, const int32_t* sample_hist_sum, int64_t n_global, int64_t sample_global,
+                   int r2, int exact, int32_t* cand_hist) {
+  Index* h = reinterpret_cast<Index*>(index);
+  if (!h || h->kind != KIND_FLAT || h->shard_nq < 1) { set_error("shard_begin first"); return DPQ_ERR_STATE; }
+  cudaSetDevice(h->device);
+  const int nb = h->shard_nq;
+  Workspace& w = h->ws;
+  const int tiles = tiles_of(nb, h->mpad);
+  DPQ_CUDA(cudaMemcpyAsync(w.hist, sample_hist_sum, (size_t)nb * 256 * 4, cudaMemcpyHostToDevice, h->stream));
+  const bool ex = exact || n_global <= h->exact_limit;
+  const double lambda = (double)r2 * (double)sample_global / (double)std::max<int64_t>(n_global, 1);
+  k_guard<<<(nb + 127) / 128, 128, 0, h->stream>>>(w.hist, nb, r2, lambda, ex ? 1 : 0, nullptr, w.guard_b, w.gword,
+                                                    nullptr);
+  DPQ_LAUNCHED(h);
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    DPQ_CUDA(cudaMemsetAsync(w.emit_cnt, 0, (size_t)nb * 4, h->stream));
+    if (h->n > 0) {
+      EmitArgs ea;
+      ea.plane = h->plane; ea.row_begin = 0; ea.row_end = h->n; ea.rows_per_cta = 0;
+      ea.lut = w.lut; ea.gword = w.gword; ea.tile_list = nullptr;
+      ea.slot_query = nullptr; ea.slot_probe = nullptr;
+      ea.unit_tile = nullptr; ea.unit_r0 = nullptr; ea.unit_r1 = nullptr;
+      ea.emit_cnt = w.emit_cnt; ea.emit = w.emit; ea.cap = w.cap;
+      DPQ_TRY(launch_emit(h, ea, tiles, h->n));
+      h->counters[2] += (int64_t)nb * h->n;
+    }
+    k_threshold<256><<<nb, 256, 0, h->stream>>>(w.emit, w.emit_cnt, w.cap, w.guard_b, r2, nullptr, w.bstar,
+                                                w.ncand, w.flags, w.hist_i, h->d_nemit);
+    DPQ_LAUNCHED(h);
+    DPQ_CUDA(cudaMemcpyAsync(w.h_flags, w.flags, nb, cudaMemcpyDeviceToHost, h->stream));
+    DPQ_CUDA(cudaMemcpyAsync(w.h_cnt, w.emit_cnt, (size_t)nb * 4, cudaMemcpyDeviceToHost, h->stream));
+    DPQ_CUDA(cudaStreamSynchronize(h->stream));
+    uint32_t need = 0;
+    for (int q = 0; q < nb; ++q)
+      if (w.h_flags[q] == 2) need = std::max(need, w.h_cnt[q]);
+    if (!need) {
+      DPQ_CUDA(cudaMemcpy(cand_hist, w.hist_i, (size_t)nb * 256 * 4, cudaMemcpyDeviceToHost));
+      return DPQ_OK;
+    }
+    DPQ_TRY(grow_emit(h, need));
+  }
+  set_error("shard scan: emit buffer did not converge");
+  return DPQ_ERR_NOMEM;
 }
-int dpq_shard_finish(dpq_index_t*, const int32_t*, int, int, double*, int64_t*, uint8_t*) {
-  set_error("shard: not implemented yet");
-  return DPQ_ERR_STATE;
+
+int dpq_shard_finish(dpq_index_t* index, const int32_t* cand_hist_sum, int r, int r2, double* dists, int64_t* ids,
+                     uint8_t* need_exact) {
+  Index* h = reinterpret_cast<Index*>(index);
+  if (!h || h->kind != KIND_FLAT || h->shard_nq < 1) { set_error("shard_begin first"); return DPQ_ERR_STATE; }
+  if (r < 1 || r > r2) { set_error("need 1 <= r <= r2"); return DPQ_ERR_ARG; }
+  cudaSetDevice(h->device);
+  const int nb = h->shard_nq;
+  DPQ_TRY(ensure_ws(h, nb, r, h->d, -1));
+  Workspace& w = h->ws;
+  DPQ_CUDA(cudaMemcpyAsync(w.hist_i, cand_hist_sum, (size_t)nb * 256 * 4, cudaMemcpyHostToDevice, h->stream));
+  k_bstar_from_hist<<<(nb + 127) / 128, 128, 0, h->stream>>>(w.hist_i, w.guard_b, nb, r2, w.bstar, w.ncand,
+                                                              w.flags);
+  DPQ_LAUNCHED(h);
+  RefineArgs ra = make_refine_args(h, r);
+  if (group_tables_fit(h, nb)) {
+    DPQ_TRY(run_group_tables(h, nb, h->d));
+    ra.tables = w.tables;
+    DPQ_TRY(launch_refine<MODE_EMIT_TABLE>(h, ra, nb));
+  } else {
+    DPQ_TRY(launch_refine<MODE_EMIT>(h, ra, nb));
+  }
+  DPQ_CUDA(cudaMemcpyAsync(w.h_d, w.out_d, (size_t)nb * r * 8, cudaMemcpyDeviceToHost, h->stream));
+  DPQ_CUDA(cudaMemcpyAsync(w.h_i, w.out_i, (size_t)nb * r * 8, cudaMemcpyDeviceToHost, h->stream));
+  DPQ_CUDA(cudaMemcpyAsync(need_exact, w.flags, nb, cudaMemcpyDeviceToHost, h->stream));
+  DPQ_CUDA(cudaStreamSynchronize(h->stream));
+  memcpy(dists, w.h_d, (size_t)nb * r * 8);
+  memcpy(ids, w.h_i, (size_t)nb * r * 8);
+  for (int q = 0; q < nb; ++q) need_exact[q] = need_exact[q] == 1;
+  h->counters[1] += nb;
+  return DPQ_OK;
 }
 
 }  // extern "C"
