@@ -297,7 +297,7 @@ static int launch_refine_buf(Index* h, const RefineArgs& ra, int nq) {
 
 template <int MODE>
 static int launch_refine(Index* h, const RefineArgs& ra, int nq) {
-  const int need = ra.r + kTopThreads;
+  const int need = ra.r + kTopThreads;  // one candidate per thread per round
   if (need <= 1024) return launch_refine_buf<1024, MODE>(h, ra, nq);
   if (need <= 2048) return launch_refine_buf<2048, MODE>(h, ra, nq);
   if (need <= 4096) return launch_refine_buf<4096, MODE>(h, ra, nq);
@@ -331,6 +331,13 @@ int run_small_tables(Index* h, int nslot, const void* prefix, int64_t npre,
     attr = true;
   }
   k_small_tables<<<nslot, 256, smem, h->stream>>>(ta);
+  DPQ_LAUNCHED(h);
+  const int ntiles = tiles_of(nslot, h->mpad);
+  const int64_t threads = (int64_t)ntiles * h->mpad * 256;
+  if (h->mpad == 4)
+    k_build_lut<4><<<(unsigned)((threads + 255) / 256), 256, 0, h->stream>>>(w.q8, nslot, h->m, h->kbar, w.lut, ntiles);
+  else
+    k_build_lut<8><<<(unsigned)((threads + 255) / 256), 256, 0, h->stream>>>(w.q8, nslot, h->m, h->kbar, w.lut, ntiles);
   DPQ_LAUNCHED(h);
   return DPQ_OK;
 }

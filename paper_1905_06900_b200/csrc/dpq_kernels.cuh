@@ -102,6 +102,7 @@ struct TablesArgs {
 };
 
 __global__ void __launch_bounds__(256) k_small_tables(TablesArgs a) {
+  // (the scan-layout LUT is built from q8_out by k_build_lut)
   extern __shared__ __align__(16) float sm_f[];
   __shared__ float red_f[8];
   __shared__ double red_d[8];
@@ -163,14 +164,39 @@ __global__ void __launch_bounds__(256) k_small_tables(TablesArgs a) {
     a.qmax_out[s] = degenerate ? qmin : qmax;
   }
   __syncthreads();
-  // scan-layout LUT (see lut_index)
-  const int tile = s / a.qt, qq = s % a.qt;
-  const int spr = 256 / a.qt;
-  uint8_t* L = a.lut + (int64_t)tile * a.mpad * 256 * a.qt;
-  for (int e = tid; e < a.mpad * 256; e += 256) {
-    const int j = e >> 8, i = e & 255;
-    uint8_t v = (j < a.m && i < a.kbar) ? q8[j * a.kbar + i] : (uint8_t)0;
-    L[lut_index(j, i, qq, spr, a.qt)] = v;
+}
+
+// Scan-layout LUT tiles from the u8 tables q8 [nslot][m][kbar] (see
+// lut_index): one thread per (tile, subspace, table row) writes the row's
+// LPC lane words (QT/4 queries x 4 bytes, contiguous) with 16-B stores;
+// the q8 reads are coalesced across consecutive rows.
+template <int MPAD>
+__global__ void __launch_bounds__(256) k_build_lut(const uint8_t* __restrict__ q8, int nslot, int m, int kbar,
+                                                   uint8_t* __restrict__ lut, int ntiles) {
+  using G = ScanGeom<MPAD>;
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (int64_t)ntiles * MPAD * 256) return;
+  const int i = (int)(gid & 255);
+  const int j = (int)((gid >> 8) % MPAD);
+  const int t = (int)(gid / (MPAD * 256));
+  uint4* dst = reinterpret_cast<uint4*>(lut + (int64_t)t * G::LUT_BYTES +
+                                        (int64_t)((j / G::SPR) * 256 + i) * 256 + (j % G::SPR) * G::ROWB);
+  const bool live = j < m && i < kbar;
+#pragma unroll
+  for (int l4 = 0; l4 < G::LPC / 4; ++l4) {
+    uint32_t w[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      uint32_t v = 0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int q = t * G::QT + 4 * (4 * l4 + u) + b;
+        const uint32_t e = (live && q < nslot) ? q8[((int64_t)q * m + j) * kbar + i] : 0u;
+        v |= e << (8 * b);
+      }
+      w[u] = v;
+    }
+    dst[l4] = make_uint4(w[0], w[1], w[2], w[3]);
   }
 }
 
@@ -779,48 +805,65 @@ __global__ void __launch_bounds__(NT) k_refine_topk(RefineArgs a) {
     ntot = a.n_rows;
   }
   unsigned long long my_ref = 0;
-  for (int64_t base = 0; base < ntot; base += NT) {
-    const int64_t idx = base + threadIdx.x;
-    bool keep = false;
-    uint64_t key = 0;
-    int64_t id = 0;
-    if (idx < ntot) {
-      int64_t row;
-      uint32_t probe = 0;
-      bool cand = true;
-      if (MODE != MODE_ALL) {
-        const uint64_t v = e[idx];
-        cand = (int)emit_score(v) <= bs;
-        row = emit_row(v);
-        probe = emit_probe(v);
-      } else {
-        row = idx;
-      }
-      if (cand) {
-        ++my_ref;
-        double dist = 0.0;
-        const float* yq = ys + (int64_t)probe * d;
-        for (int j = 0; j < a.m; ++j) {
-          const uint32_t c = code_at(a.codes, a.code_bytes, row * a.m + j);
-          float t;
-          if (MODE != MODE_EMIT) t = a.tables[table_index(q, j, c, a.m, a.kbar, a.bbar, a.k / a.kbar)];
-          else t = entry_dist<DSUB>(a.cb + ((int64_t)j * a.k + c) * a.dsub, yq + j * a.dsub, a.dsub);
-          dist = __dadd_rn(dist, (double)t);
-        }
-        key = (uint64_t)__double_as_longlong(dist);
-        id = a.row_ids ? a.row_ids[row] : a.id_base + row;
-        keep = pair_less(key, id, thr_k, thr_i);
+  // candidate -> (key, id); false when it is not a candidate (score > b*)
+  auto eval = [&](int64_t idx, uint64_t& key, int64_t& id) -> bool {
+    int64_t row;
+    uint32_t probe = 0;
+    if (MODE != MODE_ALL) {
+      const uint64_t v = e[idx];
+      if ((int)emit_score(v) > bs) return false;
+      row = emit_row(v);
+      probe = emit_probe(v);
+    } else {
+      row = idx;
+    }
+    ++my_ref;
+    double dist = 0.0;
+    const float* yq = ys + (int64_t)probe * d;
+    if (MODE == MODE_EMIT_TABLE && a.code_bytes == 2 && a.m == 4) {
+      // one 8-byte code load, four independent table gathers
+      const uint2 v = *reinterpret_cast<const uint2*>((const uint16_t*)a.codes + row * 4);
+      const int gs = a.k / a.kbar;
+      const float t0 = __ldg(a.tables + table_index(q, 0, v.x & 0xFFFFu, 4, a.kbar, a.bbar, gs));
+      const float t1 = __ldg(a.tables + table_index(q, 1, v.x >> 16, 4, a.kbar, a.bbar, gs));
+      const float t2 = __ldg(a.tables + table_index(q, 2, v.y & 0xFFFFu, 4, a.kbar, a.bbar, gs));
+      const float t3 = __ldg(a.tables + table_index(q, 3, v.y >> 16, 4, a.kbar, a.bbar, gs));
+      dist = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(dist, (double)t0), (double)t1), (double)t2), (double)t3);
+    } else {
+      for (int j = 0; j < a.m; ++j) {
+        const uint32_t c = code_at(a.codes, a.code_bytes, row * a.m + j);
+        float t;
+        if (MODE != MODE_EMIT) t = __ldg(a.tables + table_index(q, j, c, a.m, a.kbar, a.bbar, a.k / a.kbar));
+        else t = entry_dist<DSUB>(a.cb + ((int64_t)j * a.k + c) * a.dsub, yq + j * a.dsub, a.dsub);
+        dist = __dadd_rn(dist, (double)t);
       }
     }
-    if (keep) {
-      const int p = atomicAdd(&fill, 1);
-      keys[p] = key;
-      ids[p] = id;
+    key = (uint64_t)__double_as_longlong(dist);
+    id = a.row_ids ? a.row_ids[row] : a.id_base + row;
+    return true;
+  };
+  constexpr int U = 1;  // candidates per thread per round (U > 1 measured slower: bigger buffer, lower occupancy)
+  for (int64_t base = 0; base < ntot; base += (int64_t)U * NT) {
+    uint64_t key[U];
+    int64_t id[U];
+    bool keep[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t idx = base + (int64_t)u * NT + threadIdx.x;
+      keep[u] = idx < ntot && eval(idx, key[u], id[u]) && pair_less(key[u], id[u], thr_k, thr_i);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (keep[u]) {
+        const int p = atomicAdd(&fill, 1);
+        keys[p] = key[u];
+        ids[p] = id[u];
+      }
     }
     __syncthreads();
     const int f = fill;
     __syncthreads();
-    if (f > BUF - NT) {
+    if (f > BUF - U * NT) {
       for (int i = f + threadIdx.x; i < BUF; i += NT) { keys[i] = ~0ull; ids[i] = INT64_MAX; }
       __syncthreads();
       sort_pairs<BUF, NT>(keys, ids);
