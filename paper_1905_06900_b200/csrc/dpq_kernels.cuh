@@ -367,9 +367,11 @@ constexpr uint32_t kLutShared = 0x10000;  // LUT at shared address 64 KB
 // per-warp hit counters above it.
 template <int MPAD, int NT>
 __host__ __device__ constexpr int emit_low_bytes() { return (NT / 32) * (32 * 16 + kWarpBuf * 8); }
+constexpr int kLaneQ = 8;  // lane-private hit records per chunk (u16 each)
 template <int MPAD, int NT>
 __host__ __device__ constexpr int emit_smem_bytes() {
-  return (int)kLutShared + ScanGeom<MPAD>::LUT_BYTES + (NT / 32) * ScanGeom<MPAD>::QT * 4;
+  return (int)kLutShared + ScanGeom<MPAD>::LUT_BYTES + (NT / 32) * ScanGeom<MPAD>::QT * 4 +
+         (NT / 32) * kLaneQ * 32 * 2;
 }
 
 template <int MPAD, int NT>
@@ -390,6 +392,7 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
   uint4* wst = stage + warp * 32;
   uint64_t* hbuf = hbuf_all + warp * kWarpBuf;
   uint32_t* hcnt = hcnt_all + warp * G::QT;
+  uint16_t* lq = reinterpret_cast<uint16_t*>(hcnt_all + NW * G::QT) + warp * kLaneQ * 32 + lane;
   const uint32_t lt = (1u << lane) - 1u;
   const uint32_t one = a.one, mone = 0u - a.one;  // opaque 1 / -1 (see fma_add)
   int cur_tile = -1;
@@ -485,6 +488,23 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
       const uint32_t xl = glo - sm.lo, xh = ghi - sm.hi;
       return ((xl >> 15) & 1u) | ((xh >> 14) & 2u) | ((xl >> 29) & 4u) | ((xh >> 28) & 8u);
     };
+    // hit bits of one code from (guard - sum): qs0 lo.15, qs1 hi.15, qs2 lo.31, qs3 hi.31
+    auto bits_x = [](uint32_t xl, uint32_t xh) -> uint32_t {
+      return ((xl >> 15) & 1u) | ((xh >> 14) & 2u) | ((xl >> 29) & 4u) | ((xh >> 28) & 8u);
+    };
+    // The (rare) hit path of the inner loop only appends a 16-bit record
+    // (i, code, query) to a lane-private shared queue; the records are
+    // turned into emit entries once per 128-code chunk (drain below).
+    int lcnt = 0;
+    auto record = [&](uint32_t xl, uint32_t xh, int i, int k) {
+      uint32_t hm = bits_x(xl, xh);
+      do {
+        const int qs = __ffs(hm) - 1;
+        hm &= hm - 1u;
+        if (lcnt < kLaneQ) lq[lcnt * 32] = (uint16_t)((i << 4) | (k << 2) | qs);
+        ++lcnt;
+      } while (hm);
+    };
     uint4 nxt = ldg_stream(chunk_ptr(c));
     for (; c < nchunks; c += NW) {
       __syncwarp();
@@ -503,33 +523,65 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
         if (MPAD == 4) {
           const Sum4 s0 = lut_sum_fast<MPAD>(lbase, v.x, 0, one), s1 = lut_sum_fast<MPAD>(lbase, v.y, 0, one);
           const Sum4 s2 = lut_sum_fast<MPAD>(lbase, v.z, 0, one), s3 = lut_sum_fast<MPAD>(lbase, v.w, 0, one);
-          const uint32_t any = (fma_add(s0.lo, mone, glo) | fma_add(s0.hi, mone, ghi) | fma_add(s1.lo, mone, glo) |
-                                fma_add(s1.hi, mone, ghi) | fma_add(s2.lo, mone, glo) | fma_add(s2.hi, mone, ghi) |
-                                fma_add(s3.lo, mone, glo) | fma_add(s3.hi, mone, ghi)) & 0x80008000u;
-          if (__any_sync(0xffffffffu, any != 0u)) {
-            uint32_t hm = code_bits(s0) | (code_bits(s1) << 4) | (code_bits(s2) << 8) | (code_bits(s3) << 12);
-            if (edge) {
-              uint32_t ok = 0;
-              for (int k = 0; k < 4; ++k) {
-                const uint32_t r = 4 * i + k;
-                if (r >= lo && r < hi) ok |= 0xFu << (4 * k);
-              }
-              hm &= ok;
-            }
-            stage_hits(hm, s0, s1, s2, s3, rboff + 4 * i);
-          }
+          const uint32_t xl0 = fma_add(s0.lo, mone, glo), xh0 = fma_add(s0.hi, mone, ghi);
+          const uint32_t xl1 = fma_add(s1.lo, mone, glo), xh1 = fma_add(s1.hi, mone, ghi);
+          const uint32_t xl2 = fma_add(s2.lo, mone, glo), xh2 = fma_add(s2.hi, mone, ghi);
+          const uint32_t xl3 = fma_add(s3.lo, mone, glo), xh3 = fma_add(s3.hi, mone, ghi);
+          if ((xl0 | xh0) & 0x80008000u) record(xl0, xh0, i, 0);
+          if ((xl1 | xh1) & 0x80008000u) record(xl1, xh1, i, 1);
+          if ((xl2 | xh2) & 0x80008000u) record(xl2, xh2, i, 2);
+          if ((xl3 | xh3) & 0x80008000u) record(xl3, xh3, i, 3);
         } else {
           const uint32_t w0 = half ? v.z : v.x;
           const uint32_t w1 = half ? v.w : v.y;
           const Sum4 s0 = lut_sum_fast<MPAD>(lbase, w0, w1, one);
-          const uint32_t any = ((glo - s0.lo) | (ghi - s0.hi)) & 0x80008000u;
-          if (__any_sync(0xffffffffu, any != 0u)) {
-            uint32_t hm = code_bits(s0);
-            const uint32_t r = 2 * i + half;
-            if (edge && !(r >= lo && r < hi)) hm = 0u;
-            stage_hits(hm, s0, s0, s0, s0, rboff + r);
+          const uint32_t xl0 = fma_add(s0.lo, mone, glo), xh0 = fma_add(s0.hi, mone, ghi);
+          if ((xl0 | xh0) & 0x80008000u) record(xl0, xh0, i, 0);
+        }
+      }
+      // drain: records -> emit entries (scores recomputed from the staged codes)
+      if (__any_sync(0xffffffffu, lcnt > 0)) {
+        if (__any_sync(0xffffffffu, lcnt > kLaneQ)) {
+          // a lane overflowed its queue (degenerate data): redo the whole
+          // chunk with warp-wide staging (exact, just slower)
+          for (int i = 0; i < 32; ++i) {
+            const uint4 v = wst[i];
+            for (int k = 0; k < (MPAD == 4 ? 4 : 1); ++k) {
+              uint32_t w0, w1 = 0;
+              if (MPAD == 4) w0 = k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
+              else { w0 = half ? v.z : v.x; w1 = half ? v.w : v.y; }
+              const uint32_t r = MPAD == 4 ? 4 * i + k : 2 * i + half;
+              const Sum4 sm = lut_sum_fast<MPAD>(lbase, w0, w1, one);
+              uint32_t hm = bits_x(glo - sm.lo, ghi - sm.hi);
+              if (edge && !(r >= lo && r < hi)) hm = 0u;
+              stage_hits(hm, sm, sm, sm, sm, rboff + r);
+            }
+          }
+        } else {
+          const int maxc = __reduce_max_sync(0xffffffffu, (unsigned)lcnt);
+          for (int e = 0; e < maxc; ++e) {
+            bool has = e < lcnt;
+            uint32_t sc = 0, roff = 0, slot = 0;
+            if (has) {
+              const uint32_t rec = lq[e * 32];
+              const int i = (int)(rec >> 4), k = (int)((rec >> 2) & 3), qs = (int)(rec & 3);
+              const uint4 v = wst[i];
+              uint32_t w0, w1 = 0;
+              if (MPAD == 4) w0 = k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
+              else { w0 = half ? v.z : v.x; w1 = half ? v.w : v.y; }
+              const uint32_t r = MPAD == 4 ? 4 * i + k : 2 * i + half;
+              has = !edge || (r >= lo && r < hi);
+              sc = sum_of(lut_sum_fast<MPAD>(lbase, w0, w1, one), qs);
+              roff = rboff + r;
+              slot = 4 * lic + qs;
+            }
+            const uint32_t bal = __ballot_sync(0xffffffffu, has);
+            if (wc + 32 > kWarpBuf) flush();
+            if (has) hbuf[wc + __popc(bal & lt)] = (uint64_t)roff | ((uint64_t)slot << 32) | ((uint64_t)sc << 40);
+            wc += __popc(bal);
           }
         }
+        lcnt = 0;
       }
     }
     if (wc > 0) flush();
