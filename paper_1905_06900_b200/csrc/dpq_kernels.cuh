@@ -244,8 +244,13 @@ __device__ __forceinline__ Sum4 lut_sum_fast(uint32_t base, uint32_t w0, uint32_
     uint32_t v;
     if (j / G::SPR == 0) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
     else asm volatile("ld.shared.u32 %0, [%1+65536];" : "=r"(v) : "r"(a));
-    s.lo = fma_add(v & 0x00FF00FFu, one, s.lo);
-    s.hi = fma_add(__byte_perm(v, 0u, 0x4341u), one, s.hi);
+    if (j == 0) {
+      s.lo = v & 0x00FF00FFu;
+      s.hi = __byte_perm(v, 0u, 0x4341u);
+    } else {
+      s.lo = fma_add(v & 0x00FF00FFu, one, s.lo);
+      s.hi = fma_add(__byte_perm(v, 0u, 0x4341u), one, s.hi);
+    }
   }
   return s;
 }
