@@ -115,6 +115,7 @@ int ensure_ws(Index* h, int nslot, int r, int ystride, int nq) {
     DPQ_TRY(dmalloc(&w.flags, (size_t)qn));
     DPQ_TRY(dmalloc(&w.only, (size_t)std::max(tiles * qt, qn)));
     DPQ_TRY(dmalloc(&w.tile_list, (size_t)tiles));
+    DPQ_TRY(dmalloc(&w.tile_fast, (size_t)tiles));
     if (!w.counter) DPQ_TRY(dmalloc(&w.counter, 4));
     DPQ_TRY(dmalloc(&w.slot_query, (size_t)tiles * qt));
     DPQ_TRY(dmalloc(&w.slot_probe, (size_t)tiles * qt));
@@ -235,6 +236,7 @@ static int launch_emit_t(Index* h, EmitArgs ea, int ntiles, int64_t rows) {
   const int sms = num_sms(h);
   ea.unit_counter = h->ws.counter;
   ea.one = 1u;
+  ea.tile_fast = h->ws.tile_fast;
   if (ea.unit_tile) {  // caller-built units (ivf lists)
     if (ea.n_units < 1) return DPQ_OK;
     DPQ_CUDA(cudaMemsetAsync(h->ws.counter, 0, sizeof(unsigned), h->stream));
@@ -309,6 +311,7 @@ static int launch_refine(Index* h, const RefineArgs& ra, int nq) {
 // ---------------------------------------------------------------------------
 // K1 for nslot slots whose queries are already in ws.y.
 // ---------------------------------------------------------------------------
+int build_lut(Index* h, int nslot, const uint16_t* gword);
 int run_small_tables(Index* h, int nslot, const void* prefix, int64_t npre,
                      const int64_t* pre_off, const int64_t* pre_len, const double* bounds_in,
                      bool export_debug, const float* y_slots) {
@@ -332,12 +335,22 @@ int run_small_tables(Index* h, int nslot, const void* prefix, int64_t npre,
   }
   k_small_tables<<<nslot, 256, smem, h->stream>>>(ta);
   DPQ_LAUNCHED(h);
+  return build_lut(h, nslot, nullptr);
+}
+
+// Scan-layout LUT tiles from ws.q8; with gword (guards known) tiles whose
+// guards are all <= 126 are clamped to 7-bit entries and flagged fast.
+int build_lut(Index* h, int nslot, const uint16_t* gword) {
+  Workspace& w = h->ws;
   const int ntiles = tiles_of(nslot, h->mpad);
   const int64_t threads = (int64_t)ntiles * h->mpad * 256;
+  int* tf = w.tile_fast;  // reset to 0 when gword is null (unclamped LUT)
   if (h->mpad == 4)
-    k_build_lut<4><<<(unsigned)((threads + 255) / 256), 256, 0, h->stream>>>(w.q8, nslot, h->m, h->kbar, w.lut, ntiles);
+    k_build_lut<4><<<(unsigned)((threads + 255) / 256), 256, 0, h->stream>>>(w.q8, nslot, h->m, h->kbar, w.lut,
+                                                                             ntiles, gword, tf);
   else
-    k_build_lut<8><<<(unsigned)((threads + 255) / 256), 256, 0, h->stream>>>(w.q8, nslot, h->m, h->kbar, w.lut, ntiles);
+    k_build_lut<8><<<(unsigned)((threads + 255) / 256), 256, 0, h->stream>>>(w.q8, nslot, h->m, h->kbar, w.lut,
+                                                                             ntiles, gword, tf);
   DPQ_LAUNCHED(h);
   return DPQ_OK;
 }
@@ -363,6 +376,7 @@ static int flat_first_pass(Index* h, int nb, int r2) {
   k_guard<<<(nb + 127) / 128, 128, 0, h->stream>>>(w.hist, nb, r2, lambda, exact ? 1 : 0, nullptr,
                                                     w.guard_b, w.gword, nullptr);
   DPQ_LAUNCHED(h);
+  DPQ_TRY(build_lut(h, nb, w.gword));  // 7-bit tiles where every guard <= 126
   ev_rec(h, 2);
   bool first = true;
   for (int attempt = 0; attempt < 8; ++attempt) {
@@ -412,10 +426,12 @@ static int flat_first_pass(Index* h, int nb, int r2) {
       DPQ_CUDA(cudaMemcpyAsync(w.tile_list, tl.data(), tl.size() * sizeof(int), cudaMemcpyHostToDevice,
                                h->stream));
       DPQ_CUDA(cudaMemsetAsync(w.hist, 0, (size_t)tiles * qt * 256 * 4, h->stream));
+      DPQ_TRY(build_lut(h, nb, nullptr));  // exact histogram needs unclamped entries
       DPQ_TRY(launch_hist(h, (int)tl.size(), w.tile_list, 1, n, h->plane));
       k_guard<<<(nb + 127) / 128, 128, 0, h->stream>>>(w.hist, nb, r2, 0.0, 1, w.only, w.guard_b, w.gword,
                                                         nullptr);
       DPQ_LAUNCHED(h);
+      DPQ_TRY(build_lut(h, nb, w.gword));
       DPQ_CUDA(cudaStreamSynchronize(h->stream));
     }
   }
@@ -660,7 +676,7 @@ void index_free(Index* h) {
                  h->offsets, h->sorted_ids, h->d_nref, h->d_nemit, h->d_nent, w.y, w.small, w.q8, w.qmin, w.qmax, w.bounds,
                  w.lut, w.hist, w.hist_i, w.guard_b, w.gword, w.emit_cnt, w.emit, w.bstar, w.ncand,
                  w.flags, w.only, w.tile_list, w.out_d, w.out_i, w.tables, w.slot_query, w.slot_probe,
-                 w.slot_pre_off, w.slot_pre_len, w.counter};
+                 w.slot_pre_off, w.slot_pre_len, w.counter, w.tile_fast};
   for (void* p : dev)
     if (p) cudaFree(p);
   void* host[] = {w.h_y, w.h_d, w.h_i, w.h_flags, w.h_cnt};

@@ -41,6 +41,7 @@ struct Workspace {
   uint8_t* flags = nullptr;
   uint8_t* only = nullptr;
   int* tile_list = nullptr;
+  int* tile_fast = nullptr;     // per tile: LUT clamped to 7-bit entries
   unsigned* counter = nullptr;  // persistent-scan unit counter
   double* out_d = nullptr;
   int64_t* out_i = nullptr;

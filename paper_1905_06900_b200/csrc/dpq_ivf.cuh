@@ -511,6 +511,7 @@ static int ivf_batch(Index* h, int nb, int r, int ma, int r2, bool derived, cons
         mx = std::max(mx, ns[t]);
       }
       DPQ_TRY(h2d(B.tile_nsamp, ns, h->stream));
+      DPQ_TRY(build_lut(h, P.nts, nullptr));  // histograms need unclamped entries
       DPQ_TRY(launch_hist(h, P.ntiles, nullptr, stride, mx, h->plane, B.tile_row0, B.tile_nsamp));
       k_slot_hist_to_query<<<(unsigned)(((int64_t)P.nts * 256 + 255) / 256), 256, 0, h->stream>>>(
           w.hist, w.slot_query, P.nts, B.hist_q);
@@ -520,6 +521,7 @@ static int ivf_batch(Index* h, int nb, int r, int ma, int r2, bool derived, cons
       DPQ_LAUNCHED(h);
       k_expand_gword<<<(P.nts + 255) / 256, 256, 0, h->stream>>>(B.gword_q, w.slot_query, P.nts, w.gword);
       DPQ_LAUNCHED(h);
+      DPQ_TRY(build_lut(h, P.nts, w.gword));
       return DPQ_OK;
     };
     DPQ_TRY(make_guards(P.stride, P.stride == 1, nullptr));
@@ -759,6 +761,7 @@ int dpq_shard_scan(dpq_index_t* index, const int32_t* sample_hist_sum, int64_t n
   k_guard<<<(nb + 127) / 128, 128, 0, h->stream>>>(w.hist, nb, r2, lambda, ex ? 1 : 0, nullptr, w.guard_b, w.gword,
                                                     nullptr);
   DPQ_LAUNCHED(h);
+  DPQ_TRY(build_lut(h, nb, w.gword));
   for (int attempt = 0; attempt < 4; ++attempt) {
     DPQ_CUDA(cudaMemsetAsync(w.emit_cnt, 0, (size_t)nb * 4, h->stream));
     if (h->n > 0) {

@@ -26,6 +26,8 @@
 //                             entries of queries 2l, 2l+1 for one table row
 //                             with one conflict-free 32-bit LDS.
 #pragma once
+#include <type_traits>
+
 #include "dpq_device.cuh"
 
 namespace dpq {
@@ -170,15 +172,33 @@ __global__ void __launch_bounds__(256) k_small_tables(TablesArgs a) {
 // lut_index): one thread per (tile, subspace, table row) writes the row's
 // LPC lane words (QT/4 queries x 4 bytes, contiguous) with 16-B stores;
 // the q8 reads are coalesced across consecutive rows.
+//
+// With gword given (after the guards are known) a tile whose every query has
+// guard B <= 126 is written with entries clamped to 127 and flagged "fast":
+// an entry >= 127 > B rules a hit out either way, and every hit has all its
+// entries < 127, so hits and their scores are unchanged, while two 7-bit
+// words add without carries (k_scan_emit's fast inner loop).
+constexpr uint32_t kClampMaxGuard = 126;
+
 template <int MPAD>
 __global__ void __launch_bounds__(256) k_build_lut(const uint8_t* __restrict__ q8, int nslot, int m, int kbar,
-                                                   uint8_t* __restrict__ lut, int ntiles) {
+                                                   uint8_t* __restrict__ lut, int ntiles,
+                                                   const uint16_t* __restrict__ gword, int* __restrict__ tile_fast) {
   using G = ScanGeom<MPAD>;
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= (int64_t)ntiles * MPAD * 256) return;
   const int i = (int)(gid & 255);
   const int j = (int)((gid >> 8) % MPAD);
   const int t = (int)(gid / (MPAD * 256));
+  bool clamp = false;
+  if (gword) {
+    clamp = true;
+    for (int qq = 0; qq < G::QT; ++qq) {
+      const uint32_t gw = gword[t * G::QT + qq];
+      if (gw >= 0x8000u && gw - 0x8000u > kClampMaxGuard) { clamp = false; break; }
+    }
+  }
+  if (tile_fast && i == 0 && j == 0) tile_fast[t] = clamp ? 1 : 0;
   uint4* dst = reinterpret_cast<uint4*>(lut + (int64_t)t * G::LUT_BYTES +
                                         (int64_t)((j / G::SPR) * 256 + i) * 256 + (j % G::SPR) * G::ROWB);
   const bool live = j < m && i < kbar;
@@ -191,7 +211,8 @@ __global__ void __launch_bounds__(256) k_build_lut(const uint8_t* __restrict__ q
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
         const int q = t * G::QT + 4 * (4 * l4 + u) + b;
-        const uint32_t e = (live && q < nslot) ? q8[((int64_t)q * m + j) * kbar + i] : 0u;
+        uint32_t e = (live && q < nslot) ? q8[((int64_t)q * m + j) * kbar + i] : 0u;
+        if (clamp) e = min(e, 127u);
         v |= e << (8 * b);
       }
       w[u] = v;
@@ -252,6 +273,24 @@ __device__ __forceinline__ Sum4 lut_sum_fast(uint32_t base, uint32_t w0, uint32_
       s.hi = fma_add(__byte_perm(v, 0u, 0x4341u), one, s.hi);
     }
   }
+  return s;
+}
+
+// Fast variant for 7-bit (clamped) tiles, MPAD = 4: add the words of
+// subspaces (0,1) and (2,3) first (bytes <= 254, no carries), then split the
+// two pair sums.
+__device__ __forceinline__ Sum4 lut_sum_fast7(uint32_t base, uint32_t w, uint32_t one) {
+  uint32_t v[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t a = __byte_perm(w, base + (j % 2) * 128, 0x7604u | ((j & 3) << 4));
+    if (j < 2) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v[j]) : "r"(a));
+    else asm volatile("ld.shared.u32 %0, [%1+65536];" : "=r"(v[j]) : "r"(a));
+  }
+  const uint32_t p01 = fma_add(v[0], one, v[1]), p23 = fma_add(v[2], one, v[3]);
+  Sum4 s;
+  s.lo = fma_add(p01 & 0x00FF00FFu, one, p23 & 0x00FF00FFu);
+  s.hi = fma_add(__byte_perm(p01, 0u, 0x4341u), one, __byte_perm(p23, 0u, 0x4341u));
   return s;
 }
 
@@ -350,6 +389,7 @@ struct EmitArgs {
   const int64_t* unit_r0;       // optional per-unit row range (ivf)
   const int64_t* unit_r1;
   uint32_t one;                 // = 1 (opaque to the compiler, see fma_add)
+  const int* tile_fast;         // optional per-tile flag: LUT clamped to 7 bits
   int n_units;                  // tiles * units_per_tile
   int units_per_tile;
 };
@@ -426,6 +466,7 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
       cur_tile = tile;
       __syncthreads();
     }
+    const bool fast_tile = a.tile_fast != nullptr && a.tile_fast[tile] != 0;
     const int q0 = tile * G::QT + 4 * lic;
     const uint32_t glo = (uint32_t)a.gword[q0] | ((uint32_t)a.gword[q0 + 2] << 16);
     const uint32_t ghi = (uint32_t)a.gword[q0 + 1] | ((uint32_t)a.gword[q0 + 3] << 16);
@@ -522,6 +563,28 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
       const uint32_t lo = edge ? (uint32_t)max((int64_t)0, r0 - rb) : 0u;
       const uint32_t hi = edge ? (uint32_t)min((int64_t)G::CHUNK_ROWS, r1 - rb) : (uint32_t)G::CHUNK_ROWS;
       const uint32_t rboff = (uint32_t)(rb - r0a);
+      auto group4 = [&](const uint4 v, int i, auto fast7) {
+        Sum4 s0, s1, s2, s3;
+        if constexpr (decltype(fast7)::value) {
+          s0 = lut_sum_fast7(lbase, v.x, one); s1 = lut_sum_fast7(lbase, v.y, one);
+          s2 = lut_sum_fast7(lbase, v.z, one); s3 = lut_sum_fast7(lbase, v.w, one);
+        } else {
+          s0 = lut_sum_fast<MPAD>(lbase, v.x, 0, one); s1 = lut_sum_fast<MPAD>(lbase, v.y, 0, one);
+          s2 = lut_sum_fast<MPAD>(lbase, v.z, 0, one); s3 = lut_sum_fast<MPAD>(lbase, v.w, 0, one);
+        }
+        const uint32_t xl0 = fma_add(s0.lo, mone, glo), xh0 = fma_add(s0.hi, mone, ghi);
+        const uint32_t xl1 = fma_add(s1.lo, mone, glo), xh1 = fma_add(s1.hi, mone, ghi);
+        const uint32_t xl2 = fma_add(s2.lo, mone, glo), xh2 = fma_add(s2.hi, mone, ghi);
+        const uint32_t xl3 = fma_add(s3.lo, mone, glo), xh3 = fma_add(s3.hi, mone, ghi);
+        if ((xl0 | xh0) & 0x80008000u) record(xl0, xh0, i, 0);
+        if ((xl1 | xh1) & 0x80008000u) record(xl1, xh1, i, 1);
+        if ((xl2 | xh2) & 0x80008000u) record(xl2, xh2, i, 2);
+        if ((xl3 | xh3) & 0x80008000u) record(xl3, xh3, i, 3);
+      };
+      if (MPAD == 4 && fast_tile) {
+#pragma unroll 2
+        for (int i = 0; i < 32; ++i) group4(wst[i], i, std::integral_constant<bool, true>());
+      } else
 #pragma unroll 2
       for (int i = 0; i < 32; ++i) {
         const uint4 v = wst[i];

@@ -222,3 +222,19 @@ def test_timings_and_errors():
         idx.search(g["queries"], 5, mode="hybrid")
     dists, ids = idx.search(g["queries"][:1], len(g["codes"]) + 10)
     assert (ids[0] >= 0).sum() == len(g["codes"]) and np.isinf(dists[0, len(g["codes"]):]).all()
+
+
+def test_seven_bit_fast_tiles_vs_oracle():
+    """Small r2 over a larger database puts every guard <= 126, so every tile
+    takes the clamped 7-bit scan path; results must stay bit-exact."""
+    cb, der, codes, Y = _sift_setup(150_000, 40, seed=8)
+    idx = FlatIndex.from_arrays(cb, der, codes)
+    bstar, _ = idx.candidate_counts(Y, 60)
+    assert bstar.max() <= 120, bstar.max()
+    d0, i0 = _oracle(cb, der, codes, Y, 20, 60)
+    d1, i1 = idx.search(Y, 20, mode="derived", r2=60)
+    assert np.array_equal(i0, i1) and _same(d0, d1)
+    # and a mixed batch: half the tile with large r2 guards (not clamped)
+    d0, i0 = _oracle(cb, der, codes, Y[:8], 20, 3000)
+    d1, i1 = idx.search(Y[:8], 20, mode="derived", r2=3000)
+    assert np.array_equal(i0, i1) and _same(d0, d1)
