@@ -140,6 +140,9 @@ class FlatIndex(BaseEstimator):
                 raise ValueError(f"r={r} must not exceed r2={r2}")
             if self.codes_.shape[0] == 0 or r2 < 1:  # twopass.py:76-77
                 raise ValueError("need at least one code to estimate qmax")
+        m, _, dsub = self.quantizer.codebooks_.shape
+        if Y.shape[1] != m * dsub:  # search.py:42-43
+            raise ValueError(f"query dimension {Y.shape[1]} != {m}*{dsub}")
         if r < 1:  # search.py:99-101 (ResultSet)
             raise ValueError(f"result size must be >= 1, got {r}")
         yr = rotated_queries(self.quantizer, Y)

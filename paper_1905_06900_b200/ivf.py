@@ -130,6 +130,8 @@ class IVFIndex(BaseEstimator):
             return (d, i, _timings(0, None)) if return_timings else (d, i)
         if not (1 <= ma <= self.n_cells):  # ivf.py:115-116 (first query's probe)
             raise ValueError(f"ma must be in [1, {self.n_cells}], got {ma}")
+        if Y.shape[1] != self.centers_.shape[1]:  # ivf.py:117 broadcasting error
+            raise ValueError(f"query dimension {Y.shape[1]} != {self.centers_.shape[1]}")
         if r < 1:
             raise ValueError(f"result size must be >= 1, got {r}")
         h = self._handle()
