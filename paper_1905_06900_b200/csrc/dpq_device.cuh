@@ -100,6 +100,24 @@ __device__ __forceinline__ float pw_sqdist(const float* __restrict__ c,
   return n <= 128 ? pw_block(c, y, n) : pw_sqdist_long(c, y, n);
 }
 
+// Runtime n with 8 | n <= 128 and 16-B aligned rows: same association
+// order as pw_block, 128-bit loads for both operands.
+__device__ __forceinline__ float pw_sqdist_v8(const float* __restrict__ c, const float* __restrict__ y, int n) {
+  const float4* c4 = reinterpret_cast<const float4*>(c);
+  const float4* y4 = reinterpret_cast<const float4*>(y);
+  float r[8];
+  for (int i = 0; i < n / 8; ++i) {
+    const float4 a = c4[2 * i], b = c4[2 * i + 1];
+    const float4 p = y4[2 * i], q = y4[2 * i + 1];
+    const float v[8] = {sqdiff(a.x, p.x), sqdiff(a.y, p.y), sqdiff(a.z, p.z), sqdiff(a.w, p.w),
+                        sqdiff(b.x, q.x), sqdiff(b.y, q.y), sqdiff(b.z, q.z), sqdiff(b.w, q.w)};
+#pragma unroll
+    for (int l = 0; l < 8; ++l) r[l] = (i == 0) ? v[l] : __fadd_rn(r[l], v[l]);
+  }
+  return __fadd_rn(__fadd_rn(__fadd_rn(r[0], r[1]), __fadd_rn(r[2], r[3])),
+                   __fadd_rn(__fadd_rn(r[4], r[5]), __fadd_rn(r[6], r[7])));
+}
+
 // Compile-time dsub specialisation (dsub % 4 == 0, <= 128): codebook row
 // fetched with 128-bit loads, same association order as pw_block.
 template <int DSUB>

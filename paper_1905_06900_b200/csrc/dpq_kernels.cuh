@@ -11,9 +11,10 @@
 //   K3 k_threshold      CappedBuckets bound + refine bucket walk
 //                       (twopass.py:171-201, 276-308) in closed form:
 //                       b* = min{b : #(s <= b) >= r2}, else 254
-//   K5 k_full_tables    compute_tables(yr, codebooks_) (conventional path)
-//   K6 k_refine_topk    LazyTables + _refine_batch + adc_batch + top-r
-//                       (twopass.py:220-273, search.py:64-88): exact f64
+//   K5 k_group_tables   LazyTables (twopass.py:220-251) at derived-group
+//                       granularity; k_full_tables for the conventional path
+//   K6 k_refine_topk    _refine_batch + adc_batch + top-r
+//                       (twopass.py:269-273, search.py:64-88): exact f64
 //                       distance of every candidate, exact (dist,id) top-r
 //
 // Data layout in HBM (per index):
@@ -21,10 +22,8 @@
 //                             padded to MPAD in {4, 8} with zero bytes; the
 //                             first pass reads only this (4 or 8 B/code).
 //   codes  (n, m) u8/u16      original codes, gathered per candidate.
-//   lut    (tiles, MPAD, 256, QT) u16  8-bit tables of QT queries
-//                             interleaved so lane l of a warp reads the
-//                             entries of queries 2l, 2l+1 for one table row
-//                             with one conflict-free 32-bit LDS.
+//   lut    per query tile of QT = 128 (MPAD 4) / 64 (MPAD 8) queries: u8
+//          entries, 4 queries per 32-bit word, see lut_index.
 #pragma once
 #include <type_traits>
 
@@ -117,9 +116,11 @@ __global__ void __launch_bounds__(256) k_small_tables(TablesArgs a) {
   __syncthreads();
   // compute_tables: row_sq_dists per derived centroid (search.py:24-25,46-47)
   float mn = INFINITY;
+  const bool v8 = (a.dsub & 7) == 0 && a.dsub <= 128;
   for (int e = tid; e < ne; e += 256) {
     const int j = e / a.kbar;
-    float v = pw_sqdist(a.dcb + (int64_t)e * a.dsub, ys + j * a.dsub, a.dsub);
+    float v = v8 ? pw_sqdist_v8(a.dcb + (int64_t)e * a.dsub, ys + j * a.dsub, a.dsub)
+                 : pw_sqdist(a.dcb + (int64_t)e * a.dsub, ys + j * a.dsub, a.dsub);
     st[e] = v;
     mn = fminf(mn, v);
   }
@@ -366,11 +367,12 @@ __global__ void __launch_bounds__(NT, 1)
 // each warp pulls 512-B chunks of the low-byte plane with 128-bit
 // non-allocating loads (double-buffered through registers), re-reads them as
 // warp-uniform 128-bit shared loads, and every lane sums the table entries of
-// its two queries for each row with four (MPAD=4) conflict-free 32-bit LDS:
-// two u16 lanes per register, no carries (sum <= MPAD*255 < 2^15).  A row is
-// emitted for a query iff its raw sum <= guard (so score = raw sum < 255),
-// tested with one subtract on the packed pair:
-//   G = (0x8000 + B0) | (0x8000 + B1) << 16;  hit_k = bit 15+16k of (G - s).
+// its four queries for each row with MPAD conflict-free 32-bit LDS (one row
+// of one table = one 128-B line read by the 32 lanes), split into two u16x2
+// accumulators (queries 0,2 and 1,3) that never carry (sum <= 8*255 < 2^15).
+// A row is emitted for a query iff its raw sum <= guard (then score = raw
+// sum < 255), tested with one subtract per accumulator:
+//   G = (0x8000 + B0) | (0x8000 + B2) << 16;  hit = bit 15 / 31 of (G - s).
 // ============================================================================
 struct EmitArgs {
   const uint8_t* plane;
@@ -527,12 +529,6 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
         }
         wc += __popc(bal);
       }
-    };
-    // hit bits of one code: query qs hits iff bit 15 (lo half) / 31 (hi half)
-    // of (guard - sum) is set: qs0 = lo.15, qs1 = hi.15, qs2 = lo.31, qs3 = hi.31
-    auto code_bits = [&](Sum4 sm) -> uint32_t {
-      const uint32_t xl = glo - sm.lo, xh = ghi - sm.hi;
-      return ((xl >> 15) & 1u) | ((xh >> 14) & 2u) | ((xl >> 29) & 4u) | ((xh >> 28) & 8u);
     };
     // hit bits of one code from (guard - sum): qs0 lo.15, qs1 hi.15, qs2 lo.31, qs3 hi.31
     auto bits_x = [](uint32_t xl, uint32_t xh) -> uint32_t {
@@ -908,7 +904,7 @@ __global__ void __launch_bounds__(NT) k_refine_topk(RefineArgs a) {
   __shared__ int fill;
   __shared__ uint64_t thr_k;
   __shared__ int64_t thr_i;
-  __shared__ unsigned long long nref;
+  __shared__ unsigned nref;
   const int q = blockIdx.x;
   for (int i = threadIdx.x; i < a.ystride; i += NT) ys[i] = a.y[(int64_t)q * a.ystride + i];
   if (threadIdx.x == 0) { fill = 0; thr_k = ~0ull; thr_i = INT64_MAX; nref = 0; }
@@ -924,7 +920,8 @@ __global__ void __launch_bounds__(NT) k_refine_topk(RefineArgs a) {
   } else {
     ntot = a.n_rows;
   }
-  unsigned long long my_ref = 0;
+  unsigned my_ref = 0;
+  const float* tq = a.tables ? a.tables + (int64_t)q * a.m * a.k : nullptr;
   // candidate -> (key, id); false when it is not a candidate (score > b*)
   auto eval = [&](int64_t idx, uint64_t& key, int64_t& id) -> bool {
     int64_t row;
@@ -941,13 +938,15 @@ __global__ void __launch_bounds__(NT) k_refine_topk(RefineArgs a) {
     double dist = 0.0;
     const float* yq = ys + (int64_t)probe * d;
     if (MODE == MODE_EMIT_TABLE && a.code_bytes == 2 && a.m == 4) {
-      // one 8-byte code load, four independent table gathers
+      // one 8-byte code load, four independent table gathers with 32-bit
+      // offsets inside this query's table block (m * k floats)
       const uint2 v = *reinterpret_cast<const uint2*>((const uint16_t*)a.codes + row * 4);
-      const int gs = a.k / a.kbar;
-      const float t0 = __ldg(a.tables + table_index(q, 0, v.x & 0xFFFFu, 4, a.kbar, a.bbar, gs));
-      const float t1 = __ldg(a.tables + table_index(q, 1, v.x >> 16, 4, a.kbar, a.bbar, gs));
-      const float t2 = __ldg(a.tables + table_index(q, 2, v.y & 0xFFFFu, 4, a.kbar, a.bbar, gs));
-      const float t3 = __ldg(a.tables + table_index(q, 3, v.y >> 16, 4, a.kbar, a.bbar, gs));
+      const uint32_t kmask = (uint32_t)a.kbar - 1u, gs = (uint32_t)(a.k >> a.bbar);
+      auto off = [&](uint32_t j, uint32_t c) { return ((j << a.bbar) + (c & kmask)) * gs + (c >> a.bbar); };
+      const float t0 = __ldg(tq + off(0, v.x & 0xFFFFu));
+      const float t1 = __ldg(tq + off(1, v.x >> 16));
+      const float t2 = __ldg(tq + off(2, v.y & 0xFFFFu));
+      const float t3 = __ldg(tq + off(3, v.y >> 16));
       dist = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(dist, (double)t0), (double)t1), (double)t2), (double)t3);
     } else {
       for (int j = 0; j < a.m; ++j) {
@@ -1011,9 +1010,11 @@ __global__ void __launch_bounds__(NT) k_refine_topk(RefineArgs a) {
     }
   }
   if (a.n_refined) {
-    atomicAdd(&nref, my_ref);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) my_ref += __shfl_xor_sync(0xffffffffu, my_ref, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(&nref, my_ref);
     __syncthreads();
-    if (threadIdx.x == 0) atomicAdd(a.n_refined, nref);
+    if (threadIdx.x == 0) atomicAdd(a.n_refined, (unsigned long long)nref);
   }
 }
 
