@@ -463,7 +463,7 @@ static int ensure_tables(Index* h, int nq) {
 }
 
 static bool group_tables_fit(Index* h, int nq) {
-  const size_t smem = (size_t)(h->k / h->kbar) * (h->dsub + 1) * 4 + (size_t)nq * 4;
+  const size_t smem = (size_t)(h->k / h->kbar) * (h->dsub + 4) * 4 + (size_t)nq * 4;
   return smem <= 200 * 1024;
 }
 
@@ -476,7 +476,8 @@ int run_group_tables(Index* h, int nq, int ystride) {
   ga.nq = nq; ga.m = h->m; ga.k = h->k; ga.kbar = h->kbar; ga.bbar = h->bbar; ga.dsub = h->dsub;
   ga.tables = w.tables; ga.n_entries = h->d_nent;
   const int gsize = h->k / h->kbar;
-  const size_t smem = (size_t)gsize * (h->dsub + 1) * 4 + (size_t)nq * 4;
+  const int ld = h->dsub == 32 ? 36 : h->dsub + 1;
+  const size_t smem = (size_t)gsize * ld * 4 + (size_t)nq * 4;
   static size_t attr = 0;
   dim3 grid(h->kbar, h->m);
   if (h->dsub == 32) {

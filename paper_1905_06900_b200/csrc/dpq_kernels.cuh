@@ -784,11 +784,13 @@ struct GroupTablesArgs {
 
 template <int DSUB>
 __global__ void __launch_bounds__(256) k_group_tables(GroupTablesArgs a) {
-  extern __shared__ __align__(16) float tile[];  // [gsize][dsub+1]
+  extern __shared__ __align__(16) float tile[];  // [gsize][ld]
   __shared__ int nact;
   const int g = blockIdx.x, j = blockIdx.y;
   const int dsub = DSUB > 0 ? DSUB : a.dsub;
-  const int gsize = a.k / a.kbar, ld = dsub + 1;
+  // DSUB > 0: rows padded to 16-B multiples + 4 floats (conflict-free float4
+  // reads across consecutive rows); generic: +1 float
+  const int gsize = a.k / a.kbar, ld = DSUB > 0 ? DSUB + 4 : dsub + 1;
   int* act = reinterpret_cast<int*>(tile + gsize * ld);
   if (threadIdx.x == 0) nact = 0;
   for (int e = threadIdx.x; e < gsize * dsub; e += 256) {
@@ -806,16 +808,7 @@ __global__ void __launch_bounds__(256) k_group_tables(GroupTablesArgs a) {
     const float* row = tile + ib * ld;
     float v;
     if constexpr (DSUB > 0) {
-      float r[8];
-#pragma unroll
-      for (int i = 0; i < DSUB / 8; ++i)
-#pragma unroll
-        for (int l = 0; l < 8; ++l) {
-          const float sq = sqdiff(row[8 * i + l], __ldg(yq + 8 * i + l));
-          r[l] = i == 0 ? sq : __fadd_rn(r[l], sq);
-        }
-      v = __fadd_rn(__fadd_rn(__fadd_rn(r[0], r[1]), __fadd_rn(r[2], r[3])),
-                    __fadd_rn(__fadd_rn(r[4], r[5]), __fadd_rn(r[6], r[7])));
+      v = pw_sqdist_v8(row, yq, DSUB);  // both operands 16-B aligned
     } else {
       v = pw_sqdist(row, yq, dsub);
     }
