@@ -54,6 +54,32 @@ __device__ __forceinline__ uint32_t lds32(const uint8_t* p) {
   return *reinterpret_cast<const uint32_t*>(p);
 }
 
+// ---- TMA bulk copies (cp.async.bulk, completion on an mbarrier) -----------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 template <int MPAD>
 struct ScanGeom {
   static constexpr int QT = MPAD == 4 ? 128 : 64;  // queries per tile
@@ -427,8 +453,11 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
   constexpr int NW = NT / 32;
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ int s_unit;
+  __shared__ __align__(8) uint64_t lut_bar;  // completion of the LUT bulk copy
+  uint32_t lut_phase = 0;
   const uint32_t dyn = (uint32_t)__cvta_generic_to_shared(smem);
   if (dyn + emit_low_bytes<MPAD, NT>() > kLutShared) __trap();  // layout invariant
+  if (threadIdx.x == 0) mbar_init(&lut_bar, 1);
   uint8_t* slut = smem + (kLutShared - dyn);
   uint4* stage = reinterpret_cast<uint4*>(smem);
   uint64_t* hbuf_all = reinterpret_cast<uint64_t*>(smem + NW * 32 * 16);
@@ -463,10 +492,16 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
       r1 = min(a.row_end, r0 + a.rows_per_cta);
     }
     if (tile != cur_tile) {
-      const uint4* src = reinterpret_cast<const uint4*>(a.lut + (int64_t)tile * G::LUT_BYTES);
-      for (int i = threadIdx.x; i < G::LUT_BYTES / 16; i += NT) reinterpret_cast<uint4*>(slut)[i] = src[i];
+      // every warp is past the previous unit (barrier above): one thread
+      // moves the 128-KB tile with a TMA bulk copy, all wait on the mbarrier
+      if (threadIdx.x == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&lut_bar, G::LUT_BYTES);
+        bulk_g2s(slut, a.lut + (int64_t)tile * G::LUT_BYTES, G::LUT_BYTES, &lut_bar);
+      }
+      mbar_wait(&lut_bar, lut_phase);
+      lut_phase ^= 1u;
       cur_tile = tile;
-      __syncthreads();
     }
     const bool fast_tile = a.tile_fast != nullptr && a.tile_fast[tile] != 0;
     const int q0 = tile * G::QT + 4 * lic;
