@@ -186,7 +186,8 @@ int dpq_last_phase_ms(dpq_index_t* index, float* ms7);
 /* Counters since creation (8 x i64): kernel launches, queries searched,
  * code rows scanned (sum over queries), candidates refined, exact-redo
  * rounds, first-pass rows emitted (score <= guard), full-table entries
- * computed by the group-lazy table builder, 0.                            */
+ * computed by the group-lazy table builder, scan units run by the wide
+ * (5/6-bit, 16 queries per lane) loop.                                    */
 int dpq_counters(dpq_index_t* index, int64_t* out8);
 
 #ifdef __cplusplus

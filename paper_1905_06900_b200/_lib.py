@@ -132,7 +132,7 @@ class Handle:
         out = np.zeros(8, dtype=np.int64)
         check(lib().dpq_counters(self.raw, ptr(out)))
         return dict(zip(("launches", "queries", "rows_scanned", "refined", "fallbacks", "emitted",
-                             "table_entries"),
+                             "table_entries", "wide_units"),
                         out.tolist()))
 
     def set_timing(self, on: bool) -> None:

@@ -237,6 +237,7 @@ static int launch_emit_t(Index* h, EmitArgs ea, int ntiles, int64_t rows) {
   ea.unit_counter = h->ws.counter;
   ea.one = 1u;
   ea.tile_fast = h->ws.tile_fast;
+  ea.n_wide = h->d_nwide;
   if (ea.unit_tile) {  // caller-built units (ivf lists)
     if (ea.n_units < 1) return DPQ_OK;
     DPQ_CUDA(cudaMemsetAsync(h->ws.counter, 0, sizeof(unsigned), h->stream));
@@ -347,10 +348,10 @@ int build_lut(Index* h, int nslot, const uint16_t* gword) {
   int* tf = w.tile_fast;  // reset to 0 when gword is null (unclamped LUT)
   if (h->mpad == 4)
     k_build_lut<4><<<(unsigned)((threads + 255) / 256), 256, 0, h->stream>>>(w.q8, nslot, h->m, h->kbar, w.lut,
-                                                                             ntiles, gword, tf);
+                                                                             ntiles, gword, tf, h->wide);
   else
     k_build_lut<8><<<(unsigned)((threads + 255) / 256), 256, 0, h->stream>>>(w.q8, nslot, h->m, h->kbar, w.lut,
-                                                                             ntiles, gword, tf);
+                                                                             ntiles, gword, tf, h->wide);
   DPQ_LAUNCHED(h);
   return DPQ_OK;
 }
@@ -651,6 +652,7 @@ int index_common_init(Index* h, int device, int m, int k, int kbar, int dsub, co
   if (const char* e = getenv("DPQ_GUARD_SAMPLE")) h->sample = std::max<int64_t>(1, atoll(e));
   if (const char* e = getenv("DPQ_EXACT_LIMIT")) h->exact_limit = std::max<int64_t>(0, atoll(e));
   if (const char* e = getenv("DPQ_EMIT_CAP")) h->cap0 = std::max<int64_t>(1, atoll(e));
+  if (const char* e = getenv("DPQ_SCAN_WIDE")) h->wide = atoi(e) != 0;
   DPQ_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   h->own_stream = true;
   for (int i = 0; i < 8; ++i) DPQ_CUDA(cudaEventCreate(&h->ev[i]));
@@ -659,7 +661,9 @@ int index_common_init(Index* h, int device, int m, int k, int kbar, int dsub, co
   DPQ_TRY(dmalloc(&h->d_nref, 1));
   DPQ_TRY(dmalloc(&h->d_nemit, 1));
   DPQ_TRY(dmalloc(&h->d_nent, 1));
+  DPQ_TRY(dmalloc(&h->d_nwide, 1));
   DPQ_CUDA(cudaMemset(h->d_nent, 0, 8));
+  DPQ_CUDA(cudaMemset(h->d_nwide, 0, 8));
   DPQ_CUDA(cudaMemcpy(h->cb, codebooks, (size_t)m * k * dsub * 4, cudaMemcpyHostToDevice));
   DPQ_CUDA(cudaMemcpy(h->dcb, derived, (size_t)m * kbar * dsub * 4, cudaMemcpyHostToDevice));
   DPQ_CUDA(cudaMemset(h->d_nref, 0, 8));
@@ -674,7 +678,7 @@ void index_free(Index* h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   Workspace& w = h->ws;
   void* dev[] = {h->cb, h->dcb, h->codes, h->plane, h->own_prefix ? h->prefix : nullptr, h->centers,
-                 h->offsets, h->sorted_ids, h->d_nref, h->d_nemit, h->d_nent, w.y, w.small, w.q8, w.qmin, w.qmax, w.bounds,
+                 h->offsets, h->sorted_ids, h->d_nref, h->d_nemit, h->d_nent, h->d_nwide, w.y, w.small, w.q8, w.qmin, w.qmax, w.bounds,
                  w.lut, w.hist, w.hist_i, w.guard_b, w.gword, w.emit_cnt, w.emit, w.bstar, w.ncand,
                  w.flags, w.only, w.tile_list, w.out_d, w.out_i, w.tables, w.slot_query, w.slot_probe,
                  w.slot_pre_off, w.slot_pre_len, w.counter, w.tile_fast};
@@ -913,14 +917,16 @@ int dpq_last_phase_ms(dpq_index_t* index, float* ms7) {
 int dpq_counters(dpq_index_t* index, int64_t* out8) {
   Index* h = reinterpret_cast<Index*>(index);
   if (!h || !out8) { set_error("null argument"); return DPQ_ERR_ARG; }
-  unsigned long long nref = 0, nemit = 0, nent = 0;
+  unsigned long long nref = 0, nemit = 0, nent = 0, nwide = 0;
   cudaSetDevice(h->device);
   DPQ_CUDA(cudaMemcpy(&nref, h->d_nref, 8, cudaMemcpyDeviceToHost));
   DPQ_CUDA(cudaMemcpy(&nemit, h->d_nemit, 8, cudaMemcpyDeviceToHost));
   DPQ_CUDA(cudaMemcpy(&nent, h->d_nent, 8, cudaMemcpyDeviceToHost));
+  DPQ_CUDA(cudaMemcpy(&nwide, h->d_nwide, 8, cudaMemcpyDeviceToHost));
   h->counters[3] = (int64_t)nref;
   h->counters[5] = (int64_t)nemit;
   h->counters[6] = (int64_t)nent;
+  h->counters[7] = (int64_t)nwide;
   for (int i = 0; i < 8; ++i) out8[i] = h->counters[i];
   return DPQ_OK;
 }

@@ -87,16 +87,18 @@ struct Index {
   bool timing = false;
   cudaEvent_t ev[8] = {};
   float phase_ms[PH_N] = {};
-  int64_t counters[8] = {};  // launches, queries, rows scanned, refined, fallbacks, emitted
+  int64_t counters[8] = {};  // launches, queries, rows scanned, refined, fallbacks, emitted, table entries, wide units
   unsigned long long* d_nref = nullptr;
   unsigned long long* d_nemit = nullptr;
   unsigned long long* d_nent = nullptr;   // lazily computed table entries
+  unsigned long long* d_nwide = nullptr;  // scan units run by the wide loop
   size_t emit_budget = (size_t)16 << 30;  // bytes for emit buffers
   // guard sampling (env DPQ_GUARD_SAMPLE / DPQ_EXACT_LIMIT / DPQ_EMIT_CAP
   // override them so tests can force the exact-redo and overflow paths)
   int64_t sample = 16384;
   int64_t exact_limit = 65536;
   int64_t cap0 = 0;
+  int wide = 1;  // wide scan tiles (env DPQ_SCAN_WIDE=0 disables)
   Workspace ws;
   // sharded-search state between dpq_shard_* calls
   int shard_nq = 0;

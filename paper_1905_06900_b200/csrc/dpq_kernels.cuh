@@ -207,25 +207,46 @@ __global__ void __launch_bounds__(256) k_small_tables(TablesArgs a) {
 // words add without carries (k_scan_emit's fast inner loop).
 constexpr uint32_t kClampMaxGuard = 126;
 
+// Tile modes (tile_fast[t]), chosen from the largest guard B of the tile:
+//   0  generic 8-bit entries
+//   7  B <= 126: entries clamped to 127, pair sums in bytes (fast7 loop)
+//   6  B <= 62 : entries clamped to 63, four-entry sums <= 252 in bytes
+//   5  B <= 30 : entries clamped to 31 and the per-query bias C = 127 - B
+//                folded into subspace 0, so a query hits iff bit 7 of its
+//                byte sum is clear (C = 128 for slots without a guard)
+// Modes 5/6 are scanned by the "wide" loop of k_scan_emit (MPAD = 4): 16
+// queries per lane per 128-bit LDS, 4 codes per warp step.
+enum { kModeGeneric = 0, kModeWide5 = 5, kModeWide6 = 6, kMode7 = 7 };
+
+__device__ __forceinline__ uint32_t wide_bias(uint32_t gw) {  // C of one slot
+  return gw >= 0x8000u ? 127u - (gw - 0x8000u) : 128u;
+}
+
 template <int MPAD>
 __global__ void __launch_bounds__(256) k_build_lut(const uint8_t* __restrict__ q8, int nslot, int m, int kbar,
                                                    uint8_t* __restrict__ lut, int ntiles,
-                                                   const uint16_t* __restrict__ gword, int* __restrict__ tile_fast) {
+                                                   const uint16_t* __restrict__ gword, int* __restrict__ tile_fast,
+                                                   int allow_wide) {
   using G = ScanGeom<MPAD>;
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= (int64_t)ntiles * MPAD * 256) return;
   const int i = (int)(gid & 255);
   const int j = (int)((gid >> 8) % MPAD);
   const int t = (int)(gid / (MPAD * 256));
-  bool clamp = false;
+  int mode = kModeGeneric;
   if (gword) {
-    clamp = true;
+    uint32_t bmax = 0;
     for (int qq = 0; qq < G::QT; ++qq) {
       const uint32_t gw = gword[t * G::QT + qq];
-      if (gw >= 0x8000u && gw - 0x8000u > kClampMaxGuard) { clamp = false; break; }
+      if (gw >= 0x8000u) bmax = max(bmax, gw - 0x8000u);
     }
+    if (MPAD == 4 && allow_wide && bmax <= 30u) mode = kModeWide5;
+    else if (MPAD == 4 && allow_wide && bmax <= 62u) mode = kModeWide6;
+    else if (bmax <= kClampMaxGuard) mode = kMode7;
   }
-  if (tile_fast && i == 0 && j == 0) tile_fast[t] = clamp ? 1 : 0;
+  const uint32_t cmax = mode == kModeWide5 ? 31u : (mode == kModeWide6 ? 63u : (mode == kMode7 ? 127u : 255u));
+  const bool fold = mode == kModeWide5 && j == 0;
+  if (tile_fast && i == 0 && j == 0) tile_fast[t] = mode;
   uint4* dst = reinterpret_cast<uint4*>(lut + (int64_t)t * G::LUT_BYTES +
                                         (int64_t)((j / G::SPR) * 256 + i) * 256 + (j % G::SPR) * G::ROWB);
   const bool live = j < m && i < kbar;
@@ -239,7 +260,8 @@ __global__ void __launch_bounds__(256) k_build_lut(const uint8_t* __restrict__ q
       for (int b = 0; b < 4; ++b) {
         const int q = t * G::QT + 4 * (4 * l4 + u) + b;
         uint32_t e = (live && q < nslot) ? q8[((int64_t)q * m + j) * kbar + i] : 0u;
-        if (clamp) e = min(e, 127u);
+        e = min(e, cmax);
+        if (fold) e += wide_bias(gword[q]);  // <= 31 + 128
         v |= e << (8 * b);
       }
       w[u] = v;
@@ -319,6 +341,40 @@ __device__ __forceinline__ Sum4 lut_sum_fast7(uint32_t base, uint32_t w, uint32_
   s.lo = fma_add(p01 & 0x00FF00FFu, one, p23 & 0x00FF00FFu);
   s.hi = fma_add(__byte_perm(p01, 0u, 0x4341u), one, __byte_perm(p23, 0u, 0x4341u));
   return s;
+}
+
+// 128-bit shared loads of the wide loop (hi: + 64 KB, subspaces 2/3)
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint4 lds128_hi(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4+65536];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(a));
+  return v;
+}
+
+// Wide loop, one code word w: byte sums of the four subspace entries for
+// the lane's 16 queries (4 words x 4 bytes).  b0 = lane base (64-KB aligned
+// LUT | chunk part * 16), b1 = b0 + 128 (odd subspaces).
+__device__ __forceinline__ void wide_sums(uint32_t w, uint32_t b0, uint32_t b1, uint32_t one, uint32_t t[4]) {
+  const uint4 A0 = lds128(__byte_perm(w, b0, 0x7604u));
+  const uint4 A1 = lds128(__byte_perm(w, b1, 0x7614u));
+  const uint4 A2 = lds128_hi(__byte_perm(w, b0, 0x7624u));
+  const uint4 A3 = lds128_hi(__byte_perm(w, b1, 0x7634u));
+  t[0] = fma_add(A3.x, one, A0.x + A1.x + A2.x);
+  t[1] = fma_add(A3.y, one, A0.y + A1.y + A2.y);
+  t[2] = fma_add(A3.z, one, A0.z + A1.z + A2.z);
+  t[3] = fma_add(A3.w, one, A0.w + A1.w + A2.w);
+}
+
+// per word: bit 7 of byte b clear <=> query b of the word hits
+template <int MODE>
+__device__ __forceinline__ uint32_t wide_u(uint32_t t, uint32_t c, uint32_t one) {
+  if constexpr (MODE == kModeWide5) return t;  // bias folded into the table
+  else return t | fma_add(t & 0x7F7F7F7Fu, one, c);
 }
 
 // score of lane query qsel (0..3) from the packed sums
@@ -417,7 +473,8 @@ struct EmitArgs {
   const int64_t* unit_r0;       // optional per-unit row range (ivf)
   const int64_t* unit_r1;
   uint32_t one;                 // = 1 (opaque to the compiler, see fma_add)
-  const int* tile_fast;         // optional per-tile flag: LUT clamped to 7 bits
+  const int* tile_fast;         // optional per-tile mode (kMode*, see k_build_lut)
+  unsigned long long* n_wide;   // optional: units scanned by the wide loop
   int n_units;                  // tiles * units_per_tile
   int units_per_tile;
 };
@@ -441,6 +498,7 @@ constexpr uint32_t kLutShared = 0x10000;  // LUT at shared address 64 KB
 template <int MPAD, int NT>
 __host__ __device__ constexpr int emit_low_bytes() { return (NT / 32) * (32 * 16 + kWarpBuf * 8); }
 constexpr int kLaneQ = 8;  // lane-private hit records per chunk (u16 each)
+constexpr int kLaneQW = 2 * kLaneQ;  // wide loop: u8 step records in the same space
 template <int MPAD, int NT>
 __host__ __device__ constexpr int emit_smem_bytes() {
   return (int)kLutShared + ScanGeom<MPAD>::LUT_BYTES + (NT / 32) * ScanGeom<MPAD>::QT * 4 +
@@ -469,6 +527,7 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
   uint64_t* hbuf = hbuf_all + warp * kWarpBuf;
   uint32_t* hcnt = hcnt_all + warp * G::QT;
   uint16_t* lq = reinterpret_cast<uint16_t*>(hcnt_all + NW * G::QT) + warp * kLaneQ * 32 + lane;
+  uint8_t* lq8 = reinterpret_cast<uint8_t*>(hcnt_all + NW * G::QT) + warp * kLaneQ * 64 + lane;  // wide loop
   const uint32_t lt = (1u << lane) - 1u;
   const uint32_t one = a.one, mone = 0u - a.one;  // opaque 1 / -1 (see fma_add)
   int cur_tile = -1;
@@ -503,10 +562,27 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
       lut_phase ^= 1u;
       cur_tile = tile;
     }
-    const bool fast_tile = a.tile_fast != nullptr && a.tile_fast[tile] != 0;
+    const int tmode = a.tile_fast != nullptr ? a.tile_fast[tile] : kModeGeneric;
+    const bool fast_tile = tmode == kMode7;
+    const bool wide = MPAD == 4 && (tmode == kModeWide5 || tmode == kModeWide6);
     const int q0 = tile * G::QT + 4 * lic;
     const uint32_t glo = (uint32_t)a.gword[q0] | ((uint32_t)a.gword[q0 + 2] << 16);
     const uint32_t ghi = (uint32_t)a.gword[q0 + 1] | ((uint32_t)a.gword[q0 + 3] << 16);
+    // wide loop: lane = (quarter qd: code stream, part cp: queries 16cp..16cp+15)
+    const int qd = lane >> 3, cp = lane & 7;
+    const uint32_t wb0 = kLutShared | (uint32_t)(cp << 4), wb1 = wb0 + 128u;
+    uint32_t cw0 = 0, cw1 = 0, cw2 = 0, cw3 = 0;  // per-query bias C, word k byte b = query 16cp+4k+b
+    if (wide) {
+      if (a.n_wide && threadIdx.x == 0) atomicAdd(a.n_wide, 1ull);
+      const uint16_t* gq = a.gword + tile * G::QT + 16 * cp;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        cw0 |= wide_bias(gq[b]) << (8 * b);
+        cw1 |= wide_bias(gq[4 + b]) << (8 * b);
+        cw2 |= wide_bias(gq[8 + b]) << (8 * b);
+        cw3 |= wide_bias(gq[12 + b]) << (8 * b);
+      }
+    }
     // Logical range [r0, r1); loads start at the 512-B aligned row r0a and
     // rows outside the range are never emitted.
     if (r0 >= r1) continue;
@@ -594,6 +670,80 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
       const uint32_t lo = edge ? (uint32_t)max((int64_t)0, r0 - rb) : 0u;
       const uint32_t hi = edge ? (uint32_t)min((int64_t)G::CHUNK_ROWS, r1 - rb) : (uint32_t)G::CHUNK_ROWS;
       const uint32_t rboff = (uint32_t)(rb - r0a);
+      if constexpr (MPAD == 4) {
+        if (wide) {
+          // Wide loop: quarter qd scans rows 32qd .. 32qd+31 of the chunk,
+          // one row per step; each lane sums its 16 queries with 4 x LDS.128
+          // (4 codes per warp step, conflict-free: the 8 lanes of a quarter
+          // read the 8 16-B parts of one 128-B table row).  A step with a hit
+          // only appends its step index to a lane-private u8 queue.
+          auto wide_chunk = [&](auto md) {
+            constexpr int MODE = decltype(md)::value;
+            const uint32_t* wsw = reinterpret_cast<const uint32_t*>(wst);
+            int lc = 0;
+#pragma unroll 2
+            for (int i4 = 0; i4 < 8; ++i4) {
+              const uint4 cv = wst[qd * 8 + i4];
+              const uint32_t cws[4] = {cv.x, cv.y, cv.z, cv.w};
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                uint32_t t[4];
+                wide_sums(cws[u], wb0, wb1, one, t);
+                const uint32_t all = wide_u<MODE>(t[0], cw0, one) & wide_u<MODE>(t[1], cw1, one) &
+                                     wide_u<MODE>(t[2], cw2, one) & wide_u<MODE>(t[3], cw3, one);
+                const bool h = (~all & 0x80808080u) != 0u;
+                if (h && lc < kLaneQW) lq8[lc * 32] = (uint8_t)(4 * i4 + u);
+                lc += h ? 1 : 0;
+              }
+            }
+            if (!__any_sync(0xffffffffu, lc > 0)) return;
+            // drain: recompute the recorded steps, stage their hits
+            auto emit_step = [&](bool has, int i) {
+              uint32_t hm = 0u, t[4] = {0u, 0u, 0u, 0u};
+              const uint32_t r = 32u * (uint32_t)qd + (uint32_t)i;
+              if (has) {
+                wide_sums(wsw[32 * qd + i], wb0, wb1, one, t);
+                const uint32_t cwk[4] = {cw0, cw1, cw2, cw3};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                  const uint32_t hb = ~wide_u<MODE>(t[k], cwk[k], one) & 0x80808080u;
+                  hm |= (((hb >> 7) & 1u) | ((hb >> 14) & 2u) | ((hb >> 21) & 4u) | ((hb >> 28) & 8u)) << (4 * k);
+                }
+                if (edge && !(r >= lo && r < hi)) hm = 0u;
+              }
+              for (;;) {
+                const bool hh = hm != 0u;
+                const uint32_t bal = __ballot_sync(0xffffffffu, hh);
+                if (!bal) break;
+                if (wc + 32 > kWarpBuf) flush();
+                if (hh) {
+                  const int b = __ffs(hm) - 1;
+                  hm &= hm - 1u;
+                  const int k = b >> 2, sh = 8 * (b & 3);
+                  const uint32_t tw = k == 0 ? t[0] : (k == 1 ? t[1] : (k == 2 ? t[2] : t[3]));
+                  uint32_t sc = (tw >> sh) & 0xFFu;
+                  if (MODE == kModeWide5) {
+                    const uint32_t ck = k == 0 ? cw0 : (k == 1 ? cw1 : (k == 2 ? cw2 : cw3));
+                    sc -= (ck >> sh) & 0xFFu;
+                  }
+                  hbuf[wc + __popc(bal & lt)] =
+                      (uint64_t)(rboff + r) | ((uint64_t)(16 * cp + b) << 32) | ((uint64_t)sc << 40);
+                }
+                wc += __popc(bal);
+              }
+            };
+            if (__any_sync(0xffffffffu, lc > kLaneQW)) {
+              for (int i = 0; i < 32; ++i) emit_step(true, i);  // a queue overflowed: every step
+            } else {
+              const int maxc = (int)__reduce_max_sync(0xffffffffu, (unsigned)lc);
+              for (int e = 0; e < maxc; ++e) emit_step(e < lc, e < lc ? (int)lq8[e * 32] : 0);
+            }
+          };
+          if (tmode == kModeWide5) wide_chunk(std::integral_constant<int, kModeWide5>());
+          else wide_chunk(std::integral_constant<int, kModeWide6>());
+          continue;
+        }
+      }
       auto group4 = [&](const uint4 v, int i, auto fast7) {
         Sum4 s0, s1, s2, s3;
         if constexpr (decltype(fast7)::value) {

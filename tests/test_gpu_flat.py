@@ -238,3 +238,35 @@ def test_seven_bit_fast_tiles_vs_oracle():
     d0, i0 = _oracle(cb, der, codes, Y[:8], 20, 3000)
     d1, i1 = idx.search(Y[:8], 20, mode="derived", r2=3000)
     assert np.array_equal(i0, i1) and _same(d0, d1)
+
+
+@pytest.mark.parametrize("r2", [20, 150, 1200])
+def test_wide_tiles_vs_oracle(r2, monkeypatch):
+    """Guards <= 62 put tiles in the wide 5/6-bit scan loop (16 queries per
+    lane, bias folded into subspace 0 for 5-bit tiles).  Bit-exact against
+    the oracle, and identical to the scan with the wide loop disabled."""
+    cb, der, codes, Y = _sift_setup(150_000, 40, seed=11)
+    idx = FlatIndex.from_arrays(cb, der, codes)
+    bstar, _ = idx.candidate_counts(Y, r2)
+    d0, i0 = _oracle(cb, der, codes, Y, 20, r2)
+    d1, i1 = idx.search(Y, 20, mode="derived", r2=r2)
+    assert np.array_equal(i0, i1) and _same(d0, d1)
+    wide = idx._handle().counters()["wide_units"]
+    if bstar.max() <= 50:  # guards near b*: every tile fits 6 bits
+        assert wide > 0, (bstar.max(), wide)
+    monkeypatch.setenv("DPQ_SCAN_WIDE", "0")
+    idx2 = FlatIndex.from_arrays(cb, der, codes)
+    d2, i2 = idx2.search(Y, 20, mode="derived", r2=r2)
+    assert np.array_equal(i2, i1) and _same(d2, d1)
+    assert idx2._handle().counters()["wide_units"] == 0
+
+
+def test_wide_tiles_mixed_guards_and_padding():
+    """Batch sizes that leave padded slots in the last tile, and queries whose
+    guards differ by tile mode (5-bit, 6-bit, 7-bit, generic) in one batch."""
+    cb, der, codes, Y = _sift_setup(100_000, 130, seed=12)
+    idx = FlatIndex.from_arrays(cb, der, codes)
+    for nq, r2 in ((1, 30), (33, 100), (130, 400), (130, 5000)):
+        d0, i0 = _oracle(cb, der, codes, Y[:nq], 10, r2)
+        d1, i1 = idx.search(Y[:nq], 10, mode="derived", r2=r2)
+        assert np.array_equal(i0, i1) and _same(d0, d1), (nq, r2)
