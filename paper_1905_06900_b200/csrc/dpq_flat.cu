@@ -8,6 +8,7 @@
 // after K3 (guard too tight / emit overflow), which decides whether the
 // exact redo runs.
 #include <cuda_runtime.h>
+#include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
 #include <cmath>
@@ -54,6 +55,7 @@ const char* last_error() { return g_last_error.c_str(); }
   } while (0)
 
 static constexpr int kScanThreads = 1024;
+static constexpr int kEmitThreads = 1024;  // (512 x 128 registers measured slower)
 static constexpr int kTopThreads = 256;
 
 template <class T>
@@ -110,6 +112,7 @@ int ensure_ws(Index* h, int nslot, int r, int ystride, int nq) {
     DPQ_TRY(dmalloc(&w.hist_i, (size_t)qn * 256));
     DPQ_TRY(dmalloc(&w.guard_b, (size_t)std::max(tiles * qt, qn)));
     DPQ_TRY(dmalloc(&w.gword, (size_t)std::max(tiles * qt, qn)));
+    DPQ_TRY(dmalloc(&w.gword_p, (size_t)tiles * qt));
     DPQ_TRY(dmalloc(&w.bstar, (size_t)qn));
     DPQ_TRY(dmalloc(&w.ncand, (size_t)qn));
     DPQ_TRY(dmalloc(&w.flags, (size_t)qn));
@@ -224,11 +227,11 @@ static int num_sms(Index* h) {
 template <int MPAD>
 static int launch_emit_t(Index* h, EmitArgs ea, int ntiles, int64_t rows) {
   using G = ScanGeom<MPAD>;
-  constexpr int NW = kScanThreads / 32;
-  const size_t smem = emit_smem_bytes<MPAD, kScanThreads>();
+  constexpr int NW = kEmitThreads / 32;
+  const size_t smem = emit_smem_bytes<MPAD, kEmitThreads>();
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_scan_emit<MPAD, kScanThreads>,
+    cudaFuncSetAttribute(k_scan_emit<MPAD, kEmitThreads>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
@@ -238,10 +241,11 @@ static int launch_emit_t(Index* h, EmitArgs ea, int ntiles, int64_t rows) {
   ea.one = 1u;
   ea.tile_fast = h->ws.tile_fast;
   ea.n_wide = h->d_nwide;
+  ea.runs = h->rows_sorted ? 1 : 0;
   if (ea.unit_tile) {  // caller-built units (ivf lists)
     if (ea.n_units < 1) return DPQ_OK;
     DPQ_CUDA(cudaMemsetAsync(h->ws.counter, 0, sizeof(unsigned), h->stream));
-    k_scan_emit<MPAD, kScanThreads><<<std::min(sms, ea.n_units), kScanThreads, smem, h->stream>>>(ea);
+    k_scan_emit<MPAD, kEmitThreads><<<std::min(sms, ea.n_units), kEmitThreads, smem, h->stream>>>(ea);
     DPQ_LAUNCHED(h);
     return DPQ_OK;
   }
@@ -258,7 +262,7 @@ static int launch_emit_t(Index* h, EmitArgs ea, int ntiles, int64_t rows) {
   ea.one = 1u;
   DPQ_CUDA(cudaMemsetAsync(h->ws.counter, 0, sizeof(unsigned), h->stream));
   const int grid = (int)std::min<int64_t>(sms, ea.n_units);
-  k_scan_emit<MPAD, kScanThreads><<<grid, kScanThreads, smem, h->stream>>>(ea);
+  k_scan_emit<MPAD, kEmitThreads><<<grid, kEmitThreads, smem, h->stream>>>(ea);
   DPQ_LAUNCHED(h);
   return DPQ_OK;
 }
@@ -312,7 +316,7 @@ static int launch_refine(Index* h, const RefineArgs& ra, int nq) {
 // ---------------------------------------------------------------------------
 // K1 for nslot slots whose queries are already in ws.y.
 // ---------------------------------------------------------------------------
-int build_lut(Index* h, int nslot, const uint16_t* gword);
+int build_lut(Index* h, int nslot, const uint16_t* gword, const int* slot_query = nullptr);
 int run_small_tables(Index* h, int nslot, const void* prefix, int64_t npre,
                      const int64_t* pre_off, const int64_t* pre_len, const double* bounds_in,
                      bool export_debug, const float* y_slots) {
@@ -341,17 +345,17 @@ int run_small_tables(Index* h, int nslot, const void* prefix, int64_t npre,
 
 // Scan-layout LUT tiles from ws.q8; with gword (guards known) tiles whose
 // guards are all <= 126 are clamped to 7-bit entries and flagged fast.
-int build_lut(Index* h, int nslot, const uint16_t* gword) {
+int build_lut(Index* h, int nslot, const uint16_t* gword, const int* slot_query) {
   Workspace& w = h->ws;
   const int ntiles = tiles_of(nslot, h->mpad);
   const int64_t threads = (int64_t)ntiles * h->mpad * 256;
   int* tf = w.tile_fast;  // reset to 0 when gword is null (unclamped LUT)
   if (h->mpad == 4)
     k_build_lut<4><<<(unsigned)((threads + 255) / 256), 256, 0, h->stream>>>(w.q8, nslot, h->m, h->kbar, w.lut,
-                                                                             ntiles, gword, tf, h->wide);
+                                                                             ntiles, gword, tf, h->wide, slot_query);
   else
     k_build_lut<8><<<(unsigned)((threads + 255) / 256), 256, 0, h->stream>>>(w.q8, nslot, h->m, h->kbar, w.lut,
-                                                                             ntiles, gword, tf, h->wide);
+                                                                             ntiles, gword, tf, h->wide, slot_query);
   DPQ_LAUNCHED(h);
   return DPQ_OK;
 }
@@ -377,15 +381,26 @@ static int flat_first_pass(Index* h, int nb, int r2) {
   k_guard<<<(nb + 127) / 128, 128, 0, h->stream>>>(w.hist, nb, r2, lambda, exact ? 1 : 0, nullptr,
                                                     w.guard_b, w.gword, nullptr);
   DPQ_LAUNCHED(h);
-  DPQ_TRY(build_lut(h, nb, w.gword));  // 7-bit tiles where every guard <= 126
+  // query tiles ordered by guard (homogeneous tiles -> more 5-bit wide tiles)
+  const bool sorted = h->sort_slots && h->wide && h->mpad == 4 && nb > 1;
+  const uint16_t* gw_scan = sorted ? w.gword_p : w.gword;
+  const int* slot_q = sorted ? w.slot_query : nullptr;
+  auto sort_and_build = [&]() -> int {
+    if (sorted) {
+      k_sort_slots<<<1, 1024, 0, h->stream>>>(w.gword, nb, tiles * qt, w.slot_query, w.gword_p);
+      DPQ_LAUNCHED(h);
+    }
+    return build_lut(h, nb, gw_scan, slot_q);  // clamped tiles (modes 5/6/7) where the guards allow
+  };
+  DPQ_TRY(sort_and_build());
   ev_rec(h, 2);
   bool first = true;
   for (int attempt = 0; attempt < 8; ++attempt) {
     DPQ_CUDA(cudaMemsetAsync(w.emit_cnt, 0, (size_t)nb * 4, h->stream));
     EmitArgs ea;
     ea.plane = h->plane; ea.row_begin = 0; ea.row_end = n; ea.rows_per_cta = 0;
-    ea.lut = w.lut; ea.gword = w.gword; ea.tile_list = nullptr;
-    ea.slot_query = nullptr; ea.slot_probe = nullptr;
+    ea.lut = w.lut; ea.gword = gw_scan; ea.tile_list = nullptr;
+    ea.slot_query = slot_q; ea.slot_probe = nullptr;
     ea.unit_tile = nullptr; ea.unit_r0 = nullptr; ea.unit_r1 = nullptr;
     ea.emit_cnt = w.emit_cnt; ea.emit = w.emit; ea.cap = w.cap;
     DPQ_TRY(launch_emit(h, ea, tiles, n));
@@ -432,7 +447,7 @@ static int flat_first_pass(Index* h, int nb, int r2) {
       k_guard<<<(nb + 127) / 128, 128, 0, h->stream>>>(w.hist, nb, r2, 0.0, 1, w.only, w.guard_b, w.gword,
                                                         nullptr);
       DPQ_LAUNCHED(h);
-      DPQ_TRY(build_lut(h, nb, w.gword));
+      DPQ_TRY(sort_and_build());
       DPQ_CUDA(cudaStreamSynchronize(h->stream));
     }
   }
@@ -448,7 +463,7 @@ static RefineArgs make_refine_args(Index* h, int r) {
   ra.codes = h->codes; ra.code_bytes = h->code_bytes; ra.m = h->m; ra.k = h->k; ra.dsub = h->dsub;
   ra.kbar = h->kbar; ra.bbar = h->bbar;
   ra.cb = h->cb; ra.tables = w.tables; ra.y = w.y; ra.ystride = h->d;
-  ra.row_ids = nullptr; ra.id_base = h->id_base; ra.r = r;
+  ra.row_ids = h->sorted_ids; ra.id_base = h->id_base; ra.r = r;  // sorted flat rows -> ids
   ra.out_d = w.out_d; ra.out_i = w.out_i; ra.n_refined = h->d_nref;
   return ra;
 }
@@ -619,6 +634,64 @@ __global__ void k_make_plane(const void* codes, int code_bytes, int64_t n, int m
   for (int j = 0; j < mpad; ++j) plane[row * mpad + j] = b[j];
 }
 
+// Flat row order.  The index keeps its rows sorted (stably) by the low bytes
+// of subspaces 0 and 1, so runs of consecutive rows share those two 8-bit
+// table rows and the wide scan loop gathers only subspaces 2 and 3 per row.
+// sorted_ids[row] = id_base + original row (ids and (dist, id) ties are the
+// reference's); the original codes stay as the qmax prefix (first r2 rows in
+// insertion order, twopass.py:76-84).
+__global__ void k_row_keys(const void* codes, int code_bytes, int64_t n, int m, int mask, uint32_t* keys,
+                           int32_t* rows) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  keys[i] = (code_at(codes, code_bytes, i * m) & mask) | ((code_at(codes, code_bytes, i * m + 1) & mask) << 8);
+  rows[i] = (int32_t)i;
+}
+__global__ void k_gather_rows(const uint8_t* codes, int row_bytes, int64_t n, const int32_t* perm, int64_t id_base,
+                              uint8_t* out, int64_t* ids) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t src = perm[i];
+  for (int b = 0; b < row_bytes; ++b) out[i * row_bytes + b] = codes[src * row_bytes + b];
+  ids[i] = id_base + src;
+}
+
+static int sort_rows(Index* h) {
+  const int64_t n = h->n;
+  uint32_t *k0 = nullptr, *k1 = nullptr;
+  int32_t *r0 = nullptr, *r1 = nullptr;
+  uint8_t* tmp = nullptr;
+  uint8_t* sorted = nullptr;
+  size_t tbytes = 0;
+  auto cleanup = [&]() { cudaFree(k0); cudaFree(k1); cudaFree(r0); cudaFree(r1); cudaFree(tmp); };
+  int rc = DPQ_OK;
+  if ((rc = dmalloc(&k0, (size_t)n)) || (rc = dmalloc(&k1, (size_t)n)) || (rc = dmalloc(&r0, (size_t)n)) ||
+      (rc = dmalloc(&r1, (size_t)n))) { cleanup(); return rc; }
+  const unsigned blocks = (unsigned)((n + 255) / 256);
+  k_row_keys<<<blocks, 256, 0, h->stream>>>(h->codes, h->code_bytes, n, h->m, h->mask, k0, r0);
+  cub::DeviceRadixSort::SortPairs(nullptr, tbytes, k0, k1, r0, r1, (int)n, 0, 16, h->stream);
+  if ((rc = dmalloc(&tmp, tbytes))) { cleanup(); return rc; }
+  if (cub::DeviceRadixSort::SortPairs(tmp, tbytes, k0, k1, r0, r1, (int)n, 0, 16, h->stream) != cudaSuccess) {
+    cleanup(); set_error("row sort failed"); return DPQ_ERR_CUDA;
+  }
+  const int row_bytes = h->m * h->code_bytes;
+  if ((rc = dmalloc(&sorted, (size_t)n * row_bytes + 16)) || (rc = dmalloc(&h->sorted_ids, (size_t)n))) {
+    cudaFree(sorted); cleanup(); return rc;
+  }
+  k_gather_rows<<<blocks, 256, 0, h->stream>>>((const uint8_t*)h->codes, row_bytes, n, r1, h->id_base, sorted,
+                                               h->sorted_ids);
+  if (cudaStreamSynchronize(h->stream) != cudaSuccess) { cleanup(); set_error("row sort failed"); return DPQ_ERR_CUDA; }
+  cleanup();
+  if (h->prefix == h->codes) {  // original order stays as the qmax prefix
+    h->own_prefix = true;
+  } else {
+    cudaFree(h->codes);
+  }
+  h->codes = sorted;
+  h->rows_sorted = true;
+  return DPQ_OK;
+}
+
 static int make_plane(Index* h) {
   const int64_t pad_rows = ((h->n + 127) / 128) * 128 + 128;
   h->n_pad = pad_rows;
@@ -653,6 +726,8 @@ int index_common_init(Index* h, int device, int m, int k, int kbar, int dsub, co
   if (const char* e = getenv("DPQ_EXACT_LIMIT")) h->exact_limit = std::max<int64_t>(0, atoll(e));
   if (const char* e = getenv("DPQ_EMIT_CAP")) h->cap0 = std::max<int64_t>(1, atoll(e));
   if (const char* e = getenv("DPQ_SCAN_WIDE")) h->wide = atoi(e) != 0;
+  if (const char* e = getenv("DPQ_SORT_SLOTS")) h->sort_slots = atoi(e) != 0;
+  if (const char* e = getenv("DPQ_SORT_ROWS")) h->sort_rows = atoi(e) != 0;
   DPQ_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   h->own_stream = true;
   for (int i = 0; i < 8; ++i) DPQ_CUDA(cudaEventCreate(&h->ev[i]));
@@ -679,7 +754,7 @@ void index_free(Index* h) {
   Workspace& w = h->ws;
   void* dev[] = {h->cb, h->dcb, h->codes, h->plane, h->own_prefix ? h->prefix : nullptr, h->centers,
                  h->offsets, h->sorted_ids, h->d_nref, h->d_nemit, h->d_nent, h->d_nwide, w.y, w.small, w.q8, w.qmin, w.qmax, w.bounds,
-                 w.lut, w.hist, w.hist_i, w.guard_b, w.gword, w.emit_cnt, w.emit, w.bstar, w.ncand,
+                 w.lut, w.hist, w.hist_i, w.guard_b, w.gword, w.gword_p, w.emit_cnt, w.emit, w.bstar, w.ncand,
                  w.flags, w.only, w.tile_list, w.out_d, w.out_i, w.tables, w.slot_query, w.slot_probe,
                  w.slot_pre_off, w.slot_pre_len, w.counter, w.tile_fast};
   for (void* p : dev)
@@ -742,6 +817,8 @@ int dpq_flat_create(int device, int m, int k, int kbar, int dsub, const float* c
     h->prefix = h->codes;
     h->n_prefix = n;
   }
+  if (h->sort_rows && h->mpad == 4 && m >= 2 && n > 1 && n < ((int64_t)1 << 31) &&
+      (rc = sort_rows(h)) != DPQ_OK) { index_free(h); return rc; }
   if ((rc = make_plane(h)) != DPQ_OK) { index_free(h); return rc; }
   if (cudaStreamSynchronize(h->stream) != cudaSuccess) {
     set_error("index build failed"); index_free(h); return DPQ_ERR_CUDA;

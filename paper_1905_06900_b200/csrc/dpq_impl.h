@@ -34,6 +34,7 @@ struct Workspace {
   int32_t* hist_i = nullptr;  // [qb][256] (sharded exchange)
   uint16_t* guard_b = nullptr;
   uint16_t* gword = nullptr;
+  uint16_t* gword_p = nullptr;  // guard words in sorted-slot order (flat)
   uint32_t* emit_cnt = nullptr;
   uint64_t* emit = nullptr;
   int32_t* bstar = nullptr;
@@ -98,7 +99,10 @@ struct Index {
   int64_t sample = 16384;
   int64_t exact_limit = 65536;
   int64_t cap0 = 0;
-  int wide = 1;  // wide scan tiles (env DPQ_SCAN_WIDE=0 disables)
+  int wide = 1;       // wide scan tiles (env DPQ_SCAN_WIDE=0 disables)
+  int sort_slots = 1; // flat: order query tiles by guard (env DPQ_SORT_SLOTS=0)
+  int sort_rows = 1;  // flat: rows sorted by (g0, g1) at build (env DPQ_SORT_ROWS=0)
+  bool rows_sorted = false;
   Workspace ws;
   // sharded-search state between dpq_shard_* calls
   int shard_nq = 0;

@@ -226,7 +226,7 @@ template <int MPAD>
 __global__ void __launch_bounds__(256) k_build_lut(const uint8_t* __restrict__ q8, int nslot, int m, int kbar,
                                                    uint8_t* __restrict__ lut, int ntiles,
                                                    const uint16_t* __restrict__ gword, int* __restrict__ tile_fast,
-                                                   int allow_wide) {
+                                                   int allow_wide, const int* __restrict__ slot_query) {
   using G = ScanGeom<MPAD>;
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= (int64_t)ntiles * MPAD * 256) return;
@@ -258,15 +258,45 @@ __global__ void __launch_bounds__(256) k_build_lut(const uint8_t* __restrict__ q
       uint32_t v = 0;
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
-        const int q = t * G::QT + 4 * (4 * l4 + u) + b;
-        uint32_t e = (live && q < nslot) ? q8[((int64_t)q * m + j) * kbar + i] : 0u;
+        const int sl = t * G::QT + 4 * (4 * l4 + u) + b;  // slot
+        const int q = slot_query ? slot_query[sl] : sl;     // its query (-1: padding)
+        uint32_t e = (live && q >= 0 && q < nslot) ? q8[((int64_t)q * m + j) * kbar + i] : 0u;
         e = min(e, cmax);
-        if (fold) e += wide_bias(gword[q]);  // <= 31 + 128
+        if (fold) e += wide_bias(gword[sl]);  // <= 31 + 128
         v |= e << (8 * b);
       }
       w[u] = v;
     }
     dst[l4] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+// Flat batches: slots ordered by guard B (counting sort, one CTA), so each
+// query tile holds similar guards and most tiles qualify for the 5-bit wide
+// mode.  slot_query[s] = query in slot s (-1 for padding slots), gword_p[s]
+// = its guard word.  Only the scan layout changes; emit lists stay per query.
+__global__ void __launch_bounds__(1024) k_sort_slots(const uint16_t* __restrict__ gword, int nq, int nslot_pad,
+                                                      int* __restrict__ slot_query, uint16_t* __restrict__ gword_p) {
+  __shared__ int cnt[258];
+  for (int i = threadIdx.x; i < 258; i += blockDim.x) cnt[i] = 0;
+  __syncthreads();
+  auto key = [&](int q) {
+    const uint32_t gw = gword[q];
+    return gw >= 0x8000u ? (int)min(gw - 0x8000u, 255u) : 256;
+  };
+  for (int q = threadIdx.x; q < nq; q += blockDim.x) atomicAdd(&cnt[key(q) + 1], 1);
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int i = 1; i < 258; ++i) cnt[i] += cnt[i - 1];  // cnt[k] = first slot of key k
+  __syncthreads();
+  for (int q = threadIdx.x; q < nq; q += blockDim.x) {
+    const int s = atomicAdd(&cnt[key(q)], 1);
+    slot_query[s] = q;
+    gword_p[s] = gword[q];
+  }
+  for (int s = nq + threadIdx.x; s < nslot_pad; s += blockDim.x) {
+    slot_query[s] = -1;
+    gword_p[s] = 0x7F7Fu;
   }
 }
 
@@ -475,6 +505,7 @@ struct EmitArgs {
   uint32_t one;                 // = 1 (opaque to the compiler, see fma_add)
   const int* tile_fast;         // optional per-tile mode (kMode*, see k_build_lut)
   unsigned long long* n_wide;   // optional: units scanned by the wide loop
+  int runs;                     // rows sorted by (subspace 0, 1) low bytes: reuse their sums
   int n_units;                  // tiles * units_per_tile
   int units_per_tile;
 };
@@ -498,7 +529,6 @@ constexpr uint32_t kLutShared = 0x10000;  // LUT at shared address 64 KB
 template <int MPAD, int NT>
 __host__ __device__ constexpr int emit_low_bytes() { return (NT / 32) * (32 * 16 + kWarpBuf * 8); }
 constexpr int kLaneQ = 8;  // lane-private hit records per chunk (u16 each)
-constexpr int kLaneQW = 2 * kLaneQ;  // wide loop: u8 step records in the same space
 template <int MPAD, int NT>
 __host__ __device__ constexpr int emit_smem_bytes() {
   return (int)kLutShared + ScanGeom<MPAD>::LUT_BYTES + (NT / 32) * ScanGeom<MPAD>::QT * 4 +
@@ -527,7 +557,7 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
   uint64_t* hbuf = hbuf_all + warp * kWarpBuf;
   uint32_t* hcnt = hcnt_all + warp * G::QT;
   uint16_t* lq = reinterpret_cast<uint16_t*>(hcnt_all + NW * G::QT) + warp * kLaneQ * 32 + lane;
-  uint8_t* lq8 = reinterpret_cast<uint8_t*>(hcnt_all + NW * G::QT) + warp * kLaneQ * 64 + lane;  // wide loop
+  uint16_t* cq = reinterpret_cast<uint16_t*>(hcnt_all + NW * G::QT) + warp * kLaneQ * 32;  // wide drain (128)
   const uint32_t lt = (1u << lane) - 1u;
   const uint32_t one = a.one, mone = 0u - a.one;  // opaque 1 / -1 (see fma_add)
   int cur_tile = -1;
@@ -544,8 +574,12 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
       r0 = a.unit_r0[u];
       r1 = a.unit_r1[u];
     } else {
-      const int tix = u / a.units_per_tile;
-      const int64_t chunk_u = u % a.units_per_tile;
+      // tile-minor order: CTAs running at the same time cover all tiles of
+      // the same rows (plane rows re-read from L2, emit counters of every
+      // query tile shared out instead of one tile's at a time)
+      const int ntl = a.n_units / a.units_per_tile;
+      const int tix = u % ntl;
+      const int64_t chunk_u = u / ntl;
       tile = a.tile_list ? a.tile_list[tix] : tix;
       r0 = a.row_begin + chunk_u * a.rows_per_cta;
       r1 = min(a.row_end, r0 + a.rows_per_cta);
@@ -572,6 +606,7 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
     const int qd = lane >> 3, cp = lane & 7;
     const uint32_t wb0 = kLutShared | (uint32_t)(cp << 4), wb1 = wb0 + 128u;
     uint32_t cw0 = 0, cw1 = 0, cw2 = 0, cw3 = 0;  // per-query bias C, word k byte b = query 16cp+4k+b
+    uint32_t kprev = 0x10000u, bs0 = 0, bs1 = 0, bs2 = 0, bs3 = 0;  // run state (sorted rows): key, 0+1 sums
     if (wide) {
       if (a.n_wide && threadIdx.x == 0) atomicAdd(a.n_wide, 1ull);
       const uint16_t* gq = a.gword + tile * G::QT + 16 * cp;
@@ -677,10 +712,11 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
           // (4 codes per warp step, conflict-free: the 8 lanes of a quarter
           // read the 8 16-B parts of one 128-B table row).  A step with a hit
           // only appends its step index to a lane-private u8 queue.
-          auto wide_chunk = [&](auto md) {
+          auto wide_chunk = [&](auto md, auto rn) {
             constexpr int MODE = decltype(md)::value;
             const uint32_t* wsw = reinterpret_cast<const uint32_t*>(wst);
-            int lc = 0;
+            constexpr bool RUNS = decltype(rn)::value;
+            uint32_t smask = 0u;  // bit i: step i had a hit (lane-private, never overflows)
 #pragma unroll 2
             for (int i4 = 0; i4 < 8; ++i4) {
               const uint4 cv = wst[qd * 8 + i4];
@@ -688,59 +724,102 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
                 uint32_t t[4];
-                wide_sums(cws[u], wb0, wb1, one, t);
+                if constexpr (RUNS) {
+                  // sorted rows: subspace 0/1 part reloaded only when the
+                  // (g0, g1) key of the quarter's row changes
+                  const uint32_t w = cws[u];
+                  if ((w & 0xFFFFu) != kprev) {
+                    const uint4 A0 = lds128(__byte_perm(w, wb0, 0x7604u));
+                    const uint4 A1 = lds128(__byte_perm(w, wb1, 0x7614u));
+                    bs0 = A0.x + A1.x; bs1 = A0.y + A1.y; bs2 = A0.z + A1.z; bs3 = A0.w + A1.w;
+                    kprev = w & 0xFFFFu;
+                  }
+                  const uint4 A2 = lds128_hi(__byte_perm(w, wb0, 0x7624u));
+                  const uint4 A3 = lds128_hi(__byte_perm(w, wb1, 0x7634u));
+                  t[0] = bs0 + A2.x + A3.x; t[1] = bs1 + A2.y + A3.y;
+                  t[2] = bs2 + A2.z + A3.z; t[3] = bs3 + A2.w + A3.w;
+                } else {
+                  wide_sums(cws[u], wb0, wb1, one, t);
+                }
                 const uint32_t all = wide_u<MODE>(t[0], cw0, one) & wide_u<MODE>(t[1], cw1, one) &
                                      wide_u<MODE>(t[2], cw2, one) & wide_u<MODE>(t[3], cw3, one);
-                const bool h = (~all & 0x80808080u) != 0u;
-                if (h && lc < kLaneQW) lq8[lc * 32] = (uint8_t)(4 * i4 + u);
-                lc += h ? 1 : 0;
+                smask |= (uint32_t)((~all & 0x80808080u) != 0u) << (4 * i4 + u);
               }
             }
-            if (!__any_sync(0xffffffffu, lc > 0)) return;
-            // drain: recompute the recorded steps, stage their hits
-            auto emit_step = [&](bool has, int i) {
-              uint32_t hm = 0u, t[4] = {0u, 0u, 0u, 0u};
-              const uint32_t r = 32u * (uint32_t)qd + (uint32_t)i;
-              if (has) {
-                wide_sums(wsw[32 * qd + i], wb0, wb1, one, t);
-                const uint32_t cwk[4] = {cw0, cw1, cw2, cw3};
+            if (!__any_sync(0xffffffffu, smask != 0u)) return;
+            // Drain: the warp's (lane, step) records are compacted (up to 4
+            // per lane per pass, <= 128 per pass) and spread over the lanes;
+            // each recomputes its step's sums for the recording lane's 16
+            // queries and stages the hits.
+            const uint32_t cwk[4] = {cw0, cw1, cw2, cw3};
+            for (;;) {
+              uint32_t sel = 0u, rest = smask;
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                  const uint32_t hb = ~wide_u<MODE>(t[k], cwk[k], one) & 0x80808080u;
-                  hm |= (((hb >> 7) & 1u) | ((hb >> 14) & 2u) | ((hb >> 21) & 4u) | ((hb >> 28) & 8u)) << (4 * k);
-                }
-                if (edge && !(r >= lo && r < hi)) hm = 0u;
+              for (int k = 0; k < 4; ++k) { const uint32_t bit = rest & (0u - rest); sel |= bit; rest ^= bit; }
+              const int nsel = __popc(sel);
+              int off = nsel;  // inclusive scan over lanes
+#pragma unroll
+              for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, off, o);
+                if (lane >= o) off += v;
               }
-              for (;;) {
-                const bool hh = hm != 0u;
-                const uint32_t bal = __ballot_sync(0xffffffffu, hh);
-                if (!bal) break;
-                if (wc + 32 > kWarpBuf) flush();
-                if (hh) {
-                  const int b = __ffs(hm) - 1;
-                  hm &= hm - 1u;
-                  const int k = b >> 2, sh = 8 * (b & 3);
-                  const uint32_t tw = k == 0 ? t[0] : (k == 1 ? t[1] : (k == 2 ? t[2] : t[3]));
-                  uint32_t sc = (tw >> sh) & 0xFFu;
-                  if (MODE == kModeWide5) {
-                    const uint32_t ck = k == 0 ? cw0 : (k == 1 ? cw1 : (k == 2 ? cw2 : cw3));
-                    sc -= (ck >> sh) & 0xFFu;
+              const int total = __shfl_sync(0xffffffffu, off, 31);
+              if (total == 0) break;
+              off -= nsel;
+              for (uint32_t tt = sel; tt; tt &= tt - 1u) cq[off++] = (uint16_t)((lane << 5) | (__ffs(tt) - 1));
+              smask = rest;
+              __syncwarp();
+              for (int base = 0; base < total; base += 32) {
+                const bool has = base + lane < total;
+                const uint32_t rec = has ? cq[base + lane] : 0u;
+                const int src = (int)(rec >> 5), i = (int)(rec & 31u);
+                const int sq = src >> 3, sp = src & 7;
+                uint32_t c4[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) c4[k] = __shfl_sync(0xffffffffu, cwk[k], src);
+                uint32_t hm = 0u, t[4] = {0u, 0u, 0u, 0u};
+                const uint32_t r = 32u * (uint32_t)sq + (uint32_t)i;
+                if (has) {
+                  const uint32_t sb0 = kLutShared | (uint32_t)(sp << 4);
+                  wide_sums(wsw[32 * sq + i], sb0, sb0 + 128u, one, t);
+#pragma unroll
+                  for (int k = 0; k < 4; ++k) {
+                    const uint32_t hb = ~wide_u<MODE>(t[k], c4[k], one) & 0x80808080u;
+                    hm |= (((hb >> 7) & 1u) | ((hb >> 14) & 2u) | ((hb >> 21) & 4u) | ((hb >> 28) & 8u)) << (4 * k);
                   }
-                  hbuf[wc + __popc(bal & lt)] =
-                      (uint64_t)(rboff + r) | ((uint64_t)(16 * cp + b) << 32) | ((uint64_t)sc << 40);
+                  if (edge && !(r >= lo && r < hi)) hm = 0u;
                 }
-                wc += __popc(bal);
+                for (;;) {
+                  const bool hh = hm != 0u;
+                  const uint32_t bal = __ballot_sync(0xffffffffu, hh);
+                  if (!bal) break;
+                  if (wc + 32 > kWarpBuf) flush();
+                  if (hh) {
+                    const int b = __ffs(hm) - 1;
+                    hm &= hm - 1u;
+                    const int k = b >> 2, sh = 8 * (b & 3);
+                    const uint32_t tw = k == 0 ? t[0] : (k == 1 ? t[1] : (k == 2 ? t[2] : t[3]));
+                    uint32_t sc = (tw >> sh) & 0xFFu;
+                    if (MODE == kModeWide5) {
+                      const uint32_t ck = k == 0 ? c4[0] : (k == 1 ? c4[1] : (k == 2 ? c4[2] : c4[3]));
+                      sc -= (ck >> sh) & 0xFFu;
+                    }
+                    hbuf[wc + __popc(bal & lt)] =
+                        (uint64_t)(rboff + r) | ((uint64_t)(16 * sp + b) << 32) | ((uint64_t)sc << 40);
+                  }
+                  wc += __popc(bal);
+                }
               }
-            };
-            if (__any_sync(0xffffffffu, lc > kLaneQW)) {
-              for (int i = 0; i < 32; ++i) emit_step(true, i);  // a queue overflowed: every step
-            } else {
-              const int maxc = (int)__reduce_max_sync(0xffffffffu, (unsigned)lc);
-              for (int e = 0; e < maxc; ++e) emit_step(e < lc, e < lc ? (int)lq8[e * 32] : 0);
+              __syncwarp();
             }
           };
-          if (tmode == kModeWide5) wide_chunk(std::integral_constant<int, kModeWide5>());
-          else wide_chunk(std::integral_constant<int, kModeWide6>());
+          if (a.runs) {
+            if (tmode == kModeWide5) wide_chunk(std::integral_constant<int, kModeWide5>(), std::true_type());
+            else wide_chunk(std::integral_constant<int, kModeWide6>(), std::true_type());
+          } else {
+            if (tmode == kModeWide5) wide_chunk(std::integral_constant<int, kModeWide5>(), std::false_type());
+            else wide_chunk(std::integral_constant<int, kModeWide6>(), std::false_type());
+          }
           continue;
         }
       }
@@ -1101,6 +1180,9 @@ __global__ void __launch_bounds__(NT) k_refine_topk(RefineArgs a) {
   unsigned my_ref = 0;
   const float* tq = a.tables ? a.tables + (int64_t)q * a.m * a.k : nullptr;
   // candidate -> (key, id); false when it is not a candidate (score > b*)
+  // row -> id (sorted flat rows / ivf lists: row_ids), looked up only for a
+  // candidate that ties the threshold distance or enters the buffer
+  auto id_of = [&](int64_t row) -> int64_t { return a.row_ids ? a.row_ids[row] : a.id_base + row; };
   auto eval = [&](int64_t idx, uint64_t& key, int64_t& id) -> bool {
     int64_t row;
     uint32_t probe = 0;
@@ -1136,7 +1218,7 @@ __global__ void __launch_bounds__(NT) k_refine_topk(RefineArgs a) {
       }
     }
     key = (uint64_t)__double_as_longlong(dist);
-    id = a.row_ids ? a.row_ids[row] : a.id_base + row;
+    id = row;  // (a row until id_of)
     return true;
   };
   constexpr int U = 1;  // candidates per thread per round (U > 1 measured slower: bigger buffer, lower occupancy)
@@ -1147,7 +1229,11 @@ __global__ void __launch_bounds__(NT) k_refine_topk(RefineArgs a) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t idx = base + (int64_t)u * NT + threadIdx.x;
-      keep[u] = idx < ntot && eval(idx, key[u], id[u]) && pair_less(key[u], id[u], thr_k, thr_i);
+      keep[u] = idx < ntot && eval(idx, key[u], id[u]) && key[u] <= thr_k;
+      if (keep[u]) {
+        id[u] = id_of(id[u]);
+        keep[u] = pair_less(key[u], id[u], thr_k, thr_i);
+      }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {

@@ -270,3 +270,40 @@ def test_wide_tiles_mixed_guards_and_padding():
         d0, i0 = _oracle(cb, der, codes, Y[:nq], 10, r2)
         d1, i1 = idx.search(Y[:nq], 10, mode="derived", r2=r2)
         assert np.array_equal(i0, i1) and _same(d0, d1), (nq, r2)
+
+
+def test_guard_sorted_slots_match_unsorted(monkeypatch):
+    """Query tiles ordered by guard (flat batches) give the same results as
+    the identity slot order, including a partial last tile."""
+    cb, der, codes, Y = _sift_setup(120_000, 200, seed=13)
+    idx = FlatIndex.from_arrays(cb, der, codes)
+    d1, i1 = idx.search(Y, 15, mode="derived", r2=300)
+    monkeypatch.setenv("DPQ_SORT_SLOTS", "0")
+    idx2 = FlatIndex.from_arrays(cb, der, codes)
+    d2, i2 = idx2.search(Y, 15, mode="derived", r2=300)
+    assert np.array_equal(i1, i2) and _same(d1, d2)
+    d0, i0 = _oracle(cb, der, codes, Y[:40], 15, 300)
+    assert np.array_equal(i0, i1[:40]) and _same(d0, d1[:40])
+
+
+def test_sorted_rows_ties_and_ids(monkeypatch):
+    """The flat index stores rows sorted by (g0, g1); ids, (dist, id) tie
+    order, the qmax prefix (first r2 rows in insertion order) and the
+    conventional path are unchanged.  Duplicated rows force exact ties."""
+    cb, der, codes, Y = _sift_setup(60_000, 12, seed=14)
+    rng = np.random.default_rng(14)
+    codes[rng.choice(60_000, 20_000, replace=False)] = codes[rng.integers(0, 500, 20_000)]
+    d0, i0 = _oracle(cb, der, codes, Y, 40, 500)
+    idx = FlatIndex.from_arrays(cb, der, codes)
+    d1, i1 = idx.search(Y, 40, mode="derived", r2=500)
+    assert np.array_equal(i0, i1) and _same(d0, d1)
+    dc, ic = idx.search(Y[:3], 40)
+    monkeypatch.setenv("DPQ_SORT_ROWS", "0")
+    idx2 = FlatIndex.from_arrays(cb, der, codes)
+    d2, i2 = idx2.search(Y, 40, mode="derived", r2=500)
+    assert np.array_equal(i2, i1) and _same(d2, d1)
+    dc2, ic2 = idx2.search(Y[:3], 40)
+    assert np.array_equal(ic, ic2) and _same(dc, dc2)
+    b1, n1 = idx.candidate_counts(Y, 500)
+    b2, n2 = idx2.candidate_counts(Y, 500)
+    assert np.array_equal(b1, b2) and np.array_equal(n1, n2)
