@@ -249,6 +249,16 @@ static int launch_emit_t(Index* h, EmitArgs ea, int ntiles, int64_t rows) {
     DPQ_LAUNCHED(h);
     return DPQ_OK;
   }
+  if (ea.chunk_list) {  // run-filtered chunk lists: fixed slices per tile (lengths on the device)
+    const int upt = std::max(1, (4 * sms + ntiles - 1) / ntiles);
+    ea.units_per_tile = upt;
+    ea.n_units = upt * ntiles;
+    ea.rows_per_cta = 0;
+    DPQ_CUDA(cudaMemsetAsync(h->ws.counter, 0, sizeof(unsigned), h->stream));
+    k_scan_emit<MPAD, kEmitThreads><<<std::min(sms, ea.n_units), kEmitThreads, smem, h->stream>>>(ea);
+    DPQ_LAUNCHED(h);
+    return DPQ_OK;
+  }
   const int64_t min_rows = (int64_t)G::CHUNK_ROWS * NW;
   int64_t upt = std::max<int64_t>(1, (8LL * sms + ntiles - 1) / ntiles);  // ~8 units per CTA
   int64_t per = (rows + upt - 1) / upt;
@@ -383,14 +393,33 @@ static int flat_first_pass(Index* h, int nb, int r2) {
   DPQ_LAUNCHED(h);
   // query tiles ordered by guard (homogeneous tiles -> more 5-bit wide tiles)
   const bool sorted = h->sort_slots && h->wide && h->mpad == 4 && nb > 1;
+  const bool use_list = h->rows_sorted && h->run_filter && h->m >= 2 && h->mpad == 4;
+  if (use_list && (w.list_tiles < tiles || w.list_chunks < h->n_chunks)) {
+    DPQ_TRY(dmalloc(&w.pot, (size_t)tiles * 65536));
+    DPQ_TRY(dmalloc(&w.chunk_list, (size_t)tiles * h->n_chunks));
+    DPQ_TRY(dmalloc(&w.list_len, (size_t)tiles));
+    w.list_tiles = tiles;
+    w.list_chunks = h->n_chunks;
+  }
   const uint16_t* gw_scan = sorted ? w.gword_p : w.gword;
   const int* slot_q = sorted ? w.slot_query : nullptr;
   auto sort_and_build = [&]() -> int {
     if (sorted) {
-      k_sort_slots<<<1, 1024, 0, h->stream>>>(w.gword, nb, tiles * qt, w.slot_query, w.gword_p);
+      k_sort_slots<<<1, 1024, 0, h->stream>>>(w.gword, w.q8, h->m, h->kbar, nb, tiles * qt, w.slot_query,
+                                              w.gword_p);
       DPQ_LAUNCHED(h);
     }
-    return build_lut(h, nb, gw_scan, slot_q);  // clamped tiles (modes 5/6/7) where the guards allow
+    DPQ_TRY(build_lut(h, nb, gw_scan, slot_q));  // clamped tiles (modes 5/6/7) where the guards allow
+    if (use_list) {  // run filter: per tile, the chunks whose (g0, g1) keys can reach a guard
+      DPQ_CUDA(cudaMemsetAsync(w.list_len, 0, (size_t)tiles * 4, h->stream));
+      k_run_potential<<<dim3(64, tiles), 256, (size_t)qt * 64 * 4 + 4 * qt * 4, h->stream>>>(
+          w.q8, h->m, h->kbar, slot_q, gw_scan, qt, nb, w.pot);
+      DPQ_LAUNCHED(h);
+      k_chunk_list<<<dim3((unsigned)((h->n_chunks + 255) / 256), tiles), 256, 0, h->stream>>>(
+          h->chunk_keys, (int)h->n_chunks, w.pot, w.chunk_list, w.list_len, h->n, nb, qt, h->d_nrows);
+      DPQ_LAUNCHED(h);
+    }
+    return DPQ_OK;
   };
   DPQ_TRY(sort_and_build());
   ev_rec(h, 2);
@@ -401,10 +430,11 @@ static int flat_first_pass(Index* h, int nb, int r2) {
     ea.plane = h->plane; ea.row_begin = 0; ea.row_end = n; ea.rows_per_cta = 0;
     ea.lut = w.lut; ea.gword = gw_scan; ea.tile_list = nullptr;
     ea.slot_query = slot_q; ea.slot_probe = nullptr;
+    ea.chunk_list = use_list ? w.chunk_list : nullptr; ea.list_len = w.list_len; ea.list_stride = h->n_chunks;
     ea.unit_tile = nullptr; ea.unit_r0 = nullptr; ea.unit_r1 = nullptr;
     ea.emit_cnt = w.emit_cnt; ea.emit = w.emit; ea.cap = w.cap;
     DPQ_TRY(launch_emit(h, ea, tiles, n));
-    h->counters[2] += (int64_t)nb * n;
+    if (!use_list) h->counters[2] += (int64_t)nb * n;  // (list mode: counted on the device)
     if (first) ev_rec(h, 3);
     k_threshold<256><<<nb, 256, 0, h->stream>>>(w.emit, w.emit_cnt, w.cap, w.guard_b, r2, nullptr,
                                                 w.bstar, w.ncand, w.flags, nullptr, h->d_nemit);
@@ -644,8 +674,15 @@ __global__ void k_row_keys(const void* codes, int code_bytes, int64_t n, int m, 
                            int32_t* rows) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  keys[i] = (code_at(codes, code_bytes, i * m) & mask) | ((code_at(codes, code_bytes, i * m + 1) & mask) << 8);
+  keys[i] = ((code_at(codes, code_bytes, i * m) & mask) << 8) | (code_at(codes, code_bytes, i * m + 1) & mask);
   rows[i] = (int32_t)i;
+}
+// key range [first row, last row] of every 128-row chunk (rows sorted by key)
+__global__ void k_chunk_keys(const uint32_t* skeys, int64_t n, int64_t nchunks, uint32_t* chunk_keys) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nchunks) return;
+  const int64_t a = c * 128, b = std::min<int64_t>(a + 127, n - 1);
+  chunk_keys[c] = skeys[a] | (skeys[b] << 16);
 }
 __global__ void k_gather_rows(const uint8_t* codes, int row_bytes, int64_t n, const int32_t* perm, int64_t id_base,
                               uint8_t* out, int64_t* ids) {
@@ -680,6 +717,9 @@ static int sort_rows(Index* h) {
   }
   k_gather_rows<<<blocks, 256, 0, h->stream>>>((const uint8_t*)h->codes, row_bytes, n, r1, h->id_base, sorted,
                                                h->sorted_ids);
+  h->n_chunks = (n + 127) / 128;
+  if ((rc = dmalloc(&h->chunk_keys, (size_t)h->n_chunks))) { cudaFree(sorted); cleanup(); return rc; }
+  k_chunk_keys<<<(unsigned)((h->n_chunks + 255) / 256), 256, 0, h->stream>>>(k1, n, h->n_chunks, h->chunk_keys);
   if (cudaStreamSynchronize(h->stream) != cudaSuccess) { cleanup(); set_error("row sort failed"); return DPQ_ERR_CUDA; }
   cleanup();
   if (h->prefix == h->codes) {  // original order stays as the qmax prefix
@@ -728,6 +768,7 @@ int index_common_init(Index* h, int device, int m, int k, int kbar, int dsub, co
   if (const char* e = getenv("DPQ_SCAN_WIDE")) h->wide = atoi(e) != 0;
   if (const char* e = getenv("DPQ_SORT_SLOTS")) h->sort_slots = atoi(e) != 0;
   if (const char* e = getenv("DPQ_SORT_ROWS")) h->sort_rows = atoi(e) != 0;
+  if (const char* e = getenv("DPQ_RUN_FILTER")) h->run_filter = atoi(e) != 0;
   DPQ_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   h->own_stream = true;
   for (int i = 0; i < 8; ++i) DPQ_CUDA(cudaEventCreate(&h->ev[i]));
@@ -737,6 +778,8 @@ int index_common_init(Index* h, int device, int m, int k, int kbar, int dsub, co
   DPQ_TRY(dmalloc(&h->d_nemit, 1));
   DPQ_TRY(dmalloc(&h->d_nent, 1));
   DPQ_TRY(dmalloc(&h->d_nwide, 1));
+  DPQ_TRY(dmalloc(&h->d_nrows, 1));
+  DPQ_CUDA(cudaMemset(h->d_nrows, 0, 8));
   DPQ_CUDA(cudaMemset(h->d_nent, 0, 8));
   DPQ_CUDA(cudaMemset(h->d_nwide, 0, 8));
   DPQ_CUDA(cudaMemcpy(h->cb, codebooks, (size_t)m * k * dsub * 4, cudaMemcpyHostToDevice));
@@ -753,7 +796,7 @@ void index_free(Index* h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   Workspace& w = h->ws;
   void* dev[] = {h->cb, h->dcb, h->codes, h->plane, h->own_prefix ? h->prefix : nullptr, h->centers,
-                 h->offsets, h->sorted_ids, h->d_nref, h->d_nemit, h->d_nent, h->d_nwide, w.y, w.small, w.q8, w.qmin, w.qmax, w.bounds,
+                 h->offsets, h->sorted_ids, h->d_nref, h->d_nemit, h->d_nent, h->d_nwide, h->d_nrows, h->chunk_keys, w.pot, w.chunk_list, w.list_len, w.y, w.small, w.q8, w.qmin, w.qmax, w.bounds,
                  w.lut, w.hist, w.hist_i, w.guard_b, w.gword, w.gword_p, w.emit_cnt, w.emit, w.bstar, w.ncand,
                  w.flags, w.only, w.tile_list, w.out_d, w.out_i, w.tables, w.slot_query, w.slot_probe,
                  w.slot_pre_off, w.slot_pre_len, w.counter, w.tile_fast};
@@ -994,17 +1037,19 @@ int dpq_last_phase_ms(dpq_index_t* index, float* ms7) {
 int dpq_counters(dpq_index_t* index, int64_t* out8) {
   Index* h = reinterpret_cast<Index*>(index);
   if (!h || !out8) { set_error("null argument"); return DPQ_ERR_ARG; }
-  unsigned long long nref = 0, nemit = 0, nent = 0, nwide = 0;
+  unsigned long long nref = 0, nemit = 0, nent = 0, nwide = 0, nrows = 0;
   cudaSetDevice(h->device);
   DPQ_CUDA(cudaMemcpy(&nref, h->d_nref, 8, cudaMemcpyDeviceToHost));
   DPQ_CUDA(cudaMemcpy(&nemit, h->d_nemit, 8, cudaMemcpyDeviceToHost));
   DPQ_CUDA(cudaMemcpy(&nent, h->d_nent, 8, cudaMemcpyDeviceToHost));
   DPQ_CUDA(cudaMemcpy(&nwide, h->d_nwide, 8, cudaMemcpyDeviceToHost));
+  DPQ_CUDA(cudaMemcpy(&nrows, h->d_nrows, 8, cudaMemcpyDeviceToHost));
   h->counters[3] = (int64_t)nref;
   h->counters[5] = (int64_t)nemit;
   h->counters[6] = (int64_t)nent;
   h->counters[7] = (int64_t)nwide;
   for (int i = 0; i < 8; ++i) out8[i] = h->counters[i];
+  out8[2] += (int64_t)nrows;
   return DPQ_OK;
 }
 

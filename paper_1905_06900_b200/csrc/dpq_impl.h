@@ -35,6 +35,11 @@ struct Workspace {
   uint16_t* guard_b = nullptr;
   uint16_t* gword = nullptr;
   uint16_t* gword_p = nullptr;  // guard words in sorted-slot order (flat)
+  uint8_t* pot = nullptr;       // run filter: [tiles][65536] key has potential
+  int* chunk_list = nullptr;    // [tiles][n_chunks] chunks to scan
+  int* list_len = nullptr;      // [tiles]
+  int list_tiles = 0;
+  int64_t list_chunks = 0;
   uint32_t* emit_cnt = nullptr;
   uint64_t* emit = nullptr;
   int32_t* bstar = nullptr;
@@ -93,6 +98,7 @@ struct Index {
   unsigned long long* d_nemit = nullptr;
   unsigned long long* d_nent = nullptr;   // lazily computed table entries
   unsigned long long* d_nwide = nullptr;  // scan units run by the wide loop
+  unsigned long long* d_nrows = nullptr;  // query-rows scanned in run-filtered (list) mode
   size_t emit_budget = (size_t)16 << 30;  // bytes for emit buffers
   // guard sampling (env DPQ_GUARD_SAMPLE / DPQ_EXACT_LIMIT / DPQ_EMIT_CAP
   // override them so tests can force the exact-redo and overflow paths)
@@ -103,6 +109,9 @@ struct Index {
   int sort_slots = 1; // flat: order query tiles by guard (env DPQ_SORT_SLOTS=0)
   int sort_rows = 1;  // flat: rows sorted by (g0, g1) at build (env DPQ_SORT_ROWS=0)
   bool rows_sorted = false;
+  int run_filter = 1;  // flat sorted rows: scan only chunks whose keys can reach a guard (env DPQ_RUN_FILTER=0)
+  uint32_t* chunk_keys = nullptr;  // [n_chunks] first | last key << 16 of each 128-row chunk
+  int64_t n_chunks = 0;
   Workspace ws;
   // sharded-search state between dpq_shard_* calls
   int shard_nq = 0;

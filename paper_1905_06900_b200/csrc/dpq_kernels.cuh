@@ -271,33 +271,148 @@ __global__ void __launch_bounds__(256) k_build_lut(const uint8_t* __restrict__ q
   }
 }
 
-// Flat batches: slots ordered by guard B (counting sort, one CTA), so each
-// query tile holds similar guards and most tiles qualify for the 5-bit wide
-// mode.  slot_query[s] = query in slot s (-1 for padding slots), gword_p[s]
-// = its guard word.  Only the scan layout changes; emit lists stay per query.
-__global__ void __launch_bounds__(1024) k_sort_slots(const uint16_t* __restrict__ gword, int nq, int nslot_pad,
+// Flat batches: query slots ordered so each query tile holds similar
+// queries.  With q8 (and nq <= kSortMax) the key is (guard class, g0*, g1*):
+// class 0/1/2/3 = B <= 30 / <= 62 / larger / no guard (tile modes 5/6/7),
+// g*_j = the derived group nearest to the query in subspace j (first argmin
+// of its 8-bit table).  Clustered tiles make the per-tile run filter
+// (k_run_potential) skip most rows; otherwise slots are counting-sorted by B.
+// slot_query[s] = query in slot s (-1: padding), gword_p[s] = its guard word.
+// Only the scan layout changes; emit lists stay per query.
+constexpr int kSortMax = 4096;
+__global__ void __launch_bounds__(1024) k_sort_slots(const uint16_t* __restrict__ gword, const uint8_t* __restrict__ q8,
+                                                      int m, int kbar, int nq, int nslot_pad,
                                                       int* __restrict__ slot_query, uint16_t* __restrict__ gword_p) {
+  __shared__ uint64_t kv[kSortMax];
   __shared__ int cnt[258];
-  for (int i = threadIdx.x; i < 258; i += blockDim.x) cnt[i] = 0;
-  __syncthreads();
-  auto key = [&](int q) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  auto gkey = [&](int q) {
     const uint32_t gw = gword[q];
     return gw >= 0x8000u ? (int)min(gw - 0x8000u, 255u) : 256;
   };
-  for (int q = threadIdx.x; q < nq; q += blockDim.x) atomicAdd(&cnt[key(q) + 1], 1);
-  __syncthreads();
-  if (threadIdx.x == 0)
-    for (int i = 1; i < 258; ++i) cnt[i] += cnt[i - 1];  // cnt[k] = first slot of key k
-  __syncthreads();
-  for (int q = threadIdx.x; q < nq; q += blockDim.x) {
-    const int s = atomicAdd(&cnt[key(q)], 1);
-    slot_query[s] = q;
-    gword_p[s] = gword[q];
+  if (q8 && nq <= kSortMax && m >= 2) {
+    int P = 1;
+    while (P < nq) P <<= 1;
+    for (int q = warp; q < P; q += 32) {
+      if (q >= nq) { if (lane == 0) kv[q] = ~0ull; continue; }
+      uint32_t best[2];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        uint32_t b = 0xFFFFFFFFu;  // (value << 16) | index, first argmin
+        for (int g = lane; g < kbar; g += 32) b = min(b, ((uint32_t)q8[((int64_t)q * m + j) * kbar + g] << 16) | (uint32_t)g);
+        best[j] = __reduce_min_sync(0xffffffffu, b) & 0xFFFFu;
+      }
+      if (lane == 0) {
+        const int B = gkey(q);
+        const uint32_t cls = B == 256 ? 3u : (B <= 30 ? 0u : (B <= 62 ? 1u : 2u));
+        kv[q] = ((uint64_t)((cls << 16) | (best[0] << 8) | best[1]) << 32) | (uint32_t)q;
+      }
+    }
+    __syncthreads();
+    for (int size = 2; size <= P; size <<= 1) {
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int t = tid; t < P / 2; t += blockDim.x) {
+          const int i = 2 * t - (t & (stride - 1)), j = i + stride;
+          const bool asc = (i & size) == 0;
+          const uint64_t x = kv[i], y = kv[j];
+          if ((x > y) == asc) { kv[i] = y; kv[j] = x; }
+        }
+        __syncthreads();
+      }
+    }
+    for (int sl = tid; sl < nq; sl += blockDim.x) {
+      const int q = (int)(kv[sl] & 0xFFFFFFFFu);
+      slot_query[sl] = q;
+      gword_p[sl] = gword[q];
+    }
+  } else {
+    for (int i = tid; i < 258; i += blockDim.x) cnt[i] = 0;
+    __syncthreads();
+    for (int q = tid; q < nq; q += blockDim.x) atomicAdd(&cnt[gkey(q) + 1], 1);
+    __syncthreads();
+    if (tid == 0)
+      for (int i = 1; i < 258; ++i) cnt[i] += cnt[i - 1];  // cnt[k] = first slot of key k
+    __syncthreads();
+    for (int q = tid; q < nq; q += blockDim.x) {
+      const int sl = atomicAdd(&cnt[gkey(q)], 1);
+      slot_query[sl] = q;
+      gword_p[sl] = gword[q];
+    }
   }
-  for (int s = nq + threadIdx.x; s < nslot_pad; s += blockDim.x) {
-    slot_query[s] = -1;
-    gword_p[s] = 0x7F7Fu;
+  for (int sl = nq + tid; sl < nslot_pad; sl += blockDim.x) {
+    slot_query[sl] = -1;
+    gword_p[sl] = 0x7F7Fu;
   }
+}
+
+// Run filter for indexes whose rows are sorted by key = g0 << 8 | g1 (low
+// bytes of subspaces 0 and 1).  Every entry is >= 0, so a row of key
+// (g0, g1) can only reach a query's guard B if e0[g0] + e1[g1] <= B.
+//   k_run_potential: pot[tile][key] = 1 iff some slot of the tile passes
+//     (grid: 64 x tiles, 4 values of g0 per CTA, 4 of g1 per thread)
+//   k_chunk_list: per tile, the 128-row chunks whose key range holds a key
+//     with pot = 1 (unordered list + length); the scan visits only those.
+// Skipped rows have score > B, so they would never be emitted: exact.
+__global__ void __launch_bounds__(256) k_run_potential(const uint8_t* __restrict__ q8, int m, int kbar,
+                                                       const int* __restrict__ slot_query,
+                                                       const uint16_t* __restrict__ gword, int qt, int nq,
+                                                       uint8_t* __restrict__ pot) {
+  extern __shared__ __align__(16) uint32_t bw[];  // [qt][64] words: 4 x min(e1, 127)
+  uint32_t* c4 = bw + qt * 64;                    // [4][qt] bias words
+  const int tile = blockIdx.y, tid = threadIdx.x;
+  for (int i = tid; i < qt * 64; i += 256) {
+    const int sl = i >> 6, g = (i & 63) * 4;
+    const int q = slot_query ? slot_query[tile * qt + sl] : tile * qt + sl;
+    uint32_t w = 0;
+    if (q >= 0 && q < nq)
+      for (int b = 0; b < 4; ++b)
+        w |= (g + b < kbar ? min((uint32_t)q8[((int64_t)q * m + 1) * kbar + g + b], 127u) : 127u) << (8 * b);
+    bw[i] = w;
+  }
+  for (int i = tid; i < 4 * qt; i += 256) {
+    const int gi = i / qt, sl = i % qt, g0 = blockIdx.x * 4 + gi;
+    const int q = slot_query ? slot_query[tile * qt + sl] : tile * qt + sl;
+    const uint32_t gw = gword[tile * qt + sl];
+    uint32_t c = 0x80808080u;  // never
+    if (q >= 0 && q < nq && gw >= 0x8000u && g0 < kbar) {
+      const int D = (int)(gw - 0x8000u) - (int)q8[(int64_t)q * m * kbar + g0];  // e1 must be <= D
+      if (D >= 127) c = 0u;  // any (clamped, <= 127) e1 passes
+      else if (D >= 0) c = (uint32_t)(127 - D) * 0x01010101u;
+    }
+    c4[i] = c;
+  }
+  __syncthreads();
+  const int gi = tid >> 6, t = tid & 63, g0 = blockIdx.x * 4 + gi;
+  uint32_t acc = 0xFFFFFFFFu;
+  for (int sl = 0; sl < qt; ++sl) {
+    const uint32_t b = bw[sl * 64 + t], c = c4[gi * qt + sl];
+    acc &= b | ((b & 0x7F7F7F7Fu) + c);  // bit 7 clear: e1 <= D for this slot
+  }
+  // byte b of the word = key (g0, 4t + b) has potential
+  if (g0 < kbar) reinterpret_cast<uint32_t*>(pot + (int64_t)tile * 65536 + g0 * 256)[t] = (~acc & 0x80808080u) >> 7;
+}
+
+__global__ void __launch_bounds__(256) k_chunk_list(const uint32_t* __restrict__ chunk_keys, int nchunks,
+                                                    const uint8_t* __restrict__ pot, int* __restrict__ list,
+                                                    int* __restrict__ list_len, int64_t n, int nb, int qt,
+                                                    unsigned long long* __restrict__ n_rows) {
+  const int tile = blockIdx.y, lane = threadIdx.x & 31;
+  const int c = blockIdx.x * 256 + threadIdx.x;
+  bool f = false;
+  if (c < nchunks) {
+    const uint32_t kk = chunk_keys[c];
+    const uint8_t* p = pot + (int64_t)tile * 65536;
+    for (uint32_t k = kk & 0xFFFFu; k <= (kk >> 16) && !f; ++k) f = p[k] != 0;
+  }
+  const uint32_t bal = __ballot_sync(0xffffffffu, f);
+  int base = 0;
+  if (lane == 0 && bal) base = atomicAdd(list_len + tile, __popc(bal));
+  if (n_rows && f) {  // query-rows this tile will scan (its real queries x listed rows)
+    const int64_t rows = min((int64_t)128, n - (int64_t)c * 128);
+    atomicAdd(n_rows, (unsigned long long)(rows * min(qt, nb - tile * qt)));
+  }
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (f) list[(int64_t)tile * nchunks + base + __popc(bal & ((1u << lane) - 1u))] = c;
 }
 
 // ============================================================================
@@ -503,9 +618,12 @@ struct EmitArgs {
   const int64_t* unit_r0;       // optional per-unit row range (ivf)
   const int64_t* unit_r1;
   uint32_t one;                 // = 1 (opaque to the compiler, see fma_add)
-  const int* tile_fast;         // optional per-tile mode (kMode*, see k_build_lut)
-  unsigned long long* n_wide;   // optional: units scanned by the wide loop
-  int runs;                     // rows sorted by (subspace 0, 1) low bytes: reuse their sums
+  const int* tile_fast = nullptr;  // optional per-tile mode (kMode*, see k_build_lut)
+  unsigned long long* n_wide = nullptr;  // optional: units scanned by the wide loop
+  int runs = 0;                 // rows sorted by (subspace 0, 1) low bytes: reuse their sums
+  const int* chunk_list = nullptr;  // optional per-tile lists of 128-row chunks to scan (run filter)
+  const int* list_len = nullptr;    //   [tiles] list lengths (device); list of tile t at t * list_stride
+  int64_t list_stride = 0;
   int n_units;                  // tiles * units_per_tile
   int units_per_tile;
 };
@@ -581,8 +699,14 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
       const int tix = u % ntl;
       const int64_t chunk_u = u / ntl;
       tile = a.tile_list ? a.tile_list[tix] : tix;
-      r0 = a.row_begin + chunk_u * a.rows_per_cta;
-      r1 = min(a.row_end, r0 + a.rows_per_cta);
+      if (a.chunk_list) {  // unit = a slice of the tile's chunk list
+        const int64_t len = a.list_len[tile];
+        r0 = chunk_u * len / a.units_per_tile;
+        r1 = (chunk_u + 1) * len / a.units_per_tile;
+      } else {
+        r0 = a.row_begin + chunk_u * a.rows_per_cta;
+        r1 = min(a.row_end, r0 + a.rows_per_cta);
+      }
     }
     if (tile != cur_tile) {
       // every warp is past the previous unit (barrier above): one thread
@@ -621,13 +745,19 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
     // Logical range [r0, r1); loads start at the 512-B aligned row r0a and
     // rows outside the range are never emitted.
     if (r0 >= r1) continue;
-    const int64_t r0a = r0 & ~(int64_t)(G::CHUNK_ROWS - 1);
-    const int64_t nchunks = (r1 - r0a + G::CHUNK_ROWS - 1) / G::CHUNK_ROWS;
+    // list mode: [r0, r1) indexes the tile's chunk list, rows are absolute
+    const int* clist = a.chunk_list ? a.chunk_list + tile * a.list_stride + r0 : nullptr;
+    const int64_t r0a = clist ? 0 : (r0 & ~(int64_t)(G::CHUNK_ROWS - 1));
+    const int64_t nchunks = clist ? r1 - r0 : (r1 - r0a + G::CHUNK_ROWS - 1) / G::CHUNK_ROWS;
+    if (clist) { r0 = a.row_begin; r1 = a.row_end; }
     int64_t c = warp;
     if (c >= nchunks) continue;
     int wc = 0;  // staged hits (warp-uniform)
+    auto chunk_row = [&](int64_t ci) -> int64_t {
+      return clist ? (int64_t)clist[ci] * G::CHUNK_ROWS : r0a + ci * G::CHUNK_ROWS;
+    };
     auto chunk_ptr = [&](int64_t ci) {
-      return reinterpret_cast<const uint4*>(a.plane + (r0a + ci * G::CHUNK_ROWS) * MPAD) + lane;
+      return reinterpret_cast<const uint4*>(a.plane + chunk_row(ci) * MPAD) + lane;
     };
     // entry: row offset from r0a (32 b) | local slot << 32 | score << 40
     auto flush = [&]() {
@@ -699,7 +829,7 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
       wst[lane] = nxt;
       __syncwarp();
       if (c + NW < nchunks) nxt = ldg_stream(chunk_ptr(c + NW));
-      const int64_t rb = r0a + c * G::CHUNK_ROWS;
+      const int64_t rb = chunk_row(c);
       // rows of this chunk outside [r0, r1) only at the unit's two ends
       const bool edge = rb < r0 || rb + G::CHUNK_ROWS > r1;
       const uint32_t lo = edge ? (uint32_t)max((int64_t)0, r0 - rb) : 0u;
