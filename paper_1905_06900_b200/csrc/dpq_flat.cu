@@ -194,7 +194,7 @@ static int launch_hist_t(Index* h, int ntiles, const int* tile_list, int64_t str
     attr = true;
   }
   int chunks = (int)std::max<int64_t>(1, std::min<int64_t>((148 * 2 + ntiles - 1) / ntiles,
-                                                          (nsamp + 4095) / 4096));
+                                                          (nsamp + 511) / 512));
   int64_t per = (nsamp + chunks - 1) / chunks;
   per = (per + 31) / 32 * 32;
   per = std::min<int64_t>(per, kHistRowsPerCta / 32 * 32);  // u16 counters never wrap
@@ -314,12 +314,12 @@ static int launch_refine_buf(Index* h, const RefineArgs& ra, int nq) {
 
 template <int MODE>
 static int launch_refine(Index* h, const RefineArgs& ra, int nq) {
-  const int need = ra.r + kTopThreads;  // one candidate per thread per round
+  const int need = ra.r + 2 * kTopThreads;  // two candidates per thread per round
   if (need <= 1024) return launch_refine_buf<1024, MODE>(h, ra, nq);
   if (need <= 2048) return launch_refine_buf<2048, MODE>(h, ra, nq);
   if (need <= 4096) return launch_refine_buf<4096, MODE>(h, ra, nq);
   if (need <= 8192) return launch_refine_buf<8192, MODE>(h, ra, nq);
-  set_error("r=" + std::to_string(ra.r) + " exceeds the device top-r limit (7936)");
+  set_error("r=" + std::to_string(ra.r) + " exceeds the device top-r limit (7680)");
   return DPQ_ERR_ARG;
 }
 
@@ -527,8 +527,9 @@ int run_group_tables(Index* h, int nq, int ystride) {
   static size_t attr = 0;
   dim3 grid(h->kbar, h->m);
   if (h->dsub == 32) {
-    if (smem > attr) cudaFuncSetAttribute(k_group_tables<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 49152));
-    k_group_tables<32><<<grid, 256, smem, h->stream>>>(ga);
+    const size_t sm2 = (size_t)32 * 32 * 4 + (size_t)nq * 4;
+    if (sm2 > 49152) cudaFuncSetAttribute(k_group_tables_reg<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+    k_group_tables_reg<32><<<grid, 256, sm2, h->stream>>>(ga);
   } else {
     if (smem > attr) cudaFuncSetAttribute(k_group_tables<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 49152));
     k_group_tables<0><<<grid, 256, smem, h->stream>>>(ga);

@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(NT) k_probe(const float* __restrict__ y, int d
     if (f > BUF - NT) {
       for (int i = f + threadIdx.x; i < BUF; i += NT) { keys[i] = ~0ull; ids[i] = INT64_MAX; }
       __syncthreads();
-      sort_pairs<BUF, NT>(keys, ids);
+      sort_pairs<NT>(keys, ids, BUF);
       if (threadIdx.x == 0) {
         const int nf = min(f, ma);
         fill = nf;
@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(NT) k_probe(const float* __restrict__ y, int d
   const int f = fill;
   for (int i = f + threadIdx.x; i < BUF; i += NT) { keys[i] = ~0ull; ids[i] = INT64_MAX; }
   __syncthreads();
-  sort_pairs<BUF, NT>(keys, ids);
+  sort_pairs<NT>(keys, ids, BUF);
   for (int i = threadIdx.x; i < ma; i += NT) cells[(int64_t)q * ma + i] = ids[i];
 }
 
@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(NT) k_ivf_conventional(IvfConvArgs a) {
       if (f > BUF - NT) {
         for (int i = f + threadIdx.x; i < BUF; i += NT) { keys[i] = ~0ull; ids[i] = INT64_MAX; }
         __syncthreads();
-        sort_pairs<BUF, NT>(keys, ids);
+        sort_pairs<NT>(keys, ids, BUF);
         if (threadIdx.x == 0) {
           const int nf = min(f, a.r);
           fill = nf;
@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(NT) k_ivf_conventional(IvfConvArgs a) {
   const int f = fill;
   for (int i = f + threadIdx.x; i < BUF; i += NT) { keys[i] = ~0ull; ids[i] = INT64_MAX; }
   __syncthreads();
-  sort_pairs<BUF, NT>(keys, ids);
+  sort_pairs<NT>(keys, ids, BUF);
   const int got = min(f, a.r);
   for (int i = threadIdx.x; i < a.r; i += NT) {
     const int64_t o = (int64_t)q * a.r + i;

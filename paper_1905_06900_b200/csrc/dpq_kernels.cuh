@@ -293,20 +293,35 @@ __global__ void __launch_bounds__(1024) k_sort_slots(const uint16_t* __restrict_
   if (q8 && nq <= kSortMax && m >= 2) {
     int P = 1;
     while (P < nq) P <<= 1;
-    for (int q = warp; q < P; q += 32) {
-      if (q >= nq) { if (lane == 0) kv[q] = ~0ull; continue; }
-      uint32_t best[2];
+    for (int q = tid; q < P; q += blockDim.x) kv[q] = 0ull;
+    __syncthreads();
+    // first argmin of the 8-bit table of subspace j (j = 0, 1) per query:
+    // one thread per (query, j), 16-B loads; (value << 16 | index) minima
+    for (int i = tid; i < 2 * P; i += blockDim.x) {
+      const int q = i >> 1, j = i & 1;
+      if (q >= nq) continue;
+      const uint8_t* row = q8 + ((int64_t)q * m + j) * kbar;
+      uint32_t b = 0xFFFFFFFFu;
+      if ((kbar & 15) == 0 && (((uintptr_t)row) & 15) == 0) {
+        for (int g = 0; g < kbar; g += 16) {
+          const uint4 v = *reinterpret_cast<const uint4*>(row + g);
+          const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        uint32_t b = 0xFFFFFFFFu;  // (value << 16) | index, first argmin
-        for (int g = lane; g < kbar; g += 32) b = min(b, ((uint32_t)q8[((int64_t)q * m + j) * kbar + g] << 16) | (uint32_t)g);
-        best[j] = __reduce_min_sync(0xffffffffu, b) & 0xFFFFu;
+          for (int u = 0; u < 16; ++u) b = min(b, (((w4[u >> 2] >> (8 * (u & 3))) & 0xFFu) << 16) | (uint32_t)(g + u));
+        }
+      } else {
+        for (int g = 0; g < kbar; ++g) b = min(b, ((uint32_t)row[g] << 16) | (uint32_t)g);
       }
-      if (lane == 0) {
-        const int B = gkey(q);
-        const uint32_t cls = B == 256 ? 3u : (B <= 30 ? 0u : (B <= 62 ? 1u : 2u));
-        kv[q] = ((uint64_t)((cls << 16) | (best[0] << 8) | best[1]) << 32) | (uint32_t)q;
-      }
+      // pack both subspaces into kv (low word = query, filled below)
+      if (j == 0) atomicOr(reinterpret_cast<unsigned long long*>(&kv[q]), (unsigned long long)(b & 0xFFu) << 40);
+      else atomicOr(reinterpret_cast<unsigned long long*>(&kv[q]), (unsigned long long)(b & 0xFFu) << 32);
+    }
+    __syncthreads();
+    for (int q = tid; q < P; q += blockDim.x) {
+      if (q >= nq) { kv[q] = ~0ull; continue; }
+      const int B = gkey(q);
+      const uint64_t cls = B == 256 ? 3u : (B <= 30 ? 0u : (B <= 62 ? 1u : 2u));
+      kv[q] = ((kv[q] | (cls << 48)) & ~0xFFFFFFFFull) | (uint32_t)q;
     }
     __syncthreads();
     for (int size = 2; size <= P; size <<= 1) {
@@ -407,9 +422,10 @@ __global__ void __launch_bounds__(256) k_chunk_list(const uint32_t* __restrict__
   const uint32_t bal = __ballot_sync(0xffffffffu, f);
   int base = 0;
   if (lane == 0 && bal) base = atomicAdd(list_len + tile, __popc(bal));
-  if (n_rows && f) {  // query-rows this tile will scan (its real queries x listed rows)
-    const int64_t rows = min((int64_t)128, n - (int64_t)c * 128);
-    atomicAdd(n_rows, (unsigned long long)(rows * min(qt, nb - tile * qt)));
+  if (n_rows) {  // query-rows this tile will scan (its real queries x listed rows), one atomic per warp
+    const unsigned rows = f ? (unsigned)min((int64_t)128, n - (int64_t)c * 128) : 0u;
+    const unsigned wr = __reduce_add_sync(0xffffffffu, rows);
+    if (lane == 0 && wr) atomicAdd(n_rows, (unsigned long long)wr * (unsigned long long)min(qt, nb - tile * qt));
   }
   base = __shfl_sync(0xffffffffu, base, 0);
   if (f) list[(int64_t)tile * nchunks + base + __popc(bal & ((1u << lane) - 1u))] = c;
@@ -1176,6 +1192,67 @@ struct GroupTablesArgs {
   unsigned long long* n_entries;
 };
 
+// Register-row variant (DSUB = 32): thread ib holds codebook row ib of the
+// group in registers and loops over the group's active queries, whose
+// sub-vectors are staged 32 at a time in shared memory.  Same association
+// order as pw_block / pw_sqdist_v8 (8 running sums, pairwise combine).
+template <int DSUB>
+__global__ void __launch_bounds__(256) k_group_tables_reg(GroupTablesArgs a) {
+  extern __shared__ __align__(16) float gsm[];
+  float* ys = gsm;                                      // [32][DSUB]
+  int* act = reinterpret_cast<int*>(gsm + 32 * DSUB);   // [nq]
+  __shared__ int nact;
+  const int g = blockIdx.x, j = blockIdx.y, tid = threadIdx.x;
+  const int gsize = a.k / a.kbar;
+  if (tid == 0) nact = 0;
+  __syncthreads();
+  for (int q = tid; q < a.nq; q += 256)
+    if ((int)a.q8[((int64_t)q * a.m + j) * a.kbar + g] <= a.bstar[q]) act[atomicAdd(&nact, 1)] = q;
+  __syncthreads();
+  const int n = nact;
+  for (int ib0 = 0; ib0 < gsize; ib0 += 256) {
+    const int ib = ib0 + tid;
+    float c[DSUB];
+    if (ib < gsize) {
+      const float4* src = reinterpret_cast<const float4*>(a.cb + (((int64_t)j * a.k) + (int64_t)ib * a.kbar + g) * DSUB);
+#pragma unroll
+      for (int i = 0; i < DSUB / 4; ++i) {
+        const float4 v = __ldg(src + i);
+        c[4 * i] = v.x; c[4 * i + 1] = v.y; c[4 * i + 2] = v.z; c[4 * i + 3] = v.w;
+      }
+    }
+    for (int base = 0; base < n; base += 32) {
+      const int nb = min(32, n - base);
+      __syncthreads();
+      for (int e = tid; e < nb * DSUB; e += 256) {
+        const int qi = act[base + e / DSUB];
+        ys[e] = a.y[(int64_t)qi * a.ystride + j * DSUB + e % DSUB];
+      }
+      __syncthreads();
+      if (ib < gsize) {
+        for (int t = 0; t < nb; ++t) {
+          const float4* y4 = reinterpret_cast<const float4*>(ys + t * DSUB);
+          float r[8];
+#pragma unroll
+          for (int i = 0; i < DSUB / 8; ++i) {
+            const float4 p = y4[2 * i], q = y4[2 * i + 1];
+            const float yv[8] = {p.x, p.y, p.z, p.w, q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int l = 0; l < 8; ++l) {
+              const float sd = sqdiff(c[8 * i + l], yv[l]);
+              r[l] = i == 0 ? sd : __fadd_rn(r[l], sd);
+            }
+          }
+          const float v = __fadd_rn(__fadd_rn(__fadd_rn(r[0], r[1]), __fadd_rn(r[2], r[3])),
+                                    __fadd_rn(__fadd_rn(r[4], r[5]), __fadd_rn(r[6], r[7])));
+          a.tables[(((int64_t)act[base + t] * a.m + j) * a.kbar + g) * gsize + ib] = v;
+        }
+      }
+    }
+  }
+  if (a.n_entries && tid == 0) atomicAdd(a.n_entries, (unsigned long long)n * gsize);
+}
+
 template <int DSUB>
 __global__ void __launch_bounds__(256) k_group_tables(GroupTablesArgs a) {
   extern __shared__ __align__(16) float tile[];  // [gsize][ld]
@@ -1258,11 +1335,12 @@ struct RefineArgs {
   unsigned long long* n_refined;
 };
 
-template <int BUF, int NT>
-__device__ void sort_pairs(uint64_t* keys, int64_t* ids) {
-  for (int size = 2; size <= BUF; size <<= 1) {
+// Bitonic sort of the first P (power of two) entries of the buffer.
+template <int NT>
+__device__ void sort_pairs(uint64_t* keys, int64_t* ids, int P) {
+  for (int size = 2; size <= P; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int t = threadIdx.x; t < BUF / 2; t += NT) {
+      for (int t = threadIdx.x; t < P / 2; t += NT) {
         const int i = 2 * t - (t & (stride - 1));
         const int j = i + stride;
         const bool asc = (i & size) == 0;
@@ -1313,11 +1391,11 @@ __global__ void __launch_bounds__(NT) k_refine_topk(RefineArgs a) {
   // row -> id (sorted flat rows / ivf lists: row_ids), looked up only for a
   // candidate that ties the threshold distance or enters the buffer
   auto id_of = [&](int64_t row) -> int64_t { return a.row_ids ? a.row_ids[row] : a.id_base + row; };
-  auto eval = [&](int64_t idx, uint64_t& key, int64_t& id) -> bool {
+  // v: the candidate's emit entry (prefetched one round ahead)
+  auto eval = [&](int64_t idx, uint64_t v, uint64_t& key, int64_t& id) -> bool {
     int64_t row;
     uint32_t probe = 0;
     if (MODE != MODE_ALL) {
-      const uint64_t v = e[idx];
       if ((int)emit_score(v) > bs) return false;
       row = emit_row(v);
       probe = emit_probe(v);
@@ -1351,15 +1429,28 @@ __global__ void __launch_bounds__(NT) k_refine_topk(RefineArgs a) {
     id = row;  // (a row until id_of)
     return true;
   };
-  constexpr int U = 1;  // candidates per thread per round (U > 1 measured slower: bigger buffer, lower occupancy)
-  for (int64_t base = 0; base < ntot; base += (int64_t)U * NT) {
-    uint64_t key[U];
-    int64_t id[U];
-    bool keep[U];
+  constexpr int U = 2;  // candidates per thread per round (two independent gather chains)
+  auto pow2_at_least = [](int v) { int p = 2; while (p < v) p <<= 1; return p; };
+  uint64_t ev[U];
+  auto load_e = [&](int64_t base) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t idx = base + (int64_t)u * NT + threadIdx.x;
-      keep[u] = idx < ntot && eval(idx, key[u], id[u]) && key[u] <= thr_k;
+      ev[u] = (MODE != MODE_ALL && idx < ntot) ? e[idx] : 0ull;
+    }
+  };
+  load_e(0);
+  for (int64_t base = 0; base < ntot; base += (int64_t)U * NT) {
+    uint64_t key[U], cur[U];
+    int64_t id[U];
+    bool keep[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) cur[u] = ev[u];
+    load_e(base + (int64_t)U * NT);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t idx = base + (int64_t)u * NT + threadIdx.x;
+      keep[u] = idx < ntot && eval(idx, cur[u], key[u], id[u]) && key[u] <= thr_k;
       if (keep[u]) {
         id[u] = id_of(id[u]);
         keep[u] = pair_less(key[u], id[u], thr_k, thr_i);
@@ -1377,9 +1468,10 @@ __global__ void __launch_bounds__(NT) k_refine_topk(RefineArgs a) {
     const int f = fill;
     __syncthreads();
     if (f > BUF - U * NT) {
-      for (int i = f + threadIdx.x; i < BUF; i += NT) { keys[i] = ~0ull; ids[i] = INT64_MAX; }
+      const int P = pow2_at_least(f);
+      for (int i = f + threadIdx.x; i < P; i += NT) { keys[i] = ~0ull; ids[i] = INT64_MAX; }
       __syncthreads();
-      sort_pairs<BUF, NT>(keys, ids);
+      sort_pairs<NT>(keys, ids, P);
       if (threadIdx.x == 0) {
         const int nf = min(f, a.r);
         fill = nf;
@@ -1389,9 +1481,10 @@ __global__ void __launch_bounds__(NT) k_refine_topk(RefineArgs a) {
     }
   }
   const int f = fill;
-  for (int i = f + threadIdx.x; i < BUF; i += NT) { keys[i] = ~0ull; ids[i] = INT64_MAX; }
+  const int P = pow2_at_least(f);
+  for (int i = f + threadIdx.x; i < P; i += NT) { keys[i] = ~0ull; ids[i] = INT64_MAX; }
   __syncthreads();
-  sort_pairs<BUF, NT>(keys, ids);
+  sort_pairs<NT>(keys, ids, P);
   const int got = min(f, a.r);
   for (int i = threadIdx.x; i < a.r; i += NT) {
     const int64_t o = (int64_t)q * a.r + i;
