@@ -1467,7 +1467,10 @@ __global__ void __launch_bounds__(NT) k_refine_topk(RefineArgs a) {
     __syncthreads();
     const int f = fill;
     __syncthreads();
-    if (f > BUF - U * NT) {
+    // sort + truncate once the buffer is half full (the next round adds at
+    // most U * NT <= BUF / 2 entries): early, small sorts tighten the
+    // threshold sooner than waiting for a full buffer
+    if (f >= BUF - U * NT || (f >= 2 * a.r && f >= (BUF - U * NT) / 2 && thr_k == ~0ull)) {
       const int P = pow2_at_least(f);
       for (int i = f + threadIdx.x; i < P; i += NT) { keys[i] = ~0ull; ids[i] = INT64_MAX; }
       __syncthreads();
