@@ -9,12 +9,13 @@ device is visible, every search raises.
 from __future__ import annotations
 
 import ctypes
+import os
 from ctypes import POINTER, c_double, c_float, c_int, c_int32, c_int64, c_uint8, c_void_p
 from pathlib import Path
 
 import numpy as np
 
-_PATH = Path(__file__).with_name("libdpq.so")
+_PATH = Path(os.environ.get("DPQ_LIB") or Path(__file__).with_name("libdpq.so"))  # DPQ_LIB: A/B another build
 _lib = None
 
 DPQ_OK, DPQ_ERR_ARG, DPQ_ERR_CUDA, DPQ_ERR_NOMEM, DPQ_ERR_STATE = 0, 1, 2, 3, 4

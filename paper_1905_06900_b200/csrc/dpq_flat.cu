@@ -249,13 +249,13 @@ static int launch_emit_t(Index* h, EmitArgs ea, int ntiles, int64_t rows) {
     DPQ_LAUNCHED(h);
     return DPQ_OK;
   }
-  if (ea.chunk_list) {  // run-filtered chunk lists: fixed slices per tile (lengths on the device)
-    const int upt = std::max(1, (4 * sms + ntiles - 1) / ntiles);
-    ea.units_per_tile = upt;
-    ea.n_units = upt * ntiles;
+  if (ea.chunk_list) {  // run-filtered chunk lists, handed out dynamically (lengths on the device)
+    ea.units_per_tile = 1;
+    ea.n_units = ntiles;  // (list mode: the tile count)
     ea.rows_per_cta = 0;
-    DPQ_CUDA(cudaMemsetAsync(h->ws.counter, 0, sizeof(unsigned), h->stream));
-    k_scan_emit<MPAD, kEmitThreads><<<std::min(sms, ea.n_units), kEmitThreads, smem, h->stream>>>(ea);
+    ea.list_next = h->ws.list_len + ntiles;
+    DPQ_CUDA(cudaMemsetAsync(h->ws.list_len + ntiles, 0, (size_t)ntiles * sizeof(int), h->stream));
+    k_scan_emit<MPAD, kEmitThreads><<<sms, kEmitThreads, smem, h->stream>>>(ea);
     DPQ_LAUNCHED(h);
     return DPQ_OK;
   }
@@ -397,7 +397,7 @@ static int flat_first_pass(Index* h, int nb, int r2) {
   if (use_list && (w.list_tiles < tiles || w.list_chunks < h->n_chunks)) {
     DPQ_TRY(dmalloc(&w.pot, (size_t)tiles * 65536));
     DPQ_TRY(dmalloc(&w.chunk_list, (size_t)tiles * h->n_chunks));
-    DPQ_TRY(dmalloc(&w.list_len, (size_t)tiles));
+    DPQ_TRY(dmalloc(&w.list_len, (size_t)tiles * 2));  // lengths | handed-out counters
     w.list_tiles = tiles;
     w.list_chunks = h->n_chunks;
   }

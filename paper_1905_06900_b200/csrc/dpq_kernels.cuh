@@ -639,6 +639,7 @@ struct EmitArgs {
   int runs = 0;                 // rows sorted by (subspace 0, 1) low bytes: reuse their sums
   const int* chunk_list = nullptr;  // optional per-tile lists of 128-row chunks to scan (run filter)
   const int* list_len = nullptr;    //   [tiles] list lengths (device); list of tile t at t * list_stride
+  const int* list_next = nullptr;   //   [tiles] chunks handed out so far (zeroed before the launch)
   int64_t list_stride = 0;
   int n_units;                  // tiles * units_per_tile
   int units_per_tile;
@@ -695,15 +696,46 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
   const uint32_t lt = (1u << lane) - 1u;
   const uint32_t one = a.one, mone = 0u - a.one;  // opaque 1 / -1 (see fma_add)
   int cur_tile = -1;
+  bool first_unit = true;
   for (;;) {
     __syncthreads();  // previous unit finished by every warp
-    if (threadIdx.x == 0) s_unit = (int)atomicAdd(a.unit_counter, 1u);
+    if (threadIdx.x == 0) {
+      if (a.chunk_list) {
+        // list mode, dynamic: start on a tile in proportion to the list
+        // lengths, then move to the tile with the most chunks left
+        int nt = a.n_units, pick = -1;
+        if (first_unit) {
+          int64_t tot = 0;
+          for (int t = 0; t < nt; ++t) tot += a.list_len[t];
+          const int64_t target = (int64_t)blockIdx.x * tot / gridDim.x;
+          int64_t cum = 0;
+          for (int t = 0; t < nt && pick < 0; ++t) {
+            cum += a.list_len[t];
+            if (cum > target) pick = t;
+          }
+        } else {
+          int best = 0;
+          for (int t = 0; t < nt; ++t) {
+            const int left = a.list_len[t] - *((volatile int*)a.list_next + t);
+            if (left > best) { best = left; pick = t; }
+          }
+        }
+        s_unit = pick;
+      } else {
+        s_unit = (int)atomicAdd(a.unit_counter, 1u);
+      }
+    }
     __syncthreads();
+    first_unit = false;
     const int u = s_unit;
-    if (u >= a.n_units) break;
+    if (a.chunk_list ? u < 0 : u >= a.n_units) break;
     int tile;
     int64_t r0, r1;
-    if (a.unit_tile) {
+    if (a.chunk_list) {
+      tile = u;
+      r0 = 0;
+      r1 = a.list_len[tile];
+    } else if (a.unit_tile) {
       tile = a.unit_tile[u];
       r0 = a.unit_r0[u];
       r1 = a.unit_r1[u];
@@ -715,14 +747,8 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
       const int tix = u % ntl;
       const int64_t chunk_u = u / ntl;
       tile = a.tile_list ? a.tile_list[tix] : tix;
-      if (a.chunk_list) {  // unit = a slice of the tile's chunk list
-        const int64_t len = a.list_len[tile];
-        r0 = chunk_u * len / a.units_per_tile;
-        r1 = (chunk_u + 1) * len / a.units_per_tile;
-      } else {
-        r0 = a.row_begin + chunk_u * a.rows_per_cta;
-        r1 = min(a.row_end, r0 + a.rows_per_cta);
-      }
+      r0 = a.row_begin + chunk_u * a.rows_per_cta;
+      r1 = min(a.row_end, r0 + a.rows_per_cta);
     }
     if (tile != cur_tile) {
       // every warp is past the previous unit (barrier above): one thread
@@ -762,11 +788,19 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
     // rows outside the range are never emitted.
     if (r0 >= r1) continue;
     // list mode: [r0, r1) indexes the tile's chunk list, rows are absolute
-    const int* clist = a.chunk_list ? a.chunk_list + tile * a.list_stride + r0 : nullptr;
+    const int* clist = a.chunk_list ? a.chunk_list + tile * a.list_stride : nullptr;
     const int64_t r0a = clist ? 0 : (r0 & ~(int64_t)(G::CHUNK_ROWS - 1));
     const int64_t nchunks = clist ? r1 - r0 : (r1 - r0a + G::CHUNK_ROWS - 1) / G::CHUNK_ROWS;
     if (clist) { r0 = a.row_begin; r1 = a.row_end; }
-    int64_t c = warp;
+    // next chunk of this warp: strided, or (list mode) pulled from the
+    // tile's global counter so chunks of uneven cost balance across warps/CTAs
+    auto next_chunk = [&](int64_t cprev) -> int64_t {
+      if (!clist) return cprev + NW;
+      int v = 0;
+      if (lane == 0) v = atomicAdd(const_cast<int*>(a.list_next) + tile, 1);
+      return (int64_t)__shfl_sync(0xffffffffu, v, 0);
+    };
+    int64_t c = clist ? next_chunk(0) : warp;
     if (c >= nchunks) continue;
     int wc = 0;  // staged hits (warp-uniform)
     auto chunk_row = [&](int64_t ci) -> int64_t {
@@ -840,11 +874,13 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
       } while (hm);
     };
     uint4 nxt = ldg_stream(chunk_ptr(c));
-    for (; c < nchunks; c += NW) {
+    int64_t cn = c;
+    for (; c < nchunks; c = cn) {
       __syncwarp();
       wst[lane] = nxt;
       __syncwarp();
-      if (c + NW < nchunks) nxt = ldg_stream(chunk_ptr(c + NW));
+      cn = next_chunk(c);
+      if (cn < nchunks) nxt = ldg_stream(chunk_ptr(cn));
       const int64_t rb = chunk_row(c);
       // rows of this chunk outside [r0, r1) only at the unit's two ends
       const bool edge = rb < r0 || rb + G::CHUNK_ROWS > r1;
@@ -935,14 +971,23 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
                   }
                   if (edge && !(r >= lo && r < hi)) hm = 0u;
                 }
-                for (;;) {
-                  const bool hh = hm != 0u;
-                  const uint32_t bal = __ballot_sync(0xffffffffu, hh);
-                  if (!bal) break;
-                  if (wc + 32 > kWarpBuf) flush();
-                  if (hh) {
-                    const int b = __ffs(hm) - 1;
-                    hm &= hm - 1u;
+                // stage: one warp prefix sum, then every lane writes its hits
+                const int nh = __popc(hm);
+                int incl = nh;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                  const int v = __shfl_up_sync(0xffffffffu, incl, o);
+                  if (lane >= o) incl += v;
+                }
+                const int tot = __shfl_sync(0xffffffffu, incl, 31);
+                if (tot > 0) {
+                  if (wc + tot > kWarpBuf) flush();
+                  int o = wc + incl - nh;
+                  const int lim = min(kWarpBuf, wc + tot);  // (tot > kWarpBuf: rest below)
+                  uint32_t hr = hm;
+                  while (hr && o < lim) {
+                    const int b = __ffs(hr) - 1;
+                    hr &= hr - 1u;
                     const int k = b >> 2, sh = 8 * (b & 3);
                     const uint32_t tw = k == 0 ? t[0] : (k == 1 ? t[1] : (k == 2 ? t[2] : t[3]));
                     uint32_t sc = (tw >> sh) & 0xFFu;
@@ -950,10 +995,30 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
                       const uint32_t ck = k == 0 ? c4[0] : (k == 1 ? c4[1] : (k == 2 ? c4[2] : c4[3]));
                       sc -= (ck >> sh) & 0xFFu;
                     }
-                    hbuf[wc + __popc(bal & lt)] =
-                        (uint64_t)(rboff + r) | ((uint64_t)(16 * sp + b) << 32) | ((uint64_t)sc << 40);
+                    hbuf[o++] = (uint64_t)(rboff + r) | ((uint64_t)(16 * sp + b) << 32) | ((uint64_t)sc << 40);
                   }
-                  wc += __popc(bal);
+                  wc = lim;
+                  // more hits than one buffer holds (<= 512): the rest, one ballot round each
+                  for (;;) {
+                    const bool hh = hr != 0u;
+                    const uint32_t bal = __ballot_sync(0xffffffffu, hh);
+                    if (!bal) break;
+                    if (wc + 32 > kWarpBuf) flush();
+                    if (hh) {
+                      const int b = __ffs(hr) - 1;
+                      hr &= hr - 1u;
+                      const int k = b >> 2, sh = 8 * (b & 3);
+                      const uint32_t tw = k == 0 ? t[0] : (k == 1 ? t[1] : (k == 2 ? t[2] : t[3]));
+                      uint32_t sc = (tw >> sh) & 0xFFu;
+                      if (MODE == kModeWide5) {
+                        const uint32_t ck = k == 0 ? c4[0] : (k == 1 ? c4[1] : (k == 2 ? c4[2] : c4[3]));
+                        sc -= (ck >> sh) & 0xFFu;
+                      }
+                      hbuf[wc + __popc(bal & lt)] =
+                          (uint64_t)(rboff + r) | ((uint64_t)(16 * sp + b) << 32) | ((uint64_t)sc << 40);
+                    }
+                    wc += __popc(bal);
+                  }
                 }
               }
               __syncwarp();
