@@ -118,6 +118,7 @@ int ensure_ws(Index* h, int nslot, int r, int ystride, int nq) {
     DPQ_TRY(dmalloc(&w.flags, (size_t)qn));
     DPQ_TRY(dmalloc(&w.only, (size_t)std::max(tiles * qt, qn)));
     DPQ_TRY(dmalloc(&w.tile_list, (size_t)tiles));
+    DPQ_TRY(dmalloc(&w.order, (size_t)qn));
     DPQ_TRY(dmalloc(&w.tile_fast, (size_t)tiles));
     if (!w.counter) DPQ_TRY(dmalloc(&w.counter, 4));
     DPQ_TRY(dmalloc(&w.slot_query, (size_t)tiles * qt));
@@ -550,6 +551,11 @@ static int flat_derived_batch(Index* h, int nb, int r, int r2) {
   if (rc != DPQ_OK) return rc;
   ev_rec(h, 5);
   RefineArgs ra = make_refine_args(h, r);
+  if (nb > 1) {  // heaviest emit lists first
+    k_order_by_count<<<1, 1024, 0, h->stream>>>(h->ws.emit_cnt, nb, h->ws.cap, h->ws.order);
+    DPQ_LAUNCHED(h);
+    ra.order = h->ws.order;
+  }
   if (group_tables_fit(h, nb)) {
     DPQ_TRY(run_group_tables(h, nb, h->d));
     ra.tables = h->ws.tables;  // (re)allocated by run_group_tables
@@ -799,7 +805,7 @@ void index_free(Index* h) {
   void* dev[] = {h->cb, h->dcb, h->codes, h->plane, h->own_prefix ? h->prefix : nullptr, h->centers,
                  h->offsets, h->sorted_ids, h->d_nref, h->d_nemit, h->d_nent, h->d_nwide, h->d_nrows, h->chunk_keys, w.pot, w.chunk_list, w.list_len, w.y, w.small, w.q8, w.qmin, w.qmax, w.bounds,
                  w.lut, w.hist, w.hist_i, w.guard_b, w.gword, w.gword_p, w.emit_cnt, w.emit, w.bstar, w.ncand,
-                 w.flags, w.only, w.tile_list, w.out_d, w.out_i, w.tables, w.slot_query, w.slot_probe,
+                 w.flags, w.only, w.tile_list, w.order, w.out_d, w.out_i, w.tables, w.slot_query, w.slot_probe,
                  w.slot_pre_off, w.slot_pre_len, w.counter, w.tile_fast};
   for (void* p : dev)
     if (p) cudaFree(p);

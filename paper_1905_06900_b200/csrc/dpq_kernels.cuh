@@ -1398,7 +1398,32 @@ struct RefineArgs {
   int r;
   double* out_d; int64_t* out_i;
   unsigned long long* n_refined;
+  const int* order = nullptr;  // optional CTA -> query (heaviest emit lists first)
 };
+
+// Query order for the refine launch: descending emitted count (coarse
+// counting sort, one CTA), so the longest lists start first and the short
+// ones fill in behind them (LPT scheduling over the CTA slots).
+__global__ void __launch_bounds__(1024) k_order_by_count(const uint32_t* __restrict__ emit_cnt, int nq,
+                                                         uint32_t cap, int* __restrict__ order) {
+  __shared__ int cnt[1025];
+  __shared__ unsigned mx;
+  const int tid = threadIdx.x;
+  if (tid == 0) mx = 0;
+  for (int i = tid; i < 1025; i += 1024) cnt[i] = 0;
+  __syncthreads();
+  for (int q = tid; q < nq; q += 1024) atomicMax(&mx, min(emit_cnt[q], cap));
+  __syncthreads();
+  int shift = 0;
+  while ((mx >> shift) >= 1024u) ++shift;
+  auto key = [&](int q) { return 1023 - (int)(min(emit_cnt[q], cap) >> shift); };  // descending
+  for (int q = tid; q < nq; q += 1024) atomicAdd(&cnt[key(q) + 1], 1);
+  __syncthreads();
+  if (tid == 0)
+    for (int i = 1; i < 1025; ++i) cnt[i] += cnt[i - 1];
+  __syncthreads();
+  for (int q = tid; q < nq; q += 1024) order[atomicAdd(&cnt[key(q)], 1)] = q;
+}
 
 // Bitonic sort of the first P (power of two) entries of the buffer.
 template <int NT>
@@ -1435,7 +1460,7 @@ __global__ void __launch_bounds__(NT) k_refine_topk(RefineArgs a) {
   __shared__ uint64_t thr_k;
   __shared__ int64_t thr_i;
   __shared__ unsigned nref;
-  const int q = blockIdx.x;
+  const int q = a.order ? a.order[blockIdx.x] : blockIdx.x;
   for (int i = threadIdx.x; i < a.ystride; i += NT) ys[i] = a.y[(int64_t)q * a.ystride + i];
   if (threadIdx.x == 0) { fill = 0; thr_k = ~0ull; thr_i = INT64_MAX; nref = 0; }
   __syncthreads();
