@@ -47,6 +47,10 @@ const char* dpq_last_error(void);
 int dpq_abi_version(void);
 /* Number of visible CUDA devices (0 on a CPU-only host, never an error). */
 int dpq_device_count(void);
+/* Host-side finiteness scan of n float32 values (the input check of
+ * sklearn check_array that flat.py:71 / ivf.py:125 run on the queries):
+ * 0 = all finite, 1 = contains NaN, 2 = contains +-inf (NaN wins).  No GPU. */
+int dpq_all_finite(const float* x, int64_t n);
 
 /* ---------------------------------------------------------------- flat --
  * Replaces the fitted state FlatIndex holds after fit (flat.py:45-52):

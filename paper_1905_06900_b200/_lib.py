@@ -25,6 +25,7 @@ SIGNATURES = {
     "dpq_last_error": (ctypes.c_char_p, []),
     "dpq_abi_version": (c_int, []),
     "dpq_device_count": (c_int, []),
+    "dpq_all_finite": (c_int, [c_void_p, c_int64]),
     "dpq_flat_create": (c_int, [c_int, c_int, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p, c_int,
                                 c_int64, c_int64, c_void_p, c_int64, POINTER(c_void_p)]),
     "dpq_ivf_create": (c_int, [c_int, c_int, c_int, c_int, c_int, c_void_p, c_void_p, c_int, c_void_p,
@@ -195,3 +196,18 @@ def ivf_create(codebooks, derived, centers, offsets, sorted_codes, sorted_ids, d
                               ptr(sorted_ids), int(sorted_ids.shape[0]), ctypes.byref(out))
     check(rc, "dpq_ivf_create")
     return Handle(out, device)
+
+
+def query_array(Y):
+    """Y as the reference's check_array(Y, dtype=float32, order="C") would
+    return it (flat.py:71, ivf.py:125), with the common case (a 2-D,
+    C-contiguous float32 ndarray) validated by one native finiteness scan
+    instead of sklearn's; anything else, and every failure, goes through
+    check_array itself so types and messages are the reference's."""
+    if (isinstance(Y, np.ndarray) and type(Y) is np.ndarray and Y.ndim == 2 and Y.dtype == np.float32
+            and Y.flags.c_contiguous and Y.shape[0] > 0 and Y.shape[1] > 0
+            and lib().dpq_all_finite(Y.ctypes.data, Y.size) == 0):
+        return Y
+    from sklearn.utils.validation import check_array
+
+    return check_array(Y, dtype=np.float32, order="C")

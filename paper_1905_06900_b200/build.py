@@ -25,6 +25,7 @@ NVCC_FLAGS = [
     "-O3", "-lineinfo", "-std=c++17",
     "-fmad=false",               # exactness: no FMA contraction anywhere
     "-Xcompiler", "-fPIC",
+    "-Xcompiler", "-fopenmp",    # host staging copies on a few threads
     "-Xptxas", "-v",
     "--expt-relaxed-constexpr",
 ]
@@ -63,7 +64,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         objs.append(str(obj))
     out_tmp = LIB.with_suffix(".so.tmp")
     cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
-           *objs, "-o", str(out_tmp), "-lcudart"]
+           *objs, "-o", str(out_tmp), "-lcudart", "-lgomp"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)

@@ -9,6 +9,7 @@
 // exact redo runs.
 #include <cuda_runtime.h>
 #include <cub/device/device_radix_sort.cuh>
+#include <omp.h>
 
 #include <algorithm>
 #include <cmath>
@@ -443,6 +444,13 @@ static int flat_first_pass(Index* h, int nb, int r2) {
     if (first) ev_rec(h, 4);
     first = false;
     DPQ_CUDA(cudaMemcpyAsync(w.h_flags, w.flags, nb, cudaMemcpyDeviceToHost, h->stream));
+    if (!h->no_spec) {
+      // speculative: the batch goes on (flagged queries have b* = -1 and
+      // refine nothing); the caller checks h_flags after its final sync and
+      // redoes the batch without speculation if any query was flagged
+      h->spec_nb = nb;
+      return DPQ_OK;
+    }
     DPQ_CUDA(cudaStreamSynchronize(h->stream));
     bool any_exact = false, any_over = false;
     for (int q = 0; q < nb; ++q) {
@@ -603,6 +611,29 @@ static int flat_conventional_batch(Index* h, int nb, int r) {
 
 // Generic host-buffer driver: splits nq into batches, stages through pinned
 // memory, calls `batch(nb)` and copies results back.
+// Host staging copies (queries in, results out) split over a few OpenMP
+// threads: one thread moves ~20 GB/s, a 1024-query batch is ~2 MB.
+static void par_memcpy(void* dst, const void* src, size_t bytes) {
+  constexpr size_t kMin = 256 << 10;
+  if (bytes < kMin) { memcpy(dst, src, bytes); return; }
+  const int nt = (int)std::min<size_t>(8, bytes / (kMin / 2));
+#pragma omp parallel for num_threads(nt) schedule(static)
+  for (int t = 0; t < nt; ++t) {
+    const size_t a = bytes * t / nt, b = bytes * (t + 1) / nt;
+    memcpy((char*)dst + a, (const char*)src + a, b - a);
+  }
+}
+
+// After a stream sync: did the last speculative first pass flag a query?
+// (clears the pending state either way)
+static bool spec_failed(Index* h) {
+  const int nb = h->spec_nb;
+  h->spec_nb = 0;
+  for (int q = 0; q < nb; ++q)
+    if (h->ws.h_flags[q]) return true;
+  return false;
+}
+
 template <class F>
 static int host_driver(Index* h, const float* y, int64_t nq, int r, int batch_limit, double* dists,
                        int64_t* ids, double* phase_us, F&& batch) {
@@ -612,8 +643,12 @@ static int host_driver(Index* h, const float* y, int64_t nq, int r, int batch_li
     const int nb = (int)std::min<int64_t>(bsz, nq - q0);
     DPQ_TRY(ensure_ws(h, nb, r, h->d, -1));
     Workspace& w = h->ws;
-    memcpy(w.h_y, y + q0 * h->d, (size_t)nb * h->d * 4);
-    DPQ_CUDA(cudaMemcpyAsync(w.y, w.h_y, (size_t)nb * h->d * 4, cudaMemcpyHostToDevice, h->stream));
+    if (h->direct_copy) {
+      DPQ_CUDA(cudaMemcpyAsync(w.y, y + q0 * h->d, (size_t)nb * h->d * 4, cudaMemcpyHostToDevice, h->stream));
+    } else {
+      par_memcpy(w.h_y, y + q0 * h->d, (size_t)nb * h->d * 4);
+      DPQ_CUDA(cudaMemcpyAsync(w.y, w.h_y, (size_t)nb * h->d * 4, cudaMemcpyHostToDevice, h->stream));
+    }
     const bool want_t = phase_us != nullptr;
     const bool old_t = h->timing;
     if (want_t) h->timing = true;
@@ -624,14 +659,31 @@ static int host_driver(Index* h, const float* y, int64_t nq, int r, int batch_li
       continue;
     }
     if (rc != DPQ_OK) return rc;
-    if (r > 0) {
-      DPQ_CUDA(cudaMemcpyAsync(w.h_d, w.out_d, (size_t)nb * r * 8, cudaMemcpyDeviceToHost, h->stream));
-      DPQ_CUDA(cudaMemcpyAsync(w.h_i, w.out_i, (size_t)nb * r * 8, cudaMemcpyDeviceToHost, h->stream));
+    bool redo = false;
+  copy_out:
+    if (r > 0 && h->direct_copy) {
+      DPQ_CUDA(cudaMemcpyAsync(dists + q0 * r, w.out_d, (size_t)nb * r * 8, cudaMemcpyDeviceToHost, h->stream));
+      DPQ_CUDA(cudaMemcpyAsync(ids + q0 * r, w.out_i, (size_t)nb * r * 8, cudaMemcpyDeviceToHost, h->stream));
+      DPQ_CUDA(cudaStreamSynchronize(h->stream));
+    } else {
+      if (r > 0) {
+        DPQ_CUDA(cudaMemcpyAsync(w.h_d, w.out_d, (size_t)nb * r * 8, cudaMemcpyDeviceToHost, h->stream));
+        DPQ_CUDA(cudaMemcpyAsync(w.h_i, w.out_i, (size_t)nb * r * 8, cudaMemcpyDeviceToHost, h->stream));
+      }
+      DPQ_CUDA(cudaStreamSynchronize(h->stream));
     }
-    DPQ_CUDA(cudaStreamSynchronize(h->stream));
-    if (r > 0) {
-      memcpy(dists + q0 * r, w.h_d, (size_t)nb * r * 8);
-      memcpy(ids + q0 * r, w.h_i, (size_t)nb * r * 8);
+    if (!redo && spec_failed(h)) {  // a speculative batch had a flagged query: redo it exactly
+      redo = true;
+      h->no_spec = true;
+      rc = batch(nb);
+      h->no_spec = false;
+      if (rc == 100) { bsz = std::max(1, nb / 2); continue; }
+      if (rc != DPQ_OK) return rc;
+      goto copy_out;
+    }
+    if (r > 0 && !h->direct_copy) {
+      par_memcpy(dists + q0 * r, w.h_d, (size_t)nb * r * 8);
+      par_memcpy(ids + q0 * r, w.h_i, (size_t)nb * r * 8);
     }
     if (want_t) {
       const double per = 1000.0 / nb;  // ms per batch -> us per query
@@ -776,6 +828,8 @@ int index_common_init(Index* h, int device, int m, int k, int kbar, int dsub, co
   if (const char* e = getenv("DPQ_SORT_SLOTS")) h->sort_slots = atoi(e) != 0;
   if (const char* e = getenv("DPQ_SORT_ROWS")) h->sort_rows = atoi(e) != 0;
   if (const char* e = getenv("DPQ_RUN_FILTER")) h->run_filter = atoi(e) != 0;
+  if (const char* e = getenv("DPQ_DIRECT_COPY")) h->direct_copy = atoi(e) != 0;
+  if (const char* e = getenv("DPQ_SPECULATE")) h->no_spec = atoi(e) == 0;
   DPQ_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   h->own_stream = true;
   for (int i = 0; i < 8; ++i) DPQ_CUDA(cudaEventCreate(&h->ev[i]));
@@ -827,6 +881,17 @@ extern "C" {
 
 const char* dpq_last_error(void) { return dpq::last_error(); }
 int dpq_abi_version(void) { return 1; }
+int dpq_all_finite(const float* x, int64_t n) {
+  if (!x || n <= 0) return 0;
+  const uint32_t* b = reinterpret_cast<const uint32_t*>(x);
+  uint32_t any_special = 0;  // vectorizable: exponent all ones
+  for (int64_t i = 0; i < n; ++i) any_special |= (uint32_t)((b[i] & 0x7F800000u) == 0x7F800000u);
+  if (!any_special) return 0;
+  for (int64_t i = 0; i < n; ++i)
+    if ((b[i] & 0x7F800000u) == 0x7F800000u && (b[i] & 0x007FFFFFu)) return 1;
+  return 2;
+}
+
 int dpq_device_count(void) {
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess) {
@@ -944,6 +1009,16 @@ int dpq_flat_search_derived_dev(dpq_index_t* index, const float* yr, int64_t nq,
     int rc = flat_derived_batch(h, nb, r, r2);
     if (rc == 100) { bsz = std::max(1, nb / 2); continue; }
     if (rc != DPQ_OK) return rc;
+    if (h->spec_nb) {
+      DPQ_CUDA(cudaStreamSynchronize(h->stream));
+      if (spec_failed(h)) {
+        h->no_spec = true;
+        rc = flat_derived_batch(h, nb, r, r2);
+        h->no_spec = false;
+        if (rc == 100) { bsz = std::max(1, nb / 2); continue; }
+        if (rc != DPQ_OK) return rc;
+      }
+    }
     DPQ_CUDA(cudaMemcpyAsync(dists + q0 * r, w.out_d, (size_t)nb * r * 8, cudaMemcpyDeviceToDevice, h->stream));
     DPQ_CUDA(cudaMemcpyAsync(ids + q0 * r, w.out_i, (size_t)nb * r * 8, cudaMemcpyDeviceToDevice, h->stream));
     q0 += nb;
@@ -996,7 +1071,10 @@ int dpq_debug_candidates(dpq_index_t* index, const float* yr, int64_t nq, int r2
     DPQ_CUDA(cudaMemcpyAsync(w.y, yr + q0 * h->d, (size_t)nb * h->d * 4, cudaMemcpyHostToDevice, h->stream));
     DPQ_TRY(run_small_tables(h, nb, h->prefix, std::min<int64_t>(r2, h->n_prefix), nullptr, nullptr, nullptr,
                              false, nullptr));
+    const bool ns = h->no_spec;
+    h->no_spec = true;  // exact b* needed right here
     int rc = flat_first_pass(h, nb, r2);
+    h->no_spec = ns;
     if (rc == 100) { set_error("debug_candidates: emit budget exceeded, use a smaller batch"); return DPQ_ERR_NOMEM; }
     if (rc != DPQ_OK) return rc;
     DPQ_CUDA(cudaMemcpyAsync(bstar + q0, w.bstar, (size_t)nb * 4, cudaMemcpyDeviceToHost, h->stream));

@@ -110,6 +110,9 @@ struct Index {
   int sort_slots = 1; // flat: order query tiles by guard (env DPQ_SORT_SLOTS=0)
   int sort_rows = 1;  // flat: rows sorted by (g0, g1) at build (env DPQ_SORT_ROWS=0)
   bool rows_sorted = false;
+  bool no_spec = false;  // first pass waits for its flags (no speculative refine)
+  int spec_nb = 0;       // flags of a speculative first pass still to check
+  int direct_copy = 0;  // host API: copy straight from/to the caller's (pageable) buffers (env DPQ_DIRECT_COPY)
   int run_filter = 1;  // flat sorted rows: scan only chunks whose keys can reach a guard (env DPQ_RUN_FILTER=0)
   uint32_t* chunk_keys = nullptr;  // [n_chunks] first | last key << 16 of each 128-row chunk
   int64_t n_chunks = 0;

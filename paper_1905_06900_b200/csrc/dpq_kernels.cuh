@@ -1175,7 +1175,7 @@ __global__ void __launch_bounds__(NT)
   if (only && !only[q]) return;
   const uint32_t n = emit_cnt[q];
   if (n > cap) {
-    if (threadIdx.x == 0) flags[q] = 2;
+    if (threadIdx.x == 0) { flags[q] = 2; bstar[q] = -1; }  // (-1: refine nothing until redone)
     return;
   }
   for (int i = threadIdx.x; i < 256; i += NT) h[i] = 0;
@@ -1203,6 +1203,7 @@ __global__ void __launch_bounds__(NT)
       bstar[q] = 254; ncand[q] = cum; flags[q] = 0;
     } else {
       flags[q] = 1;
+      bstar[q] = -1;
     }
   }
 }

@@ -125,7 +125,7 @@ class FlatIndex(BaseEstimator):
                return_timings: bool = False):
         """Top-r neighbours for each query row (see derivedpq.FlatIndex.search)."""
         check_is_fitted(self, "codes_")
-        Y = check_array(Y, dtype=np.float32, order="C")
+        Y = _lib.query_array(Y)
         if mode not in ("conventional", "derived"):
             raise ValueError(f"unknown mode {mode!r}")
         nq = Y.shape[0]

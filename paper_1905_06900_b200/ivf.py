@@ -116,7 +116,7 @@ class IVFIndex(BaseEstimator):
         """Top-r neighbours of each query over the ma nearest cells
         (see derivedpq.IVFIndex.search, ivf.py:125-160)."""
         check_is_fitted(self, "centers_")
-        Y = check_array(Y, dtype=np.float32, order="C")
+        Y = _lib.query_array(Y)
         if mode not in ("conventional", "derived"):
             raise ValueError(f"unknown mode {mode!r}")
         if mode == "derived":

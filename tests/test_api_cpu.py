@@ -90,3 +90,21 @@ def test_array_quantizer_rotate_matches_reference_semantics():
     X = rng.normal(size=(3, 8)).astype(np.float32)
     assert np.array_equal(q.rotate(X), (X @ R).astype(np.float32))
     assert q.rotate(X).dtype == np.float32
+
+
+def test_non_finite_queries_rejected_like_check_array(flat):
+    """The native finiteness fast path raises sklearn's own messages, NaN
+    before infinity, for flat and ivf searches (flat.py:71, ivf.py:125)."""
+    idx, g = flat
+    Y = np.array(g["queries"][:3], dtype=np.float32)
+    Y[1, 2] = np.inf
+    with pytest.raises(ValueError, match="infinity"):
+        idx.search(Y, 5, mode="derived", r2=20)
+    Y[2, 0] = np.nan
+    with pytest.raises(ValueError, match="NaN"):
+        idx.search(Y, 5)
+    assert _lib.lib().dpq_all_finite(Y[:1].ctypes.data, Y[:1].size) == 0
+    # non-float32 / non-contiguous input still goes through check_array
+    idx2 = FlatIndex.from_arrays(g["codebooks"], g["derived"], g["codes"])
+    with pytest.raises(ValueError, match="NaN"):
+        idx2.search(np.asfortranarray(Y.astype(np.float64)), 5)
