@@ -360,14 +360,14 @@ int run_small_tables(Index* h, int nslot, const void* prefix, int64_t npre,
 int build_lut(Index* h, int nslot, const uint16_t* gword, const int* slot_query) {
   Workspace& w = h->ws;
   const int ntiles = tiles_of(nslot, h->mpad);
-  const int64_t threads = (int64_t)ntiles * h->mpad * 256;
   int* tf = w.tile_fast;  // reset to 0 when gword is null (unclamped LUT)
+  const dim3 grid((unsigned)ntiles, (unsigned)h->mpad);
   if (h->mpad == 4)
-    k_build_lut<4><<<(unsigned)((threads + 255) / 256), 256, 0, h->stream>>>(w.q8, nslot, h->m, h->kbar, w.lut,
-                                                                             ntiles, gword, tf, h->wide, slot_query);
+    k_build_lut<4><<<grid, 256, 0, h->stream>>>(w.q8, nslot, h->m, h->kbar, w.lut, ntiles, gword, tf, h->wide,
+                                                slot_query);
   else
-    k_build_lut<8><<<(unsigned)((threads + 255) / 256), 256, 0, h->stream>>>(w.q8, nslot, h->m, h->kbar, w.lut,
-                                                                             ntiles, gword, tf, h->wide, slot_query);
+    k_build_lut<8><<<grid, 256, 0, h->stream>>>(w.q8, nslot, h->m, h->kbar, w.lut, ntiles, gword, tf, h->wide,
+                                                slot_query);
   DPQ_LAUNCHED(h);
   return DPQ_OK;
 }

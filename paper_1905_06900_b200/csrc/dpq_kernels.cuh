@@ -227,47 +227,62 @@ __global__ void __launch_bounds__(256) k_build_lut(const uint8_t* __restrict__ q
                                                    uint8_t* __restrict__ lut, int ntiles,
                                                    const uint16_t* __restrict__ gword, int* __restrict__ tile_fast,
                                                    int allow_wide, const int* __restrict__ slot_query) {
+  // One CTA per (tile, subspace j): the QT slots' u8 rows of subspace j are
+  // staged in shared memory ([slot][group], rows padded to 65 words so the
+  // transposed reads below are conflict-free), then written as the tile's
+  // 256 table rows of QT bytes with coalesced 32-bit stores.
   using G = ScanGeom<MPAD>;
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid >= (int64_t)ntiles * MPAD * 256) return;
-  const int i = (int)(gid & 255);
-  const int j = (int)((gid >> 8) % MPAD);
-  const int t = (int)(gid / (MPAD * 256));
+  constexpr int RW = 65;  // words per staged row (256 groups + pad)
+  __shared__ uint32_t st[G::QT * RW];
+  __shared__ uint32_t s_bmax;
+  const int t = blockIdx.x, j = blockIdx.y, tid = threadIdx.x;
+  if (tid == 0) s_bmax = 0;
+  __syncthreads();
+  if (gword)
+    for (int qq = tid; qq < G::QT; qq += 256) {
+      const uint32_t gw = gword[t * G::QT + qq];
+      if (gw >= 0x8000u) atomicMax(&s_bmax, gw - 0x8000u);
+    }
+  const bool live_j = j < m;
+  for (int i = tid; i < G::QT * 64; i += 256) {
+    const int sl = i >> 6, w = i & 63;
+    const int slot = t * G::QT + sl;
+    const int q = slot_query ? slot_query[slot] : slot;
+    uint32_t v = 0;
+    if (live_j && q >= 0 && q < nslot && 4 * w < kbar) {
+      const uint8_t* row = q8 + ((int64_t)q * m + j) * kbar;
+      if ((kbar & 3) == 0) v = *reinterpret_cast<const uint32_t*>(row + 4 * w);
+      else
+        for (int b = 0; b < 4 && 4 * w + b < kbar; ++b) v |= (uint32_t)row[4 * w + b] << (8 * b);
+    }
+    st[sl * RW + w] = v;
+  }
+  __syncthreads();
   int mode = kModeGeneric;
   if (gword) {
-    uint32_t bmax = 0;
-    for (int qq = 0; qq < G::QT; ++qq) {
-      const uint32_t gw = gword[t * G::QT + qq];
-      if (gw >= 0x8000u) bmax = max(bmax, gw - 0x8000u);
-    }
+    const uint32_t bmax = s_bmax;
     if (MPAD == 4 && allow_wide && bmax <= 30u) mode = kModeWide5;
     else if (MPAD == 4 && allow_wide && bmax <= 62u) mode = kModeWide6;
     else if (bmax <= kClampMaxGuard) mode = kMode7;
   }
   const uint32_t cmax = mode == kModeWide5 ? 31u : (mode == kModeWide6 ? 63u : (mode == kMode7 ? 127u : 255u));
   const bool fold = mode == kModeWide5 && j == 0;
-  if (tile_fast && i == 0 && j == 0) tile_fast[t] = mode;
-  uint4* dst = reinterpret_cast<uint4*>(lut + (int64_t)t * G::LUT_BYTES +
-                                        (int64_t)((j / G::SPR) * 256 + i) * 256 + (j % G::SPR) * G::ROWB);
-  const bool live = j < m && i < kbar;
+  if (tile_fast && j == 0 && tid == 0) tile_fast[t] = mode;
+  const uint8_t* sb = reinterpret_cast<const uint8_t*>(st);
+  uint8_t* tbase = lut + (int64_t)t * G::LUT_BYTES + (int64_t)(j / G::SPR) * 256 * 256 + (j % G::SPR) * G::ROWB;
+  constexpr int WPR = G::QT / 4;  // 32-bit words per table row
+  for (int i = tid; i < 256 * WPR; i += 256) {
+    const int g = i / WPR, w = i % WPR;
+    uint32_t v = 0;
 #pragma unroll
-  for (int l4 = 0; l4 < G::LPC / 4; ++l4) {
-    uint32_t w[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      uint32_t v = 0;
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const int sl = t * G::QT + 4 * (4 * l4 + u) + b;  // slot
-        const int q = slot_query ? slot_query[sl] : sl;     // its query (-1: padding)
-        uint32_t e = (live && q >= 0 && q < nslot) ? q8[((int64_t)q * m + j) * kbar + i] : 0u;
-        e = min(e, cmax);
-        if (fold) e += wide_bias(gword[sl]);  // <= 31 + 128
-        v |= e << (8 * b);
-      }
-      w[u] = v;
+    for (int b = 0; b < 4; ++b) {
+      const int sl = 4 * w + b;
+      uint32_t e = g < kbar ? (uint32_t)sb[sl * RW * 4 + g] : 0u;
+      e = min(e, cmax);
+      if (fold) e += wide_bias(gword[t * G::QT + sl]);  // <= 31 + 128
+      v |= e << (8 * b);
     }
-    dst[l4] = make_uint4(w[0], w[1], w[2], w[3]);
+    reinterpret_cast<uint32_t*>(tbase + (int64_t)g * 256)[w] = v;
   }
 }
 
