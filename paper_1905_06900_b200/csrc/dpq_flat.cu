@@ -377,6 +377,63 @@ int build_lut(Index* h, int nslot, const uint16_t* gword, const int* slot_query)
 // the rare exact redo and emit overflow.  On return ws.bstar / emit are
 // valid for every query of the batch.
 // ---------------------------------------------------------------------------
+// Flat scan preparation once the guards are known (ws.gword by query):
+// query slots clustered into tiles (k_sort_slots), clamped LUT tiles, and
+// with sorted rows the run-filtered chunk lists.  Shared by the single-GPU
+// first pass and the sharded scan (dpq_shard_scan).
+struct ScanPlan {
+  bool sorted = false, list = false;
+  const uint16_t* gw = nullptr;
+  const int* slot_q = nullptr;
+};
+
+int plan_flat_scan(Index* h, int nb, ScanPlan& sp) {
+  Workspace& w = h->ws;
+  const int tiles = tiles_of(nb, h->mpad);
+  sp.sorted = h->sort_slots && h->wide && h->mpad == 4 && nb > 1;
+  sp.list = h->rows_sorted && h->run_filter && h->m >= 2 && h->mpad == 4 && h->n > 0;
+  if (sp.list && (w.list_tiles < tiles || w.list_chunks < h->n_chunks)) {
+    DPQ_TRY(dmalloc(&w.pot, (size_t)tiles * 65536));
+    DPQ_TRY(dmalloc(&w.chunk_list, (size_t)tiles * h->n_chunks));
+    DPQ_TRY(dmalloc(&w.list_len, (size_t)tiles * 2));  // lengths | handed-out counters
+    w.list_tiles = tiles;
+    w.list_chunks = h->n_chunks;
+  }
+  sp.gw = sp.sorted ? w.gword_p : w.gword;
+  sp.slot_q = sp.sorted ? w.slot_query : nullptr;
+  return DPQ_OK;
+}
+
+int prepare_flat_scan(Index* h, int nb, const ScanPlan& sp) {
+  Workspace& w = h->ws;
+  const int qt = qt_of(h->mpad);
+  const int tiles = tiles_of(nb, h->mpad);
+  if (sp.sorted) {
+    k_sort_slots<<<1, 1024, 0, h->stream>>>(w.gword, w.q8, h->m, h->kbar, nb, tiles * qt, w.slot_query,
+                                            w.gword_p);
+    DPQ_LAUNCHED(h);
+  }
+  DPQ_TRY(build_lut(h, nb, sp.gw, sp.slot_q));  // clamped tiles (modes 5/6/7) where the guards allow
+  if (sp.list) {  // run filter: per tile, the chunks whose (g0, g1) keys can reach a guard
+    DPQ_CUDA(cudaMemsetAsync(w.list_len, 0, (size_t)tiles * 4, h->stream));
+    k_run_potential<<<dim3(64, tiles), 256, (size_t)qt * 64 * 4 + 4 * qt * 4, h->stream>>>(
+        w.q8, h->m, h->kbar, sp.slot_q, sp.gw, qt, nb, w.pot);
+    DPQ_LAUNCHED(h);
+    k_chunk_list<<<dim3((unsigned)((h->n_chunks + 255) / 256), tiles), 256, 0, h->stream>>>(
+        h->chunk_keys, (int)h->n_chunks, w.pot, w.chunk_list, w.list_len, h->n, nb, qt, h->d_nrows);
+    DPQ_LAUNCHED(h);
+  }
+  return DPQ_OK;
+}
+
+void plan_emit_args(Index* h, const ScanPlan& sp, EmitArgs& ea) {
+  ea.gword = sp.gw;
+  ea.slot_query = sp.slot_q;
+  ea.chunk_list = sp.list ? h->ws.chunk_list : nullptr;
+  ea.list_len = h->ws.list_len;
+  ea.list_stride = h->n_chunks;
+}
+
 static int flat_first_pass(Index* h, int nb, int r2) {
   Workspace& w = h->ws;
   const int qt = qt_of(h->mpad);
@@ -393,36 +450,9 @@ static int flat_first_pass(Index* h, int nb, int r2) {
   k_guard<<<(nb + 127) / 128, 128, 0, h->stream>>>(w.hist, nb, r2, lambda, exact ? 1 : 0, nullptr,
                                                     w.guard_b, w.gword, nullptr);
   DPQ_LAUNCHED(h);
-  // query tiles ordered by guard (homogeneous tiles -> more 5-bit wide tiles)
-  const bool sorted = h->sort_slots && h->wide && h->mpad == 4 && nb > 1;
-  const bool use_list = h->rows_sorted && h->run_filter && h->m >= 2 && h->mpad == 4;
-  if (use_list && (w.list_tiles < tiles || w.list_chunks < h->n_chunks)) {
-    DPQ_TRY(dmalloc(&w.pot, (size_t)tiles * 65536));
-    DPQ_TRY(dmalloc(&w.chunk_list, (size_t)tiles * h->n_chunks));
-    DPQ_TRY(dmalloc(&w.list_len, (size_t)tiles * 2));  // lengths | handed-out counters
-    w.list_tiles = tiles;
-    w.list_chunks = h->n_chunks;
-  }
-  const uint16_t* gw_scan = sorted ? w.gword_p : w.gword;
-  const int* slot_q = sorted ? w.slot_query : nullptr;
-  auto sort_and_build = [&]() -> int {
-    if (sorted) {
-      k_sort_slots<<<1, 1024, 0, h->stream>>>(w.gword, w.q8, h->m, h->kbar, nb, tiles * qt, w.slot_query,
-                                              w.gword_p);
-      DPQ_LAUNCHED(h);
-    }
-    DPQ_TRY(build_lut(h, nb, gw_scan, slot_q));  // clamped tiles (modes 5/6/7) where the guards allow
-    if (use_list) {  // run filter: per tile, the chunks whose (g0, g1) keys can reach a guard
-      DPQ_CUDA(cudaMemsetAsync(w.list_len, 0, (size_t)tiles * 4, h->stream));
-      k_run_potential<<<dim3(64, tiles), 256, (size_t)qt * 64 * 4 + 4 * qt * 4, h->stream>>>(
-          w.q8, h->m, h->kbar, slot_q, gw_scan, qt, nb, w.pot);
-      DPQ_LAUNCHED(h);
-      k_chunk_list<<<dim3((unsigned)((h->n_chunks + 255) / 256), tiles), 256, 0, h->stream>>>(
-          h->chunk_keys, (int)h->n_chunks, w.pot, w.chunk_list, w.list_len, h->n, nb, qt, h->d_nrows);
-      DPQ_LAUNCHED(h);
-    }
-    return DPQ_OK;
-  };
+  ScanPlan sp;
+  DPQ_TRY(plan_flat_scan(h, nb, sp));
+  auto sort_and_build = [&]() -> int { return prepare_flat_scan(h, nb, sp); };
   DPQ_TRY(sort_and_build());
   ev_rec(h, 2);
   bool first = true;
@@ -430,13 +460,12 @@ static int flat_first_pass(Index* h, int nb, int r2) {
     DPQ_CUDA(cudaMemsetAsync(w.emit_cnt, 0, (size_t)nb * 4, h->stream));
     EmitArgs ea;
     ea.plane = h->plane; ea.row_begin = 0; ea.row_end = n; ea.rows_per_cta = 0;
-    ea.lut = w.lut; ea.gword = gw_scan; ea.tile_list = nullptr;
-    ea.slot_query = slot_q; ea.slot_probe = nullptr;
-    ea.chunk_list = use_list ? w.chunk_list : nullptr; ea.list_len = w.list_len; ea.list_stride = h->n_chunks;
+    ea.lut = w.lut; ea.tile_list = nullptr; ea.slot_probe = nullptr;
+    plan_emit_args(h, sp, ea);
     ea.unit_tile = nullptr; ea.unit_r0 = nullptr; ea.unit_r1 = nullptr;
     ea.emit_cnt = w.emit_cnt; ea.emit = w.emit; ea.cap = w.cap;
     DPQ_TRY(launch_emit(h, ea, tiles, n));
-    if (!use_list) h->counters[2] += (int64_t)nb * n;  // (list mode: counted on the device)
+    if (!sp.list) h->counters[2] += (int64_t)nb * n;  // (list mode: counted on the device)
     if (first) ev_rec(h, 3);
     k_threshold<256><<<nb, 256, 0, h->stream>>>(w.emit, w.emit_cnt, w.cap, w.guard_b, r2, nullptr,
                                                 w.bstar, w.ncand, w.flags, nullptr, h->d_nemit);

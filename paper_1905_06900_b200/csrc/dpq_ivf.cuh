@@ -761,18 +761,22 @@ int dpq_shard_scan(dpq_index_t* index, const int32_t* sample_hist_sum, int64_t n
   k_guard<<<(nb + 127) / 128, 128, 0, h->stream>>>(w.hist, nb, r2, lambda, ex ? 1 : 0, nullptr, w.guard_b, w.gword,
                                                     nullptr);
   DPQ_LAUNCHED(h);
-  DPQ_TRY(build_lut(h, nb, w.gword));
+  // same scan preparation as the single-GPU first pass (slot clustering,
+  // clamped tiles, run-filtered chunk lists over this shard's sorted rows)
+  ScanPlan sp;
+  DPQ_TRY(plan_flat_scan(h, nb, sp));
+  DPQ_TRY(prepare_flat_scan(h, nb, sp));
   for (int attempt = 0; attempt < 4; ++attempt) {
     DPQ_CUDA(cudaMemsetAsync(w.emit_cnt, 0, (size_t)nb * 4, h->stream));
     if (h->n > 0) {
       EmitArgs ea;
       ea.plane = h->plane; ea.row_begin = 0; ea.row_end = h->n; ea.rows_per_cta = 0;
-      ea.lut = w.lut; ea.gword = w.gword; ea.tile_list = nullptr;
-      ea.slot_query = nullptr; ea.slot_probe = nullptr;
+      ea.lut = w.lut; ea.tile_list = nullptr; ea.slot_probe = nullptr;
+      plan_emit_args(h, sp, ea);
       ea.unit_tile = nullptr; ea.unit_r0 = nullptr; ea.unit_r1 = nullptr;
       ea.emit_cnt = w.emit_cnt; ea.emit = w.emit; ea.cap = w.cap;
       DPQ_TRY(launch_emit(h, ea, tiles, h->n));
-      h->counters[2] += (int64_t)nb * h->n;
+      if (!sp.list) h->counters[2] += (int64_t)nb * h->n;
     }
     k_threshold<256><<<nb, 256, 0, h->stream>>>(w.emit, w.emit_cnt, w.cap, w.guard_b, r2, nullptr, w.bstar,
                                                 w.ncand, w.flags, w.hist_i, h->d_nemit);
