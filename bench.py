@@ -46,7 +46,7 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--n", type=int, default=10_000_000)
+    p.add_argument("--n", "--rows", dest="n", type=int, default=10_000_000)
     p.add_argument("--batch", type=int, default=1024)
     p.add_argument("--r", type=int, default=100)
     p.add_argument("--r2", type=int, default=1000)
@@ -57,6 +57,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--profile-once", action="store_true", help="one short step only (for ncu)")
+    p.add_argument("--mode", default="replicas", choices=["replicas", "shard"],
+                   help="N > 1: query-parallel replicas of the index (default: configs[1] fits one GPU) or "
+                        "the database sharded across GPUs with the NCCL exchange (configs[2]-[4] layout)")
     return p.parse_args()
 
 
@@ -66,7 +69,7 @@ def log(*a):
 
 # ------------------------------------------------------------------ setup --
 
-def build_workload(args, device, rank: int = 0, world: int = 1):
+def build_workload(args, device, rank: int = 0, world: int = 1, shard: bool = True, comm_device=None):
     """Seeded data, GPU-trained 4x16/8 model, GPU-encoded codes, queries,
     exact ground truth.  With world > 1 every rank generates the same
     database (seeded Philox chunks) and encodes only its contiguous shard;
@@ -87,17 +90,18 @@ def build_workload(args, device, rank: int = 0, world: int = 1):
     if world > 1:
         import torch.distributed as dist
 
-        cbt = torch.as_tensor(codebooks, device=device) if rank == 0 else torch.empty(cb_shape, device=device)
-        dt = torch.as_tensor(derived, device=device) if rank == 0 else torch.empty(der_shape, device=device)
+        cd = comm_device if comm_device is not None else device
+        cbt = torch.as_tensor(codebooks, device=cd) if rank == 0 else torch.empty(cb_shape, device=cd)
+        dt = torch.as_tensor(derived, device=cd) if rank == 0 else torch.empty(der_shape, device=cd)
         dist.broadcast(cbt, 0)
         dist.broadcast(dt, 0)
         codebooks, derived = cbt.cpu().numpy(), dt.cpu().numpy()
     t1 = time.time()
     db = datagen.sift_like_torch(args.n, args.seed + 1, centres, device=device)
-    lo, hi = rank * args.n // world, (rank + 1) * args.n // world
+    lo, hi = (rank * args.n // world, (rank + 1) * args.n // world) if shard else (0, args.n)
     codes = train.encode(db[lo:hi], codebooks).to(torch.int32).cpu().numpy().astype(np.uint16)
     prefix = None
-    if world > 1:
+    if world > 1 and shard:
         import torch.distributed as dist
 
         npre = min(args.n, args.r2)
@@ -105,9 +109,16 @@ def build_workload(args, device, rank: int = 0, world: int = 1):
               else torch.empty((npre, M), dtype=torch.int32, device=device))
         dist.broadcast(pt, 0)
         prefix = pt.cpu().numpy().astype(np.uint16)
-    nq = (args.steps + args.warmup) * args.batch
+    nq = (args.steps + args.warmup) * args.batch * (1 if shard else world)
     queries = datagen.sift_like_torch(nq, args.seed + 2, centres, device=device)
-    truth = train.exact_nn_gpu(db, queries, depth=1) if rank == 0 else None
+    if shard:
+        truth = train.exact_nn_gpu(db, queries, depth=1) if rank == 0 else None
+    else:  # replicas: ground truth only for this rank's batches (s * world + rank)
+        Bq = args.batch
+        mine = np.concatenate([np.arange((s * world + rank) * Bq, (s * world + rank + 1) * Bq)
+                               for s in range(args.steps + args.warmup)])
+        truth = np.full((nq, 1), -1, dtype=np.int64)
+        truth[mine] = train.exact_nn_gpu(db, queries[torch.as_tensor(mine, device=device)], depth=1)
     del db
     torch.cuda.empty_cache()
     t2 = time.time()
@@ -120,52 +131,60 @@ def build_workload(args, device, rank: int = 0, world: int = 1):
 # ---------------------------------------------------------------- clocks --
 
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    """SM clock and throttle reasons sampled DURING the timed region: an NVML
+    polling thread (~1 ms period) that has taken its first sample before the
+    region starts and stops right after it (nvidia-smi's >= 100 ms period
+    cannot see a ~10 ms region)."""
+
+    REASONS = (("hw_slowdown", 0x8), ("sw_thermal_slowdown", 0x20), ("hw_thermal_slowdown", 0x40),
+               ("sw_power_cap", 0x4))
 
     def __init__(self, index: int):
         self.index = index
-        self.proc = None
+        self.samples = []
+        self.smax = None
+        self._stop = None
 
     def __enter__(self):
+        import threading
+
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except FileNotFoundError:
-            self.proc = None
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.smax = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # no NVML: report no samples
+            return self
+        self._stop = threading.Event()
+        first = threading.Event()
+
+        def poll():
+            while not self._stop.is_set():
+                try:
+                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.samples.append((sm, rs))
+                except Exception:
+                    pass
+                first.set()
+                time.sleep(0.001)
+
+        self._thread = threading.Thread(target=poll, daemon=True)
+        self._thread.start()
+        first.wait(2.0)
         return self
 
     def __exit__(self, *exc):
-        self.lines = []
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                out, _ = self.proc.communicate(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
-                out, _ = self.proc.communicate()
-            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+        if self._stop is not None:
+            self._stop.set()
+            self._thread.join(2.0)
 
     def summary(self):
-        sm, smax, reasons = [], None, set()
-        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for ln in getattr(self, "lines", []):
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                smax = float(parts[1])
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[3:7]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        sm = [a for a, _ in self.samples]
+        reasons = sorted({nm for _, rs in self.samples for nm, bit in self.REASONS if rs & bit})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.smax,
+                "reasons": reasons, "samples": len(sm), "source": "NVML, ~1 ms polling during the timed steps"}
 
 
 # ------------------------------------------------------------------- CPU --
@@ -230,7 +249,7 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
-        return run_sharded(args, rank, world, local)
+        return run_sharded(args, rank, world, local) if args.mode == "shard" else run_replicas(args, rank, world, local)
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     wl = build_workload(args, device)
@@ -361,6 +380,121 @@ def run_ours(args):
         "clocks": clocks, "setup_s": round(wl["setup_s"], 1),
     }
     print(json.dumps(result), flush=True)
+
+
+def run_replicas(args, rank, world, local):
+    """N > 1 for configs[1]: the 10M index fits one GPU, so queries are the
+    unit of parallelism (tier rule: shard independent units, no data-path
+    collective).  Every rank holds the whole index (codebooks trained on rank
+    0 and broadcast) and searches its own 1024-query batches; the step time is
+    the max over ranks, value = all ranks' queries / that time (weak scaling:
+    per-GPU work is fixed)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1905_06900_b200 import _lib
+    from paper_1905_06900_b200.flat import FlatIndex
+
+    ngpu = max(1, torch.cuda.device_count())
+    local = local % ngpu  # (functional runs with more ranks than GPUs use gloo)
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    nccl = world <= ngpu
+    if nccl:
+        dist.init_process_group("nccl", device_id=device)
+    else:
+        dist.init_process_group("gloo")
+    cdev = device if nccl else torch.device("cpu")
+    wl = build_workload(args, device, rank, world, shard=False, comm_device=cdev)
+    idx = FlatIndex.from_arrays(wl["codebooks"], wl["derived"], wl["codes"], device=local)
+    h = idx._handle()
+    stream = torch.cuda.Stream(device=device)
+    h.set_stream(stream.cuda_stream)
+    h.set_batch(args.batch)
+    Bq, r, r2 = args.batch, args.r, args.r2
+    qdev, qh = wl["queries_dev"], wl["queries"]
+    out_d = torch.empty((Bq, r), dtype=torch.float64, device=device)
+    out_i = torch.empty((Bq, r), dtype=torch.int64, device=device)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+    L = _lib.lib()
+    mine = lambda s: slice((s * world + rank) * Bq, (s * world + rank + 1) * Bq)  # noqa: E731
+    hits = 0
+
+    def step(s):
+        rc = L.dpq_flat_search_derived_dev(h.raw, _lib.ptr(qdev[mine(s)]), Bq, r, r2, _lib.ptr(out_d),
+                                           _lib.ptr(out_i))
+        _lib.check(rc, "search")
+
+    for s in range(args.warmup):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+        step(s)
+    torch.cuda.synchronize()
+    c0 = h.counters()
+    evs = []
+    with ClockSampler(local) as clk:
+        for s in range(args.warmup, args.warmup + args.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            stream.synchronize()
+            dist.barrier()
+            with torch.cuda.stream(stream):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            step(s)
+            with torch.cuda.stream(stream):
+                e1.record(stream)
+            evs.append((e0, e1))
+            stream.synchronize()
+            ids = out_i.cpu().numpy()
+            hits += int((ids == wl["truth"][mine(s), :1]).any(axis=1).sum())
+    c1 = h.counters()
+    dev_ms = sum(a.elapsed_time(b) for a, b in evs)
+    # e2e: the public API with host queries, same per-rank batches
+    wall = 0.0
+    if not args.no_e2e:
+        for s in range(args.warmup):
+            idx.search(qh[mine(s)], r, mode="derived", r2=r2)
+        for s in range(args.warmup, args.warmup + args.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            stream.synchronize()
+            dist.barrier()
+            t0 = time.perf_counter()
+            idx.search(qh[mine(s)], r, mode="derived", r2=r2)
+            wall += time.perf_counter() - t0
+    tot = torch.tensor([dev_ms, wall, c1["launches"] - c0["launches"], hits], dtype=torch.float64, device=cdev)
+    mx = tot.clone()
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    sm = tot.clone()
+    dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+    clocks = clk.summary()
+    if rank == 0:
+        total_ms = float(mx[0])
+        nq = world * args.steps * Bq
+        recall = float(sm[3]) / nq
+        result = {
+            "metric": "queries/s at Recall@100 (flat derived search, PQ 4x16 + derived 4x8, N=10M, r2=1000, k=100)",
+            "value": round(nq / (total_ms / 1e3), 1), "unit": "queries/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u8/u16 scan, f32 tables, f64 distances",
+            "data": "synthetic (seeded SIFT-like stand-in; GPU-trained 4x16/8 codebooks)",
+            "config": {"workload": "BASELINE configs[1] (N=10M fits one GPU): query-parallel replicas",
+                       "n": args.n, "batch": Bq, "r": r, "r2": r2, "recall_at_100": round(recall, 4),
+                       "l2": "flushed (256 MB write) before each timed step",
+                       "parallelism": f"dp{world}: every GPU holds the index and searches its own 1024-query "
+                                      "batches; step time = max over ranks"},
+            "recall_at_100": round(recall, 4),
+            "e2e": None if args.no_e2e else {
+                "value": round(nq / float(mx[1]), 1), "unit": "queries/s",
+                "h2d_bytes_per_step": world * Bq * D * 4, "d2h_bytes_per_step": world * Bq * r * 16,
+                "api": "FlatIndex.search(Y_host, 100, mode='derived', r2=1000) per rank, max wall over ranks"},
+            "gpu_launches": int(sm[2]), "clocks": clocks, "setup_s": round(wl["setup_s"], 1),
+        }
+        print(json.dumps(result), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
 
 
 def run_sharded(args, rank, world, local):
