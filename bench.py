@@ -367,10 +367,13 @@ def run_ours(args):
         "phase_ms": phases,
         "roofline": {"bound": "hbm", "kernel": "k_scan_emit (first-pass scan)",
                      "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 3), "traffic": None,
-                     "note": "algorithmic bytes = N*m*2 B per query x 1024 queries per launch; the scan reads "
-                             "a 4 B/code low-byte plane once per 64-query tile (L2-resident re-reads), so "
-                             "frac > 1 is the query-tiling gain, see DESIGN.md",
+                     "frac": round(achieved / peak, 3), "traffic": scan_traffic(),
+                     "note": "achieved = algorithmic bytes (SURVEY 8d: N*m*2 B of codes per query x 1024 queries "
+                             "per launch) / CUDA-event time of the launch; frac > 1 because one pass over the "
+                             "4 B/code plane serves a 128-query tile, runs of equal (g0, g1) share half the "
+                             "gathers and the run filter skips ~88% of the rows (DESIGN.md 1, 4); traffic = "
+                             "DRAM read + write bytes per launch from profiles/r1_ncu_full_metrics.json, "
+                             "mostly the emitted candidate lists",
                      "per_launch_ms": round(scan_ms, 4)},
         "cpu_baseline": cpu, "parity_sample": parity,
         "e2e": e2e, "gpu_launches": int(launches),
@@ -380,6 +383,19 @@ def run_ours(args):
         "clocks": clocks, "setup_s": round(wl["setup_s"], 1),
     }
     print(json.dumps(result), flush=True)
+
+
+def scan_traffic():
+    """DRAM bytes (read + write) of one k_scan_emit launch, from the
+    committed ncu --set full capture of the same command (profiles/)."""
+    try:
+        prof = json.loads((ROOT / "profiles" / "r1_ncu_full_metrics.json").read_text())
+        for k in prof["kernels"]:
+            if "k_scan_emit" in k["kernel"]:
+                return int(k["traffic_bytes"])
+    except (OSError, ValueError, KeyError):
+        pass
+    return None
 
 
 def run_replicas(args, rank, world, local):
