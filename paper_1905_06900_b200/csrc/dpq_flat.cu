@@ -120,6 +120,7 @@ int ensure_ws(Index* h, int nslot, int r, int ystride, int nq) {
     DPQ_TRY(dmalloc(&w.only, (size_t)std::max(tiles * qt, qn)));
     DPQ_TRY(dmalloc(&w.tile_list, (size_t)tiles));
     DPQ_TRY(dmalloc(&w.order, (size_t)qn));
+    DPQ_TRY(dmalloc(&w.cluster, (size_t)qb));
     DPQ_TRY(dmalloc(&w.tile_fast, (size_t)tiles));
     if (!w.counter) DPQ_TRY(dmalloc(&w.counter, 4));
     DPQ_TRY(dmalloc(&w.slot_query, (size_t)tiles * qt));
@@ -344,6 +345,7 @@ int run_small_tables(Index* h, int nslot, const void* prefix, int64_t npre,
   ta.q8_out = w.q8;  // read by k_group_tables
   ta.qmin_out = w.qmin; ta.qmax_out = w.qmax;
   ta.lut = w.lut; ta.mpad = h->mpad; ta.qt = qt_of(h->mpad);
+  ta.cluster = (!pre_off && h->m >= 2) ? w.cluster : nullptr;  // flat: slot clustering keys
   const size_t smem = (size_t)(h->d + h->m * h->kbar) * 4 + (size_t)h->m * h->kbar + 16;
   static bool attr = false;
   if (!attr) {
@@ -409,8 +411,8 @@ int prepare_flat_scan(Index* h, int nb, const ScanPlan& sp) {
   const int qt = qt_of(h->mpad);
   const int tiles = tiles_of(nb, h->mpad);
   if (sp.sorted) {
-    k_sort_slots<<<1, 1024, 0, h->stream>>>(w.gword, w.q8, h->m, h->kbar, nb, tiles * qt, w.slot_query,
-                                            w.gword_p);
+    k_sort_slots<<<1, 1024, 0, h->stream>>>(w.gword, h->m >= 2 ? w.cluster : nullptr, nb, tiles * qt,
+                                            w.slot_query, w.gword_p);
     DPQ_LAUNCHED(h);
   }
   DPQ_TRY(build_lut(h, nb, sp.gw, sp.slot_q));  // clamped tiles (modes 5/6/7) where the guards allow
@@ -888,7 +890,7 @@ void index_free(Index* h) {
   void* dev[] = {h->cb, h->dcb, h->codes, h->plane, h->own_prefix ? h->prefix : nullptr, h->centers,
                  h->offsets, h->sorted_ids, h->d_nref, h->d_nemit, h->d_nent, h->d_nwide, h->d_nrows, h->chunk_keys, w.pot, w.chunk_list, w.list_len, w.y, w.small, w.q8, w.qmin, w.qmax, w.bounds,
                  w.lut, w.hist, w.hist_i, w.guard_b, w.gword, w.gword_p, w.emit_cnt, w.emit, w.bstar, w.ncand,
-                 w.flags, w.only, w.tile_list, w.order, w.out_d, w.out_i, w.tables, w.slot_query, w.slot_probe,
+                 w.flags, w.only, w.tile_list, w.order, w.cluster, w.out_d, w.out_i, w.tables, w.slot_query, w.slot_probe,
                  w.slot_pre_off, w.slot_pre_len, w.counter, w.tile_fast};
   for (void* p : dev)
     if (p) cudaFree(p);

@@ -35,6 +35,7 @@ struct Workspace {
   uint16_t* guard_b = nullptr;
   uint16_t* gword = nullptr;
   int* order = nullptr;         // refine CTA -> query
+  uint16_t* cluster = nullptr;  // per slot: g0* << 8 | g1* (flat slot clustering)
   uint16_t* gword_p = nullptr;  // guard words in sorted-slot order (flat)
   uint8_t* pot = nullptr;       // run filter: [tiles][65536] key has potential
   int* chunk_list = nullptr;    // [tiles][n_chunks] chunks to scan

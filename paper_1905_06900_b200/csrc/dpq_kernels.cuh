@@ -126,6 +126,7 @@ struct TablesArgs {
   double* qmax_out;        // [nslot]
   uint8_t* lut;            // [tiles][mpad][256][qt] (see lut_index)
   int mpad, qt;
+  uint16_t* cluster = nullptr;  // optional [nslot]: g0* << 8 | g1* (first argmin of the u8 tables)
 };
 
 __global__ void __launch_bounds__(256) k_small_tables(TablesArgs a) {
@@ -191,6 +192,19 @@ __global__ void __launch_bounds__(256) k_small_tables(TablesArgs a) {
   if (tid == 0) {
     a.qmin_out[s] = qmin;
     a.qmax_out[s] = degenerate ? qmin : qmax;
+  }
+  if (a.cluster && a.m >= 2) {  // nearest derived group in subspaces 0 and 1 (slot clustering key)
+    __syncthreads();
+    const int w = tid >> 5, lane = tid & 31;
+    __shared__ uint32_t best[2];
+    if (w < 2) {
+      uint32_t b = 0xFFFFFFFFu;
+      for (int g = lane; g < a.kbar; g += 32) b = min(b, ((uint32_t)q8[w * a.kbar + g] << 16) | (uint32_t)g);
+      b = __reduce_min_sync(0xffffffffu, b);
+      if (lane == 0) best[w] = b & 0xFFu;
+    }
+    __syncthreads();
+    if (tid == 0) a.cluster[s] = (uint16_t)((best[0] << 8) | best[1]);
   }
   __syncthreads();
 }
@@ -295,8 +309,8 @@ __global__ void __launch_bounds__(256) k_build_lut(const uint8_t* __restrict__ q
 // slot_query[s] = query in slot s (-1: padding), gword_p[s] = its guard word.
 // Only the scan layout changes; emit lists stay per query.
 constexpr int kSortMax = 4096;
-__global__ void __launch_bounds__(1024) k_sort_slots(const uint16_t* __restrict__ gword, const uint8_t* __restrict__ q8,
-                                                      int m, int kbar, int nq, int nslot_pad,
+__global__ void __launch_bounds__(1024) k_sort_slots(const uint16_t* __restrict__ gword,
+                                                      const uint16_t* __restrict__ cluster, int nq, int nslot_pad,
                                                       int* __restrict__ slot_query, uint16_t* __restrict__ gword_p) {
   __shared__ uint64_t kv[kSortMax];
   __shared__ int cnt[258];
@@ -305,38 +319,14 @@ __global__ void __launch_bounds__(1024) k_sort_slots(const uint16_t* __restrict_
     const uint32_t gw = gword[q];
     return gw >= 0x8000u ? (int)min(gw - 0x8000u, 255u) : 256;
   };
-  if (q8 && nq <= kSortMax && m >= 2) {
+  if (cluster && nq <= kSortMax) {
     int P = 1;
     while (P < nq) P <<= 1;
-    for (int q = tid; q < P; q += blockDim.x) kv[q] = 0ull;
-    __syncthreads();
-    // first argmin of the 8-bit table of subspace j (j = 0, 1) per query:
-    // one thread per (query, j), 16-B loads; (value << 16 | index) minima
-    for (int i = tid; i < 2 * P; i += blockDim.x) {
-      const int q = i >> 1, j = i & 1;
-      if (q >= nq) continue;
-      const uint8_t* row = q8 + ((int64_t)q * m + j) * kbar;
-      uint32_t b = 0xFFFFFFFFu;
-      if ((kbar & 15) == 0 && (((uintptr_t)row) & 15) == 0) {
-        for (int g = 0; g < kbar; g += 16) {
-          const uint4 v = *reinterpret_cast<const uint4*>(row + g);
-          const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-          for (int u = 0; u < 16; ++u) b = min(b, (((w4[u >> 2] >> (8 * (u & 3))) & 0xFFu) << 16) | (uint32_t)(g + u));
-        }
-      } else {
-        for (int g = 0; g < kbar; ++g) b = min(b, ((uint32_t)row[g] << 16) | (uint32_t)g);
-      }
-      // pack both subspaces into kv (low word = query, filled below)
-      if (j == 0) atomicOr(reinterpret_cast<unsigned long long*>(&kv[q]), (unsigned long long)(b & 0xFFu) << 40);
-      else atomicOr(reinterpret_cast<unsigned long long*>(&kv[q]), (unsigned long long)(b & 0xFFu) << 32);
-    }
-    __syncthreads();
     for (int q = tid; q < P; q += blockDim.x) {
       if (q >= nq) { kv[q] = ~0ull; continue; }
       const int B = gkey(q);
       const uint64_t cls = B == 256 ? 3u : (B <= 30 ? 0u : (B <= 62 ? 1u : 2u));
-      kv[q] = ((kv[q] | (cls << 48)) & ~0xFFFFFFFFull) | (uint32_t)q;
+      kv[q] = (((cls << 16) | cluster[q]) << 32) | (uint32_t)q;
     }
     __syncthreads();
     for (int size = 2; size <= P; size <<= 1) {
@@ -573,11 +563,16 @@ __global__ void __launch_bounds__(NT, 1)
   extern __shared__ __align__(16) uint8_t smem[];
   uint8_t* slut = smem;
   uint32_t* sh = reinterpret_cast<uint32_t*>(smem + G::LUT_BYTES);  // [QT][128] u16 pairs
+  __shared__ __align__(8) uint64_t lut_bar;
   const int tile = tile_list ? tile_list[blockIdx.y] : blockIdx.y;
-  const uint4* src = reinterpret_cast<const uint4*>(lut + (int64_t)tile * G::LUT_BYTES);
-  for (int i = threadIdx.x; i < G::LUT_BYTES / 16; i += NT) reinterpret_cast<uint4*>(slut)[i] = src[i];
+  if (threadIdx.x == 0) {  // the 128-KB tile by one TMA bulk copy while the counters are cleared
+    mbar_init(&lut_bar, 1);
+    mbar_expect_tx(&lut_bar, G::LUT_BYTES);
+    bulk_g2s(slut, lut + (int64_t)tile * G::LUT_BYTES, G::LUT_BYTES, &lut_bar);
+  }
   for (int i = threadIdx.x; i < G::QT * 128; i += NT) sh[i] = 0;
   __syncthreads();
+  mbar_wait(&lut_bar, 0);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int lic = lane % G::LPC, half = lane / G::LPC;
   const uint8_t* L = slut + lic * 4;
