@@ -383,10 +383,22 @@ __global__ void __launch_bounds__(256) k_run_potential(const uint8_t* __restrict
   for (int i = tid; i < qt * 64; i += 256) {
     const int sl = i >> 6, g = (i & 63) * 4;
     const int q = slot_query ? slot_query[tile * qt + sl] : tile * qt + sl;
-    uint32_t w = 0;
-    if (q >= 0 && q < nq)
-      for (int b = 0; b < 4; ++b)
-        w |= (g + b < kbar ? min((uint32_t)q8[((int64_t)q * m + 1) * kbar + g + b], 127u) : 127u) << (8 * b);
+    uint32_t w = 0x7F7F7F7Fu;
+    if (q >= 0 && q < nq) {
+      const uint8_t* row = q8 + ((int64_t)q * m + 1) * kbar;
+      if ((kbar & 3) == 0) {
+        if (g < kbar) {
+          const uint32_t v = *reinterpret_cast<const uint32_t*>(row + g);  // min(e1, 127) per byte
+          const uint32_t hi = v & 0x80808080u;                             // bytes >= 128
+          w = (v & ~(hi | (hi >> 1) | (hi >> 2) | (hi >> 3) | (hi >> 4) | (hi >> 5) | (hi >> 6) | (hi >> 7))) |
+              (hi ? (((hi >> 7) * 0x7Fu) & 0x7F7F7F7Fu) : 0u);
+        }
+      } else {
+        w = 0;
+        for (int b = 0; b < 4; ++b)
+          w |= (g + b < kbar ? min((uint32_t)row[g + b], 127u) : 127u) << (8 * b);
+      }
+    }
     bw[i] = w;
   }
   for (int i = tid; i < 4 * qt; i += 256) {
