@@ -1467,6 +1467,119 @@ __device__ void sort_pairs(uint64_t* keys, int64_t* ids, int P) {
   }
 }
 
+// Radix select of the r smallest (key, id) pairs among buffer[0, f)
+// (keys: non-negative doubles as u64, ids unique), r < f <= NT * EPT.
+// 8-bit digit passes over the key bits that vary within the buffer, stopping
+// as soon as the target's bucket holds one element; remaining key ties are
+// broken by id.  The r kept pairs are compacted to [0, r) (unordered) and
+// (thr_k, thr_i) is set to the r-th pair.  Replaces a full bitonic sort of
+// the buffer: ~EPT shared loads per pass instead of two per stage.
+struct SelShared {
+  uint32_t hist[256];
+  uint64_t red_k[32];
+  int64_t red_i[32];
+  uint64_t pfx, K;
+  int64_t I;
+  int bits, need, done, cnt;
+};
+
+template <int NT, int EPT>
+__device__ void select_r(uint64_t* keys, int64_t* ids, int f, int r, SelShared& S, uint64_t& thr_k,
+                         int64_t& thr_i) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint64_t k[EPT];
+  int64_t v[EPT];
+  uint64_t mn = ~0ull, mx = 0ull;
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    const int i = tid + e * NT;
+    k[e] = i < f ? keys[i] : ~0ull;
+    v[e] = i < f ? ids[i] : INT64_MAX;
+    if (i < f) { mn = min(mn, k[e]); mx = max(mx, k[e]); }
+  }
+  // block min / max of the keys
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = min(mn, (uint64_t)__shfl_xor_sync(0xffffffffu, mn, o));
+    mx = max(mx, (uint64_t)__shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  if (lane == 0) { S.red_k[warp] = mn; S.red_i[warp] = (int64_t)mx; }
+  __syncthreads();
+  if (tid == 0) {
+    uint64_t a = ~0ull, b = 0ull;
+    for (int w = 0; w < NT / 32; ++w) { a = min(a, S.red_k[w]); b = max(b, (uint64_t)S.red_i[w]); }
+    const int bits = a == b ? 0 : 64 - __clzll((long long)(a ^ b));
+    S.bits = bits;
+    S.pfx = bits == 64 ? 0ull : (a >> bits) << bits;
+    S.need = r;
+    S.done = 0;
+  }
+  __syncthreads();
+  // digit passes
+  for (;;) {
+    const int bits = S.bits;
+    if (bits == 0 || S.done) break;
+    const int w = min(8, bits), sft = bits - w;
+    const uint64_t pfx = S.pfx;
+    for (int i = tid; i < 256; i += NT) S.hist[i] = 0;
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < EPT; ++e)
+      if (tid + e * NT < f && (bits == 64 || (k[e] >> bits) == (pfx >> bits)))
+        atomicAdd(&S.hist[(uint32_t)(k[e] >> sft) & ((1u << w) - 1u)], 1u);
+    __syncthreads();
+    if (tid == 0) {
+      int need = S.need, d = 0;
+      uint32_t below = 0;
+      for (; d < (1 << w); ++d) {
+        if (below + S.hist[d] >= (uint32_t)need) break;
+        below += S.hist[d];
+      }
+      S.need = need - (int)below;
+      S.pfx = (bits == 64 ? 0ull : pfx) | ((uint64_t)d << sft);
+      S.bits = sft;
+      S.done = S.hist[d] == 1u;  // the target is the only element of its bucket
+      S.cnt = 0;
+    }
+    __syncthreads();
+  }
+  // resolve the target pair (K, I): unique element of the bucket, or the
+  // need-th smallest id among the elements whose key equals the prefix
+  const int bits = S.bits;
+  const uint64_t pfx = S.pfx;
+  if (tid == 0) { S.cnt = 0; S.I = INT64_MAX; }
+  __syncthreads();
+  if (S.done) {
+#pragma unroll
+    for (int e = 0; e < EPT; ++e)
+      if (tid + e * NT < f && (bits == 64 || (k[e] >> bits) == (pfx >> bits))) { S.K = k[e]; S.I = v[e]; }
+  } else {
+    // all remaining keys equal pfx; ties by id (rare): rank ids among them
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      if (tid + e * NT < f && k[e] == pfx) {
+        int rank = 0;
+        for (int j = 0; j < f; ++j) rank += (keys[j] == pfx && ids[j] < v[e]) ? 1 : 0;
+        if (rank == S.need - 1) { S.K = pfx; S.I = v[e]; }
+      }
+    }
+  }
+  __syncthreads();
+  const uint64_t K = S.K;
+  const int64_t I = S.I;
+  // compact the kept pairs (registers -> [0, r))
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    if (tid + e * NT < f && !pair_less(K, I, k[e], v[e])) {  // (k, v) <= (K, I)
+      const int p = atomicAdd(&S.cnt, 1);
+      keys[p] = k[e];
+      ids[p] = v[e];
+    }
+  }
+  if (tid == 0) { thr_k = K; thr_i = I; }
+  __syncthreads();
+}
+
 template <int DSUB>
 __device__ __forceinline__ float entry_dist(const float* cbrow, const float* ys, int dsub) {
   if constexpr (DSUB > 0) return pw_sqdist_fixed<DSUB>(cbrow, ys);
@@ -1474,7 +1587,7 @@ __device__ __forceinline__ float entry_dist(const float* cbrow, const float* ys,
 }
 
 template <int BUF, int NT, int MODE, int DSUB>
-__global__ void __launch_bounds__(NT) k_refine_topk(RefineArgs a) {
+__global__ void __launch_bounds__(NT, 6) k_refine_topk(RefineArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   uint64_t* keys = reinterpret_cast<uint64_t*>(smem);
   int64_t* ids = reinterpret_cast<int64_t*>(keys + BUF);
@@ -1584,16 +1697,24 @@ __global__ void __launch_bounds__(NT) k_refine_topk(RefineArgs a) {
     // most U * NT <= BUF / 2 entries): early, small sorts tighten the
     // threshold sooner than waiting for a full buffer
     if (f >= BUF - U * NT || (f >= 2 * a.r && f >= (BUF - U * NT) / 2 && thr_k == ~0ull)) {
-      const int P = pow2_at_least(f);
-      for (int i = f + threadIdx.x; i < P; i += NT) { keys[i] = ~0ull; ids[i] = INT64_MAX; }
-      __syncthreads();
-      sort_pairs<NT>(keys, ids, P);
-      if (threadIdx.x == 0) {
-        const int nf = min(f, a.r);
-        fill = nf;
-        if (nf == a.r) { thr_k = keys[nf - 1]; thr_i = ids[nf - 1]; }
+      if (BUF == NT * 4 && f > a.r) {
+        // keep the r smallest (unordered) and set the threshold: radix select
+        __shared__ SelShared sel;
+        select_r<NT, BUF / NT>(keys, ids, f, a.r, sel, thr_k, thr_i);
+        if (threadIdx.x == 0) fill = a.r;
+        __syncthreads();
+      } else {
+        const int P = pow2_at_least(f);
+        for (int i = f + threadIdx.x; i < P; i += NT) { keys[i] = ~0ull; ids[i] = INT64_MAX; }
+        __syncthreads();
+        sort_pairs<NT>(keys, ids, P);
+        if (threadIdx.x == 0) {
+          const int nf = min(f, a.r);
+          fill = nf;
+          if (nf == a.r) { thr_k = keys[nf - 1]; thr_i = ids[nf - 1]; }
+        }
+        __syncthreads();
       }
-      __syncthreads();
     }
   }
   const int f = fill;
