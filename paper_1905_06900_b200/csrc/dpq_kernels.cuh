@@ -1592,13 +1592,13 @@ __global__ void __launch_bounds__(NT, 6) k_refine_topk(RefineArgs a) {
   uint64_t* keys = reinterpret_cast<uint64_t*>(smem);
   int64_t* ids = reinterpret_cast<int64_t*>(keys + BUF);
   float* ys = reinterpret_cast<float*>(ids + BUF);
-  __shared__ int fill;
+  __shared__ int cnt3[3];  // insert counters, round r uses cnt3[r % 3] (one barrier per round)
   __shared__ uint64_t thr_k;
   __shared__ int64_t thr_i;
   __shared__ unsigned nref;
   const int q = a.order ? a.order[blockIdx.x] : blockIdx.x;
   for (int i = threadIdx.x; i < a.ystride; i += NT) ys[i] = a.y[(int64_t)q * a.ystride + i];
-  if (threadIdx.x == 0) { fill = 0; thr_k = ~0ull; thr_i = INT64_MAX; nref = 0; }
+  if (threadIdx.x == 0) { cnt3[0] = cnt3[1] = cnt3[2] = 0; thr_k = ~0ull; thr_i = INT64_MAX; nref = 0; }
   __syncthreads();
   const int d = a.m * a.dsub;
   int64_t ntot;
@@ -1666,7 +1666,9 @@ __global__ void __launch_bounds__(NT, 6) k_refine_topk(RefineArgs a) {
     }
   };
   load_e(0);
-  for (int64_t base = 0; base < ntot; base += (int64_t)U * NT) {
+  int fb = 0;   // buffer fill before this round (same value in every thread)
+  int rnd = 0;  // round index mod 3
+  for (int64_t base = 0; base < ntot; base += (int64_t)U * NT, rnd = rnd == 2 ? 0 : rnd + 1) {
     uint64_t key[U], cur[U];
     int64_t id[U];
     bool keep[U];
@@ -1685,14 +1687,17 @@ __global__ void __launch_bounds__(NT, 6) k_refine_topk(RefineArgs a) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       if (keep[u]) {
-        const int p = atomicAdd(&fill, 1);
+        const int p = fb + atomicAdd(&cnt3[rnd], 1);
         keys[p] = key[u];
         ids[p] = id[u];
       }
     }
     __syncthreads();
-    const int f = fill;
-    __syncthreads();
+    // every thread reads this round's counter after the barrier; the counter
+    // of round + 2 (last read before this barrier) is cleared for reuse
+    const int f = fb + cnt3[rnd];
+    if (threadIdx.x == 0) cnt3[rnd == 0 ? 2 : rnd - 1] = 0;
+    fb = f;
     // sort + truncate once the buffer is half full (the next round adds at
     // most U * NT <= BUF / 2 entries): early, small sorts tighten the
     // threshold sooner than waiting for a full buffer
@@ -1701,23 +1706,19 @@ __global__ void __launch_bounds__(NT, 6) k_refine_topk(RefineArgs a) {
         // keep the r smallest (unordered) and set the threshold: radix select
         __shared__ SelShared sel;
         select_r<NT, BUF / NT>(keys, ids, f, a.r, sel, thr_k, thr_i);
-        if (threadIdx.x == 0) fill = a.r;
-        __syncthreads();
+        fb = a.r;
       } else {
         const int P = pow2_at_least(f);
         for (int i = f + threadIdx.x; i < P; i += NT) { keys[i] = ~0ull; ids[i] = INT64_MAX; }
         __syncthreads();
         sort_pairs<NT>(keys, ids, P);
-        if (threadIdx.x == 0) {
-          const int nf = min(f, a.r);
-          fill = nf;
-          if (nf == a.r) { thr_k = keys[nf - 1]; thr_i = ids[nf - 1]; }
-        }
+        fb = min(f, a.r);
+        if (threadIdx.x == 0 && fb == a.r) { thr_k = keys[fb - 1]; thr_i = ids[fb - 1]; }
         __syncthreads();
       }
     }
   }
-  const int f = fill;
+  const int f = fb;
   const int P = pow2_at_least(f);
   for (int i = f + threadIdx.x; i < P; i += NT) { keys[i] = ~0ull; ids[i] = INT64_MAX; }
   __syncthreads();
