@@ -12,6 +12,7 @@
 #include <omp.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -59,8 +60,11 @@ static constexpr int kScanThreads = 1024;
 static constexpr int kEmitThreads = 1024;  // (512 x 128 registers measured slower)
 static constexpr int kTopThreads = 256;
 
-template <class T>
+static uint64_t g_alloc_epoch = 0;  // bumped by every device (re)allocation (invalidates captured graphs)
+
+template <typename T>
 static int dmalloc(T** p, size_t count) {
+  ++g_alloc_epoch;
   if (*p) { cudaFree(*p); *p = nullptr; }
   if (count == 0) count = 1;
   cudaError_t e = cudaMalloc((void**)p, count * sizeof(T));
@@ -581,7 +585,58 @@ int run_group_tables(Index* h, int nq, int ystride) {
 
 // One flat derived batch: queries already in ws.y (nb rows), results into
 // ws.out_d / ws.out_i.  Returns 100 when the batch must be split.
+static int flat_derived_batch_body(Index* h, int nb, int r, int r2);
+
+// One flat derived batch.  The speculative pipeline (no host decision until
+// the flags come back with the results) is captured once per (batch size,
+// r, r2, allocation epoch) into a CUDA graph and replayed: one launch instead
+// of ~20 kernel launches and memsets per batch.  The first call with a new
+// configuration runs eagerly (it sizes every buffer), the second captures.
 static int flat_derived_batch(Index* h, int nb, int r, int r2) {
+  const bool graphable = h->use_graph && !h->timing && !h->no_spec;
+  if (!graphable) return flat_derived_batch_body(h, nb, r, r2);
+  BatchGraph& G = h->graph;
+  const bool same = G.nb == nb && G.r == r && G.r2 == r2 && G.epoch == g_alloc_epoch;
+  if (G.exec && same) {
+    DPQ_CUDA(cudaGraphLaunch(G.exec, h->stream));
+    for (int i = 0; i < 8; ++i) h->counters[i] += G.counters[i];
+    h->spec_nb = nb;
+    return DPQ_OK;
+  }
+  if (!same || !G.warm) {  // eager run; capture on the next call with this configuration
+    if (G.exec) { cudaGraphExecDestroy(G.exec); G.exec = nullptr; }
+    const int rc = flat_derived_batch_body(h, nb, r, r2);
+    G.nb = nb; G.r = r; G.r2 = r2; G.epoch = g_alloc_epoch; G.warm = rc == DPQ_OK;
+    return rc;
+  }
+  int64_t c0[8];
+  for (int i = 0; i < 8; ++i) c0[i] = h->counters[i];
+  DPQ_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+  const int rc = flat_derived_batch_body(h, nb, r, r2);
+  cudaGraph_t graph = nullptr;
+  const cudaError_t ce = cudaStreamEndCapture(h->stream, &graph);
+  if (rc != DPQ_OK || ce != cudaSuccess || G.epoch != g_alloc_epoch) {
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    G.warm = false;
+    h->use_graph = 0;  // something in the pipeline is not capturable: stay eager
+    return flat_derived_batch_body(h, nb, r, r2);
+  }
+  for (int i = 0; i < 8; ++i) G.counters[i] = h->counters[i] - c0[i];
+  const cudaError_t ie = cudaGraphInstantiate(&G.exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (ie != cudaSuccess) {
+    cudaGetLastError();
+    G.exec = nullptr;
+    h->use_graph = 0;
+    return flat_derived_batch_body(h, nb, r, r2);
+  }
+  DPQ_CUDA(cudaGraphLaunch(G.exec, h->stream));
+  h->spec_nb = nb;
+  return DPQ_OK;
+}
+
+static int flat_derived_batch_body(Index* h, int nb, int r, int r2) {
   ev_rec(h, 0);
   const int64_t npre = std::min<int64_t>(r2, h->n_prefix);
   DPQ_TRY(run_small_tables(h, nb, h->prefix, npre, nullptr, nullptr, nullptr, false, nullptr));
@@ -644,16 +699,22 @@ static int flat_conventional_batch(Index* h, int nb, int r) {
 // memory, calls `batch(nb)` and copies results back.
 // Host staging copies (queries in, results out) split over a few OpenMP
 // threads: one thread moves ~20 GB/s, a 1024-query batch is ~2 MB.
-static void par_memcpy(void* dst, const void* src, size_t bytes) {
+static void par_memcpy2(void* d0, const void* s0, size_t b0, void* d1, const void* s1, size_t b1) {
   constexpr size_t kMin = 256 << 10;
-  if (bytes < kMin) { memcpy(dst, src, bytes); return; }
-  const int nt = (int)std::min<size_t>(8, bytes / (kMin / 2));
+  const size_t tot = b0 + b1;
+  if (tot < kMin) { memcpy(d0, s0, b0); if (b1) memcpy(d1, s1, b1); return; }
+  const int nt = (int)std::min<size_t>(8, tot / (kMin / 2));
 #pragma omp parallel for num_threads(nt) schedule(static)
-  for (int t = 0; t < nt; ++t) {
-    const size_t a = bytes * t / nt, b = bytes * (t + 1) / nt;
-    memcpy((char*)dst + a, (const char*)src + a, b - a);
+  for (int t = 0; t < nt; ++t) {  // thread t copies bytes [a, b) of the concatenation
+    const size_t a = tot * t / nt, b = tot * (t + 1) / nt;
+    if (a < b0) memcpy((char*)d0 + a, (const char*)s0 + a, std::min(b, b0) - a);
+    if (b > b0) {
+      const size_t a1 = std::max(a, b0) - b0, e1 = b - b0;
+      memcpy((char*)d1 + a1, (const char*)s1 + a1, e1 - a1);
+    }
   }
 }
+static void par_memcpy(void* dst, const void* src, size_t bytes) { par_memcpy2(dst, src, bytes, nullptr, nullptr, 0); }
 
 // After a stream sync: did the last speculative first pass flag a query?
 // (clears the pending state either way)
@@ -670,6 +731,10 @@ static int host_driver(Index* h, const float* y, int64_t nq, int r, int batch_li
                        int64_t* ids, double* phase_us, F&& batch) {
   int bsz = std::max(1, std::min<int>(h->batch, batch_limit));
   int64_t q0 = 0;
+  static const bool trace = getenv("DPQ_HOST_TRACE") != nullptr;  // per-segment host timings (stderr)
+  auto now = []() { return std::chrono::duration<double, std::micro>(
+                        std::chrono::steady_clock::now().time_since_epoch()).count(); };
+  double t_0 = trace ? now() : 0.0, t_in = 0, t_enq = 0, t_sync = 0;
   while (q0 < nq) {
     const int nb = (int)std::min<int64_t>(bsz, nq - q0);
     DPQ_TRY(ensure_ws(h, nb, r, h->d, -1));
@@ -683,7 +748,9 @@ static int host_driver(Index* h, const float* y, int64_t nq, int r, int batch_li
     const bool want_t = phase_us != nullptr;
     const bool old_t = h->timing;
     if (want_t) h->timing = true;
+    if (trace) t_in = now();
     int rc = batch(nb);
+    if (trace) t_enq = now();
     h->timing = old_t;
     if (rc == 100) {  // split
       bsz = std::max(1, nb / 2);
@@ -703,6 +770,7 @@ static int host_driver(Index* h, const float* y, int64_t nq, int r, int batch_li
       }
       DPQ_CUDA(cudaStreamSynchronize(h->stream));
     }
+    if (trace) t_sync = now();
     if (!redo && spec_failed(h)) {  // a speculative batch had a flagged query: redo it exactly
       redo = true;
       h->no_spec = true;
@@ -713,8 +781,13 @@ static int host_driver(Index* h, const float* y, int64_t nq, int r, int batch_li
       goto copy_out;
     }
     if (r > 0 && !h->direct_copy) {
-      par_memcpy(dists + q0 * r, w.h_d, (size_t)nb * r * 8);
-      par_memcpy(ids + q0 * r, w.h_i, (size_t)nb * r * 8);
+      par_memcpy2(dists + q0 * r, w.h_d, (size_t)nb * r * 8, ids + q0 * r, w.h_i, (size_t)nb * r * 8);
+    }
+    if (trace) {
+      const double t_out = now();
+      fprintf(stderr, "[dpq host] in %.1f us | enqueue %.1f us | wait %.1f us | out %.1f us | total %.1f us\n",
+              t_in - t_0, t_enq - t_in, t_sync - t_enq, t_out - t_sync, t_out - t_0);
+      t_0 = t_out;
     }
     if (want_t) {
       const double per = 1000.0 / nb;  // ms per batch -> us per query
@@ -861,6 +934,7 @@ int index_common_init(Index* h, int device, int m, int k, int kbar, int dsub, co
   if (const char* e = getenv("DPQ_RUN_FILTER")) h->run_filter = atoi(e) != 0;
   if (const char* e = getenv("DPQ_DIRECT_COPY")) h->direct_copy = atoi(e) != 0;
   if (const char* e = getenv("DPQ_SPECULATE")) h->no_spec = atoi(e) == 0;
+  if (const char* e = getenv("DPQ_GRAPH")) h->use_graph = atoi(e) != 0;
   DPQ_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   h->own_stream = true;
   for (int i = 0; i < 8; ++i) DPQ_CUDA(cudaEventCreate(&h->ev[i]));
@@ -886,6 +960,7 @@ void index_free(Index* h) {
   cudaSetDevice(h->device);
   ivf_free(h);
   if (h->stream) cudaStreamSynchronize(h->stream);
+  if (h->graph.exec) cudaGraphExecDestroy(h->graph.exec);
   Workspace& w = h->ws;
   void* dev[] = {h->cb, h->dcb, h->codes, h->plane, h->own_prefix ? h->prefix : nullptr, h->centers,
                  h->offsets, h->sorted_ids, h->d_nref, h->d_nemit, h->d_nent, h->d_nwide, h->d_nrows, h->chunk_keys, w.pot, w.chunk_list, w.list_len, w.y, w.small, w.q8, w.qmin, w.qmax, w.bounds,

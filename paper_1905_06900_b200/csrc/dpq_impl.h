@@ -69,6 +69,14 @@ struct Workspace {
   size_t h_y_bytes = 0, h_out_elems = 0;
 };
 
+struct BatchGraph {
+  cudaGraphExec_t exec = nullptr;
+  int nb = -1, r = -1, r2 = -1;
+  uint64_t epoch = 0;
+  bool warm = false;
+  int64_t counters[8] = {};  // host counter increments of one captured batch
+};
+
 struct Index {
   int device = 0;
   int kind = KIND_FLAT;
@@ -112,6 +120,8 @@ struct Index {
   int sort_rows = 1;  // flat: rows sorted by (g0, g1) at build (env DPQ_SORT_ROWS=0)
   bool rows_sorted = false;
   bool no_spec = false;  // first pass waits for its flags (no speculative refine)
+  int use_graph = 1;     // replay speculative batches as a CUDA graph (env DPQ_GRAPH=0 disables)
+  BatchGraph graph;
   int spec_nb = 0;       // flags of a speculative first pass still to check
   int direct_copy = 0;  // host API: copy straight from/to the caller's (pageable) buffers (env DPQ_DIRECT_COPY)
   int run_filter = 1;  // flat sorted rows: scan only chunks whose keys can reach a guard (env DPQ_RUN_FILTER=0)
