@@ -271,7 +271,9 @@ def run_ours(args):
         rc = L.dpq_flat_search_derived_dev(h.raw, _lib.ptr(q), Bq, r, r2, _lib.ptr(out_d), _lib.ptr(out_i))
         _lib.check(rc, "search")
 
-    h.set_timing(True)
+    # timed steps run as a caller's would: no phase events, so batches replay
+    # as a CUDA graph (the first warm-up call sizes buffers, the second captures)
+    h.set_timing(False)
     for s in range(args.warmup):
         with torch.cuda.stream(stream):
             flush.zero_()
@@ -280,7 +282,6 @@ def run_ours(args):
     c0 = h.counters()
     torch.cuda.synchronize()
     evs = []
-    phase = []
     with ClockSampler(local) as clk:
         for s in range(args.warmup, args.warmup + args.steps):
             with torch.cuda.stream(stream):
@@ -292,10 +293,20 @@ def run_ours(args):
             with torch.cuda.stream(stream):
                 e1.record(stream)
             evs.append((e0, e1))
-            phase.append(h.phase_ms().copy())
             all_ids[s * Bq:(s + 1) * Bq] = out_i.cpu().numpy()
         torch.cuda.synchronize()
     c1 = h.counters()
+    # per-phase CUDA-event times (incl. the scan launch for the roofline) from
+    # a separate instrumented pass over the first timed batches
+    phase = []
+    h.set_timing(True)
+    for s in range(args.warmup, args.warmup + min(args.steps, 3)):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+        step(s)
+        phase.append(h.phase_ms().copy())
+    h.set_timing(False)
+    torch.cuda.synchronize()
     step_ms = [a.elapsed_time(b) for a, b in evs]
     total_ms = sum(step_ms)
     phase = np.array(phase)
@@ -318,8 +329,9 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e:
         qh = wl["queries"]
-        times, dev_ms = [], []
-        for s in range(args.warmup):  # untimed e2e warm-up (first-call imports, pinned staging)
+        times = []
+        h.set_timing(False)  # a caller's search has no phase events (return_timings=False)
+        for s in range(args.warmup):  # untimed e2e warm-up (first-call imports, pinned staging, graph)
             idx.search(qh[s * Bq:(s + 1) * Bq], r, mode="derived", r2=r2)
         for s in range(args.warmup, args.warmup + args.steps):
             with torch.cuda.stream(stream):
@@ -328,11 +340,10 @@ def run_ours(args):
             t0 = time.perf_counter()
             d, i = idx.search(qh[s * Bq:(s + 1) * Bq], r, mode="derived", r2=r2)
             times.append(time.perf_counter() - t0)
-            dev_ms.append(float(h.phase_ms()[6]))
             assert np.array_equal(i, all_ids[s * Bq:(s + 1) * Bq]), "e2e results differ from device run"
         e2e = {"value": args.steps * Bq / sum(times), "unit": "queries/s",
                "h2d_bytes_per_step": Bq * D * 4, "d2h_bytes_per_step": Bq * r * 16,
-               "step_ms": [round(1e3 * t, 3) for t in times], "device_batch_ms": [round(x, 3) for x in dev_ms],
+               "step_ms": [round(1e3 * t, 3) for t in times],
                "api": "FlatIndex.search(Y_host, 100, mode='derived', r2=1000) -> libdpq C ABI"}
     # comparator: conventional 16-bit search (flat.py:82-93) on a query sample
     nconv = min(256, args.steps * Bq)
