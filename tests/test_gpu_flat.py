@@ -335,3 +335,29 @@ def test_run_filter_on_encoded_data_vs_oracle(monkeypatch):
     assert np.array_equal(i1, i2) and _same(d1, d2)
     d0, i0 = _oracle(cb, der, codes, Y[:30], 25, 100)
     assert np.array_equal(i0, i1[:30]) and _same(d0, d1[:30])
+
+
+def test_graph_replay_and_speculation_match_eager(monkeypatch):
+    """Repeated batches replay a captured CUDA graph of the speculative first
+    pass; results equal the eager, non-speculative pipeline bit for bit, and a
+    batch whose speculative pass is flagged (tiny guard sample -> exact redo)
+    is redone exactly."""
+    cb, der, codes, Y = _sift_setup(90_000, 64, seed=15)
+    idx = FlatIndex.from_arrays(cb, der, codes)
+    outs = [idx.search(Y, 12, mode="derived", r2=200) for _ in range(4)]  # eager, capture, replay, replay
+    for d, i in outs[1:]:
+        assert np.array_equal(i, outs[0][1]) and _same(d, outs[0][0])
+    monkeypatch.setenv("DPQ_GRAPH", "0")
+    monkeypatch.setenv("DPQ_SPECULATE", "0")
+    idx2 = FlatIndex.from_arrays(cb, der, codes)
+    d2, i2 = idx2.search(Y, 12, mode="derived", r2=200)
+    assert np.array_equal(i2, outs[0][1]) and _same(d2, outs[0][0])
+    monkeypatch.delenv("DPQ_GRAPH")
+    monkeypatch.delenv("DPQ_SPECULATE")
+    monkeypatch.setenv("DPQ_GUARD_SAMPLE", "8")
+    monkeypatch.setenv("DPQ_EXACT_LIMIT", "0")
+    idx3 = FlatIndex.from_arrays(cb, der, codes)
+    for _ in range(3):
+        d3, i3 = idx3.search(Y, 12, mode="derived", r2=200)
+        assert np.array_equal(i3, outs[0][1]) and _same(d3, outs[0][0])
+    assert idx3._handle().counters()["fallbacks"] > 0
