@@ -182,6 +182,28 @@ int dpq_debug_candidates(dpq_index_t* index, const float* yr, int64_t nq,
 int dpq_debug_full_tables(dpq_index_t* index, const float* yr, int64_t nq,
                           float* tables);
 
+/* ------------------------------------------------------------ encoder --
+ * Nearest-centroid encoding on the tensor cores (tcgen05, 3xTF32): replaces
+ * ProductQuantizer._encode_with (quantizer.py:75-83) -> nearest_centroids
+ * (clustering.py:53-77): code[i,j] = argmin_c ||x[i, j*dsub:(j+1)*dsub] -
+ * codebooks[j,c]||^2, ties to the lowest index.  Also the IVF coarse
+ * assignment (ivf.py:83-101) with m = 1.  The reference's cross term is an
+ * f32 BLAS GEMM, so near-ties (equal at f32 rounding) may pick a different
+ * minimiser; every other row agrees.  Requires dsub <= 32.
+ *   dpq_encoder_create: codebooks (m,k,dsub) f32 host; the handle owns the
+ *     prepared device operand.
+ *   dpq_encode:     x (n, m*dsub) f32 host -> codes (n, m) u16 host (k <= 65536).
+ *   dpq_encode_dev: x device (n rows, row stride ldx floats) -> codes (n, m)
+ *     i32 device, enqueued on `stream` (NULL: the encoder's own stream).   */
+typedef struct dpq_encoder dpq_encoder_t;
+int dpq_encoder_create(int device, int m, int k, int dsub,
+                       const float* codebooks, dpq_encoder_t** out);
+void dpq_encoder_destroy(dpq_encoder_t* enc);
+int dpq_encode(dpq_encoder_t* enc, const float* x, int64_t n,
+               uint16_t* codes);
+int dpq_encode_dev(dpq_encoder_t* enc, const float* x, int64_t n,
+                   int64_t ldx, int32_t* codes, void* stream);
+
 /* ------------------------------------------------------- measurement --
  * Milliseconds of the last batch's phases when timing is enabled:
  * [0] tables (K1), [1] sample+guard, [2] scan (K2), [3] threshold (K3),

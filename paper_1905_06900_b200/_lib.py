@@ -53,6 +53,10 @@ SIGNATURES = {
     "dpq_debug_low_scores": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_void_p]),
     "dpq_debug_candidates": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_void_p, c_void_p]),
     "dpq_debug_full_tables": (c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
+    "dpq_encoder_create": (c_int, [c_int, c_int, c_int, c_int, c_void_p, POINTER(c_void_p)]),
+    "dpq_encoder_destroy": (None, [c_void_p]),
+    "dpq_encode": (c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
+    "dpq_encode_dev": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
     "dpq_last_phase_ms": (c_int, [c_void_p, c_void_p]),
     "dpq_counters": (c_int, [c_void_p, c_void_p]),
 }
@@ -211,3 +215,37 @@ def query_array(Y):
     from sklearn.utils.validation import check_array
 
     return check_array(Y, dtype=np.float32, order="C")
+
+
+class Encoder:
+    """Owns one dpq_encoder_t* (tensor-core nearest-centroid encoder)."""
+
+    def __init__(self, codebooks, device: int = 0):
+        require_device(device)
+        cb = _c(codebooks, np.float32)
+        self.m, self.k, self.dsub = cb.shape
+        self.device = device
+        out = c_void_p()
+        check(lib().dpq_encoder_create(int(device), self.m, self.k, self.dsub, ptr(cb), ctypes.byref(out)),
+              "dpq_encoder_create")
+        self.raw = out
+
+    def __del__(self):
+        raw = getattr(self, "raw", None)
+        if raw and _lib is not None:
+            _lib.dpq_encoder_destroy(raw)
+            self.raw = None
+
+    def encode(self, x) -> np.ndarray:
+        """(n, m*dsub) f32 host -> (n, m) uint16 codes."""
+        x = _c(x, np.float32)
+        if x.ndim != 2 or x.shape[1] != self.m * self.dsub:
+            raise ValueError(f"expected (n, {self.m * self.dsub}) input, got {x.shape}")
+        out = np.empty((x.shape[0], self.m), np.uint16)
+        check(lib().dpq_encode(self.raw, ptr(x), int(x.shape[0]), ptr(out)), "dpq_encode")
+        return out
+
+    def encode_dev(self, x, codes, stream_ptr: int | None = None) -> None:
+        """x: CUDA tensor (n, >= m*dsub) f32 row-major; codes: CUDA int32 (n, m)."""
+        check(lib().dpq_encode_dev(self.raw, ptr(x), int(x.shape[0]), int(x.stride(0)), ptr(codes),
+                                   c_void_p(stream_ptr) if stream_ptr else None), "dpq_encode_dev")

@@ -111,6 +111,27 @@ def encode(x: torch.Tensor, codebooks: np.ndarray, chunk: int = 16384) -> torch.
     return out
 
 
+def make_encoder(codebooks: np.ndarray, device=None, kind: str = "torch"):
+    """x (n, m*dsub) f32 cuda tensor -> (n, m) int32 codes."""
+    if kind == "torch":
+        return lambda x: encode(x, codebooks)
+    if kind == "tc":  # tcgen05 3xTF32 GEMM + argmin (libdpq dpq_encode_dev)
+        from . import _lib
+
+        dev = torch.device(device) if device is not None else torch.device("cuda", 0)
+        enc = _lib.Encoder(codebooks, device=dev.index or 0)
+
+        def run(x):
+            x = x.contiguous()
+            out = torch.empty((x.shape[0], enc.m), dtype=torch.int32, device=x.device)
+            enc.encode_dev(x, out, torch.cuda.current_stream(x.device).cuda_stream)
+            return out
+
+        run.encoder = enc
+        return run
+    raise ValueError(f"unknown encoder {kind!r}")
+
+
 def exact_nn_gpu(db: torch.Tensor, queries: torch.Tensor, depth: int = 1, short: int = 16,
                  qchunk: int = 2048, dchunk: int = 1 << 21) -> np.ndarray:
     """Exact rank-ordered neighbours (evaluation.py:28-62 semantics)."""

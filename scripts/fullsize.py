@@ -1,0 +1,275 @@
+"""Full-size parity runs at BASELINE.json's configs (GPU), checked through
+size-independent properties plus a sampled bit-exact comparison with the
+CPU oracle.
+
+    python scripts/fullsize.py --config c3 [--n 100000000] [--queries 1024] [--check 4]
+
+Configs (BASELINE.json configs[1..4], one GPU holds the whole database):
+  c2  flat PQ 4x16 + derived 4x8, SIFT-like, N = 10M,  r2 = 1000
+  c3  OPQ 4x16 + derived 4x8 (data rotated by a seeded orthogonal matrix,
+      quantizer rotation undoes it), N = 100M, r2 = 2000
+  c4  IVF K = 8192 + residual PQ 4x16/8, ma = 64, r2 = 1000; N = 125M
+      (one of the eight 1B shards)
+  c5  flat PQ 8x16 + derived 8x8, 960-d GIST-like, dsub = 120, N = 50M,
+      r2 = 2000, Q = 4096
+
+Properties checked on every query of the batch (any size):
+  * distances ascending, ids unique, ids in [0, N), no padding (r <= N);
+  * every returned distance equals the f64 subspace-order sum of exact
+    full-table entries (dpq_debug_full_tables) of the returned code;
+  * |candidate set| >= r2 and b* in [0, 254] (dpq_debug_candidates);
+  * batch invariance: a sub-batch searched alone returns the same rows.
+And bit-exact equality with oracle/derived_search.py (the checker) for
+`--check` queries, run on forked CPU workers.
+
+Data are seeded synthetic stand-ins (SIFT1B / GIST are not available);
+codebooks are trained on the GPU (train.py) and codes encoded on the GPU
+with the tensor-core encoder (dpq_encode) in chunks, so no 50-190 GB float
+database is ever resident.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    "c2": dict(kind="flat", m=4, dsub=32, n=10_000_000, r2=1000, data="sift", opq=False),
+    "c3": dict(kind="flat", m=4, dsub=32, n=100_000_000, r2=2000, data="sift", opq=True),
+    "c4": dict(kind="ivf", m=4, dsub=32, n=125_000_000, r2=1000, data="sift", opq=False, cells=8192, ma=64),
+    "c5": dict(kind="flat", m=8, dsub=120, n=50_000_000, r2=2000, data="gist", opq=False),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def _gen_chunk(cfg, centres, seed, start, count, device):
+    """Rows [start, start+count) of the seeded database (chunked Philox)."""
+    import torch
+
+    from paper_1905_06900_b200 import datagen
+
+    c = torch.as_tensor(np.asarray(centres), dtype=torch.float32, device=device)
+    g = torch.Generator(device=device)
+    g.manual_seed(seed * 1_000_003 + start // (1 << 20))
+    pick = torch.randint(0, c.shape[0], (count,), generator=g, device=device)
+    noise = torch.randn((count, c.shape[1]), generator=g, device=device)
+    if cfg["data"] == "sift":
+        return (c[pick] + noise.abs_().mul_(20.0)).round_().clamp_(0, 255)
+    return (c[pick] + noise.mul_(0.05)).clamp_(0.0, 1.0)
+
+
+def build(cfg, seed=42, device=None, chunk=1 << 20, nq=1024, encoder="tc"):
+    """Train on 100k seeded vectors, encode N rows chunk by chunk."""
+    import torch
+
+    from paper_1905_06900_b200 import datagen, train
+
+    device = device or torch.device("cuda", 0)
+    st = datagen.seed_streams(seed)
+    d = cfg["m"] * cfg["dsub"]
+    if cfg["data"] == "sift":
+        centres = datagen.sift_centres(st["centres"])
+        tr = datagen.sift_like(st["train"], centres, 100_000)
+        Y = datagen.sift_like(st["queries"], centres, nq)
+    else:
+        centres = datagen.gist_centres(st["centres"])
+        tr = datagen.gist_like(st["train"], centres, 100_000)
+        Y = datagen.gist_like(st["queries"], centres, nq)
+    rot = None
+    if cfg["opq"]:  # data live in a rotated frame; the quantizer's rotation undoes it
+        R0 = datagen.random_orthogonal(d, seed + 3)
+        tr = (tr @ R0).astype(np.float32)
+        Y = (Y @ R0).astype(np.float32)
+        rot = np.ascontiguousarray(R0.T)
+        rot_t = torch.as_tensor(rot, device=device)
+        R0_t = torch.as_tensor(R0, device=device)
+    trt = torch.as_tensor(tr, device=device)
+    if rot is not None:
+        trt = trt @ rot_t
+    t0 = time.time()
+    coarse = None
+    if cfg["kind"] == "ivf":
+        coarse = train.kmeans_gpu(trt, cfg["cells"], 10, seed)
+        trt = trt - coarse[train.coarse_assign(trt, coarse)]
+    cb, der = train.train_pq(trt, cfg["m"], 16, 8, iters=10, seed=seed)
+    t1 = time.time()
+    n = cfg["n"]
+    codes = np.empty((n, cfg["m"]), np.uint16)
+    cells = np.empty(n, np.int64) if coarse is not None else None
+    enc = train.make_encoder(cb, device=device, kind=encoder)
+    for s in range(0, n, chunk):
+        e = min(n, s + chunk)
+        x = _gen_chunk(cfg, centres, seed + 1, s, e - s, device)
+        if rot is not None:
+            x = (x @ R0_t) @ rot_t  # rotated data, back through the quantizer rotation
+        if coarse is not None:
+            cl = train.coarse_assign(x, coarse)
+            cells[s:e] = cl.cpu().numpy()
+            x = x - coarse[cl]
+        codes[s:e] = enc(x).cpu().numpy().astype(np.uint16)
+    t2 = time.time()
+    log(f"[fullsize] train {t1 - t0:.1f}s, generate+encode {n} rows {t2 - t1:.1f}s")
+    out = {"codebooks": cb, "derived": der, "codes": codes, "queries": Y, "rotation": rot, "cfg": cfg}
+    if coarse is not None:
+        order = np.argsort(cells, kind="stable")
+        offsets = np.zeros(cfg["cells"] + 1, np.int64)
+        offsets[1:] = np.cumsum(np.bincount(cells, minlength=cfg["cells"]))
+        out.update(centers=coarse.cpu().numpy(), offsets=offsets, sorted_codes=codes[order],
+                   sorted_ids=order.astype(np.int64), cell_of=cells)
+        del out["codes"]
+    return out
+
+
+def make_index(w, device=0):
+    if w["cfg"]["kind"] == "flat":
+        from paper_1905_06900_b200.flat import FlatIndex
+
+        return FlatIndex.from_arrays(w["codebooks"], w["derived"], w["codes"], rotation=w["rotation"],
+                                     device=device)
+    from paper_1905_06900_b200.ivf import IVFIndex
+
+    return IVFIndex.from_arrays(w["codebooks"], w["derived"], w["centers"], w["offsets"], w["sorted_codes"],
+                                w["sorted_ids"], cell_of=w["cell_of"], rotation=w["rotation"], device=device)
+
+
+# -------------------------------------------------------------- oracle --
+
+_W = {}
+
+
+def _oracle_worker(qi):
+    from oracle import derived_search as O
+
+    w = _W
+    cfg = w["cfg"]
+    y = w["queries"][qi: qi + 1]
+    if cfg["kind"] == "flat":
+        d, i = O.flat_search(w["codebooks"], w["derived"], w["codes"], y, w["r"], "derived", cfg["r2"],
+                             rotation=w["rotation"])
+    else:
+        row_of = w["row_of"]
+        iv = {"centers": w["centers"], "offsets": w["offsets"], "sorted_codes": w["sorted_codes"],
+              "sorted_ids": w["sorted_ids"], "cell_of": w["cell_of"], "row_of": row_of,
+              "codebooks": w["codebooks"], "derived": w["derived"], "bbar": 8,
+              "rotate": O.make_rotate(w["rotation"])}
+        d, i = O.ivf_search(iv, y, w["r"], ma=cfg["ma"], mode="derived", r2=cfg["r2"])
+    return qi, d[0], i[0]
+
+
+def oracle_rows(w, qis, r):
+    """Oracle results of the given query rows on forked CPU workers."""
+    import multiprocessing as mp
+
+    _W.clear()
+    _W.update(w)
+    _W["r"] = r
+    if w["cfg"]["kind"] == "ivf" and "row_of" not in _W:
+        row_of = np.empty_like(w["sorted_ids"])
+        row_of[w["sorted_ids"]] = np.arange(w["sorted_ids"].shape[0])
+        _W["row_of"] = row_of
+    procs = max(1, min(len(qis), os.cpu_count() or 1))
+    with mp.get_context("fork").Pool(procs) as pool:
+        res = pool.map(_oracle_worker, list(qis))
+    return {qi: (d, i) for qi, d, i in res}
+
+
+# -------------------------------------------------------------- checks --
+
+def check(w, r=100, check_queries=4, sub=8, device=0):
+    cfg = w["cfg"]
+    idx = make_index(w, device=device)
+    Y = w["queries"]
+    kw = dict(mode="derived", r2=cfg["r2"])
+    if cfg["kind"] == "ivf":
+        kw["ma"] = cfg["ma"]
+    t = time.time()
+    d, i = idx.search(Y, r, **kw)  # first call: sizes buffers
+    t_first = time.time() - t
+    t = time.time()
+    d, i = idx.search(Y, r, **kw)
+    t_second = time.time() - t
+    n = cfg["n"]
+    rep = {"config": {k: v for k, v in cfg.items()}, "queries": int(Y.shape[0]), "r": r,
+           "search_s_first": round(t_first, 4), "search_s": round(t_second, 4),
+           "qps_host": round(Y.shape[0] / t_second, 1)}
+    # ---- ordering / ids
+    assert np.all(np.isfinite(d)) and np.all(i >= 0) and np.all(i < n), "padding or id out of range"
+    assert np.all(np.diff(d, axis=1) >= 0), "distances not ascending"
+    assert all(len(np.unique(row)) == r for row in i), "duplicate ids"
+    ties = (np.diff(d, axis=1) == 0)
+    assert np.all(np.diff(i, axis=1)[ties] > 0), "ties not in ascending id order"
+    # ---- distances = f64 sums of exact full-table entries of the returned codes
+    m = cfg["m"]
+    nt = min(Y.shape[0], 64)
+    if cfg["kind"] == "flat":
+        tabs = idx.full_tables(Y[:nt])  # (nt, m, k) exact f32 entries (bitwise numpy, other tests)
+        cods = w["codes"][i[:nt]]  # (nt, r, m)
+        acc = np.zeros((nt, r))
+        for j in range(m):
+            acc += np.take_along_axis(tabs[:, j, :], cods[:, :, j].astype(np.int64), axis=1).astype(np.float64)
+        assert np.array_equal(acc, d[:nt]), "distance != f64 sum of exact table entries"
+        bstar, ncand = idx.candidate_counts(Y, cfg["r2"])
+        assert np.all(ncand >= min(cfg["r2"], n)) and np.all((bstar >= 0) & (bstar <= 254))
+        rep.update(bstar_median=float(np.median(bstar)), bstar_max=int(bstar.max()),
+                   candidates_mean=float(ncand.mean()), candidates_max=int(ncand.max()))
+        c = idx._handle().counters()
+        rep["counters"] = c
+    # ---- batch invariance
+    sel = np.linspace(0, Y.shape[0] - 1, sub).astype(int)
+    d2, i2 = idx.search(Y[sel], r, **kw)
+    assert np.array_equal(i2, i[sel]) and np.array_equal(d2, d[sel]), "batch invariance"
+    rep["properties"] = "ok"
+    # ---- phase split (CUDA events per batch, amortised per query)
+    _, _, tm = idx.search(Y, r, return_timings=True, **kw)
+    rep["phase_us_per_query"] = {k2: round(float(v.mean()), 3) for k2, v in tm.items()}
+    if cfg["kind"] == "flat":
+        pm = idx._handle().phase_ms()
+        rep["last_batch_ms"] = dict(zip(("tables", "guard", "scan", "threshold", "refine", "fallback", "total"),
+                                        [round(float(v), 4) for v in pm]))
+    # ---- oracle, sampled
+    if check_queries:
+        qis = np.linspace(0, Y.shape[0] - 1, check_queries).astype(int)
+        t = time.time()
+        orc = oracle_rows(w, qis, r)
+        same_i = sum(bool(np.array_equal(orc[q][1], i[q])) for q in qis)
+        same_d = sum(bool(np.array_equal(orc[q][0], d[q])) for q in qis)
+        rep["oracle"] = {"queries": len(qis), "ids_identical": same_i, "dists_identical": same_d,
+                         "cpu_s": round(time.time() - t, 1)}
+        assert same_i == len(qis) and same_d == len(qis), f"oracle mismatch {rep['oracle']}"
+    return rep
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--queries", type=int, default=None)
+    ap.add_argument("--check", type=int, default=4)
+    ap.add_argument("--encoder", default="tc", choices=["tc", "torch"])
+    a = ap.parse_args()
+    cfg = dict(CONFIGS[a.config])
+    if a.n:
+        cfg["n"] = a.n
+    nq = a.queries or (4096 if a.config == "c5" else 1024)
+    t = time.time()
+    w = build(cfg, nq=nq, encoder=a.encoder)
+    setup = time.time() - t
+    rep = check(w, check_queries=a.check)
+    rep["setup_s"] = round(setup, 1)
+    print(json.dumps(rep))
+
+
+if __name__ == "__main__":
+    main()
