@@ -99,7 +99,9 @@ def build_workload(args, device, rank: int = 0, world: int = 1, shard: bool = Tr
     t1 = time.time()
     db = datagen.sift_like_torch(args.n, args.seed + 1, centres, device=device)
     lo, hi = (rank * args.n // world, (rank + 1) * args.n // world) if shard else (0, args.n)
-    codes = train.encode(db[lo:hi], codebooks).to(torch.int32).cpu().numpy().astype(np.uint16)
+    enc = train.make_encoder(codebooks, device=device, kind="tc")  # tcgen05 3xTF32 GEMM + argmin
+    codes = enc(db[lo:hi]).cpu().numpy().astype(np.uint16)
+    del enc
     prefix = None
     if world > 1 and shard:
         import torch.distributed as dist

@@ -246,6 +246,13 @@ class Encoder:
         return out
 
     def encode_dev(self, x, codes, stream_ptr: int | None = None) -> None:
-        """x: CUDA tensor (n, >= m*dsub) f32 row-major; codes: CUDA int32 (n, m)."""
+        """x: CUDA tensor (n, >= m*dsub) f32 row-major; codes: CUDA int32 (n, m).
+        Enqueued on `stream_ptr`, default torch's current stream of x's device
+        (the legacy default stream is passed as cudaStreamLegacy, not NULL,
+        which would select the encoder's private stream)."""
+        if stream_ptr is None:
+            import torch
+
+            stream_ptr = torch.cuda.current_stream(x.device).cuda_stream
         check(lib().dpq_encode_dev(self.raw, ptr(x), int(x.shape[0]), int(x.stride(0)), ptr(codes),
-                                   c_void_p(stream_ptr) if stream_ptr else None), "dpq_encode_dev")
+                                   c_void_p(stream_ptr or 1)), "dpq_encode_dev")

@@ -124,7 +124,7 @@ def make_encoder(codebooks: np.ndarray, device=None, kind: str = "torch"):
         def run(x):
             x = x.contiguous()
             out = torch.empty((x.shape[0], enc.m), dtype=torch.int32, device=x.device)
-            enc.encode_dev(x, out, torch.cuda.current_stream(x.device).cuda_stream)
+            enc.encode_dev(x, out)
             return out
 
         run.encoder = enc

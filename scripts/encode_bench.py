@@ -45,7 +45,7 @@ for kind in ("sift_int", "float"):
     for _ in range(a.reps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        enc.encode_dev(x, codes, torch.cuda.current_stream().cuda_stream)
+        enc.encode_dev(x, codes)
         e1.record()
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1) / 1e3)

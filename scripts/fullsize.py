@@ -108,7 +108,7 @@ def build(cfg, seed=42, device=None, chunk=1 << 20, nq=1024, encoder="tc"):
     n = cfg["n"]
     codes = np.empty((n, cfg["m"]), np.uint16)
     cells = np.empty(n, np.int64) if coarse is not None else None
-    enc = train.make_encoder(cb, device=device, kind=encoder)
+    enc = train.make_encoder(cb, device=device, kind=encoder if cfg["dsub"] <= 32 else "torch")
     for s in range(0, n, chunk):
         e = min(n, s + chunk)
         x = _gen_chunk(cfg, centres, seed + 1, s, e - s, device)
