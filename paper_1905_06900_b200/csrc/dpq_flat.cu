@@ -334,10 +334,14 @@ static int launch_refine(Index* h, const RefineArgs& ra, int nq) {
 // ---------------------------------------------------------------------------
 // K1 for nslot slots whose queries are already in ws.y.
 // ---------------------------------------------------------------------------
-int build_lut(Index* h, int nslot, const uint16_t* gword, const int* slot_query = nullptr);
+int build_lut(Index* h, int nslot, const uint16_t* gword, const int* slot_query = nullptr,
+              const int* slot_live = nullptr);
+// K1 over nslot slots (or only the n_list slots of slot_list) and, with lut,
+// the scan-layout LUT tiles of all nslot slots (slot_live: padding slots < 0).
 int run_small_tables(Index* h, int nslot, const void* prefix, int64_t npre,
                      const int64_t* pre_off, const int64_t* pre_len, const double* bounds_in,
-                     bool export_debug, const float* y_slots) {
+                     bool export_debug, const float* y_slots, const int* slot_list = nullptr,
+                     int n_list = 0, bool lut = true, const int* slot_live = nullptr) {
   Workspace& w = h->ws;
   TablesArgs ta;
   ta.y = y_slots ? y_slots : w.y;
@@ -357,24 +361,28 @@ int run_small_tables(Index* h, int nslot, const void* prefix, int64_t npre,
     cudaFuncSetAttribute(k_small_tables, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  k_small_tables<<<nslot, 256, smem, h->stream>>>(ta);
-  DPQ_LAUNCHED(h);
-  return build_lut(h, nslot, nullptr);
+  ta.slot_list = slot_list;
+  const int nlaunch = slot_list ? n_list : nslot;
+  if (nlaunch > 0) {
+    k_small_tables<<<nlaunch, 256, smem, h->stream>>>(ta);
+    DPQ_LAUNCHED(h);
+  }
+  return lut ? build_lut(h, nslot, nullptr, nullptr, slot_live) : DPQ_OK;
 }
 
 // Scan-layout LUT tiles from ws.q8; with gword (guards known) tiles whose
 // guards are all <= 126 are clamped to 7-bit entries and flagged fast.
-int build_lut(Index* h, int nslot, const uint16_t* gword, const int* slot_query) {
+int build_lut(Index* h, int nslot, const uint16_t* gword, const int* slot_query, const int* slot_live) {
   Workspace& w = h->ws;
   const int ntiles = tiles_of(nslot, h->mpad);
   int* tf = w.tile_fast;  // reset to 0 when gword is null (unclamped LUT)
   const dim3 grid((unsigned)ntiles, (unsigned)h->mpad);
   if (h->mpad == 4)
     k_build_lut<4><<<grid, 256, 0, h->stream>>>(w.q8, nslot, h->m, h->kbar, w.lut, ntiles, gword, tf, h->wide,
-                                                slot_query);
+                                                slot_query, slot_live);
   else
     k_build_lut<8><<<grid, 256, 0, h->stream>>>(w.q8, nslot, h->m, h->kbar, w.lut, ntiles, gword, tf, h->wide,
-                                                slot_query);
+                                                slot_query, slot_live);
   DPQ_LAUNCHED(h);
   return DPQ_OK;
 }

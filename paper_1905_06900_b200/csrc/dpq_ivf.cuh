@@ -93,13 +93,13 @@ __global__ void k_residuals(const float* __restrict__ y, const float* __restrict
 
 // per tile-slot copy of its (query, probe) residual; zeros for padding
 __global__ void k_gather_slots(const float* __restrict__ ynat, const int* __restrict__ slot_query,
-                               const int* __restrict__ slot_probe, int ma, int d, int nts,
-                               float* __restrict__ yts) {
+                               const int* __restrict__ slot_probe, int ma, int d, int nlive,
+                               const int* __restrict__ live, float* __restrict__ yts) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= (int64_t)nts * d) return;
-  const int ts = (int)(i / d), t = (int)(i % d);
+  if (i >= (int64_t)nlive * d) return;
+  const int ts = live[i / d], t = (int)(i % d);
   const int q = slot_query[ts];
-  yts[i] = q < 0 ? 0.f : ynat[((int64_t)q * ma + slot_probe[ts]) * d + t];
+  yts[(int64_t)ts * d + t] = q < 0 ? 0.f : ynat[((int64_t)q * ma + slot_probe[ts]) * d + t];
 }
 
 // bounds of every slot = (qmin, qmax) of its query's first non-empty list
@@ -214,6 +214,7 @@ struct IvfPlan {
   int nq = 0, ma = 0, nts = 0, ntiles = 0;
   std::vector<int64_t> cells;          // (nq, ma)
   std::vector<int> slot_query, slot_probe, tile_cell, bound_ts;
+  std::vector<int> live, bsrc;         // live (non-padding) slots; bound-source slots
   std::vector<int64_t> pre_off, pre_len, tile_row0, tile_nsamp;
   std::vector<int> unit_tile;
   std::vector<int64_t> unit_r0, unit_r1;
@@ -227,6 +228,8 @@ struct IvfBuffers {
   float* ynat = nullptr;
   float* yts = nullptr;
   int* bound_ts = nullptr;
+  int* live = nullptr;                 // [cap_ts]
+  int* bsrc = nullptr;                 // [cap_q]
   double* lambda = nullptr;
   uint32_t* hist_q = nullptr;
   uint16_t* gword_q = nullptr;
@@ -249,6 +252,7 @@ static int ivf_ensure(Index* h, int nq, int ma, int nts, int ntiles, int nunits)
     DPQ_TRY(dmalloc(&b.cells, (size_t)b.cap_q * b.cap_ma));
     DPQ_TRY(dmalloc(&b.ynat, (size_t)b.cap_q * b.cap_ma * d));
     DPQ_TRY(dmalloc(&b.bound_ts, (size_t)b.cap_q));
+    DPQ_TRY(dmalloc(&b.bsrc, (size_t)b.cap_q));
     DPQ_TRY(dmalloc(&b.lambda, (size_t)b.cap_q));
     DPQ_TRY(dmalloc(&b.hist_q, (size_t)b.cap_q * 256));
     DPQ_TRY(dmalloc(&b.gword_q, (size_t)b.cap_q));
@@ -257,6 +261,7 @@ static int ivf_ensure(Index* h, int nq, int ma, int nts, int ntiles, int nunits)
   if (nts > b.cap_ts) {
     b.cap_ts = nts;
     DPQ_TRY(dmalloc(&b.yts, (size_t)b.cap_ts * d));
+    DPQ_TRY(dmalloc(&b.live, (size_t)b.cap_ts));
   }
   if (ntiles > b.cap_tiles) {
     b.cap_tiles = ntiles;
@@ -275,7 +280,7 @@ static int ivf_ensure(Index* h, int nq, int ma, int nts, int ntiles, int nunits)
 static void ivf_free(Index* h) {
   if (!h->ivf_state) return;
   IvfBuffers& b = ivf_bufs(h);
-  void* p[] = {b.cells, b.ynat, b.yts, b.bound_ts, b.lambda, b.hist_q, b.gword_q, b.guard_q,
+  void* p[] = {b.cells, b.ynat, b.yts, b.bound_ts, b.live, b.bsrc, b.lambda, b.hist_q, b.gword_q, b.guard_q,
                b.unit_tile, b.unit_r0, b.unit_r1, b.tile_row0, b.tile_nsamp};
   for (void* x : p)
     if (x) cudaFree(x);
@@ -347,6 +352,9 @@ static void ivf_plan(Index* h, IvfPlan& P, int nb, int ma, int r2) {
   }
   P.ntiles = (int)P.tile_cell.size();
   P.nts = P.ntiles * qt;
+  P.live.clear();
+  for (int ts = 0; ts < P.nts; ++ts)
+    if (P.slot_query[ts] >= 0) P.live.push_back(ts);
   // qmax prefix: first min(r2, len) rows of each query's first non-empty list
   P.pre_off.assign(P.nts, 0);
   P.pre_len.assign(P.nts, 0);
@@ -359,6 +367,9 @@ static void ivf_plan(Index* h, IvfPlan& P, int nb, int ma, int r2) {
     P.pre_off[ts] = off[c];
     P.pre_len[ts] = std::min<int64_t>(r2, off[c + 1] - off[c]);
   }
+  P.bsrc.clear();
+  for (int q = 0; q < nb; ++q)
+    if (P.bound_ts[q] >= 0) P.bsrc.push_back(P.bound_ts[q]);
   // guard sampling: one stride for the batch, exact when lists are short
   const int64_t avg = nb > 0 ? tot_rows / std::max(1, nb) : 0;
   P.stride = (avg <= h->exact_limit) ? 1 : std::max<int64_t>(1, avg / std::max<int64_t>(1, h->sample));
@@ -487,17 +498,23 @@ static int ivf_batch(Index* h, int nb, int r, int ma, int r2, bool derived, cons
   if (P.nts == 0) {  // every probed list is empty: empty results (ivf.py:230-233)
     DPQ_CUDA(cudaMemsetAsync(w.bstar, 0xFF, (size_t)nb * 4, h->stream));
   } else {
-    const int64_t tot = (int64_t)P.nts * d;
+    const int nlive = (int)P.live.size(), nbsrc = (int)P.bsrc.size();
+    DPQ_TRY(h2d(B.live, P.live, h->stream));
+    DPQ_TRY(h2d(B.bsrc, P.bsrc, h->stream));
+    const int64_t tot = (int64_t)nlive * d;
     k_gather_slots<<<(unsigned)((tot + 255) / 256), 256, 0, h->stream>>>(B.ynat, w.slot_query, w.slot_probe, ma, d,
-                                                                        P.nts, B.yts);
+                                                                        nlive, B.live, B.yts);
     DPQ_LAUNCHED(h);
-    // K1 pass A: per-slot tables; qmin/qmax of the bound-source slots
-    DPQ_TRY(run_small_tables(h, P.nts, h->codes, 0, w.slot_pre_off, w.slot_pre_len, nullptr, false, B.yts));
+    // K1 pass A: qmin/qmax of the bound-source slots only (their tables are
+    // recomputed in pass B; padding slots are never computed)
+    DPQ_TRY(run_small_tables(h, P.nts, h->codes, 0, w.slot_pre_off, w.slot_pre_len, nullptr, false, B.yts,
+                             B.bsrc, nbsrc, false));
     k_slot_bounds<<<(P.nts + 255) / 256, 256, 0, h->stream>>>(w.qmin, w.qmax, B.bound_ts, w.slot_query, P.nts,
                                                               w.bounds);
     DPQ_LAUNCHED(h);
     // K1 pass B: quantize every slot with its query's bounds -> LUT tiles
-    DPQ_TRY(run_small_tables(h, P.nts, h->codes, 0, nullptr, nullptr, w.bounds, false, B.yts));
+    DPQ_TRY(run_small_tables(h, P.nts, h->codes, 0, nullptr, nullptr, w.bounds, false, B.yts, B.live, nlive, true,
+                             w.slot_query));
     ev_rec(h, 2);
     // guard per query from per-list sampled histograms
     auto make_guards = [&](int64_t stride, bool exact, const uint8_t* only) -> int {
@@ -511,7 +528,7 @@ static int ivf_batch(Index* h, int nb, int r, int ma, int r2, bool derived, cons
         mx = std::max(mx, ns[t]);
       }
       DPQ_TRY(h2d(B.tile_nsamp, ns, h->stream));
-      DPQ_TRY(build_lut(h, P.nts, nullptr));  // histograms need unclamped entries
+      DPQ_TRY(build_lut(h, P.nts, nullptr, nullptr, w.slot_query));  // histograms need unclamped entries
       DPQ_TRY(launch_hist(h, P.ntiles, nullptr, stride, mx, h->plane, B.tile_row0, B.tile_nsamp));
       k_slot_hist_to_query<<<(unsigned)(((int64_t)P.nts * 256 + 255) / 256), 256, 0, h->stream>>>(
           w.hist, w.slot_query, P.nts, B.hist_q);
@@ -521,7 +538,7 @@ static int ivf_batch(Index* h, int nb, int r, int ma, int r2, bool derived, cons
       DPQ_LAUNCHED(h);
       k_expand_gword<<<(P.nts + 255) / 256, 256, 0, h->stream>>>(B.gword_q, w.slot_query, P.nts, w.gword);
       DPQ_LAUNCHED(h);
-      DPQ_TRY(build_lut(h, P.nts, w.gword));
+      DPQ_TRY(build_lut(h, P.nts, w.gword, nullptr, w.slot_query));
       return DPQ_OK;
     };
     DPQ_TRY(make_guards(P.stride, P.stride == 1, nullptr));
@@ -590,7 +607,8 @@ static int ivf_batch(Index* h, int nb, int r, int ma, int r2, bool derived, cons
 // host-buffer driver for ivf (queries + optional rotated residuals/cells)
 static int ivf_driver(Index* h, const float* y, int64_t nq, int r, int ma, int r2, bool derived,
                       const float* res_rot, const int64_t* cells, double* dists, int64_t* ids, double* phase_us) {
-  int bsz = std::max(1, std::min(h->batch, std::max(1, (1 << 16) / std::max(ma, 1))));
+  static const int env_batch = getenv("DPQ_IVF_BATCH") ? atoi(getenv("DPQ_IVF_BATCH")) : 0;
+  int bsz = env_batch > 0 ? env_batch : std::max(1, std::min(h->batch, std::max(1, (1 << 16) / std::max(ma, 1))));
   int64_t q0 = 0;
   while (q0 < nq) {
     const int nb = (int)std::min<int64_t>(bsz, nq - q0);

@@ -127,6 +127,7 @@ struct TablesArgs {
   uint8_t* lut;            // [tiles][mpad][256][qt] (see lut_index)
   int mpad, qt;
   uint16_t* cluster = nullptr;  // optional [nslot]: g0* << 8 | g1* (first argmin of the u8 tables)
+  const int* slot_list = nullptr;  // optional: CTA b computes slot slot_list[b] (ivf: live slots only)
 };
 
 __global__ void __launch_bounds__(256) k_small_tables(TablesArgs a) {
@@ -134,7 +135,7 @@ __global__ void __launch_bounds__(256) k_small_tables(TablesArgs a) {
   extern __shared__ __align__(16) float sm_f[];
   __shared__ float red_f[8];
   __shared__ double red_d[8];
-  const int s = blockIdx.x, tid = threadIdx.x;
+  const int s = a.slot_list ? a.slot_list[blockIdx.x] : (int)blockIdx.x, tid = threadIdx.x;
   const int d = a.m * a.dsub, ne = a.m * a.kbar;
   float* ys = sm_f;
   float* st = sm_f + d;
@@ -240,7 +241,8 @@ template <int MPAD>
 __global__ void __launch_bounds__(256) k_build_lut(const uint8_t* __restrict__ q8, int nslot, int m, int kbar,
                                                    uint8_t* __restrict__ lut, int ntiles,
                                                    const uint16_t* __restrict__ gword, int* __restrict__ tile_fast,
-                                                   int allow_wide, const int* __restrict__ slot_query) {
+                                                   int allow_wide, const int* __restrict__ slot_query,
+                                                   const int* __restrict__ slot_live) {
   // One CTA per (tile, subspace j): the QT slots' u8 rows of subspace j are
   // staged in shared memory ([slot][group], rows padded to 65 words so the
   // transposed reads below are conflict-free), then written as the tile's
@@ -263,7 +265,9 @@ __global__ void __launch_bounds__(256) k_build_lut(const uint8_t* __restrict__ q
     const int slot = t * G::QT + sl;
     const int q = slot_query ? slot_query[slot] : slot;
     uint32_t v = 0;
-    if (live_j && q >= 0 && q < nslot && 4 * w < kbar) {
+    if (slot_live && slot_live[slot] < 0) {
+      v = 0xFFFFFFFFu;  // padding slot (ivf): saturated entries, its q8 row is never computed
+    } else if (live_j && q >= 0 && q < nslot && 4 * w < kbar) {
       const uint8_t* row = q8 + ((int64_t)q * m + j) * kbar;
       if ((kbar & 3) == 0) v = *reinterpret_cast<const uint32_t*>(row + 4 * w);
       else
