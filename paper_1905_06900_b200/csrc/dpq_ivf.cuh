@@ -78,6 +78,72 @@ __global__ void __launch_bounds__(NT) k_probe(const float* __restrict__ y, int d
   for (int i = threadIdx.x; i < ma; i += NT) cells[(int64_t)q * ma + i] = ids[i];
 }
 
+// Query-tiled probe (K <= 8192): k_probe_dist computes d2 for a tile of 16
+// queries x 256 centres per CTA with the centres staged through shared memory
+// (each centre row read once per 16 queries instead of once per query), same
+// f64 arithmetic as k_probe; k_probe_select sorts each query's K (d2, cell)
+// pairs with a stable block radix sort (cells ascending on input, so equal d2
+// keep the lower cell first) and writes the first ma.
+constexpr int kProbeQT = 16, kProbeCT = 256, kProbeDC = 32;
+__global__ void __launch_bounds__(kProbeCT) k_probe_dist(const float* __restrict__ y, int d, int nq,
+                                                          const float* __restrict__ centers, int K,
+                                                          double* __restrict__ d2) {
+  __shared__ float cs[kProbeCT][kProbeDC + 1];
+  __shared__ float ys[kProbeQT][kProbeDC];
+  const int c0 = blockIdx.x * kProbeCT, q0 = blockIdx.y * kProbeQT, tid = threadIdx.x;
+  double acc[kProbeQT];
+#pragma unroll
+  for (int q = 0; q < kProbeQT; ++q) acc[q] = 0.0;
+  for (int t0 = 0; t0 < d; t0 += kProbeDC) {
+    const int dc = min(kProbeDC, d - t0);
+    __syncthreads();
+    for (int i = tid; i < kProbeCT * kProbeDC; i += kProbeCT) {
+      const int r = i / kProbeDC, t = i % kProbeDC;
+      cs[r][t] = (c0 + r < K && t < dc) ? centers[(int64_t)(c0 + r) * d + t0 + t] : 0.f;
+    }
+    for (int i = tid; i < kProbeQT * kProbeDC; i += kProbeCT) {
+      const int q = i / kProbeDC, t = i % kProbeDC;
+      ys[q][t] = (q0 + q < nq && t < dc) ? y[(int64_t)(q0 + q) * d + t0 + t] : 0.f;
+    }
+    __syncthreads();
+    for (int t = 0; t < dc; ++t) {
+      const double c = (double)cs[tid][t];
+#pragma unroll
+      for (int q = 0; q < kProbeQT; ++q) {
+        const double df = __dsub_rn(c, (double)ys[q][t]);
+        acc[q] = __dadd_rn(acc[q], __dmul_rn(df, df));
+      }
+    }
+  }
+  if (c0 + tid < K)
+#pragma unroll
+    for (int q = 0; q < kProbeQT; ++q)
+      if (q0 + q < nq) d2[(int64_t)(q0 + q) * K + c0 + tid] = acc[q];
+}
+
+template <int ITEMS>
+__global__ void __launch_bounds__(256) k_probe_select(const double* __restrict__ d2, int K, int ma,
+                                                      int64_t* __restrict__ cells) {
+  using Sort = cub::BlockRadixSort<uint64_t, 256, ITEMS, int>;
+  extern __shared__ __align__(16) uint8_t probe_smem[];  // Sort::TempStorage (> 48 KB at ITEMS = 32)
+  typename Sort::TempStorage& tmp = *reinterpret_cast<typename Sort::TempStorage*>(probe_smem);
+  const int q = blockIdx.x;
+  uint64_t key[ITEMS];
+  int id[ITEMS];
+#pragma unroll
+  for (int e = 0; e < ITEMS; ++e) {  // blocked arrangement: thread t holds ids t*ITEMS .. +ITEMS-1
+    const int c = threadIdx.x * ITEMS + e;
+    key[e] = c < K ? (uint64_t)__double_as_longlong(d2[(int64_t)q * K + c]) : ~0ull;  // d2 >= 0: bits order
+    id[e] = c;
+  }
+  Sort(tmp).Sort(key, id);  // stable: equal keys keep ascending cell ids
+#pragma unroll
+  for (int e = 0; e < ITEMS; ++e) {
+    const int rank = threadIdx.x * ITEMS + e;
+    if (rank < ma) cells[(int64_t)q * ma + rank] = id[e];
+  }
+}
+
 // residuals y - centre in f32 (ivf.py:120), natural (query, probe) order
 __global__ void k_residuals(const float* __restrict__ y, const float* __restrict__ centers,
                             const int64_t* __restrict__ cells, int nq, int ma, int d,
@@ -239,6 +305,8 @@ struct IvfBuffers {
   int64_t* unit_r1 = nullptr;
   int64_t* tile_row0 = nullptr;
   int64_t* tile_nsamp = nullptr;
+  double* d2 = nullptr;                // probe distances (nq, K)
+  int64_t cap_d2 = 0;
 };
 
 static IvfBuffers& ivf_bufs(Index* h) { return *reinterpret_cast<IvfBuffers*>(h->ivf_state); }
@@ -281,7 +349,7 @@ static void ivf_free(Index* h) {
   if (!h->ivf_state) return;
   IvfBuffers& b = ivf_bufs(h);
   void* p[] = {b.cells, b.ynat, b.yts, b.bound_ts, b.live, b.bsrc, b.lambda, b.hist_q, b.gword_q, b.guard_q,
-               b.unit_tile, b.unit_r0, b.unit_r1, b.tile_row0, b.tile_nsamp};
+               b.unit_tile, b.unit_r0, b.unit_r1, b.tile_row0, b.tile_nsamp, b.d2};
   for (void* x : p)
     if (x) cudaFree(x);
   delete reinterpret_cast<IvfBuffers*>(h->ivf_state);
@@ -291,6 +359,28 @@ static void ivf_free(Index* h) {
 // Probe on device: cells (nb, ma) into bufs.cells.
 static int ivf_probe_dev(Index* h, int nb, int ma) {
   IvfBuffers& b = ivf_bufs(h);
+  if (h->n_cells <= 8192 && nb > 0) {  // query-tiled distances + block radix sort per query
+    if ((int64_t)nb * h->n_cells > b.cap_d2) {
+      if (b.d2) cudaFree(b.d2);
+      b.d2 = nullptr;
+      b.cap_d2 = (int64_t)nb * h->n_cells;
+      DPQ_TRY(dmalloc(&b.d2, (size_t)b.cap_d2));
+    }
+    const dim3 grid((unsigned)((h->n_cells + kProbeCT - 1) / kProbeCT), (unsigned)((nb + kProbeQT - 1) / kProbeQT));
+    k_probe_dist<<<grid, kProbeCT, 0, h->stream>>>(h->ws.y, h->d, nb, h->centers, h->n_cells, b.d2);
+    DPQ_LAUNCHED(h);
+    const int items = (h->n_cells + 255) / 256;
+    auto sel = [&](auto kern, size_t tmp) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tmp);
+      kern<<<nb, 256, tmp, h->stream>>>(b.d2, h->n_cells, ma, b.cells);
+    };
+    if (items <= 4) sel(k_probe_select<4>, sizeof(typename cub::BlockRadixSort<uint64_t, 256, 4, int>::TempStorage));
+    else if (items <= 8) sel(k_probe_select<8>, sizeof(typename cub::BlockRadixSort<uint64_t, 256, 8, int>::TempStorage));
+    else if (items <= 16) sel(k_probe_select<16>, sizeof(typename cub::BlockRadixSort<uint64_t, 256, 16, int>::TempStorage));
+    else sel(k_probe_select<32>, sizeof(typename cub::BlockRadixSort<uint64_t, 256, 32, int>::TempStorage));
+    DPQ_LAUNCHED(h);
+    return DPQ_OK;
+  }
   const int need = ma + 256;
   const size_t ys = (size_t)h->d * 4;
   auto go = [&](auto kern, int BUF) {
@@ -311,65 +401,69 @@ static int ivf_probe_dev(Index* h, int nb, int ma) {
 static void ivf_plan(Index* h, IvfPlan& P, int nb, int ma, int r2) {
   const int qt = qt_of(h->mpad);
   const std::vector<int64_t>& off = h->h_offsets;
+  const int K = h->n_cells;
   P.nq = nb;
   P.ma = ma;
   struct S { int64_t cell; int q, p; };
-  std::vector<S> ne;
-  ne.reserve((size_t)nb * ma);
+  // non-empty probes grouped by cell, (query, probe) order kept inside a
+  // cell: a counting sort over the K cells (stable, O(nb*ma + K))
+  std::vector<int> cnt(K + 1, 0);
   std::vector<int> first(nb, -1);
   int64_t tot_rows = 0;
+  int nne = 0;
   for (int q = 0; q < nb; ++q)
     for (int p = 0; p < ma; ++p) {
       const int64_t c = P.cells[(size_t)q * ma + p];
       const int64_t len = off[c + 1] - off[c];
       if (len <= 0) continue;
       if (first[q] < 0) first[q] = p;
-      ne.push_back({c, q, p});
+      ++cnt[c + 1];
+      ++nne;
       tot_rows += len;
     }
-  std::stable_sort(ne.begin(), ne.end(), [](const S& x, const S& y) { return x.cell < y.cell; });
-  P.slot_query.clear(); P.slot_probe.clear(); P.tile_cell.clear();
-  std::vector<int> ts_of((size_t)nb * ma, -1);
-  for (size_t i = 0; i < ne.size();) {
-    size_t j = i;
-    while (j < ne.size() && ne[j].cell == ne[i].cell) ++j;
-    for (size_t t0 = i; t0 < j; t0 += qt) {
-      const int tile = (int)P.tile_cell.size();
-      P.tile_cell.push_back((int)ne[i].cell);
-      for (int qq = 0; qq < qt; ++qq) {
-        const size_t k = t0 + qq;
-        if (k < j) {
-          P.slot_query.push_back(ne[k].q);
-          P.slot_probe.push_back(ne[k].p);
-          ts_of[(size_t)ne[k].q * ma + ne[k].p] = tile * qt + qq;
-        } else {
-          P.slot_query.push_back(-1);
-          P.slot_probe.push_back(0);
-        }
-      }
-    }
-    i = j;
-  }
-  P.ntiles = (int)P.tile_cell.size();
+  // tiles per cell and the first tile of each cell
+  std::vector<int> tile0(K + 1, 0);
+  for (int c = 0; c < K; ++c) tile0[c + 1] = tile0[c] + (cnt[c + 1] + qt - 1) / qt;
+  P.ntiles = tile0[K];
   P.nts = P.ntiles * qt;
-  P.live.clear();
-  for (int ts = 0; ts < P.nts; ++ts)
-    if (P.slot_query[ts] >= 0) P.live.push_back(ts);
-  // qmax prefix: first min(r2, len) rows of each query's first non-empty list
-  P.pre_off.assign(P.nts, 0);
-  P.pre_len.assign(P.nts, 0);
+  P.tile_cell.resize(P.ntiles);
+  for (int c = 0; c < K; ++c)
+    for (int t = tile0[c]; t < tile0[c + 1]; ++t) P.tile_cell[t] = c;
+  P.slot_query.assign(P.nts, -1);
+  P.slot_probe.assign(P.nts, 0);
+  std::vector<int> fill(K, 0);
+  std::vector<int> ts_first(nb, -1);  // slot of each query's first non-empty probe
+  P.live.resize(nne);
+  std::vector<S> ne(nne);
+  int k = 0;
+  for (int q = 0; q < nb; ++q)
+    for (int p = 0; p < ma; ++p) {
+      const int64_t c = P.cells[(size_t)q * ma + p];
+      if (off[c + 1] - off[c] <= 0) continue;
+      const int ts = tile0[c] * qt + fill[c]++;  // slots of a cell's tiles fill front to back
+      P.slot_query[ts] = q;
+      P.slot_probe[ts] = p;
+      if (p == first[q]) ts_first[q] = ts;
+      ne[k++] = {c, q, p};
+    }
+  k = 0;
+  for (int c = 0; c < K; ++c)  // live slots in slot order
+    for (int i = 0; i < fill[c]; ++i) P.live[k++] = tile0[c] * qt + i;
+  // qmax prefix: first min(r2, len) rows of each query's first non-empty
+  // list, one entry per bound-source slot (list order of P.bsrc)
   P.bound_ts.assign(nb, -1);
+  P.bsrc.clear();
+  P.pre_off.clear();
+  P.pre_len.clear();
   for (int q = 0; q < nb; ++q) {
     if (first[q] < 0) continue;
     const int64_t c = P.cells[(size_t)q * ma + first[q]];
-    const int ts = ts_of[(size_t)q * ma + first[q]];
+    const int ts = ts_first[q];
     P.bound_ts[q] = ts;
-    P.pre_off[ts] = off[c];
-    P.pre_len[ts] = std::min<int64_t>(r2, off[c + 1] - off[c]);
+    P.bsrc.push_back(ts);
+    P.pre_off.push_back(off[c]);
+    P.pre_len.push_back(std::min<int64_t>(r2, off[c + 1] - off[c]));
   }
-  P.bsrc.clear();
-  for (int q = 0; q < nb; ++q)
-    if (P.bound_ts[q] >= 0) P.bsrc.push_back(P.bound_ts[q]);
   // guard sampling: one stride for the batch, exact when lists are short
   const int64_t avg = nb > 0 ? tot_rows / std::max(1, nb) : 0;
   P.stride = (avg <= h->exact_limit) ? 1 : std::max<int64_t>(1, avg / std::max<int64_t>(1, h->sample));
@@ -480,7 +574,12 @@ static int ivf_batch(Index* h, int nb, int r, int ma, int r2, bool derived, cons
     h->counters[1] += nb;
     return DPQ_OK;
   }
+  static const bool trace = getenv("DPQ_HOST_TRACE") != nullptr;
+  auto now = []() { return std::chrono::duration<double, std::micro>(
+                        std::chrono::steady_clock::now().time_since_epoch()).count(); };
+  const double t_plan0 = trace ? now() : 0.0;
   ivf_plan(h, P, nb, ma, r2);
+  const double t_plan1 = trace ? now() : 0.0;
   DPQ_TRY(ensure_ws(h, std::max(P.nts, 1), r, d, nb));
   DPQ_TRY(ivf_ensure(h, nb, ma, std::max(P.nts, 1), std::max(P.ntiles, 1), std::max((int)P.unit_tile.size(), 1)));
   DPQ_TRY(h2d(w.slot_query, P.slot_query, h->stream));
@@ -583,6 +682,9 @@ static int ivf_batch(Index* h, int nb, int r, int ma, int r2, bool derived, cons
     }
   }
   ev_rec(h, 4);
+  if (trace)
+    fprintf(stderr, "[dpq ivf] plan %.1f us | uploads+first pass (host) %.1f us | live %zu of %d slots, %d tiles\n",
+            t_plan1 - t_plan0, now() - t_plan1, P.live.size(), P.nts, P.ntiles);
   RefineArgs ra = make_refine_args(h, r);
   ra.y = B.ynat;
   ra.ystride = ma * d;

@@ -127,7 +127,8 @@ struct TablesArgs {
   uint8_t* lut;            // [tiles][mpad][256][qt] (see lut_index)
   int mpad, qt;
   uint16_t* cluster = nullptr;  // optional [nslot]: g0* << 8 | g1* (first argmin of the u8 tables)
-  const int* slot_list = nullptr;  // optional: CTA b computes slot slot_list[b] (ivf: live slots only)
+  const int* slot_list = nullptr;  // optional: CTA b computes slot slot_list[b] (ivf: live slots only);
+                                   // prefix_off/prefix_len are then indexed by b
 };
 
 __global__ void __launch_bounds__(256) k_small_tables(TablesArgs a) {
@@ -157,8 +158,9 @@ __global__ void __launch_bounds__(256) k_small_tables(TablesArgs a) {
   __syncthreads();
   // qmax: max over prefix codes of the f64 masked table sum, j ascending
   // (twopass.py:41-47, 83-84)
-  int64_t pre_off = a.prefix_off ? a.prefix_off[s] : 0;
-  int64_t npre = a.prefix_len ? a.prefix_len[s] : a.npre;
+  const int pi = a.slot_list ? (int)blockIdx.x : s;  // prefix arrays follow slot_list when given
+  int64_t pre_off = a.prefix_off ? a.prefix_off[pi] : 0;
+  int64_t npre = a.prefix_len ? a.prefix_len[pi] : a.npre;
   double mx = -INFINITY;
   for (int64_t p = tid; p < npre; p += 256) {
     double acc = 0.0;
