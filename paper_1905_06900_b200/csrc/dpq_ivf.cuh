@@ -710,7 +710,11 @@ static int ivf_batch(Index* h, int nb, int r, int ma, int r2, bool derived, cons
 static int ivf_driver(Index* h, const float* y, int64_t nq, int r, int ma, int r2, bool derived,
                       const float* res_rot, const int64_t* cells, double* dists, int64_t* ids, double* phase_us) {
   static const int env_batch = getenv("DPQ_IVF_BATCH") ? atoi(getenv("DPQ_IVF_BATCH")) : 0;
-  int bsz = env_batch > 0 ? env_batch : std::max(1, std::min(h->batch, std::max(1, (1 << 16) / std::max(ma, 1))));
+  // IVF tiles are per cell: larger batches fill them (tile occupancy ~ nq * ma / cells), so the IVF
+  // batch is at least 2^18 / ma probes' worth of queries (4096 at ma = 64), capped at 4096 queries
+  int bsz = env_batch > 0 ? env_batch
+                          : std::max(1, std::max(std::min(h->batch, (1 << 16) / std::max(ma, 1)),
+                                                 std::min(4096, (1 << 18) / std::max(ma, 1))));
   int64_t q0 = 0;
   while (q0 < nq) {
     const int nb = (int)std::min<int64_t>(bsz, nq - q0);

@@ -47,6 +47,8 @@ CONFIGS = {
     "c3": dict(kind="flat", m=4, dsub=32, n=100_000_000, r2=2000, data="sift", opq=True),
     "c4": dict(kind="ivf", m=4, dsub=32, n=125_000_000, r2=1000, data="sift", opq=False, cells=8192, ma=64),
     "c5": dict(kind="flat", m=8, dsub=120, n=50_000_000, r2=2000, data="gist", opq=False),
+    # configs[3] at its full 1B rows on ONE GPU (~28 GB of index in HBM)
+    "c4b": dict(kind="ivf", m=4, dsub=32, n=1_000_000_000, r2=1000, data="sift", opq=False, cells=8192, ma=64),
 }
 
 
@@ -106,29 +108,41 @@ def build(cfg, seed=42, device=None, chunk=1 << 20, nq=1024, encoder="tc"):
     cb, der = train.train_pq(trt, cfg["m"], 16, 8, iters=10, seed=seed)
     t1 = time.time()
     n = cfg["n"]
-    codes = np.empty((n, cfg["m"]), np.uint16)
-    cells = np.empty(n, np.int64) if coarse is not None else None
     enc = train.make_encoder(cb, device=device, kind=encoder if cfg["dsub"] <= 32 else "torch")
-    for s in range(0, n, chunk):
-        e = min(n, s + chunk)
-        x = _gen_chunk(cfg, centres, seed + 1, s, e - s, device)
-        if rot is not None:
-            x = (x @ R0_t) @ rot_t  # rotated data, back through the quantizer rotation
-        if coarse is not None:
+    out = {"codebooks": cb, "derived": der, "queries": Y, "rotation": rot, "cfg": cfg}
+    if coarse is None:
+        codes = np.empty((n, cfg["m"]), np.uint16)
+        for s in range(0, n, chunk):
+            e = min(n, s + chunk)
+            x = _gen_chunk(cfg, centres, seed + 1, s, e - s, device)
+            if rot is not None:
+                x = (x @ R0_t) @ rot_t  # rotated data, back through the quantizer rotation
+            codes[s:e] = enc(x).cpu().numpy().astype(np.uint16)
+        out["codes"] = codes
+    else:  # IVF: cells and codes stay on the GPU (u16 bit patterns in int16), lists sorted there
+        cells_t = torch.empty(n, dtype=torch.int32, device=device)
+        codes_t = torch.empty((n, cfg["m"]), dtype=torch.int16, device=device)
+        for s in range(0, n, chunk):
+            e = min(n, s + chunk)
+            x = _gen_chunk(cfg, centres, seed + 1, s, e - s, device)
+            if rot is not None:
+                x = (x @ R0_t) @ rot_t
             cl = train.coarse_assign(x, coarse)
-            cells[s:e] = cl.cpu().numpy()
-            x = x - coarse[cl]
-        codes[s:e] = enc(x).cpu().numpy().astype(np.uint16)
+            cells_t[s:e] = cl.to(torch.int32)
+            codes_t[s:e] = enc(x - coarse[cl]).to(torch.int16)
+            del x, cl
+        sorted_cells, order = torch.sort(cells_t, stable=True)
+        counts = torch.bincount(cells_t, minlength=cfg["cells"])
+        del sorted_cells
+        offsets = np.zeros(cfg["cells"] + 1, np.int64)
+        offsets[1:] = np.cumsum(counts.cpu().numpy())
+        out.update(centers=coarse.cpu().numpy(), offsets=offsets,
+                   sorted_codes=codes_t[order].cpu().numpy().view(np.uint16),
+                   sorted_ids=order.cpu().numpy(), cell_of=cells_t.cpu().numpy().astype(np.int64))
+        del cells_t, codes_t, order
+        torch.cuda.empty_cache()
     t2 = time.time()
     log(f"[fullsize] train {t1 - t0:.1f}s, generate+encode {n} rows {t2 - t1:.1f}s")
-    out = {"codebooks": cb, "derived": der, "codes": codes, "queries": Y, "rotation": rot, "cfg": cfg}
-    if coarse is not None:
-        order = np.argsort(cells, kind="stable")
-        offsets = np.zeros(cfg["cells"] + 1, np.int64)
-        offsets[1:] = np.cumsum(np.bincount(cells, minlength=cfg["cells"]))
-        out.update(centers=coarse.cpu().numpy(), offsets=offsets, sorted_codes=codes[order],
-                   sorted_ids=order.astype(np.int64), cell_of=cells)
-        del out["codes"]
     return out
 
 
