@@ -144,7 +144,9 @@ int ensure_ws(Index* h, int nslot, int r, int ystride, int nq) {
   if (w.qcap_emit < w.qn || w.emit == nullptr) {
     if (w.cap == 0 && h->cap0 > 0) w.cap = (uint32_t)h->cap0;
     if (w.cap == 0) {
-      int64_t c = h->n / 64;
+      // flat: ~n/64 rows emitted per query at most on the bench data (19.5k
+      // of 10M); growth (grow_emit) covers outliers, so cap the first guess
+      int64_t c = std::min<int64_t>(h->n / 64, (int64_t)1 << 20);
       c = std::max<int64_t>(c, 16384);
       c = std::min<int64_t>(c, std::max<int64_t>(h->n, 1));
       int64_t p2 = 1;
@@ -363,7 +365,18 @@ int run_small_tables(Index* h, int nslot, const void* prefix, int64_t npre,
   }
   ta.slot_list = slot_list;
   const int nlaunch = slot_list ? n_list : nslot;
-  if (nlaunch > 0) {
+  constexpr int SPC = 8;
+  const bool many = nlaunch >= 8192 && (h->dsub & 7) == 0 && h->dsub <= 128;
+  if (nlaunch > 0 && many) {  // IVF-size slot counts: SPC slots per CTA
+    const size_t smem_ms = (size_t)SPC * (h->d + h->m * h->kbar) * 4;
+    static bool attr_ms = false;
+    if (!attr_ms) {
+      cudaFuncSetAttribute(k_small_tables_ms<SPC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr_ms = true;
+    }
+    k_small_tables_ms<SPC><<<(nlaunch + SPC - 1) / SPC, 256, smem_ms, h->stream>>>(ta, nlaunch);
+    DPQ_LAUNCHED(h);
+  } else if (nlaunch > 0) {
     k_small_tables<<<nlaunch, 256, smem, h->stream>>>(ta);
     DPQ_LAUNCHED(h);
   }

@@ -580,6 +580,20 @@ static int ivf_batch(Index* h, int nb, int r, int ma, int r2, bool derived, cons
   const double t_plan0 = trace ? now() : 0.0;
   ivf_plan(h, P, nb, ma, r2);
   const double t_plan1 = trace ? now() : 0.0;
+  if (h->ws.cap == 0 && h->cap0 == 0) {
+    // first emit capacity per query from the probed rows (a query emits ~r2
+    // to a few r2 rows; growth covers outliers): avg probed / 256, pow2
+    int64_t probed = 0;
+    for (int q = 0; q < nb; ++q)
+      for (int p = 0; p < ma; ++p) {
+        const int64_t c = P.cells[(size_t)q * ma + p];
+        probed += h->h_offsets[c + 1] - h->h_offsets[c];
+      }
+    int64_t c = std::max<int64_t>(16384, std::min<int64_t>(probed / std::max(nb, 1) / 256, (int64_t)1 << 20));
+    int64_t p2 = 1;
+    while (p2 < c) p2 <<= 1;
+    h->cap0 = p2;
+  }
   DPQ_TRY(ensure_ws(h, std::max(P.nts, 1), r, d, nb));
   DPQ_TRY(ivf_ensure(h, nb, ma, std::max(P.nts, 1), std::max(P.ntiles, 1), std::max((int)P.unit_tile.size(), 1)));
   DPQ_TRY(h2d(w.slot_query, P.slot_query, h->stream));

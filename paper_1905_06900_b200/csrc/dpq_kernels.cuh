@@ -212,6 +212,101 @@ __global__ void __launch_bounds__(256) k_small_tables(TablesArgs a) {
   __syncthreads();
 }
 
+// K1, many-slot form (IVF batches: ~10^5 slots): SPC slots per CTA so each
+// derived-codebook row is fetched once per SPC slots instead of once per slot
+// (the per-slot kernel re-reads the whole m x kbar x dsub codebook per slot).
+// Entry arithmetic is pw_sqdist_v8's, reductions and quantization are
+// k_small_tables' — bitwise the same tables, bounds and u8 entries.
+// Requires 8 | dsub <= 128 (16-B rows); one warp per slot after the tables.
+template <int SPC>
+__global__ void __launch_bounds__(256, 2) k_small_tables_ms(TablesArgs a, int n_slots) {
+  extern __shared__ __align__(16) float sm_ms[];
+  const int d = a.m * a.dsub, ne = a.m * a.kbar, tid = threadIdx.x;
+  float* ys = sm_ms;            // [SPC][d]
+  float* st = sm_ms + SPC * d;  // [SPC][ne]
+  __shared__ int sl[SPC];
+  if (tid < SPC) {
+    const int b = blockIdx.x * SPC + tid;
+    sl[tid] = b < n_slots ? (a.slot_list ? a.slot_list[b] : b) : -1;
+  }
+  __syncthreads();
+  for (int i = tid; i < SPC * d; i += 256) {
+    const int k = i / d, t = i % d;
+    ys[i] = sl[k] >= 0 ? a.y[(int64_t)sl[k] * d + t] : 0.f;
+  }
+  __syncthreads();
+  for (int e = tid; e < ne; e += 256) {
+    const int j = e / a.kbar;
+    const float4* c4 = reinterpret_cast<const float4*>(a.dcb + (int64_t)e * a.dsub);
+    float r[SPC][8];
+    for (int i = 0; i < a.dsub / 8; ++i) {
+      const float4 ca = c4[2 * i], cb = c4[2 * i + 1];
+#pragma unroll
+      for (int k = 0; k < SPC; ++k) {
+        const float4* y4 = reinterpret_cast<const float4*>(ys + k * d + j * a.dsub);
+        const float4 p = y4[2 * i], q = y4[2 * i + 1];
+        const float v[8] = {sqdiff(ca.x, p.x), sqdiff(ca.y, p.y), sqdiff(ca.z, p.z), sqdiff(ca.w, p.w),
+                            sqdiff(cb.x, q.x), sqdiff(cb.y, q.y), sqdiff(cb.z, q.z), sqdiff(cb.w, q.w)};
+#pragma unroll
+        for (int l = 0; l < 8; ++l) r[k][l] = (i == 0) ? v[l] : __fadd_rn(r[k][l], v[l]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < SPC; ++k)
+      st[k * ne + e] = __fadd_rn(__fadd_rn(__fadd_rn(r[k][0], r[k][1]), __fadd_rn(r[k][2], r[k][3])),
+                                 __fadd_rn(__fadd_rn(r[k][4], r[k][5]), __fadd_rn(r[k][6], r[k][7])));
+  }
+  __syncthreads();
+  const int w = tid >> 5, lane = tid & 31;
+  for (int k = w; k < SPC; k += 8) {
+    const int s = sl[k];
+    if (s < 0) continue;
+    const float* t = st + k * ne;
+    float mn = INFINITY;
+    for (int e = lane; e < ne; e += 32) mn = fminf(mn, t[e]);
+    mn = warp_min_f(mn);
+    double qmin = (double)mn, qmax;
+    if (a.bounds_in) {
+      qmin = a.bounds_in[2 * s];
+      qmax = a.bounds_in[2 * s + 1];
+    } else {
+      const int pi = a.slot_list ? blockIdx.x * SPC + k : s;
+      const int64_t pre_off = a.prefix_off ? a.prefix_off[pi] : 0;
+      const int64_t npre = a.prefix_len ? a.prefix_len[pi] : a.npre;
+      double mx = -INFINITY;
+      for (int64_t p = lane; p < npre; p += 32) {
+        double acc = 0.0;
+        for (int j = 0; j < a.m; ++j) {
+          const uint32_t c = code_at(a.prefix, a.code_bytes, (pre_off + p) * a.m + j);
+          acc = __dadd_rn(acc, (double)t[j * a.kbar + (c & a.mask)]);
+        }
+        mx = fmax(mx, acc);
+      }
+      qmax = warp_max_d(mx);
+    }
+    const bool degenerate = !(qmax > qmin);
+    const double scale = degenerate ? 0.0 : __ddiv_rn(255.0, __dsub_rn(qmax, qmin));
+    const float qmaxf = __double2float_rn(qmax);
+    uint32_t best0 = 0xFFFFFFFFu, best1 = 0xFFFFFFFFu;
+    for (int e = lane; e < ne; e += 32) {
+      const uint8_t q = degenerate ? (uint8_t)0 : quantize_entry(t[e], qmin, scale, qmaxf);
+      if (a.small_out) a.small_out[(int64_t)s * ne + e] = t[e];
+      if (a.q8_out) a.q8_out[(int64_t)s * ne + e] = q;
+      if (e < a.kbar) best0 = min(best0, ((uint32_t)q << 16) | (uint32_t)e);
+      else if (e < 2 * a.kbar) best1 = min(best1, ((uint32_t)q << 16) | (uint32_t)(e - a.kbar));
+    }
+    if (lane == 0) {
+      a.qmin_out[s] = qmin;
+      a.qmax_out[s] = degenerate ? qmin : qmax;
+    }
+    if (a.cluster && a.m >= 2) {
+      best0 = __reduce_min_sync(0xffffffffu, best0);
+      best1 = __reduce_min_sync(0xffffffffu, best1);
+      if (lane == 0) a.cluster[s] = (uint16_t)(((best0 & 0xFFu) << 8) | (best1 & 0xFFu));
+    }
+  }
+}
+
 // Scan-layout LUT tiles from the u8 tables q8 [nslot][m][kbar] (see
 // lut_index): one thread per (tile, subspace, table row) writes the row's
 // LPC lane words (QT/4 queries x 4 bytes, contiguous) with 16-B stores;
