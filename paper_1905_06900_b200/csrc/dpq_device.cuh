@@ -27,6 +27,38 @@ __device__ __forceinline__ float sqdiff(float c, float y) {
   return __fmul_rn(d, d);
 }
 
+// ---- paired FP32 (sm_100 FADD2 / FFMA2): two lanes of sqdiff / add per
+// instruction, each lane rounded exactly like the scalar __fsub_rn /
+// __fmul_rn / __fadd_rn.  The square is fma(d, d, z) with z = (-0, -0) a
+// RUNTIME value (kernel argument): RN(d*d + -0) == RN(d*d) for every d, and
+// since ptxas cannot prove z == -0 it cannot contract the following add into
+// the square (with a literal -0 or a plain mul.rn it emits one FFMA2, which
+// would change the rounding).
+typedef unsigned long long f32x2_t;
+constexpr unsigned long long kNegZero2 = 0x8000000080000000ull;
+__device__ __forceinline__ f32x2_t pack2(float lo, float hi) {
+  return (f32x2_t)__float_as_uint(lo) | ((f32x2_t)__float_as_uint(hi) << 32);
+}
+__device__ __forceinline__ float lo2(f32x2_t v) { return __uint_as_float((uint32_t)v); }
+__device__ __forceinline__ float hi2(f32x2_t v) { return __uint_as_float((uint32_t)(v >> 32)); }
+__device__ __forceinline__ f32x2_t sqdiff2(f32x2_t c, f32x2_t y, f32x2_t z) {
+  f32x2_t d, q;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(c), "l"(y));
+  asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(q) : "l"(d), "l"(z));
+  return q;
+}
+__device__ __forceinline__ f32x2_t add2(f32x2_t a, f32x2_t b) {
+  f32x2_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// pw_block / pw_sqdist_v8 association for 8 | n <= 128 with the 8 running
+// sums held as 4 pairs (r0,r1) (r2,r3) (r4,r5) (r6,r7); c and y as pairs.
+__device__ __forceinline__ float pw_combine2(const f32x2_t r[4]) {
+  return __fadd_rn(__fadd_rn(__fadd_rn(lo2(r[0]), hi2(r[0])), __fadd_rn(lo2(r[1]), hi2(r[1]))),
+                   __fadd_rn(__fadd_rn(lo2(r[2]), hi2(r[2])), __fadd_rn(lo2(r[3]), hi2(r[3]))));
+}
+
 // n <= 128 block of the pairwise sum, c/y may be any address space.
 __device__ __forceinline__ float pw_block(const float* __restrict__ c,
                                           const float* __restrict__ y, int n) {

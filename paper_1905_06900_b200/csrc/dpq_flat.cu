@@ -366,7 +366,9 @@ int run_small_tables(Index* h, int nslot, const void* prefix, int64_t npre,
   ta.slot_list = slot_list;
   const int nlaunch = slot_list ? n_list : nslot;
   constexpr int SPC = 8;
-  const bool many = nlaunch >= 8192 && (h->dsub & 7) == 0 && h->dsub <= 128;
+  const char* ms_env = getenv("DPQ_MS_MIN");  // test hook: many-slot K1 from this slot count (default 8192)
+  const int ms_min = ms_env ? atoi(ms_env) : 8192;
+  const bool many = nlaunch >= ms_min && (h->dsub & 7) == 0 && h->dsub <= 128;
   if (nlaunch > 0 && many) {  // IVF-size slot counts: SPC slots per CTA
     const size_t smem_ms = (size_t)SPC * (h->d + h->m * h->kbar) * 4;
     static bool attr_ms = false;

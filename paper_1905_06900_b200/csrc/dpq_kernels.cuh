@@ -127,6 +127,7 @@ struct TablesArgs {
   uint8_t* lut;            // [tiles][mpad][256][qt] (see lut_index)
   int mpad, qt;
   uint16_t* cluster = nullptr;  // optional [nslot]: g0* << 8 | g1* (first argmin of the u8 tables)
+  unsigned long long negzero2 = kNegZero2;  // runtime (-0, -0) pair for sqdiff2
   const int* slot_list = nullptr;  // optional: CTA b computes slot slot_list[b] (ivf: live slots only);
                                    // prefix_off/prefix_len are then indexed by b
 };
@@ -235,26 +236,28 @@ __global__ void __launch_bounds__(256, 2) k_small_tables_ms(TablesArgs a, int n_
     ys[i] = sl[k] >= 0 ? a.y[(int64_t)sl[k] * d + t] : 0.f;
   }
   __syncthreads();
+  const f32x2_t z2 = a.negzero2;
   for (int e = tid; e < ne; e += 256) {
     const int j = e / a.kbar;
-    const float4* c4 = reinterpret_cast<const float4*>(a.dcb + (int64_t)e * a.dsub);
-    float r[SPC][8];
+    const ulonglong2* c2 = reinterpret_cast<const ulonglong2*>(a.dcb + (int64_t)e * a.dsub);
+    f32x2_t r[SPC][4];
     for (int i = 0; i < a.dsub / 8; ++i) {
-      const float4 ca = c4[2 * i], cb = c4[2 * i + 1];
+      const ulonglong2 ca = c2[2 * i], cb = c2[2 * i + 1];
+      const f32x2_t cv[4] = {ca.x, ca.y, cb.x, cb.y};
 #pragma unroll
       for (int k = 0; k < SPC; ++k) {
-        const float4* y4 = reinterpret_cast<const float4*>(ys + k * d + j * a.dsub);
-        const float4 p = y4[2 * i], q = y4[2 * i + 1];
-        const float v[8] = {sqdiff(ca.x, p.x), sqdiff(ca.y, p.y), sqdiff(ca.z, p.z), sqdiff(ca.w, p.w),
-                            sqdiff(cb.x, q.x), sqdiff(cb.y, q.y), sqdiff(cb.z, q.z), sqdiff(cb.w, q.w)};
+        const ulonglong2* y2 = reinterpret_cast<const ulonglong2*>(ys + k * d + j * a.dsub);
+        const ulonglong2 p = y2[2 * i], q = y2[2 * i + 1];
+        const f32x2_t yv[4] = {p.x, p.y, q.x, q.y};
 #pragma unroll
-        for (int l = 0; l < 8; ++l) r[k][l] = (i == 0) ? v[l] : __fadd_rn(r[k][l], v[l]);
+        for (int l = 0; l < 4; ++l) {
+          const f32x2_t v = sqdiff2(cv[l], yv[l], z2);
+          r[k][l] = (i == 0) ? v : add2(r[k][l], v);
+        }
       }
     }
 #pragma unroll
-    for (int k = 0; k < SPC; ++k)
-      st[k * ne + e] = __fadd_rn(__fadd_rn(__fadd_rn(r[k][0], r[k][1]), __fadd_rn(r[k][2], r[k][3])),
-                                 __fadd_rn(__fadd_rn(r[k][4], r[k][5]), __fadd_rn(r[k][6], r[k][7])));
+    for (int k = 0; k < SPC; ++k) st[k * ne + e] = pw_combine2(r[k]);
   }
   __syncthreads();
   const int w = tid >> 5, lane = tid & 31;
@@ -1379,6 +1382,7 @@ struct GroupTablesArgs {
   int nq, m, k, kbar, bbar, dsub;
   float* tables;
   unsigned long long* n_entries;
+  unsigned long long negzero2 = kNegZero2;  // runtime (-0, -0) pair for sqdiff2 (see dpq_device.cuh)
 };
 
 // Register-row variant (DSUB = 32): thread ib holds codebook row ib of the
@@ -1401,13 +1405,15 @@ __global__ void __launch_bounds__(256) k_group_tables_reg(GroupTablesArgs a) {
   const int n = nact;
   for (int ib0 = 0; ib0 < gsize; ib0 += 256) {
     const int ib = ib0 + tid;
-    float c[DSUB];
+    f32x2_t c2[DSUB / 2];  // the codebook row as lane pairs
+    const f32x2_t z2 = a.negzero2;
     if (ib < gsize) {
       const float4* src = reinterpret_cast<const float4*>(a.cb + (((int64_t)j * a.k) + (int64_t)ib * a.kbar + g) * DSUB);
 #pragma unroll
       for (int i = 0; i < DSUB / 4; ++i) {
         const float4 v = __ldg(src + i);
-        c[4 * i] = v.x; c[4 * i + 1] = v.y; c[4 * i + 2] = v.z; c[4 * i + 3] = v.w;
+        c2[2 * i] = pack2(v.x, v.y);
+        c2[2 * i + 1] = pack2(v.z, v.w);
       }
     }
     for (int base = 0; base < n; base += 32) {
@@ -1420,20 +1426,19 @@ __global__ void __launch_bounds__(256) k_group_tables_reg(GroupTablesArgs a) {
       __syncthreads();
       if (ib < gsize) {
         for (int t = 0; t < nb; ++t) {
-          const float4* y4 = reinterpret_cast<const float4*>(ys + t * DSUB);
-          float r[8];
+          const ulonglong2* y2 = reinterpret_cast<const ulonglong2*>(ys + t * DSUB);
+          f32x2_t r[4];
 #pragma unroll
-          for (int i = 0; i < DSUB / 8; ++i) {
-            const float4 p = y4[2 * i], q = y4[2 * i + 1];
-            const float yv[8] = {p.x, p.y, p.z, p.w, q.x, q.y, q.z, q.w};
+          for (int i = 0; i < DSUB / 8; ++i) {  // 8 elements = 4 lane pairs (running sums r0..r7)
+            const ulonglong2 p = y2[2 * i], q = y2[2 * i + 1];
+            const f32x2_t yv[4] = {p.x, p.y, q.x, q.y};
 #pragma unroll
-            for (int l = 0; l < 8; ++l) {
-              const float sd = sqdiff(c[8 * i + l], yv[l]);
-              r[l] = i == 0 ? sd : __fadd_rn(r[l], sd);
+            for (int l = 0; l < 4; ++l) {
+              const f32x2_t sd = sqdiff2(c2[4 * i + l], yv[l], z2);
+              r[l] = i == 0 ? sd : add2(r[l], sd);
             }
           }
-          const float v = __fadd_rn(__fadd_rn(__fadd_rn(r[0], r[1]), __fadd_rn(r[2], r[3])),
-                                    __fadd_rn(__fadd_rn(r[4], r[5]), __fadd_rn(r[6], r[7])));
+          const float v = pw_combine2(r);
           a.tables[(((int64_t)act[base + t] * a.m + j) * a.kbar + g) * gsize + ib] = v;
         }
       }

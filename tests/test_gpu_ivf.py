@@ -96,6 +96,18 @@ def test_random_ivf_vs_oracle(seed, n, K, ma, r, r2, empty):
     assert np.array_equal(i0, i1) and _same(d0, d1)
 
 
+@pytest.mark.parametrize("dsub,kbar", [(8, 16), (16, 256), (32, 64)])
+def test_many_slot_tables_vs_oracle(dsub, kbar, monkeypatch):
+    """The many-slot K1 (8 slots per CTA, paired-FP32 entries) that IVF
+    batches with >= 8192 live slots use, forced on small batches."""
+    monkeypatch.setenv("DPQ_MS_MIN", "1")
+    idx, Y = _random_ivf(11 + dsub, 6000, 24, k=1024, kbar=kbar, dsub=dsub, empty=3)
+    ivf = _oracle_ivf(idx)
+    d0, i0 = O.ivf_search(ivf, Y, 30, 6, "derived", 400)
+    d1, i1 = idx.search(Y, 30, ma=6, mode="derived", r2=400)
+    assert np.array_equal(i0, i1) and _same(d0, d1)
+
+
 def test_ivf_sampled_guard_vs_oracle(monkeypatch):
     """Long lists: the per-query guard comes from strided list samples; a tiny
     sample forces exact redos."""
