@@ -46,15 +46,18 @@ def _stale() -> bool:
     return any(p.stat().st_mtime > t for p in deps if p.exists())
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, extra=(), out: Path | None = None) -> Path:
+    """Compile every source and link libdpq.so (or `out`, with `extra` nvcc
+    flags: A/B variants for scripts/ab.py)."""
+    lib = Path(out) if out else LIB
+    if not force and not extra and out is None and not _stale():
         return LIB
     objs = []
-    tmp = PKG / "build"
+    tmp = PKG / ("build" if not extra else "build_ab")
     tmp.mkdir(exist_ok=True)
     for src in SOURCES:
         obj = tmp / (Path(src).stem + ".o")
-        cmd = [nvcc(), *NVCC_FLAGS, "-I", str(ROOT / "include"), "-c", str(CSRC / src), "-o", str(obj)]
+        cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I", str(ROOT / "include"), "-c", str(CSRC / src), "-o", str(obj)]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if verbose or res.returncode != 0:
             sys.stderr.write(res.stdout + res.stderr)
@@ -62,15 +65,15 @@ def build(force: bool = False, verbose: bool = False) -> Path:
             raise RuntimeError(f"nvcc failed on {src}")
         (tmp / (Path(src).stem + ".ptxas.txt")).write_text(res.stderr)
         objs.append(str(obj))
-    out_tmp = LIB.with_suffix(".so.tmp")
+    out_tmp = lib.with_suffix(".so.tmp")
     cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
            *objs, "-o", str(out_tmp), "-lcudart", "-lgomp"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("link failed")
-    os.replace(out_tmp, LIB)
-    return LIB
+    os.replace(out_tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

@@ -1693,7 +1693,10 @@ __device__ __forceinline__ float entry_dist(const float* cbrow, const float* ys,
 }
 
 template <int BUF, int NT, int MODE, int DSUB>
-__global__ void __launch_bounds__(NT, 6) k_refine_topk(RefineArgs a) {
+#ifndef DPQ_REFINE_MINB
+#define DPQ_REFINE_MINB 5  // CTAs per SM the register budget is sized for (6: 40 regs, spills)
+#endif
+__global__ void __launch_bounds__(NT, DPQ_REFINE_MINB) k_refine_topk(RefineArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   uint64_t* keys = reinterpret_cast<uint64_t*>(smem);
   int64_t* ids = reinterpret_cast<int64_t*>(keys + BUF);
