@@ -2,7 +2,13 @@
 1024-query batch (L2 flushed between steps), interleaved A, B, A, B ...
 
     python scripts/ab.py OLD.so NEW.so [--reps 4] [--steps 10]
+    python scripts/ab.py LIB.so:DPQ_REFINE_WARP=0 LIB.so:DPQ_REFINE_WARP=1
+
+A spec PATH:VAR=VAL[,VAR=VAL] sets environment variables while that
+variant's index is created.  Also checks that every variant returns the
+same ids and distances as the first.
 """
+import os
 import argparse
 import sys
 from pathlib import Path
@@ -26,13 +32,25 @@ w = bench.build_workload(args, "cuda:0")
 Q = torch.as_tensor(w["queries"][: a.steps * 1024], device="cuda")
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 results = {p: [] for p in a.libs}
+ref_out = None
 phases = {p: [] for p in a.libs}
 for rep in range(a.reps):
     for path in a.libs:
-        _lib._PATH = Path(path).resolve()
+        lib_path, _, env = path.partition(":")
+        saved = {}
+        for kv in filter(None, env.split(",")):
+            kk, vv = kv.split("=", 1)
+            saved[kk] = os.environ.get(kk)
+            os.environ[kk] = vv
+        _lib._PATH = Path(lib_path).resolve()
         _lib._lib = None
         idx = FlatIndex.from_arrays(w["codebooks"], w["derived"], w["codes"])
         h = idx._handle()
+        for kk, vv in saved.items():
+            if vv is None:
+                os.environ.pop(kk, None)
+            else:
+                os.environ[kk] = vv
         stream = torch.cuda.Stream()
         h.set_stream(stream.cuda_stream)
         L = _lib.lib()
@@ -57,6 +75,11 @@ for rep in range(a.reps):
                                                      _lib.ptr(out_i)), "search")
         stream.synchronize()
         phases[path].append(h.phase_ms().copy())
+        got = (out_d.cpu().numpy().copy(), out_i.cpu().numpy().copy())
+        if ref_out is None:
+            ref_out = got
+        elif not (np.array_equal(got[0], ref_out[0]) and np.array_equal(got[1], ref_out[1])):
+            print(f"RESULTS DIFFER: {path}", flush=True)
         h.set_stream(None)
         del idx, h
         torch.cuda.synchronize()
