@@ -563,6 +563,10 @@ static RefineArgs make_refine_args(Index* h, int r) {
   ra.cb = h->cb; ra.tables = w.tables; ra.y = w.y; ra.ystride = h->d;
   ra.row_ids = h->sorted_ids; ra.id_base = h->id_base; ra.r = r;  // sorted flat rows -> ids
   ra.out_d = w.out_d; ra.out_i = w.out_i; ra.n_refined = h->d_nref;
+  if (h->host_out) {  // pinned host memory is device-addressable (UVA): results cross PCIe as CTAs finish
+    ra.out_d = w.h_d;
+    ra.out_i = w.h_i;
+  }
   return ra;
 }
 
@@ -620,7 +624,8 @@ static int flat_derived_batch(Index* h, int nb, int r, int r2) {
   const bool graphable = h->use_graph && !h->timing && !h->no_spec;
   if (!graphable) return flat_derived_batch_body(h, nb, r, r2);
   BatchGraph& G = h->graph;
-  const bool same = G.nb == nb && G.r == r && G.r2 == r2 && G.epoch == g_alloc_epoch;
+  const bool same = G.nb == nb && G.r == r && G.r2 == r2 && G.host_out == (int)h->host_out &&
+                    G.epoch == g_alloc_epoch;
   if (G.exec && same) {
     DPQ_CUDA(cudaGraphLaunch(G.exec, h->stream));
     for (int i = 0; i < 8; ++i) h->counters[i] += G.counters[i];
@@ -630,7 +635,7 @@ static int flat_derived_batch(Index* h, int nb, int r, int r2) {
   if (!same || !G.warm) {  // eager run; capture on the next call with this configuration
     if (G.exec) { cudaGraphExecDestroy(G.exec); G.exec = nullptr; }
     const int rc = flat_derived_batch_body(h, nb, r, r2);
-    G.nb = nb; G.r = r; G.r2 = r2; G.epoch = g_alloc_epoch; G.warm = rc == DPQ_OK;
+    G.nb = nb; G.r = r; G.r2 = r2; G.host_out = (int)h->host_out; G.epoch = g_alloc_epoch; G.warm = rc == DPQ_OK;
     return rc;
   }
   int64_t c0[8];
@@ -789,6 +794,10 @@ static bool spec_failed(Index* h) {
 template <class F>
 static int host_driver(Index* h, const float* y, int64_t nq, int r, int batch_limit, double* dists,
                        int64_t* ids, double* phase_us, F&& batch) {
+  struct HostOutReset {  // host_out is set per batch below; cleared on every exit
+    Index* h;
+    ~HostOutReset() { h->host_out = false; }
+  } host_out_reset{h};
   int bsz = std::max(1, std::min<int>(h->batch, batch_limit));
   int64_t q0 = 0;
   static const bool trace = getenv("DPQ_HOST_TRACE") != nullptr;  // per-segment host timings (stderr)
@@ -809,6 +818,7 @@ static int host_driver(Index* h, const float* y, int64_t nq, int r, int batch_li
     const bool old_t = h->timing;
     if (want_t) h->timing = true;
     if (trace) t_in = now();
+    h->host_out = r > 0 && !h->direct_copy;
     int rc = batch(nb);
     if (trace) t_enq = now();
     h->timing = old_t;
@@ -823,11 +833,10 @@ static int host_driver(Index* h, const float* y, int64_t nq, int r, int batch_li
       DPQ_CUDA(cudaMemcpyAsync(dists + q0 * r, w.out_d, (size_t)nb * r * 8, cudaMemcpyDeviceToHost, h->stream));
       DPQ_CUDA(cudaMemcpyAsync(ids + q0 * r, w.out_i, (size_t)nb * r * 8, cudaMemcpyDeviceToHost, h->stream));
       DPQ_CUDA(cudaStreamSynchronize(h->stream));
-    } else if (r > 0) {
-      DPQ_CUDA(cudaMemcpyAsync(w.h_d, w.out_d, (size_t)nb * r * 8, cudaMemcpyDeviceToHost, h->stream));
-      DPQ_CUDA(cudaMemcpyAsync(w.h_i, w.out_i, (size_t)nb * r * 8, cudaMemcpyDeviceToHost, h->stream));
-      DPQ_CUDA(sync_copy_out(h->stream, dists + q0 * r, w.h_d, (size_t)nb * r * 8, ids + q0 * r, w.h_i,
-                             (size_t)nb * r * 8));
+    } else if (r > 0) {  // results already in w.h_d / w.h_i (host_out)
+      const cudaError_t ce = sync_copy_out(h->stream, dists + q0 * r, w.h_d, (size_t)nb * r * 8, ids + q0 * r,
+                                           w.h_i, (size_t)nb * r * 8);
+      if (ce != cudaSuccess) { h->host_out = false; DPQ_CUDA(ce); }
     } else {
       DPQ_CUDA(cudaStreamSynchronize(h->stream));
     }
