@@ -272,10 +272,13 @@ def main():
     ap.add_argument("--queries", type=int, default=None)
     ap.add_argument("--check", type=int, default=4)
     ap.add_argument("--encoder", default="tc", choices=["tc", "torch"])
+    ap.add_argument("--r2", type=int, default=None, help="override the config's r2 (the paper uses 9k-200k)")
     a = ap.parse_args()
     cfg = dict(CONFIGS[a.config])
     if a.n:
         cfg["n"] = a.n
+    if a.r2:
+        cfg["r2"] = a.r2
     nq = a.queries or (4096 if a.config == "c5" else 1024)
     t = time.time()
     w = build(cfg, nq=nq, encoder=a.encoder)
