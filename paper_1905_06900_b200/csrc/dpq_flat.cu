@@ -365,18 +365,24 @@ int run_small_tables(Index* h, int nslot, const void* prefix, int64_t npre,
   }
   ta.slot_list = slot_list;
   const int nlaunch = slot_list ? n_list : nslot;
-  constexpr int SPC = 8;
   const char* ms_env = getenv("DPQ_MS_MIN");  // test hook: many-slot K1 from this slot count (default 8192)
   const int ms_min = ms_env ? atoi(ms_env) : 8192;
+  const char* spc_env = getenv("DPQ_MS_SPC");  // slots per CTA of the many-slot K1 (2, 4 or 8)
+  const int spc = spc_env ? atoi(spc_env) : 8;
   const bool many = nlaunch >= ms_min && (h->dsub & 7) == 0 && h->dsub <= 128;
-  if (nlaunch > 0 && many) {  // IVF-size slot counts: SPC slots per CTA
-    const size_t smem_ms = (size_t)SPC * (h->d + h->m * h->kbar) * 4;
-    static bool attr_ms = false;
-    if (!attr_ms) {
-      cudaFuncSetAttribute(k_small_tables_ms<SPC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      attr_ms = true;
-    }
-    k_small_tables_ms<SPC><<<(nlaunch + SPC - 1) / SPC, 256, smem_ms, h->stream>>>(ta, nlaunch);
+  if (nlaunch > 0 && many) {  // IVF-size slot counts: spc slots per CTA
+    auto go = [&](auto kern, int S) {
+      static bool attr_ms[9] = {};
+      if (!attr_ms[S]) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr_ms[S] = true;
+      }
+      const size_t smem_ms = (size_t)S * (h->d + h->m * h->kbar) * 4;
+      kern<<<(nlaunch + S - 1) / S, 256, smem_ms, h->stream>>>(ta, nlaunch);
+    };
+    if (spc == 2) go(k_small_tables_ms<2>, 2);
+    else if (spc == 4) go(k_small_tables_ms<4>, 4);
+    else go(k_small_tables_ms<8>, 8);
     DPQ_LAUNCHED(h);
   } else if (nlaunch > 0) {
     k_small_tables<<<nlaunch, 256, smem, h->stream>>>(ta);

@@ -46,11 +46,6 @@ for rep in range(a.reps):
         _lib._lib = None
         idx = FlatIndex.from_arrays(w["codebooks"], w["derived"], w["codes"])
         h = idx._handle()
-        for kk, vv in saved.items():
-            if vv is None:
-                os.environ.pop(kk, None)
-            else:
-                os.environ[kk] = vv
         stream = torch.cuda.Stream()
         h.set_stream(stream.cuda_stream)
         L = _lib.lib()
@@ -82,6 +77,11 @@ for rep in range(a.reps):
             print(f"RESULTS DIFFER: {path}", flush=True)
         h.set_stream(None)
         del idx, h
+        for kk, vv in saved.items():  # the variant's environment held for its searches too
+            if vv is None:
+                os.environ.pop(kk, None)
+            else:
+                os.environ[kk] = vv
         torch.cuda.synchronize()
         results[path].append(float(np.median(ts)))
 for path in a.libs:
