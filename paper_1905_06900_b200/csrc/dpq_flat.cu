@@ -365,10 +365,11 @@ int run_small_tables(Index* h, int nslot, const void* prefix, int64_t npre,
   }
   ta.slot_list = slot_list;
   const int nlaunch = slot_list ? n_list : nslot;
-  const char* ms_env = getenv("DPQ_MS_MIN");  // test hook: many-slot K1 from this slot count (default 8192)
-  const int ms_min = ms_env ? atoi(ms_env) : 8192;
+  const char* ms_env = getenv("DPQ_MS_MIN");  // many-slot K1 from this slot count (default 256; test hook)
+  const int ms_min = ms_env ? atoi(ms_env) : 256;
   const char* spc_env = getenv("DPQ_MS_SPC");  // slots per CTA of the many-slot K1 (2, 4 or 8)
-  const int spc = spc_env ? atoi(spc_env) : 8;
+  // 4 slots per CTA at flat batch sizes (1024 queries: 256 CTAs, tables 59 -> 48 us), 8 for IVF slot counts
+  const int spc = spc_env ? atoi(spc_env) : (nlaunch >= 8192 ? 8 : 4);
   const bool many = nlaunch >= ms_min && (h->dsub & 7) == 0 && h->dsub <= 128;
   if (nlaunch > 0 && many) {  // IVF-size slot counts: spc slots per CTA
     auto go = [&](auto kern, int S) {
