@@ -58,6 +58,21 @@ __device__ __forceinline__ float pw_combine2(const f32x2_t r[4]) {
   return __fadd_rn(__fadd_rn(__fadd_rn(lo2(r[0]), hi2(r[0])), __fadd_rn(lo2(r[1]), hi2(r[1]))),
                    __fadd_rn(__fadd_rn(lo2(r[2]), hi2(r[2])), __fadd_rn(lo2(r[3]), hi2(r[3]))));
 }
+// pw_sqdist_v8 (8 | n <= 128, 16-B aligned rows) on lane pairs
+__device__ __forceinline__ float pw_sqdist_v8_x2(const float* __restrict__ c, const float* __restrict__ y, int n,
+                                                 f32x2_t z2) {
+  const ulonglong2* c2 = reinterpret_cast<const ulonglong2*>(c);
+  const ulonglong2* y2 = reinterpret_cast<const ulonglong2*>(y);
+  f32x2_t r[4];
+  for (int i = 0; i < n / 8; ++i) {
+    const ulonglong2 a = c2[2 * i], b = c2[2 * i + 1], p = y2[2 * i], q = y2[2 * i + 1];
+    const f32x2_t v[4] = {sqdiff2(a.x, p.x, z2), sqdiff2(a.y, p.y, z2), sqdiff2(b.x, q.x, z2),
+                          sqdiff2(b.y, q.y, z2)};
+#pragma unroll
+    for (int l = 0; l < 4; ++l) r[l] = (i == 0) ? v[l] : add2(r[l], v[l]);
+  }
+  return pw_combine2(r);
+}
 
 // n <= 128 block of the pairwise sum, c/y may be any address space.
 __device__ __forceinline__ float pw_block(const float* __restrict__ c,

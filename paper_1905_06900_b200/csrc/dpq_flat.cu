@@ -601,7 +601,7 @@ int run_group_tables(Index* h, int nq, int ystride) {
   ga.nq = nq; ga.m = h->m; ga.k = h->k; ga.kbar = h->kbar; ga.bbar = h->bbar; ga.dsub = h->dsub;
   ga.tables = w.tables; ga.n_entries = h->d_nent;
   const int gsize = h->k / h->kbar;
-  const int ld = h->dsub == 32 ? 36 : h->dsub + 1;
+  const int ld = ((h->dsub & 7) == 0 && h->dsub <= 128) ? h->dsub + 4 : h->dsub + 1;  // k_group_tables rows
   const size_t smem = (size_t)gsize * ld * 4 + (size_t)nq * 4;
   static size_t attr = 0;
   dim3 grid(h->kbar, h->m);

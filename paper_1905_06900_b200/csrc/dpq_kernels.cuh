@@ -1453,9 +1453,11 @@ __global__ void __launch_bounds__(256) k_group_tables(GroupTablesArgs a) {
   __shared__ int nact;
   const int g = blockIdx.x, j = blockIdx.y;
   const int dsub = DSUB > 0 ? DSUB : a.dsub;
-  // DSUB > 0: rows padded to 16-B multiples + 4 floats (conflict-free float4
-  // reads across consecutive rows); generic: +1 float
-  const int gsize = a.k / a.kbar, ld = DSUB > 0 ? DSUB + 4 : dsub + 1;
+  // DSUB > 0 or 8 | dsub <= 128: rows padded to 16-B multiples + 4 floats
+  // (conflict-free float4 reads across consecutive rows, paired-FP32 path);
+  // otherwise +1 float
+  const bool v8 = DSUB > 0 || ((dsub & 7) == 0 && dsub <= 128);
+  const int gsize = a.k / a.kbar, ld = DSUB > 0 ? DSUB + 4 : (v8 ? dsub + 4 : dsub + 1);
   int* act = reinterpret_cast<int*>(tile + gsize * ld);
   if (threadIdx.x == 0) nact = 0;
   for (int e = threadIdx.x; e < gsize * dsub; e += 256) {
@@ -1474,6 +1476,8 @@ __global__ void __launch_bounds__(256) k_group_tables(GroupTablesArgs a) {
     float v;
     if constexpr (DSUB > 0) {
       v = pw_sqdist_v8(row, yq, DSUB);  // both operands 16-B aligned
+    } else if (v8 && (reinterpret_cast<uintptr_t>(yq) & 15) == 0) {
+      v = pw_sqdist_v8_x2(row, yq, dsub, a.negzero2);  // e.g. config 5: dsub = 120
     } else {
       v = pw_sqdist(row, yq, dsub);
     }
