@@ -729,6 +729,10 @@ static int ivf_driver(Index* h, const float* y, int64_t nq, int r, int ma, int r
   int bsz = env_batch > 0 ? env_batch
                           : std::max(1, std::max(std::min(h->batch, (1 << 16) / std::max(ma, 1)),
                                                  std::min(4096, (1 << 18) / std::max(ma, 1))));
+  struct HostOutReset {
+    Index* h;
+    ~HostOutReset() { h->host_out = false; }
+  } host_out_reset{h};
   int64_t q0 = 0;
   while (q0 < nq) {
     const int nb = (int)std::min<int64_t>(bsz, nq - q0);
@@ -738,16 +742,19 @@ static int ivf_driver(Index* h, const float* y, int64_t nq, int r, int ma, int r
     const bool want_t = phase_us != nullptr;
     const bool old_t = h->timing;
     if (want_t) h->timing = true;
+    // derived: the refine writes its rows straight into the pinned staging buffers (see host_driver)
+    h->host_out = derived && r > 0;
     int rc = ivf_batch(h, nb, r, ma, r2, derived, res_rot ? res_rot + q0 * ma * h->d : nullptr,
                        cells ? cells + q0 * ma : nullptr);
     h->timing = old_t;
     if (rc == 100) { bsz = std::max(1, nb / 2); continue; }
     if (rc != DPQ_OK) return rc;
-    DPQ_CUDA(cudaMemcpyAsync(w.h_d, w.out_d, (size_t)nb * r * 8, cudaMemcpyDeviceToHost, h->stream));
-    DPQ_CUDA(cudaMemcpyAsync(w.h_i, w.out_i, (size_t)nb * r * 8, cudaMemcpyDeviceToHost, h->stream));
-    DPQ_CUDA(cudaStreamSynchronize(h->stream));
-    memcpy(dists + q0 * r, w.h_d, (size_t)nb * r * 8);
-    memcpy(ids + q0 * r, w.h_i, (size_t)nb * r * 8);
+    if (!h->host_out) {
+      DPQ_CUDA(cudaMemcpyAsync(w.h_d, w.out_d, (size_t)nb * r * 8, cudaMemcpyDeviceToHost, h->stream));
+      DPQ_CUDA(cudaMemcpyAsync(w.h_i, w.out_i, (size_t)nb * r * 8, cudaMemcpyDeviceToHost, h->stream));
+    }
+    DPQ_CUDA(sync_copy_out(h->stream, dists + q0 * r, w.h_d, (size_t)nb * r * 8, ids + q0 * r, w.h_i,
+                           (size_t)nb * r * 8));
     if (want_t) {
       const double per = 1000.0 / nb;
       for (int i = 0; i < nb; ++i) {
