@@ -276,10 +276,40 @@ __global__ void __launch_bounds__(NT) k_ivf_conventional(IvfConvArgs a) {
 // ---------------------------------------------------------------------------
 // Host side
 // ---------------------------------------------------------------------------
+// Page-locked host allocator: the plan's per-slot arrays (~1M entries per
+// 4096-query batch) are DMA'd to the device every batch.
+template <class T>
+struct PinnedAllocator {
+  using value_type = T;
+  PinnedAllocator() = default;
+  template <class U>
+  PinnedAllocator(const PinnedAllocator<U>&) {}
+  T* allocate(size_t n) {
+    void* p = nullptr;
+    if (cudaMallocHost(&p, n * sizeof(T)) != cudaSuccess) {
+      cudaGetLastError();
+      throw std::bad_alloc();
+    }
+    return static_cast<T*>(p);
+  }
+  void deallocate(T* p, size_t) { cudaFreeHost(p); }
+  template <class U>
+  bool operator==(const PinnedAllocator<U>&) const { return true; }
+  template <class U>
+  bool operator!=(const PinnedAllocator<U>&) const { return false; }
+};
+template <class T>
+using pinned_vector = std::vector<T, PinnedAllocator<T>>;
+
+struct IvfProbe { int64_t cell; int q, p; };  // one non-empty probe of a batch
+
 struct IvfPlan {
   int nq = 0, ma = 0, nts = 0, ntiles = 0;
   std::vector<int64_t> cells;          // (nq, ma)
-  std::vector<int> slot_query, slot_probe, tile_cell, bound_ts;
+  pinned_vector<int> slot_query, slot_probe;
+  std::vector<int> tile_cell, bound_ts;
+  std::vector<int> cnt, first, tile0, fill, ts_first;  // scratch of ivf_plan (capacity kept across batches)
+  std::vector<IvfProbe> ne;
   std::vector<int> live, bsrc;         // live (non-padding) slots; bound-source slots
   std::vector<int64_t> pre_off, pre_len, tile_row0, tile_nsamp;
   std::vector<int> unit_tile;
@@ -289,6 +319,7 @@ struct IvfPlan {
 };
 
 struct IvfBuffers {
+  IvfPlan plan;  // host plan of the last batch (reused: no per-batch allocation)
   int cap_q = 0, cap_ts = 0, cap_units = 0, cap_tiles = 0, cap_ma = 0;
   int64_t* cells = nullptr;
   float* ynat = nullptr;
@@ -404,11 +435,13 @@ static void ivf_plan(Index* h, IvfPlan& P, int nb, int ma, int r2) {
   const int K = h->n_cells;
   P.nq = nb;
   P.ma = ma;
-  struct S { int64_t cell; int q, p; };
+  using S = IvfProbe;
   // non-empty probes grouped by cell, (query, probe) order kept inside a
   // cell: a counting sort over the K cells (stable, O(nb*ma + K))
-  std::vector<int> cnt(K + 1, 0);
-  std::vector<int> first(nb, -1);
+  std::vector<int>& cnt = P.cnt;
+  std::vector<int>& first = P.first;
+  cnt.assign(K + 1, 0);
+  first.assign(nb, -1);
   int64_t tot_rows = 0;
   int nne = 0;
   for (int q = 0; q < nb; ++q)
@@ -422,7 +455,8 @@ static void ivf_plan(Index* h, IvfPlan& P, int nb, int ma, int r2) {
       tot_rows += len;
     }
   // tiles per cell and the first tile of each cell
-  std::vector<int> tile0(K + 1, 0);
+  std::vector<int>& tile0 = P.tile0;
+  tile0.assign(K + 1, 0);
   for (int c = 0; c < K; ++c) tile0[c + 1] = tile0[c] + (cnt[c + 1] + qt - 1) / qt;
   P.ntiles = tile0[K];
   P.nts = P.ntiles * qt;
@@ -431,10 +465,13 @@ static void ivf_plan(Index* h, IvfPlan& P, int nb, int ma, int r2) {
     for (int t = tile0[c]; t < tile0[c + 1]; ++t) P.tile_cell[t] = c;
   P.slot_query.assign(P.nts, -1);
   P.slot_probe.assign(P.nts, 0);
-  std::vector<int> fill(K, 0);
-  std::vector<int> ts_first(nb, -1);  // slot of each query's first non-empty probe
+  std::vector<int>& fill = P.fill;
+  std::vector<int>& ts_first = P.ts_first;  // slot of each query's first non-empty probe
+  fill.assign(K, 0);
+  ts_first.assign(nb, -1);
   P.live.resize(nne);
-  std::vector<S> ne(nne);
+  std::vector<S>& ne = P.ne;
+  ne.resize(nne);
   int k = 0;
   for (int q = 0; q < nb; ++q)
     for (int p = 0; p < ma; ++p) {
@@ -505,8 +542,8 @@ static void ivf_plan(Index* h, IvfPlan& P, int nb, int ma, int r2) {
   }
 }
 
-template <class T>
-static int h2d(T* dst, const std::vector<T>& v, cudaStream_t s) {
+template <class T, class A>
+static int h2d(T* dst, const std::vector<T, A>& v, cudaStream_t s) {
   if (v.empty()) return DPQ_OK;
   DPQ_CUDA(cudaMemcpyAsync(dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
   return DPQ_OK;
@@ -522,7 +559,7 @@ static int ivf_batch(Index* h, int nb, int r, int ma, int r2, bool derived, cons
   const int qt = qt_of(h->mpad);
   ev_rec(h, 0);
   DPQ_TRY(ivf_ensure(h, nb, ma, 0, 0, 0));
-  IvfPlan P;
+  IvfPlan& P = B.plan;  // persistent: vectors keep their capacity (no re-faulting per batch)
   P.cells.resize((size_t)nb * ma);
   if (cells_in) {
     memcpy(P.cells.data(), cells_in, P.cells.size() * 8);
@@ -578,7 +615,12 @@ static int ivf_batch(Index* h, int nb, int r, int ma, int r2, bool derived, cons
   auto now = []() { return std::chrono::duration<double, std::micro>(
                         std::chrono::steady_clock::now().time_since_epoch()).count(); };
   const double t_plan0 = trace ? now() : 0.0;
-  ivf_plan(h, P, nb, ma, r2);
+  try {
+    ivf_plan(h, P, nb, ma, r2);
+  } catch (const std::bad_alloc&) {
+    set_error("ivf plan: pinned host allocation failed");
+    return DPQ_ERR_NOMEM;
+  }
   const double t_plan1 = trace ? now() : 0.0;
   if (h->ws.cap == 0 && h->cap0 == 0) {
     // first emit capacity per query from the probed rows (a query emits ~r2
