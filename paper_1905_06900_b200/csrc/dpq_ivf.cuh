@@ -301,15 +301,14 @@ struct PinnedAllocator {
 template <class T>
 using pinned_vector = std::vector<T, PinnedAllocator<T>>;
 
-struct IvfProbe { int64_t cell; int q, p; };  // one non-empty probe of a batch
 
 struct IvfPlan {
   int nq = 0, ma = 0, nts = 0, ntiles = 0;
   std::vector<int64_t> cells;          // (nq, ma)
   pinned_vector<int> slot_query, slot_probe;
   std::vector<int> tile_cell, bound_ts;
-  std::vector<int> cnt, first, tile0, fill, ts_first;  // scratch of ivf_plan (capacity kept across batches)
-  std::vector<IvfProbe> ne;
+  std::vector<int> cnt, first, tile0, ts_first, cnt_t, base_t;  // scratch of ivf_plan (capacity kept)
+  std::vector<int64_t> nr, sq;
   std::vector<int> live, bsrc;         // live (non-padding) slots; bound-source slots
   std::vector<int64_t> pre_off, pre_len, tile_row0, tile_nsamp;
   std::vector<int> unit_tile;
@@ -431,61 +430,92 @@ static int ivf_probe_dev(Index* h, int nb, int ma) {
 // Build the slot / tile / unit plan on the host from the probe result.
 static void ivf_plan(Index* h, IvfPlan& P, int nb, int ma, int r2) {
   const int qt = qt_of(h->mpad);
-  const std::vector<int64_t>& off = h->h_offsets;
+  const int64_t* off = h->h_offsets.data();
   const int K = h->n_cells;
   P.nq = nb;
   P.ma = ma;
-  using S = IvfProbe;
-  // non-empty probes grouped by cell, (query, probe) order kept inside a
-  // cell: a counting sort over the K cells (stable, O(nb*ma + K))
-  std::vector<int>& cnt = P.cnt;
+  // Non-empty probes grouped by cell, (query, probe) order kept inside a
+  // cell: a counting sort over the K cells, parallel over contiguous query
+  // ranges with per-thread cell counts (thread t's probes of cell c follow
+  // those of threads < t, so the order is the sequential one).
+  const int T = std::max(1, std::min(8, nb / 256));
+  P.cnt_t.assign((size_t)T * K, 0);
   std::vector<int>& first = P.first;
-  cnt.assign(K + 1, 0);
   first.assign(nb, -1);
-  int64_t tot_rows = 0;
-  int nne = 0;
-  for (int q = 0; q < nb; ++q)
-    for (int p = 0; p < ma; ++p) {
-      const int64_t c = P.cells[(size_t)q * ma + p];
-      const int64_t len = off[c + 1] - off[c];
-      if (len <= 0) continue;
-      if (first[q] < 0) first[q] = p;
-      ++cnt[c + 1];
-      ++nne;
-      tot_rows += len;
-    }
-  // tiles per cell and the first tile of each cell
+  P.nr.assign(nb, 0);
+  P.sq.assign(nb, 0);
+  const int64_t* cells = P.cells.data();
+#pragma omp parallel num_threads(T)
+  {
+    const int t = omp_get_thread_num();
+    int* ct = P.cnt_t.data() + (size_t)t * K;
+    for (int q = nb * t / T; q < nb * (t + 1) / T; ++q)
+      for (int p = 0; p < ma; ++p) {
+        const int64_t c = cells[(size_t)q * ma + p];
+        const int64_t len = off[c + 1] - off[c];
+        if (len <= 0) continue;
+        if (first[q] < 0) first[q] = p;
+        ++ct[c];
+        P.nr[q] += len;
+      }
+  }
+  // tiles per cell, the first tile of each cell, per-thread slot bases
+  std::vector<int>& cnt = P.cnt;
   std::vector<int>& tile0 = P.tile0;
+  cnt.assign(K, 0);
   tile0.assign(K + 1, 0);
-  for (int c = 0; c < K; ++c) tile0[c + 1] = tile0[c] + (cnt[c + 1] + qt - 1) / qt;
+  P.base_t.assign((size_t)T * K, 0);
+  for (int c = 0; c < K; ++c) {
+    int acc = 0;
+    for (int t = 0; t < T; ++t) {
+      P.base_t[(size_t)t * K + c] = acc;
+      acc += P.cnt_t[(size_t)t * K + c];
+    }
+    cnt[c] = acc;
+    tile0[c + 1] = tile0[c] + (acc + qt - 1) / qt;
+  }
+  int64_t tot_rows = 0;
+  for (int q = 0; q < nb; ++q) tot_rows += P.nr[q];
   P.ntiles = tile0[K];
   P.nts = P.ntiles * qt;
   P.tile_cell.resize(P.ntiles);
   for (int c = 0; c < K; ++c)
     for (int t = tile0[c]; t < tile0[c + 1]; ++t) P.tile_cell[t] = c;
-  P.slot_query.assign(P.nts, -1);
-  P.slot_probe.assign(P.nts, 0);
-  std::vector<int>& fill = P.fill;
+  // guard sampling: one stride for the batch, exact when lists are short
+  const int64_t avg = nb > 0 ? tot_rows / std::max(1, nb) : 0;
+  P.stride = (avg <= h->exact_limit) ? 1 : std::max<int64_t>(1, avg / std::max<int64_t>(1, h->sample));
+  const int64_t stride = P.stride;
+  P.slot_query.resize(P.nts);
+  P.slot_probe.resize(P.nts);
   std::vector<int>& ts_first = P.ts_first;  // slot of each query's first non-empty probe
-  fill.assign(K, 0);
   ts_first.assign(nb, -1);
+  int* sqv = P.slot_query.data();
+  int* spv = P.slot_probe.data();
+  const int nts = P.nts;
+#pragma omp parallel num_threads(T)
+  {
+#pragma omp for schedule(static)
+    for (int i = 0; i < nts; ++i) { sqv[i] = -1; spv[i] = 0; }
+    const int t = omp_get_thread_num();
+    int* bt = P.base_t.data() + (size_t)t * K;
+    for (int q = nb * t / T; q < nb * (t + 1) / T; ++q)
+      for (int p = 0; p < ma; ++p) {
+        const int64_t c = cells[(size_t)q * ma + p];
+        const int64_t len = off[c + 1] - off[c];
+        if (len <= 0) continue;
+        const int ts = tile0[c] * qt + bt[c]++;  // slots of a cell's tiles fill front to back
+        sqv[ts] = q;
+        spv[ts] = p;
+        if (p == first[q]) ts_first[q] = ts;
+        if (stride > 1) P.sq[q] += (len + stride - 1) / stride;
+      }
+  }
+  int nne = 0;
+  for (int c = 0; c < K; ++c) nne += cnt[c];
   P.live.resize(nne);
-  std::vector<S>& ne = P.ne;
-  ne.resize(nne);
   int k = 0;
-  for (int q = 0; q < nb; ++q)
-    for (int p = 0; p < ma; ++p) {
-      const int64_t c = P.cells[(size_t)q * ma + p];
-      if (off[c + 1] - off[c] <= 0) continue;
-      const int ts = tile0[c] * qt + fill[c]++;  // slots of a cell's tiles fill front to back
-      P.slot_query[ts] = q;
-      P.slot_probe[ts] = p;
-      if (p == first[q]) ts_first[q] = ts;
-      ne[k++] = {c, q, p};
-    }
-  k = 0;
   for (int c = 0; c < K; ++c)  // live slots in slot order
-    for (int i = 0; i < fill[c]; ++i) P.live[k++] = tile0[c] * qt + i;
+    for (int i = 0; i < cnt[c]; ++i) P.live[k++] = tile0[c] * qt + i;
   // qmax prefix: first min(r2, len) rows of each query's first non-empty
   // list, one entry per bound-source slot (list order of P.bsrc)
   P.bound_ts.assign(nb, -1);
@@ -501,9 +531,6 @@ static void ivf_plan(Index* h, IvfPlan& P, int nb, int ma, int r2) {
     P.pre_off.push_back(off[c]);
     P.pre_len.push_back(std::min<int64_t>(r2, off[c + 1] - off[c]));
   }
-  // guard sampling: one stride for the batch, exact when lists are short
-  const int64_t avg = nb > 0 ? tot_rows / std::max(1, nb) : 0;
-  P.stride = (avg <= h->exact_limit) ? 1 : std::max<int64_t>(1, avg / std::max<int64_t>(1, h->sample));
   P.tile_row0.assign(P.ntiles, 0);
   P.tile_nsamp.assign(P.ntiles, 0);
   P.max_nsamp = 0;
@@ -515,16 +542,9 @@ static void ivf_plan(Index* h, IvfPlan& P, int nb, int ma, int r2) {
     P.max_nsamp = std::max(P.max_nsamp, P.tile_nsamp[t]);
   }
   P.lambda.assign(nb, -1.0);
-  if (P.stride > 1) {
-    std::vector<int64_t> sq(nb, 0), nr(nb, 0);
-    for (const S& x : ne) {
-      const int64_t len = off[x.cell + 1] - off[x.cell];
-      sq[x.q] += (len + P.stride - 1) / P.stride;
-      nr[x.q] += len;
-    }
+  if (P.stride > 1)
     for (int q = 0; q < nb; ++q)
-      P.lambda[q] = nr[q] > 0 ? (double)r2 * (double)sq[q] / (double)nr[q] : -1.0;
-  }
+      P.lambda[q] = P.nr[q] > 0 ? (double)r2 * (double)P.sq[q] / (double)P.nr[q] : -1.0;
   // scan units: each tile's list split into row ranges, ~8 units per SM
   const int sms = num_sms(h);
   const int64_t target = std::max<int64_t>(1, (8LL * sms));
