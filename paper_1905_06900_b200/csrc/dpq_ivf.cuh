@@ -81,9 +81,8 @@ __global__ void __launch_bounds__(NT) k_probe(const float* __restrict__ y, int d
 // Query-tiled probe (K <= 8192): k_probe_dist computes d2 for a tile of 16
 // queries x 256 centres per CTA with the centres staged through shared memory
 // (each centre row read once per 16 queries instead of once per query), same
-// f64 arithmetic as k_probe; k_probe_select sorts each query's K (d2, cell)
-// pairs with a stable block radix sort (cells ascending on input, so equal d2
-// keep the lower cell first) and writes the first ma.
+// f64 arithmetic as k_probe; k_probe_select keeps each query's ma smallest
+// (d2, cell) pairs — ties to the lower cell — and writes them sorted.
 constexpr int kProbeQT = 16, kProbeCT = 256, kProbeDC = 32;
 __global__ void __launch_bounds__(kProbeCT) k_probe_dist(const float* __restrict__ y, int d, int nq,
                                                           const float* __restrict__ centers, int K,
@@ -121,27 +120,31 @@ __global__ void __launch_bounds__(kProbeCT) k_probe_dist(const float* __restrict
       if (q0 + q < nq) d2[(int64_t)(q0 + q) * K + c0 + tid] = acc[q];
 }
 
-template <int ITEMS>
-__global__ void __launch_bounds__(256) k_probe_select(const double* __restrict__ d2, int K, int ma,
-                                                      int64_t* __restrict__ cells) {
-  using Sort = cub::BlockRadixSort<uint64_t, 256, ITEMS, int>;
-  extern __shared__ __align__(16) uint8_t probe_smem[];  // Sort::TempStorage (> 48 KB at ITEMS = 32)
-  typename Sort::TempStorage& tmp = *reinterpret_cast<typename Sort::TempStorage*>(probe_smem);
+template <int NT, int EPT>
+__global__ void __launch_bounds__(NT, 1) k_probe_select(const double* __restrict__ d2, int K, int ma,
+                                                        int64_t* __restrict__ cells) {
+  // the ma smallest (d2, cell) pairs of the query's K: exact radix select
+  // (select_r, the refine's), then a bitonic sort of the ma kept pairs
+  extern __shared__ __align__(16) uint8_t probe_smem[];
+  uint64_t* keys = reinterpret_cast<uint64_t*>(probe_smem);
+  int64_t* ids = reinterpret_cast<int64_t*>(keys + NT * EPT);
+  __shared__ SelShared S;
+  __shared__ uint64_t thr_k;
+  __shared__ int64_t thr_i;
   const int q = blockIdx.x;
-  uint64_t key[ITEMS];
-  int id[ITEMS];
-#pragma unroll
-  for (int e = 0; e < ITEMS; ++e) {  // blocked arrangement: thread t holds ids t*ITEMS .. +ITEMS-1
-    const int c = threadIdx.x * ITEMS + e;
-    key[e] = c < K ? (uint64_t)__double_as_longlong(d2[(int64_t)q * K + c]) : ~0ull;  // d2 >= 0: bits order
-    id[e] = c;
+  for (int i = threadIdx.x; i < K; i += NT) {
+    keys[i] = (uint64_t)__double_as_longlong(d2[(int64_t)q * K + i]);  // d2 >= 0: bits order as values
+    ids[i] = i;
   }
-  Sort(tmp).Sort(key, id);  // stable: equal keys keep ascending cell ids
-#pragma unroll
-  for (int e = 0; e < ITEMS; ++e) {
-    const int rank = threadIdx.x * ITEMS + e;
-    if (rank < ma) cells[(int64_t)q * ma + rank] = id[e];
-  }
+  __syncthreads();
+  if (K > ma) select_r<NT, EPT>(keys, ids, K, ma, S, thr_k, thr_i);
+  const int f = min(K, ma);
+  int P = 2;
+  while (P < f) P <<= 1;
+  for (int i = f + threadIdx.x; i < P; i += NT) { keys[i] = ~0ull; ids[i] = INT64_MAX; }
+  __syncthreads();
+  sort_pairs<NT>(keys, ids, P);
+  for (int i = threadIdx.x; i < ma; i += NT) cells[(int64_t)q * ma + i] = ids[i];
 }
 
 // residuals y - centre in f32 (ivf.py:120), natural (query, probe) order
@@ -399,15 +402,13 @@ static int ivf_probe_dev(Index* h, int nb, int ma) {
     const dim3 grid((unsigned)((h->n_cells + kProbeCT - 1) / kProbeCT), (unsigned)((nb + kProbeQT - 1) / kProbeQT));
     k_probe_dist<<<grid, kProbeCT, 0, h->stream>>>(h->ws.y, h->d, nb, h->centers, h->n_cells, b.d2);
     DPQ_LAUNCHED(h);
-    const int items = (h->n_cells + 255) / 256;
-    auto sel = [&](auto kern, size_t tmp) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tmp);
-      kern<<<nb, 256, tmp, h->stream>>>(b.d2, h->n_cells, ma, b.cells);
-    };
-    if (items <= 4) sel(k_probe_select<4>, sizeof(typename cub::BlockRadixSort<uint64_t, 256, 4, int>::TempStorage));
-    else if (items <= 8) sel(k_probe_select<8>, sizeof(typename cub::BlockRadixSort<uint64_t, 256, 8, int>::TempStorage));
-    else if (items <= 16) sel(k_probe_select<16>, sizeof(typename cub::BlockRadixSort<uint64_t, 256, 16, int>::TempStorage));
-    else sel(k_probe_select<32>, sizeof(typename cub::BlockRadixSort<uint64_t, 256, 32, int>::TempStorage));
+    const size_t smem = (size_t)1024 * 8 * 16;  // 8192 (key, id) pairs
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_probe_select<1024, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    k_probe_select<1024, 8><<<nb, 1024, smem, h->stream>>>(b.d2, h->n_cells, ma, b.cells);
     DPQ_LAUNCHED(h);
     return DPQ_OK;
   }
