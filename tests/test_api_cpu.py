@@ -108,3 +108,30 @@ def test_non_finite_queries_rejected_like_check_array(flat):
     idx2 = FlatIndex.from_arrays(g["codebooks"], g["derived"], g["codes"])
     with pytest.raises(ValueError, match="NaN"):
         idx2.search(np.asfortranarray(Y.astype(np.float64)), 5)
+
+
+def test_encoder_without_device_fails_loudly():
+    """The tensor-core encoder has no CPU fallback either."""
+    if _lib.device_count() > 0:
+        pytest.skip("a device is present")
+    with pytest.raises(RuntimeError, match="not available"):
+        _lib.Encoder(np.zeros((1, 16, 8), np.float32))
+
+
+def test_train_make_encoder_kinds():
+    from paper_1905_06900_b200 import train
+
+    with pytest.raises(ValueError, match="unknown encoder"):
+        train.make_encoder(np.zeros((1, 4, 2), np.float32), kind="nope")
+
+
+def test_finiteness_scan_parallel_path():
+    """dpq_all_finite on > 256 KB (the multi-threaded branch): finite, NaN
+    and inf anywhere, NaN winning over inf (check_array's order)."""
+    L = _lib.lib()
+    x = np.random.default_rng(1).normal(size=(4096, 128)).astype(np.float32)
+    assert L.dpq_all_finite(_lib.ptr(x), x.size) == 0
+    x[4000, 7] = np.inf
+    assert L.dpq_all_finite(_lib.ptr(x), x.size) == 2
+    x[10, 0] = np.nan
+    assert L.dpq_all_finite(_lib.ptr(x), x.size) == 1
