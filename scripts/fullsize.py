@@ -248,6 +248,8 @@ def check(w, r=100, check_queries=4, sub=8, device=0):
     # ---- phase split (CUDA events per batch, amortised per query)
     _, _, tm = idx.search(Y, r, return_timings=True, **kw)
     rep["phase_us_per_query"] = {k2: round(float(v.mean()), 3) for k2, v in tm.items()}
+    if cfg["kind"] == "ivf":
+        rep["counters"] = idx._handle().counters()
     if True:
         pm = idx._handle().phase_ms()
         rep["last_batch_ms"] = dict(zip(("tables", "guard", "scan", "threshold", "refine", "fallback", "total"),
