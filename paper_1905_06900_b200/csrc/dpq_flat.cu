@@ -324,7 +324,7 @@ static int launch_refine_buf(Index* h, const RefineArgs& ra, int nq) {
 
 template <int MODE>
 static int launch_refine(Index* h, const RefineArgs& ra, int nq) {
-  const int need = ra.r + 2 * kTopThreads;  // two candidates per thread per round
+  const int need = ra.r + DPQ_REFINE_U * kTopThreads;  // DPQ_REFINE_U candidates per thread per round
   if (need <= 1024) return launch_refine_buf<1024, MODE>(h, ra, nq);
   if (need <= 2048) return launch_refine_buf<2048, MODE>(h, ra, nq);
   if (need <= 4096) return launch_refine_buf<4096, MODE>(h, ra, nq);
@@ -608,7 +608,10 @@ int run_group_tables(Index* h, int nq, int ystride) {
   if (h->dsub == 32) {
     const size_t sm2 = (size_t)32 * 32 * 4 + (size_t)nq * 4;
     if (sm2 > 49152) cudaFuncSetAttribute(k_group_tables_reg<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
-    k_group_tables_reg<32><<<grid, 256, sm2, h->stream>>>(ga);
+#ifndef DPQ_K5_SPLIT
+#define DPQ_K5_SPLIT 2  // CTAs per (group, subspace): the busiest groups bound K5 (A/B: 1 -> 2 saves ~10 us)
+#endif
+    k_group_tables_reg<32><<<dim3(grid.x, grid.y, DPQ_K5_SPLIT), 256, sm2, h->stream>>>(ga);
   } else {
     if (smem > attr) cudaFuncSetAttribute(k_group_tables<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 49152));
     k_group_tables<0><<<grid, 256, smem, h->stream>>>(ga);

@@ -1399,7 +1399,8 @@ __global__ void __launch_bounds__(256) k_group_tables_reg(GroupTablesArgs a) {
   const int gsize = a.k / a.kbar;
   if (tid == 0) nact = 0;
   __syncthreads();
-  for (int q = tid; q < a.nq; q += 256)
+  // blockIdx.z of gridDim.z CTAs per group: queries q = z (mod gridDim.z)
+  for (int q = blockIdx.z + tid * gridDim.z; q < a.nq; q += 256 * gridDim.z)
     if ((int)a.q8[((int64_t)q * a.m + j) * a.kbar + g] <= a.bstar[q]) act[atomicAdd(&nact, 1)] = q;
   __syncthreads();
   const int n = nact;
@@ -1768,7 +1769,10 @@ __global__ void __launch_bounds__(NT, DPQ_REFINE_MINB) k_refine_topk(RefineArgs 
     id = row;  // (a row until id_of)
     return true;
   };
-  constexpr int U = 2;  // candidates per thread per round (two independent gather chains)
+#ifndef DPQ_REFINE_U
+#define DPQ_REFINE_U 2
+#endif
+  constexpr int U = DPQ_REFINE_U;  // candidates per thread per round (independent gather chains)
   auto pow2_at_least = [](int v) { int p = 2; while (p < v) p <<= 1; return p; };
   uint64_t ev[U];
   auto load_e = [&](int64_t base) {
