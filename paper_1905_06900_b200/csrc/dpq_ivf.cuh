@@ -759,6 +759,18 @@ static int ivf_batch(Index* h, int nb, int r, int ma, int r2, bool derived, cons
     }
   }
   ev_rec(h, 4);
+  if (trace && P.nts > 0) {  // guard and tile-mode histograms of this batch
+    std::vector<uint16_t> gq(nb);
+    std::vector<int> tf(P.ntiles);
+    cudaMemcpyAsync(gq.data(), B.guard_q, (size_t)nb * 2, cudaMemcpyDeviceToHost, h->stream);
+    cudaMemcpyAsync(tf.data(), w.tile_fast, (size_t)P.ntiles * 4, cudaMemcpyDeviceToHost, h->stream);
+    cudaStreamSynchronize(h->stream);
+    int gc[5] = {0, 0, 0, 0, 0}, tc[8] = {0};
+    for (int q = 0; q < nb; ++q) gc[gq[q] <= 30 ? 0 : gq[q] <= 62 ? 1 : gq[q] <= 126 ? 2 : gq[q] <= 254 ? 3 : 4]++;
+    for (int t = 0; t < P.ntiles; ++t) tc[std::min(7, std::max(0, tf[t]))]++;
+    fprintf(stderr, "[dpq ivf] guards <=30 %d, <=62 %d, <=126 %d, <=254 %d, other %d | tiles generic %d wide5 %d "
+            "wide6 %d 7bit %d\n", gc[0], gc[1], gc[2], gc[3], gc[4], tc[0], tc[5], tc[6], tc[7]);
+  }
   if (trace)
     fprintf(stderr, "[dpq ivf] plan %.1f us | uploads+first pass (host) %.1f us | live %zu of %d slots, %d tiles\n",
             t_plan1 - t_plan0, now() - t_plan1, P.live.size(), P.nts, P.ntiles);
