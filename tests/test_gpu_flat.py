@@ -135,6 +135,27 @@ def test_seeded_random_models_vs_oracle(case):
     assert _same(d0, d1)
 
 
+@pytest.mark.parametrize("seed", [1, 2, 3])
+@pytest.mark.parametrize("case", CASES)
+def test_seeded_random_models_more_seeds(case, seed):
+    """More seeds of the same shapes, plus single-query searches against the
+    batched ones (batch invariance at small sizes, padding-heavy tiles)."""
+    m, k, kbar, dsub, n, nq, r, r2 = case
+    rng = np.random.default_rng(seed * 7919 + CASES.index(case))
+    cb, der = _model(rng, m, k, kbar, dsub)
+    X = (cb[np.arange(m)[None, :], rng.integers(0, k, size=(n, m))].reshape(n, m * dsub)
+         + rng.normal(scale=0.5, size=(n, m * dsub))).astype(np.float32)
+    codes = _encode(cb, X)
+    Y = (X[rng.integers(0, n, size=nq)] + rng.normal(scale=0.3, size=(nq, m * dsub))).astype(np.float32)
+    d0, i0 = _oracle(cb, der, codes, Y, r, r2)
+    idx = FlatIndex.from_arrays(cb, der, codes)
+    d1, i1 = idx.search(Y, r, mode="derived", r2=r2)
+    assert np.array_equal(i0, i1) and _same(d0, d1)
+    for qi in range(min(nq, 3)):
+        d2, i2 = idx.search(Y[qi:qi + 1], r, mode="derived", r2=r2)
+        assert np.array_equal(i2[0], i0[qi]) and _same(d2[0], d0[qi])
+
+
 def test_edge_cases_vs_oracle():
     rng = np.random.default_rng(7)
     cb, der = _model(rng, 4, 256, 16, 4)
