@@ -360,6 +360,14 @@ __global__ void __launch_bounds__(256) k_build_lut(const uint8_t* __restrict__ q
       if (gw >= 0x8000u) atomicMax(&s_bmax, gw - 0x8000u);
     }
   const bool live_j = j < m;
+  __shared__ uint32_t sbias[G::QT / 4];  // wide-5 bias bytes of slots 4w..4w+3 (subspace 0 only)
+  if (gword && j == 0)
+    for (int w = tid; w < G::QT / 4; w += 256) {
+      uint32_t b4 = 0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) b4 |= wide_bias(gword[t * G::QT + 4 * w + b]) << (8 * b);
+      sbias[w] = b4;
+    }
   for (int i = tid; i < G::QT * 64; i += 256) {
     const int sl = i >> 6, w = i & 63;
     const int slot = t * G::QT + sl;
@@ -386,20 +394,26 @@ __global__ void __launch_bounds__(256) k_build_lut(const uint8_t* __restrict__ q
   const uint32_t cmax = mode == kModeWide5 ? 31u : (mode == kModeWide6 ? 63u : (mode == kMode7 ? 127u : 255u));
   const bool fold = mode == kModeWide5 && j == 0;
   if (tile_fast && j == 0 && tid == 0) tile_fast[t] = mode;
-  const uint8_t* sb = reinterpret_cast<const uint8_t*>(st);
   uint8_t* tbase = lut + (int64_t)t * G::LUT_BYTES + (int64_t)(j / G::SPR) * 256 * 256 + (j % G::SPR) * G::ROWB;
   constexpr int WPR = G::QT / 4;  // 32-bit words per table row
-  for (int i = tid; i < 256 * WPR; i += 256) {
-    const int g = i / WPR, w = i % WPR;
-    uint32_t v = 0;
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int sl = 4 * w + b;
-      uint32_t e = g < kbar ? (uint32_t)sb[sl * RW * 4 + g] : 0u;
-      e = min(e, cmax);
-      if (fold) e += wide_bias(gword[t * G::QT + sl]);  // <= 31 + 128
-      v |= e << (8 * b);
-    }
+  constexpr int WG = WPR / 8;     // 8-word groups per table row
+  // 4x4 byte transposes: lane (wi, c) of a warp reads staged word (slot
+  // 4w + c, groups 4gq..4gq+3) — conflict-free, RW = 65 — the 4 lanes of a
+  // quad exchange their words and each keeps byte c of all four, i.e. the
+  // table word (group 4gq + c, slots 4w..4w+3); clamped per byte, the wide-5
+  // bias added per slot byte (entries <= 31, bias <= 128: no carries).
+  const int lane = tid & 31, wi = lane >> 2, c = lane & 3, quad = lane & ~3;
+  const uint32_t sel = (uint32_t)c | ((uint32_t)(c + 4) << 4);
+  const uint32_t cmax4 = cmax * 0x01010101u;
+  for (int blk = tid >> 5; blk < 64 * WG; blk += 8) {
+    const int gq = blk / WG, w = (blk % WG) * 8 + wi;
+    const uint32_t mine = st[(4 * w + c) * RW + gq];
+    const uint32_t i0 = __shfl_sync(0xffffffffu, mine, quad), i1 = __shfl_sync(0xffffffffu, mine, quad + 1);
+    const uint32_t i2 = __shfl_sync(0xffffffffu, mine, quad + 2), i3 = __shfl_sync(0xffffffffu, mine, quad + 3);
+    const int g = 4 * gq + c;
+    uint32_t v = g < kbar ? __byte_perm(__byte_perm(i0, i1, sel), __byte_perm(i2, i3, sel), 0x5410) : 0u;
+    if (cmax < 255u) v = __vminu4(v, cmax4);
+    if (fold) v += sbias[w];
     reinterpret_cast<uint32_t*>(tbase + (int64_t)g * 256)[w] = v;
   }
 }
