@@ -183,13 +183,14 @@ __global__ void k_slot_bounds(const double* __restrict__ qmin, const double* __r
   bounds[2 * ts + 1] = b < 0 ? 0.0 : qmax[b];
 }
 
+// per-query histograms from the live slots' histograms (padding slots skipped)
 __global__ void k_slot_hist_to_query(const uint32_t* __restrict__ hts, const int* __restrict__ slot_query,
-                                     int nts, uint32_t* __restrict__ hq) {
+                                     const int* __restrict__ live, int nlive, uint32_t* __restrict__ hq) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= (int64_t)nts * 256) return;
-  const int ts = (int)(i >> 8), b = (int)(i & 255);
+  if (i >= (int64_t)nlive * 256) return;
+  const int ts = live[i >> 8], b = (int)(i & 255);
   const int q = slot_query[ts];
-  const uint32_t v = hts[i];
+  const uint32_t v = hts[(int64_t)ts * 256 + b];
   if (q >= 0 && v) atomicAdd(hq + (int64_t)q * 256 + b, v);
 }
 
@@ -706,8 +707,8 @@ static int ivf_batch(Index* h, int nb, int r, int ma, int r2, bool derived, cons
       DPQ_TRY(h2d(B.tile_nsamp, ns, h->stream));
       DPQ_TRY(build_lut(h, P.nts, nullptr, nullptr, w.slot_query));  // histograms need unclamped entries
       DPQ_TRY(launch_hist(h, P.ntiles, nullptr, stride, mx, h->plane, B.tile_row0, B.tile_nsamp));
-      k_slot_hist_to_query<<<(unsigned)(((int64_t)P.nts * 256 + 255) / 256), 256, 0, h->stream>>>(
-          w.hist, w.slot_query, P.nts, B.hist_q);
+      k_slot_hist_to_query<<<(unsigned)(((int64_t)P.live.size() * 256 + 255) / 256), 256, 0, h->stream>>>(
+          w.hist, w.slot_query, B.live, (int)P.live.size(), B.hist_q);
       DPQ_LAUNCHED(h);
       k_guard<<<(nb + 127) / 128, 128, 0, h->stream>>>(B.hist_q, nb, r2, 0.0, exact ? 1 : 0, only, B.guard_q,
                                                         B.gword_q, exact ? nullptr : B.lambda);
