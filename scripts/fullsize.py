@@ -275,6 +275,7 @@ def main():
     ap.add_argument("--check", type=int, default=4)
     ap.add_argument("--encoder", default="tc", choices=["tc", "torch"])
     ap.add_argument("--r2", type=int, default=None, help="override the config's r2 (the paper uses 9k-200k)")
+    ap.add_argument("--r", type=int, default=100, help="results per query (k)")
     a = ap.parse_args()
     cfg = dict(CONFIGS[a.config])
     if a.n:
@@ -285,7 +286,7 @@ def main():
     t = time.time()
     w = build(cfg, nq=nq, encoder=a.encoder)
     setup = time.time() - t
-    rep = check(w, check_queries=a.check)
+    rep = check(w, r=a.r, check_queries=a.check)
     rep["setup_s"] = round(setup, 1)
     print(json.dumps(rep))
 
