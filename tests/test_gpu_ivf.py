@@ -96,6 +96,21 @@ def test_random_ivf_vs_oracle(seed, n, K, ma, r, r2, empty):
     assert np.array_equal(i0, i1) and _same(d0, d1)
 
 
+@pytest.mark.parametrize("seed", [21, 22, 23])
+@pytest.mark.parametrize("n,K,ma,r,r2,empty", [(4000, 16, 4, 10, 300, 0), (3000, 32, 8, 20, 500, 5),
+                                               (500, 64, 3, 40, 60, 30), (8000, 128, 16, 50, 800, 40)])
+def test_random_ivf_more_seeds(seed, n, K, ma, r, r2, empty):
+    """More seeds, plus single-query searches against the batched ones."""
+    idx, Y = _random_ivf(seed * 31 + K, n, K, empty=empty)
+    ivf = _oracle_ivf(idx)
+    d0, i0 = O.ivf_search(ivf, Y, r, ma, "derived", r2)
+    d1, i1 = idx.search(Y, r, ma=ma, mode="derived", r2=r2)
+    assert np.array_equal(i0, i1) and _same(d0, d1)
+    for qi in range(3):
+        d2, i2 = idx.search(Y[qi:qi + 1], r, ma=ma, mode="derived", r2=r2)
+        assert np.array_equal(i2[0], i0[qi]) and _same(d2[0], d0[qi])
+
+
 @pytest.mark.parametrize("dsub,kbar", [(8, 16), (16, 256), (32, 64)])
 def test_many_slot_tables_vs_oracle(dsub, kbar, monkeypatch):
     """The many-slot K1 (8 slots per CTA, paired-FP32 entries) that IVF
