@@ -21,17 +21,19 @@
 //
 // Kernel structure (persistent, one CTA per SM, 10 warps):
 //   warp 0     TMA producer: cp.async.bulk of pre-swizzled centroid tiles
-//              (128 centroids x [hi 128 B | lo 128 B | norm 32 B] = 36 KB)
-//              into a 4-stage smem ring (full/empty mbarriers)
-//   warp 1     TMEM allocator + MMA issuer (one elected thread): per tile
-//              and 128-row block, 9 or 13 tcgen05.mma (M=128, N=128, K=8)
-//              into a double-buffered TMEM accumulator (2 x 256 columns)
-//   warps 2-9  epilogue: tcgen05.ld 32 columns at a time, running min and
-//              argmin per row (one TMEM lane per thread); they also stage the
-//              next unit's 256 query rows (x_hi/x_lo, SWIZZLE_128B) in smem.
-// A unit is (subspace j, 256 consecutive rows); CTAs sweep units so that the
+//              (256 centroids x [hi 128 B | lo 128 B | norm 32 B] = 72 KB)
+//              into a 2-stage smem ring (full/empty mbarriers)
+//   warp 1     TMEM allocator + MMA issuer (one elected thread): per tile,
+//              9 or 13 tcgen05.mma (M=128, N=256, K=8) into a double-buffered
+//              TMEM accumulator (2 x 256 columns)
+//   warps 2-9  epilogue: 4 lane quarters x 2 column halves; tcgen05.ld 32
+//              columns at a time, running (min, first index) per row, the two
+//              halves merged per unit; they also stage the next unit's 128
+//              query rows (x_hi/x_lo, SWIZZLE_128B) in smem.
+// A unit is (subspace j, 128 consecutive rows); CTAs sweep units so that the
 // CTAs running at any moment share one subspace's 18 MB centroid operand in
-// L2.
+// L2.  (N = 128 tiles with 2 row blocks measured 1.23x slower: the single
+// issuing thread pays ~100-200 cycles per MMA, so fewer, wider MMAs win.)
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -46,21 +48,23 @@
 namespace dpq {
 namespace enc {
 
-constexpr int BN = 128;                    // centroids per tile (MMA N)
+constexpr int BN = 256;                    // centroids per tile (MMA N)
 constexpr int BM = 128;                    // rows per row block (MMA M)
-constexpr int RB = 2;                      // row blocks per unit
-constexpr int STAGES = 4;
-constexpr int ATOM = BM * 128;             // 16 KB: 128 rows x 32 f32, SWIZZLE_128B K-major
-constexpr int NORMB = 128 * 32;            // 4 KB: 128 rows x 8 f32, no swizzle (core matrices)
-constexpr int TILE_B = 2 * ATOM + NORMB;   // 36 KB per centroid tile
-constexpr int A_RB = 2 * ATOM;             // x_hi, x_lo of one row block
+constexpr int RB = 1;                      // row blocks per unit
+constexpr int STAGES = 2;
+constexpr int ATOM = BN * 128;             // 32 KB: 256 centroid rows x 32 f32, SWIZZLE_128B K-major
+constexpr int ATOM_A = BM * 128;           // 16 KB: 128 query rows
+constexpr int NORMB = BN * 32;             // 8 KB: 256 rows x 8 f32, no swizzle (core matrices)
+constexpr int NORMB_A = BM * 32;           // 4 KB: the constant "ones" A block
+constexpr int TILE_B = 2 * ATOM + NORMB;   // 72 KB per centroid tile
+constexpr int A_RB = 2 * ATOM_A;           // x_hi, x_lo of one row block
 constexpr int kThreads = 320;
 constexpr int kEpiWarps = 8;
 // smem carve-up (offsets from a 1024-B aligned base)
 constexpr int OFF_B = 0;
 constexpr int OFF_A = OFF_B + STAGES * TILE_B;  // 147456
 constexpr int OFF_ONES = OFF_A + RB * A_RB;     // +65536
-constexpr int OFF_BAR = OFF_ONES + NORMB;       // +4096
+constexpr int OFF_BAR = OFF_ONES + NORMB_A;     // +4096
 constexpr int SMEM_BYTES = OFF_BAR + 256 + 1024;  // barriers + alignment slack
 constexpr uint32_t kTmemCols = 512;
 constexpr float kPadNorm = 1.2676506e30f;  // 2^100: padded centroids never win
@@ -302,7 +306,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_encode_tc(EncArgs a) {
             if (three) {
 #pragma unroll
               for (int kk = 0; kk < 4; ++kk)  // x_lo . (-2c)_hi
-                mma_tf32(d, desc_sw128(ab + ATOM + kk * 32), desc_sw128(bb + kk * 32), 1);
+                mma_tf32(d, desc_sw128(ab + ATOM_A + kk * 32), desc_sw128(bb + kk * 32), 1);
             }
             mma_tf32(d, desc_plain(sOnes32), desc_plain(bb + 2 * ATOM), 1);  // + ||c||^2
           }
@@ -314,17 +318,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_encode_tc(EncArgs a) {
     }
   } else {
     // ---------------------------------------------------------- epilogue --
-    const int et = threadIdx.x - 64;        // 0..255: row staged by this thread
+    const int et = threadIdx.x - 64;        // 0..255
     const int q = warp & 3;                 // TMEM lane quarter this warp may access
-    const int rb = (warp - 2) >> 2;         // row block whose accumulator it reads
+    const int half = (warp - 2) >> 2;       // column half of each tile it scans
+    const int rb = 0;
     const int row_in_blk = q * 32 + lane;
+    __shared__ float hbest[BM];
+    __shared__ int hidx[BM];
     uint64_t acc_t = 0;
     for (int64_t u = blockIdx.x; u < a.units; u += gridDim.x) {
       const int j = (int)(u / a.nblk);
       const int64_t r0 = (u % a.nblk) * (RB * BM);
-      {  // stage x_hi / x_lo of rows r0 .. r0+255 (all MMAs of the previous unit are complete)
-        const int64_t gr = r0 + et;
-        const int rba = et >> 7, rr = et & 127;
+      {  // stage x_hi / x_lo of rows r0 .. r0+127 (all MMAs of the previous unit are complete)
+        const int64_t gr = et < BM ? r0 + et : a.n;  // threads 128..255 stage nothing
+        const int rba = 0, rr = et & 127;
         uint8_t* dst = sA + rba * A_RB;
         int any_lo = 0;
         const float* src = a.x + gr * a.ldx + (int64_t)j * a.dsub;
@@ -346,8 +353,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_encode_tc(EncArgs a) {
             lo[e] = v[e] - hi[e];
             any_lo |= lo[e] != 0.f;
           }
-          *reinterpret_cast<float4*>(dst + sw128(rr, ch)) = make_float4(hi[0], hi[1], hi[2], hi[3]);
-          *reinterpret_cast<float4*>(dst + ATOM + sw128(rr, ch)) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+          if (et < BM) *reinterpret_cast<float4*>(dst + sw128(rr, ch)) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+          if (et < BM) *reinterpret_cast<float4*>(dst + ATOM_A + sw128(rr, ch)) = make_float4(lo[0], lo[1], lo[2], lo[3]);
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         int any;
@@ -370,9 +377,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_encode_tc(EncArgs a) {
         const uint32_t buf = (uint32_t)(acc_t & 1), ap = (uint32_t)((acc_t >> 1) & 1);
         bar_wait(&tfull[buf], ap);
         tc_after_sync();
-        const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + buf * (RB * BN) + rb * BN;
+        const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + buf * (RB * BN) + rb * BN + half * (BN / 2);
 #pragma unroll 1
-        for (int ch = 0; ch < BN / 32; ++ch) {
+        for (int ch = 0; ch < BN / 64; ++ch) {
           float v[32];
           tmem_ld32(base + ch * 32, v);
           float m8[8];
@@ -385,15 +392,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_encode_tc(EncArgs a) {
 #pragma unroll
             for (int i = 31; i >= 0; --i) f = v[i] == mn ? i : f;
             best = mn;
-            bidx = t * BN + ch * 32 + f;
+            bidx = t * BN + half * (BN / 2) + ch * 32 + f;
           }
         }
         tc_before_sync();
         __syncwarp();
         if (lane == 0) bar_arrive(&tempty[buf]);
       }
-      const int64_t gr = r0 + rb * BM + row_in_blk;
-      if (gr < a.n) a.codes[gr * a.m + j] = bidx;
+      // merge the two column halves: (min value, then lowest index)
+      if (half == 1) { hbest[row_in_blk] = best; hidx[row_in_blk] = bidx; }
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      if (half == 0) {
+        const float ob = hbest[row_in_blk];
+        const int oi = hidx[row_in_blk];
+        if (ob < best || (ob == best && oi < bidx)) { best = ob; bidx = oi; }
+        const int64_t gr = r0 + row_in_blk;
+        if (gr < a.n) a.codes[gr * a.m + j] = bidx;
+      }
+      asm volatile("bar.sync 1, 256;" ::: "memory");
     }
   }
   tc_before_sync();
