@@ -456,6 +456,28 @@ using dpq::Encoder;
 
 extern "C" {
 
+static int encoder_init(Encoder* e, const float* codebooks) {
+  const int m = e->m, k = e->k, dsub = e->dsub;
+  ENC_CUDA(cudaDeviceGetAttribute(&e->sms, cudaDevAttrMultiProcessorCount, e->device));
+  ENC_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+  ENC_CUDA(cudaMalloc(&e->gB, (size_t)m * e->nt * dpq::enc::TILE_B));
+  float* d_cb = nullptr;
+  const size_t cb_bytes = (size_t)m * k * dsub * sizeof(float);
+  ENC_CUDA(cudaMalloc(&d_cb, cb_bytes));
+  struct FreeCb {
+    float* p;
+    ~FreeCb() { cudaFree(p); }
+  } free_cb{d_cb};
+  ENC_CUDA(cudaMemcpyAsync(d_cb, codebooks, cb_bytes, cudaMemcpyHostToDevice, e->stream));
+  const int64_t total = (int64_t)m * e->nt * dpq::enc::BN;
+  dpq::enc::k_enc_prep<<<(unsigned)((total + 255) / 256), 256, 0, e->stream>>>(d_cb, m, k, dsub, e->nt, e->gB);
+  ENC_CUDA(cudaGetLastError());
+  ENC_CUDA(cudaStreamSynchronize(e->stream));
+  ENC_CUDA(cudaFuncSetAttribute(dpq::enc::k_encode_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                dpq::enc::SMEM_BYTES));
+  return DPQ_OK;
+}
+
 int dpq_encoder_create(int device, int m, int k, int dsub, const float* codebooks, dpq_encoder_t** out) {
   if (!out || !codebooks || m < 1 || k < 1 || dsub < 1) {
     dpq::set_error("dpq_encoder_create: invalid arguments");
@@ -471,20 +493,11 @@ int dpq_encoder_create(int device, int m, int k, int dsub, const float* codebook
   e->device = device;
   e->m = m; e->k = k; e->dsub = dsub;
   e->nt = (k + dpq::enc::BN - 1) / dpq::enc::BN;
-  ENC_CUDA(cudaDeviceGetAttribute(&e->sms, cudaDevAttrMultiProcessorCount, device));
-  ENC_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
-  float* d_cb = nullptr;
-  const size_t cb_bytes = (size_t)m * k * dsub * sizeof(float);
-  ENC_CUDA(cudaMalloc(&d_cb, cb_bytes));
-  ENC_CUDA(cudaMalloc(&e->gB, (size_t)m * e->nt * dpq::enc::TILE_B));
-  ENC_CUDA(cudaMemcpyAsync(d_cb, codebooks, cb_bytes, cudaMemcpyHostToDevice, e->stream));
-  const int64_t total = (int64_t)m * e->nt * dpq::enc::BN;
-  dpq::enc::k_enc_prep<<<(unsigned)((total + 255) / 256), 256, 0, e->stream>>>(d_cb, m, k, dsub, e->nt, e->gB);
-  ENC_CUDA(cudaGetLastError());
-  ENC_CUDA(cudaStreamSynchronize(e->stream));
-  cudaFree(d_cb);
-  ENC_CUDA(cudaFuncSetAttribute(dpq::enc::k_encode_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                dpq::enc::SMEM_BYTES));
+  const int rc = encoder_init(e, codebooks);
+  if (rc != DPQ_OK) {  // no leak on a failed creation
+    dpq_encoder_destroy(reinterpret_cast<dpq_encoder_t*>(e));
+    return rc;
+  }
   *out = reinterpret_cast<dpq_encoder_t*>(e);
   return DPQ_OK;
 }
