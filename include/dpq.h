@@ -163,6 +163,36 @@ int dpq_shard_finish(dpq_index_t* index, const int32_t* cand_hist_sum,
                      int r, int r2, double* dists, int64_t* ids,
                      uint8_t* need_exact);
 
+/* Device-resident form of the same protocol: every buffer is a device
+ * pointer on the index's device and every call only enqueues work on the
+ * index stream (no host synchronisation), so the caller runs the two
+ * histogram all-reduces in place on that stream (NCCL) between the calls.
+ * Instead of redoing internally, a query whose guard proved too tight (1)
+ * or whose emit list overflowed on this shard (2) is flagged in `flags`
+ * (nq u8, device); the caller all-reduces the flags (max) and repeats a
+ * flagged batch through the host-buffer protocol above (exact = 1).
+ * n_sampled is written on the host at once (it depends only on the
+ * shard's size).  The per-shard top-r of all shards, all-gathered as
+ * (n_parts, nq, r), is merged by dpq_merge_topr_dev.                      */
+int dpq_shard_begin_dev(dpq_index_t* index, const float* yr, int64_t nq,
+                        int r2, int64_t n_global, int exact,
+                        int32_t* sample_hist, int64_t* n_sampled);
+int dpq_shard_scan_dev(dpq_index_t* index, const int32_t* sample_hist_sum,
+                       int64_t n_global, int64_t sample_global, int r2,
+                       int exact, int32_t* cand_hist);
+int dpq_shard_finish_dev(dpq_index_t* index, const int32_t* cand_hist_sum,
+                         int r, int r2, double* dists, int64_t* ids,
+                         uint8_t* flags);
+/* Exact (dist, id) top-r of n_parts per-shard top-r lists, each sorted and
+ * padded with (+inf, -1): part_dists/part_ids (n_parts, nq, r) device ->
+ * dists/ids (nq, r) device (ResultSet.from_arrays over the union,
+ * search.py:115-124).  Enqueued on the index stream.                      */
+int dpq_merge_topr_dev(dpq_index_t* index, const double* part_dists,
+                       const int64_t* part_ids, int n_parts, int64_t nq,
+                       int r, double* dists, int64_t* ids);
+/* Wait for everything enqueued on the index stream. */
+int dpq_sync(dpq_index_t* index);
+
 /* ------------------------------------------------ unit seams (debug) --
  * Replace compute_tables(yr, derived_codebooks_) + quantize_tables
  * (search.py:28-48, twopass.py:63-85) for nq queries: small (nq,m,kbar) f32,
@@ -170,10 +200,20 @@ int dpq_shard_finish(dpq_index_t* index, const int32_t* cand_hist_sum,
 int dpq_debug_quantize_tables(dpq_index_t* index, const float* yr,
                               int64_t nq, int r2, float* small, uint8_t* q,
                               double* qmin, double* qmax);
-/* adc_low_batch (twopass.py:99-106) of every code for nq queries:
- * scores (nq, n) u8.                                                      */
+/* adc_low_batch (twopass.py:99-106) of every code for nq queries, with
+ * the tables quantize_tables (twopass.py:63-85) builds from the first
+ * min(r2, n) codes: scores (nq, n) u8 in the caller's row order.          */
 int dpq_debug_low_scores(dpq_index_t* index, const float* yr, int64_t nq,
                          int r2, uint8_t* scores);
+/* The candidate ids refine scores (scan_derived -> CappedBuckets ->
+ * refine's bucket walk, twopass.py:171-217, 276-302), in walk order:
+ * ascending score, ties by ascending id.  For query q, counts[q] = number
+ * of candidates; the first min(counts[q], cap) ids go to ids[q*cap ...]
+ * and, when scores != NULL, their 8-bit scores to scores[q*cap ...].
+ * Call with cap = 0 to size the buffers.                                  */
+int dpq_debug_candidate_ids(dpq_index_t* index, const float* yr, int64_t nq,
+                            int r2, int64_t cap, int64_t* ids,
+                            uint8_t* scores, int64_t* counts);
 /* CappedBuckets bound + refine walk (twopass.py:171-201, 276-308):
  * bstar (nq) i32 and ncand (nq) i64 = |{s <= b*, s < 255}|.               */
 int dpq_debug_candidates(dpq_index_t* index, const float* yr, int64_t nq,
@@ -215,6 +255,11 @@ int dpq_last_phase_ms(dpq_index_t* index, float* ms7);
  * computed by the group-lazy table builder, scan units run by the wide
  * (5/6-bit, 16 queries per lane) loop.                                    */
 int dpq_counters(dpq_index_t* index, int64_t* out8);
+/* Extended counters (n of them; unknown slots read 0): [0..7] as
+ * dpq_counters, [8] code-plane rows the first-pass scan read (summed over
+ * query tiles; 4 or 8 B each), [9] LUT tile loads of the scan (128 KB each).
+ * With [5] (emitted entries, 8 B each) they give the scan's bytes moved. */
+int dpq_counters_ex(dpq_index_t* index, int64_t* out, int n);
 
 #ifdef __cplusplus
 }

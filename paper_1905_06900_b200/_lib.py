@@ -48,10 +48,17 @@ SIGNATURES = {
     "dpq_shard_begin": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_int64, c_int, c_void_p, c_void_p]),
     "dpq_shard_scan": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int, c_int, c_void_p]),
     "dpq_shard_finish": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p]),
+    "dpq_shard_begin_dev": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_int64, c_int, c_void_p, c_void_p]),
+    "dpq_shard_scan_dev": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int, c_int, c_void_p]),
+    "dpq_shard_finish_dev": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p]),
+    "dpq_merge_topr_dev": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int64, c_int, c_void_p, c_void_p]),
+    "dpq_sync": (c_int, [c_void_p]),
     "dpq_debug_quantize_tables": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_void_p, c_void_p,
                                           c_void_p, c_void_p]),
     "dpq_debug_low_scores": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_void_p]),
     "dpq_debug_candidates": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_void_p, c_void_p]),
+    "dpq_debug_candidate_ids": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_int64, c_void_p, c_void_p,
+                                        c_void_p]),
     "dpq_debug_full_tables": (c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
     "dpq_encoder_create": (c_int, [c_int, c_int, c_int, c_int, c_void_p, POINTER(c_void_p)]),
     "dpq_encoder_destroy": (None, [c_void_p]),
@@ -59,6 +66,7 @@ SIGNATURES = {
     "dpq_encode_dev": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
     "dpq_last_phase_ms": (c_int, [c_void_p, c_void_p]),
     "dpq_counters": (c_int, [c_void_p, c_void_p]),
+    "dpq_counters_ex": (c_int, [c_void_p, c_void_p, c_int]),
 }
 
 
@@ -140,6 +148,12 @@ class Handle:
         return dict(zip(("launches", "queries", "rows_scanned", "refined", "fallbacks", "emitted",
                              "table_entries", "wide_units"),
                         out.tolist()))
+
+    def counters_ex(self) -> dict:
+        out = np.zeros(10, dtype=np.int64)
+        check(lib().dpq_counters_ex(self.raw, ptr(out), 10))
+        return dict(zip(("launches", "queries", "rows_scanned", "refined", "fallbacks", "emitted",
+                         "table_entries", "wide_units", "plane_rows", "lut_loads"), out.tolist()))
 
     def set_timing(self, on: bool) -> None:
         check(lib().dpq_set_timing(self.raw, int(bool(on))))
@@ -250,9 +264,21 @@ class Encoder:
         Enqueued on `stream_ptr`, default torch's current stream of x's device
         (the legacy default stream is passed as cudaStreamLegacy, not NULL,
         which would select the encoder's private stream)."""
-        if stream_ptr is None:
-            import torch
+        import torch
 
+        if not (isinstance(x, torch.Tensor) and isinstance(codes, torch.Tensor)):
+            raise ValueError("encode_dev takes CUDA tensors")
+        if x.device.type != "cuda" or x.device.index != self.device:
+            raise ValueError(f"x must live on cuda:{self.device}, got {x.device}")
+        if codes.device != x.device:
+            raise ValueError(f"codes must live on {x.device}, got {codes.device}")
+        if x.dtype != torch.float32 or x.dim() != 2 or x.stride(1) != 1 or x.shape[1] < self.m * self.dsub:
+            raise ValueError(f"x must be float32 (n, >= {self.m * self.dsub}) with unit inner stride, got "
+                             f"{x.dtype} {tuple(x.shape)} strides {tuple(x.stride())}")
+        if codes.dtype != torch.int32 or tuple(codes.shape) != (x.shape[0], self.m) or not codes.is_contiguous():
+            raise ValueError(f"codes must be a contiguous int32 ({x.shape[0]}, {self.m}) tensor, got "
+                             f"{codes.dtype} {tuple(codes.shape)}")
+        if stream_ptr is None:
             stream_ptr = torch.cuda.current_stream(x.device).cuda_stream
         check(lib().dpq_encode_dev(self.raw, ptr(x), int(x.shape[0]), int(x.stride(0)), ptr(codes),
                                    c_void_p(stream_ptr or 1)), "dpq_encode_dev")

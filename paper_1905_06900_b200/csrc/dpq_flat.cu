@@ -18,7 +18,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/dpq.h"
 #include "dpq_impl.h"
@@ -89,6 +92,32 @@ static int hmalloc(T** p, size_t count) {
     return DPQ_ERR_NOMEM;
   }
   return DPQ_OK;
+}
+
+// Dynamic shared memory above 48 KB needs a per-(device, kernel) attribute.
+// The largest size set so far is cached per (device, kernel) and recorded
+// only after the call succeeds, so a failed request (too large) never
+// masks a later valid one.  Cheap enough to call before every launch.
+static int set_smem_impl(int device, const void* kern, size_t bytes) {
+  if (bytes <= 48 * 1024) return DPQ_OK;
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> done;
+  std::lock_guard<std::mutex> lock(mu);
+  const auto key = std::make_pair(device, kern);
+  const auto it = done.find(key);
+  if (it != done.end() && it->second >= bytes) return DPQ_OK;
+  const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    set_error("dynamic shared memory of " + std::to_string(bytes) + " B not available: " + cudaGetErrorString(e));
+    return DPQ_ERR_ARG;
+  }
+  done[key] = bytes;
+  return DPQ_OK;
+}
+template <class K>
+static int set_smem(const Index* h, K* kern, size_t bytes) {
+  return set_smem_impl(h->device, reinterpret_cast<const void*>(kern), bytes);
 }
 
 static inline int qt_of(int mpad) { return mpad == 4 ? ScanGeom<4>::QT : ScanGeom<8>::QT; }
@@ -197,12 +226,7 @@ static int launch_hist_t(Index* h, int ntiles, const int* tile_list, int64_t str
                          const int64_t* tile_nsamp = nullptr) {
   using G = ScanGeom<MPAD>;
   const size_t smem = G::LUT_BYTES + (size_t)G::QT * 128 * 4;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_scan_hist<MPAD, kScanThreads>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  DPQ_TRY(set_smem(h, k_scan_hist<MPAD, kScanThreads>, smem));
   int chunks = (int)std::max<int64_t>(1, std::min<int64_t>((148 * 2 + ntiles - 1) / ntiles,
                                                           (nsamp + 511) / 512));
   int64_t per = (nsamp + chunks - 1) / chunks;
@@ -227,11 +251,12 @@ static int launch_hist(Index* h, int ntiles, const int* tile_list, int64_t strid
 }
 
 static int num_sms(Index* h) {
-  static int sms = 0;
-  if (!sms) {
+  if (!h->sms) {
+    int sms = 0;
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device) != cudaSuccess || sms < 1) sms = 148;
+    h->sms = sms;
   }
-  return sms;
+  return h->sms;
 }
 
 template <int MPAD>
@@ -239,12 +264,7 @@ static int launch_emit_t(Index* h, EmitArgs ea, int ntiles, int64_t rows) {
   using G = ScanGeom<MPAD>;
   constexpr int NW = kEmitThreads / 32;
   const size_t smem = emit_smem_bytes<MPAD, kEmitThreads>();
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_scan_emit<MPAD, kEmitThreads>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  DPQ_TRY(set_smem(h, k_scan_emit<MPAD, kEmitThreads>, smem));
   // Persistent CTAs (one per SM) pulling ~8 units each from a counter.
   const int sms = num_sms(h);
   ea.unit_counter = h->ws.counter;
@@ -252,6 +272,7 @@ static int launch_emit_t(Index* h, EmitArgs ea, int ntiles, int64_t rows) {
   ea.tile_fast = h->ws.tile_fast;
   ea.n_wide = h->d_nwide;
   ea.runs = h->rows_sorted ? 1 : 0;
+  ea.n_lut = h->d_nrows + 2;
   if (ea.unit_tile) {  // caller-built units (ivf lists)
     if (ea.n_units < 1) return DPQ_OK;
     DPQ_CUDA(cudaMemsetAsync(h->ws.counter, 0, sizeof(unsigned), h->stream));
@@ -293,31 +314,22 @@ static int launch_emit(Index* h, EmitArgs ea, int ntiles, int64_t rows) {
 
 template <int BUF, int MODE>
 static int launch_refine_buf(Index* h, const RefineArgs& ra, int nq) {
-  const size_t smem = (size_t)BUF * 16 + (size_t)ra.ystride * 4;
-  static int attr = 0;
-  auto set_attr = [&](auto kern) {
-    if ((int)smem > attr) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 49152));
-    }
+  // the query's residual block (ystride floats) is staged in shared memory
+  // when it fits next to the buffer; otherwise it is read from global/L2
+  // (ivf with a large ma * d)
+  const size_t buf_bytes = (size_t)BUF * 16;
+  RefineArgs rb = ra;
+  rb.y_in_smem = buf_bytes + (size_t)ra.ystride * 4 <= kRefineSmemMax ? 1 : 0;
+  const size_t smem = buf_bytes + (rb.y_in_smem ? (size_t)ra.ystride * 4 : 0);
+  auto go = [&](auto kern) -> int {
+    DPQ_TRY(set_smem(h, kern, smem));
+    kern<<<nq, kTopThreads, smem, h->stream>>>(rb);
+    return DPQ_OK;
   };
-  if (MODE != MODE_EMIT) {
-    auto kern = k_refine_topk<BUF, kTopThreads, MODE, 0>;
-    set_attr(kern);
-    kern<<<nq, kTopThreads, smem, h->stream>>>(ra);
-  } else if (ra.dsub == 32) {
-    auto kern = k_refine_topk<BUF, kTopThreads, MODE, 32>;
-    set_attr(kern);
-    kern<<<nq, kTopThreads, smem, h->stream>>>(ra);
-  } else if (ra.dsub == 120) {
-    auto kern = k_refine_topk<BUF, kTopThreads, MODE, 120>;
-    set_attr(kern);
-    kern<<<nq, kTopThreads, smem, h->stream>>>(ra);
-  } else {
-    auto kern = k_refine_topk<BUF, kTopThreads, MODE, 0>;
-    set_attr(kern);
-    kern<<<nq, kTopThreads, smem, h->stream>>>(ra);
-  }
-  if ((int)smem > attr) attr = (int)smem;
+  if (MODE != MODE_EMIT) DPQ_TRY(go(k_refine_topk<BUF, kTopThreads, MODE, 0>));
+  else if (ra.dsub == 32) DPQ_TRY(go(k_refine_topk<BUF, kTopThreads, MODE, 32>));
+  else if (ra.dsub == 120) DPQ_TRY(go(k_refine_topk<BUF, kTopThreads, MODE, 120>));
+  else DPQ_TRY(go(k_refine_topk<BUF, kTopThreads, MODE, 0>));
   DPQ_LAUNCHED(h);
   return DPQ_OK;
 }
@@ -358,11 +370,6 @@ int run_small_tables(Index* h, int nslot, const void* prefix, int64_t npre,
   ta.lut = w.lut; ta.mpad = h->mpad; ta.qt = qt_of(h->mpad);
   ta.cluster = (!pre_off && h->m >= 2) ? w.cluster : nullptr;  // flat: slot clustering keys
   const size_t smem = (size_t)(h->d + h->m * h->kbar) * 4 + (size_t)h->m * h->kbar + 16;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_small_tables, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
   ta.slot_list = slot_list;
   const int nlaunch = slot_list ? n_list : nslot;
   const char* ms_env = getenv("DPQ_MS_MIN");  // many-slot K1 from this slot count (default 256; test hook)
@@ -372,20 +379,18 @@ int run_small_tables(Index* h, int nslot, const void* prefix, int64_t npre,
   const int spc = spc_env ? atoi(spc_env) : (nlaunch >= 8192 ? 8 : 4);
   const bool many = nlaunch >= ms_min && (h->dsub & 7) == 0 && h->dsub <= 128;
   if (nlaunch > 0 && many) {  // IVF-size slot counts: spc slots per CTA
-    auto go = [&](auto kern, int S) {
-      static bool attr_ms[9] = {};
-      if (!attr_ms[S]) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr_ms[S] = true;
-      }
+    auto go = [&](auto kern, int S) -> int {
       const size_t smem_ms = (size_t)S * (h->d + h->m * h->kbar) * 4;
+      DPQ_TRY(set_smem(h, kern, smem_ms));
       kern<<<(nlaunch + S - 1) / S, 256, smem_ms, h->stream>>>(ta, nlaunch);
+      return DPQ_OK;
     };
-    if (spc == 2) go(k_small_tables_ms<2>, 2);
-    else if (spc == 4) go(k_small_tables_ms<4>, 4);
-    else go(k_small_tables_ms<8>, 8);
+    if (spc == 2) DPQ_TRY(go(k_small_tables_ms<2>, 2));
+    else if (spc == 4) DPQ_TRY(go(k_small_tables_ms<4>, 4));
+    else DPQ_TRY(go(k_small_tables_ms<8>, 8));
     DPQ_LAUNCHED(h);
   } else if (nlaunch > 0) {
+    DPQ_TRY(set_smem(h, k_small_tables, smem));
     k_small_tables<<<nlaunch, 256, smem, h->stream>>>(ta);
     DPQ_LAUNCHED(h);
   }
@@ -502,7 +507,10 @@ static int flat_first_pass(Index* h, int nb, int r2) {
     ea.unit_tile = nullptr; ea.unit_r0 = nullptr; ea.unit_r1 = nullptr;
     ea.emit_cnt = w.emit_cnt; ea.emit = w.emit; ea.cap = w.cap;
     DPQ_TRY(launch_emit(h, ea, tiles, n));
-    if (!sp.list) h->counters[2] += (int64_t)nb * n;  // (list mode: counted on the device)
+    if (!sp.list) {  // (list mode: counted on the device)
+      h->counters[2] += (int64_t)nb * n;
+      h->plane_rows += (int64_t)tiles * n;
+    }
     if (first) ev_rec(h, 3);
     k_threshold<256><<<nb, 256, 0, h->stream>>>(w.emit, w.emit_cnt, w.cap, w.guard_b, r2, nullptr,
                                                 w.bstar, w.ncand, w.flags, nullptr, h->d_nemit);
@@ -603,20 +611,18 @@ int run_group_tables(Index* h, int nq, int ystride) {
   const int gsize = h->k / h->kbar;
   const int ld = ((h->dsub & 7) == 0 && h->dsub <= 128) ? h->dsub + 4 : h->dsub + 1;  // k_group_tables rows
   const size_t smem = (size_t)gsize * ld * 4 + (size_t)nq * 4;
-  static size_t attr = 0;
   dim3 grid(h->kbar, h->m);
   if (h->dsub == 32) {
     const size_t sm2 = (size_t)32 * 32 * 4 + (size_t)nq * 4;
-    if (sm2 > 49152) cudaFuncSetAttribute(k_group_tables_reg<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+    DPQ_TRY(set_smem(h, k_group_tables_reg<32>, sm2));
 #ifndef DPQ_K5_SPLIT
 #define DPQ_K5_SPLIT 2  // CTAs per (group, subspace): the busiest groups bound K5 (A/B: 1 -> 2 saves ~10 us)
 #endif
     k_group_tables_reg<32><<<dim3(grid.x, grid.y, DPQ_K5_SPLIT), 256, sm2, h->stream>>>(ga);
   } else {
-    if (smem > attr) cudaFuncSetAttribute(k_group_tables<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 49152));
+    DPQ_TRY(set_smem(h, k_group_tables<0>, smem));
     k_group_tables<0><<<grid, 256, smem, h->stream>>>(ga);
   }
-  attr = std::max(attr, smem);
   DPQ_LAUNCHED(h);
   return DPQ_OK;
 }
@@ -933,6 +939,37 @@ __global__ void k_gather_rows(const uint8_t* codes, int row_bytes, int64_t n, co
   ids[i] = id_base + src;
 }
 
+// Unit seams: adc_low_batch (twopass.py:99-106) of every row for a batch of
+// queries, written in original row order (scores[q * n + original row]).
+__global__ void k_low_scores(const void* codes, int code_bytes, int64_t n, int m, int kbar, const uint8_t* q8,
+                             const int64_t* sorted_ids, int64_t id_base, uint8_t* scores) {
+  const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int q = blockIdx.y;
+  if (row >= n) return;
+  uint32_t acc = 0;
+  for (int j = 0; j < m; ++j)
+    acc += q8[((int64_t)q * m + j) * kbar + (code_at(codes, code_bytes, row * m + j) & (uint32_t)(kbar - 1))];
+  const int64_t orig = sorted_ids ? sorted_ids[row] - id_base : row;
+  scores[(int64_t)q * n + orig] = (uint8_t)min(acc, 255u);
+}
+
+// Emit entries of query q -> (score << 56 | id) for candidates (score <= b*,
+// i.e. the rows the refine walk takes, twopass.py:295-302), ~0 otherwise.
+__global__ void k_emit_keys(uint64_t* emit, const uint32_t* emit_cnt, uint32_t cap, const int32_t* bstar,
+                            const int64_t* sorted_ids, int64_t id_base) {
+  const int q = blockIdx.x;
+  const uint32_t n = min(emit_cnt[q], cap);
+  const int bs = bstar[q];
+  uint64_t* e = emit + (int64_t)q * cap;
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const uint64_t v = e[i];
+    const uint32_t sc = emit_score(v);
+    const int64_t row = emit_row(v);
+    const int64_t id = sorted_ids ? sorted_ids[row] : id_base + row;
+    e[i] = ((int)sc <= bs && sc < 255u) ? (((uint64_t)sc << 56) | (uint64_t)id) : ~0ull;
+  }
+}
+
 static int sort_rows(Index* h) {
   const int64_t n = h->n;
   uint32_t *k0 = nullptr, *k1 = nullptr;
@@ -1021,8 +1058,8 @@ int index_common_init(Index* h, int device, int m, int k, int kbar, int dsub, co
   DPQ_TRY(dmalloc(&h->d_nemit, 1));
   DPQ_TRY(dmalloc(&h->d_nent, 1));
   DPQ_TRY(dmalloc(&h->d_nwide, 1));
-  DPQ_TRY(dmalloc(&h->d_nrows, 1));
-  DPQ_CUDA(cudaMemset(h->d_nrows, 0, 8));
+  DPQ_TRY(dmalloc(&h->d_nrows, 4));  // query-rows, plane rows, LUT tile loads (scan), spare
+  DPQ_CUDA(cudaMemset(h->d_nrows, 0, 32));
   DPQ_CUDA(cudaMemset(h->d_nent, 0, 8));
   DPQ_CUDA(cudaMemset(h->d_nwide, 0, 8));
   DPQ_CUDA(cudaMemcpy(h->cb, codebooks, (size_t)m * k * dsub * 4, cudaMemcpyHostToDevice));
@@ -1063,7 +1100,7 @@ void index_free(Index* h) {
 extern "C" {
 
 const char* dpq_last_error(void) { return dpq::last_error(); }
-int dpq_abi_version(void) { return 1; }
+int dpq_abi_version(void) { return 2; }
 int dpq_all_finite(const float* x, int64_t n) {
   if (!x || n <= 0) return 0;
   const uint32_t* b = reinterpret_cast<const uint32_t*>(x);
@@ -1292,15 +1329,106 @@ int dpq_debug_full_tables(dpq_index_t* index, const float* yr, int64_t nq, float
 }
 
 int dpq_debug_low_scores(dpq_index_t* index, const float* yr, int64_t nq, int r2, uint8_t* scores) {
-  (void)index; (void)yr; (void)nq; (void)r2; (void)scores;
-  set_error("dpq_debug_low_scores: use dpq_debug_quantize_tables + host gather");
-  return DPQ_ERR_STATE;
+  Index* h = reinterpret_cast<Index*>(index);
+  DPQ_TRY(check_search(h, nq, 1, r2, true));
+  if (h->kind != KIND_FLAT) { set_error("not a flat index"); return DPQ_ERR_STATE; }
+  if (nq > 0 && !scores) { set_error("null scores"); return DPQ_ERR_ARG; }
+  const int bq = (int)std::max<int64_t>(1, std::min<int64_t>(h->batch, ((int64_t)1 << 30) / std::max<int64_t>(1, h->n)));
+  uint8_t* d_scores = nullptr;
+  DPQ_TRY(dmalloc(&d_scores, (size_t)bq * std::max<int64_t>(1, h->n)));
+  int rc = DPQ_OK;
+  for (int64_t q0 = 0; q0 < nq && rc == DPQ_OK; q0 += bq) {
+    const int nb = (int)std::min<int64_t>(bq, nq - q0);
+    if ((rc = ensure_ws(h, nb, 1, h->d, -1)) != DPQ_OK) break;
+    Workspace& w = h->ws;
+    if (cudaMemcpyAsync(w.y, yr + q0 * h->d, (size_t)nb * h->d * 4, cudaMemcpyHostToDevice, h->stream) != cudaSuccess) {
+      rc = DPQ_ERR_CUDA; set_error("query upload failed"); break;
+    }
+    if ((rc = run_small_tables(h, nb, h->prefix, std::min<int64_t>(r2, h->n_prefix), nullptr, nullptr, nullptr,
+                               false, nullptr, nullptr, 0, false)) != DPQ_OK) break;
+    if (h->n > 0) {
+      k_low_scores<<<dim3((unsigned)((h->n + 255) / 256), (unsigned)nb), 256, 0, h->stream>>>(
+          h->codes, h->code_bytes, h->n, h->m, h->kbar, w.q8, h->rows_sorted ? h->sorted_ids : nullptr, h->id_base,
+          d_scores);
+      if (cudaGetLastError() != cudaSuccess) { rc = DPQ_ERR_CUDA; set_error("k_low_scores launch failed"); break; }
+      h->counters[0]++;
+      if (cudaMemcpyAsync(scores + q0 * h->n, d_scores, (size_t)nb * h->n, cudaMemcpyDeviceToHost, h->stream) !=
+              cudaSuccess ||
+          cudaStreamSynchronize(h->stream) != cudaSuccess) {
+        rc = DPQ_ERR_CUDA; set_error("low scores download failed"); break;
+      }
+    }
+  }
+  cudaFree(d_scores);
+  return rc;
+}
+
+int dpq_debug_candidate_ids(dpq_index_t* index, const float* yr, int64_t nq, int r2, int64_t cap, int64_t* ids,
+                            uint8_t* scores, int64_t* counts) {
+  Index* h = reinterpret_cast<Index*>(index);
+  DPQ_TRY(check_search(h, nq, 1, r2, true));
+  if (h->kind != KIND_FLAT) { set_error("not a flat index"); return DPQ_ERR_STATE; }
+  if (cap < 0 || (nq > 0 && (!counts || (cap > 0 && !ids)))) { set_error("bad candidate buffers"); return DPQ_ERR_ARG; }
+  std::vector<uint64_t> keys;
+  std::vector<uint32_t> cnt;
+  std::vector<int32_t> bs;
+  for (int64_t q0 = 0; q0 < nq; q0 += h->batch) {
+    const int nb = (int)std::min<int64_t>(h->batch, nq - q0);
+    DPQ_TRY(ensure_ws(h, nb, 1, h->d, -1));
+    Workspace& w = h->ws;
+    DPQ_CUDA(cudaMemcpyAsync(w.y, yr + q0 * h->d, (size_t)nb * h->d * 4, cudaMemcpyHostToDevice, h->stream));
+    DPQ_TRY(run_small_tables(h, nb, h->prefix, std::min<int64_t>(r2, h->n_prefix), nullptr, nullptr, nullptr,
+                             false, nullptr));
+    const bool ns = h->no_spec;
+    h->no_spec = true;  // exact b* needed right here
+    int rc = flat_first_pass(h, nb, r2);
+    h->no_spec = ns;
+    if (rc == 100) { set_error("debug_candidate_ids: emit budget exceeded, use a smaller batch"); return DPQ_ERR_NOMEM; }
+    if (rc != DPQ_OK) return rc;
+    // emit entries -> (score << 56 | id) in place, ~0 for non-candidates
+    k_emit_keys<<<nb, 256, 0, h->stream>>>(w.emit, w.emit_cnt, w.cap, w.bstar, h->rows_sorted ? h->sorted_ids : nullptr,
+                                           h->id_base);
+    DPQ_LAUNCHED(h);
+    cnt.resize(nb);
+    bs.resize(nb);
+    DPQ_CUDA(cudaMemcpyAsync(cnt.data(), w.emit_cnt, (size_t)nb * 4, cudaMemcpyDeviceToHost, h->stream));
+    DPQ_CUDA(cudaMemcpyAsync(bs.data(), w.bstar, (size_t)nb * 4, cudaMemcpyDeviceToHost, h->stream));
+    DPQ_CUDA(cudaStreamSynchronize(h->stream));
+    for (int q = 0; q < nb; ++q) {
+      const uint32_t c = std::min(cnt[q], w.cap);
+      keys.resize(c);
+      if (c) DPQ_CUDA(cudaMemcpy(keys.data(), w.emit + (int64_t)q * w.cap, (size_t)c * 8, cudaMemcpyDeviceToHost));
+      keys.erase(std::remove(keys.begin(), keys.end(), ~0ull), keys.end());
+      std::sort(keys.begin(), keys.end());  // (score, id): the bucket walk order
+      const int64_t gq = q0 + q;
+      counts[gq] = (int64_t)keys.size();
+      const int64_t nw = std::min<int64_t>(cap, (int64_t)keys.size());
+      for (int64_t i = 0; i < nw; ++i) {
+        ids[gq * cap + i] = (int64_t)(keys[i] & kRowMask);
+        if (scores) scores[gq * cap + i] = (uint8_t)(keys[i] >> 56);
+      }
+    }
+  }
+  return DPQ_OK;
 }
 
 int dpq_last_phase_ms(dpq_index_t* index, float* ms7) {
   Index* h = reinterpret_cast<Index*>(index);
   if (!h || !ms7) { set_error("null argument"); return DPQ_ERR_ARG; }
   for (int i = 0; i < PH_N; ++i) ms7[i] = h->phase_ms[i];
+  return DPQ_OK;
+}
+
+int dpq_counters_ex(dpq_index_t* index, int64_t* out, int n) {
+  Index* h = reinterpret_cast<Index*>(index);
+  if (!h || !out || n < 0) { set_error("null argument"); return DPQ_ERR_ARG; }
+  int64_t base[8];
+  DPQ_TRY(dpq_counters(index, base));
+  unsigned long long dv[4] = {};
+  DPQ_CUDA(cudaMemcpy(dv, h->d_nrows, sizeof(dv), cudaMemcpyDeviceToHost));
+  const int64_t all[kCountersEx] = {base[0], base[1], base[2], base[3], base[4], base[5], base[6], base[7],
+                                    (int64_t)dv[1] + h->plane_rows, (int64_t)dv[2]};
+  for (int i = 0; i < n; ++i) out[i] = i < kCountersEx ? all[i] : 0;
   return DPQ_OK;
 }
 

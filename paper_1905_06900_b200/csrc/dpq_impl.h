@@ -13,6 +13,8 @@ void set_error(const std::string& msg);
 enum Kind { KIND_FLAT = 0, KIND_IVF = 1 };
 
 // Phase slots of dpq_last_phase_ms.
+constexpr int kCountersEx = 10;  // dpq_counters_ex
+
 enum Phase { PH_TABLES = 0, PH_GUARD, PH_SCAN, PH_THRESH, PH_REFINE, PH_FALLBACK, PH_TOTAL, PH_N };
 
 // Per-batch device workspace, grown on demand.
@@ -108,7 +110,8 @@ struct Index {
   unsigned long long* d_nemit = nullptr;
   unsigned long long* d_nent = nullptr;   // lazily computed table entries
   unsigned long long* d_nwide = nullptr;  // scan units run by the wide loop
-  unsigned long long* d_nrows = nullptr;  // query-rows scanned in run-filtered (list) mode
+  unsigned long long* d_nrows = nullptr;  // [4]: query-rows (list mode), plane rows (list mode), LUT loads, spare
+  int64_t plane_rows = 0;                 // plane rows read by the scan (non-list mode, host-counted)
   size_t emit_budget = (size_t)16 << 30;  // bytes for emit buffers
   // guard sampling (env DPQ_GUARD_SAMPLE / DPQ_EXACT_LIMIT / DPQ_EMIT_CAP
   // override them so tests can force the exact-redo and overflow paths)
@@ -124,6 +127,7 @@ struct Index {
   int use_graph = 1;     // replay speculative batches as a CUDA graph (env DPQ_GRAPH=0 disables)
   BatchGraph graph;
   int spec_nb = 0;       // flags of a speculative first pass still to check
+  int sms = 0;           // SM count of the device (cached)
   int direct_copy = 0;  // host API: copy straight from/to the caller's (pageable) buffers (env DPQ_DIRECT_COPY)
   int run_filter = 1;  // flat sorted rows: scan only chunks whose keys can reach a guard (env DPQ_RUN_FILTER=0)
   uint32_t* chunk_keys = nullptr;  // [n_chunks] first | last key << 16 of each 128-row chunk

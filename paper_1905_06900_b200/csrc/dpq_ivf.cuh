@@ -209,6 +209,7 @@ struct IvfConvArgs {
   const void* codes; int code_bytes; int m, k, dsub;
   const float* cb; const float* ynat; const int64_t* sorted_ids;
   int r; double* out_d; int64_t* out_i;
+  int y_in_smem = 1;  // residual block staged in shared memory (else read from global)
 };
 
 template <int BUF, int NT>
@@ -216,13 +217,15 @@ __global__ void __launch_bounds__(NT) k_ivf_conventional(IvfConvArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   uint64_t* keys = reinterpret_cast<uint64_t*>(smem);
   int64_t* ids = reinterpret_cast<int64_t*>(keys + BUF);
-  float* ys = reinterpret_cast<float*>(ids + BUF);
+  float* ys_s = reinterpret_cast<float*>(ids + BUF);
   __shared__ int fill;
   __shared__ uint64_t thr_k;
   __shared__ int64_t thr_i;
   const int q = blockIdx.x;
   const int d = a.m * a.dsub;
-  for (int i = threadIdx.x; i < a.ma * d; i += NT) ys[i] = a.ynat[(int64_t)q * a.ma * d + i];
+  const float* ys = a.y_in_smem ? ys_s : a.ynat + (int64_t)q * a.ma * d;
+  if (a.y_in_smem)
+    for (int i = threadIdx.x; i < a.ma * d; i += NT) ys_s[i] = a.ynat[(int64_t)q * a.ma * d + i];
   if (threadIdx.x == 0) { fill = 0; thr_k = ~0ull; thr_i = INT64_MAX; }
   __syncthreads();
   for (int p = 0; p < a.ma; ++p) {
@@ -404,26 +407,23 @@ static int ivf_probe_dev(Index* h, int nb, int ma) {
     k_probe_dist<<<grid, kProbeCT, 0, h->stream>>>(h->ws.y, h->d, nb, h->centers, h->n_cells, b.d2);
     DPQ_LAUNCHED(h);
     const size_t smem = (size_t)1024 * 8 * 16;  // 8192 (key, id) pairs
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_probe_select<1024, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr = true;
-    }
+    DPQ_TRY(set_smem(h, k_probe_select<1024, 8>, smem));
     k_probe_select<1024, 8><<<nb, 1024, smem, h->stream>>>(b.d2, h->n_cells, ma, b.cells);
     DPQ_LAUNCHED(h);
     return DPQ_OK;
   }
   const int need = ma + 256;
   const size_t ys = (size_t)h->d * 4;
-  auto go = [&](auto kern, int BUF) {
+  auto go = [&](auto kern, int BUF) -> int {
     const size_t smem = (size_t)BUF * 16 + ys;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 49152));
+    DPQ_TRY(set_smem(h, kern, smem));
     kern<<<nb, 256, smem, h->stream>>>(h->ws.y, h->d, h->centers, h->n_cells, ma, b.cells);
+    return DPQ_OK;
   };
-  if (need <= 1024) go(k_probe<1024, 256>, 1024);
-  else if (need <= 2048) go(k_probe<2048, 256>, 2048);
-  else if (need <= 4096) go(k_probe<4096, 256>, 4096);
-  else if (need <= 8192) go(k_probe<8192, 256>, 8192);
+  if (need <= 1024) DPQ_TRY(go(k_probe<1024, 256>, 1024));
+  else if (need <= 2048) DPQ_TRY(go(k_probe<2048, 256>, 2048));
+  else if (need <= 4096) DPQ_TRY(go(k_probe<4096, 256>, 4096));
+  else if (need <= 8192) DPQ_TRY(go(k_probe<8192, 256>, 8192));
   else { set_error("ma too large for the device probe (<= 7936)"); return DPQ_ERR_ARG; }
   DPQ_LAUNCHED(h);
   return DPQ_OK;
@@ -607,16 +607,19 @@ static int ivf_batch(Index* h, int nb, int r, int ma, int r2, bool derived, cons
     a.cb = h->cb; a.ynat = B.ynat; a.sorted_ids = h->sorted_ids;
     a.r = r; a.out_d = w.out_d; a.out_i = w.out_i;
     const size_t ysm = (size_t)ma * d * 4;
-    auto go = [&](auto kern, int BUF) {
-      const size_t smem = (size_t)BUF * 16 + ysm;
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 49152));
+    auto go = [&](auto kern, int BUF) -> int {
+      // residuals staged in shared memory when they fit, else read from global
+      a.y_in_smem = (size_t)BUF * 16 + ysm <= kRefineSmemMax ? 1 : 0;
+      const size_t smem = (size_t)BUF * 16 + (a.y_in_smem ? ysm : 0);
+      DPQ_TRY(set_smem(h, kern, smem));
       kern<<<nb, 256, smem, h->stream>>>(a);
+      return DPQ_OK;
     };
     const int need = r + 256;
-    if (need <= 1024) go(k_ivf_conventional<1024, 256>, 1024);
-    else if (need <= 2048) go(k_ivf_conventional<2048, 256>, 2048);
-    else if (need <= 4096) go(k_ivf_conventional<4096, 256>, 4096);
-    else if (need <= 8192) go(k_ivf_conventional<8192, 256>, 8192);
+    if (need <= 1024) DPQ_TRY(go(k_ivf_conventional<1024, 256>, 1024));
+    else if (need <= 2048) DPQ_TRY(go(k_ivf_conventional<2048, 256>, 2048));
+    else if (need <= 4096) DPQ_TRY(go(k_ivf_conventional<4096, 256>, 4096));
+    else if (need <= 8192) DPQ_TRY(go(k_ivf_conventional<8192, 256>, 8192));
     else { set_error("r exceeds the device top-r limit (7936)"); return DPQ_ERR_ARG; }
     DPQ_LAUNCHED(h);
     ev_rec(h, 6);
@@ -1047,6 +1050,133 @@ int dpq_shard_finish(dpq_index_t* index, const int32_t* cand_hist_sum, int r, in
   memcpy(ids, w.h_i, (size_t)nb * r * 8);
   for (int q = 0; q < nb; ++q) need_exact[q] = need_exact[q] == 1;
   h->counters[1] += nb;
+  return DPQ_OK;
+}
+
+
+// ---------------------------------------------------------------------------
+// Device-resident shard protocol: the same three phases on device buffers,
+// enqueued on the index stream with no host synchronisation, so the caller
+// runs the histogram all-reduces (NCCL) in place on the same stream.  Guard
+// too tight / emit overflow are flagged per query (flags: 1 / 2) instead of
+// being handled synchronously; the caller all-reduces the flags (max) and
+// redoes a flagged batch through the host-staged protocol above.
+// ---------------------------------------------------------------------------
+int dpq_shard_begin_dev(dpq_index_t* index, const float* yr, int64_t nq, int r2, int64_t n_global, int exact,
+                        int32_t* sample_hist, int64_t* n_sampled) {
+  Index* h = reinterpret_cast<Index*>(index);
+  if (!h || h->kind != KIND_FLAT) { set_error("not a flat index"); return DPQ_ERR_STATE; }
+  if (nq < 1 || nq > (1 << 20) || r2 < 1 || !yr || !sample_hist || !n_sampled) {
+    set_error("bad shard_begin_dev arguments"); return DPQ_ERR_ARG;
+  }
+  const int64_t npre = std::min<int64_t>(r2, n_global);
+  if (h->n_prefix < npre) {
+    set_error("shard prefix holds " + std::to_string(h->n_prefix) + " rows, need min(r2, N) = " +
+              std::to_string(npre));
+    return DPQ_ERR_ARG;
+  }
+  cudaSetDevice(h->device);
+  const int nb = (int)nq;
+  DPQ_TRY(ensure_ws(h, nb, 1, h->d, -1));
+  Workspace& w = h->ws;
+  const int qt = qt_of(h->mpad);
+  const int tiles = tiles_of(nb, h->mpad);
+  DPQ_CUDA(cudaMemcpyAsync(w.y, yr, (size_t)nb * h->d * 4, cudaMemcpyDeviceToDevice, h->stream));
+  DPQ_TRY(run_small_tables(h, nb, h->prefix, npre, nullptr, nullptr, nullptr, false, nullptr));
+  DPQ_CUDA(cudaMemsetAsync(w.gword, 0x7F, (size_t)tiles * qt * 2, h->stream));
+  DPQ_CUDA(cudaMemsetAsync(w.hist, 0, (size_t)tiles * qt * 256 * 4, h->stream));
+  const bool ex = exact || n_global <= h->exact_limit;
+  const int64_t ns = h->n == 0 ? 0 : (ex ? h->n : std::min<int64_t>(h->n, h->sample));
+  const int64_t stride = ns ? h->n / ns : 1;
+  if (ns > 0) DPQ_TRY(launch_hist(h, tiles, nullptr, stride, ns, h->plane));
+  DPQ_CUDA(cudaMemcpyAsync(sample_hist, w.hist, (size_t)nb * 256 * 4, cudaMemcpyDeviceToDevice, h->stream));
+  *n_sampled = ns;
+  h->shard_nq = nb;
+  return DPQ_OK;
+}
+
+int dpq_shard_scan_dev(dpq_index_t* index, const int32_t* sample_hist_sum, int64_t n_global, int64_t sample_global,
+                       int r2, int exact, int32_t* cand_hist) {
+  Index* h = reinterpret_cast<Index*>(index);
+  if (!h || h->kind != KIND_FLAT || h->shard_nq < 1) { set_error("shard_begin first"); return DPQ_ERR_STATE; }
+  if (!sample_hist_sum || !cand_hist) { set_error("null histogram"); return DPQ_ERR_ARG; }
+  cudaSetDevice(h->device);
+  const int nb = h->shard_nq;
+  Workspace& w = h->ws;
+  const int tiles = tiles_of(nb, h->mpad);
+  DPQ_CUDA(cudaMemcpyAsync(w.hist, sample_hist_sum, (size_t)nb * 256 * 4, cudaMemcpyDeviceToDevice, h->stream));
+  const bool ex = exact || n_global <= h->exact_limit;
+  const double lambda = (double)r2 * (double)sample_global / (double)std::max<int64_t>(n_global, 1);
+  k_guard<<<(nb + 127) / 128, 128, 0, h->stream>>>(w.hist, nb, r2, lambda, ex ? 1 : 0, nullptr, w.guard_b, w.gword,
+                                                    nullptr);
+  DPQ_LAUNCHED(h);
+  ScanPlan sp;
+  DPQ_TRY(plan_flat_scan(h, nb, sp));
+  DPQ_TRY(prepare_flat_scan(h, nb, sp));
+  DPQ_CUDA(cudaMemsetAsync(w.emit_cnt, 0, (size_t)nb * 4, h->stream));
+  if (h->n > 0) {
+    EmitArgs ea;
+    ea.plane = h->plane; ea.row_begin = 0; ea.row_end = h->n; ea.rows_per_cta = 0;
+    ea.lut = w.lut; ea.tile_list = nullptr; ea.slot_probe = nullptr;
+    plan_emit_args(h, sp, ea);
+    ea.unit_tile = nullptr; ea.unit_r0 = nullptr; ea.unit_r1 = nullptr;
+    ea.emit_cnt = w.emit_cnt; ea.emit = w.emit; ea.cap = w.cap;
+    DPQ_TRY(launch_emit(h, ea, tiles, h->n));
+    if (!sp.list) h->counters[2] += (int64_t)nb * h->n;
+  }
+  k_threshold<256><<<nb, 256, 0, h->stream>>>(w.emit, w.emit_cnt, w.cap, w.guard_b, r2, nullptr, w.bstar, w.ncand,
+                                              w.flags, cand_hist, h->d_nemit);
+  DPQ_LAUNCHED(h);
+  return DPQ_OK;
+}
+
+int dpq_shard_finish_dev(dpq_index_t* index, const int32_t* cand_hist_sum, int r, int r2, double* dists,
+                         int64_t* ids, uint8_t* flags) {
+  Index* h = reinterpret_cast<Index*>(index);
+  if (!h || h->kind != KIND_FLAT || h->shard_nq < 1) { set_error("shard_begin first"); return DPQ_ERR_STATE; }
+  if (r < 1 || r > r2) { set_error("need 1 <= r <= r2"); return DPQ_ERR_ARG; }
+  if (!cand_hist_sum || !dists || !ids || !flags) { set_error("null argument"); return DPQ_ERR_ARG; }
+  cudaSetDevice(h->device);
+  const int nb = h->shard_nq;
+  DPQ_TRY(ensure_ws(h, nb, r, h->d, -1));
+  Workspace& w = h->ws;
+  k_bstar_from_hist<<<(nb + 127) / 128, 128, 0, h->stream>>>(cand_hist_sum, w.guard_b, nb, r2, w.bstar, w.ncand,
+                                                              w.flags);
+  DPQ_LAUNCHED(h);
+  RefineArgs ra = make_refine_args(h, r);
+  ra.out_d = dists;
+  ra.out_i = ids;
+  if (group_tables_fit(h, nb)) {
+    DPQ_TRY(run_group_tables(h, nb, h->d));
+    ra.tables = w.tables;
+    DPQ_TRY(launch_refine<MODE_EMIT_TABLE>(h, ra, nb));
+  } else {
+    DPQ_TRY(launch_refine<MODE_EMIT>(h, ra, nb));
+  }
+  DPQ_CUDA(cudaMemcpyAsync(flags, w.flags, nb, cudaMemcpyDeviceToDevice, h->stream));
+  h->counters[1] += nb;
+  return DPQ_OK;
+}
+
+int dpq_merge_topr_dev(dpq_index_t* index, const double* part_dists, const int64_t* part_ids, int n_parts,
+                       int64_t nq, int r, double* dists, int64_t* ids) {
+  Index* h = reinterpret_cast<Index*>(index);
+  if (!h) { set_error("null index"); return DPQ_ERR_ARG; }
+  if (n_parts < 1 || nq < 0 || nq > INT32_MAX || r < 1 || (nq > 0 && (!part_dists || !part_ids || !dists || !ids))) {
+    set_error("bad merge arguments"); return DPQ_ERR_ARG;
+  }
+  if (nq == 0) return DPQ_OK;
+  cudaSetDevice(h->device);
+  k_merge_topr<<<(unsigned)nq, 256, 0, h->stream>>>(part_dists, part_ids, n_parts, (int)nq, r, dists, ids);
+  DPQ_LAUNCHED(h);
+  return DPQ_OK;
+}
+
+int dpq_sync(dpq_index_t* index) {
+  Index* h = reinterpret_cast<Index*>(index);
+  if (!h) { set_error("null index"); return DPQ_ERR_ARG; }
+  cudaSetDevice(h->device);
+  DPQ_CUDA(cudaStreamSynchronize(h->stream));
   return DPQ_OK;
 }
 

@@ -557,10 +557,13 @@ __global__ void __launch_bounds__(256) k_chunk_list(const uint32_t* __restrict__
   const uint32_t bal = __ballot_sync(0xffffffffu, f);
   int base = 0;
   if (lane == 0 && bal) base = atomicAdd(list_len + tile, __popc(bal));
-  if (n_rows) {  // query-rows this tile will scan (its real queries x listed rows), one atomic per warp
+  if (n_rows) {  // query-rows this tile will scan (its real queries x listed rows) and the listed plane rows
     const unsigned rows = f ? (unsigned)min((int64_t)128, n - (int64_t)c * 128) : 0u;
     const unsigned wr = __reduce_add_sync(0xffffffffu, rows);
-    if (lane == 0 && wr) atomicAdd(n_rows, (unsigned long long)wr * (unsigned long long)min(qt, nb - tile * qt));
+    if (lane == 0 && wr) {
+      atomicAdd(n_rows, (unsigned long long)wr * (unsigned long long)min(qt, nb - tile * qt));
+      atomicAdd(n_rows + 1, (unsigned long long)wr);
+    }
   }
   base = __shfl_sync(0xffffffffu, base, 0);
   if (f) list[(int64_t)tile * nchunks + base + __popc(bal & ((1u << lane) - 1u))] = c;
@@ -783,6 +786,7 @@ struct EmitArgs {
   int64_t list_stride = 0;
   int n_units;                  // tiles * units_per_tile
   int units_per_tile;
+  unsigned long long* n_lut = nullptr;  // optional: LUT tile loads (bulk copies of G::LUT_BYTES)
 };
 
 // Persistent scan.  Work unit = (query tile, contiguous row range); CTAs
@@ -894,6 +898,7 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
       // every warp is past the previous unit (barrier above): one thread
       // moves the 128-KB tile with a TMA bulk copy, all wait on the mbarrier
       if (threadIdx.x == 0) {
+        if (a.n_lut) atomicAdd(a.n_lut, 1ull);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(&lut_bar, G::LUT_BYTES);
         bulk_g2s(slut, a.lut + (int64_t)tile * G::LUT_BYTES, G::LUT_BYTES, &lut_bar);
@@ -1316,6 +1321,8 @@ __global__ void __launch_bounds__(NT)
   const uint32_t n = emit_cnt[q];
   if (n > cap) {
     if (threadIdx.x == 0) { flags[q] = 2; bstar[q] = -1; }  // (-1: refine nothing until redone)
+    if (hist_out)  // sharded: this shard's histogram is unknown, export zeros (the query is redone)
+      for (int i = threadIdx.x; i < 256; i += NT) hist_out[(int64_t)q * 256 + i] = 0;
     return;
   }
   for (int i = threadIdx.x; i < 256; i += NT) h[i] = 0;
@@ -1362,9 +1369,55 @@ __global__ void k_bstar_from_hist(const int32_t* __restrict__ hist, const uint16
     cum += h[b];
     if (cum >= r2) { bs = b; break; }
   }
-  if (bs >= 0) { bstar[q] = bs; ncand[q] = cum; flags[q] = 0; }
-  else if (B >= 254) { bstar[q] = 254; ncand[q] = cum; flags[q] = 0; }
-  else { flags[q] = 1; }
+  const bool over = flags[q] == 2;  // this shard's emit list overflowed in the scan: keep the flag
+  if (bs >= 0) { bstar[q] = over ? -1 : bs; ncand[q] = cum; flags[q] = over ? 2 : 0; }
+  else if (B >= 254) { bstar[q] = over ? -1 : 254; ncand[q] = cum; flags[q] = over ? 2 : 0; }
+  else { flags[q] = 1; bstar[q] = -1; }
+}
+
+// Exact top-r of the union of n_parts per-shard top-r lists (each sorted
+// by (dist, id), padded with (+inf, -1)), i.e. ResultSet.from_arrays over the
+// concatenation (search.py:115-124) / shard.merge_topr: the rank of element
+// (g, p) in the union is p plus, for every other list, the number of its
+// elements ordered before it (binary search), with padding last and ties
+// between paddings broken by (list, position).  Elements of rank < r are
+// written; one CTA per query, no shared-memory limit on n_parts * r.
+__device__ __forceinline__ bool merge_before(double da, int64_t ia, int ga, int pa, double db, int64_t ib, int gb,
+                                             int pb) {
+  const int64_t ka = ia < 0 ? INT64_MAX : ia, kb = ib < 0 ? INT64_MAX : ib;
+  if (da != db) return da < db;
+  if (ka != kb) return ka < kb;
+  if (ga != gb) return ga < gb;
+  return pa < pb;
+}
+
+__global__ void __launch_bounds__(256) k_merge_topr(const double* __restrict__ pd, const int64_t* __restrict__ pi,
+                                                    int n_parts, int nq, int r, double* __restrict__ out_d,
+                                                    int64_t* __restrict__ out_i) {
+  const int q = blockIdx.x;
+  const int64_t stride = (int64_t)nq * r;  // parts are (n_parts, nq, r)
+  for (int e = threadIdx.x; e < n_parts * r; e += blockDim.x) {
+    const int g = e / r, p = e % r;
+    const double d = pd[g * stride + (int64_t)q * r + p];
+    const int64_t id = pi[g * stride + (int64_t)q * r + p];
+    int rank = p;
+    for (int h = 0; h < n_parts && rank < r; ++h) {
+      if (h == g) continue;
+      const double* hd = pd + h * stride + (int64_t)q * r;
+      const int64_t* hi = pi + h * stride + (int64_t)q * r;
+      int lo = 0, up = r;  // first position of list h not before (d, id, g, p)
+      while (lo < up) {
+        const int mid = (lo + up) >> 1;
+        if (merge_before(hd[mid], hi[mid], h, mid, d, id, g, p)) lo = mid + 1;
+        else up = mid;
+      }
+      rank += lo;
+    }
+    if (rank < r) {
+      out_d[(int64_t)q * r + rank] = id < 0 ? INFINITY : d;
+      out_i[(int64_t)q * r + rank] = id;
+    }
+  }
 }
 
 // ============================================================================
@@ -1547,7 +1600,11 @@ struct RefineArgs {
   double* out_d; int64_t* out_i;
   unsigned long long* n_refined;
   const int* order = nullptr;  // optional CTA -> query (heaviest emit lists first)
+  int y_in_smem = 1;           // stage the query's y block in shared memory (else read it from global)
 };
+
+// Dynamic shared-memory budget of one refine CTA (buffer + staged y block).
+constexpr size_t kRefineSmemMax = 220 * 1024;
 
 // Query order for the refine launch: descending emitted count (coarse
 // counting sort, one CTA), so the longest lists start first and the short
@@ -1719,13 +1776,17 @@ __global__ void __launch_bounds__(NT, DPQ_REFINE_MINB) k_refine_topk(RefineArgs 
   extern __shared__ __align__(16) uint8_t smem[];
   uint64_t* keys = reinterpret_cast<uint64_t*>(smem);
   int64_t* ids = reinterpret_cast<int64_t*>(keys + BUF);
-  float* ys = reinterpret_cast<float*>(ids + BUF);
+  float* ys_s = reinterpret_cast<float*>(ids + BUF);
   __shared__ int cnt3[3];  // insert counters, round r uses cnt3[r % 3] (one barrier per round)
   __shared__ uint64_t thr_k;
   __shared__ int64_t thr_i;
   __shared__ unsigned nref;
   const int q = a.order ? a.order[blockIdx.x] : blockIdx.x;
-  for (int i = threadIdx.x; i < a.ystride; i += NT) ys[i] = a.y[(int64_t)q * a.ystride + i];
+  // query / per-probe residual block: staged in shared memory when it fits
+  // (launch_refine_buf), else read through L1/L2 (ivf with a large ma * d)
+  const float* ys = a.y_in_smem ? ys_s : a.y + (int64_t)q * a.ystride;
+  if (a.y_in_smem)
+    for (int i = threadIdx.x; i < a.ystride; i += NT) ys_s[i] = a.y[(int64_t)q * a.ystride + i];
   if (threadIdx.x == 0) { cnt3[0] = cnt3[1] = cnt3[2] = 0; thr_k = ~0ull; thr_i = INT64_MAX; nref = 0; }
   __syncthreads();
   const int d = a.m * a.dsub;

@@ -194,6 +194,33 @@ class FlatIndex(BaseEstimator):
                                                    _lib.ptr(bstar), _lib.ptr(ncand)))
         return bstar, ncand
 
+    def low_scores(self, Y, r2: int):
+        """adc_low_batch(codes_, quantize_tables(...)) per query
+        (twopass.py:63-106): (nq, n) uint8 first-pass scores."""
+        Y = check_array(Y, dtype=np.float32, order="C")
+        yr = rotated_queries(self.quantizer, Y)
+        out = np.empty((yr.shape[0], self.codes_.shape[0]), np.uint8)
+        _lib.check(_lib.lib().dpq_debug_low_scores(self._handle().raw, _lib.ptr(yr), yr.shape[0], int(r2),
+                                                   _lib.ptr(out)))
+        return out
+
+    def candidate_ids(self, Y, r2: int):
+        """Per query, the ids refine scores, in the bucket-walk order of
+        scan_derived + refine (twopass.py:187-217, 295-302): a list of
+        (ids int64, scores uint8) pairs."""
+        Y = check_array(Y, dtype=np.float32, order="C")
+        yr = rotated_queries(self.quantizer, Y)
+        nq = yr.shape[0]
+        L, raw = _lib.lib(), self._handle().raw
+        counts = np.zeros(nq, np.int64)
+        _lib.check(L.dpq_debug_candidate_ids(raw, _lib.ptr(yr), nq, int(r2), 0, None, None, _lib.ptr(counts)))
+        cap = int(counts.max(initial=0))
+        ids = np.empty((nq, max(cap, 1)), np.int64)
+        sc = np.empty((nq, max(cap, 1)), np.uint8)
+        _lib.check(L.dpq_debug_candidate_ids(raw, _lib.ptr(yr), nq, int(r2), cap, _lib.ptr(ids), _lib.ptr(sc),
+                                             _lib.ptr(counts)))
+        return [(ids[q, :counts[q]].copy(), sc[q, :counts[q]].copy()) for q in range(nq)]
+
     def full_tables(self, Y):
         """compute_tables(yr, codebooks_) per query: (nq, m, k) f32."""
         Y = check_array(Y, dtype=np.float32, order="C")

@@ -14,9 +14,21 @@ histograms, so the union of the shards' candidates is exactly the unsharded
 candidate set {score <= b*} (twopass.py:171-201, 295-302) and the merged
 top-r by (dist, id) equals the unsharded result bit for bit.
 
-The orchestration (`sharded_search`) is engine- and transport-agnostic:
-`GpuShardEngine` drives libdpq; `TorchComm` moves the small arrays with
-torch.distributed (NCCL on GPUs, gloo for the CPU tests of this protocol).
+Two drivers of the same protocol:
+
+* `sharded_search_dev` (the fast path): queries, histograms, flags and
+  results stay in device memory; the phases only enqueue work on the shard's
+  stream and the collectives run in place on that stream (NCCL), the merge
+  is a device kernel (dpq_merge_topr_dev).  The only host synchronisation is
+  reading the all-reduced flag byte at the end of the batch; a batch whose
+  guard proved too tight or whose emit list overflowed on some shard is
+  redone through the host driver.
+* `sharded_search`: the host-buffer driver (numpy in and out between the
+  phases), used for those rare redos and by the CPU protocol tests.
+
+Both are engine- and transport-agnostic: `GpuShardEngine` drives libdpq;
+`TorchComm` moves arrays/tensors with torch.distributed (NCCL on GPUs, gloo
+for the CPU tests of this protocol).
 """
 
 from __future__ import annotations
@@ -30,15 +42,25 @@ from .flat import rotated_queries
 class GpuShardEngine:
     """One shard on one GPU: rows [row_base, row_base + len(codes)) of a
     database of n_global rows.  prefix_codes = the global first
-    min(N, max r2) rows, replicated on every shard (qmax, twopass.py:83-84)."""
+    min(N, max r2) rows, replicated on every shard (qmax, twopass.py:83-84).
+    All device work of the shard runs on `self.stream`."""
 
-    def __init__(self, codebooks, derived, codes, row_base: int, n_global: int, prefix_codes, device: int = 0):
+    def __init__(self, codebooks, derived, codes, row_base: int, n_global: int, prefix_codes, device: int = 0,
+                 stream=None):
+        import torch
+
+        self.torch = torch
         self.handle = _lib.flat_create(codebooks, derived, codes, device=device, id_base=row_base,
                                        prefix_codes=prefix_codes)
         self.n_global = int(n_global)
         self.n_local = int(np.asarray(codes).shape[0])
         self.row_base = int(row_base)
+        self.device = torch.device("cuda", device)
+        self.stream = stream if stream is not None else torch.cuda.Stream(device=self.device)
+        self.handle.set_stream(self.stream.cuda_stream)
+        self.sample_global = {}  # exact -> total sampled rows over the shards (all-reduced once)
 
+    # ---- host-buffer protocol ------------------------------------------
     def begin(self, yr: np.ndarray, r2: int, exact: bool):
         nq = yr.shape[0]
         hist = np.zeros((nq, 256), dtype=np.int32)
@@ -64,10 +86,58 @@ class GpuShardEngine:
                                                _lib.ptr(i), _lib.ptr(need)), "shard_finish")
         return d, i, need.astype(bool)
 
+    # ---- device protocol (enqueue only, on self.stream) -----------------
+    def context(self):
+        return self.torch.cuda.stream(self.stream)
+
+    def to_device(self, a):
+        return self.torch.as_tensor(np.ascontiguousarray(a), device=self.device)
+
+    def begin_dev(self, y, r2: int, exact: bool):
+        torch = self.torch
+        nq = y.shape[0]
+        hist = torch.empty((nq, 256), dtype=torch.int32, device=self.device)
+        ns = np.zeros(1, dtype=np.int64)
+        _lib.check(_lib.lib().dpq_shard_begin_dev(self.handle.raw, _lib.ptr(y), nq, int(r2), self.n_global,
+                                                  int(bool(exact)), _lib.ptr(hist), _lib.ptr(ns)), "shard_begin_dev")
+        return hist, int(ns[0])
+
+    def scan_dev(self, hist_sum, sample_global: int, r2: int, exact: bool):
+        cand = self.torch.empty_like(hist_sum)
+        _lib.check(_lib.lib().dpq_shard_scan_dev(self.handle.raw, _lib.ptr(hist_sum), self.n_global,
+                                                 int(sample_global), int(r2), int(bool(exact)), _lib.ptr(cand)),
+                   "shard_scan_dev")
+        return cand
+
+    def finish_dev(self, cand_sum, r: int, r2: int):
+        torch = self.torch
+        nq = cand_sum.shape[0]
+        d = torch.empty((nq, r), dtype=torch.float64, device=self.device)
+        i = torch.empty((nq, r), dtype=torch.int64, device=self.device)
+        flags = torch.empty(nq, dtype=torch.uint8, device=self.device)
+        _lib.check(_lib.lib().dpq_shard_finish_dev(self.handle.raw, _lib.ptr(cand_sum), int(r), int(r2),
+                                                   _lib.ptr(d), _lib.ptr(i), _lib.ptr(flags)), "shard_finish_dev")
+        return d, i, flags
+
+    def merge_dev(self, parts_d, parts_i, r: int):
+        torch = self.torch
+        g, nq = parts_d.shape[0], parts_d.shape[1]
+        d = torch.empty((nq, r), dtype=torch.float64, device=self.device)
+        i = torch.empty((nq, r), dtype=torch.int64, device=self.device)
+        _lib.check(_lib.lib().dpq_merge_topr_dev(self.handle.raw, _lib.ptr(parts_d), _lib.ptr(parts_i), g, nq,
+                                                 int(r), _lib.ptr(d), _lib.ptr(i)), "merge_topr_dev")
+        return d, i
+
+    def search_dev(self, y, r: int, r2: int, comm=None):
+        """Sharded derived search of device queries y (already rotated)."""
+        return sharded_search_dev(self, comm or self.comm, y, r, r2)
+
 
 class TorchComm:
-    """Sum / max all-reduce and all-gather of small numpy arrays over a
-    torch.distributed process group (device = cuda for NCCL, cpu for gloo)."""
+    """All-reduce / all-gather over a torch.distributed process group.
+    Host arrays (the host protocol) travel through tensors on `device` (cuda
+    for NCCL, cpu for gloo); tensors (the device protocol) are reduced in
+    place on the current stream."""
 
     def __init__(self, group=None, device=None):
         import torch
@@ -79,11 +149,12 @@ class TorchComm:
         self.device = device
         self.world = dist.get_world_size(group)
 
+    # ---- host arrays ----------------------------------------------------
     def _t(self, a):
         return self.torch.from_numpy(np.ascontiguousarray(a)).to(self.device)
 
     def allreduce_sum(self, a: np.ndarray) -> np.ndarray:
-        t = self._t(a.astype(np.int64))
+        t = self._t(np.asarray(a).astype(np.int64))
         self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
         return t.cpu().numpy()
 
@@ -97,6 +168,21 @@ class TorchComm:
         out = [self.torch.empty_like(t) for _ in range(self.world)]
         self.dist.all_gather(out, t, group=self.group)
         return [o.cpu().numpy() for o in out]
+
+    # ---- tensors, in place ----------------------------------------------
+    def sum_(self, t):
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
+        return t
+
+    def max_(self, t):
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return t
+
+    def gather_stack(self, t):
+        """(world, *t.shape) tensor of every rank's t."""
+        out = self.torch.empty((self.world, *t.shape), dtype=t.dtype, device=t.device)
+        self.dist.all_gather(list(out.unbind(0)), t.contiguous(), group=self.group)
+        return out
 
 
 def merge_topr(dist_parts, id_parts, r: int):
@@ -114,8 +200,8 @@ def merge_topr(dist_parts, id_parts, r: int):
 
 
 def sharded_search(engine, comm, yr: np.ndarray, r: int, r2: int):
-    """Derived search of yr (already rotated) over all shards.  Returns the
-    same (dists, ids) on every rank."""
+    """Derived search of yr (already rotated) over all shards, host-buffer
+    driver.  Returns the same (dists, ids) on every rank."""
     if r > r2:
         raise ValueError(f"r={r} must not exceed r2={r2}")
     yr = np.ascontiguousarray(yr, dtype=np.float32)
@@ -133,6 +219,33 @@ def sharded_search(engine, comm, yr: np.ndarray, r: int, r2: int):
     return merge_topr(comm.allgather(d), comm.allgather(i), r)
 
 
+def sharded_search_dev(engine, comm, y, r: int, r2: int):
+    """Device-resident driver of the same protocol: y is a (nq, d) tensor on
+    the engine's device (already rotated); returns (dists, ids) tensors,
+    identical on every rank.  Collectives run in place on the engine's
+    stream; the host waits only for the all-reduced flags at the end."""
+    if r > r2:
+        raise ValueError(f"r={r} must not exceed r2={r2}")
+    with engine.context():
+        hist, ns = engine.begin_dev(y, r2, False)
+        if False not in engine.sample_global:  # total sampled rows: fixed per shard layout, reduced once
+            engine.sample_global[False] = int(comm.allreduce_sum(np.array([ns], dtype=np.int64))[0])
+        comm.sum_(hist)
+        cand = engine.scan_dev(hist, engine.sample_global[False], r2, False)
+        comm.sum_(cand)
+        d, i, flags = engine.finish_dev(cand, r, r2)
+        parts_d = comm.gather_stack(d)
+        parts_i = comm.gather_stack(i)
+        fl = comm.max_(flags.to(engine.torch.int32).max().reshape(1))
+        md, mi = engine.merge_dev(parts_d, parts_i, r)
+        redo = int(fl.item()) != 0  # the batch's only host synchronisation
+    if redo:  # a guard proved too tight or an emit list overflowed on some shard: redo through the host driver
+        yh = y.detach().cpu().numpy()
+        dh, ih = sharded_search(engine, comm, yh, r, r2)
+        md, mi = engine.to_device(dh), engine.to_device(ih)
+    return md, mi
+
+
 class ShardedFlatIndex:
     """FlatIndex.search(mode="derived") over a database split across ranks.
 
@@ -140,25 +253,33 @@ class ShardedFlatIndex:
     (every rank calls it with the same queries) and returns the global
     result on every rank."""
 
-    def __init__(self, quantizer, codes_shard, row_base: int, n_global: int, prefix_codes, comm,
-                 device: int = 0):
+    def __init__(self, quantizer, codes_shard, row_base: int, n_global: int, prefix_codes, comm=None,
+                 device: int = 0, batch: int = 1024):
         self.quantizer = quantizer
-        self.comm = comm
+        self.comm = comm if comm is not None else TorchComm()
+        self.batch = int(batch)
         self.engine = GpuShardEngine(quantizer.codebooks_, quantizer.derived_codebooks_, codes_shard, row_base,
                                      n_global, prefix_codes, device=device)
+        self.engine.comm = self.comm
 
-    def search(self, Y, r: int, mode: str = "derived", r2=None, batch: int = 1024):
+    def search(self, Y, r: int, mode: str = "derived", r2=None):
         if mode != "derived":
             raise ValueError("ShardedFlatIndex supports mode='derived'")
         if r2 is None:
             raise ValueError("derived mode requires r2")
-        Y = np.ascontiguousarray(Y, dtype=np.float32)
+        Y = _lib.query_array(Y)
         yr = rotated_queries(self.quantizer, Y)
-        out_d, out_i = [], []
-        for s in range(0, yr.shape[0], batch):
-            d, i = sharded_search(self.engine, self.comm, yr[s:s + batch], r, r2)
-            out_d.append(d)
-            out_i.append(i)
-        if not out_d:
+        if yr.shape[0] == 0:
             return np.full((0, r), np.inf), np.full((0, r), -1, dtype=np.int64)
-        return np.concatenate(out_d), np.concatenate(out_i)
+        eng = self.engine
+        out_d = np.empty((yr.shape[0], r), np.float64)
+        out_i = np.empty((yr.shape[0], r), np.int64)
+        with eng.context():
+            ydev = eng.to_device(yr)
+        for s in range(0, yr.shape[0], self.batch):
+            d, i = sharded_search_dev(eng, self.comm, ydev[s:s + self.batch], r, r2)
+            with eng.context():
+                out_d[s:s + self.batch] = d.cpu().numpy()
+                out_i[s:s + self.batch] = i.cpu().numpy()
+        return out_d, out_i
+

@@ -3,10 +3,12 @@ restated with the CPU oracle, so the multi-rank host protocol in
 paper_1905_06900_b200/shard.py can be checked on CPU (gloo) exactly as the
 GPU engine is driven on B200s."""
 
+import contextlib
 import math
 import threading
 
 import numpy as np
+import torch
 
 from oracle import derived_search as O
 
@@ -29,6 +31,7 @@ class OracleShardEngine:
         self.cb, self.der, self.codes = codebooks, derived, np.asarray(codes)
         self.base, self.n_global, self.prefix = row_base, n_global, np.asarray(prefix_codes)
         self.sample, self.exact_limit = sample, exact_limit
+        self.sample_global = {}
 
     def begin(self, yr, r2, exact):
         self.yr = yr
@@ -82,6 +85,33 @@ class OracleShardEngine:
                 i[q, :len(ids)] = ids
         return d, i, need
 
+    # device-protocol twins (CPU tensors): the same contract as
+    # GpuShardEngine.*_dev, so shard.sharded_search_dev runs unchanged
+    def context(self):
+        return contextlib.nullcontext()
+
+    def to_device(self, a):
+        return torch.as_tensor(np.ascontiguousarray(a))
+
+    torch = torch
+
+    def begin_dev(self, y, r2, exact):
+        hist, ns = self.begin(y.numpy(), r2, exact)
+        return torch.as_tensor(hist.astype(np.int32)), ns
+
+    def scan_dev(self, hist_sum, sample_global, r2, exact):
+        return torch.as_tensor(self.scan(hist_sum.numpy().astype(np.int64), sample_global, r2, exact).astype(np.int32))
+
+    def finish_dev(self, cand_sum, r, r2):
+        d, i, need = self.finish(cand_sum.numpy().astype(np.int64), r, r2)
+        return torch.as_tensor(d), torch.as_tensor(i), torch.as_tensor(need.astype(np.uint8))
+
+    def merge_dev(self, parts_d, parts_i, r):
+        from paper_1905_06900_b200.shard import merge_topr
+
+        d, i = merge_topr(list(parts_d.numpy()), list(parts_i.numpy()), r)
+        return torch.as_tensor(d), torch.as_tensor(i)
+
 
 class ThreadComm:
     """In-process stand-in for TorchComm: shards run as threads of one
@@ -112,3 +142,25 @@ class ThreadComm:
 
     def allgather(self, a):
         return self._exchange(a)
+
+    # tensors (device protocol): the producing stream is drained before the
+    # exchange, the result is written back in place
+    def _sync(self, t):
+        if t.is_cuda:
+            torch.cuda.current_stream(t.device).synchronize()
+
+    def sum_(self, t):
+        self._sync(t)
+        parts = self._exchange(t.clone())
+        t.copy_(torch.stack(parts).sum(0).to(t.dtype))
+        return t
+
+    def max_(self, t):
+        self._sync(t)
+        parts = self._exchange(t.clone())
+        t.copy_(torch.stack(parts).max(0).values)
+        return t
+
+    def gather_stack(self, t):
+        self._sync(t)
+        return torch.stack(self._exchange(t.clone()))

@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_device_count():
     L = _lib.lib()
-    assert L.dpq_abi_version() == 1
+    assert L.dpq_abi_version() == 2
     assert _lib.device_count() >= 0
 
 

@@ -11,7 +11,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from oracle import derived_search as O
-from paper_1905_06900_b200.shard import TorchComm, merge_topr, sharded_search
+from paper_1905_06900_b200.shard import TorchComm, merge_topr, sharded_search, sharded_search_dev
 from shard_engines import OracleShardEngine
 
 
@@ -36,12 +36,18 @@ def _free_port():
 def _worker(rank, world, port, args, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    cb, der, codes, Y, r, r2, sample, exact_limit = args
+    cb, der, codes, Y, r, r2, sample, exact_limit, dev = args
     n = codes.shape[0]
     lo, hi = rank * n // world, (rank + 1) * n // world
     eng = OracleShardEngine(cb, der, codes[lo:hi], lo, n, codes[:max(r2, 1)], sample=sample,
                             exact_limit=exact_limit)
-    d, i = sharded_search(eng, TorchComm(), Y, r, r2)
+    if dev:  # the device-resident driver (tensors, in-place collectives, merge_dev)
+        import torch
+
+        d, i = sharded_search_dev(eng, TorchComm(), torch.as_tensor(Y), r, r2)
+        d, i = d.numpy(), i.numpy()
+    else:
+        d, i = sharded_search(eng, TorchComm(), Y, r, r2)
     q.put((rank, d, i))
     dist.barrier()
     dist.destroy_process_group()
@@ -61,11 +67,12 @@ def _run(world, args):
     return {rk: (d, i) for rk, d, i in out}
 
 
+@pytest.mark.parametrize("dev", [False, True])
 @pytest.mark.parametrize("sample,exact_limit", [(16384, 65536), (8, 0)])
-def test_two_rank_gloo_equals_unsharded(sample, exact_limit):
+def test_two_rank_gloo_equals_unsharded(sample, exact_limit, dev):
     cb, der, codes, Y = _data()
     r, r2 = 10, 200
-    res = _run(2, (cb, der, codes, Y, r, r2, sample, exact_limit))
+    res = _run(2, (cb, der, codes, Y, r, r2, sample, exact_limit, dev))
     d0, i0 = O.flat_search(cb, der, codes, Y, r, "derived", r2)
     for rk in (0, 1):
         d, i = res[rk]
