@@ -94,12 +94,13 @@ static int hmalloc(T** p, size_t count) {
   return DPQ_OK;
 }
 
-// Dynamic shared memory above 48 KB needs a per-(device, kernel) attribute.
-// The largest size set so far is cached per (device, kernel) and recorded
-// only after the call succeeds, so a failed request (too large) never
-// masks a later valid one.  Cheap enough to call before every launch.
+// Static + dynamic shared memory above 48 KB needs a per-(device, kernel)
+// attribute.  The largest dynamic size set so far is cached per (device,
+// kernel) and recorded only after the call succeeds, so a failed request
+// (too large) never masks a later valid one.  Called before every launch
+// with dynamic shared memory.
 static int set_smem_impl(int device, const void* kern, size_t bytes) {
-  if (bytes <= 48 * 1024) return DPQ_OK;
+  if (bytes == 0) return DPQ_OK;
   static std::mutex mu;
   static std::map<std::pair<int, const void*>, size_t> done;
   std::lock_guard<std::mutex> lock(mu);
