@@ -222,6 +222,17 @@ int dpq_debug_candidates(dpq_index_t* index, const float* yr, int64_t nq,
 int dpq_debug_full_tables(dpq_index_t* index, const float* yr, int64_t nq,
                           float* tables);
 
+/* Tensor-core full tables (tcgen05 kind::tf32, 3xTF32 with centred
+ * operands and cached centroid norms): the approximation of
+ * compute_tables(yr, codebooks_) (search.py:28-48) that the derived refine
+ * uses when dsub >= 64 (env DPQ_TC_TABLES=0/1 overrides).  tables (nq, m, k)
+ * f32 in centroid order, eps (nq, m) f64: a rigorous bound on
+ * |tables - numpy's entry| for every entry of (query, subspace).  The search
+ * stays bit-exact: candidates within the bound of the r-th best are
+ * re-ranked with exact entries.                                           */
+int dpq_debug_tc_tables(dpq_index_t* index, const float* yr, int64_t nq,
+                        float* tables, double* eps);
+
 /* ------------------------------------------------------------ encoder --
  * Nearest-centroid encoding on the tensor cores (tcgen05, 3xTF32): replaces
  * ProductQuantizer._encode_with (quantizer.py:75-83) -> nearest_centroids

@@ -60,6 +60,7 @@ SIGNATURES = {
     "dpq_debug_candidate_ids": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_int64, c_void_p, c_void_p,
                                         c_void_p]),
     "dpq_debug_full_tables": (c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
+    "dpq_debug_tc_tables": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
     "dpq_encoder_create": (c_int, [c_int, c_int, c_int, c_int, c_void_p, POINTER(c_void_p)]),
     "dpq_encoder_destroy": (None, [c_void_p]),
     "dpq_encode": (c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
@@ -150,10 +151,11 @@ class Handle:
                         out.tolist()))
 
     def counters_ex(self) -> dict:
-        out = np.zeros(10, dtype=np.int64)
-        check(lib().dpq_counters_ex(self.raw, ptr(out), 10))
+        out = np.zeros(11, dtype=np.int64)
+        check(lib().dpq_counters_ex(self.raw, ptr(out), 11))
         return dict(zip(("launches", "queries", "rows_scanned", "refined", "fallbacks", "emitted",
-                         "table_entries", "wide_units", "plane_rows", "lut_loads"), out.tolist()))
+                         "table_entries", "wide_units", "plane_rows", "lut_loads", "exact_reranked"),
+                        out.tolist()))
 
     def set_timing(self, on: bool) -> None:
         check(lib().dpq_set_timing(self.raw, int(bool(on))))

@@ -327,7 +327,7 @@ static int launch_refine_buf(Index* h, const RefineArgs& ra, int nq) {
     kern<<<nq, kTopThreads, smem, h->stream>>>(rb);
     return DPQ_OK;
   };
-  if (MODE != MODE_EMIT) DPQ_TRY(go(k_refine_topk<BUF, kTopThreads, MODE, 0>));
+  if (MODE != MODE_EMIT && MODE != MODE_EMIT_APPROX) DPQ_TRY(go(k_refine_topk<BUF, kTopThreads, MODE, 0>));
   else if (ra.dsub == 32) DPQ_TRY(go(k_refine_topk<BUF, kTopThreads, MODE, 32>));
   else if (ra.dsub == 120) DPQ_TRY(go(k_refine_topk<BUF, kTopThreads, MODE, 120>));
   else DPQ_TRY(go(k_refine_topk<BUF, kTopThreads, MODE, 0>));
@@ -628,6 +628,33 @@ int run_group_tables(Index* h, int nq, int ystride) {
   return DPQ_OK;
 }
 
+// Tensor-core full tables (dpq_tctab.cu) instead of the lazy exact group
+// tables: used where the lazy builder's CUDA-core work is large (dsub >= 64,
+// e.g. BASELINE configs[4]: 8 x 65536 x 120), or forced by DPQ_TC_TABLES.
+static bool use_tc_tables(Index* h) {
+  const int mode = h->use_tc >= 0 ? h->use_tc : (h->dsub >= 64 ? 1 : 0);
+  return mode != 0 && tct_supported(h->m, h->k, h->kbar, h->dsub);
+}
+
+static int ensure_tct(Index* h) {
+  if (h->tct) return DPQ_OK;
+  return tct_prepare(h->device, h->cb, h->m, h->k, h->kbar, h->dsub, h->stream, &h->tct);
+}
+
+// Approximate full tables of nq query rows y (device, row stride ystride)
+// into ws.tables (group-major) with their error bounds in tct_eps.
+int run_tc_tables(Index* h, int nq, const float* y, int64_t ystride) {
+  DPQ_TRY(ensure_tct(h));
+  DPQ_TRY(ensure_tables(h, nq));
+  if ((int64_t)nq * h->m > h->tct_eps_cap) {
+    DPQ_TRY(dmalloc(&h->tct_eps, (size_t)nq * h->m));
+    h->tct_eps_cap = (int64_t)nq * h->m;
+  }
+  DPQ_TRY(tct_build(h->tct, y, ystride, nq, h->ws.tables, h->tct_eps, h->tc_eps_scale, h->stream));
+  h->counters[0]++;
+  return DPQ_OK;
+}
+
 // One flat derived batch: queries already in ws.y (nb rows), results into
 // ws.out_d / ws.out_i.  Returns 100 when the batch must be split.
 static int flat_derived_batch_body(Index* h, int nb, int r, int r2);
@@ -638,6 +665,7 @@ static int flat_derived_batch_body(Index* h, int nb, int r, int r2);
 // of ~20 kernel launches and memsets per batch.  The first call with a new
 // configuration runs eagerly (it sizes every buffer), the second captures.
 static int flat_derived_batch(Index* h, int nb, int r, int r2) {
+  if (use_tc_tables(h)) DPQ_TRY(ensure_tct(h));  // (synchronous, never inside a graph capture)
   const bool graphable = h->use_graph && !h->timing && !h->no_spec;
   if (!graphable) return flat_derived_batch_body(h, nb, r, r2);
   BatchGraph& G = h->graph;
@@ -696,7 +724,13 @@ static int flat_derived_batch_body(Index* h, int nb, int r, int r2) {
     DPQ_LAUNCHED(h);
     ra.order = h->ws.order;
   }
-  if (group_tables_fit(h, nb)) {
+  if (use_tc_tables(h)) {  // tensor-core full tables + exact re-rank of the margin set
+    DPQ_TRY(run_tc_tables(h, nb, h->ws.y, h->d));
+    ra.tables = h->ws.tables;
+    ra.eps = h->tct_eps;
+    ra.n_exact = h->d_nrows + 3;
+    DPQ_TRY(launch_refine<MODE_EMIT_APPROX>(h, ra, nb));
+  } else if (group_tables_fit(h, nb)) {
     DPQ_TRY(run_group_tables(h, nb, h->d));
     ra.tables = h->ws.tables;  // (re)allocated by run_group_tables
     DPQ_TRY(launch_refine<MODE_EMIT_TABLE>(h, ra, nb));
@@ -1050,6 +1084,8 @@ int index_common_init(Index* h, int device, int m, int k, int kbar, int dsub, co
   if (const char* e = getenv("DPQ_DIRECT_COPY")) h->direct_copy = atoi(e) != 0;
   if (const char* e = getenv("DPQ_SPECULATE")) h->no_spec = atoi(e) == 0;
   if (const char* e = getenv("DPQ_GRAPH")) h->use_graph = atoi(e) != 0;
+  if (const char* e = getenv("DPQ_TC_TABLES")) h->use_tc = atoi(e);
+  if (const char* e = getenv("DPQ_TC_EPS_SCALE")) h->tc_eps_scale = atof(e);
   DPQ_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   h->own_stream = true;
   for (int i = 0; i < 8; ++i) DPQ_CUDA(cudaEventCreate(&h->ev[i]));
@@ -1075,6 +1111,8 @@ void index_free(Index* h) {
   cudaSetDevice(h->device);
   ivf_free(h);
   if (h->stream) cudaStreamSynchronize(h->stream);
+  tct_free(h->tct);
+  if (h->tct_eps) cudaFree(h->tct_eps);
   if (h->graph.exec) cudaGraphExecDestroy(h->graph.exec);
   Workspace& w = h->ws;
   void* dev[] = {h->cb, h->dcb, h->codes, h->plane, h->own_prefix ? h->prefix : nullptr, h->centers,
@@ -1413,6 +1451,34 @@ int dpq_debug_candidate_ids(dpq_index_t* index, const float* yr, int64_t nq, int
   return DPQ_OK;
 }
 
+int dpq_debug_tc_tables(dpq_index_t* index, const float* yr, int64_t nq, float* tables, double* eps) {
+  Index* h = reinterpret_cast<Index*>(index);
+  DPQ_TRY(check_search(h, nq, 1, 1, false));
+  if (!tct_supported(h->m, h->k, h->kbar, h->dsub)) { set_error("unsupported shape for tensor-core tables"); return DPQ_ERR_ARG; }
+  if (nq > 0 && (!tables || !eps)) { set_error("null output"); return DPQ_ERR_ARG; }
+  const int64_t per = (int64_t)h->m * h->k;
+  const int gsize = h->k / h->kbar;
+  std::vector<float> gm;
+  const int bq = std::max(1, std::min(h->batch, 256));
+  for (int64_t q0 = 0; q0 < nq; q0 += bq) {
+    const int nb = (int)std::min<int64_t>(bq, nq - q0);
+    DPQ_TRY(ensure_ws(h, nb, 1, h->d, -1));
+    Workspace& w = h->ws;
+    DPQ_CUDA(cudaMemcpyAsync(w.y, yr + q0 * h->d, (size_t)nb * h->d * 4, cudaMemcpyHostToDevice, h->stream));
+    DPQ_TRY(run_tc_tables(h, nb, w.y, h->d));
+    gm.resize((size_t)nb * per);
+    DPQ_CUDA(cudaMemcpyAsync(gm.data(), w.tables, (size_t)nb * per * 4, cudaMemcpyDeviceToHost, h->stream));
+    DPQ_CUDA(cudaMemcpyAsync(eps + q0 * h->m, h->tct_eps, (size_t)nb * h->m * 8, cudaMemcpyDeviceToHost, h->stream));
+    DPQ_CUDA(cudaStreamSynchronize(h->stream));
+    for (int q = 0; q < nb; ++q)  // group-major -> centroid order
+      for (int j = 0; j < h->m; ++j)
+        for (int c = 0; c < h->k; ++c)
+          tables[(q0 + q) * per + (int64_t)j * h->k + c] =
+              gm[(size_t)q * per + (size_t)j * h->k + (size_t)(c & h->mask) * gsize + (c >> h->bbar)];
+  }
+  return DPQ_OK;
+}
+
 int dpq_last_phase_ms(dpq_index_t* index, float* ms7) {
   Index* h = reinterpret_cast<Index*>(index);
   if (!h || !ms7) { set_error("null argument"); return DPQ_ERR_ARG; }
@@ -1428,7 +1494,7 @@ int dpq_counters_ex(dpq_index_t* index, int64_t* out, int n) {
   unsigned long long dv[4] = {};
   DPQ_CUDA(cudaMemcpy(dv, h->d_nrows, sizeof(dv), cudaMemcpyDeviceToHost));
   const int64_t all[kCountersEx] = {base[0], base[1], base[2], base[3], base[4], base[5], base[6], base[7],
-                                    (int64_t)dv[1] + h->plane_rows, (int64_t)dv[2]};
+                                    (int64_t)dv[1] + h->plane_rows, (int64_t)dv[2], (int64_t)dv[3]};
   for (int i = 0; i < n; ++i) out[i] = i < kCountersEx ? all[i] : 0;
   return DPQ_OK;
 }

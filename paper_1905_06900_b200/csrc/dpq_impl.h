@@ -10,10 +10,17 @@ namespace dpq {
 
 void set_error(const std::string& msg);
 
+// tensor-core full tables (dpq_tctab.cu)
+bool tct_supported(int m, int k, int kbar, int dsub);
+int tct_prepare(int device, const float* cb, int m, int k, int kbar, int dsub, cudaStream_t stream, void** out);
+int tct_build(void* t, const float* y, int64_t ystride, int nq, float* tables, double* eps, double eps_scale,
+              cudaStream_t stream);
+void tct_free(void* t);
+
 enum Kind { KIND_FLAT = 0, KIND_IVF = 1 };
 
 // Phase slots of dpq_last_phase_ms.
-constexpr int kCountersEx = 10;  // dpq_counters_ex
+constexpr int kCountersEx = 11;  // dpq_counters_ex
 
 enum Phase { PH_TABLES = 0, PH_GUARD, PH_SCAN, PH_THRESH, PH_REFINE, PH_FALLBACK, PH_TOTAL, PH_N };
 
@@ -132,6 +139,13 @@ struct Index {
   int run_filter = 1;  // flat sorted rows: scan only chunks whose keys can reach a guard (env DPQ_RUN_FILTER=0)
   uint32_t* chunk_keys = nullptr;  // [n_chunks] first | last key << 16 of each 128-row chunk
   int64_t n_chunks = 0;
+  // tensor-core full tables (dpq_tctab.cu): prepared operand, per-batch
+  // entry error bounds, mode (-1 auto: dsub >= 64; env DPQ_TC_TABLES=0/1)
+  void* tct = nullptr;
+  double* tct_eps = nullptr;
+  int64_t tct_eps_cap = 0;
+  int use_tc = -1;
+  double tc_eps_scale = 1.0;  // env DPQ_TC_EPS_SCALE (tests: tighten to force more exact re-ranks)
   Workspace ws;
   // sharded-search state between dpq_shard_* calls
   int shard_nq = 0;

@@ -1583,7 +1583,14 @@ __global__ void __launch_bounds__(256)
 //   MODE_EMIT: emit list entries with score <= b*  (derived search)
 //   MODE_ALL : every row of [0, n_rows)            (conventional, tables)
 // ============================================================================
-enum { MODE_EMIT = 0, MODE_ALL = 1, MODE_EMIT_TABLE = 2 };
+// MODE_EMIT_APPROX: tables are the tensor-core approximations of
+// dpq_tctab.cu with per-(query, subspace) error bounds `eps`; pass 0 finds the
+// r-th smallest approximate distance A_r, pass 1 recomputes exactly (numpy
+// entries, entry_dist) every candidate whose approximate distance is
+// <= A_r + 2 sum_j eps[q, j] and keeps the exact top-r.  Every exact top-r
+// member d <= D_r <= A_r + E passes (|approx - exact| <= E), so the result is
+// the exact one.
+enum { MODE_EMIT = 0, MODE_ALL = 1, MODE_EMIT_TABLE = 2, MODE_EMIT_APPROX = 3 };
 
 struct RefineArgs {
   const uint64_t* emit; const uint32_t* emit_cnt; uint32_t cap;
@@ -1601,6 +1608,8 @@ struct RefineArgs {
   unsigned long long* n_refined;
   const int* order = nullptr;  // optional CTA -> query (heaviest emit lists first)
   int y_in_smem = 1;           // stage the query's y block in shared memory (else read it from global)
+  const double* eps = nullptr;  // MODE_EMIT_APPROX: (nq, m) entry error bounds of the tables
+  unsigned long long* n_exact = nullptr;  // MODE_EMIT_APPROX: candidates recomputed exactly
 };
 
 // Dynamic shared-memory budget of one refine CTA (buffer + staged y block).
@@ -1807,6 +1816,9 @@ __global__ void __launch_bounds__(NT, DPQ_REFINE_MINB) k_refine_topk(RefineArgs 
   // candidate that ties the threshold distance or enters the buffer
   auto id_of = [&](int64_t row) -> int64_t { return a.row_ids ? a.row_ids[row] : a.id_base + row; };
   // v: the candidate's emit entry (prefetched one round ahead)
+  int pass = 0;                 // MODE_EMIT_APPROX: 0 = approximate ranking, 1 = exact re-rank
+  double tau = 0.0;             //   pass-1 filter on the approximate distance
+  unsigned my_exact = 0;
   auto eval = [&](int64_t idx, uint64_t v, uint64_t& key, int64_t& id) -> bool {
     int64_t row;
     uint32_t probe = 0;
@@ -1817,10 +1829,10 @@ __global__ void __launch_bounds__(NT, DPQ_REFINE_MINB) k_refine_topk(RefineArgs 
     } else {
       row = idx;
     }
-    ++my_ref;
+    if (MODE != MODE_EMIT_APPROX || pass == 0) ++my_ref;
     double dist = 0.0;
     const float* yq = ys + (int64_t)probe * d;
-    if (MODE == MODE_EMIT_TABLE && a.code_bytes == 2 && a.m == 4) {
+    if ((MODE == MODE_EMIT_TABLE || MODE == MODE_EMIT_APPROX) && a.code_bytes == 2 && a.m == 4) {
       // one 8-byte code load, four independent table gathers with 32-bit
       // offsets inside this query's table block (m * k floats)
       const uint2 v = *reinterpret_cast<const uint2*>((const uint16_t*)a.codes + row * 4);
@@ -1840,6 +1852,16 @@ __global__ void __launch_bounds__(NT, DPQ_REFINE_MINB) k_refine_topk(RefineArgs 
         dist = __dadd_rn(dist, (double)t);
       }
     }
+    if (MODE == MODE_EMIT_APPROX && pass == 1) {  // exact re-rank of the candidates inside the margin
+      if (!(dist <= tau)) return false;
+      ++my_exact;
+      dist = 0.0;
+      for (int j = 0; j < a.m; ++j) {
+        const uint32_t c = code_at(a.codes, a.code_bytes, row * a.m + j);
+        dist = __dadd_rn(dist, (double)entry_dist<DSUB>(a.cb + ((int64_t)j * a.k + c) * a.dsub, yq + j * a.dsub,
+                                                        a.dsub));
+      }
+    }
     key = (uint64_t)__double_as_longlong(dist);
     id = row;  // (a row until id_of)
     return true;
@@ -1857,9 +1879,28 @@ __global__ void __launch_bounds__(NT, DPQ_REFINE_MINB) k_refine_topk(RefineArgs 
       ev[u] = (MODE != MODE_ALL && idx < ntot) ? e[idx] : 0ull;
     }
   };
-  load_e(0);
   int fb = 0;   // buffer fill before this round (same value in every thread)
   int rnd = 0;  // round index mod 3
+  constexpr int NPASS = MODE == MODE_EMIT_APPROX ? 2 : 1;
+  for (pass = 0; pass < NPASS; ++pass) {
+  if (pass == 1) {
+    // A_r = r-th smallest approximate distance (all pass when fewer than r)
+    const int P = pow2_at_least(fb);
+    for (int i = fb + threadIdx.x; i < P; i += NT) { keys[i] = ~0ull; ids[i] = INT64_MAX; }
+    __syncthreads();
+    sort_pairs<NT>(keys, ids, P);
+    double E = 0.0;
+    for (int j = 0; j < a.m; ++j) E += a.eps[(int64_t)q * a.m + j];
+    const double ar = fb >= a.r ? __longlong_as_double((long long)keys[a.r - 1]) : INFINITY;
+    tau = ar + 2.0 * E;
+    tau = tau + fabs(tau) * 1e-12;  // (the f64 sums themselves)
+    __syncthreads();
+    if (threadIdx.x == 0) { cnt3[0] = cnt3[1] = cnt3[2] = 0; thr_k = ~0ull; thr_i = INT64_MAX; }
+    __syncthreads();
+    fb = 0;
+    rnd = 0;
+  }
+  load_e(0);
   for (int64_t base = 0; base < ntot; base += (int64_t)U * NT, rnd = rnd == 2 ? 0 : rnd + 1) {
     uint64_t key[U], cur[U];
     int64_t id[U];
@@ -1910,6 +1951,7 @@ __global__ void __launch_bounds__(NT, DPQ_REFINE_MINB) k_refine_topk(RefineArgs 
       }
     }
   }
+  }  // pass
   const int f = fb;
   const int P = pow2_at_least(f);
   for (int i = f + threadIdx.x; i < P; i += NT) { keys[i] = ~0ull; ids[i] = INT64_MAX; }
@@ -1932,6 +1974,11 @@ __global__ void __launch_bounds__(NT, DPQ_REFINE_MINB) k_refine_topk(RefineArgs 
     if ((threadIdx.x & 31) == 0) atomicAdd(&nref, my_ref);
     __syncthreads();
     if (threadIdx.x == 0) atomicAdd(a.n_refined, (unsigned long long)nref);
+  }
+  if (MODE == MODE_EMIT_APPROX && a.n_exact) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) my_exact += __shfl_xor_sync(0xffffffffu, my_exact, o);
+    if ((threadIdx.x & 31) == 0 && my_exact) atomicAdd(a.n_exact, (unsigned long long)my_exact);
   }
 }
 

@@ -231,6 +231,18 @@ class FlatIndex(BaseEstimator):
                                                     _lib.ptr(out)))
         return out
 
+    def tc_tables(self, Y):
+        """Tensor-core approximation of compute_tables(yr, codebooks_) with
+        its error bound: (tables (nq, m, k) f32, eps (nq, m) f64)."""
+        Y = check_array(Y, dtype=np.float32, order="C")
+        yr = rotated_queries(self.quantizer, Y)
+        m, k = self.quantizer.codebooks_.shape[:2]
+        out = np.empty((yr.shape[0], m, k), np.float32)
+        eps = np.empty((yr.shape[0], m), np.float64)
+        _lib.check(_lib.lib().dpq_debug_tc_tables(self._handle().raw, _lib.ptr(yr), yr.shape[0], _lib.ptr(out),
+                                                  _lib.ptr(eps)))
+        return out, eps
+
     # -- persistence helpers kept from the reference (flat.py:112-126) -----
     def validate(self) -> None:
         from .errors import InvariantError
