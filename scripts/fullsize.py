@@ -158,22 +158,66 @@ def make_index(w, device=0):
                                 w["sorted_ids"], cell_of=w["cell_of"], rotation=w["rotation"], device=device)
 
 
-# -------------------------------------------------------------- oracle --
+# ----------------------------------------------------- CPU reference --
 
 _W = {}
+REF_PATH = ROOT / "baseline" / "_ref"
 
 
-def _oracle_worker(qi):
-    from oracle import derived_search as O
+def _reference_index(w):
+    """The unmodified reference (derivedpq, baseline/_ref) over the same
+    arrays: fitted attributes set directly, codes / inverted lists injected
+    (SURVEY 8c).  None when the reference is not installed."""
+    if str(REF_PATH) not in sys.path:
+        sys.path.insert(0, str(REF_PATH))
+    try:
+        from derivedpq import FlatIndex as RFlat, IVFIndex as RIVF, ProductQuantizer
+    except ImportError:
+        return None
+    cb, der = w["codebooks"], w["derived"]
+    m, k, dsub = cb.shape
+    kbar = der.shape[1]
+    pq = ProductQuantizer(m=m, b=int(k).bit_length() - 1, bbar=int(kbar).bit_length() - 1, seed=42)
+    pq.codebooks_, pq.derived_codebooks_ = cb, der
+    pq.derived_assignments_ = np.tile((np.arange(k) & (kbar - 1)).astype(np.int32), (m, 1))
+    pq.distortions_ = np.zeros(m)
+    pq.rotation_ = w["rotation"]
+    pq.d_, pq.dsub_, pq.k_, pq.kbar_, pq.bbar_ = m * dsub, dsub, k, kbar, int(kbar).bit_length() - 1
+    pq.code_dtype_ = np.uint16
+    if w["cfg"]["kind"] == "flat":
+        idx = RFlat(pq)
+        idx.codes_ = w["codes"]
+        idx.n_ = w["codes"].shape[0]
+        return idx
+    idx = RIVF(pq, n_cells=w["centers"].shape[0])
+    idx.centers_ = w["centers"]
+    idx.sorted_ids_ = w["sorted_ids"]
+    idx.sorted_codes_ = w["sorted_codes"]
+    idx.offsets_ = w["offsets"]
+    idx.cell_of_ = w["cell_of"]
+    n = w["sorted_ids"].shape[0]
+    idx.row_of_ = np.empty(n, dtype=np.int64)
+    idx.row_of_[w["sorted_ids"]] = np.arange(n)
+    idx.n_ = n
+    return idx
 
+
+def _ref_worker(qi):
     w = _W
     cfg = w["cfg"]
     y = w["queries"][qi: qi + 1]
+    if w["ref"] is not None:
+        kw = {"ma": cfg["ma"]} if cfg["kind"] == "ivf" else {}
+        d, i = w["ref"].search(y, w["r"], mode="derived", r2=cfg["r2"], **kw)
+        return qi, d[0], i[0]
+    from oracle import derived_search as O  # labelled fallback: the oracle port
+
     if cfg["kind"] == "flat":
         d, i = O.flat_search(w["codebooks"], w["derived"], w["codes"], y, w["r"], "derived", cfg["r2"],
                              rotation=w["rotation"])
     else:
-        row_of = w["row_of"]
+        row_of = np.empty_like(w["sorted_ids"])
+        row_of[w["sorted_ids"]] = np.arange(w["sorted_ids"].shape[0])
         iv = {"centers": w["centers"], "offsets": w["offsets"], "sorted_codes": w["sorted_codes"],
               "sorted_ids": w["sorted_ids"], "cell_of": w["cell_of"], "row_of": row_of,
               "codebooks": w["codebooks"], "derived": w["derived"], "bbar": 8,
@@ -182,21 +226,22 @@ def _oracle_worker(qi):
     return qi, d[0], i[0]
 
 
-def oracle_rows(w, qis, r):
-    """Oracle results of the given query rows on forked CPU workers."""
+def reference_rows(w, qis, r):
+    """Results of the given query rows from the unmodified reference (or,
+    when it is not installed, the oracle port) on forked CPU workers."""
     import multiprocessing as mp
+
+    from threadpoolctl import threadpool_limits
 
     _W.clear()
     _W.update(w)
     _W["r"] = r
-    if w["cfg"]["kind"] == "ivf" and "row_of" not in _W:
-        row_of = np.empty_like(w["sorted_ids"])
-        row_of[w["sorted_ids"]] = np.arange(w["sorted_ids"].shape[0])
-        _W["row_of"] = row_of
+    _W["ref"] = _reference_index(w)
     procs = max(1, min(len(qis), os.cpu_count() or 1))
-    with mp.get_context("fork").Pool(procs) as pool:
-        res = pool.map(_oracle_worker, list(qis))
-    return {qi: (d, i) for qi, d, i in res}
+    with threadpool_limits(1), mp.get_context("fork").Pool(procs) as pool:
+        res = pool.map(_ref_worker, list(qis))
+    kind = "reference" if _W["ref"] is not None else "port"
+    return {qi: (d, i) for qi, d, i in res}, kind
 
 
 # -------------------------------------------------------------- checks --
@@ -239,7 +284,28 @@ def check(w, r=100, check_queries=4, sub=8, device=0):
         rep.update(bstar_median=float(np.median(bstar)), bstar_max=int(bstar.max()),
                    candidates_mean=float(ncand.mean()), candidates_max=int(ncand.max()))
         c = idx._handle().counters()
-        rep["counters"] = c
+
+    elif w["rotation"] is None:  # ivf: each distance = f64 sum of exact entries in its own cell frame (ivf.py:253-268)
+        from paper_1905_06900_b200.flat import FlatIndex
+
+        tab_idx = FlatIndex.from_arrays(w["codebooks"], w["derived"], w["sorted_codes"][:1], rotation=w["rotation"],
+                                        device=device)
+        row_of = np.empty_like(w["sorted_ids"])
+        row_of[w["sorted_ids"]] = np.arange(w["sorted_ids"].shape[0])
+        nt = min(Y.shape[0], 16)
+        ok = 0
+        for q in range(nt):
+            cells = w["cell_of"][i[q]]
+            ucells, inv = np.unique(cells, return_inverse=True)
+            res = (Y[q][None, :] - w["centers"][ucells]).astype(np.float32)  # ivf.py:120, f32
+            tabs = tab_idx.full_tables(res)  # quantizer.rotate in the (ma, d) shape is applied inside
+            cods = w["sorted_codes"][row_of[i[q]]].astype(np.int64)
+            acc = np.zeros(r)
+            for j in range(m):
+                acc += tabs[inv, j, cods[:, j]].astype(np.float64)
+            ok += int(np.array_equal(acc, d[q]))
+        assert ok == nt, f"ivf distance recompute {ok}/{nt}"
+        rep["ivf_distance_recompute_queries"] = nt
     # ---- batch invariance
     sel = np.linspace(0, Y.shape[0] - 1, sub).astype(int)
     d2, i2 = idx.search(Y[sel], r, **kw)
@@ -248,22 +314,21 @@ def check(w, r=100, check_queries=4, sub=8, device=0):
     # ---- phase split (CUDA events per batch, amortised per query)
     _, _, tm = idx.search(Y, r, return_timings=True, **kw)
     rep["phase_us_per_query"] = {k2: round(float(v.mean()), 3) for k2, v in tm.items()}
-    if cfg["kind"] == "ivf":
-        rep["counters"] = idx._handle().counters()
+    rep["counters"] = idx._handle().counters_ex() if cfg["kind"] == "flat" else idx._handle().counters()
     if True:
         pm = idx._handle().phase_ms()
         rep["last_batch_ms"] = dict(zip(("tables", "guard", "scan", "threshold", "refine", "fallback", "total"),
                                         [round(float(v), 4) for v in pm]))
-    # ---- oracle, sampled
+    # ---- the unmodified reference (CPU), sampled queries
     if check_queries:
         qis = np.linspace(0, Y.shape[0] - 1, check_queries).astype(int)
         t = time.time()
-        orc = oracle_rows(w, qis, r)
+        orc, kind = reference_rows(w, qis, r)
         same_i = sum(bool(np.array_equal(orc[q][1], i[q])) for q in qis)
-        same_d = sum(bool(np.array_equal(orc[q][0], d[q])) for q in qis)
+        same_d = sum(bool(np.array_equal(orc[q][0].view(np.uint64), d[q].view(np.uint64))) for q in qis)
         rep["oracle"] = {"queries": len(qis), "ids_identical": same_i, "dists_identical": same_d,
-                         "cpu_s": round(time.time() - t, 1)}
-        assert same_i == len(qis) and same_d == len(qis), f"oracle mismatch {rep['oracle']}"
+                         "against": kind, "cpu_s": round(time.time() - t, 1)}
+        assert same_i == len(qis) and same_d == len(qis), f"reference mismatch {rep['oracle']}"
     return rep
 
 
@@ -272,7 +337,7 @@ def main():
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--queries", type=int, default=None)
-    ap.add_argument("--check", type=int, default=4)
+    ap.add_argument("--check", type=int, default=64, help="queries checked against the unmodified reference")
     ap.add_argument("--encoder", default="tc", choices=["tc", "torch"])
     ap.add_argument("--r2", type=int, default=None, help="override the config's r2 (the paper uses 9k-200k)")
     ap.add_argument("--r", type=int, default=100, help="results per query (k)")
