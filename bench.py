@@ -530,25 +530,56 @@ def run_single(args, cfg):
     print(json.dumps(result), flush=True)
 
 
+R2_GRID = (1000, 2000, 5000, 10_000, 20_000, 50_000, 100_000, 200_000)
+
+
 def comparator(idx, wl, cfg, args, der_ids, stream, flush):
-    """The paper's comparator on the same queries: conventional 16-bit search
-    (flat.py:82-93) queries/s and Recall@100 on one batch."""
+    """The paper's operating point on the same queries: the conventional
+    16-bit search (flat.py:82-93) as the recall reference, the smallest r2 of
+    a grid whose derived Recall@100 reaches 99% of it (calibrate_r2,
+    evaluation.py:95-128, restated), and queries/s of both through the public
+    API (host buffers) at that fixed recall."""
     import torch
 
     Bq, r = cfg["batch"], cfg["r"]
-    sel = slice(args.warmup * Bq, args.warmup * Bq + Bq)
-    Y = wl["queries"][sel]
+    cal = slice(args.warmup * Bq, args.warmup * Bq + Bq)  # calibration batch
+    Y, truth = wl["queries"][cal], wl["truth"][cal]
+
+    def timed(fn, reps=3):
+        best = []
+        for _ in range(reps):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            stream.synchronize()
+            t0 = time.perf_counter()
+            out = fn()
+            best.append(time.perf_counter() - t0)
+        return out, statistics.median(best)
+
     idx.search(Y[:8], r)  # warm-up (sizes the full-table buffers)
-    with torch.cuda.stream(stream):
-        flush.zero_()
-    stream.synchronize()
-    t0 = time.perf_counter()
-    _, ic = idx.search(Y, r)
-    t_conv = time.perf_counter() - t0
-    return {"recall_vs_conventional": {
-        "queries": Bq, "derived": round(recall_at(der_ids[sel], wl["truth"][sel], r), 4),
-        "conventional_16bit": round(recall_at(ic, wl["truth"][sel], r), 4),
-        "conventional_qps_e2e": round(Bq / t_conv, 1)}}
+    (_, ic), t_conv = timed(lambda: idx.search(Y, r), reps=1)
+    full = recall_at(ic, truth, r)
+    r2_fix, rec_fix = R2_GRID[-1], None
+    for r2 in R2_GRID:
+        if r2 > cfg["n"]:
+            break
+        _, i = idx.search(Y, r, mode="derived", r2=r2)
+        rec = recall_at(i, truth, r)
+        if rec >= 0.99 * full:
+            r2_fix, rec_fix = r2, rec
+            break
+    if rec_fix is None:
+        _, i = idx.search(Y, r, mode="derived", r2=r2_fix)
+        rec_fix = recall_at(i, truth, r)
+    idx.search(Y, r, mode="derived", r2=r2_fix)  # warm-up (graph of this configuration)
+    _, t_der = timed(lambda: idx.search(Y, r, mode="derived", r2=r2_fix))
+    return {"fixed_recall": {
+        "queries": Bq, "rule": "smallest grid r2 with derived Recall@100 >= 0.99 x conventional (calibrate_r2)",
+        "r2_grid": list(R2_GRID), "conventional_16bit": {"recall_at_100": round(full, 4),
+                                                         "qps_e2e": round(Bq / t_conv, 1)},
+        "derived": {"r2": r2_fix, "recall_at_100": round(rec_fix, 4), "qps_e2e": round(Bq / t_der, 1)},
+        "derived_at_bench_r2": {"r2": cfg["r2"],
+                                "recall_at_100": round(recall_at(der_ids[cal], truth, r), 4)}}}
 
 
 # ------------------------------------------------------------ multi-GPU --

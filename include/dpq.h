@@ -52,6 +52,18 @@ int dpq_device_count(void);
  * 0 = all finite, 1 = contains NaN, 2 = contains +-inf (NaN wins).  No GPU. */
 int dpq_all_finite(const float* x, int64_t n);
 
+/* quantizer.rotate (quantizer.py:235-239) in the reference's call shapes,
+ * for n rows of x (n, d) f32: rows_per_call = 1 is the per-query (1, d) @ R
+ * of the flat search (twopass.py:334), rows_per_call = ma the per-query
+ * (ma, d) @ R of the IVF residuals (ivf.py:202).  sgemv / sgemm are the
+ * CBLAS entry points of the BLAS numpy itself links (ilp64 = 1 for 64-bit
+ * integer builds); every call is numpy's own (sgemv RowMajor/Trans for one
+ * row, sgemm RowMajor/NoTrans for a block), so the bits are the reference's,
+ * and the calls run on `threads` host threads.  No GPU.                   */
+int dpq_rotate_rows(const float* x, int64_t n, int64_t rows_per_call, int d,
+                    const float* rotation, float* out, void* sgemv,
+                    void* sgemm, int ilp64, int threads);
+
 /* ---------------------------------------------------------------- flat --
  * Replaces the fitted state FlatIndex holds after fit (flat.py:45-52):
  * quantizer.codebooks_ (m,k,dsub) f32, quantizer.derived_codebooks_

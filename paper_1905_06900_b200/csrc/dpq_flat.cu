@@ -648,9 +648,10 @@ int run_tc_tables(Index* h, int nq, const float* y, int64_t ystride) {
   DPQ_TRY(ensure_tables(h, nq));
   if ((int64_t)nq * h->m > h->tct_eps_cap) {
     DPQ_TRY(dmalloc(&h->tct_eps, (size_t)nq * h->m));
+    DPQ_TRY(dmalloc(&h->tct_ny, (size_t)nq * h->m));
     h->tct_eps_cap = (int64_t)nq * h->m;
   }
-  DPQ_TRY(tct_build(h->tct, y, ystride, nq, h->ws.tables, h->tct_eps, h->tc_eps_scale, h->stream));
+  DPQ_TRY(tct_build(h->tct, y, ystride, nq, h->ws.tables, h->tct_eps, h->tct_ny, h->tc_eps_scale, h->stream));
   h->counters[0]++;
   return DPQ_OK;
 }
@@ -727,7 +728,9 @@ static int flat_derived_batch_body(Index* h, int nb, int r, int r2) {
   if (use_tc_tables(h)) {  // tensor-core full tables + exact re-rank of the margin set
     DPQ_TRY(run_tc_tables(h, nb, h->ws.y, h->d));
     ra.tables = h->ws.tables;
-    ra.eps = h->tct_eps;
+    ra.ny = h->tct_ny;
+    ra.cnorm = tct_cnorm(h->tct);
+    ra.gamma = tct_gamma(h->tct, h->tc_eps_scale);
     ra.n_exact = h->d_nrows + 3;
     DPQ_TRY(launch_refine<MODE_EMIT_APPROX>(h, ra, nb));
   } else if (group_tables_fit(h, nb)) {
@@ -1113,6 +1116,7 @@ void index_free(Index* h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   tct_free(h->tct);
   if (h->tct_eps) cudaFree(h->tct_eps);
+  if (h->tct_ny) cudaFree(h->tct_ny);
   if (h->graph.exec) cudaGraphExecDestroy(h->graph.exec);
   Workspace& w = h->ws;
   void* dev[] = {h->cb, h->dcb, h->codes, h->plane, h->own_prefix ? h->prefix : nullptr, h->centers,
@@ -1151,6 +1155,44 @@ int dpq_all_finite(const float* x, int64_t n) {
   for (int64_t i = 0; i < n; ++i)
     if ((b[i] & 0x7F800000u) == 0x7F800000u && (b[i] & 0x007FFFFFu)) return 1;
   return 2;
+}
+
+// quantizer.rotate (quantizer.py:235-239) of many rows in the reference's
+// call shapes through the caller's CBLAS: (1, d) @ R per row is numpy's
+// sgemv (RowMajor, Trans), a (g, d) @ R block (g >= 2) numpy's sgemm
+// (RowMajor, NoTrans, NoTrans); identical calls, so identical bits, run on
+// a few OpenMP threads.
+typedef void (*sgemv_lp64_t)(int, int, int, int, float, const float*, int, const float*, int, float, float*, int);
+typedef void (*sgemm_lp64_t)(int, int, int, int, int, int, float, const float*, int, const float*, int, float, float*,
+                             int);
+typedef void (*sgemv_ilp64_t)(int, int, int64_t, int64_t, float, const float*, int64_t, const float*, int64_t, float,
+                              float*, int64_t);
+typedef void (*sgemm_ilp64_t)(int, int, int, int64_t, int64_t, int64_t, float, const float*, int64_t, const float*,
+                              int64_t, float, float*, int64_t);
+int dpq_rotate_rows(const float* x, int64_t n, int64_t rows_per_call, int d, const float* rotation, float* out,
+                    void* sgemv, void* sgemm, int ilp64, int threads) {
+  if (n < 0 || d < 1 || rows_per_call < 1 || (n > 0 && (!x || !rotation || !out)) || n % rows_per_call) {
+    set_error("dpq_rotate_rows: bad arguments"); return DPQ_ERR_ARG;
+  }
+  if ((rows_per_call == 1 && !sgemv) || (rows_per_call > 1 && !sgemm)) {
+    set_error("dpq_rotate_rows: missing BLAS entry point"); return DPQ_ERR_ARG;
+  }
+  const int64_t calls = n / rows_per_call;
+  const int g = (int)rows_per_call;
+  const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(threads > 0 ? threads : 8, calls / 16));
+#pragma omp parallel for num_threads(nt) schedule(static)
+  for (int64_t c = 0; c < calls; ++c) {
+    const float* a = x + c * g * d;
+    float* o = out + c * g * d;
+    if (g == 1) {
+      if (ilp64) ((sgemv_ilp64_t)sgemv)(101, 112, d, d, 1.f, rotation, d, a, 1, 0.f, o, 1);
+      else ((sgemv_lp64_t)sgemv)(101, 112, d, d, 1.f, rotation, d, a, 1, 0.f, o, 1);
+    } else {
+      if (ilp64) ((sgemm_ilp64_t)sgemm)(101, 111, 111, g, d, d, 1.f, a, d, rotation, d, 0.f, o, d);
+      else ((sgemm_lp64_t)sgemm)(101, 111, 111, g, d, d, 1.f, a, d, rotation, d, 0.f, o, d);
+    }
+  }
+  return DPQ_OK;
 }
 
 int dpq_device_count(void) {

@@ -13,8 +13,10 @@ void set_error(const std::string& msg);
 // tensor-core full tables (dpq_tctab.cu)
 bool tct_supported(int m, int k, int kbar, int dsub);
 int tct_prepare(int device, const float* cb, int m, int k, int kbar, int dsub, cudaStream_t stream, void** out);
-int tct_build(void* t, const float* y, int64_t ystride, int nq, float* tables, double* eps, double eps_scale,
-              cudaStream_t stream);
+int tct_build(void* t, const float* y, int64_t ystride, int nq, float* tables, double* eps, double* ny,
+              double eps_scale, cudaStream_t stream);
+double tct_gamma(void* t, double eps_scale);
+const float* tct_cnorm(void* t);
 void tct_free(void* t);
 
 enum Kind { KIND_FLAT = 0, KIND_IVF = 1 };
@@ -142,7 +144,8 @@ struct Index {
   // tensor-core full tables (dpq_tctab.cu): prepared operand, per-batch
   // entry error bounds, mode (-1 auto: dsub >= 64; env DPQ_TC_TABLES=0/1)
   void* tct = nullptr;
-  double* tct_eps = nullptr;
+  double* tct_eps = nullptr;  // (nq, m) per-(query, subspace) bounds
+  double* tct_ny = nullptr;   // (nq, m) ||y'||
   int64_t tct_eps_cap = 0;
   int use_tc = -1;
   double tc_eps_scale = 1.0;  // env DPQ_TC_EPS_SCALE (tests: tighten to force more exact re-ranks)

@@ -1584,12 +1584,13 @@ __global__ void __launch_bounds__(256)
 //   MODE_ALL : every row of [0, n_rows)            (conventional, tables)
 // ============================================================================
 // MODE_EMIT_APPROX: tables are the tensor-core approximations of
-// dpq_tctab.cu with per-(query, subspace) error bounds `eps`; pass 0 finds the
-// r-th smallest approximate distance A_r, pass 1 recomputes exactly (numpy
-// entries, entry_dist) every candidate whose approximate distance is
-// <= A_r + 2 sum_j eps[q, j] and keeps the exact top-r.  Every exact top-r
-// member d <= D_r <= A_r + E passes (|approx - exact| <= E), so the result is
-// the exact one.
+// dpq_tctab.cu; entry (q, j, c) is within g (||y'_qj|| + ||c'_jc||)^2 of
+// numpy's, so a candidate's approximate distance a is within E = the sum of
+// its m entry bounds of the exact one d.  Pass 0 ranks the upper bounds
+// a + E and takes U = the r-th smallest (>= r candidates have d <= U, so the
+// exact r-th distance D_r <= U); pass 1 recomputes exactly (numpy entries,
+// entry_dist) every candidate with a - E <= U — which includes every exact
+// top-r member (d <= D_r) — and keeps the exact top-r.
 enum { MODE_EMIT = 0, MODE_ALL = 1, MODE_EMIT_TABLE = 2, MODE_EMIT_APPROX = 3 };
 
 struct RefineArgs {
@@ -1608,7 +1609,9 @@ struct RefineArgs {
   unsigned long long* n_refined;
   const int* order = nullptr;  // optional CTA -> query (heaviest emit lists first)
   int y_in_smem = 1;           // stage the query's y block in shared memory (else read it from global)
-  const double* eps = nullptr;  // MODE_EMIT_APPROX: (nq, m) entry error bounds of the tables
+  const double* ny = nullptr;     // MODE_EMIT_APPROX: (nq, m) ||y'|| (centred query sub-vectors)
+  const float* cnorm = nullptr;   //   (m, k) ||c'|| in group-major entry order
+  double gamma = 0.0;             //   entry bound coefficient
   unsigned long long* n_exact = nullptr;  // MODE_EMIT_APPROX: candidates recomputed exactly
 };
 
@@ -1781,7 +1784,7 @@ template <int BUF, int NT, int MODE, int DSUB>
 #ifndef DPQ_REFINE_MINB
 #define DPQ_REFINE_MINB 5  // CTAs per SM the register budget is sized for (6: 40 regs, spills)
 #endif
-__global__ void __launch_bounds__(NT, DPQ_REFINE_MINB) k_refine_topk(RefineArgs a) {
+__global__ void __launch_bounds__(NT, MODE == MODE_EMIT_APPROX ? 3 : DPQ_REFINE_MINB) k_refine_topk(RefineArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   uint64_t* keys = reinterpret_cast<uint64_t*>(smem);
   int64_t* ids = reinterpret_cast<int64_t*>(keys + BUF);
@@ -1832,6 +1835,12 @@ __global__ void __launch_bounds__(NT, DPQ_REFINE_MINB) k_refine_topk(RefineArgs 
     if (MODE != MODE_EMIT_APPROX || pass == 0) ++my_ref;
     double dist = 0.0;
     const float* yq = ys + (int64_t)probe * d;
+    double E = 0.0;  // MODE_EMIT_APPROX: bound on |approx - exact| of this candidate
+    auto ebound = [&](int j, uint32_t c) {
+      const int64_t ej = (int64_t)j * a.k + ((c & (uint32_t)(a.kbar - 1)) * (uint32_t)(a.k >> a.bbar) + (c >> a.bbar));
+      const double s = a.ny[(int64_t)q * a.m + j] + (double)__ldg(a.cnorm + ej);
+      E += a.gamma * s * s;
+    };
     if ((MODE == MODE_EMIT_TABLE || MODE == MODE_EMIT_APPROX) && a.code_bytes == 2 && a.m == 4) {
       // one 8-byte code load, four independent table gathers with 32-bit
       // offsets inside this query's table block (m * k floats)
@@ -1843,6 +1852,9 @@ __global__ void __launch_bounds__(NT, DPQ_REFINE_MINB) k_refine_topk(RefineArgs 
       const float t2 = __ldg(tq + off(2, v.y & 0xFFFFu));
       const float t3 = __ldg(tq + off(3, v.y >> 16));
       dist = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(dist, (double)t0), (double)t1), (double)t2), (double)t3);
+      if (MODE == MODE_EMIT_APPROX) {
+        ebound(0, v.x & 0xFFFFu); ebound(1, v.x >> 16); ebound(2, v.y & 0xFFFFu); ebound(3, v.y >> 16);
+      }
     } else {
       for (int j = 0; j < a.m; ++j) {
         const uint32_t c = code_at(a.codes, a.code_bytes, row * a.m + j);
@@ -1850,10 +1862,13 @@ __global__ void __launch_bounds__(NT, DPQ_REFINE_MINB) k_refine_topk(RefineArgs 
         if (MODE != MODE_EMIT) t = __ldg(a.tables + table_index(q, j, c, a.m, a.kbar, a.bbar, a.k / a.kbar));
         else t = entry_dist<DSUB>(a.cb + ((int64_t)j * a.k + c) * a.dsub, yq + j * a.dsub, a.dsub);
         dist = __dadd_rn(dist, (double)t);
+        if (MODE == MODE_EMIT_APPROX) ebound(j, c);
       }
     }
+    if (MODE == MODE_EMIT_APPROX) E = E * (1.0 + 1e-9) + fabs(dist) * 1e-12;  // (f64 sums themselves)
+    if (MODE == MODE_EMIT_APPROX && pass == 0) dist = dist + E;  // rank by the upper bound
     if (MODE == MODE_EMIT_APPROX && pass == 1) {  // exact re-rank of the candidates inside the margin
-      if (!(dist <= tau)) return false;
+      if (!(dist - E <= tau)) return false;
       ++my_exact;
       dist = 0.0;
       for (int j = 0; j < a.m; ++j) {
@@ -1884,16 +1899,12 @@ __global__ void __launch_bounds__(NT, DPQ_REFINE_MINB) k_refine_topk(RefineArgs 
   constexpr int NPASS = MODE == MODE_EMIT_APPROX ? 2 : 1;
   for (pass = 0; pass < NPASS; ++pass) {
   if (pass == 1) {
-    // A_r = r-th smallest approximate distance (all pass when fewer than r)
     const int P = pow2_at_least(fb);
     for (int i = fb + threadIdx.x; i < P; i += NT) { keys[i] = ~0ull; ids[i] = INT64_MAX; }
     __syncthreads();
     sort_pairs<NT>(keys, ids, P);
-    double E = 0.0;
-    for (int j = 0; j < a.m; ++j) E += a.eps[(int64_t)q * a.m + j];
-    const double ar = fb >= a.r ? __longlong_as_double((long long)keys[a.r - 1]) : INFINITY;
-    tau = ar + 2.0 * E;
-    tau = tau + fabs(tau) * 1e-12;  // (the f64 sums themselves)
+    // U = r-th smallest upper bound a + E (all candidates pass when fewer than r)
+    tau = fb >= a.r ? __longlong_as_double((long long)keys[a.r - 1]) : INFINITY;
     __syncthreads();
     if (threadIdx.x == 0) { cnt3[0] = cnt3[1] = cnt3[2] = 0; thr_k = ~0ull; thr_i = INT64_MAX; }
     __syncthreads();

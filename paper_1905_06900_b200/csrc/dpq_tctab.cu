@@ -193,7 +193,8 @@ __global__ void k_tct_mean(const float* __restrict__ cb, int k, int dsub, float*
 // Centroid operand: one thread per (subspace, padded group-major entry e).
 // Also R[j] = max_c ||c'|| (f64 bits, atomic max of the non-negative value).
 __global__ void k_tct_prep(const float* __restrict__ cb, const float* __restrict__ mu, int m, int k, int kbar,
-                           int dsub, int kc, int nt, uint8_t* __restrict__ img, unsigned long long* __restrict__ rmax) {
+                           int dsub, int kc, int nt, uint8_t* __restrict__ img, unsigned long long* __restrict__ rmax,
+                           float* __restrict__ cnorm) {
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t kp = (int64_t)nt * BN;
   if (gid >= (int64_t)m * kp) return;
@@ -228,6 +229,7 @@ __global__ void k_tct_prep(const float* __restrict__ cb, const float* __restrict
     const float cc = tf32_rna((float)(r1 - (double)b));
     p[0] = a; p[1] = b; p[2] = cc;
     atomicMax(rmax + j, (unsigned long long)__double_as_longlong(sqrt(n2)));
+    cnorm[(int64_t)j * k + e] = __double2float_ru(sqrt(n2));  // ||c'|| rounded up, group-major entry order
   } else {
     p[0] = kPadNorm;
   }
@@ -243,7 +245,8 @@ struct Args {
   const float* mu;      // (m, dsub)
   const double* rmax;   // (m)
   float* tables;        // (nq, m, k) group-major
-  double* eps;          // (nq, m) entry error bounds
+  double* eps;          // (nq, m) entry error bounds (with the subspace's largest ||c'||)
+  double* ny;           // (nq, m) ||y'|| (optional: per-entry bounds gamma (||y'|| + ||c'||)^2)
   double gamma;         // error-bound coefficient (see tct_build)
   int ntr, tpr, nqb;    // tile ranges, tiles per range, query blocks
   int64_t units;        // m * ntr * nqb
@@ -397,6 +400,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tct_gemm(Args a) {
           if (live && t0 == 0) {  // entry error bound of (query, subspace): once per (j, query block)
             const double s = sqrt(n2) + a.rmax[j];
             a.eps[gq * a.m + j] = a.gamma * s * s;
+            if (a.ny) a.ny[gq * a.m + j] = sqrt(n2);
           }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -460,6 +464,7 @@ struct TcTables {
   uint8_t* img = nullptr;
   float* mu = nullptr;
   double* rmax = nullptr;
+  float* cnorm = nullptr;  // (m, k) ||c'|| in group-major entry order, rounded up
   int sms = 148;
 };
 
@@ -483,6 +488,7 @@ void tct_free(void* p) {
   cudaFree(t->img);
   cudaFree(t->mu);
   cudaFree(t->rmax);
+  cudaFree(t->cnorm);
   delete t;
 }
 
@@ -500,7 +506,8 @@ int tct_prepare(int device, const float* cb, int m, int k, int kbar, int dsub, c
   auto fail = [&](int rc) { tct_free(t); return rc; };
   cudaDeviceGetAttribute(&t->sms, cudaDevAttrMultiProcessorCount, device);
   if (cudaMalloc(&t->img, (size_t)m * t->nt * tct::tile_bytes(t->kc)) != cudaSuccess ||
-      cudaMalloc(&t->mu, (size_t)m * dsub * 4) != cudaSuccess || cudaMalloc(&t->rmax, (size_t)m * 8) != cudaSuccess) {
+      cudaMalloc(&t->mu, (size_t)m * dsub * 4) != cudaSuccess || cudaMalloc(&t->rmax, (size_t)m * 8) != cudaSuccess ||
+      cudaMalloc(&t->cnorm, (size_t)m * k * 4) != cudaSuccess) {
     cudaGetLastError();
     set_error("tensor-core tables: operand allocation failed");
     return fail(DPQ_ERR_NOMEM);
@@ -509,7 +516,7 @@ int tct_prepare(int device, const float* cb, int m, int k, int kbar, int dsub, c
   tct::k_tct_mean<<<dim3(m, dsub), 256, 0, stream>>>(cb, k, dsub, t->mu);
   const int64_t tot = (int64_t)m * t->nt * tct::BN;
   tct::k_tct_prep<<<(unsigned)((tot + 255) / 256), 256, 0, stream>>>(
-      cb, t->mu, m, k, kbar, dsub, t->kc, t->nt, t->img, reinterpret_cast<unsigned long long*>(t->rmax));
+      cb, t->mu, m, k, kbar, dsub, t->kc, t->nt, t->img, reinterpret_cast<unsigned long long*>(t->rmax), t->cnorm);
   if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(stream) != cudaSuccess) {
     set_error("tensor-core tables: operand preparation failed");
     return fail(DPQ_ERR_CUDA);
@@ -528,23 +535,30 @@ int tct_prepare(int device, const float* cb, int m, int k, int kbar, int dsub, c
 // floats) into tables (nq, m, k) group-major, and per (query, subspace) the
 // entry error bound eps (nq, m):  |T~ - T_numpy| <= eps.
 //
-// Bound (f64): eps = gamma * (||y'|| + max_c ||c'||)^2 with
+// Bound (f64), per entry: |T~ - T| <= gamma * (||y'|| + ||c'||)^2 (the
+// refine uses this with the stored ||y'|| (ny) and ||c'|| (tct_cnorm));
+// eps = gamma * (||y'|| + max_c ||c'||)^2 bounds a whole (query, subspace); with
 //   gamma = (4 * Kp + 64) * 2^-23,  Kp = 16 * ceil(dsub / 16):
 // the 3xTF32 GEMM accumulates 3 Kp + 3 products in f32 (each add <= 2^-23
 // relative to the running magnitude <= (||y'|| + ||c'||)^2, allowing
 // truncation), the dropped lo.lo term is <= 2^-22 |y'||c'|, ||y'||^2 adds Kp
 // roundings, the centring y - mu, c - mu one rounding per component, and
 // numpy's own pairwise sum <= (Kp / 8 + 8) 2^-24 of the same magnitude.
-int tct_build(void* p, const float* y, int64_t ystride, int nq, float* tables, double* eps, double eps_scale,
-              cudaStream_t stream) {
+double tct_gamma(void* p, double eps_scale) {
+  const TcTables* t = reinterpret_cast<const TcTables*>(p);
+  return eps_scale * (4.0 * t->kc * tct::KCH + 64.0) * std::ldexp(1.0, -23);
+}
+const float* tct_cnorm(void* p) { return reinterpret_cast<const TcTables*>(p)->cnorm; }
+
+int tct_build(void* p, const float* y, int64_t ystride, int nq, float* tables, double* eps, double* ny,
+              double eps_scale, cudaStream_t stream) {
   TcTables* t = reinterpret_cast<TcTables*>(p);
   if (!t) { set_error("tensor-core tables not prepared"); return DPQ_ERR_STATE; }
   if (nq <= 0) return DPQ_OK;
   tct::Args a;
   a.y = y; a.ystride = ystride; a.nq = nq; a.m = t->m; a.k = t->k; a.dsub = t->dsub; a.kc = t->kc; a.nt = t->nt;
-  a.img = t->img; a.mu = t->mu; a.rmax = t->rmax; a.tables = tables; a.eps = eps;
-  const int kp = t->kc * tct::KCH;
-  a.gamma = eps_scale * (4.0 * kp + 64.0) * std::ldexp(1.0, -23);
+  a.img = t->img; a.mu = t->mu; a.rmax = t->rmax; a.tables = tables; a.eps = eps; a.ny = ny;
+  a.gamma = tct_gamma(p, eps_scale);
   a.nqb = (nq + tct::BM - 1) / tct::BM;
   const int64_t base = (int64_t)t->m * a.nqb;
   a.ntr = (int)std::max<int64_t>(1, std::min<int64_t>(t->nt, (4LL * t->sms + base - 1) / base));

@@ -47,6 +47,9 @@ def rotated_queries(quantizer, Y: np.ndarray) -> np.ndarray:
     from the per-row product under OpenBLAS (SURVEY Appendix A rule 11)."""
     if getattr(quantizer, "rotation_", None) is None:
         return np.ascontiguousarray(Y, dtype=np.float32)
+    fast = _lib.rotate_rows(quantizer, Y, 1)  # the same BLAS call per row, on a few host threads
+    if fast is not None:
+        return fast
     out = np.empty((Y.shape[0], quantizer.codebooks_.shape[0] * quantizer.codebooks_.shape[2]),
                    dtype=np.float32)
     for i in range(Y.shape[0]):

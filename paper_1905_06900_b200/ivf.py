@@ -140,10 +140,15 @@ class IVFIndex(BaseEstimator):
             # OPQ: residuals rotated by the reference's own rotate in its
             # (ma, d) call shape (ivf.py:202), so tables are bitwise its own
             cells = self._probe_cells(Y, ma)
-            res_rot = np.empty((nq, ma, Y.shape[1]), dtype=np.float32)
-            for qi in range(nq):
-                res = Y[qi][None, :] - self.centers_[cells[qi]]
-                res_rot[qi] = np.asarray(self.quantizer.rotate(res), dtype=np.float32)
+            res = (Y[:, None, :] - self.centers_[cells]).reshape(nq * ma, Y.shape[1])  # ivf.py:120, f32
+            fast = _lib.rotate_rows(self.quantizer, res, ma)  # the same BLAS call per query, threaded
+            if fast is not None:
+                res_rot = fast.reshape(nq, ma, Y.shape[1])
+            else:
+                res_rot = np.empty((nq, ma, Y.shape[1]), dtype=np.float32)
+                for qi in range(nq):
+                    res_q = Y[qi][None, :] - self.centers_[cells[qi]]
+                    res_rot[qi] = np.asarray(self.quantizer.rotate(res_q), dtype=np.float32)
         dists = np.empty((nq, r), dtype=np.float64)
         ids = np.empty((nq, r), dtype=np.int64)
         phase = np.zeros((nq, 4), dtype=np.float64) if return_timings else None
