@@ -433,8 +433,10 @@ struct ScanPlan {
 int plan_flat_scan(Index* h, int nb, ScanPlan& sp) {
   Workspace& w = h->ws;
   const int tiles = tiles_of(nb, h->mpad);
-  sp.sorted = h->sort_slots && h->wide && h->mpad == 4 && nb > 1;
-  sp.list = h->rows_sorted && h->run_filter && h->m >= 2 && h->mpad == 4 && h->n > 0;
+  sp.list = h->rows_sorted && h->run_filter && h->m >= 2 && h->n > 0;
+  // query tiles clustered by guard class and nearest (g0, g1): feeds the
+  // wide loop (MPAD 4) and makes the per-tile run filter selective
+  sp.sorted = h->sort_slots && nb > 1 && (h->mpad == 4 ? h->wide != 0 : sp.list);
   if (sp.list && (w.list_tiles < tiles || w.list_chunks < h->n_chunks)) {
     DPQ_TRY(dmalloc(&w.pot, (size_t)tiles * 65536));
     DPQ_TRY(dmalloc(&w.chunk_list, (size_t)tiles * h->n_chunks));
@@ -463,7 +465,7 @@ int prepare_flat_scan(Index* h, int nb, const ScanPlan& sp) {
         w.q8, h->m, h->kbar, sp.slot_q, sp.gw, qt, nb, w.pot);
     DPQ_LAUNCHED(h);
     k_chunk_list<<<dim3((unsigned)((h->n_chunks + 255) / 256), tiles), 256, 0, h->stream>>>(
-        h->chunk_keys, (int)h->n_chunks, w.pot, w.chunk_list, w.list_len, h->n, nb, qt, h->d_nrows);
+        h->chunk_keys, (int)h->n_chunks, 512 / h->mpad, w.pot, w.chunk_list, w.list_len, h->n, nb, qt, h->d_nrows);
     DPQ_LAUNCHED(h);
   }
   return DPQ_OK;
@@ -961,11 +963,11 @@ __global__ void k_row_keys(const void* codes, int code_bytes, int64_t n, int m, 
   keys[i] = ((code_at(codes, code_bytes, i * m) & mask) << 8) | (code_at(codes, code_bytes, i * m + 1) & mask);
   rows[i] = (int32_t)i;
 }
-// key range [first row, last row] of every 128-row chunk (rows sorted by key)
-__global__ void k_chunk_keys(const uint32_t* skeys, int64_t n, int64_t nchunks, uint32_t* chunk_keys) {
+// key range [first row, last row] of every scan chunk (512 B of plane: 128 rows at MPAD 4, 64 at 8)
+__global__ void k_chunk_keys(const uint32_t* skeys, int64_t n, int64_t nchunks, int cr, uint32_t* chunk_keys) {
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= nchunks) return;
-  const int64_t a = c * 128, b = std::min<int64_t>(a + 127, n - 1);
+  const int64_t a = c * cr, b = std::min<int64_t>(a + cr - 1, n - 1);
   chunk_keys[c] = skeys[a] | (skeys[b] << 16);
 }
 __global__ void k_gather_rows(const uint8_t* codes, int row_bytes, int64_t n, const int32_t* perm, int64_t id_base,
@@ -1032,9 +1034,10 @@ static int sort_rows(Index* h) {
   }
   k_gather_rows<<<blocks, 256, 0, h->stream>>>((const uint8_t*)h->codes, row_bytes, n, r1, h->id_base, sorted,
                                                h->sorted_ids);
-  h->n_chunks = (n + 127) / 128;
+  const int cr = 512 / h->mpad;  // rows per scan chunk
+  h->n_chunks = (n + cr - 1) / cr;
   if ((rc = dmalloc(&h->chunk_keys, (size_t)h->n_chunks))) { cudaFree(sorted); cleanup(); return rc; }
-  k_chunk_keys<<<(unsigned)((h->n_chunks + 255) / 256), 256, 0, h->stream>>>(k1, n, h->n_chunks, h->chunk_keys);
+  k_chunk_keys<<<(unsigned)((h->n_chunks + 255) / 256), 256, 0, h->stream>>>(k1, n, h->n_chunks, cr, h->chunk_keys);
   if (cudaStreamSynchronize(h->stream) != cudaSuccess) { cleanup(); set_error("row sort failed"); return DPQ_ERR_CUDA; }
   cleanup();
   if (h->prefix == h->codes) {  // original order stays as the qmax prefix
@@ -1235,7 +1238,7 @@ int dpq_flat_create(int device, int m, int k, int kbar, int dsub, const float* c
     h->prefix = h->codes;
     h->n_prefix = n;
   }
-  if (h->sort_rows && h->mpad == 4 && m >= 2 && n > 1 && n < ((int64_t)1 << 31) &&
+  if (h->sort_rows && m >= 2 && n > 1 && n < ((int64_t)1 << 31) &&
       (rc = sort_rows(h)) != DPQ_OK) { index_free(h); return rc; }
   if ((rc = make_plane(h)) != DPQ_OK) { index_free(h); return rc; }
   if (cudaStreamSynchronize(h->stream) != cudaSuccess) {

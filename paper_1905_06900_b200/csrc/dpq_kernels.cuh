@@ -488,7 +488,7 @@ __global__ void __launch_bounds__(1024) k_sort_slots(const uint16_t* __restrict_
 // (g0, g1) can only reach a query's guard B if e0[g0] + e1[g1] <= B.
 //   k_run_potential: pot[tile][key] = 1 iff some slot of the tile passes
 //     (grid: 64 x tiles, 4 values of g0 per CTA, 4 of g1 per thread)
-//   k_chunk_list: per tile, the 128-row chunks whose key range holds a key
+//   k_chunk_list: per tile, the scan chunks (512 B of plane) whose key range holds a key
 //     with pot = 1 (unordered list + length); the scan visits only those.
 // Skipped rows have score > B, so they would never be emitted: exact.
 __global__ void __launch_bounds__(256) k_run_potential(const uint8_t* __restrict__ q8, int m, int kbar,
@@ -542,7 +542,7 @@ __global__ void __launch_bounds__(256) k_run_potential(const uint8_t* __restrict
   if (g0 < kbar) reinterpret_cast<uint32_t*>(pot + (int64_t)tile * 65536 + g0 * 256)[t] = (~acc & 0x80808080u) >> 7;
 }
 
-__global__ void __launch_bounds__(256) k_chunk_list(const uint32_t* __restrict__ chunk_keys, int nchunks,
+__global__ void __launch_bounds__(256) k_chunk_list(const uint32_t* __restrict__ chunk_keys, int nchunks, int cr,
                                                     const uint8_t* __restrict__ pot, int* __restrict__ list,
                                                     int* __restrict__ list_len, int64_t n, int nb, int qt,
                                                     unsigned long long* __restrict__ n_rows) {
@@ -558,7 +558,7 @@ __global__ void __launch_bounds__(256) k_chunk_list(const uint32_t* __restrict__
   int base = 0;
   if (lane == 0 && bal) base = atomicAdd(list_len + tile, __popc(bal));
   if (n_rows) {  // query-rows this tile will scan (its real queries x listed rows) and the listed plane rows
-    const unsigned rows = f ? (unsigned)min((int64_t)128, n - (int64_t)c * 128) : 0u;
+    const unsigned rows = f ? (unsigned)min((int64_t)cr, n - (int64_t)c * cr) : 0u;
     const unsigned wr = __reduce_add_sync(0xffffffffu, rows);
     if (lane == 0 && wr) {
       atomicAdd(n_rows, (unsigned long long)wr * (unsigned long long)min(qt, nb - tile * qt));
