@@ -84,9 +84,7 @@ def resolve(args, world: int):
     """(cfg, mode) of this run; identical in both arms."""
     from paper_1905_06900_b200 import workloads
 
-    mode = args.mode or ("shard" if world > 1 else "single")
-    if world == 1:
-        mode = "single"
+    mode = args.mode or ("shard" if world > 1 else "single")  # (--mode shard at N = 1: the protocol on one GPU)
     name = args.config or ("c3" if mode == "shard" else "c2")
     cfg = dict(workloads.CONFIGS[name])
     if args.n:

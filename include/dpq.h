@@ -205,6 +205,41 @@ int dpq_merge_topr_dev(dpq_index_t* index, const double* part_dists,
 /* Wait for everything enqueued on the index stream. */
 int dpq_sync(dpq_index_t* index);
 
+/* ------------------------------------------------- sharded (ivf) --
+ * IVF list-split sharding: every inverted list is cut evenly
+ * across the shards, keeping cell order; each shard's handle is created
+ * with dpq_ivf_create over its slice of every list (sorted_ids = GLOBAL
+ * ids) and then told the global lists: global_offsets (K+1) and, per list,
+ * its first min(prefix_rows, len) global rows (prefix_codes, row offsets
+ * prefix_offsets (K+1)) — the rows qmax is estimated from (ivf.py:205-217;
+ * r2 <= prefix_rows).  The protocol mirrors the flat one, host buffers:
+ *   1. dpq_ivf_shard_begin: probe (identical on every shard), per-cell
+ *      tables, bounds from the first non-empty GLOBAL probed list, score
+ *      histogram of this shard's sampled rows -> sample_hist (nq,256),
+ *      n_sampled (nq) [sum both over shards]; n_rows (nq) = rows of the
+ *      probed global lists (identical on every shard); exact != 0 samples
+ *      every row.
+ *   2. dpq_ivf_shard_scan: guards from the sums, scan of the local slices
+ *      -> cand_hist (nq,256) [sum over shards]
+ *   3. dpq_ivf_shard_finish: b*, refine of the local candidates in their
+ *      own cell frames, local top-r with global ids; need_exact (nq) = 1
+ *      where the guard proved too tight (repeat 1-3 with exact = 1).
+ * The merged top-r (dpq_merge_topr_dev or the host merge) equals the
+ * unsharded IVFIndex.search result bit for bit.                          */
+int dpq_ivf_set_shard(dpq_index_t* index, const int64_t* global_offsets,
+                      const void* prefix_codes, const int64_t* prefix_offsets,
+                      int64_t prefix_rows);
+int dpq_ivf_shard_begin(dpq_index_t* index, const float* y, int64_t nq,
+                        int ma, int r2, int exact, const float* res_rot,
+                        const int64_t* cells, int32_t* sample_hist,
+                        int64_t* n_sampled, int64_t* n_rows);
+int dpq_ivf_shard_scan(dpq_index_t* index, const int32_t* sample_hist_sum,
+                       const int64_t* sampled_sum, const int64_t* rows_sum,
+                       int r2, int32_t* cand_hist);
+int dpq_ivf_shard_finish(dpq_index_t* index, const int32_t* cand_hist_sum,
+                         int r, int r2, double* dists, int64_t* ids,
+                         uint8_t* need_exact);
+
 /* ------------------------------------------------ unit seams (debug) --
  * Replace compute_tables(yr, derived_codebooks_) + quantize_tables
  * (search.py:28-48, twopass.py:63-85) for nq queries: small (nq,m,kbar) f32,

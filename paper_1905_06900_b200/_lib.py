@@ -55,6 +55,11 @@ SIGNATURES = {
     "dpq_shard_finish_dev": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p]),
     "dpq_merge_topr_dev": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int64, c_int, c_void_p, c_void_p]),
     "dpq_sync": (c_int, [c_void_p]),
+    "dpq_ivf_set_shard": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64]),
+    "dpq_ivf_shard_begin": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p,
+                                    c_void_p, c_void_p]),
+    "dpq_ivf_shard_scan": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p]),
+    "dpq_ivf_shard_finish": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p]),
     "dpq_debug_quantize_tables": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_void_p, c_void_p,
                                           c_void_p, c_void_p]),
     "dpq_debug_low_scores": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_void_p]),

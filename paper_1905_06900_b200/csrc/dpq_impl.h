@@ -107,6 +107,13 @@ struct Index {
   std::vector<int64_t> h_offsets; // host copy
   int64_t* sorted_ids = nullptr;  // [n]
   void* ivf_state = nullptr;      // IvfBuffers (dpq_ivf.cuh)
+  // ivf list-split shard (dpq_ivf_set_shard): this handle holds a slice of
+  // every inverted list; bounds and sampling follow the GLOBAL lists
+  bool ivf_shard = false;
+  std::vector<int64_t> g_offsets;  // (K+1) global list offsets
+  std::vector<int64_t> g_pre_off;  // (K+1) offsets of each list's prefix rows in g_prefix
+  void* g_prefix = nullptr;        // device: first min(P, len) rows of every global list (qmax, ivf.py:205-217)
+  int64_t g_pre_rows = 0;          // P
   // execution
   cudaStream_t stream = nullptr;
   bool own_stream = false;
@@ -153,6 +160,8 @@ struct Index {
   // sharded-search state between dpq_shard_* calls
   int shard_nq = 0;
   int64_t shard_samp = 0;
+  int shard_ma = 0;          // ivf shard: probes of the current batch
+  int64_t shard_stride = 1;  // ivf shard: sampling stride of the current batch (1 = exact)
 };
 
 }  // namespace dpq

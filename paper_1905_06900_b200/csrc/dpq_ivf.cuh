@@ -311,6 +311,9 @@ using pinned_vector = std::vector<T, PinnedAllocator<T>>;
 
 struct IvfPlan {
   int nq = 0, ma = 0, nts = 0, ntiles = 0;
+  int nph = 0;                         // shard: bound-source slots after the tile slots (list empty here)
+  std::vector<int> phantom;            // their slot indices
+  std::vector<int64_t> nr_global;      // shard: rows of the probed GLOBAL lists per query
   std::vector<int64_t> cells;          // (nq, ma)
   pinned_vector<int> slot_query, slot_probe;
   std::vector<int> tile_cell, bound_ts;
@@ -342,6 +345,7 @@ struct IvfBuffers {
   int64_t* unit_r1 = nullptr;
   int64_t* tile_row0 = nullptr;
   int64_t* tile_nsamp = nullptr;
+  int* phantom = nullptr;              // [cap_q] shard bound-source slots
   double* d2 = nullptr;                // probe distances (nq, K)
   int64_t cap_d2 = 0;
 };
@@ -362,6 +366,7 @@ static int ivf_ensure(Index* h, int nq, int ma, int nts, int ntiles, int nunits)
     DPQ_TRY(dmalloc(&b.hist_q, (size_t)b.cap_q * 256));
     DPQ_TRY(dmalloc(&b.gword_q, (size_t)b.cap_q));
     DPQ_TRY(dmalloc(&b.guard_q, (size_t)b.cap_q));
+    DPQ_TRY(dmalloc(&b.phantom, (size_t)b.cap_q));
   }
   if (nts > b.cap_ts) {
     b.cap_ts = nts;
@@ -386,11 +391,13 @@ static void ivf_free(Index* h) {
   if (!h->ivf_state) return;
   IvfBuffers& b = ivf_bufs(h);
   void* p[] = {b.cells, b.ynat, b.yts, b.bound_ts, b.live, b.bsrc, b.lambda, b.hist_q, b.gword_q, b.guard_q,
-               b.unit_tile, b.unit_r0, b.unit_r1, b.tile_row0, b.tile_nsamp, b.d2};
+               b.unit_tile, b.unit_r0, b.unit_r1, b.tile_row0, b.tile_nsamp, b.d2, b.phantom};
   for (void* x : p)
     if (x) cudaFree(x);
   delete reinterpret_cast<IvfBuffers*>(h->ivf_state);
   h->ivf_state = nullptr;
+  if (h->g_prefix) cudaFree(h->g_prefix);
+  h->g_prefix = nullptr;
 }
 
 // Probe on device: cells (nb, ma) into bufs.cells.
@@ -447,6 +454,9 @@ static void ivf_plan(Index* h, IvfPlan& P, int nb, int ma, int r2) {
   P.nr.assign(nb, 0);
   P.sq.assign(nb, 0);
   const int64_t* cells = P.cells.data();
+  const bool shard = h->ivf_shard;
+  const int64_t* goff = shard ? h->g_offsets.data() : off;  // bound source and sampling follow the global lists
+  if (shard) P.nr_global.assign(nb, 0);
 #pragma omp parallel num_threads(T)
   {
     const int t = omp_get_thread_num();
@@ -454,9 +464,14 @@ static void ivf_plan(Index* h, IvfPlan& P, int nb, int ma, int r2) {
     for (int q = nb * t / T; q < nb * (t + 1) / T; ++q)
       for (int p = 0; p < ma; ++p) {
         const int64_t c = cells[(size_t)q * ma + p];
+        if (shard) {
+          const int64_t glen = goff[c + 1] - goff[c];
+          if (glen > 0 && first[q] < 0) first[q] = p;
+          P.nr_global[q] += glen;
+        }
         const int64_t len = off[c + 1] - off[c];
         if (len <= 0) continue;
-        if (first[q] < 0) first[q] = p;
+        if (!shard && first[q] < 0) first[q] = p;
         ++ct[c];
         P.nr[q] += len;
       }
@@ -484,11 +499,16 @@ static void ivf_plan(Index* h, IvfPlan& P, int nb, int ma, int r2) {
   for (int c = 0; c < K; ++c)
     for (int t = tile0[c]; t < tile0[c + 1]; ++t) P.tile_cell[t] = c;
   // guard sampling: one stride for the batch, exact when lists are short
+  // (shard: from the global lists, so every shard samples alike)
+  if (shard) {
+    tot_rows = 0;
+    for (int q = 0; q < nb; ++q) tot_rows += P.nr_global[q];
+  }
   const int64_t avg = nb > 0 ? tot_rows / std::max(1, nb) : 0;
   P.stride = (avg <= h->exact_limit) ? 1 : std::max<int64_t>(1, avg / std::max<int64_t>(1, h->sample));
   const int64_t stride = P.stride;
-  P.slot_query.resize(P.nts);
-  P.slot_probe.resize(P.nts);
+  P.slot_query.resize(P.nts + nb);  // (+ room for shard bound-source slots)
+  P.slot_probe.resize(P.nts + nb);
   std::vector<int>& ts_first = P.ts_first;  // slot of each query's first non-empty probe
   ts_first.assign(nb, -1);
   int* sqv = P.slot_query.data();
@@ -519,20 +539,37 @@ static void ivf_plan(Index* h, IvfPlan& P, int nb, int ma, int r2) {
   for (int c = 0; c < K; ++c)  // live slots in slot order
     for (int i = 0; i < cnt[c]; ++i) P.live[k++] = tile0[c] * qt + i;
   // qmax prefix: first min(r2, len) rows of each query's first non-empty
-  // list, one entry per bound-source slot (list order of P.bsrc)
+  // list, one entry per bound-source slot (list order of P.bsrc).  A shard
+  // takes them from the replicated global prefixes; when that list is empty
+  // on this shard the bound source is an extra slot after the tile slots.
   P.bound_ts.assign(nb, -1);
   P.bsrc.clear();
   P.pre_off.clear();
   P.pre_len.clear();
+  P.phantom.clear();
+  P.nph = 0;
   for (int q = 0; q < nb; ++q) {
     if (first[q] < 0) continue;
     const int64_t c = P.cells[(size_t)q * ma + first[q]];
-    const int ts = ts_first[q];
+    int ts = ts_first[q];
+    if (ts < 0) {  // (shard only)
+      ts = P.nts + P.nph++;
+      P.slot_query[ts] = q;
+      P.slot_probe[ts] = first[q];
+      P.phantom.push_back(ts);
+    }
     P.bound_ts[q] = ts;
     P.bsrc.push_back(ts);
-    P.pre_off.push_back(off[c]);
-    P.pre_len.push_back(std::min<int64_t>(r2, off[c + 1] - off[c]));
+    if (shard) {
+      P.pre_off.push_back(h->g_pre_off[c]);
+      P.pre_len.push_back(std::min<int64_t>(r2, goff[c + 1] - goff[c]));
+    } else {
+      P.pre_off.push_back(off[c]);
+      P.pre_len.push_back(std::min<int64_t>(r2, off[c + 1] - off[c]));
+    }
   }
+  P.slot_query.resize(P.nts + P.nph);
+  P.slot_probe.resize(P.nts + P.nph);
   P.tile_row0.assign(P.ntiles, 0);
   P.tile_nsamp.assign(P.ntiles, 0);
   P.max_nsamp = 0;
@@ -571,17 +608,14 @@ static int h2d(T* dst, const std::vector<T, A>& v, cudaStream_t s) {
   return DPQ_OK;
 }
 
-// One IVF batch: raw queries in ws.y (nb x d).  res_rot / cells_in are host
-// arrays for the OPQ path (residuals rotated by the caller), else NULL.
-static int ivf_batch(Index* h, int nb, int r, int ma, int r2, bool derived, const float* res_rot,
-                     const int64_t* cells_in) {
+// Probe (or take the caller's cells) and form the residuals in natural
+// (query, probe) order: B.cells, P.cells (host), B.ynat.
+static int ivf_probe_residuals(Index* h, int nb, int ma, const float* res_rot, const int64_t* cells_in) {
   Workspace& w = h->ws;
   IvfBuffers& B = ivf_bufs(h);
+  IvfPlan& P = B.plan;
   const int d = h->d;
-  const int qt = qt_of(h->mpad);
-  ev_rec(h, 0);
   DPQ_TRY(ivf_ensure(h, nb, ma, 0, 0, 0));
-  IvfPlan& P = B.plan;  // persistent: vectors keep their capacity (no re-faulting per batch)
   P.cells.resize((size_t)nb * ma);
   if (cells_in) {
     memcpy(P.cells.data(), cells_in, P.cells.size() * 8);
@@ -592,7 +626,6 @@ static int ivf_batch(Index* h, int nb, int r, int ma, int r2, bool derived, cons
     DPQ_CUDA(cudaStreamSynchronize(h->stream));
   }
   ev_rec(h, 1);
-  // residuals in natural (query, probe) order
   if (res_rot) {
     DPQ_CUDA(cudaMemcpyAsync(B.ynat, res_rot, (size_t)nb * ma * d * 4, cudaMemcpyHostToDevice, h->stream));
   } else {
@@ -600,6 +633,176 @@ static int ivf_batch(Index* h, int nb, int r, int ma, int r2, bool derived, cons
     k_residuals<<<(unsigned)((tot + 255) / 256), 256, 0, h->stream>>>(w.y, h->centers, B.cells, nb, ma, d, B.ynat);
     DPQ_LAUNCHED(h);
   }
+  return DPQ_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Derived-mode pieces shared by ivf_batch and the list-split shard protocol.
+// ---------------------------------------------------------------------------
+// After probe + residuals (B.cells, B.ynat): plan, uploads, slot residuals,
+// K1 pass A (qmin/qmax of each query's bound-source slot, from the first
+// min(r2, len) rows of its first non-empty probed list — the replicated
+// global prefixes on a shard) and pass B (every live slot quantized with its
+// query's bounds).  *empty: no probed list holds rows here.
+static int ivf_derived_setup(Index* h, int nb, int r, int ma, int r2, bool* empty) {
+  Workspace& w = h->ws;
+  IvfBuffers& B = ivf_bufs(h);
+  IvfPlan& P = B.plan;
+  const int d = h->d;
+  try {
+    ivf_plan(h, P, nb, ma, r2);
+  } catch (const std::bad_alloc&) {
+    set_error("ivf plan: pinned host allocation failed");
+    return DPQ_ERR_NOMEM;
+  }
+  if (h->ws.cap == 0 && h->cap0 == 0) {
+    // first emit capacity per query from the probed rows (a query emits ~r2
+    // to a few r2 rows; growth covers outliers): avg probed / 256, pow2
+    int64_t probed = 0;
+    for (int q = 0; q < nb; ++q)
+      for (int p = 0; p < ma; ++p) {
+        const int64_t c = P.cells[(size_t)q * ma + p];
+        probed += h->h_offsets[c + 1] - h->h_offsets[c];
+      }
+    int64_t c = std::max<int64_t>(16384, std::min<int64_t>(probed / std::max(nb, 1) / 256, (int64_t)1 << 20));
+    int64_t p2 = 1;
+    while (p2 < c) p2 <<= 1;
+    h->cap0 = p2;
+  }
+  const int nslot = P.nts + P.nph;
+  DPQ_TRY(ensure_ws(h, std::max(nslot, 1), r, d, nb));
+  DPQ_TRY(ivf_ensure(h, nb, ma, std::max(nslot, 1), std::max(P.ntiles, 1), std::max((int)P.unit_tile.size(), 1)));
+  DPQ_TRY(h2d(w.slot_query, P.slot_query, h->stream));
+  DPQ_TRY(h2d(w.slot_probe, P.slot_probe, h->stream));
+  DPQ_TRY(h2d(w.slot_pre_off, P.pre_off, h->stream));
+  DPQ_TRY(h2d(w.slot_pre_len, P.pre_len, h->stream));
+  DPQ_TRY(h2d(B.bound_ts, P.bound_ts, h->stream));
+  DPQ_TRY(h2d(B.lambda, P.lambda, h->stream));
+  DPQ_TRY(h2d(B.tile_row0, P.tile_row0, h->stream));
+  DPQ_TRY(h2d(B.tile_nsamp, P.tile_nsamp, h->stream));
+  DPQ_TRY(h2d(B.unit_tile, P.unit_tile, h->stream));
+  DPQ_TRY(h2d(B.unit_r0, P.unit_r0, h->stream));
+  DPQ_TRY(h2d(B.unit_r1, P.unit_r1, h->stream));
+  DPQ_CUDA(cudaMemsetAsync(w.emit_cnt, 0, (size_t)nb * 4, h->stream));
+  *empty = P.nts == 0;
+  if (*empty) return DPQ_OK;
+  const int nlive = (int)P.live.size(), nbsrc = (int)P.bsrc.size();
+  DPQ_TRY(h2d(B.live, P.live, h->stream));
+  DPQ_TRY(h2d(B.bsrc, P.bsrc, h->stream));
+  const int64_t tot = (int64_t)nlive * d;
+  k_gather_slots<<<(unsigned)((tot + 255) / 256), 256, 0, h->stream>>>(B.ynat, w.slot_query, w.slot_probe, ma, d,
+                                                                      nlive, B.live, B.yts);
+  DPQ_LAUNCHED(h);
+  if (P.nph > 0) {  // shard: bound-source slots whose list is empty here
+    DPQ_TRY(h2d(B.phantom, P.phantom, h->stream));
+    const int64_t tp = (int64_t)P.nph * d;
+    k_gather_slots<<<(unsigned)((tp + 255) / 256), 256, 0, h->stream>>>(B.ynat, w.slot_query, w.slot_probe, ma, d,
+                                                                       P.nph, B.phantom, B.yts);
+    DPQ_LAUNCHED(h);
+  }
+  const void* prefix = h->ivf_shard ? h->g_prefix : h->codes;
+  // K1 pass A: qmin/qmax of the bound-source slots only (their tables are
+  // recomputed in pass B; padding slots are never computed)
+  DPQ_TRY(run_small_tables(h, nslot, prefix, 0, w.slot_pre_off, w.slot_pre_len, nullptr, false, B.yts, B.bsrc, nbsrc,
+                           false));
+  k_slot_bounds<<<(P.nts + 255) / 256, 256, 0, h->stream>>>(w.qmin, w.qmax, B.bound_ts, w.slot_query, P.nts,
+                                                            w.bounds);
+  DPQ_LAUNCHED(h);
+  // K1 pass B: quantize every slot with its query's bounds -> LUT tiles
+  DPQ_TRY(run_small_tables(h, P.nts, prefix, 0, nullptr, nullptr, w.bounds, false, B.yts, B.live, nlive, true,
+                           w.slot_query));
+  ev_rec(h, 2);
+  return DPQ_OK;
+}
+
+// Per-query score histograms (B.hist_q) of every stride-th row of the live
+// slots' lists (stride 1: exact).
+static int ivf_sample_hist(Index* h, int nb, int64_t stride) {
+  Workspace& w = h->ws;
+  IvfBuffers& B = ivf_bufs(h);
+  IvfPlan& P = B.plan;
+  DPQ_CUDA(cudaMemsetAsync(w.hist, 0, (size_t)P.nts * 256 * 4, h->stream));
+  DPQ_CUDA(cudaMemsetAsync(B.hist_q, 0, (size_t)nb * 256 * 4, h->stream));
+  if (P.nts == 0) return DPQ_OK;
+  std::vector<int64_t> ns(P.ntiles);
+  int64_t mx = 0;
+  for (int t = 0; t < P.ntiles; ++t) {
+    const int64_t len = h->h_offsets[P.tile_cell[t] + 1] - h->h_offsets[P.tile_cell[t]];
+    ns[t] = (len + stride - 1) / stride;
+    mx = std::max(mx, ns[t]);
+  }
+  DPQ_TRY(h2d(B.tile_nsamp, ns, h->stream));
+  DPQ_TRY(build_lut(h, P.nts, nullptr, nullptr, w.slot_query));  // histograms need unclamped entries
+  DPQ_TRY(launch_hist(h, P.ntiles, nullptr, stride, mx, h->plane, B.tile_row0, B.tile_nsamp));
+  k_slot_hist_to_query<<<(unsigned)(((int64_t)P.live.size() * 256 + 255) / 256), 256, 0, h->stream>>>(
+      w.hist, w.slot_query, B.live, (int)P.live.size(), B.hist_q);
+  DPQ_LAUNCHED(h);
+  return DPQ_OK;
+}
+
+// Guards from B.hist_q (sampled: per-query lambda in B.lambda; exact: r2),
+// then the clamped LUT tiles.  only: recompute the flagged queries only.
+static int ivf_set_guards(Index* h, int nb, int r2, bool exact, const uint8_t* only) {
+  Workspace& w = h->ws;
+  IvfBuffers& B = ivf_bufs(h);
+  IvfPlan& P = B.plan;
+  k_guard<<<(nb + 127) / 128, 128, 0, h->stream>>>(B.hist_q, nb, r2, 0.0, exact ? 1 : 0, only, B.guard_q, B.gword_q,
+                                                    exact ? nullptr : B.lambda);
+  DPQ_LAUNCHED(h);
+  if (P.nts == 0) return DPQ_OK;
+  k_expand_gword<<<(P.nts + 255) / 256, 256, 0, h->stream>>>(B.gword_q, w.slot_query, P.nts, w.gword);
+  DPQ_LAUNCHED(h);
+  DPQ_TRY(build_lut(h, P.nts, w.gword, nullptr, w.slot_query));
+  return DPQ_OK;
+}
+
+// First-pass scan of the planned units + K3 (hist_out: export the local
+// candidate histogram instead of deciding b*, shard protocol).
+static int ivf_scan(Index* h, int nb, int r2, int32_t* hist_out) {
+  Workspace& w = h->ws;
+  IvfBuffers& B = ivf_bufs(h);
+  IvfPlan& P = B.plan;
+  DPQ_CUDA(cudaMemsetAsync(w.emit_cnt, 0, (size_t)nb * 4, h->stream));
+  if (P.nts > 0) {
+    EmitArgs ea;
+    ea.plane = h->plane; ea.row_begin = 0; ea.row_end = h->n; ea.rows_per_cta = 0;
+    ea.lut = w.lut; ea.gword = w.gword; ea.tile_list = nullptr;
+    ea.slot_query = w.slot_query; ea.slot_probe = w.slot_probe;
+    ea.emit_cnt = w.emit_cnt; ea.emit = w.emit; ea.cap = w.cap;
+    ea.unit_tile = B.unit_tile; ea.unit_r0 = B.unit_r0; ea.unit_r1 = B.unit_r1;
+    ea.n_units = (int)P.unit_tile.size(); ea.units_per_tile = 1;
+    DPQ_TRY(launch_emit(h, ea, P.ntiles, 0));
+  }
+  k_threshold<256><<<nb, 256, 0, h->stream>>>(w.emit, w.emit_cnt, w.cap, B.guard_q, r2, nullptr, w.bstar, w.ncand,
+                                              w.flags, hist_out, h->d_nemit);
+  DPQ_LAUNCHED(h);
+  return DPQ_OK;
+}
+
+// Grow the emit lists to the largest flagged (overflowed) count; 100 = split the batch.
+static int ivf_grow_emit(Index* h, int nb) {
+  Workspace& w = h->ws;
+  DPQ_CUDA(cudaMemcpyAsync(w.h_cnt, w.emit_cnt, (size_t)nb * 4, cudaMemcpyDeviceToHost, h->stream));
+  DPQ_CUDA(cudaStreamSynchronize(h->stream));
+  uint32_t need = 0;
+  for (int q = 0; q < nb; ++q)
+    if (w.h_flags[q] == 2) need = std::max(need, w.h_cnt[q]);
+  if ((size_t)w.qcap_emit * need * 8 > h->emit_budget && nb > 1) return 100;
+  DPQ_TRY(grow_emit(h, need));
+  return DPQ_OK;
+}
+
+// One IVF batch: raw queries in ws.y (nb x d).  res_rot / cells_in are host
+// arrays for the OPQ path (residuals rotated by the caller), else NULL.
+static int ivf_batch(Index* h, int nb, int r, int ma, int r2, bool derived, const float* res_rot,
+                     const int64_t* cells_in) {
+  Workspace& w = h->ws;
+  IvfBuffers& B = ivf_bufs(h);
+  const int d = h->d;
+  const int qt = qt_of(h->mpad);
+  ev_rec(h, 0);
+  IvfPlan& P = B.plan;  // persistent: vectors keep their capacity (no re-faulting per batch)
+  DPQ_TRY(ivf_probe_residuals(h, nb, ma, res_rot, cells_in));
   if (!derived) {
     IvfConvArgs a;
     a.cells = B.cells; a.offsets = h->offsets; a.ma = ma;
@@ -640,102 +843,17 @@ static int ivf_batch(Index* h, int nb, int r, int ma, int r2, bool derived, cons
   auto now = []() { return std::chrono::duration<double, std::micro>(
                         std::chrono::steady_clock::now().time_since_epoch()).count(); };
   const double t_plan0 = trace ? now() : 0.0;
-  try {
-    ivf_plan(h, P, nb, ma, r2);
-  } catch (const std::bad_alloc&) {
-    set_error("ivf plan: pinned host allocation failed");
-    return DPQ_ERR_NOMEM;
-  }
+  bool empty = false;
+  DPQ_TRY(ivf_derived_setup(h, nb, r, ma, r2, &empty));
   const double t_plan1 = trace ? now() : 0.0;
-  if (h->ws.cap == 0 && h->cap0 == 0) {
-    // first emit capacity per query from the probed rows (a query emits ~r2
-    // to a few r2 rows; growth covers outliers): avg probed / 256, pow2
-    int64_t probed = 0;
-    for (int q = 0; q < nb; ++q)
-      for (int p = 0; p < ma; ++p) {
-        const int64_t c = P.cells[(size_t)q * ma + p];
-        probed += h->h_offsets[c + 1] - h->h_offsets[c];
-      }
-    int64_t c = std::max<int64_t>(16384, std::min<int64_t>(probed / std::max(nb, 1) / 256, (int64_t)1 << 20));
-    int64_t p2 = 1;
-    while (p2 < c) p2 <<= 1;
-    h->cap0 = p2;
-  }
-  DPQ_TRY(ensure_ws(h, std::max(P.nts, 1), r, d, nb));
-  DPQ_TRY(ivf_ensure(h, nb, ma, std::max(P.nts, 1), std::max(P.ntiles, 1), std::max((int)P.unit_tile.size(), 1)));
-  DPQ_TRY(h2d(w.slot_query, P.slot_query, h->stream));
-  DPQ_TRY(h2d(w.slot_probe, P.slot_probe, h->stream));
-  DPQ_TRY(h2d(w.slot_pre_off, P.pre_off, h->stream));
-  DPQ_TRY(h2d(w.slot_pre_len, P.pre_len, h->stream));
-  DPQ_TRY(h2d(B.bound_ts, P.bound_ts, h->stream));
-  DPQ_TRY(h2d(B.lambda, P.lambda, h->stream));
-  DPQ_TRY(h2d(B.tile_row0, P.tile_row0, h->stream));
-  DPQ_TRY(h2d(B.tile_nsamp, P.tile_nsamp, h->stream));
-  DPQ_TRY(h2d(B.unit_tile, P.unit_tile, h->stream));
-  DPQ_TRY(h2d(B.unit_r0, P.unit_r0, h->stream));
-  DPQ_TRY(h2d(B.unit_r1, P.unit_r1, h->stream));
-  DPQ_CUDA(cudaMemsetAsync(w.emit_cnt, 0, (size_t)nb * 4, h->stream));
-  if (P.nts == 0) {  // every probed list is empty: empty results (ivf.py:230-233)
+  if (empty) {  // every probed list is empty: empty results (ivf.py:230-233)
     DPQ_CUDA(cudaMemsetAsync(w.bstar, 0xFF, (size_t)nb * 4, h->stream));
   } else {
-    const int nlive = (int)P.live.size(), nbsrc = (int)P.bsrc.size();
-    DPQ_TRY(h2d(B.live, P.live, h->stream));
-    DPQ_TRY(h2d(B.bsrc, P.bsrc, h->stream));
-    const int64_t tot = (int64_t)nlive * d;
-    k_gather_slots<<<(unsigned)((tot + 255) / 256), 256, 0, h->stream>>>(B.ynat, w.slot_query, w.slot_probe, ma, d,
-                                                                        nlive, B.live, B.yts);
-    DPQ_LAUNCHED(h);
-    // K1 pass A: qmin/qmax of the bound-source slots only (their tables are
-    // recomputed in pass B; padding slots are never computed)
-    DPQ_TRY(run_small_tables(h, P.nts, h->codes, 0, w.slot_pre_off, w.slot_pre_len, nullptr, false, B.yts,
-                             B.bsrc, nbsrc, false));
-    k_slot_bounds<<<(P.nts + 255) / 256, 256, 0, h->stream>>>(w.qmin, w.qmax, B.bound_ts, w.slot_query, P.nts,
-                                                              w.bounds);
-    DPQ_LAUNCHED(h);
-    // K1 pass B: quantize every slot with its query's bounds -> LUT tiles
-    DPQ_TRY(run_small_tables(h, P.nts, h->codes, 0, nullptr, nullptr, w.bounds, false, B.yts, B.live, nlive, true,
-                             w.slot_query));
-    ev_rec(h, 2);
-    // guard per query from per-list sampled histograms
-    auto make_guards = [&](int64_t stride, bool exact, const uint8_t* only) -> int {
-      DPQ_CUDA(cudaMemsetAsync(w.hist, 0, (size_t)P.nts * 256 * 4, h->stream));
-      DPQ_CUDA(cudaMemsetAsync(B.hist_q, 0, (size_t)nb * 256 * 4, h->stream));
-      std::vector<int64_t> ns(P.ntiles);
-      int64_t mx = 0;
-      for (int t = 0; t < P.ntiles; ++t) {
-        const int64_t len = h->h_offsets[P.tile_cell[t] + 1] - h->h_offsets[P.tile_cell[t]];
-        ns[t] = (len + stride - 1) / stride;
-        mx = std::max(mx, ns[t]);
-      }
-      DPQ_TRY(h2d(B.tile_nsamp, ns, h->stream));
-      DPQ_TRY(build_lut(h, P.nts, nullptr, nullptr, w.slot_query));  // histograms need unclamped entries
-      DPQ_TRY(launch_hist(h, P.ntiles, nullptr, stride, mx, h->plane, B.tile_row0, B.tile_nsamp));
-      k_slot_hist_to_query<<<(unsigned)(((int64_t)P.live.size() * 256 + 255) / 256), 256, 0, h->stream>>>(
-          w.hist, w.slot_query, B.live, (int)P.live.size(), B.hist_q);
-      DPQ_LAUNCHED(h);
-      k_guard<<<(nb + 127) / 128, 128, 0, h->stream>>>(B.hist_q, nb, r2, 0.0, exact ? 1 : 0, only, B.guard_q,
-                                                        B.gword_q, exact ? nullptr : B.lambda);
-      DPQ_LAUNCHED(h);
-      k_expand_gword<<<(P.nts + 255) / 256, 256, 0, h->stream>>>(B.gword_q, w.slot_query, P.nts, w.gword);
-      DPQ_LAUNCHED(h);
-      DPQ_TRY(build_lut(h, P.nts, w.gword, nullptr, w.slot_query));
-      return DPQ_OK;
-    };
-    DPQ_TRY(make_guards(P.stride, P.stride == 1, nullptr));
+    DPQ_TRY(ivf_sample_hist(h, nb, P.stride));
+    DPQ_TRY(ivf_set_guards(h, nb, r2, P.stride == 1, nullptr));
     ev_rec(h, 3);
     for (int attempt = 0; attempt < 8; ++attempt) {
-      DPQ_CUDA(cudaMemsetAsync(w.emit_cnt, 0, (size_t)nb * 4, h->stream));
-      EmitArgs ea;
-      ea.plane = h->plane; ea.row_begin = 0; ea.row_end = h->n; ea.rows_per_cta = 0;
-      ea.lut = w.lut; ea.gword = w.gword; ea.tile_list = nullptr;
-      ea.slot_query = w.slot_query; ea.slot_probe = w.slot_probe;
-      ea.emit_cnt = w.emit_cnt; ea.emit = w.emit; ea.cap = w.cap;
-      ea.unit_tile = B.unit_tile; ea.unit_r0 = B.unit_r0; ea.unit_r1 = B.unit_r1;
-      ea.n_units = (int)P.unit_tile.size(); ea.units_per_tile = 1;
-      DPQ_TRY(launch_emit(h, ea, P.ntiles, 0));
-      k_threshold<256><<<nb, 256, 0, h->stream>>>(w.emit, w.emit_cnt, w.cap, B.guard_q, r2, nullptr, w.bstar,
-                                                  w.ncand, w.flags, nullptr, h->d_nemit);
-      DPQ_LAUNCHED(h);
+      DPQ_TRY(ivf_scan(h, nb, r2, nullptr));
       DPQ_CUDA(cudaMemcpyAsync(w.h_flags, w.flags, nb, cudaMemcpyDeviceToHost, h->stream));
       DPQ_CUDA(cudaStreamSynchronize(h->stream));
       bool any_exact = false, any_over = false;
@@ -747,18 +865,14 @@ static int ivf_batch(Index* h, int nb, int r, int ma, int r2, bool derived, cons
       if (attempt == 7) { set_error("ivf first pass did not converge"); return DPQ_ERR_CUDA; }
       h->counters[4]++;
       if (any_over) {
-        DPQ_CUDA(cudaMemcpyAsync(w.h_cnt, w.emit_cnt, (size_t)nb * 4, cudaMemcpyDeviceToHost, h->stream));
-        DPQ_CUDA(cudaStreamSynchronize(h->stream));
-        uint32_t need = 0;
-        for (int q = 0; q < nb; ++q)
-          if (w.h_flags[q] == 2) need = std::max(need, w.h_cnt[q]);
-        if ((size_t)w.qcap_emit * need * 8 > h->emit_budget && nb > 1) return 100;
-        DPQ_TRY(grow_emit(h, need));
+        const int rc = ivf_grow_emit(h, nb);
+        if (rc != DPQ_OK) return rc;
       }
       if (any_exact) {
         for (int q = 0; q < nb; ++q) w.h_flags[q] = w.h_flags[q] == 1;
         DPQ_CUDA(cudaMemcpyAsync(w.only, w.h_flags, nb, cudaMemcpyHostToDevice, h->stream));
-        DPQ_TRY(make_guards(1, true, w.only));
+        DPQ_TRY(ivf_sample_hist(h, nb, 1));
+        DPQ_TRY(ivf_set_guards(h, nb, r2, true, w.only));
       }
     }
   }
@@ -935,6 +1049,139 @@ int dpq_ivf_search_conventional(dpq_index_t* index, const float* y, int64_t nq, 
   if (ma < 1 || ma > h->n_cells) { set_error("ma out of range"); return DPQ_ERR_ARG; }
   cudaSetDevice(h->device);
   return ivf_driver(h, y, nq, r, ma, 1, false, res_rot, cells, dists, ids, phase_us);
+}
+
+// ------------------------------------------------- ivf list-split shards --
+int dpq_ivf_set_shard(dpq_index_t* index, const int64_t* global_offsets, const void* prefix_codes,
+                      const int64_t* prefix_offsets, int64_t prefix_rows) {
+  Index* h = reinterpret_cast<Index*>(index);
+  if (!h || h->kind != KIND_IVF) { set_error("not an ivf index"); return DPQ_ERR_STATE; }
+  if (!global_offsets || !prefix_offsets || prefix_rows < 1) { set_error("bad shard arguments"); return DPQ_ERR_ARG; }
+  const int K = h->n_cells;
+  if (global_offsets[0] != 0 || prefix_offsets[0] != 0) { set_error("offsets must start at 0"); return DPQ_ERR_ARG; }
+  for (int c = 0; c < K; ++c) {
+    const int64_t glen = global_offsets[c + 1] - global_offsets[c], llen = h->h_offsets[c + 1] - h->h_offsets[c];
+    const int64_t plen = prefix_offsets[c + 1] - prefix_offsets[c];
+    if (glen < llen || plen != std::min(glen, prefix_rows)) {
+      set_error("shard lists inconsistent with the global lists / prefixes at cell " + std::to_string(c));
+      return DPQ_ERR_ARG;
+    }
+  }
+  cudaSetDevice(h->device);
+  const int64_t rows = prefix_offsets[K];
+  const size_t bytes = (size_t)std::max<int64_t>(rows, 1) * h->m * h->code_bytes;
+  if (h->g_prefix) { cudaFree(h->g_prefix); h->g_prefix = nullptr; }
+  DPQ_TRY(dmalloc((uint8_t**)&h->g_prefix, bytes));
+  if (rows > 0 && !prefix_codes) { set_error("null prefix codes"); return DPQ_ERR_ARG; }
+  if (rows > 0) DPQ_CUDA(cudaMemcpy(h->g_prefix, prefix_codes, (size_t)rows * h->m * h->code_bytes,
+                                    cudaMemcpyHostToDevice));
+  h->g_offsets.assign(global_offsets, global_offsets + K + 1);
+  h->g_pre_off.assign(prefix_offsets, prefix_offsets + K + 1);
+  h->g_pre_rows = prefix_rows;
+  h->ivf_shard = true;
+  return DPQ_OK;
+}
+
+int dpq_ivf_shard_begin(dpq_index_t* index, const float* y, int64_t nq, int ma, int r2, int exact,
+                        const float* res_rot, const int64_t* cells, int32_t* sample_hist, int64_t* n_sampled,
+                        int64_t* n_rows) {
+  Index* h = reinterpret_cast<Index*>(index);
+  if (!h || h->kind != KIND_IVF || !h->ivf_shard) { set_error("not an ivf shard (dpq_ivf_set_shard)"); return DPQ_ERR_STATE; }
+  if (nq < 1 || nq > (1 << 20) || r2 < 1 || !y || !sample_hist || !n_sampled || !n_rows || (res_rot && !cells)) {
+    set_error("bad ivf_shard_begin arguments"); return DPQ_ERR_ARG;
+  }
+  if (ma < 1 || ma > h->n_cells) { set_error("ma out of range"); return DPQ_ERR_ARG; }
+  if (r2 > h->g_pre_rows) {
+    set_error("r2 = " + std::to_string(r2) + " exceeds the replicated list prefixes (" + std::to_string(h->g_pre_rows) +
+              " rows)");
+    return DPQ_ERR_ARG;
+  }
+  cudaSetDevice(h->device);
+  const int nb = (int)nq;
+  DPQ_TRY(ensure_ws(h, nb, 1, h->d, nb));
+  DPQ_CUDA(cudaMemcpyAsync(h->ws.y, y, (size_t)nb * h->d * 4, cudaMemcpyHostToDevice, h->stream));
+  DPQ_TRY(ivf_probe_residuals(h, nb, ma, res_rot, cells));
+  bool empty = false;
+  DPQ_TRY(ivf_derived_setup(h, nb, 1, ma, r2, &empty));
+  IvfBuffers& B = ivf_bufs(h);
+  IvfPlan& P = B.plan;
+  const int64_t stride = exact ? 1 : P.stride;
+  DPQ_TRY(ivf_sample_hist(h, nb, stride));
+  DPQ_CUDA(cudaMemcpyAsync(sample_hist, B.hist_q, (size_t)nb * 256 * 4, cudaMemcpyDeviceToHost, h->stream));
+  DPQ_CUDA(cudaStreamSynchronize(h->stream));
+  for (int q = 0; q < nb; ++q) {
+    n_sampled[q] = stride > 1 ? P.sq[q] : P.nr[q];
+    n_rows[q] = P.nr_global[q];
+  }
+  h->shard_nq = nb;
+  h->shard_ma = ma;
+  h->shard_stride = stride;
+  return DPQ_OK;
+}
+
+int dpq_ivf_shard_scan(dpq_index_t* index, const int32_t* sample_hist_sum, const int64_t* sampled_sum,
+                       const int64_t* rows_sum, int r2, int32_t* cand_hist) {
+  Index* h = reinterpret_cast<Index*>(index);
+  if (!h || h->kind != KIND_IVF || !h->ivf_shard || h->shard_nq < 1) { set_error("ivf_shard_begin first"); return DPQ_ERR_STATE; }
+  if (!sample_hist_sum || !sampled_sum || !rows_sum || !cand_hist) { set_error("null argument"); return DPQ_ERR_ARG; }
+  cudaSetDevice(h->device);
+  const int nb = h->shard_nq;
+  Workspace& w = h->ws;
+  IvfBuffers& B = ivf_bufs(h);
+  DPQ_CUDA(cudaMemcpyAsync(B.hist_q, sample_hist_sum, (size_t)nb * 256 * 4, cudaMemcpyHostToDevice, h->stream));
+  const bool exact = h->shard_stride == 1;
+  std::vector<double> lam(nb, -1.0);  // (exact histograms: lambda < 0)
+  if (!exact)
+    for (int q = 0; q < nb; ++q)
+      lam[q] = rows_sum[q] > 0 ? (double)r2 * (double)sampled_sum[q] / (double)rows_sum[q] : -1.0;
+  DPQ_CUDA(cudaMemcpyAsync(B.lambda, lam.data(), (size_t)nb * 8, cudaMemcpyHostToDevice, h->stream));
+  DPQ_TRY(ivf_set_guards(h, nb, r2, exact, nullptr));
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    DPQ_TRY(ivf_scan(h, nb, r2, w.hist_i));
+    DPQ_CUDA(cudaMemcpyAsync(w.h_flags, w.flags, nb, cudaMemcpyDeviceToHost, h->stream));
+    DPQ_CUDA(cudaStreamSynchronize(h->stream));
+    bool over = false;
+    for (int q = 0; q < nb; ++q) over |= w.h_flags[q] == 2;
+    if (!over) {
+      DPQ_CUDA(cudaMemcpy(cand_hist, w.hist_i, (size_t)nb * 256 * 4, cudaMemcpyDeviceToHost));
+      return DPQ_OK;
+    }
+    const int rc = ivf_grow_emit(h, nb);
+    if (rc == 100) { set_error("ivf shard scan: emit budget exceeded, use a smaller batch"); return DPQ_ERR_NOMEM; }
+    if (rc != DPQ_OK) return rc;
+  }
+  set_error("ivf shard scan: emit buffer did not converge");
+  return DPQ_ERR_NOMEM;
+}
+
+int dpq_ivf_shard_finish(dpq_index_t* index, const int32_t* cand_hist_sum, int r, int r2, double* dists,
+                         int64_t* ids, uint8_t* need_exact) {
+  Index* h = reinterpret_cast<Index*>(index);
+  if (!h || h->kind != KIND_IVF || !h->ivf_shard || h->shard_nq < 1) { set_error("ivf_shard_begin first"); return DPQ_ERR_STATE; }
+  if (r < 1 || r > r2 || !cand_hist_sum || !dists || !ids || !need_exact) { set_error("bad arguments"); return DPQ_ERR_ARG; }
+  cudaSetDevice(h->device);
+  const int nb = h->shard_nq, ma = h->shard_ma;
+  DPQ_TRY(ensure_ws(h, std::max(ivf_bufs(h).plan.nts + ivf_bufs(h).plan.nph, 1), r, h->d, nb));
+  Workspace& w = h->ws;
+  IvfBuffers& B = ivf_bufs(h);
+  DPQ_CUDA(cudaMemcpyAsync(w.hist_i, cand_hist_sum, (size_t)nb * 256 * 4, cudaMemcpyHostToDevice, h->stream));
+  k_bstar_from_hist<<<(nb + 127) / 128, 128, 0, h->stream>>>(w.hist_i, B.guard_q, nb, r2, w.bstar, w.ncand, w.flags);
+  DPQ_LAUNCHED(h);
+  RefineArgs ra = make_refine_args(h, r);
+  ra.y = B.ynat;
+  ra.ystride = ma * h->d;
+  ra.row_ids = h->sorted_ids;  // global ids
+  ra.id_base = 0;
+  DPQ_TRY(launch_refine<MODE_EMIT>(h, ra, nb));
+  DPQ_CUDA(cudaMemcpyAsync(w.h_d, w.out_d, (size_t)nb * r * 8, cudaMemcpyDeviceToHost, h->stream));
+  DPQ_CUDA(cudaMemcpyAsync(w.h_i, w.out_i, (size_t)nb * r * 8, cudaMemcpyDeviceToHost, h->stream));
+  DPQ_CUDA(cudaMemcpyAsync(need_exact, w.flags, nb, cudaMemcpyDeviceToHost, h->stream));
+  DPQ_CUDA(cudaStreamSynchronize(h->stream));
+  memcpy(dists, w.h_d, (size_t)nb * r * 8);
+  memcpy(ids, w.h_i, (size_t)nb * r * 8);
+  for (int q = 0; q < nb; ++q) need_exact[q] = need_exact[q] != 0;
+  h->counters[1] += nb;
+  return DPQ_OK;
 }
 
 int dpq_shard_begin(dpq_index_t* index, const float* yr, int64_t nq, int r2, int64_t n_global, int exact,

@@ -283,3 +283,148 @@ class ShardedFlatIndex:
                 out_i[s:s + self.batch] = i.cpu().numpy()
         return out_d, out_i
 
+
+
+# --------------------------------------------------------------- IVF --------
+
+def split_lists(offsets, sorted_codes, sorted_ids, rank: int, world: int):
+    """This shard's slice of every inverted list (each list cut
+    evenly across the shards, cell order kept): local offsets (K+1), codes,
+    GLOBAL ids."""
+    offsets = np.asarray(offsets, dtype=np.int64)
+    lens = np.diff(offsets)
+    lo = offsets[:-1] + lens * rank // world
+    hi = offsets[:-1] + lens * (rank + 1) // world
+    loc = np.zeros_like(offsets)
+    loc[1:] = np.cumsum(hi - lo)
+    rows = np.concatenate([np.arange(a, b, dtype=np.int64) for a, b in zip(lo, hi)]) if len(lo) else \
+        np.empty(0, np.int64)
+    return loc, np.ascontiguousarray(np.asarray(sorted_codes)[rows]), np.ascontiguousarray(
+        np.asarray(sorted_ids)[rows])
+
+
+def list_prefixes(offsets, sorted_codes, rows: int):
+    """First min(rows, len) rows of every global list, concatenated, with
+    their row offsets (the replicated qmax prefixes, ivf.py:205-217)."""
+    offsets = np.asarray(offsets, dtype=np.int64)
+    take = np.minimum(np.diff(offsets), rows)
+    pre_off = np.zeros_like(offsets)
+    pre_off[1:] = np.cumsum(take)
+    idx = np.concatenate([np.arange(o, o + t, dtype=np.int64) for o, t in zip(offsets[:-1], take)]) if len(take) \
+        else np.empty(0, np.int64)
+    return np.ascontiguousarray(np.asarray(sorted_codes)[idx]), pre_off
+
+
+class GpuIvfShardEngine:
+    """One list-split IVF shard on one GPU (dpq_ivf_set_shard)."""
+
+    def __init__(self, codebooks, derived, centers, offsets, sorted_codes, sorted_ids, rank: int, world: int,
+                 prefix_rows: int = 4096, device: int = 0):
+        loc, codes, ids = split_lists(offsets, sorted_codes, sorted_ids, rank, world)
+        self.handle = _lib.ivf_create(codebooks, derived, centers, loc, codes, ids, device=device)
+        cb = _lib.code_bytes_of(np.asarray(sorted_codes))
+        pre, pre_off = list_prefixes(offsets, sorted_codes, prefix_rows)
+        pre = np.ascontiguousarray(pre, dtype=np.uint8 if cb == 1 else np.uint16)
+        g_off = np.ascontiguousarray(offsets, dtype=np.int64)
+        _lib.check(_lib.lib().dpq_ivf_set_shard(self.handle.raw, _lib.ptr(g_off), _lib.ptr(pre), _lib.ptr(pre_off),
+                                                int(prefix_rows)), "ivf_set_shard")
+        self.n_local = int(ids.shape[0])
+
+    def probe(self, Y: np.ndarray, ma: int) -> np.ndarray:
+        cells = np.empty((Y.shape[0], ma), np.int64)
+        _lib.check(_lib.lib().dpq_ivf_probe(self.handle.raw, _lib.ptr(Y), Y.shape[0], int(ma), _lib.ptr(cells)),
+                   "ivf_probe")
+        return cells
+
+    def begin(self, Y, ma, r2, exact, res_rot=None, cells=None):
+        nq = Y.shape[0]
+        hist = np.zeros((nq, 256), np.int32)
+        ns = np.zeros(nq, np.int64)
+        nr = np.zeros(nq, np.int64)
+        _lib.check(_lib.lib().dpq_ivf_shard_begin(self.handle.raw, _lib.ptr(Y), nq, int(ma), int(r2), int(bool(exact)),
+                                                  _lib.ptr(res_rot), _lib.ptr(cells), _lib.ptr(hist), _lib.ptr(ns),
+                                                  _lib.ptr(nr)), "ivf_shard_begin")
+        return hist, ns, nr
+
+    def scan(self, hist_sum, ns_sum, nr, r2):
+        hist_sum = np.ascontiguousarray(hist_sum, dtype=np.int32)
+        ns_sum = np.ascontiguousarray(ns_sum, dtype=np.int64)
+        nr = np.ascontiguousarray(nr, dtype=np.int64)
+        cand = np.zeros_like(hist_sum)
+        _lib.check(_lib.lib().dpq_ivf_shard_scan(self.handle.raw, _lib.ptr(hist_sum), _lib.ptr(ns_sum), _lib.ptr(nr),
+                                                 int(r2), _lib.ptr(cand)), "ivf_shard_scan")
+        return cand
+
+    def finish(self, cand_sum, r, r2):
+        cand_sum = np.ascontiguousarray(cand_sum, dtype=np.int32)
+        nq = cand_sum.shape[0]
+        d = np.empty((nq, r), np.float64)
+        i = np.empty((nq, r), np.int64)
+        need = np.zeros(nq, np.uint8)
+        _lib.check(_lib.lib().dpq_ivf_shard_finish(self.handle.raw, _lib.ptr(cand_sum), int(r), int(r2), _lib.ptr(d),
+                                                   _lib.ptr(i), _lib.ptr(need)), "ivf_shard_finish")
+        return d, i, need.astype(bool)
+
+
+def sharded_ivf_search(engine, comm, Y: np.ndarray, r: int, ma: int, r2: int, res_rot=None, cells=None):
+    """IVFIndex.search(mode="derived") over list-split shards (ivf.py:195-277):
+    one candidate pool per query across the probed lists of every shard,
+    refine in each candidate's own cell frame, merge by (dist, id)."""
+    if r > r2:
+        raise ValueError(f"r={r} must not exceed r2={r2}")
+    Y = np.ascontiguousarray(Y, dtype=np.float32)
+    exact = False
+    for _ in range(2):
+        hist, ns, nr = engine.begin(Y, ma, r2, exact, res_rot, cells)
+        hist_sum = comm.allreduce_sum(hist)
+        ns_sum = comm.allreduce_sum(ns)
+        cand = engine.scan(hist_sum, ns_sum, nr, r2)
+        cand_sum = comm.allreduce_sum(cand)
+        d, i, need = engine.finish(cand_sum, r, r2)
+        if not comm.allreduce_max(int(need.any())):
+            break
+        exact = True  # a guard proved too tight on some query: redo with exact histograms
+    return merge_topr(comm.allgather(d), comm.allgather(i), r)
+
+
+class ShardedIVFIndex:
+    """IVFIndex.search(mode="derived") over an IVF index whose every list is
+    split across ranks.  Each rank constructs it from the same global arrays
+    (it keeps only its slices); `search` is collective and returns the global
+    result on every rank."""
+
+    def __init__(self, quantizer, centers, offsets, sorted_codes, sorted_ids, rank: int, world: int, comm=None,
+                 prefix_rows: int = 4096, device: int = 0, batch: int = 4096):
+        self.quantizer = quantizer
+        self.centers_ = np.ascontiguousarray(centers, dtype=np.float32)
+        self.comm = comm if comm is not None else TorchComm()
+        self.batch = int(batch)
+        self.engine = GpuIvfShardEngine(quantizer.codebooks_, quantizer.derived_codebooks_, self.centers_, offsets,
+                                        sorted_codes, sorted_ids, rank, world, prefix_rows=prefix_rows, device=device)
+
+    def search(self, Y, r: int, ma: int = 8, mode: str = "derived", r2=None):
+        if mode != "derived":
+            raise ValueError("ShardedIVFIndex supports mode='derived'")
+        if r2 is None:
+            raise ValueError("derived mode requires r2")
+        Y = _lib.query_array(Y)
+        if not (1 <= ma <= self.centers_.shape[0]):
+            raise ValueError(f"ma must be in [1, {self.centers_.shape[0]}], got {ma}")
+        out_d, out_i = [], []
+        for s in range(0, Y.shape[0], self.batch):
+            Yb = np.ascontiguousarray(Y[s:s + self.batch])
+            res_rot = cells = None
+            if getattr(self.quantizer, "rotation_", None) is not None:  # OPQ: (ma, d) rotate per query (ivf.py:202)
+                cells = self.engine.probe(Yb, ma)
+                res = (Yb[:, None, :] - self.centers_[cells]).reshape(-1, Yb.shape[1])
+                rot = _lib.rotate_rows(self.quantizer, res, ma)
+                if rot is None:
+                    rot = np.concatenate([np.asarray(self.quantizer.rotate(res[q * ma:(q + 1) * ma]), np.float32)
+                                          for q in range(Yb.shape[0])])
+                res_rot = np.ascontiguousarray(rot, dtype=np.float32)
+            d, i = sharded_ivf_search(self.engine, self.comm, Yb, r, ma, r2, res_rot, cells)
+            out_d.append(d)
+            out_i.append(i)
+        if not out_d:
+            return np.full((0, r), np.inf), np.full((0, r), -1, dtype=np.int64)
+        return np.concatenate(out_d), np.concatenate(out_i)

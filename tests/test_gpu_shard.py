@@ -180,3 +180,80 @@ def test_sharded_flat_index_nccl_world1():
         assert np.array_equal(d.view(np.uint64), d1.view(np.uint64))
     finally:
         dist.destroy_process_group()
+
+
+def _run_ivf_shards(g, Y, r, ma, r2, world, prefix_rows=4096, rotation=None):
+    from paper_1905_06900_b200.flat import ArrayQuantizer
+    from paper_1905_06900_b200.shard import ShardedIVFIndex
+
+    comm = ThreadComm(world)
+    out = [None] * world
+    errs = []
+    q = ArrayQuantizer(g["codebooks"], g["derived"], rotation)
+    idxs = [ShardedIVFIndex(q, g["centers"], g["offsets"], g["sorted_codes"], g["sorted_ids"], rk, world, comm=comm,
+                            prefix_rows=prefix_rows, device=0) for rk in range(world)]
+
+    def go(rank):
+        try:
+            comm.bind(rank)
+            out[rank] = idxs[rank].search(Y, r, ma=ma, r2=r2)
+        except Exception as exc:  # pragma: no cover
+            errs.append(exc)
+            comm.bar.abort()
+
+    ts = [threading.Thread(target=go, args=(rk,)) for rk in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    if errs:
+        raise errs[0]
+    return out
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("name", ["ivf_blobs", "ivf_opq"])
+def test_ivf_list_split_shards_equal_reference(name, world):
+    """IVF list-split sharding on the golden fixtures: every
+    rank returns the reference's own IVFIndex.search result."""
+    from conftest import load_golden
+
+    g = load_golden(name)
+    m = g["meta"]
+    for d, i in _run_ivf_shards(g, g["queries"], m["r"], m["ma"], m["r2"], world, rotation=g.get("rotation")):
+        assert np.array_equal(i, g["exp_derived_i"])
+        assert np.array_equal(d.view(np.uint64), g["exp_derived_d"].view(np.uint64))
+
+
+@pytest.mark.parametrize("env", [{}, {"DPQ_EXACT_LIMIT": "0", "DPQ_GUARD_SAMPLE": "8"}])
+def test_ivf_list_split_random_equals_unsharded(env, monkeypatch):
+    """Random IVF model with short and empty lists (some lists empty on some
+    shards, so bound sources live on other shards) and a sampled-guard
+    variant that forces the exact redo."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    from paper_1905_06900_b200.ivf import IVFIndex
+
+    rng = np.random.default_rng(21)
+    m, k, kbar, dsub, K, n = 4, 256, 16, 4, 24, 6000
+    cb = (rng.normal(size=(m, k, dsub)) * 2).astype(np.float32)
+    der = np.stack([np.stack([cb[j][np.arange(k) % kbar == g].mean(axis=0) for g in range(kbar)])
+                    for j in range(m)]).astype(np.float32)
+    centers = rng.normal(size=(K, m * dsub)).astype(np.float32) * 3
+    sizes = rng.integers(0, 600, size=K)
+    sizes[[2, 5, 11]] = [0, 1, 2]  # empty and tiny lists
+    sizes = (sizes * n / max(1, sizes.sum())).astype(np.int64)
+    offsets = np.zeros(K + 1, np.int64)
+    offsets[1:] = np.cumsum(sizes)
+    N = int(offsets[-1])
+    g = {"codebooks": cb, "derived": der, "centers": centers, "offsets": offsets,
+         "sorted_codes": rng.integers(0, k, size=(N, m)).astype(np.uint8),
+         "sorted_ids": rng.permutation(N).astype(np.int64)}
+    Y = (centers[rng.integers(K, size=40)] + rng.normal(size=(40, m * dsub))).astype(np.float32)
+    r, ma, r2 = 15, 6, 300
+    d0, i0 = IVFIndex.from_arrays(cb, der, centers, offsets, g["sorted_codes"], g["sorted_ids"]).search(
+        Y, r, ma=ma, mode="derived", r2=r2)
+    for world in (2, 4):
+        for d, i in _run_ivf_shards(g, Y, r, ma, r2, world):
+            assert np.array_equal(i, i0)
+            assert np.array_equal(d.view(np.uint64), d0.view(np.uint64))
