@@ -596,6 +596,8 @@ def init_dist(local):
         dist.init_process_group("nccl", device_id=device)
     else:
         dist.init_process_group("gloo")
+    log(f"[rank {dist.get_rank()}] communicator: backend={dist.get_backend()} nranks={dist.get_world_size()} "
+        f"device={device} nccl={torch.cuda.nccl.version() if nccl else None}")
     return device, local, nccl
 
 
