@@ -287,7 +287,9 @@ int dpq_debug_tc_tables(dpq_index_t* index, const float* yr, int64_t nq,
  * codebooks[j,c]||^2, ties to the lowest index.  Also the IVF coarse
  * assignment (ivf.py:83-101) with m = 1.  The reference's cross term is an
  * f32 BLAS GEMM, so near-ties (equal at f32 rounding) may pick a different
- * minimiser; every other row agrees.  Requires dsub <= 32.
+ * minimiser; every other row agrees.  dsub <= 32: one K = 32 GEMM per
+ * tile; 32 < dsub <= 128 (4 | k): the K-chunked GEMM of the tensor-core
+ * tables (dpq_tctab.cu) with an argmin epilogue.
  *   dpq_encoder_create: codebooks (m,k,dsub) f32 host; the handle owns the
  *     prepared device operand.
  *   dpq_encode:     x (n, m*dsub) f32 host -> codes (n, m) u16 host (k <= 65536).

@@ -431,6 +431,10 @@ struct Encoder {
   int device = 0;
   int m = 0, k = 0, dsub = 0, nt = 0;
   uint8_t* gB = nullptr;
+  // dsub > 32: the K-chunked tensor-core GEMM of dpq_tctab.cu in encoder mode
+  void* tct = nullptr;
+  unsigned long long* scratch = nullptr;
+  int64_t scratch_rows = 0;
   cudaStream_t stream = nullptr;
   int sms = 0;
   // host-path staging
@@ -460,7 +464,6 @@ static int encoder_init(Encoder* e, const float* codebooks) {
   const int m = e->m, k = e->k, dsub = e->dsub;
   ENC_CUDA(cudaDeviceGetAttribute(&e->sms, cudaDevAttrMultiProcessorCount, e->device));
   ENC_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
-  ENC_CUDA(cudaMalloc(&e->gB, (size_t)m * e->nt * dpq::enc::TILE_B));
   float* d_cb = nullptr;
   const size_t cb_bytes = (size_t)m * k * dsub * sizeof(float);
   ENC_CUDA(cudaMalloc(&d_cb, cb_bytes));
@@ -469,6 +472,9 @@ static int encoder_init(Encoder* e, const float* codebooks) {
     ~FreeCb() { cudaFree(p); }
   } free_cb{d_cb};
   ENC_CUDA(cudaMemcpyAsync(d_cb, codebooks, cb_bytes, cudaMemcpyHostToDevice, e->stream));
+  if (dsub > 32)  // K-chunked tensor-core GEMM (dpq_tctab.cu), natural centroid order
+    return dpq::tct_prepare(e->device, d_cb, m, k, 1, dsub, e->stream, &e->tct);
+  ENC_CUDA(cudaMalloc(&e->gB, (size_t)m * e->nt * dpq::enc::TILE_B));
   const int64_t total = (int64_t)m * e->nt * dpq::enc::BN;
   dpq::enc::k_enc_prep<<<(unsigned)((total + 255) / 256), 256, 0, e->stream>>>(d_cb, m, k, dsub, e->nt, e->gB);
   ENC_CUDA(cudaGetLastError());
@@ -483,8 +489,8 @@ int dpq_encoder_create(int device, int m, int k, int dsub, const float* codebook
     dpq::set_error("dpq_encoder_create: invalid arguments");
     return DPQ_ERR_ARG;
   }
-  if (dsub > 32) {
-    dpq::set_error("dpq_encoder_create: dsub > 32 is not supported by the tensor-core encoder yet");
+  if (dsub > 128 || k % 4) {
+    dpq::set_error("dpq_encoder_create: the tensor-core encoder needs dsub <= 128 and 4 | k");
     return DPQ_ERR_ARG;
   }
   *out = nullptr;
@@ -508,6 +514,8 @@ void dpq_encoder_destroy(dpq_encoder_t* enc) {
   cudaSetDevice(e->device);
   if (e->stream) cudaStreamSynchronize(e->stream);
   cudaFree(e->gB);
+  dpq::tct_free(e->tct);
+  cudaFree(e->scratch);
   cudaFree(e->d_x);
   cudaFree(e->d_codes);
   cudaFree(e->d_u16);
@@ -523,6 +531,18 @@ int dpq_encode_dev(dpq_encoder_t* enc, const float* x, int64_t n, int64_t ldx, i
   }
   if (n == 0) return DPQ_OK;
   ENC_CUDA(cudaSetDevice(e->device));
+  cudaStream_t st0 = stream ? reinterpret_cast<cudaStream_t>(stream) : e->stream;
+  if (e->tct) {
+    if (n > e->scratch_rows) {
+      ENC_CUDA(cudaStreamSynchronize(st0));
+      cudaFree(e->scratch);
+      e->scratch = nullptr;
+      e->scratch_rows = 0;
+      ENC_CUDA(cudaMalloc(&e->scratch, (size_t)n * e->m * sizeof(unsigned long long)));
+      e->scratch_rows = n;
+    }
+    return dpq::tct_argmin(e->tct, x, ldx, n, codes, e->scratch, st0);
+  }
   dpq::enc::EncArgs a;
   a.x = x; a.ldx = ldx; a.n = n; a.m = e->m; a.dsub = e->dsub; a.nt = e->nt; a.gB = e->gB; a.codes = codes;
   a.nblk = (n + dpq::enc::RB * dpq::enc::BM - 1) / (dpq::enc::RB * dpq::enc::BM);

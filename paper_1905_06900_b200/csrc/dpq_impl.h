@@ -16,6 +16,8 @@ int tct_prepare(int device, const float* cb, int m, int k, int kbar, int dsub, c
 int tct_build(void* t, const float* y, int64_t ystride, int nq, float* tables, double* eps, double* ny,
               double eps_scale, cudaStream_t stream);
 double tct_gamma(void* t, double eps_scale);
+int tct_argmin(void* t, const float* x, int64_t ldx, int64_t n, int32_t* codes, unsigned long long* scratch,
+               cudaStream_t stream);
 const float* tct_cnorm(void* t);
 void tct_free(void* t);
 

@@ -247,6 +247,8 @@ struct Args {
   float* tables;        // (nq, m, k) group-major
   double* eps;          // (nq, m) entry error bounds (with the subspace's largest ||c'||)
   double* ny;           // (nq, m) ||y'|| (optional: per-entry bounds gamma (||y'|| + ||c'||)^2)
+  unsigned long long* argmin = nullptr;  // encoder mode (kbar = 1 operand): per (row, j) min of
+                                         // (ordered ||c'||^2 - 2 y'.c', c); no tables written
   double gamma;         // error-bound coefficient (see tct_build)
   int ntr, tpr, nqb;    // tile ranges, tiles per range, query blocks
   int64_t units;        // m * ntr * nqb
@@ -397,7 +399,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tct_gemm(Args a) {
             }
           }
           sYn[et] = yn;
-          if (live && t0 == 0) {  // entry error bound of (query, subspace): once per (j, query block)
+          if (live && t0 == 0 && a.eps) {  // entry error bound of (query, subspace): once per (j, query block)
             const double s = sqrt(n2) + a.rmax[j];
             a.eps[gq * a.m + j] = a.gamma * s * s;
             if (a.ny) a.ny[gq * a.m + j] = sqrt(n2);
@@ -420,7 +422,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_tct_gemm(Args a) {
       }
       const int64_t gq = (int64_t)qb * BM + row;
       const float yn = sYn[row];
-      float* out = a.tables + (gq * a.m + j) * (int64_t)a.k;
+      float* out = a.argmin ? nullptr : a.tables + (gq * a.m + j) * (int64_t)a.k;
+      float best = INFINITY;  // encoder mode: running (min, first centroid) of this row's half
+      int bidx = 0;
       for (int t = t0; t < t1; ++t, ++acc_t) {
         const uint32_t buf = (uint32_t)(acc_t & 1), ap = (uint32_t)((acc_t >> 1) & 1);
         bar_wait(&tfull[buf], ap);
@@ -431,6 +435,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_tct_gemm(Args a) {
           float v[32];
           tmem_ld32(base + ch * 32, v);
           const int e0 = t * BN + half * (BN / 2) + ch * 32;
+          if (a.argmin) {  // pad entries (e >= k) carry a 2^100 norm: they never win
+            float mn = v[0];
+#pragma unroll
+            for (int i = 1; i < 32; ++i) mn = fminf(mn, v[i]);
+            if (mn < best) {  // first column holding the chunk minimum (lowest index on ties)
+              int f = 31;
+#pragma unroll
+              for (int i = 31; i >= 0; --i) f = v[i] == mn ? i : f;
+              best = mn;
+              bidx = e0 + f;
+            }
+            continue;
+          }
           if (gq < a.nq && e0 + 32 <= a.k) {
             float4* o = reinterpret_cast<float4*>(out + e0);
 #pragma unroll
@@ -444,6 +461,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_tct_gemm(Args a) {
         tc_before_sync();
         __syncwarp();
         if (lane == 0) bar_arrive(&tempty[buf]);
+      }
+      if (a.argmin && gq < a.nq) {  // (min value, then lowest centroid) across halves, ranges and CTAs
+        uint32_t u = __float_as_uint(best);
+        u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);  // order-preserving float -> u32
+        atomicMin(a.argmin + gq * a.m + j, ((unsigned long long)u << 32) | (unsigned)bidx);
       }
       asm volatile("bar.sync 1, 256;" ::: "memory");  // sYn / sA reuse by the next unit
     }
@@ -567,6 +589,43 @@ int tct_build(void* p, const float* y, int64_t ystride, int nq, float* tables, d
   a.units = base * a.ntr;
   const int grid = (int)std::min<int64_t>(a.units, t->sms);
   tct::k_tct_gemm<<<grid, tct::kThreads, tct::SMEM_BYTES, stream>>>(a);
+  TCT_CUDA(cudaGetLastError());
+  return DPQ_OK;
+}
+
+__global__ void k_tct_codes(const unsigned long long* __restrict__ packed, int64_t n, int32_t* __restrict__ codes) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) codes[i] = (int32_t)(packed[i] & 0xFFFFFFFFull);
+}
+
+// Nearest centroid per (row, subspace) of x (n rows, row stride ldx floats):
+// the tensor-core GEMM in encoder mode (operand prepared with kbar = 1, so
+// entry = centroid index), argmin with ties to the lowest index
+// (clustering.py:53-77).  scratch: n * m u64.
+int tct_argmin(void* p, const float* x, int64_t ldx, int64_t n, int32_t* codes, unsigned long long* scratch,
+               cudaStream_t stream) {
+  TcTables* t = reinterpret_cast<TcTables*>(p);
+  if (!t || t->kbar != 1) { set_error("tensor-core encoder operand not prepared"); return DPQ_ERR_STATE; }
+  if (n <= 0) return DPQ_OK;
+  TCT_CUDA(cudaMemsetAsync(scratch, 0xFF, (size_t)n * t->m * 8, stream));
+  for (int64_t s0 = 0; s0 < n; s0 += (int64_t)1 << 30) {  // (nq is an int)
+    const int nq = (int)std::min<int64_t>(n - s0, (int64_t)1 << 30);
+    tct::Args a;
+    a.y = x + s0 * ldx; a.ystride = ldx; a.nq = nq; a.m = t->m; a.k = t->k; a.dsub = t->dsub; a.kc = t->kc;
+    a.nt = t->nt; a.img = t->img; a.mu = t->mu; a.rmax = t->rmax; a.tables = nullptr; a.eps = nullptr;
+    a.ny = nullptr; a.argmin = scratch + s0 * t->m; a.gamma = 0.0;
+    a.nqb = (nq + tct::BM - 1) / tct::BM;
+    const int64_t base = (int64_t)t->m * a.nqb;
+    a.ntr = (int)std::max<int64_t>(1, std::min<int64_t>(t->nt, (4LL * t->sms + base - 1) / base));
+    a.tpr = (t->nt + a.ntr - 1) / a.ntr;
+    a.ntr = (t->nt + a.tpr - 1) / a.tpr;
+    a.units = base * a.ntr;
+    const int grid = (int)std::min<int64_t>(a.units, t->sms);
+    tct::k_tct_gemm<<<grid, tct::kThreads, tct::SMEM_BYTES, stream>>>(a);
+    TCT_CUDA(cudaGetLastError());
+  }
+  const int64_t tot = n * t->m;
+  k_tct_codes<<<(unsigned)((tot + 255) / 256), 256, 0, stream>>>(scratch, tot, codes);
   TCT_CUDA(cudaGetLastError());
   return DPQ_OK;
 }

@@ -182,7 +182,7 @@ def encode_rows(cfg, codebooks, rotation, centres, seed: int, lo: int, hi: int, 
 
     from . import train
 
-    enc = train.make_encoder(codebooks, device=device, kind=encoder if cfg["dsub"] <= 32 else "torch")
+    enc = train.make_encoder(codebooks, device=device, kind=encoder if cfg["dsub"] <= 128 else "torch")
     rot_t = torch.as_tensor(rotation, device=device) if rotation is not None else None
     codes = np.empty((hi - lo, cfg["m"]), np.uint16)
     for row0, x in row_chunks(cfg, centres, seed, lo, hi, device):

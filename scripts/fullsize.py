@@ -108,7 +108,10 @@ def build(cfg, seed=42, device=None, chunk=1 << 20, nq=1024, encoder="tc"):
     cb, der = train.train_pq(trt, cfg["m"], 16, 8, iters=10, seed=seed)
     t1 = time.time()
     n = cfg["n"]
-    enc = train.make_encoder(cb, device=device, kind=encoder if cfg["dsub"] <= 32 else "torch")
+    enc = train.make_encoder(cb, device=device, kind=encoder if cfg["dsub"] <= 128 else "torch")
+    # IVF coarse assignment (ivf.py:83-101): the same tensor-core encoder with m = 1, dsub = d
+    cenc = train.make_encoder(coarse.cpu().numpy()[None], device=device, kind=encoder) if coarse is not None \
+        else None
     out = {"codebooks": cb, "derived": der, "queries": Y, "rotation": rot, "cfg": cfg}
     if coarse is None:
         codes = np.empty((n, cfg["m"]), np.uint16)
@@ -127,7 +130,7 @@ def build(cfg, seed=42, device=None, chunk=1 << 20, nq=1024, encoder="tc"):
             x = _gen_chunk(cfg, centres, seed + 1, s, e - s, device)
             if rot is not None:
                 x = (x @ R0_t) @ rot_t
-            cl = train.coarse_assign(x, coarse)
+            cl = cenc(x)[:, 0].long()
             cells_t[s:e] = cl.to(torch.int32)
             codes_t[s:e] = enc(x - coarse[cl]).to(torch.int16)
             del x, cl

@@ -46,7 +46,11 @@ def test_config1_codes_bitwise_vs_reference_encoder(c1_golden):
 
 
 @pytest.mark.parametrize("m,k,dsub,n,scale", [(2, 4096, 32, 3000, 1.0), (3, 1000, 24, 777, 50.0),
-                                              (1, 8192, 32, 1500, 0.01)])
+                                              (1, 8192, 32, 1500, 0.01),
+                                              # K-chunked path (dsub > 32): configs[4]'s dsub = 120 and the
+                                              # IVF coarse assignment (m = 1, d = 128, K = 8192)
+                                              (2, 4096, 120, 2000, 1.0), (1, 8192, 128, 1500, 30.0),
+                                              (3, 700, 48, 999, 0.5)])
 def test_float_data_matches_exact_argmin_up_to_near_ties(m, k, dsub, n, scale):
     rng = np.random.default_rng(k + n)
     cb = (rng.normal(size=(m, k, dsub)) * scale).astype(np.float32)
@@ -101,6 +105,37 @@ def test_device_entry_and_errors():
     want, _ = exact_argmin(np.ascontiguousarray(x[:, :128]), cb)
     assert np.array_equal(codes.cpu().numpy(), want)
     with pytest.raises(ValueError):
-        _lib.Encoder(np.zeros((1, 16, 40), np.float32))
+        _lib.Encoder(np.zeros((1, 16, 140), np.float32))
     with pytest.raises(ValueError):
         enc.encode(np.zeros((3, 100), np.float32))
+
+
+def test_duplicate_centroids_lowest_index_chunked():
+    rng = np.random.default_rng(6)
+    k, dsub = 1024, 100
+    cb = rng.normal(size=(1, k, dsub)).astype(np.float32)
+    cb[0, 900] = cb[0, 3]
+    cb[0, 513] = cb[0, 512]
+    x = np.stack([cb[0, 900], cb[0, 513], cb[0, 3]]).astype(np.float32)
+    got = _lib.Encoder(cb).encode(x)[:, 0]
+    assert got.tolist() == [3, 512, 3]
+
+
+def test_gist_like_codes_chunked():
+    """configs[4] shape (8 x 65536 x 120) on GIST-like data: the tensor-core
+    codes agree with the exact f64 argmin except at f32 near-ties."""
+    rng = np.random.default_rng(8)
+    centres = rng.uniform(0, 1, size=(64, 120))
+    cb = np.clip(centres[rng.integers(64, size=(8, 65536))] + rng.normal(0, 0.05, size=(8, 65536, 120)), 0, 1)
+    cb = cb.astype(np.float32)
+    x = np.clip(centres[rng.integers(64, size=(400, 8))].reshape(400, 960) + rng.normal(0, 0.05, size=(400, 960)),
+                0, 1).astype(np.float32)
+    got = _lib.Encoder(cb).encode(x).astype(np.int64)
+    want, d2s = exact_argmin(x, cb)
+    agree = got == want
+    assert agree.mean() >= 0.99, agree.mean()
+    for j in range(8):
+        bad = np.flatnonzero(~agree[:, j])
+        if bad.size:
+            gap = d2s[j][bad, got[bad, j]] - d2s[j][bad, want[bad, j]]
+            assert np.all(gap <= 1e-4), gap
