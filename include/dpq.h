@@ -304,6 +304,36 @@ int dpq_encode(dpq_encoder_t* enc, const float* x, int64_t n,
 int dpq_encode_dev(dpq_encoder_t* enc, const float* x, int64_t n,
                    int64_t ldx, int32_t* codes, void* stream);
 
+/* ---------------------------------------------------------- containers --
+ * Model/index containers straight to the device: replaces the bulk half of
+ * derivedpq.vecio.load_model (vecio.py:156-198).  The Python mirror
+ * (container.py) parses the JSON header (vecio.py:177-183) and passes each
+ * array's byte range; arrays are read by `threads` host threads into pinned
+ * buffers and copied to freshly allocated device buffers (dev_out[a], free
+ * with dpq_dev_free) while the next piece is read.  With verify, crc_out[a]
+ * is the zlib CRC-32 of array a computed ON THE DEVICE (vecio.py:141,188-192
+ * compares it with the header).  stats4 (nullable): bytes read, host read
+ * seconds, total seconds, arrays.                                          */
+int dpq_container_read(int device, const char* path, int n_arrays,
+                       const int64_t* offsets, const int64_t* nbytes,
+                       int verify, int threads, void** dev_out,
+                       uint32_t* crc_out, double* stats4);
+/* zlib CRC-32 of a 16-byte-aligned device buffer (zlib.crc32 semantics). */
+int dpq_crc32_dev(int device, const void* data, int64_t len, uint32_t* crc);
+int dpq_dev_free(int device, void* p);
+int dpq_dev_download(int device, const void* src, int64_t nbytes, void* dst);
+/* Device halves of validate() on bulk arrays (flat.py:112-118,
+ * ivf.py:280-292): the largest code (-1 if count == 0); ids out of [0, n)
+ * (out2[0]) and rows no id maps to (out2[1]) — both 0 iff ids is a
+ * permutation of arange(n); counts[c] = |{i : cells[i] == c}| with cells
+ * outside [0, n_cells) counted in *n_bad.                                  */
+int dpq_dev_codes_max(int device, const void* codes, int64_t count,
+                      int code_bytes, int64_t* out_max);
+int dpq_dev_check_permutation(int device, const int64_t* ids, int64_t n,
+                              int64_t* out2);
+int dpq_dev_bincount(int device, const int32_t* cells, int64_t n,
+                     int n_cells, int64_t* counts, int64_t* n_bad);
+
 /* ------------------------------------------------------- measurement --
  * Milliseconds of the last batch's phases when timing is enabled:
  * [0] tables (K1), [1] sample+guard, [2] scan (K2), [3] threshold (K3),

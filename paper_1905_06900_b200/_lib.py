@@ -72,6 +72,14 @@ SIGNATURES = {
     "dpq_encoder_destroy": (None, [c_void_p]),
     "dpq_encode": (c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
     "dpq_encode_dev": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
+    "dpq_container_read": (c_int, [c_int, ctypes.c_char_p, c_int, c_void_p, c_void_p, c_int, c_int, c_void_p,
+                                   c_void_p, c_void_p]),
+    "dpq_crc32_dev": (c_int, [c_int, c_void_p, c_int64, c_void_p]),
+    "dpq_dev_free": (c_int, [c_int, c_void_p]),
+    "dpq_dev_download": (c_int, [c_int, c_void_p, c_int64, c_void_p]),
+    "dpq_dev_codes_max": (c_int, [c_int, c_void_p, c_int64, c_int, c_void_p]),
+    "dpq_dev_check_permutation": (c_int, [c_int, c_void_p, c_int64, c_void_p]),
+    "dpq_dev_bincount": (c_int, [c_int, c_void_p, c_int64, c_int, c_void_p, c_void_p]),
     "dpq_last_phase_ms": (c_int, [c_void_p, c_void_p]),
     "dpq_counters": (c_int, [c_void_p, c_void_p]),
     "dpq_counters_ex": (c_int, [c_void_p, c_void_p, c_int]),

@@ -17,7 +17,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libdpq.so"
-SOURCES = ["dpq_flat.cu", "dpq_encode.cu", "dpq_tctab.cu"]
+SOURCES = ["dpq_flat.cu", "dpq_encode.cu", "dpq_tctab.cu", "dpq_container.cu"]
 HEADERS = ["dpq_device.cuh", "dpq_kernels.cuh", "dpq_impl.h", "dpq_ivf.cuh"]
 
 NVCC_FLAGS = [

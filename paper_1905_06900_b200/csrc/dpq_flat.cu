@@ -1223,13 +1223,13 @@ int dpq_flat_create(int device, int m, int k, int kbar, int dsub, const float* c
   h->id_base = id_base;
   const size_t cbytes = (size_t)n * m * code_bytes;
   if ((rc = dmalloc((uint8_t**)&h->codes, cbytes + 16)) != DPQ_OK) { index_free(h); return rc; }
-  if (n > 0 && cudaMemcpy(h->codes, codes, cbytes, cudaMemcpyHostToDevice) != cudaSuccess) {
+  if (n > 0 && cudaMemcpy(h->codes, codes, cbytes, cudaMemcpyDefault) != cudaSuccess) {
     set_error("codes upload failed"); index_free(h); return DPQ_ERR_CUDA;
   }
   if (prefix_codes && n_prefix > 0) {
     const size_t pb = (size_t)n_prefix * m * code_bytes;
     if ((rc = dmalloc((uint8_t**)&h->prefix, pb)) != DPQ_OK) { index_free(h); return rc; }
-    if (cudaMemcpy(h->prefix, prefix_codes, pb, cudaMemcpyHostToDevice) != cudaSuccess) {
+    if (cudaMemcpy(h->prefix, prefix_codes, pb, cudaMemcpyDefault) != cudaSuccess) {
       set_error("prefix upload failed"); index_free(h); return DPQ_ERR_CUDA;
     }
     h->own_prefix = true;

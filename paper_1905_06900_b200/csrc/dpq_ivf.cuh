@@ -996,8 +996,8 @@ int dpq_ivf_create(int device, int m, int k, int kbar, int dsub, const float* co
   bool ok = cudaMemcpy(h->centers, centers, (size_t)n_cells * h->d * 4, cudaMemcpyHostToDevice) == cudaSuccess &&
             cudaMemcpy(h->offsets, offsets, (size_t)(n_cells + 1) * 8, cudaMemcpyHostToDevice) == cudaSuccess;
   if (n > 0)
-    ok = ok && cudaMemcpy(h->codes, sorted_codes, cbytes, cudaMemcpyHostToDevice) == cudaSuccess &&
-         cudaMemcpy(h->sorted_ids, sorted_ids, (size_t)n * 8, cudaMemcpyHostToDevice) == cudaSuccess;
+    ok = ok && cudaMemcpy(h->codes, sorted_codes, cbytes, cudaMemcpyDefault) == cudaSuccess &&
+         cudaMemcpy(h->sorted_ids, sorted_ids, (size_t)n * 8, cudaMemcpyDefault) == cudaSuccess;
   if (!ok) { set_error("ivf upload failed"); index_free(h); return DPQ_ERR_CUDA; }
   h->prefix = h->codes;
   h->n_prefix = n;

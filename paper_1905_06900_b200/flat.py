@@ -40,6 +40,43 @@ class ArrayQuantizer:
     def fit(self, X, y=None):  # pragma: no cover - arrays are already fitted
         return self
 
+    def encode(self, X) -> np.ndarray:
+        """quantizer.encode (quantizer.py:165-170) on the tensor-core encoder
+        (dpq_encode): rotate, nearest centroid per subspace (ties to the
+        lowest index), codes in code_dtype_."""
+        X = check_array(X, dtype=np.float32, order="C")
+        enc = getattr(self, "_encoder", None)
+        if enc is None:
+            enc = self._encoder = _lib.Encoder(self.codebooks_, device=getattr(self, "device", 0))
+        return enc.encode(np.ascontiguousarray(self.rotate(X), dtype=np.float32)).astype(self.code_dtype_)
+
+    def validate(self) -> None:
+        """quantizer.validate (quantizer.py:250-274): group id = low bbar
+        bits of the centroid index, finite codebooks, orthonormal rotation."""
+        from .errors import InvariantError
+
+        expected = np.arange(self.k_, dtype=np.int32) & (self.kbar_ - 1)
+        da = getattr(self, "derived_assignments_", None)
+        if da is not None:
+            for j in range(self.m):
+                if not np.array_equal(da[j], expected):
+                    bad = np.flatnonzero(da[j] != expected)[0]
+                    raise InvariantError(f"subspace {j}: centroid {int(bad)} is in group {int(da[j][bad])}, "
+                                         f"index demands {int(expected[bad])}")
+        if not np.all(np.isfinite(self.codebooks_)):
+            raise InvariantError("non-finite centroid in full codebooks")
+        if not np.all(np.isfinite(self.derived_codebooks_)):
+            raise InvariantError("non-finite centroid in derived codebooks")
+        if self.rotation_ is not None:
+            eye = self.rotation_.T.astype(np.float64) @ self.rotation_.astype(np.float64)
+            if np.abs(eye - np.eye(self.d_)).max() > 1e-5:
+                raise InvariantError("rotation matrix is not orthonormal")
+
+    def __getstate__(self):
+        state = self.__dict__.copy()
+        state.pop("_encoder", None)
+        return state
+
 
 def rotated_queries(quantizer, Y: np.ndarray) -> np.ndarray:
     """Queries after quantizer.rotate in the reference's per-query call
