@@ -1722,18 +1722,35 @@ __device__ void select_r(uint64_t* keys, int64_t* ids, int f, int r, SelShared& 
       if (tid + e * NT < f && (bits == 64 || (k[e] >> bits) == (pfx >> bits)))
         atomicAdd(&S.hist[(uint32_t)(k[e] >> sft) & ((1u << w) - 1u)], 1u);
     __syncthreads();
-    if (tid == 0) {
-      int need = S.need, d = 0;
-      uint32_t below = 0;
-      for (; d < (1 << w); ++d) {
-        if (below + S.hist[d] >= (uint32_t)need) break;
-        below += S.hist[d];
+    if (warp == 0) {
+      // the need-th element's digit: warp prefix sum over 8 bins per lane
+      const int need = S.need, nb = 1 << w;
+      uint32_t ls = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) ls += lane * 8 + i < nb ? S.hist[lane * 8 + i] : 0u;
+      uint32_t incl = ls;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
       }
-      S.need = need - (int)below;
-      S.pfx = (bits == 64 ? 0ull : pfx) | ((uint64_t)d << sft);
-      S.bits = sft;
-      S.done = S.hist[d] == 1u;  // the target is the only element of its bucket
-      S.cnt = 0;
+      const uint32_t reach = __ballot_sync(0xffffffffu, incl >= (uint32_t)need);
+      const int L = __ffs(reach) - 1;  // first lane whose prefix reaches need (exists: need <= total)
+      if (lane == L) {
+        uint32_t below = incl - ls;
+        int d = lane * 8;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const uint32_t hb = S.hist[lane * 8 + i];
+          if (below + hb >= (uint32_t)need) { d = lane * 8 + i; break; }
+          below += hb;
+        }
+        S.need = need - (int)below;
+        S.pfx = (bits == 64 ? 0ull : pfx) | ((uint64_t)d << sft);
+        S.bits = sft;
+        S.done = S.hist[d] == 1u;  // the target is the only element of its bucket
+        S.cnt = 0;
+      }
     }
     __syncthreads();
   }
@@ -1782,7 +1799,7 @@ __device__ __forceinline__ float entry_dist(const float* cbrow, const float* ys,
 
 template <int BUF, int NT, int MODE, int DSUB>
 #ifndef DPQ_REFINE_MINB
-#define DPQ_REFINE_MINB 5  // CTAs per SM the register budget is sized for (6: 40 regs, spills)
+#define DPQ_REFINE_MINB 4  // CTAs per SM the register budget is sized for (5: 48 regs, spills since the pipelined gathers)
 #endif
 __global__ void __launch_bounds__(NT, MODE == MODE_EMIT_APPROX ? 3 : DPQ_REFINE_MINB) k_refine_topk(RefineArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -1896,38 +1913,8 @@ __global__ void __launch_bounds__(NT, MODE == MODE_EMIT_APPROX ? 3 : DPQ_REFINE_
   };
   int fb = 0;   // buffer fill before this round (same value in every thread)
   int rnd = 0;  // round index mod 3
-  constexpr int NPASS = MODE == MODE_EMIT_APPROX ? 2 : 1;
-  for (pass = 0; pass < NPASS; ++pass) {
-  if (pass == 1) {
-    const int P = pow2_at_least(fb);
-    for (int i = fb + threadIdx.x; i < P; i += NT) { keys[i] = ~0ull; ids[i] = INT64_MAX; }
-    __syncthreads();
-    sort_pairs<NT>(keys, ids, P);
-    // U = r-th smallest upper bound a + E (all candidates pass when fewer than r)
-    tau = fb >= a.r ? __longlong_as_double((long long)keys[a.r - 1]) : INFINITY;
-    __syncthreads();
-    if (threadIdx.x == 0) { cnt3[0] = cnt3[1] = cnt3[2] = 0; thr_k = ~0ull; thr_i = INT64_MAX; }
-    __syncthreads();
-    fb = 0;
-    rnd = 0;
-  }
-  load_e(0);
-  for (int64_t base = 0; base < ntot; base += (int64_t)U * NT, rnd = rnd == 2 ? 0 : rnd + 1) {
-    uint64_t key[U], cur[U];
-    int64_t id[U];
-    bool keep[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) cur[u] = ev[u];
-    load_e(base + (int64_t)U * NT);
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t idx = base + (int64_t)u * NT + threadIdx.x;
-      keep[u] = idx < ntot && eval(idx, cur[u], key[u], id[u]) && key[u] <= thr_k;
-      if (keep[u]) {
-        id[u] = id_of(id[u]);
-        keep[u] = pair_less(key[u], id[u], thr_k, thr_i);
-      }
-    }
+  // one round's survivors into the buffer; sort / select once it fills
+  auto commit = [&](const bool* keep, const uint64_t* key, const int64_t* id) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       if (keep[u]) {
@@ -1961,6 +1948,118 @@ __global__ void __launch_bounds__(NT, MODE == MODE_EMIT_APPROX ? 3 : DPQ_REFINE_
         __syncthreads();
       }
     }
+  };
+  constexpr int NPASS = MODE == MODE_EMIT_APPROX ? 2 : 1;
+  bool piped = false;
+#ifndef DPQ_REFINE_PIPE
+#define DPQ_REFINE_PIPE 1
+#endif
+  if constexpr (MODE == MODE_EMIT_TABLE && DPQ_REFINE_PIPE) {
+    if (a.code_bytes == 2 && a.m == 4) {
+      // Software-pipelined gathers (flat PQ 4x16, the configs[1-3] shape):
+      // emit entries are loaded two rounds ahead and the candidates' codes
+      // one round ahead, so a round waits on one dependent gather (its
+      // table entries) instead of the emit -> code -> table chain.
+      piped = true;
+      const uint32_t kmask = (uint32_t)a.kbar - 1u, gs = (uint32_t)(a.k >> a.bbar);
+      auto off = [&](uint32_t j, uint32_t c) { return ((j << a.bbar) + (c & kmask)) * gs + (c >> a.bbar); };
+      // k = 65536, kbar = 256: entry (j, c) sits at j << 16 | (c & 255) << 8 | c >> 8, one byte permute
+      const bool k16 = a.k == 65536 && a.bbar == 8;
+      const uint2* codes2 = reinterpret_cast<const uint2*>(a.codes);
+      auto valid = [&](uint64_t v, int64_t idx) { return idx < ntot && (int)emit_score(v) <= bs; };
+      auto ld_e = [&](int64_t idx) -> uint64_t { return idx < ntot ? e[idx] : 0ull; };
+      uint64_t e0[U], e1[U];
+      uint2 c0[U];
+      const int64_t step = (int64_t)U * NT;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t i0 = (int64_t)u * NT + threadIdx.x;
+        e0[u] = ld_e(i0);
+        e1[u] = ld_e(i0 + step);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t i0 = (int64_t)u * NT + threadIdx.x;
+        c0[u] = valid(e0[u], i0) ? __ldg(codes2 + emit_row(e0[u])) : make_uint2(0u, 0u);
+      }
+      for (int64_t base = 0; base < ntot; base += step, rnd = rnd == 2 ? 0 : rnd + 1) {
+        uint2 cn[U];
+        uint64_t en[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t i1 = base + step + (int64_t)u * NT + threadIdx.x;
+          cn[u] = valid(e1[u], i1) ? __ldg(codes2 + emit_row(e1[u])) : make_uint2(0u, 0u);
+          en[u] = ld_e(i1 + step);
+        }
+        uint64_t key[U];
+        int64_t id[U];
+        bool keep[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t i0 = base + (int64_t)u * NT + threadIdx.x;
+          keep[u] = valid(e0[u], i0);
+          if (keep[u]) {
+            ++my_ref;
+            const uint2 v = c0[u];
+            uint32_t o0, o1, o2, o3;
+            if (k16) {
+              o0 = __byte_perm(v.x, 0u, 0x5401u); o1 = __byte_perm(v.x, 1u, 0x5423u);
+              o2 = __byte_perm(v.y, 2u, 0x5401u); o3 = __byte_perm(v.y, 3u, 0x5423u);
+            } else {
+              o0 = off(0, v.x & 0xFFFFu); o1 = off(1, v.x >> 16); o2 = off(2, v.y & 0xFFFFu); o3 = off(3, v.y >> 16);
+            }
+            const float t0 = __ldg(tq + o0);
+            const float t1 = __ldg(tq + o1);
+            const float t2 = __ldg(tq + o2);
+            const float t3 = __ldg(tq + o3);
+            const double dist = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(0.0, (double)t0), (double)t1), (double)t2),
+                                          (double)t3);
+            key[u] = (uint64_t)__double_as_longlong(dist);
+            keep[u] = key[u] <= thr_k;
+            if (keep[u]) {
+              id[u] = id_of(emit_row(e0[u]));
+              keep[u] = pair_less(key[u], id[u], thr_k, thr_i);
+            }
+          }
+        }
+        commit(keep, key, id);
+#pragma unroll
+        for (int u = 0; u < U; ++u) { e0[u] = e1[u]; c0[u] = cn[u]; e1[u] = en[u]; }
+      }
+    }
+  }
+  for (pass = 0; pass < NPASS && !piped; ++pass) {
+  if (pass == 1) {
+    const int P = pow2_at_least(fb);
+    for (int i = fb + threadIdx.x; i < P; i += NT) { keys[i] = ~0ull; ids[i] = INT64_MAX; }
+    __syncthreads();
+    sort_pairs<NT>(keys, ids, P);
+    // U = r-th smallest upper bound a + E (all candidates pass when fewer than r)
+    tau = fb >= a.r ? __longlong_as_double((long long)keys[a.r - 1]) : INFINITY;
+    __syncthreads();
+    if (threadIdx.x == 0) { cnt3[0] = cnt3[1] = cnt3[2] = 0; thr_k = ~0ull; thr_i = INT64_MAX; }
+    __syncthreads();
+    fb = 0;
+    rnd = 0;
+  }
+  load_e(0);
+  for (int64_t base = 0; base < ntot; base += (int64_t)U * NT, rnd = rnd == 2 ? 0 : rnd + 1) {
+    uint64_t key[U], cur[U];
+    int64_t id[U];
+    bool keep[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) cur[u] = ev[u];
+    load_e(base + (int64_t)U * NT);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t idx = base + (int64_t)u * NT + threadIdx.x;
+      keep[u] = idx < ntot && eval(idx, cur[u], key[u], id[u]) && key[u] <= thr_k;
+      if (keep[u]) {
+        id[u] = id_of(id[u]);
+        keep[u] = pair_less(key[u], id[u], thr_k, thr_i);
+      }
+    }
+    commit(keep, key, id);
   }
   }  // pass
   const int f = fb;

@@ -28,7 +28,8 @@ ap.add_argument("--steps", type=int, default=10)
 a = ap.parse_args()
 sys.argv = [sys.argv[0], "--steps", str(a.steps), "--warmup", "3"]
 args = bench.parse()
-w = bench.build_workload(args, "cuda:0")
+cfg, _ = bench.resolve(args, 1)
+w = bench.build_flat(cfg, args, torch.device("cuda", 0), 0, cfg["n"], a.steps * 1024)
 Q = torch.as_tensor(w["queries"][: a.steps * 1024], device="cuda")
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 results = {p: [] for p in a.libs}
