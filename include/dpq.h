@@ -348,7 +348,9 @@ int dpq_counters(dpq_index_t* index, int64_t* out8);
 /* Extended counters (n of them; unknown slots read 0): [0..7] as
  * dpq_counters, [8] code-plane rows the first-pass scan read (summed over
  * query tiles; 4 or 8 B each), [9] LUT tile loads of the scan (128 KB each).
- * With [5] (emitted entries, 8 B each) they give the scan's bytes moved. */
+ * With [5] (emitted entries, 8 B each) they give the scan's bytes moved.
+ * [10] candidates re-ranked exactly after tensor-core tables, [11] exact
+ * f64 centre distances computed by the tensor-core IVF probe.           */
 int dpq_counters_ex(dpq_index_t* index, int64_t* out, int n);
 
 #ifdef __cplusplus

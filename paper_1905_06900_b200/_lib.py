@@ -166,10 +166,11 @@ class Handle:
                         out.tolist()))
 
     def counters_ex(self) -> dict:
-        out = np.zeros(11, dtype=np.int64)
-        check(lib().dpq_counters_ex(self.raw, ptr(out), 11))
+        out = np.zeros(12, dtype=np.int64)
+        check(lib().dpq_counters_ex(self.raw, ptr(out), 12))
         return dict(zip(("launches", "queries", "rows_scanned", "refined", "fallbacks", "emitted",
-                         "table_entries", "wide_units", "plane_rows", "lut_loads", "exact_reranked"),
+                         "table_entries", "wide_units", "plane_rows", "lut_loads", "exact_reranked",
+                         "probe_exact"),
                         out.tolist()))
 
     def set_timing(self, on: bool) -> None:

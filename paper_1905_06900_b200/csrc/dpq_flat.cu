@@ -1101,8 +1101,8 @@ int index_common_init(Index* h, int device, int m, int k, int kbar, int dsub, co
   DPQ_TRY(dmalloc(&h->d_nemit, 1));
   DPQ_TRY(dmalloc(&h->d_nent, 1));
   DPQ_TRY(dmalloc(&h->d_nwide, 1));
-  DPQ_TRY(dmalloc(&h->d_nrows, 4));  // query-rows, plane rows, LUT tile loads (scan), spare
-  DPQ_CUDA(cudaMemset(h->d_nrows, 0, 32));
+  DPQ_TRY(dmalloc(&h->d_nrows, 8));  // query-rows, plane rows, LUT tile loads (scan), exact re-ranks, probe exact d2
+  DPQ_CUDA(cudaMemset(h->d_nrows, 0, 64));
   DPQ_CUDA(cudaMemset(h->d_nent, 0, 8));
   DPQ_CUDA(cudaMemset(h->d_nwide, 0, 8));
   DPQ_CUDA(cudaMemcpy(h->cb, codebooks, (size_t)m * k * dsub * 4, cudaMemcpyHostToDevice));
@@ -1536,10 +1536,11 @@ int dpq_counters_ex(dpq_index_t* index, int64_t* out, int n) {
   if (!h || !out || n < 0) { set_error("null argument"); return DPQ_ERR_ARG; }
   int64_t base[8];
   DPQ_TRY(dpq_counters(index, base));
-  unsigned long long dv[4] = {};
+  unsigned long long dv[8] = {};
   DPQ_CUDA(cudaMemcpy(dv, h->d_nrows, sizeof(dv), cudaMemcpyDeviceToHost));
   const int64_t all[kCountersEx] = {base[0], base[1], base[2], base[3], base[4], base[5], base[6], base[7],
-                                    (int64_t)dv[1] + h->plane_rows, (int64_t)dv[2], (int64_t)dv[3]};
+                                    (int64_t)dv[1] + h->plane_rows, (int64_t)dv[2], (int64_t)dv[3],
+                                    (int64_t)dv[4]};
   for (int i = 0; i < n; ++i) out[i] = i < kCountersEx ? all[i] : 0;
   return DPQ_OK;
 }

@@ -24,7 +24,7 @@ void tct_free(void* t);
 enum Kind { KIND_FLAT = 0, KIND_IVF = 1 };
 
 // Phase slots of dpq_last_phase_ms.
-constexpr int kCountersEx = 11;  // dpq_counters_ex
+constexpr int kCountersEx = 12;  // dpq_counters_ex
 
 enum Phase { PH_TABLES = 0, PH_GUARD, PH_SCAN, PH_THRESH, PH_REFINE, PH_FALLBACK, PH_TOTAL, PH_N };
 
@@ -128,7 +128,7 @@ struct Index {
   unsigned long long* d_nemit = nullptr;
   unsigned long long* d_nent = nullptr;   // lazily computed table entries
   unsigned long long* d_nwide = nullptr;  // scan units run by the wide loop
-  unsigned long long* d_nrows = nullptr;  // [4]: query-rows (list mode), plane rows (list mode), LUT loads, spare
+  unsigned long long* d_nrows = nullptr;  // [8]: query-rows (list mode), plane rows (list mode), LUT loads, exact re-ranks, probe exact d2
   int64_t plane_rows = 0;                 // plane rows read by the scan (non-list mode, host-counted)
   size_t emit_budget = (size_t)16 << 30;  // bytes for emit buffers
   // guard sampling (env DPQ_GUARD_SAMPLE / DPQ_EXACT_LIMIT / DPQ_EMIT_CAP
@@ -157,6 +157,7 @@ struct Index {
   double* tct_ny = nullptr;   // (nq, m) ||y'||
   int64_t tct_eps_cap = 0;
   int use_tc = -1;
+  int probe_tc = 1;           // env DPQ_PROBE_TC at creation: 0 f64 probe, 1 tensor cores for K >= 1024, 2 always
   double tc_eps_scale = 1.0;  // env DPQ_TC_EPS_SCALE (tests: tighten to force more exact re-ranks)
   Workspace ws;
   // sharded-search state between dpq_shard_* calls

@@ -147,6 +147,72 @@ __global__ void __launch_bounds__(NT, 1) k_probe_select(const double* __restrict
   for (int i = threadIdx.x; i < ma; i += NT) cells[(int64_t)q * ma + i] = ids[i];
 }
 
+// Tensor-core probe (ivf.py:107-120 on the 5th-generation tensor cores).
+// The squared distances of a query to all K centres come from the 3xTF32
+// table GEMM of dpq_tctab.cu (centres = an m = 1 codebook, kbar = 1, so the
+// entries are in centre order) together with a rigorous per-entry bound
+// E_c = gamma (||y - mu|| + ||c - mu||)^2 >= |approx_c - d2_c|.  Per query:
+// tau = the ma-th smallest upper bound approx + E; every centre whose lower
+// bound approx - E is <= tau is a candidate (a superset of the exact ma
+// nearest), its d2 is recomputed exactly with k_probe_dist's f64 arithmetic,
+// and the ma smallest (d2, cell) pairs are kept — the same cells in the same
+// order as the all-f64 probe, from ~ma exact distances instead of K.
+template <int NT, int EPT>
+__global__ void __launch_bounds__(NT, 1) k_probe_select_tc(const float* __restrict__ approx, const double* __restrict__ ny,
+                                                           const float* __restrict__ cnorm, double gamma,
+                                                           const float* __restrict__ y, int d,
+                                                           const float* __restrict__ centers, int K, int ma,
+                                                           int64_t* __restrict__ cells,
+                                                           unsigned long long* __restrict__ n_exact) {
+  extern __shared__ __align__(16) uint8_t probe_smem[];
+  uint64_t* keys = reinterpret_cast<uint64_t*>(probe_smem);
+  int64_t* ids = reinterpret_cast<int64_t*>(keys + NT * EPT);
+  __shared__ SelShared S;
+  __shared__ uint64_t thr_k;
+  __shared__ int64_t thr_i;
+  __shared__ int ncand;
+  __shared__ float ys[512];
+  const int q = blockIdx.x;
+  const float* aq = approx + (int64_t)q * K;
+  const double nyq = ny[q];
+  auto bound = [&](int c) {
+    const double s = nyq + (double)cnorm[c];
+    return gamma * s * s * (1.0 + 1e-9) + 1e-300;
+  };
+  for (int i = threadIdx.x; i < K; i += NT) {
+    const double u = fmax((double)aq[i] + bound(i), 0.0);
+    keys[i] = (uint64_t)__double_as_longlong(u);
+    ids[i] = i;
+  }
+  for (int i = threadIdx.x; i < d; i += NT) ys[i] = y[(int64_t)q * d + i];
+  if (threadIdx.x == 0) { ncand = 0; thr_k = ~0ull; }
+  __syncthreads();
+  if (K > ma) select_r<NT, EPT>(keys, ids, K, ma, S, thr_k, thr_i);
+  const double tau = K > ma ? __longlong_as_double((long long)thr_k) : INFINITY;
+  __syncthreads();
+  for (int i = threadIdx.x; i < K; i += NT)
+    if ((double)aq[i] - bound(i) <= tau) ids[atomicAdd(&ncand, 1)] = i;
+  __syncthreads();
+  const int nc = ncand;
+  for (int i = threadIdx.x; i < nc; i += NT) {  // k_probe_dist's arithmetic, one thread per candidate
+    const int c = (int)ids[i];
+    const float* cr = centers + (int64_t)c * d;
+    double acc = 0.0;
+    for (int t = 0; t < d; ++t) {
+      const double df = __dsub_rn((double)cr[t], (double)ys[t]);
+      acc = __dadd_rn(acc, __dmul_rn(df, df));
+    }
+    keys[i] = (uint64_t)__double_as_longlong(acc);
+  }
+  int P = 2;
+  while (P < nc) P <<= 1;
+  for (int i = nc + threadIdx.x; i < P; i += NT) { keys[i] = ~0ull; ids[i] = INT64_MAX; }
+  __syncthreads();
+  sort_pairs<NT>(keys, ids, P);
+  for (int i = threadIdx.x; i < ma; i += NT) cells[(int64_t)q * ma + i] = ids[i];
+  if (threadIdx.x == 0 && n_exact) atomicAdd(n_exact, (unsigned long long)nc);
+}
+
 // residuals y - centre in f32 (ivf.py:120), natural (query, probe) order
 __global__ void k_residuals(const float* __restrict__ y, const float* __restrict__ centers,
                             const int64_t* __restrict__ cells, int nq, int ma, int d,
@@ -348,6 +414,14 @@ struct IvfBuffers {
   int* phantom = nullptr;              // [cap_q] shard bound-source slots
   double* d2 = nullptr;                // probe distances (nq, K)
   int64_t cap_d2 = 0;
+  // tensor-core probe: centres as an m = 1 codebook (dpq_tctab.cu)
+  void* ptc = nullptr;
+  int ptc_state = 0;                   // 0 untried, 1 ready, -1 unavailable
+  float* papprox = nullptr;            // (nq, K) approximate squared distances
+  double* peps = nullptr;              // (nq) entry bound of the query (unused: per-entry bounds below)
+  double* pny = nullptr;               // (nq) ||y - mu||
+  int64_t cap_pa = 0;
+  int cap_pq = 0;
 };
 
 static IvfBuffers& ivf_bufs(Index* h) { return *reinterpret_cast<IvfBuffers*>(h->ivf_state); }
@@ -391,9 +465,11 @@ static void ivf_free(Index* h) {
   if (!h->ivf_state) return;
   IvfBuffers& b = ivf_bufs(h);
   void* p[] = {b.cells, b.ynat, b.yts, b.bound_ts, b.live, b.bsrc, b.lambda, b.hist_q, b.gword_q, b.guard_q,
-               b.unit_tile, b.unit_r0, b.unit_r1, b.tile_row0, b.tile_nsamp, b.d2, b.phantom};
+               b.unit_tile, b.unit_r0, b.unit_r1, b.tile_row0, b.tile_nsamp, b.d2, b.phantom,
+               b.papprox, b.peps, b.pny};
   for (void* x : p)
     if (x) cudaFree(x);
+  tct_free(b.ptc);
   delete reinterpret_cast<IvfBuffers*>(h->ivf_state);
   h->ivf_state = nullptr;
   if (h->g_prefix) cudaFree(h->g_prefix);
@@ -403,6 +479,40 @@ static void ivf_free(Index* h) {
 // Probe on device: cells (nb, ma) into bufs.cells.
 static int ivf_probe_dev(Index* h, int nb, int ma) {
   IvfBuffers& b = ivf_bufs(h);
+  // tensor-core probe (h->probe_tc: 0 off, 1 auto = K >= 1024, 2 forced)
+  const int probe_tc = h->probe_tc;
+  const int K = h->n_cells;
+  if (nb > 0 && K <= 8192 && h->d <= 128 && ma < K && tct_supported(1, K, 1, h->d) &&
+      (probe_tc == 2 || (probe_tc == 1 && K >= 1024))) {
+    if (b.ptc_state == 0)
+      b.ptc_state = tct_prepare(h->device, h->centers, 1, K, 1, h->d, h->stream, &b.ptc) == DPQ_OK ? 1 : -1;
+    if (b.ptc_state == 1) {
+      if ((int64_t)nb * K > b.cap_pa) {
+        if (b.papprox) cudaFree(b.papprox);
+        b.papprox = nullptr;
+        b.cap_pa = (int64_t)nb * K;
+        DPQ_TRY(dmalloc(&b.papprox, (size_t)b.cap_pa));
+      }
+      if (nb > b.cap_pq) {
+        if (b.peps) cudaFree(b.peps);
+        if (b.pny) cudaFree(b.pny);
+        b.peps = b.pny = nullptr;
+        b.cap_pq = nb;
+        DPQ_TRY(dmalloc(&b.peps, (size_t)nb));
+        DPQ_TRY(dmalloc(&b.pny, (size_t)nb));
+      }
+      DPQ_TRY(tct_build(b.ptc, h->ws.y, h->d, nb, b.papprox, b.peps, b.pny, 1.0, h->stream));
+      DPQ_LAUNCHED(h);
+      const size_t smem = (size_t)1024 * 8 * 16;
+      DPQ_TRY(set_smem(h, k_probe_select_tc<1024, 8>, smem));
+      k_probe_select_tc<1024, 8><<<nb, 1024, smem, h->stream>>>(b.papprox, b.pny, tct_cnorm(b.ptc),
+                                                                tct_gamma(b.ptc, 1.0), h->ws.y, h->d, h->centers, K,
+                                                                ma, b.cells, h->d_nrows + 4);
+      DPQ_LAUNCHED(h);
+      return DPQ_OK;
+    }
+    cudaGetLastError();  // tct_prepare failed: the f64 path below
+  }
   if (h->n_cells <= 8192 && nb > 0) {  // query-tiled distances + block radix sort per query
     if ((int64_t)nb * h->n_cells > b.cap_d2) {
       if (b.d2) cudaFree(b.d2);
@@ -982,6 +1092,7 @@ int dpq_ivf_create(int device, int m, int k, int kbar, int dsub, const float* co
   int rc = index_common_init(h, device, m, k, kbar, dsub, codebooks, derived_codebooks, code_bytes);
   if (rc != DPQ_OK) { index_free(h); return rc; }
   h->ivf_state = new IvfBuffers();
+  if (const char* e = getenv("DPQ_PROBE_TC")) h->probe_tc = atoi(e);
   h->n = n;
   h->n_cells = n_cells;
   h->h_offsets.assign(offsets, offsets + n_cells + 1);

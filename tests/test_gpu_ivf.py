@@ -154,3 +154,55 @@ def test_ivf_errors_and_timings():
     dists, ids = idx.search(g["queries"][:1], 6000, ma=1)
     n_found = int((ids[0] >= 0).sum())
     assert 0 < n_found < 6000 and np.all(np.isinf(dists[0, n_found:]))
+
+
+# ---- tensor-core probe (k_probe_select_tc): same cells, same order, as the f64 probe ----
+
+def _probe_all(idx, Y, ma):
+    return idx._probe_cells(np.ascontiguousarray(Y, dtype=np.float32), ma)
+
+
+@pytest.mark.parametrize("name", IVF_CASES)
+def test_tc_probe_forced_matches_reference(monkeypatch, name):
+    g = load_golden(name)
+    K = g["centers"].shape[0]
+    if K % 4:
+        pytest.skip("tensor-core tables need 4 | K")
+    monkeypatch.setenv("DPQ_PROBE_TC", "2")
+    idx = _index(g)
+    m = g["meta"]
+    cells = _probe_all(idx, g["queries"], m["ma"])
+    assert np.array_equal(cells, g["exp_cells"])
+    d, i = idx.search(g["queries"], m["r"], ma=m["ma"], mode="derived", r2=m["r2"])
+    assert np.array_equal(i, g["exp_derived_i"]) and _same(d, g["exp_derived_d"])
+
+
+@pytest.mark.parametrize("K,d,ma", [(2048, 128, 64), (8192, 128, 64), (1024, 96, 7), (4096, 128, 1)])
+def test_tc_probe_equals_f64_probe(monkeypatch, K, d, ma):
+    rng = np.random.default_rng(K + d)
+    centers = rng.uniform(0, 64, size=(K, d)).astype(np.float32)
+    centers[5] = centers[9]          # exact distance ties: the lower cell first
+    centers[K - 1] = centers[3]
+    Y = np.concatenate([rng.uniform(0, 64, size=(200, d)), centers[[3, 5, 100]] + 0.0]).astype(np.float32)
+    m, dsub = 2, d // 2
+    cb = rng.normal(size=(m, 256, dsub)).astype(np.float32)
+    der = cb[:, :16].copy()
+    n = 4 * K
+    codes = rng.integers(0, 256, size=(n, m)).astype(np.uint8)
+    cell_of = rng.integers(0, K, size=n)
+    order = np.argsort(cell_of, kind="stable")
+    offsets = np.concatenate([[0], np.cumsum(np.bincount(cell_of, minlength=K))]).astype(np.int64)
+    args = (cb, der, centers, offsets, codes[order], order.astype(np.int64))
+    monkeypatch.setenv("DPQ_PROBE_TC", "0")
+    ref = _probe_all(IVFIndex.from_arrays(*args, cell_of=cell_of), Y, ma)
+    monkeypatch.setenv("DPQ_PROBE_TC", "2")
+    idx = IVFIndex.from_arrays(*args, cell_of=cell_of)
+    got = _probe_all(idx, Y, ma)
+    assert np.array_equal(got, ref)
+    # and the reference's own rule (ivf.py:117-120): f64 distances, ascending, lower id on ties
+    for q in (0, 7, Y.shape[0] - 1):
+        diff = centers.astype(np.float64) - Y[q].astype(np.float64)
+        d2 = np.einsum("kd,kd->k", diff, diff)
+        exp = np.lexsort((np.arange(K), d2))[:ma]
+        assert np.array_equal(got[q], exp)
+    assert idx._handle().counters_ex()["probe_exact"] >= ma * Y.shape[0]
