@@ -121,8 +121,9 @@ static int set_smem(const Index* h, K* kern, size_t bytes) {
   return set_smem_impl(h->device, reinterpret_cast<const void*>(kern), bytes);
 }
 
-static inline int qt_of(int mpad) { return mpad == 4 ? ScanGeom<4>::QT : ScanGeom<8>::QT; }
-static inline int tiles_of(int nslot, int mpad) { return (nslot + qt_of(mpad) - 1) / qt_of(mpad); }
+// Queries per scan tile of this index (ScanGeom): flat m <= 4: 128, ivf m <= 4: 64 (h->qt), m = 8: 64.
+static inline int qt_of(const Index* h) { return h->qt; }
+static inline int tiles_of(int nslot, const Index* h) { return (nslot + qt_of(h) - 1) / qt_of(h); }
 
 // Slot-indexed arrays (a slot = one query for flat, one (query, probe) of a
 // query tile for ivf) are sized by nslot; query-indexed arrays (emit lists,
@@ -130,7 +131,7 @@ static inline int tiles_of(int nslot, int mpad) { return (nslot + qt_of(mpad) - 
 int ensure_ws(Index* h, int nslot, int r, int ystride, int nq) {
   Workspace& w = h->ws;
   if (nq < 0) nq = nslot;
-  const int qt = qt_of(h->mpad);
+  const int qt = qt_of(h);
   if (nslot > w.qb || ystride > w.ystride || nq > w.qn) {
     const int qb = std::max(nslot, w.qb);
     const int qn = std::max(nq, w.qn);
@@ -221,13 +222,13 @@ static inline float ev_ms(Index* h, int a, int b) {
 // ---------------------------------------------------------------------------
 // Launch helpers (template dispatch on MPAD)
 // ---------------------------------------------------------------------------
-template <int MPAD>
+template <int MPAD, int QTX>
 static int launch_hist_t(Index* h, int ntiles, const int* tile_list, int64_t stride,
                          int64_t nsamp, const uint8_t* plane, const int64_t* tile_row0 = nullptr,
                          const int64_t* tile_nsamp = nullptr) {
-  using G = ScanGeom<MPAD>;
+  using G = ScanGeom<MPAD, QTX>;
   const size_t smem = G::LUT_BYTES + (size_t)G::QT * 128 * 4;
-  DPQ_TRY(set_smem(h, k_scan_hist<MPAD, kScanThreads>, smem));
+  DPQ_TRY(set_smem(h, k_scan_hist<MPAD, kScanThreads, QTX>, smem));
   int chunks = (int)std::max<int64_t>(1, std::min<int64_t>((148 * 2 + ntiles - 1) / ntiles,
                                                           (nsamp + 511) / 512));
   int64_t per = (nsamp + chunks - 1) / chunks;
@@ -236,7 +237,7 @@ static int launch_hist_t(Index* h, int ntiles, const int* tile_list, int64_t str
   chunks = (int)((nsamp + per - 1) / per);
   if (chunks < 1) chunks = 1;
   dim3 grid(chunks, ntiles);
-  k_scan_hist<MPAD, kScanThreads><<<grid, kScanThreads, smem, h->stream>>>(
+  k_scan_hist<MPAD, kScanThreads, QTX><<<grid, kScanThreads, smem, h->stream>>>(
       plane, stride, nsamp, per, h->ws.lut, tile_list, h->ws.hist, tile_row0, tile_nsamp);
   DPQ_LAUNCHED(h);
   return DPQ_OK;
@@ -247,8 +248,9 @@ static int launch_hist(Index* h, int ntiles, const int* tile_list, int64_t strid
                        const uint8_t* plane, const int64_t* tile_row0 = nullptr,
                        const int64_t* tile_nsamp = nullptr) {
   if (ntiles < 1 || nsamp < 1) return DPQ_OK;
-  return h->mpad == 4 ? launch_hist_t<4>(h, ntiles, tile_list, stride, nsamp, plane, tile_row0, tile_nsamp)
-                      : launch_hist_t<8>(h, ntiles, tile_list, stride, nsamp, plane, tile_row0, tile_nsamp);
+  if (h->mpad == 8) return launch_hist_t<8, 64>(h, ntiles, tile_list, stride, nsamp, plane, tile_row0, tile_nsamp);
+  if (h->qt == 64) return launch_hist_t<4, 64>(h, ntiles, tile_list, stride, nsamp, plane, tile_row0, tile_nsamp);
+  return launch_hist_t<4, 128>(h, ntiles, tile_list, stride, nsamp, plane, tile_row0, tile_nsamp);
 }
 
 static int num_sms(Index* h) {
@@ -260,12 +262,12 @@ static int num_sms(Index* h) {
   return h->sms;
 }
 
-template <int MPAD>
+template <int MPAD, int QTX>
 static int launch_emit_t(Index* h, EmitArgs ea, int ntiles, int64_t rows) {
-  using G = ScanGeom<MPAD>;
+  using G = ScanGeom<MPAD, QTX>;
   constexpr int NW = kEmitThreads / 32;
-  const size_t smem = emit_smem_bytes<MPAD, kEmitThreads>();
-  DPQ_TRY(set_smem(h, k_scan_emit<MPAD, kEmitThreads>, smem));
+  const size_t smem = emit_smem_bytes<MPAD, kEmitThreads, QTX>();
+  DPQ_TRY(set_smem(h, k_scan_emit<MPAD, kEmitThreads, QTX>, smem));
   // Persistent CTAs (one per SM) pulling ~8 units each from a counter.
   const int sms = num_sms(h);
   ea.unit_counter = h->ws.counter;
@@ -277,7 +279,7 @@ static int launch_emit_t(Index* h, EmitArgs ea, int ntiles, int64_t rows) {
   if (ea.unit_tile) {  // caller-built units (ivf lists)
     if (ea.n_units < 1) return DPQ_OK;
     DPQ_CUDA(cudaMemsetAsync(h->ws.counter, 0, sizeof(unsigned), h->stream));
-    k_scan_emit<MPAD, kEmitThreads><<<std::min(sms, ea.n_units), kEmitThreads, smem, h->stream>>>(ea);
+    k_scan_emit<MPAD, kEmitThreads, QTX><<<std::min(sms, ea.n_units), kEmitThreads, smem, h->stream>>>(ea);
     DPQ_LAUNCHED(h);
     return DPQ_OK;
   }
@@ -287,7 +289,7 @@ static int launch_emit_t(Index* h, EmitArgs ea, int ntiles, int64_t rows) {
     ea.rows_per_cta = 0;
     ea.list_next = h->ws.list_len + ntiles;
     DPQ_CUDA(cudaMemsetAsync(h->ws.list_len + ntiles, 0, (size_t)ntiles * sizeof(int), h->stream));
-    k_scan_emit<MPAD, kEmitThreads><<<sms, kEmitThreads, smem, h->stream>>>(ea);
+    k_scan_emit<MPAD, kEmitThreads, QTX><<<sms, kEmitThreads, smem, h->stream>>>(ea);
     DPQ_LAUNCHED(h);
     return DPQ_OK;
   }
@@ -304,13 +306,15 @@ static int launch_emit_t(Index* h, EmitArgs ea, int ntiles, int64_t rows) {
   ea.one = 1u;
   DPQ_CUDA(cudaMemsetAsync(h->ws.counter, 0, sizeof(unsigned), h->stream));
   const int grid = (int)std::min<int64_t>(sms, ea.n_units);
-  k_scan_emit<MPAD, kEmitThreads><<<grid, kEmitThreads, smem, h->stream>>>(ea);
+  k_scan_emit<MPAD, kEmitThreads, QTX><<<grid, kEmitThreads, smem, h->stream>>>(ea);
   DPQ_LAUNCHED(h);
   return DPQ_OK;
 }
 
 static int launch_emit(Index* h, EmitArgs ea, int ntiles, int64_t rows) {
-  return h->mpad == 4 ? launch_emit_t<4>(h, ea, ntiles, rows) : launch_emit_t<8>(h, ea, ntiles, rows);
+  if (h->mpad == 8) return launch_emit_t<8, 64>(h, ea, ntiles, rows);
+  if (h->qt == 64) return launch_emit_t<4, 64>(h, ea, ntiles, rows);
+  return launch_emit_t<4, 128>(h, ea, ntiles, rows);
 }
 
 template <int BUF, int MODE>
@@ -368,7 +372,7 @@ int run_small_tables(Index* h, int nslot, const void* prefix, int64_t npre,
   ta.small_out = export_debug ? w.small : nullptr;
   ta.q8_out = w.q8;  // read by k_group_tables
   ta.qmin_out = w.qmin; ta.qmax_out = w.qmax;
-  ta.lut = w.lut; ta.mpad = h->mpad; ta.qt = qt_of(h->mpad);
+  ta.lut = w.lut; ta.mpad = h->mpad; ta.qt = qt_of(h);
   ta.cluster = (!pre_off && h->m >= 2) ? w.cluster : nullptr;  // flat: slot clustering keys
   const size_t smem = (size_t)(h->d + h->m * h->kbar) * 4 + (size_t)h->m * h->kbar + 16;
   ta.slot_list = slot_list;
@@ -402,15 +406,18 @@ int run_small_tables(Index* h, int nslot, const void* prefix, int64_t npre,
 // guards are all <= 126 are clamped to 7-bit entries and flagged fast.
 int build_lut(Index* h, int nslot, const uint16_t* gword, const int* slot_query, const int* slot_live) {
   Workspace& w = h->ws;
-  const int ntiles = tiles_of(nslot, h->mpad);
+  const int ntiles = tiles_of(nslot, h);
   int* tf = w.tile_fast;  // reset to 0 when gword is null (unclamped LUT)
   const dim3 grid((unsigned)ntiles, (unsigned)h->mpad);
-  if (h->mpad == 4)
-    k_build_lut<4><<<grid, 256, 0, h->stream>>>(w.q8, nslot, h->m, h->kbar, w.lut, ntiles, gword, tf, h->wide,
-                                                slot_query, slot_live);
+  if (h->mpad == 8)
+    k_build_lut<8, 64><<<grid, 256, 0, h->stream>>>(w.q8, nslot, h->m, h->kbar, w.lut, ntiles, gword, tf, h->wide,
+                                                    slot_query, slot_live);
+  else if (h->qt == 64)
+    k_build_lut<4, 64><<<grid, 256, 0, h->stream>>>(w.q8, nslot, h->m, h->kbar, w.lut, ntiles, gword, tf, h->wide,
+                                                    slot_query, slot_live);
   else
-    k_build_lut<8><<<grid, 256, 0, h->stream>>>(w.q8, nslot, h->m, h->kbar, w.lut, ntiles, gword, tf, h->wide,
-                                                slot_query, slot_live);
+    k_build_lut<4, 128><<<grid, 256, 0, h->stream>>>(w.q8, nslot, h->m, h->kbar, w.lut, ntiles, gword, tf, h->wide,
+                                                     slot_query, slot_live);
   DPQ_LAUNCHED(h);
   return DPQ_OK;
 }
@@ -432,7 +439,7 @@ struct ScanPlan {
 
 int plan_flat_scan(Index* h, int nb, ScanPlan& sp) {
   Workspace& w = h->ws;
-  const int tiles = tiles_of(nb, h->mpad);
+  const int tiles = tiles_of(nb, h);
   sp.list = h->rows_sorted && h->run_filter && h->m >= 2 && h->n > 0;
   // query tiles clustered by guard class and nearest (g0, g1): feeds the
   // wide loop (MPAD 4) and makes the per-tile run filter selective
@@ -451,8 +458,8 @@ int plan_flat_scan(Index* h, int nb, ScanPlan& sp) {
 
 int prepare_flat_scan(Index* h, int nb, const ScanPlan& sp) {
   Workspace& w = h->ws;
-  const int qt = qt_of(h->mpad);
-  const int tiles = tiles_of(nb, h->mpad);
+  const int qt = qt_of(h);
+  const int tiles = tiles_of(nb, h);
   if (sp.sorted) {
     k_sort_slots<<<1, 1024, 0, h->stream>>>(w.gword, h->m >= 2 ? w.cluster : nullptr, nb, tiles * qt,
                                             w.slot_query, w.gword_p);
@@ -481,8 +488,8 @@ void plan_emit_args(Index* h, const ScanPlan& sp, EmitArgs& ea) {
 
 static int flat_first_pass(Index* h, int nb, int r2) {
   Workspace& w = h->ws;
-  const int qt = qt_of(h->mpad);
-  const int tiles = tiles_of(nb, h->mpad);
+  const int qt = qt_of(h);
+  const int tiles = tiles_of(nb, h);
   // guard words of padding slots never hit: 0x7F7F < 0x8000
   DPQ_CUDA(cudaMemsetAsync(w.gword, 0x7F, (size_t)tiles * qt * 2, h->stream));
   DPQ_CUDA(cudaMemsetAsync(w.hist, 0, (size_t)tiles * qt * 256 * 4, h->stream));
@@ -1079,6 +1086,7 @@ int index_common_init(Index* h, int device, int m, int k, int kbar, int dsub, co
   while ((1 << h->bbar) < kbar) ++h->bbar;
   if (k % kbar) { set_error("k must be a multiple of kbar"); return DPQ_ERR_ARG; }
   h->mpad = m <= 4 ? 4 : 8;
+  h->qt = h->mpad == 4 ? 128 : 64;
   h->code_bytes = code_bytes;
   if (const char* e = getenv("DPQ_GUARD_SAMPLE")) h->sample = std::max<int64_t>(1, atoll(e));
   if (const char* e = getenv("DPQ_EXACT_LIMIT")) h->exact_limit = std::max<int64_t>(0, atoll(e));

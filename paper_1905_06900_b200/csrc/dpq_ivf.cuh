@@ -548,7 +548,7 @@ static int ivf_probe_dev(Index* h, int nb, int ma) {
 
 // Build the slot / tile / unit plan on the host from the probe result.
 static void ivf_plan(Index* h, IvfPlan& P, int nb, int ma, int r2) {
-  const int qt = qt_of(h->mpad);
+  const int qt = qt_of(h);
   const int64_t* off = h->h_offsets.data();
   const int K = h->n_cells;
   P.nq = nb;
@@ -909,7 +909,7 @@ static int ivf_batch(Index* h, int nb, int r, int ma, int r2, bool derived, cons
   Workspace& w = h->ws;
   IvfBuffers& B = ivf_bufs(h);
   const int d = h->d;
-  const int qt = qt_of(h->mpad);
+  const int qt = qt_of(h);
   ev_rec(h, 0);
   IvfPlan& P = B.plan;  // persistent: vectors keep their capacity (no re-faulting per batch)
   DPQ_TRY(ivf_probe_residuals(h, nb, ma, res_rot, cells_in));
@@ -1093,6 +1093,8 @@ int dpq_ivf_create(int device, int m, int k, int kbar, int dsub, const float* co
   if (rc != DPQ_OK) { index_free(h); return rc; }
   h->ivf_state = new IvfBuffers();
   if (const char* e = getenv("DPQ_PROBE_TC")) h->probe_tc = atoi(e);
+  // per-cell tiles: 64 queries per tile for m <= 4 (DPQ_IVF_QT=128: the flat geometry)
+  if (h->mpad == 4) h->qt = getenv("DPQ_IVF_QT") && atoi(getenv("DPQ_IVF_QT")) == 128 ? 128 : 64;
   h->n = n;
   h->n_cells = n_cells;
   h->h_offsets.assign(offsets, offsets + n_cells + 1);
@@ -1312,8 +1314,8 @@ int dpq_shard_begin(dpq_index_t* index, const float* yr, int64_t nq, int r2, int
   const int nb = (int)nq;
   DPQ_TRY(ensure_ws(h, nb, 1, h->d, -1));
   Workspace& w = h->ws;
-  const int qt = qt_of(h->mpad);
-  const int tiles = tiles_of(nb, h->mpad);
+  const int qt = qt_of(h);
+  const int tiles = tiles_of(nb, h);
   DPQ_CUDA(cudaMemcpyAsync(w.y, yr, (size_t)nb * h->d * 4, cudaMemcpyHostToDevice, h->stream));
   DPQ_TRY(run_small_tables(h, nb, h->prefix, npre, nullptr, nullptr, nullptr, false, nullptr));
   DPQ_CUDA(cudaMemsetAsync(w.gword, 0x7F, (size_t)tiles * qt * 2, h->stream));
@@ -1336,7 +1338,7 @@ int dpq_shard_scan(dpq_index_t* index, const int32_t* sample_hist_sum, int64_t n
   cudaSetDevice(h->device);
   const int nb = h->shard_nq;
   Workspace& w = h->ws;
-  const int tiles = tiles_of(nb, h->mpad);
+  const int tiles = tiles_of(nb, h);
   DPQ_CUDA(cudaMemcpyAsync(w.hist, sample_hist_sum, (size_t)nb * 256 * 4, cudaMemcpyHostToDevice, h->stream));
   const bool ex = exact || n_global <= h->exact_limit;
   const double lambda = (double)r2 * (double)sample_global / (double)std::max<int64_t>(n_global, 1);
@@ -1437,8 +1439,8 @@ int dpq_shard_begin_dev(dpq_index_t* index, const float* yr, int64_t nq, int r2,
   const int nb = (int)nq;
   DPQ_TRY(ensure_ws(h, nb, 1, h->d, -1));
   Workspace& w = h->ws;
-  const int qt = qt_of(h->mpad);
-  const int tiles = tiles_of(nb, h->mpad);
+  const int qt = qt_of(h);
+  const int tiles = tiles_of(nb, h);
   DPQ_CUDA(cudaMemcpyAsync(w.y, yr, (size_t)nb * h->d * 4, cudaMemcpyDeviceToDevice, h->stream));
   DPQ_TRY(run_small_tables(h, nb, h->prefix, npre, nullptr, nullptr, nullptr, false, nullptr));
   DPQ_CUDA(cudaMemsetAsync(w.gword, 0x7F, (size_t)tiles * qt * 2, h->stream));
@@ -1461,7 +1463,7 @@ int dpq_shard_scan_dev(dpq_index_t* index, const int32_t* sample_hist_sum, int64
   cudaSetDevice(h->device);
   const int nb = h->shard_nq;
   Workspace& w = h->ws;
-  const int tiles = tiles_of(nb, h->mpad);
+  const int tiles = tiles_of(nb, h);
   DPQ_CUDA(cudaMemcpyAsync(w.hist, sample_hist_sum, (size_t)nb * 256 * 4, cudaMemcpyDeviceToDevice, h->stream));
   const bool ex = exact || n_global <= h->exact_limit;
   const double lambda = (double)r2 * (double)sample_global / (double)std::max<int64_t>(n_global, 1);

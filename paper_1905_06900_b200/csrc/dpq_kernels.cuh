@@ -80,13 +80,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-template <int MPAD>
+// Tile geometry: MPAD subspaces (4 or 8) x QT queries.  Flat m <= 4 uses
+// QT = 128; IVF m <= 4 uses QT = 64 (per-cell tiles are ~25-45% occupied at
+// QT = 128, so halving the tile halves the padding work); m = 8 uses 64.
+constexpr int default_qt(int mpad) { return mpad == 4 ? 128 : 64; }
+template <int MPAD, int QTX = default_qt(MPAD)>
 struct ScanGeom {
-  static constexpr int QT = MPAD == 4 ? 128 : 64;  // queries per tile
+  static constexpr int QT = QTX;                   // queries per tile
   static constexpr int LPC = QT / 4;               // lanes per code (4 queries/lane)
   static constexpr int CPW = 32 / LPC;             // codes per warp step
   static constexpr int ROWB = QT;                  // bytes of one subspace row (u8)
   static constexpr int SPR = 256 / ROWB;           // subspaces per 256-B row
+  static constexpr int CPL = (16 / MPAD) / CPW;    // codes per lane in one 16-B plane word group
   static constexpr int LUT_BYTES = MPAD * 256 * ROWB;  // 128 KB
   static constexpr int CHUNK_ROWS = 512 / MPAD;    // rows per 512-B warp load
 };
@@ -337,7 +342,7 @@ __device__ __forceinline__ uint32_t wide_bias(uint32_t gw) {  // C of one slot
   return gw >= 0x8000u ? 127u - (gw - 0x8000u) : 128u;
 }
 
-template <int MPAD>
+template <int MPAD, int QTX = default_qt(MPAD)>
 __global__ void __launch_bounds__(256) k_build_lut(const uint8_t* __restrict__ q8, int nslot, int m, int kbar,
                                                    uint8_t* __restrict__ lut, int ntiles,
                                                    const uint16_t* __restrict__ gword, int* __restrict__ tile_fast,
@@ -347,7 +352,7 @@ __global__ void __launch_bounds__(256) k_build_lut(const uint8_t* __restrict__ q
   // staged in shared memory ([slot][group], rows padded to 65 words so the
   // transposed reads below are conflict-free), then written as the tile's
   // 256 table rows of QT bytes with coalesced 32-bit stores.
-  using G = ScanGeom<MPAD>;
+  using G = ScanGeom<MPAD, QTX>;
   constexpr int RW = 65;  // words per staged row (256 groups + pad)
   __shared__ uint32_t st[G::QT * RW];
   __shared__ uint32_t s_bmax;
@@ -387,8 +392,8 @@ __global__ void __launch_bounds__(256) k_build_lut(const uint8_t* __restrict__ q
   int mode = kModeGeneric;
   if (gword) {
     const uint32_t bmax = s_bmax;
-    if (MPAD == 4 && allow_wide && bmax <= 30u) mode = kModeWide5;
-    else if (MPAD == 4 && allow_wide && bmax <= 62u) mode = kModeWide6;
+    if (MPAD == 4 && G::QT == 128 && allow_wide && bmax <= 30u) mode = kModeWide5;
+    else if (MPAD == 4 && G::QT == 128 && allow_wide && bmax <= 62u) mode = kModeWide6;
     else if (bmax <= kClampMaxGuard) mode = kMode7;
   }
   const uint32_t cmax = mode == kModeWide5 ? 31u : (mode == kModeWide6 ? 63u : (mode == kMode7 ? 127u : 255u));
@@ -576,10 +581,10 @@ __global__ void __launch_bounds__(256) k_chunk_list(const uint32_t* __restrict__
 // ============================================================================
 struct Sum4 { uint32_t lo, hi; };  // u16x2: queries (0,2) and (1,3) of a lane
 
-template <int MPAD>
+template <int MPAD, int QTX = default_qt(MPAD)>
 __device__ __forceinline__ Sum4 lut_sum(const uint8_t* L, uint32_t w0, uint32_t w1) {
   // L = tile base + lic * 4 (generic addressing; used off the hot path)
-  using G = ScanGeom<MPAD>;
+  using G = ScanGeom<MPAD, QTX>;
   Sum4 s{0u, 0u};
 #pragma unroll
   for (int j = 0; j < MPAD; ++j) {
@@ -601,9 +606,9 @@ __device__ __forceinline__ uint32_t fma_add(uint32_t a, uint32_t b, uint32_t c) 
 }
 
 // Hot-path variant: base = 64-KB aligned shared address | lic * 4.
-template <int MPAD>
+template <int MPAD, int QTX = default_qt(MPAD)>
 __device__ __forceinline__ Sum4 lut_sum_fast(uint32_t base, uint32_t w0, uint32_t w1, uint32_t one) {
-  using G = ScanGeom<MPAD>;
+  using G = ScanGeom<MPAD, QTX>;
   Sum4 s{0u, 0u};
 #pragma unroll
   for (int j = 0; j < MPAD; ++j) {
@@ -627,12 +632,14 @@ __device__ __forceinline__ Sum4 lut_sum_fast(uint32_t base, uint32_t w0, uint32_
 // Fast variant for 7-bit (clamped) tiles, MPAD = 4: add the words of
 // subspaces (0,1) and (2,3) first (bytes <= 254, no carries), then split the
 // two pair sums.
+template <int QTX = 128>
 __device__ __forceinline__ Sum4 lut_sum_fast7(uint32_t base, uint32_t w, uint32_t one) {
+  using G = ScanGeom<4, QTX>;
   uint32_t v[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const uint32_t a = __byte_perm(w, base + (j % 2) * 128, 0x7604u | ((j & 3) << 4));
-    if (j < 2) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v[j]) : "r"(a));
+    const uint32_t a = __byte_perm(w, base + (j % G::SPR) * G::ROWB, 0x7604u | ((j & 3) << 4));
+    if (j / G::SPR == 0) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v[j]) : "r"(a));
     else asm volatile("ld.shared.u32 %0, [%1+65536];" : "=r"(v[j]) : "r"(a));
   }
   const uint32_t p01 = fma_add(v[0], one, v[1]), p23 = fma_add(v[2], one, v[3]);
@@ -686,13 +693,13 @@ __device__ __forceinline__ uint32_t sum_of(Sum4 s, int qsel) {
 // kHistRowsPerCta rows so no counter can wrap.
 constexpr int64_t kHistRowsPerCta = 65535;
 
-template <int MPAD, int NT>
+template <int MPAD, int NT, int QTX = default_qt(MPAD)>
 __global__ void __launch_bounds__(NT, 1)
     k_scan_hist(const uint8_t* __restrict__ plane, int64_t stride, int64_t n_samp,
                 int64_t samp_per_cta, const uint8_t* __restrict__ lut,
                 const int* __restrict__ tile_list, uint32_t* __restrict__ hist,
                 const int64_t* __restrict__ tile_row0, const int64_t* __restrict__ tile_nsamp) {
-  using G = ScanGeom<MPAD>;
+  using G = ScanGeom<MPAD, QTX>;
   extern __shared__ __align__(16) uint8_t smem[];
   uint8_t* slut = smem;
   uint32_t* sh = reinterpret_cast<uint32_t*>(smem + G::LUT_BYTES);  // [QT][128] u16 pairs
@@ -731,7 +738,7 @@ __global__ void __launch_bounds__(NT, 1)
       const uint32_t c0 = __shfl_sync(0xffffffffu, w0, src_lane);
       const uint32_t c1 = __shfl_sync(0xffffffffu, w1, src_lane);
       if (src_lane < cnt) {
-        const Sum4 sm = lut_sum<MPAD>(L, c0, c1);
+        const Sum4 sm = lut_sum<MPAD, QTX>(L, c0, c1);
 #pragma unroll
         for (int qs = 0; qs < 4; ++qs) bump(4 * lic + qs, sum_of(sm, qs));
       }
@@ -807,16 +814,17 @@ constexpr uint32_t kLutShared = 0x10000;  // LUT at shared address 64 KB
 // per-warp hit counters above it.
 template <int MPAD, int NT>
 __host__ __device__ constexpr int emit_low_bytes() { return (NT / 32) * (32 * 16 + kWarpBuf * 8); }
+// (QT-independent)
 constexpr int kLaneQ = 8;  // lane-private hit records per chunk (u16 each)
-template <int MPAD, int NT>
+template <int MPAD, int NT, int QTX = default_qt(MPAD)>
 __host__ __device__ constexpr int emit_smem_bytes() {
-  return (int)kLutShared + ScanGeom<MPAD>::LUT_BYTES + (NT / 32) * ScanGeom<MPAD>::QT * 4 +
+  return (int)kLutShared + ScanGeom<MPAD, QTX>::LUT_BYTES + (NT / 32) * ScanGeom<MPAD, QTX>::QT * 4 +
          (NT / 32) * kLaneQ * 32 * 2;
 }
 
-template <int MPAD, int NT>
+template <int MPAD, int NT, int QTX = default_qt(MPAD)>
 __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
-  using G = ScanGeom<MPAD>;
+  using G = ScanGeom<MPAD, QTX>;
   constexpr int NW = NT / 32;
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ int s_unit;
@@ -909,7 +917,7 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
     }
     const int tmode = a.tile_fast != nullptr ? a.tile_fast[tile] : kModeGeneric;
     const bool fast_tile = tmode == kMode7;
-    const bool wide = MPAD == 4 && (tmode == kModeWide5 || tmode == kModeWide6);
+    const bool wide = MPAD == 4 && G::QT == 128 && (tmode == kModeWide5 || tmode == kModeWide6);
     const int q0 = tile * G::QT + 4 * lic;
     const uint32_t glo = (uint32_t)a.gword[q0] | ((uint32_t)a.gword[q0 + 2] << 16);
     const uint32_t ghi = (uint32_t)a.gword[q0 + 1] | ((uint32_t)a.gword[q0 + 3] << 16);
@@ -1032,7 +1040,7 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
       const uint32_t lo = edge ? (uint32_t)max((int64_t)0, r0 - rb) : 0u;
       const uint32_t hi = edge ? (uint32_t)min((int64_t)G::CHUNK_ROWS, r1 - rb) : (uint32_t)G::CHUNK_ROWS;
       const uint32_t rboff = (uint32_t)(rb - r0a);
-      if constexpr (MPAD == 4) {
+      if constexpr (MPAD == 4 && G::QT == 128) {
         if (wide) {
           // Wide loop: quarter qd scans rows 32qd .. 32qd+31 of the chunk,
           // one row per step; each lane sums its 16 queries with 4 x LDS.128
@@ -1179,14 +1187,28 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
           continue;
         }
       }
+      // the lane's code k (< G::CPL) of the 16-B plane group v and its row in the chunk:
+      // (4, 128) all lanes read the group's 4 codes; (4, 64) half-warps read 2 codes each;
+      // MPAD = 8 half-warps read one 8-byte code each
+      auto wsel = [&](const uint4 v, int k, uint32_t& w0, uint32_t& w1) {
+        if constexpr (MPAD == 8) {
+          w0 = half ? v.z : v.x;
+          w1 = half ? v.w : v.y;
+        } else {
+          const int c = half * G::CPL + k;
+          w0 = c == 0 ? v.x : (c == 1 ? v.y : (c == 2 ? v.z : v.w));
+          w1 = 0u;
+        }
+      };
+      auto rowof = [&](int i, int k) -> uint32_t { return (uint32_t)((16 / MPAD) * i + half * G::CPL + k); };
       auto group4 = [&](const uint4 v, int i, auto fast7) {
         Sum4 s0, s1, s2, s3;
         if constexpr (decltype(fast7)::value) {
-          s0 = lut_sum_fast7(lbase, v.x, one); s1 = lut_sum_fast7(lbase, v.y, one);
-          s2 = lut_sum_fast7(lbase, v.z, one); s3 = lut_sum_fast7(lbase, v.w, one);
+          s0 = lut_sum_fast7<QTX>(lbase, v.x, one); s1 = lut_sum_fast7<QTX>(lbase, v.y, one);
+          s2 = lut_sum_fast7<QTX>(lbase, v.z, one); s3 = lut_sum_fast7<QTX>(lbase, v.w, one);
         } else {
-          s0 = lut_sum_fast<MPAD>(lbase, v.x, 0, one); s1 = lut_sum_fast<MPAD>(lbase, v.y, 0, one);
-          s2 = lut_sum_fast<MPAD>(lbase, v.z, 0, one); s3 = lut_sum_fast<MPAD>(lbase, v.w, 0, one);
+          s0 = lut_sum_fast<MPAD, QTX>(lbase, v.x, 0, one); s1 = lut_sum_fast<MPAD, QTX>(lbase, v.y, 0, one);
+          s2 = lut_sum_fast<MPAD, QTX>(lbase, v.z, 0, one); s3 = lut_sum_fast<MPAD, QTX>(lbase, v.w, 0, one);
         }
         const uint32_t xl0 = fma_add(s0.lo, mone, glo), xh0 = fma_add(s0.hi, mone, ghi);
         const uint32_t xl1 = fma_add(s1.lo, mone, glo), xh1 = fma_add(s1.hi, mone, ghi);
@@ -1197,28 +1219,41 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
         if ((xl2 | xh2) & 0x80008000u) record(xl2, xh2, i, 2);
         if ((xl3 | xh3) & 0x80008000u) record(xl3, xh3, i, 3);
       };
-      if (MPAD == 4 && fast_tile) {
-#pragma unroll 2
-        for (int i = 0; i < 32; ++i) group4(wst[i], i, std::integral_constant<bool, true>());
-      } else
-#pragma unroll 2
-      for (int i = 0; i < 32; ++i) {
-        const uint4 v = wst[i];
-        if (MPAD == 4) {
-          const Sum4 s0 = lut_sum_fast<MPAD>(lbase, v.x, 0, one), s1 = lut_sum_fast<MPAD>(lbase, v.y, 0, one);
-          const Sum4 s2 = lut_sum_fast<MPAD>(lbase, v.z, 0, one), s3 = lut_sum_fast<MPAD>(lbase, v.w, 0, one);
-          const uint32_t xl0 = fma_add(s0.lo, mone, glo), xh0 = fma_add(s0.hi, mone, ghi);
-          const uint32_t xl1 = fma_add(s1.lo, mone, glo), xh1 = fma_add(s1.hi, mone, ghi);
-          const uint32_t xl2 = fma_add(s2.lo, mone, glo), xh2 = fma_add(s2.hi, mone, ghi);
-          const uint32_t xl3 = fma_add(s3.lo, mone, glo), xh3 = fma_add(s3.hi, mone, ghi);
-          if ((xl0 | xh0) & 0x80008000u) record(xl0, xh0, i, 0);
-          if ((xl1 | xh1) & 0x80008000u) record(xl1, xh1, i, 1);
-          if ((xl2 | xh2) & 0x80008000u) record(xl2, xh2, i, 2);
-          if ((xl3 | xh3) & 0x80008000u) record(xl3, xh3, i, 3);
+      auto group2 = [&](const uint4 v, int i, auto fast7) {  // (4, 64): this half-warp's two codes
+        const uint32_t wa = half ? v.z : v.x, wb = half ? v.w : v.y;
+        Sum4 s0, s1;
+        if constexpr (decltype(fast7)::value) {
+          s0 = lut_sum_fast7<QTX>(lbase, wa, one); s1 = lut_sum_fast7<QTX>(lbase, wb, one);
         } else {
-          const uint32_t w0 = half ? v.z : v.x;
-          const uint32_t w1 = half ? v.w : v.y;
-          const Sum4 s0 = lut_sum_fast<MPAD>(lbase, w0, w1, one);
+          s0 = lut_sum_fast<MPAD, QTX>(lbase, wa, 0, one); s1 = lut_sum_fast<MPAD, QTX>(lbase, wb, 0, one);
+        }
+        const uint32_t xl0 = fma_add(s0.lo, mone, glo), xh0 = fma_add(s0.hi, mone, ghi);
+        const uint32_t xl1 = fma_add(s1.lo, mone, glo), xh1 = fma_add(s1.hi, mone, ghi);
+        if ((xl0 | xh0) & 0x80008000u) record(xl0, xh0, i, 0);
+        if ((xl1 | xh1) & 0x80008000u) record(xl1, xh1, i, 1);
+      };
+      if constexpr (MPAD == 4 && G::CPL == 4) {
+        if (fast_tile) {
+#pragma unroll 2
+          for (int i = 0; i < 32; ++i) group4(wst[i], i, std::integral_constant<bool, true>());
+        } else {
+#pragma unroll 2
+          for (int i = 0; i < 32; ++i) group4(wst[i], i, std::integral_constant<bool, false>());
+        }
+      } else if constexpr (MPAD == 4) {
+        if (fast_tile) {
+#pragma unroll 2
+          for (int i = 0; i < 32; ++i) group2(wst[i], i, std::integral_constant<bool, true>());
+        } else {
+#pragma unroll 2
+          for (int i = 0; i < 32; ++i) group2(wst[i], i, std::integral_constant<bool, false>());
+        }
+      } else {
+#pragma unroll 2
+        for (int i = 0; i < 32; ++i) {
+          uint32_t w0, w1;
+          wsel(wst[i], 0, w0, w1);
+          const Sum4 s0 = lut_sum_fast<MPAD, QTX>(lbase, w0, w1, one);
           const uint32_t xl0 = fma_add(s0.lo, mone, glo), xh0 = fma_add(s0.hi, mone, ghi);
           if ((xl0 | xh0) & 0x80008000u) record(xl0, xh0, i, 0);
         }
@@ -1230,12 +1265,11 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
           // chunk with warp-wide staging (exact, just slower)
           for (int i = 0; i < 32; ++i) {
             const uint4 v = wst[i];
-            for (int k = 0; k < (MPAD == 4 ? 4 : 1); ++k) {
-              uint32_t w0, w1 = 0;
-              if (MPAD == 4) w0 = k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
-              else { w0 = half ? v.z : v.x; w1 = half ? v.w : v.y; }
-              const uint32_t r = MPAD == 4 ? 4 * i + k : 2 * i + half;
-              const Sum4 sm = lut_sum_fast<MPAD>(lbase, w0, w1, one);
+            for (int k = 0; k < G::CPL; ++k) {
+              uint32_t w0, w1;
+              wsel(v, k, w0, w1);
+              const uint32_t r = rowof(i, k);
+              const Sum4 sm = lut_sum_fast<MPAD, QTX>(lbase, w0, w1, one);
               uint32_t hm = bits_x(glo - sm.lo, ghi - sm.hi);
               if (edge && !(r >= lo && r < hi)) hm = 0u;
               stage_hits(hm, sm, sm, sm, sm, rboff + r);
@@ -1249,13 +1283,11 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
             if (has) {
               const uint32_t rec = lq[e * 32];
               const int i = (int)(rec >> 4), k = (int)((rec >> 2) & 3), qs = (int)(rec & 3);
-              const uint4 v = wst[i];
-              uint32_t w0, w1 = 0;
-              if (MPAD == 4) w0 = k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
-              else { w0 = half ? v.z : v.x; w1 = half ? v.w : v.y; }
-              const uint32_t r = MPAD == 4 ? 4 * i + k : 2 * i + half;
+              uint32_t w0, w1;
+              wsel(wst[i], k, w0, w1);
+              const uint32_t r = rowof(i, k);
               has = !edge || (r >= lo && r < hi);
-              sc = sum_of(lut_sum_fast<MPAD>(lbase, w0, w1, one), qs);
+              sc = sum_of(lut_sum_fast<MPAD, QTX>(lbase, w0, w1, one), qs);
               roff = rboff + r;
               slot = 4 * lic + qs;
             }
