@@ -150,67 +150,137 @@ __global__ void __launch_bounds__(NT, 1) k_probe_select(const double* __restrict
 // Tensor-core probe (ivf.py:107-120 on the 5th-generation tensor cores).
 // The squared distances of a query to all K centres come from the 3xTF32
 // table GEMM of dpq_tctab.cu (centres = an m = 1 codebook, kbar = 1, so the
-// entries are in centre order) together with a rigorous per-entry bound
-// E_c = gamma (||y - mu|| + ||c - mu||)^2 >= |approx_c - d2_c|.  Per query:
-// tau = the ma-th smallest upper bound approx + E; every centre whose lower
-// bound approx - E is <= tau is a candidate (a superset of the exact ma
-// nearest), its d2 is recomputed exactly with k_probe_dist's f64 arithmetic,
-// and the ma smallest (d2, cell) pairs are kept — the same cells in the same
-// order as the all-f64 probe, from ~ma exact distances instead of K.
-template <int NT, int EPT>
-__global__ void __launch_bounds__(NT, 1) k_probe_select_tc(const float* __restrict__ approx, const double* __restrict__ ny,
-                                                           const float* __restrict__ cnorm, double gamma,
-                                                           const float* __restrict__ y, int d,
-                                                           const float* __restrict__ centers, int K, int ma,
-                                                           int64_t* __restrict__ cells,
-                                                           unsigned long long* __restrict__ n_exact) {
-  extern __shared__ __align__(16) uint8_t probe_smem[];
-  uint64_t* keys = reinterpret_cast<uint64_t*>(probe_smem);
-  int64_t* ids = reinterpret_cast<int64_t*>(keys + NT * EPT);
-  __shared__ SelShared S;
-  __shared__ uint64_t thr_k;
-  __shared__ int64_t thr_i;
+// entries are in centre order) with rigorous bounds: |approx_c - d2_c| <=
+// E_c = gamma (||y - mu|| + ||c - mu||)^2 <= eps (the query's bound with
+// the largest centre norm).  Per query (one 256-thread CTA, K <= 8192):
+// A = the ma-th smallest approx (4-pass radix select on order-preserving
+// 32-bit keys), tau = A + eps >= the ma-th smallest upper bound, candidates
+// = {c : approx_c - E_c <= tau} (a superset of the exact ma nearest); their
+// d2 is recomputed with k_probe_dist's f64 arithmetic and the ma smallest
+// (d2, cell) pairs are written in order — the f64 probe's cells, from ~ma
+// exact distances instead of K.  More than kPtcCand candidates (not seen):
+// every centre is recomputed exactly.
+constexpr int kPtcThreads = 256, kPtcEpt = 32, kPtcCand = 1024;
+__device__ __forceinline__ uint32_t f32_order_key(float f) {
+  const uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__global__ void __launch_bounds__(kPtcThreads) k_probe_select_tc(const float* __restrict__ approx,
+                                                                 const double* __restrict__ eps,
+                                                                 const double* __restrict__ ny,
+                                                                 const float* __restrict__ cnorm, double gamma,
+                                                                 const float* __restrict__ y, int d,
+                                                                 const float* __restrict__ centers, int K, int ma,
+                                                                 int64_t* __restrict__ cells,
+                                                                 unsigned long long* __restrict__ n_exact) {
+  __shared__ uint32_t hist[256];
+  __shared__ uint32_t s_pfx, s_need;
   __shared__ int ncand;
-  __shared__ float ys[512];
-  const int q = blockIdx.x;
+  __shared__ uint64_t ckey[kPtcCand];
+  __shared__ int64_t cid[kPtcCand];
+  __shared__ float ys[128];
+  const int q = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const float* aq = approx + (int64_t)q * K;
-  const double nyq = ny[q];
-  auto bound = [&](int c) {
-    const double s = nyq + (double)cnorm[c];
-    return gamma * s * s * (1.0 + 1e-9) + 1e-300;
-  };
-  for (int i = threadIdx.x; i < K; i += NT) {
-    const double u = fmax((double)aq[i] + bound(i), 0.0);
-    keys[i] = (uint64_t)__double_as_longlong(u);
-    ids[i] = i;
+  uint32_t key[kPtcEpt];
+#pragma unroll
+  for (int e = 0; e < kPtcEpt; ++e) {
+    const int c = tid + e * kPtcThreads;
+    key[e] = c < K ? f32_order_key(aq[c]) : 0xFFFFFFFFu;
   }
-  for (int i = threadIdx.x; i < d; i += NT) ys[i] = y[(int64_t)q * d + i];
-  if (threadIdx.x == 0) { ncand = 0; thr_k = ~0ull; }
-  __syncthreads();
-  if (K > ma) select_r<NT, EPT>(keys, ids, K, ma, S, thr_k, thr_i);
-  const double tau = K > ma ? __longlong_as_double((long long)thr_k) : INFINITY;
-  __syncthreads();
-  for (int i = threadIdx.x; i < K; i += NT)
-    if ((double)aq[i] - bound(i) <= tau) ids[atomicAdd(&ncand, 1)] = i;
+  for (int i = tid; i < d; i += kPtcThreads) ys[i] = y[(int64_t)q * d + i];
+  if (tid == 0) { s_pfx = 0u; s_need = (uint32_t)ma; ncand = 0; }
+  // the ma-th smallest key: 4 digit passes (prefix known above the digit)
+  for (int pass = 0; pass < 4; ++pass) {
+    const int sft = 24 - 8 * pass;
+    for (int i = tid; i < 256; i += kPtcThreads) hist[i] = 0u;
+    __syncthreads();
+    const uint32_t pfx = s_pfx, hmask = pass == 0 ? 0u : (0xFFFFFFFFu << (sft + 8));
+#pragma unroll
+    for (int e = 0; e < kPtcEpt; ++e)
+      if ((key[e] & hmask) == pfx && tid + e * kPtcThreads < K) atomicAdd(&hist[(key[e] >> sft) & 0xFFu], 1u);
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t need = s_need;
+      uint32_t ls = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) ls += hist[lane * 8 + i];
+      uint32_t incl = ls;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      const int L = __ffs(__ballot_sync(0xffffffffu, incl >= need)) - 1;
+      if (lane == L) {
+        uint32_t below = incl - ls;
+        int dg = lane * 8;
+        for (int i = 0; i < 8; ++i) {
+          const uint32_t hb = hist[lane * 8 + i];
+          if (below + hb >= need) { dg = lane * 8 + i; break; }
+          below += hb;
+        }
+        s_need = need - below;
+        s_pfx = pfx | ((uint32_t)dg << sft);
+      }
+    }
+    __syncthreads();
+  }
+  const uint32_t kth = s_pfx;
+  const float A = __uint_as_float((kth & 0x80000000u) ? (kth & 0x7FFFFFFFu) : ~kth);
+  const double tau = (double)A + eps[q] * (1.0 + 1e-9);
+  const double nyq = ny[q];
+  const double loose = tau + eps[q] * (1.0 + 1e-9);  // approx_c <= tau + E_c <= tau + eps
+#pragma unroll
+  for (int e = 0; e < kPtcEpt; ++e) {
+    const int c = tid + e * kPtcThreads;
+    if (c < K) {
+      const double a = (double)aq[c];
+      if (a <= loose) {
+        const double sn = nyq + (double)cnorm[c];
+        if (a - gamma * sn * sn * (1.0 + 1e-9) <= tau) {
+          const int p = atomicAdd(&ncand, 1);
+          if (p < kPtcCand) cid[p] = c;
+        }
+      }
+    }
+  }
   __syncthreads();
   const int nc = ncand;
-  for (int i = threadIdx.x; i < nc; i += NT) {  // k_probe_dist's arithmetic, one thread per candidate
-    const int c = (int)ids[i];
+  auto exact = [&](int c) {  // k_probe_dist's arithmetic (sequential f64)
     const float* cr = centers + (int64_t)c * d;
     double acc = 0.0;
     for (int t = 0; t < d; ++t) {
       const double df = __dsub_rn((double)cr[t], (double)ys[t]);
       acc = __dadd_rn(acc, __dmul_rn(df, df));
     }
-    keys[i] = (uint64_t)__double_as_longlong(acc);
+    return acc;
+  };
+  if (nc <= kPtcCand) {
+    for (int i = tid; i < nc; i += kPtcThreads) ckey[i] = (uint64_t)__double_as_longlong(exact((int)cid[i]));
+    int P = 2;
+    while (P < nc) P <<= 1;
+    for (int i = nc + tid; i < P; i += kPtcThreads) { ckey[i] = ~0ull; cid[i] = INT64_MAX; }
+    __syncthreads();
+    sort_pairs<kPtcThreads>(ckey, cid, P);
+    for (int i = tid; i < ma; i += kPtcThreads) cells[(int64_t)q * ma + i] = cid[i];
+  } else {
+    // (degenerate bounds) exact top-ma of all K: running buffer of kPtcCand / 2
+    const int half = kPtcCand / 2;
+    int fill = 0;
+    for (int base = 0; base < K; base += half) {
+      const int n = min(half, K - base);
+      for (int i = tid; i < n; i += kPtcThreads) {
+        ckey[fill + i] = (uint64_t)__double_as_longlong(exact(base + i));
+        cid[fill + i] = base + i;
+      }
+      for (int i = fill + n + tid; i < kPtcCand; i += kPtcThreads) { ckey[i] = ~0ull; cid[i] = INT64_MAX; }
+      __syncthreads();
+      sort_pairs<kPtcThreads>(ckey, cid, kPtcCand);
+      fill = min(ma, fill + n);
+    }
+    for (int i = tid; i < ma; i += kPtcThreads) cells[(int64_t)q * ma + i] = cid[i];
   }
-  int P = 2;
-  while (P < nc) P <<= 1;
-  for (int i = nc + threadIdx.x; i < P; i += NT) { keys[i] = ~0ull; ids[i] = INT64_MAX; }
-  __syncthreads();
-  sort_pairs<NT>(keys, ids, P);
-  for (int i = threadIdx.x; i < ma; i += NT) cells[(int64_t)q * ma + i] = ids[i];
-  if (threadIdx.x == 0 && n_exact) atomicAdd(n_exact, (unsigned long long)nc);
+  if (tid == 0 && n_exact) atomicAdd(n_exact, (unsigned long long)(nc <= kPtcCand ? nc : K));
 }
 
 // residuals y - centre in f32 (ivf.py:120), natural (query, probe) order
@@ -482,7 +552,7 @@ static int ivf_probe_dev(Index* h, int nb, int ma) {
   // tensor-core probe (h->probe_tc: 0 off, 1 auto = K >= 1024, 2 forced)
   const int probe_tc = h->probe_tc;
   const int K = h->n_cells;
-  if (nb > 0 && K <= 8192 && h->d <= 128 && ma < K && tct_supported(1, K, 1, h->d) &&
+  if (nb > 0 && K <= 8192 && h->d <= 128 && ma < K && ma <= kPtcCand / 2 && tct_supported(1, K, 1, h->d) &&
       (probe_tc == 2 || (probe_tc == 1 && K >= 1024))) {
     if (b.ptc_state == 0)
       b.ptc_state = tct_prepare(h->device, h->centers, 1, K, 1, h->d, h->stream, &b.ptc) == DPQ_OK ? 1 : -1;
@@ -503,11 +573,9 @@ static int ivf_probe_dev(Index* h, int nb, int ma) {
       }
       DPQ_TRY(tct_build(b.ptc, h->ws.y, h->d, nb, b.papprox, b.peps, b.pny, 1.0, h->stream));
       DPQ_LAUNCHED(h);
-      const size_t smem = (size_t)1024 * 8 * 16;
-      DPQ_TRY(set_smem(h, k_probe_select_tc<1024, 8>, smem));
-      k_probe_select_tc<1024, 8><<<nb, 1024, smem, h->stream>>>(b.papprox, b.pny, tct_cnorm(b.ptc),
-                                                                tct_gamma(b.ptc, 1.0), h->ws.y, h->d, h->centers, K,
-                                                                ma, b.cells, h->d_nrows + 4);
+      k_probe_select_tc<<<nb, kPtcThreads, 0, h->stream>>>(b.papprox, b.peps, b.pny, tct_cnorm(b.ptc),
+                                                           tct_gamma(b.ptc, 1.0), h->ws.y, h->d, h->centers, K, ma,
+                                                           b.cells, h->d_nrows + 4);
       DPQ_LAUNCHED(h);
       return DPQ_OK;
     }
