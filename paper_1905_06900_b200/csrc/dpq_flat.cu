@@ -515,7 +515,7 @@ static int flat_first_pass(Index* h, int nb, int r2) {
     ea.lut = w.lut; ea.tile_list = nullptr; ea.slot_probe = nullptr;
     plan_emit_args(h, sp, ea);
     ea.unit_tile = nullptr; ea.unit_r0 = nullptr; ea.unit_r1 = nullptr;
-    ea.emit_cnt = w.emit_cnt; ea.emit = w.emit; ea.cap = w.cap;
+    ea.emit_cnt = w.emit_cnt; ea.emit = w.emit; ea.cap = w.cap; ea.emit32 = (int)h->emit32;
     DPQ_TRY(launch_emit(h, ea, tiles, n));
     if (!sp.list) {  // (list mode: counted on the device)
       h->counters[2] += (int64_t)nb * n;
@@ -523,7 +523,7 @@ static int flat_first_pass(Index* h, int nb, int r2) {
     }
     if (first) ev_rec(h, 3);
     k_threshold<256><<<nb, 256, 0, h->stream>>>(w.emit, w.emit_cnt, w.cap, w.guard_b, r2, nullptr,
-                                                w.bstar, w.ncand, w.flags, nullptr, h->d_nemit);
+                                                w.bstar, w.ncand, w.flags, nullptr, h->d_nemit, (int)h->emit32);
     DPQ_LAUNCHED(h);
     if (first) ev_rec(h, 4);
     first = false;
@@ -581,7 +581,7 @@ static int flat_first_pass(Index* h, int nb, int r2) {
 static RefineArgs make_refine_args(Index* h, int r) {
   Workspace& w = h->ws;
   RefineArgs ra;
-  ra.emit = w.emit; ra.emit_cnt = w.emit_cnt; ra.cap = w.cap; ra.bstar = w.bstar;
+  ra.emit = w.emit; ra.emit_cnt = w.emit_cnt; ra.cap = w.cap; ra.bstar = w.bstar; ra.emit32 = (int)h->emit32;
   ra.n_rows = h->n;
   ra.codes = h->codes; ra.code_bytes = h->code_bytes; ra.m = h->m; ra.k = h->k; ra.dsub = h->dsub;
   ra.kbar = h->kbar; ra.bbar = h->bbar;
@@ -745,7 +745,7 @@ static int flat_derived_batch_body(Index* h, int nb, int r, int r2) {
   } else if (group_tables_fit(h, nb)) {
     DPQ_TRY(run_group_tables(h, nb, h->d));
     ra.tables = h->ws.tables;  // (re)allocated by run_group_tables
-    DPQ_TRY(launch_refine<MODE_EMIT_TABLE>(h, ra, nb));
+    DPQ_TRY(h->emit32 ? launch_refine<MODE_EMIT_TABLE32>(h, ra, nb) : launch_refine<MODE_EMIT_TABLE>(h, ra, nb));
   } else {
     DPQ_TRY(launch_refine<MODE_EMIT>(h, ra, nb));  // entries computed per candidate
   }
@@ -1246,6 +1246,10 @@ int dpq_flat_create(int device, int m, int k, int kbar, int dsub, const float* c
     h->prefix = h->codes;
     h->n_prefix = n;
   }
+  // compact 4-byte emit records when every shard row fits in 24 bits, for the PQ 4x16 layout whose
+  // table refine is the software-pipelined loop (DPQ_EMIT32=0: 8-byte records)
+  h->emit32 = n < ((int64_t)1 << kRow32Bits) && m == 4 && code_bytes == 2 &&
+              !(getenv("DPQ_EMIT32") && atoi(getenv("DPQ_EMIT32")) == 0);
   if (h->sort_rows && m >= 2 && n > 1 && n < ((int64_t)1 << 31) &&
       (rc = sort_rows(h)) != DPQ_OK) { index_free(h); return rc; }
   if ((rc = make_plane(h)) != DPQ_OK) { index_free(h); return rc; }
@@ -1471,10 +1475,12 @@ int dpq_debug_candidate_ids(dpq_index_t* index, const float* yr, int64_t nq, int
     DPQ_CUDA(cudaMemcpyAsync(w.y, yr + q0 * h->d, (size_t)nb * h->d * 4, cudaMemcpyHostToDevice, h->stream));
     DPQ_TRY(run_small_tables(h, nb, h->prefix, std::min<int64_t>(r2, h->n_prefix), nullptr, nullptr, nullptr,
                              false, nullptr));
-    const bool ns = h->no_spec;
+    const bool ns = h->no_spec, e32 = h->emit32;
     h->no_spec = true;  // exact b* needed right here
+    h->emit32 = false;  // k_emit_keys rewrites 8-byte records in place
     int rc = flat_first_pass(h, nb, r2);
     h->no_spec = ns;
+    h->emit32 = e32;
     if (rc == 100) { set_error("debug_candidate_ids: emit budget exceeded, use a smaller batch"); return DPQ_ERR_NOMEM; }
     if (rc != DPQ_OK) return rc;
     // emit entries -> (score << 56 | id) in place, ~0 for non-candidates

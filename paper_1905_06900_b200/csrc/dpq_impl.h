@@ -157,6 +157,7 @@ struct Index {
   double* tct_ny = nullptr;   // (nq, m) ||y'||
   int64_t tct_eps_cap = 0;
   int use_tc = -1;
+  bool emit32 = false;        // 4-byte emit records (flat, n < 2^24)
   int qt = 0;                 // queries per scan tile (set at creation from mpad; ivf m <= 4: 64)
   int probe_tc = 1;           // env DPQ_PROBE_TC at creation: 0 f64 probe, 1 tensor cores for K >= 1024, 2 always
   double tc_eps_scale = 1.0;  // env DPQ_TC_EPS_SCALE (tests: tighten to force more exact re-ranks)

@@ -946,13 +946,13 @@ static int ivf_scan(Index* h, int nb, int r2, int32_t* hist_out) {
     ea.plane = h->plane; ea.row_begin = 0; ea.row_end = h->n; ea.rows_per_cta = 0;
     ea.lut = w.lut; ea.gword = w.gword; ea.tile_list = nullptr;
     ea.slot_query = w.slot_query; ea.slot_probe = w.slot_probe;
-    ea.emit_cnt = w.emit_cnt; ea.emit = w.emit; ea.cap = w.cap;
+    ea.emit_cnt = w.emit_cnt; ea.emit = w.emit; ea.cap = w.cap; ea.emit32 = (int)h->emit32;
     ea.unit_tile = B.unit_tile; ea.unit_r0 = B.unit_r0; ea.unit_r1 = B.unit_r1;
     ea.n_units = (int)P.unit_tile.size(); ea.units_per_tile = 1;
     DPQ_TRY(launch_emit(h, ea, P.ntiles, 0));
   }
   k_threshold<256><<<nb, 256, 0, h->stream>>>(w.emit, w.emit_cnt, w.cap, B.guard_q, r2, nullptr, w.bstar, w.ncand,
-                                              w.flags, hist_out, h->d_nemit);
+                                              w.flags, hist_out, h->d_nemit, (int)h->emit32);
   DPQ_LAUNCHED(h);
   return DPQ_OK;
 }
@@ -1426,12 +1426,12 @@ int dpq_shard_scan(dpq_index_t* index, const int32_t* sample_hist_sum, int64_t n
       ea.lut = w.lut; ea.tile_list = nullptr; ea.slot_probe = nullptr;
       plan_emit_args(h, sp, ea);
       ea.unit_tile = nullptr; ea.unit_r0 = nullptr; ea.unit_r1 = nullptr;
-      ea.emit_cnt = w.emit_cnt; ea.emit = w.emit; ea.cap = w.cap;
+      ea.emit_cnt = w.emit_cnt; ea.emit = w.emit; ea.cap = w.cap; ea.emit32 = (int)h->emit32;
       DPQ_TRY(launch_emit(h, ea, tiles, h->n));
       if (!sp.list) h->counters[2] += (int64_t)nb * h->n;
     }
     k_threshold<256><<<nb, 256, 0, h->stream>>>(w.emit, w.emit_cnt, w.cap, w.guard_b, r2, nullptr, w.bstar,
-                                                w.ncand, w.flags, w.hist_i, h->d_nemit);
+                                                w.ncand, w.flags, w.hist_i, h->d_nemit, (int)h->emit32);
     DPQ_LAUNCHED(h);
     DPQ_CUDA(cudaMemcpyAsync(w.h_flags, w.flags, nb, cudaMemcpyDeviceToHost, h->stream));
     DPQ_CUDA(cudaMemcpyAsync(w.h_cnt, w.emit_cnt, (size_t)nb * 4, cudaMemcpyDeviceToHost, h->stream));
@@ -1466,7 +1466,7 @@ int dpq_shard_finish(dpq_index_t* index, const int32_t* cand_hist_sum, int r, in
   if (group_tables_fit(h, nb)) {
     DPQ_TRY(run_group_tables(h, nb, h->d));
     ra.tables = w.tables;
-    DPQ_TRY(launch_refine<MODE_EMIT_TABLE>(h, ra, nb));
+    DPQ_TRY(h->emit32 ? launch_refine<MODE_EMIT_TABLE32>(h, ra, nb) : launch_refine<MODE_EMIT_TABLE>(h, ra, nb));
   } else {
     DPQ_TRY(launch_refine<MODE_EMIT>(h, ra, nb));
   }
@@ -1548,12 +1548,12 @@ int dpq_shard_scan_dev(dpq_index_t* index, const int32_t* sample_hist_sum, int64
     ea.lut = w.lut; ea.tile_list = nullptr; ea.slot_probe = nullptr;
     plan_emit_args(h, sp, ea);
     ea.unit_tile = nullptr; ea.unit_r0 = nullptr; ea.unit_r1 = nullptr;
-    ea.emit_cnt = w.emit_cnt; ea.emit = w.emit; ea.cap = w.cap;
+    ea.emit_cnt = w.emit_cnt; ea.emit = w.emit; ea.cap = w.cap; ea.emit32 = (int)h->emit32;
     DPQ_TRY(launch_emit(h, ea, tiles, h->n));
     if (!sp.list) h->counters[2] += (int64_t)nb * h->n;
   }
   k_threshold<256><<<nb, 256, 0, h->stream>>>(w.emit, w.emit_cnt, w.cap, w.guard_b, r2, nullptr, w.bstar, w.ncand,
-                                              w.flags, cand_hist, h->d_nemit);
+                                              w.flags, cand_hist, h->d_nemit, (int)h->emit32);
   DPQ_LAUNCHED(h);
   return DPQ_OK;
 }
@@ -1577,7 +1577,7 @@ int dpq_shard_finish_dev(dpq_index_t* index, const int32_t* cand_hist_sum, int r
   if (group_tables_fit(h, nb)) {
     DPQ_TRY(run_group_tables(h, nb, h->d));
     ra.tables = w.tables;
-    DPQ_TRY(launch_refine<MODE_EMIT_TABLE>(h, ra, nb));
+    DPQ_TRY(h->emit32 ? launch_refine<MODE_EMIT_TABLE32>(h, ra, nb) : launch_refine<MODE_EMIT_TABLE>(h, ra, nb));
   } else {
     DPQ_TRY(launch_refine<MODE_EMIT>(h, ra, nb));
   }

@@ -42,6 +42,14 @@ __device__ __forceinline__ uint64_t pack_emit(int64_t row, uint32_t probe,
 __device__ __forceinline__ int64_t emit_row(uint64_t v) { return (int64_t)(v & kRowMask); }
 __device__ __forceinline__ uint32_t emit_probe(uint64_t v) { return (uint32_t)((v >> kRowBits) & 0xFFFF); }
 __device__ __forceinline__ uint32_t emit_score(uint64_t v) { return (uint32_t)(v >> 56); }
+// Compact 4-byte record (flat shards of < 2^24 rows, probe 0): row | score << 24.
+constexpr int kRow32Bits = 24;
+__device__ __forceinline__ uint32_t pack_emit32(int64_t row, uint32_t score) {
+  return (uint32_t)row | (score << kRow32Bits);
+}
+__device__ __forceinline__ uint64_t widen_emit32(uint32_t v) {
+  return pack_emit(v & ((1u << kRow32Bits) - 1u), 0u, v >> kRow32Bits);
+}
 
 __device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
   uint4 r;
@@ -793,6 +801,7 @@ struct EmitArgs {
   int64_t list_stride = 0;
   int n_units;                  // tiles * units_per_tile
   int units_per_tile;
+  int emit32 = 0;               // 4-byte records (pack_emit32) instead of pack_emit
   unsigned long long* n_lut = nullptr;  // optional: LUT tile loads (bulk copies of G::LUT_BYTES)
 };
 
@@ -984,8 +993,13 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
         const int slot = tile * G::QT + s;
         const int qe = a.slot_query ? a.slot_query[slot] : slot;
         const uint32_t probe = a.slot_probe ? (uint32_t)a.slot_probe[slot] : 0u;
-        if (pos < a.cap)
-          a.emit[(int64_t)qe * a.cap + pos] = pack_emit(r0a + (int64_t)(uint32_t)e, probe, (uint32_t)(e >> 40));
+        if (pos < a.cap) {
+          if (a.emit32)
+            reinterpret_cast<uint32_t*>(a.emit)[(int64_t)qe * a.cap + pos] =
+                pack_emit32(r0a + (int64_t)(uint32_t)e, (uint32_t)(e >> 40));
+          else
+            a.emit[(int64_t)qe * a.cap + pos] = pack_emit(r0a + (int64_t)(uint32_t)e, probe, (uint32_t)(e >> 40));
+        }
       }
       __syncwarp();
       wc = 0;
@@ -1346,7 +1360,7 @@ __global__ void __launch_bounds__(NT)
                 uint32_t cap, const uint16_t* __restrict__ guard_b, int r2,
                 const uint8_t* __restrict__ only, int32_t* __restrict__ bstar,
                 int64_t* __restrict__ ncand, uint8_t* __restrict__ flags,
-                int32_t* __restrict__ hist_out, unsigned long long* __restrict__ n_emitted) {
+                int32_t* __restrict__ hist_out, unsigned long long* __restrict__ n_emitted, int emit32) {
   __shared__ uint32_t h[256];
   const int q = blockIdx.x;
   if (only && !only[q]) return;
@@ -1360,8 +1374,13 @@ __global__ void __launch_bounds__(NT)
   for (int i = threadIdx.x; i < 256; i += NT) h[i] = 0;
   if (n_emitted && threadIdx.x == 0) atomicAdd(n_emitted, (unsigned long long)n);
   __syncthreads();
-  const uint64_t* e = emit + (int64_t)q * cap;
-  for (uint32_t i = threadIdx.x; i < n; i += NT) atomicAdd(h + emit_score(e[i]), 1u);
+  if (emit32) {
+    const uint32_t* e = reinterpret_cast<const uint32_t*>(emit) + (int64_t)q * cap;
+    for (uint32_t i = threadIdx.x; i < n; i += NT) atomicAdd(h + (e[i] >> kRow32Bits), 1u);
+  } else {
+    const uint64_t* e = emit + (int64_t)q * cap;
+    for (uint32_t i = threadIdx.x; i < n; i += NT) atomicAdd(h + emit_score(e[i]), 1u);
+  }
   __syncthreads();
   if (hist_out) {
     for (int i = threadIdx.x; i < 256; i += NT) hist_out[(int64_t)q * 256 + i] = (int32_t)h[i];
@@ -1623,7 +1642,9 @@ __global__ void __launch_bounds__(256)
 // exact r-th distance D_r <= U); pass 1 recomputes exactly (numpy entries,
 // entry_dist) every candidate with a - E <= U — which includes every exact
 // top-r member (d <= D_r) — and keeps the exact top-r.
-enum { MODE_EMIT = 0, MODE_ALL = 1, MODE_EMIT_TABLE = 2, MODE_EMIT_APPROX = 3 };
+enum { MODE_EMIT = 0, MODE_ALL = 1, MODE_EMIT_TABLE = 2, MODE_EMIT_APPROX = 3, MODE_EMIT_TABLE32 = 4 };
+// MODE_EMIT_TABLE32: MODE_EMIT_TABLE over 4-byte emit records (flat PQ 4x16 shards of < 2^24 rows);
+// only the software-pipelined loop is instantiated.
 
 struct RefineArgs {
   const uint64_t* emit; const uint32_t* emit_cnt; uint32_t cap;
@@ -1645,6 +1666,7 @@ struct RefineArgs {
   const float* cnorm = nullptr;   //   (m, k) ||c'|| in group-major entry order
   double gamma = 0.0;             //   entry bound coefficient
   unsigned long long* n_exact = nullptr;  // MODE_EMIT_APPROX: candidates recomputed exactly
+  int emit32 = 0;                 // emit lists hold 4-byte records (pack_emit32)
 };
 
 // Dynamic shared-memory budget of one refine CTA (buffer + staged y block).
@@ -1854,10 +1876,12 @@ __global__ void __launch_bounds__(NT, MODE == MODE_EMIT_APPROX ? 3 : DPQ_REFINE_
   int64_t ntot;
   int bs = 254;
   const uint64_t* e = nullptr;
+  const uint32_t* e32 = nullptr;
   if (MODE != MODE_ALL) {
     ntot = min(a.emit_cnt[q], a.cap);
     bs = a.bstar[q];
     e = a.emit + (int64_t)q * a.cap;
+    e32 = reinterpret_cast<const uint32_t*>(a.emit) + (int64_t)q * a.cap;
   } else {
     ntot = a.n_rows;
   }
@@ -1940,7 +1964,10 @@ __global__ void __launch_bounds__(NT, MODE == MODE_EMIT_APPROX ? 3 : DPQ_REFINE_
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t idx = base + (int64_t)u * NT + threadIdx.x;
-      ev[u] = (MODE != MODE_ALL && idx < ntot) ? e[idx] : 0ull;
+      // (MODE_EMIT_TABLE: 4-byte records only reach the piped loop, see dpq_flat_create)
+      ev[u] = (MODE != MODE_ALL && idx < ntot)
+                  ? ((MODE != MODE_EMIT_TABLE && MODE != MODE_EMIT_TABLE32 && a.emit32) ? widen_emit32(e32[idx]) : e[idx])
+                  : 0ull;
     }
   };
   int fb = 0;   // buffer fill before this round (same value in every thread)
@@ -1986,8 +2013,8 @@ __global__ void __launch_bounds__(NT, MODE == MODE_EMIT_APPROX ? 3 : DPQ_REFINE_
 #ifndef DPQ_REFINE_PIPE
 #define DPQ_REFINE_PIPE 1
 #endif
-  if constexpr (MODE == MODE_EMIT_TABLE && DPQ_REFINE_PIPE) {
-    if (a.code_bytes == 2 && a.m == 4) {
+  if constexpr ((MODE == MODE_EMIT_TABLE && DPQ_REFINE_PIPE) || MODE == MODE_EMIT_TABLE32) {
+    if (MODE == MODE_EMIT_TABLE32 || (a.code_bytes == 2 && a.m == 4)) {
       // Software-pipelined gathers (flat PQ 4x16, the configs[1-3] shape):
       // emit entries are loaded two rounds ahead and the candidates' codes
       // one round ahead, so a round waits on one dependent gather (its
@@ -1998,69 +2025,85 @@ __global__ void __launch_bounds__(NT, MODE == MODE_EMIT_APPROX ? 3 : DPQ_REFINE_
       // k = 65536, kbar = 256: entry (j, c) sits at j << 16 | (c & 255) << 8 | c >> 8, one byte permute
       const bool k16 = a.k == 65536 && a.bbar == 8;
       const uint2* codes2 = reinterpret_cast<const uint2*>(a.codes);
-      auto valid = [&](uint64_t v, int64_t idx) { return idx < ntot && (int)emit_score(v) <= bs; };
-      auto ld_e = [&](int64_t idx) -> uint64_t { return idx < ntot ? e[idx] : 0ull; };
-      uint64_t e0[U], e1[U];
-      uint2 c0[U];
-      const int64_t step = (int64_t)U * NT;
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t i0 = (int64_t)u * NT + threadIdx.x;
-        e0[u] = ld_e(i0);
-        e1[u] = ld_e(i0 + step);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t i0 = (int64_t)u * NT + threadIdx.x;
-        c0[u] = valid(e0[u], i0) ? __ldg(codes2 + emit_row(e0[u])) : make_uint2(0u, 0u);
-      }
-      for (int64_t base = 0; base < ntot; base += step, rnd = rnd == 2 ? 0 : rnd + 1) {
-        uint2 cn[U];
-        uint64_t en[U];
+      // one loop per record width (disjoint register live ranges)
+      auto piped_loop = [&](auto w32_tag) {
+        constexpr bool W32 = decltype(w32_tag)::value;
+        using RT = std::conditional_t<W32, uint32_t, uint64_t>;
+        const RT* ep = reinterpret_cast<const RT*>(W32 ? (const void*)e32 : (const void*)e);
+        auto rrow = [](RT v) -> int64_t {
+          if constexpr (W32) return (int64_t)(v & ((1u << kRow32Bits) - 1u));
+          else return emit_row(v);
+        };
+        auto rscore = [](RT v) -> int {
+          if constexpr (W32) return (int)(v >> kRow32Bits);
+          else return (int)emit_score(v);
+        };
+        auto valid = [&](RT v, int64_t idx) { return idx < ntot && rscore(v) <= bs; };
+        auto ld_e = [&](int64_t idx) -> RT { return idx < ntot ? ep[idx] : (RT)0; };
+        RT e0[U], e1[U];
+        uint2 c0[U];
+        const int64_t step = (int64_t)U * NT;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const int64_t i1 = base + step + (int64_t)u * NT + threadIdx.x;
-          cn[u] = valid(e1[u], i1) ? __ldg(codes2 + emit_row(e1[u])) : make_uint2(0u, 0u);
-          en[u] = ld_e(i1 + step);
+          const int64_t i0 = (int64_t)u * NT + threadIdx.x;
+          e0[u] = ld_e(i0);
+          e1[u] = ld_e(i0 + step);
         }
-        uint64_t key[U];
-        int64_t id[U];
-        bool keep[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const int64_t i0 = base + (int64_t)u * NT + threadIdx.x;
-          keep[u] = valid(e0[u], i0);
-          if (keep[u]) {
-            ++my_ref;
-            const uint2 v = c0[u];
-            uint32_t o0, o1, o2, o3;
-            if (k16) {
-              o0 = __byte_perm(v.x, 0u, 0x5401u); o1 = __byte_perm(v.x, 1u, 0x5423u);
-              o2 = __byte_perm(v.y, 2u, 0x5401u); o3 = __byte_perm(v.y, 3u, 0x5423u);
-            } else {
-              o0 = off(0, v.x & 0xFFFFu); o1 = off(1, v.x >> 16); o2 = off(2, v.y & 0xFFFFu); o3 = off(3, v.y >> 16);
-            }
-            const float t0 = __ldg(tq + o0);
-            const float t1 = __ldg(tq + o1);
-            const float t2 = __ldg(tq + o2);
-            const float t3 = __ldg(tq + o3);
-            const double dist = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(0.0, (double)t0), (double)t1), (double)t2),
-                                          (double)t3);
-            key[u] = (uint64_t)__double_as_longlong(dist);
-            keep[u] = key[u] <= thr_k;
+          const int64_t i0 = (int64_t)u * NT + threadIdx.x;
+          c0[u] = valid(e0[u], i0) ? __ldg(codes2 + rrow(e0[u])) : make_uint2(0u, 0u);
+        }
+        for (int64_t base = 0; base < ntot; base += step, rnd = rnd == 2 ? 0 : rnd + 1) {
+          uint2 cn[U];
+          RT en[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int64_t i1 = base + step + (int64_t)u * NT + threadIdx.x;
+            cn[u] = valid(e1[u], i1) ? __ldg(codes2 + rrow(e1[u])) : make_uint2(0u, 0u);
+            en[u] = ld_e(i1 + step);
+          }
+          uint64_t key[U];
+          int64_t id[U];
+          bool keep[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int64_t i0 = base + (int64_t)u * NT + threadIdx.x;
+            keep[u] = valid(e0[u], i0);
             if (keep[u]) {
-              id[u] = id_of(emit_row(e0[u]));
-              keep[u] = pair_less(key[u], id[u], thr_k, thr_i);
+              ++my_ref;
+              const uint2 v = c0[u];
+              uint32_t o0, o1, o2, o3;
+              if (k16) {
+                o0 = __byte_perm(v.x, 0u, 0x5401u); o1 = __byte_perm(v.x, 1u, 0x5423u);
+                o2 = __byte_perm(v.y, 2u, 0x5401u); o3 = __byte_perm(v.y, 3u, 0x5423u);
+              } else {
+                o0 = off(0, v.x & 0xFFFFu); o1 = off(1, v.x >> 16); o2 = off(2, v.y & 0xFFFFu); o3 = off(3, v.y >> 16);
+              }
+              const float t0 = __ldg(tq + o0);
+              const float t1 = __ldg(tq + o1);
+              const float t2 = __ldg(tq + o2);
+              const float t3 = __ldg(tq + o3);
+              const double dist =
+                  __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(0.0, (double)t0), (double)t1), (double)t2), (double)t3);
+              key[u] = (uint64_t)__double_as_longlong(dist);
+              keep[u] = key[u] <= thr_k;
+              if (keep[u]) {
+                id[u] = id_of(rrow(e0[u]));
+                keep[u] = pair_less(key[u], id[u], thr_k, thr_i);
+              }
             }
           }
-        }
-        commit(keep, key, id);
+          commit(keep, key, id);
 #pragma unroll
-        for (int u = 0; u < U; ++u) { e0[u] = e1[u]; c0[u] = cn[u]; e1[u] = en[u]; }
-      }
+          for (int u = 0; u < U; ++u) { e0[u] = e1[u]; c0[u] = cn[u]; e1[u] = en[u]; }
+        }
+      };
+      if constexpr (MODE == MODE_EMIT_TABLE32) piped_loop(std::true_type());
+      else piped_loop(std::false_type());
     }
   }
-  for (pass = 0; pass < NPASS && !piped; ++pass) {
+  for (pass = 0; pass < NPASS && !piped && MODE != MODE_EMIT_TABLE32; ++pass) {
   if (pass == 1) {
     const int P = pow2_at_least(fb);
     for (int i = fb + threadIdx.x; i < P; i += NT) { keys[i] = ~0ull; ids[i] = INT64_MAX; }
