@@ -71,7 +71,8 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=20.0, help="wall budget of the cpu_baseline leg")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
-    p.add_argument("--profile-once", action="store_true", help="one short timed step only (for ncu)")
+    p.add_argument("--no-comparator", action="store_true",
+                   help="skip the fixed-recall comparator (conventional mode + r2 grid): ncu launch lists")
     p.add_argument("--emit-workload", default=None, help=argparse.SUPPRESS)  # internal: reference-arm child
     return p.parse_args()
 
@@ -507,7 +508,7 @@ def run_single(args, cfg):
                "h2d_bytes_per_step": Bq * qh.shape[1] * 4, "d2h_bytes_per_step": Bq * r * 16,
                "step_ms": [round(1e3 * t, 3) for t in times],
                "api": f"FlatIndex.search(Y_host, {r}, mode='derived', r2={r2}) -> libdpq C ABI"}
-    extra = comparator(idx, wl, cfg, args, all_ids, stream, flush)
+    extra = {} if args.no_comparator else comparator(idx, wl, cfg, args, all_ids, stream, flush)
     cpu = parity = None
     if not args.no_cpu_baseline:
         cpu, parity = cpu_baseline(wl, cfg, args, all_ids)

@@ -1134,7 +1134,8 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
 #pragma unroll
                   for (int k = 0; k < 4; ++k) {
                     const uint32_t hb = ~wide_u<MODE>(t[k], c4[k], one) & 0x80808080u;
-                    hm |= (((hb >> 7) & 1u) | ((hb >> 14) & 2u) | ((hb >> 21) & 4u) | ((hb >> 28) & 8u)) << (4 * k);
+                    // bits 7, 15, 23, 31 -> 28..31 in one multiply (the shifted copies never overlap)
+                    hm |= ((hb * 0x00204081u) >> 28) << (4 * k);
                   }
                   if (edge && !(r >= lo && r < hi)) hm = 0u;
                 }

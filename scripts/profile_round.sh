@@ -6,12 +6,12 @@
 set -u
 OUT=${1:-gpurun_out}
 mkdir -p "$OUT"
-B="python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline"
+B="python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --no-comparator"
 $B > "$OUT/plain.log" 2>&1 &&
 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"^k_" -c 200 --csv \
     --log-file "$OUT/launches.csv" $B > "$OUT/ncu_launches.log" 2>&1
 ncu --set full --clock-control none --import-source on \
-    -k regex:"k_scan_emit|k_group_tables|k_refine_topk|k_threshold" -s 4 -c 4 \
+    -k regex:"k_scan_emit|k_group_tables|k_refine_topk|k_threshold" -s 8 -c 4 \
     -o "$OUT/prof_full" $B > "$OUT/ncu_full.log" 2>&1
 python scripts/ncu_summary.py "$OUT/prof_full.ncu-rep" "$B" > "$OUT/ncu_full_metrics.json"
 python - "$OUT/ncu_full_metrics.json" "$OUT/ncu_scan_traffic.json" <<'PY'
