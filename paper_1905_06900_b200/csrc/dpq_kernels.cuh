@@ -1102,9 +1102,15 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
             // queries and stages the hits.
             const uint32_t cwk[4] = {cw0, cw1, cw2, cw3};
             for (;;) {
-              uint32_t sel = 0u, rest = smask;
+              // up to kLaneQ records per lane per pass (the cq capacity is kLaneQ * 32);
+              // usually every record of the chunk goes in one pass
+              uint32_t sel = smask, rest = 0u;
+              if (__popc(smask) > kLaneQ) {
+                sel = 0u;
+                rest = smask;
 #pragma unroll
-              for (int k = 0; k < 4; ++k) { const uint32_t bit = rest & (0u - rest); sel |= bit; rest ^= bit; }
+                for (int k = 0; k < kLaneQ; ++k) { const uint32_t bit = rest & (0u - rest); sel |= bit; rest ^= bit; }
+              }
               const int nsel = __popc(sel);
               int off = nsel;  // inclusive scan over lanes
 #pragma unroll
