@@ -9,6 +9,7 @@
 // exact redo runs.
 #include <cuda_runtime.h>
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 #include <omp.h>
 
 #include <algorithm>
@@ -61,7 +62,10 @@ const char* last_error() { return g_last_error.c_str(); }
   } while (0)
 
 static constexpr int kScanThreads = 1024;
-static constexpr int kEmitThreads = 1024;  // (512 x 128 registers measured slower)
+#ifndef DPQ_EMIT_THREADS
+#define DPQ_EMIT_THREADS 1024
+#endif
+static constexpr int kEmitThreads = DPQ_EMIT_THREADS;  // (512 x 128 registers measured slower)
 static constexpr int kTopThreads = 256;
 
 static uint64_t g_alloc_epoch = 0;  // bumped by every device (re)allocation (invalidates captured graphs)
@@ -360,10 +364,12 @@ int build_lut(Index* h, int nslot, const uint16_t* gword, const int* slot_query 
 int run_small_tables(Index* h, int nslot, const void* prefix, int64_t npre,
                      const int64_t* pre_off, const int64_t* pre_len, const double* bounds_in,
                      bool export_debug, const float* y_slots, const int* slot_list = nullptr,
-                     int n_list = 0, bool lut = true, const int* slot_live = nullptr) {
+                     int n_list = 0, bool lut = true, const int* slot_live = nullptr,
+                     const int* y_sq = nullptr, const int* y_sp = nullptr, int y_ma = 0) {
   Workspace& w = h->ws;
   TablesArgs ta;
   ta.y = y_slots ? y_slots : w.y;
+  ta.y_sq = y_sq; ta.y_sp = y_sp; ta.y_ma = y_ma;
   ta.dcb = h->dcb;
   ta.m = h->m; ta.kbar = h->kbar; ta.dsub = h->dsub; ta.mask = h->mask;
   ta.prefix = prefix; ta.code_bytes = h->code_bytes; ta.npre = npre;

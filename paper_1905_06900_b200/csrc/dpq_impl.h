@@ -159,6 +159,7 @@ struct Index {
   int use_tc = -1;
   bool emit32 = false;        // 4-byte emit records (flat, n < 2^24)
   int qt = 0;                 // queries per scan tile (set at creation from mpad; ivf m <= 4: 64)
+  bool ivf_dev_plan = true;   // env DPQ_IVF_DEVPLAN=0: the host-built ivf plan
   int probe_tc = 1;           // env DPQ_PROBE_TC at creation: 0 f64 probe, 1 tensor cores for K >= 1024, 2 always
   double tc_eps_scale = 1.0;  // env DPQ_TC_EPS_SCALE (tests: tighten to force more exact re-ranks)
   Workspace ws;

@@ -297,16 +297,6 @@ __global__ void k_residuals(const float* __restrict__ y, const float* __restrict
 }
 
 // per tile-slot copy of its (query, probe) residual; zeros for padding
-__global__ void k_gather_slots(const float* __restrict__ ynat, const int* __restrict__ slot_query,
-                               const int* __restrict__ slot_probe, int ma, int d, int nlive,
-                               const int* __restrict__ live, float* __restrict__ yts) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= (int64_t)nlive * d) return;
-  const int ts = live[i / d], t = (int)(i % d);
-  const int q = slot_query[ts];
-  yts[(int64_t)ts * d + t] = q < 0 ? 0.f : ynat[((int64_t)q * ma + slot_probe[ts]) * d + t];
-}
-
 // bounds of every slot = (qmin, qmax) of its query's first non-empty list
 __global__ void k_slot_bounds(const double* __restrict__ qmin, const double* __restrict__ qmax,
                               const int* __restrict__ bound_ts, const int* __restrict__ slot_query,
@@ -448,19 +438,22 @@ using pinned_vector = std::vector<T, PinnedAllocator<T>>;
 struct IvfPlan {
   int nq = 0, ma = 0, nts = 0, ntiles = 0;
   int nph = 0;                         // shard: bound-source slots after the tile slots (list empty here)
-  std::vector<int> phantom;            // their slot indices
+  pinned_vector<int> phantom;          // their slot indices
   std::vector<int64_t> nr_global;      // shard: rows of the probed GLOBAL lists per query
-  std::vector<int64_t> cells;          // (nq, ma)
+  pinned_vector<int64_t> cells;        // (nq, ma)
   pinned_vector<int> slot_query, slot_probe;
-  std::vector<int> tile_cell, bound_ts;
+  std::vector<int> tile_cell;
+  pinned_vector<int> bound_ts;
   std::vector<int> cnt, first, tile0, ts_first, cnt_t, base_t;  // scratch of ivf_plan (capacity kept)
   std::vector<int64_t> nr, sq;
-  std::vector<int> live, bsrc;         // live (non-padding) slots; bound-source slots
-  std::vector<int64_t> pre_off, pre_len, tile_row0, tile_nsamp;
-  std::vector<int> unit_tile;
-  std::vector<int64_t> unit_r0, unit_r1;
-  std::vector<double> lambda;          // per query, <0 = exact histogram
+  pinned_vector<int> live, bsrc;       // live (non-padding) slots; bound-source slots
+  pinned_vector<int64_t> pre_off, pre_len, tile_row0, tile_nsamp, ns_tmp;
+  pinned_vector<int> unit_tile;
+  pinned_vector<int64_t> unit_r0, unit_r1;
+  pinned_vector<double> lambda;        // per query, <0 = exact histogram
   int64_t stride = 1, max_nsamp = 0;
+  bool dev = false;                    // built on the device (ivf_plan_dev): the vectors above are unused
+  int nlive = 0, nbsrc = 0, n_units = 0;  // (device plan: n_units is an upper bound, the count is B.pl_nunits)
 };
 
 struct IvfBuffers {
@@ -492,6 +485,20 @@ struct IvfBuffers {
   double* pny = nullptr;               // (nq) ||y - mu||
   int64_t cap_pa = 0;
   int cap_pq = 0;
+  cudaEvent_t ev_cells = nullptr;      // probe cells copied to the host
+  // device plan (ivf_plan_dev)
+  int cap_pp = 0, cap_pk = 0, cap_ptiles = 0;
+  size_t cap_ptmp = 0;
+  int *pl_key = nullptr, *pl_val = nullptr, *pl_key2 = nullptr, *pl_val2 = nullptr;
+  int *pl_cnt = nullptr, *pl_cstart = nullptr, *pl_tpc = nullptr, *pl_tile0 = nullptr;
+  int *pl_first = nullptr, *pl_flag = nullptr, *pl_pos = nullptr;
+  int64_t* pl_nr = nullptr;
+  int64_t* pl_tile_len = nullptr;
+  int *pl_tile_units = nullptr, *pl_ustart = nullptr, *pl_nunits = nullptr;
+  void* pl_tmp = nullptr;
+  unsigned long long* pl_sc = nullptr;     // device scalars
+  unsigned long long* pl_sc_h = nullptr;   // pinned copy
+  int64_t max_len = -1;                    // longest inverted list (host, once)
 };
 
 static IvfBuffers& ivf_bufs(Index* h) { return *reinterpret_cast<IvfBuffers*>(h->ivf_state); }
@@ -514,7 +521,6 @@ static int ivf_ensure(Index* h, int nq, int ma, int nts, int ntiles, int nunits)
   }
   if (nts > b.cap_ts) {
     b.cap_ts = nts;
-    DPQ_TRY(dmalloc(&b.yts, (size_t)b.cap_ts * d));
     DPQ_TRY(dmalloc(&b.live, (size_t)b.cap_ts));
   }
   if (ntiles > b.cap_tiles) {
@@ -540,6 +546,13 @@ static void ivf_free(Index* h) {
   for (void* x : p)
     if (x) cudaFree(x);
   tct_free(b.ptc);
+  if (b.ev_cells) cudaEventDestroy(b.ev_cells);
+  void* pl[] = {b.pl_key, b.pl_val, b.pl_key2, b.pl_val2, b.pl_cnt, b.pl_cstart, b.pl_tpc, b.pl_tile0, b.pl_first,
+                b.pl_flag, b.pl_pos, b.pl_nr, b.pl_tile_len, b.pl_tile_units, b.pl_ustart, b.pl_nunits, b.pl_tmp,
+                b.pl_sc};
+  for (void* x : pl)
+    if (x) cudaFree(x);
+  if (b.pl_sc_h) cudaFreeHost(b.pl_sc_h);
   delete reinterpret_cast<IvfBuffers*>(h->ivf_state);
   h->ivf_state = nullptr;
   if (h->g_prefix) cudaFree(h->g_prefix);
@@ -617,6 +630,11 @@ static int ivf_probe_dev(Index* h, int nb, int ma) {
 // Build the slot / tile / unit plan on the host from the probe result.
 static void ivf_plan(Index* h, IvfPlan& P, int nb, int ma, int r2) {
   const int qt = qt_of(h);
+  static const bool ptrace = getenv("DPQ_HOST_TRACE") != nullptr;
+  double tm[8];
+  int nm = 0;
+  auto mark = [&]() { if (ptrace && nm < 8) tm[nm++] = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+  mark();
   const int64_t* off = h->h_offsets.data();
   const int K = h->n_cells;
   P.nq = nb;
@@ -625,7 +643,8 @@ static void ivf_plan(Index* h, IvfPlan& P, int nb, int ma, int r2) {
   // cell: a counting sort over the K cells, parallel over contiguous query
   // ranges with per-thread cell counts (thread t's probes of cell c follow
   // those of threads < t, so the order is the sequential one).
-  const int T = std::max(1, std::min(8, nb / 256));
+  static const int ncpu = std::max(1, omp_get_num_procs());
+  const int T = std::max(1, std::min(std::min(16, ncpu), nb / 256));
   P.cnt_t.assign((size_t)T * K, 0);
   std::vector<int>& first = P.first;
   first.assign(nb, -1);
@@ -654,6 +673,7 @@ static void ivf_plan(Index* h, IvfPlan& P, int nb, int ma, int r2) {
         P.nr[q] += len;
       }
   }
+  mark();
   // tiles per cell, the first tile of each cell, per-thread slot bases
   std::vector<int>& cnt = P.cnt;
   std::vector<int>& tile0 = P.tile0;
@@ -710,12 +730,14 @@ static void ivf_plan(Index* h, IvfPlan& P, int nb, int ma, int r2) {
         if (stride > 1) P.sq[q] += (len + stride - 1) / stride;
       }
   }
+  mark();
   int nne = 0;
   for (int c = 0; c < K; ++c) nne += cnt[c];
   P.live.resize(nne);
   int k = 0;
   for (int c = 0; c < K; ++c)  // live slots in slot order
     for (int i = 0; i < cnt[c]; ++i) P.live[k++] = tile0[c] * qt + i;
+  mark();
   // qmax prefix: first min(r2, len) rows of each query's first non-empty
   // list, one entry per bound-source slot (list order of P.bsrc).  A shard
   // takes them from the replicated global prefixes; when that list is empty
@@ -746,6 +768,7 @@ static void ivf_plan(Index* h, IvfPlan& P, int nb, int ma, int r2) {
       P.pre_len.push_back(std::min<int64_t>(r2, off[c + 1] - off[c]));
     }
   }
+  mark();
   P.slot_query.resize(P.nts + P.nph);
   P.slot_probe.resize(P.nts + P.nph);
   P.tile_row0.assign(P.ntiles, 0);
@@ -762,6 +785,7 @@ static void ivf_plan(Index* h, IvfPlan& P, int nb, int ma, int r2) {
   if (P.stride > 1)
     for (int q = 0; q < nb; ++q)
       P.lambda[q] = P.nr[q] > 0 ? (double)r2 * (double)P.sq[q] / (double)P.nr[q] : -1.0;
+  mark();
   // scan units: each tile's list split into row ranges, ~8 units per SM
   const int sms = num_sms(h);
   const int64_t target = std::max<int64_t>(1, (8LL * sms));
@@ -777,6 +801,12 @@ static void ivf_plan(Index* h, IvfPlan& P, int nb, int ma, int r2) {
       P.unit_r1.push_back(std::min(hi, r0 + per));
     }
   }
+  mark();
+  if (ptrace) {
+    fprintf(stderr, "[dpq ivf plan]");
+    for (int i = 1; i < nm; ++i) fprintf(stderr, " %.0f", tm[i] - tm[i - 1]);
+    fprintf(stderr, " us\n");
+  }
 }
 
 template <class T, class A>
@@ -785,6 +815,290 @@ static int h2d(T* dst, const std::vector<T, A>& v, cudaStream_t s) {
   DPQ_CUDA(cudaMemcpyAsync(dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
   return DPQ_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Device-built plan (unsharded IVF): the host plan's counting sort of the
+// non-empty probes by cell, as kernels over the probe result already in HBM.
+// A stable radix sort of (cell, probe index) pairs keeps (query, probe) order
+// inside a cell, so slots, tiles, bound sources and units are exactly the
+// host plan's.  One 64-byte D2H of counts (replacing the host's cells copy)
+// sizes the buffers; everything else stays on the device.
+// ---------------------------------------------------------------------------
+enum { SC_TOT_ROWS = 0, SC_TOT_TILE_ROWS, SC_NNE, SC_NTILES, SC_NBSRC, SC_N };
+
+__global__ void k_plan_probe(const int64_t* __restrict__ cells, const int64_t* __restrict__ off, int nb, int ma,
+                             int K, int* __restrict__ key, int* __restrict__ val, int* __restrict__ cnt,
+                             int* __restrict__ first, int64_t* __restrict__ nr, int* __restrict__ flag,
+                             unsigned long long* __restrict__ sc) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nb) return;
+  int f = -1;
+  int64_t s = 0;
+  for (int p = 0; p < ma; ++p) {
+    const int i = q * ma + p;
+    const int64_t c = cells[i];
+    const int64_t len = off[c + 1] - off[c];
+    if (len > 0) {
+      if (f < 0) f = p;
+      s += len;
+      key[i] = (int)c;
+      atomicAdd(&cnt[c], 1);
+    } else {
+      key[i] = K;  // sorts last
+    }
+    val[i] = i;
+  }
+  first[q] = f;
+  nr[q] = s;
+  flag[q] = f >= 0;
+  atomicAdd(&sc[SC_TOT_ROWS], (unsigned long long)s);
+}
+
+// tiles per cell and the rows all tiles of the cell will scan
+__global__ void k_plan_tpc(const int* __restrict__ cnt, const int64_t* __restrict__ off, int K, int qt,
+                           int* __restrict__ tpc, unsigned long long* __restrict__ sc) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c > K) return;
+  const int t = c < K ? (cnt[c] + qt - 1) / qt : 0;
+  tpc[c] = t;
+  if (t) atomicAdd(&sc[SC_TOT_TILE_ROWS], (unsigned long long)t * (unsigned long long)(off[c + 1] - off[c]));
+}
+
+__global__ void k_plan_counts(const int* __restrict__ cstart, const int* __restrict__ tile0,
+                              const int* __restrict__ pos, int K, int nb, unsigned long long* __restrict__ sc) {
+  sc[SC_NNE] = (unsigned long long)cstart[K];
+  sc[SC_NTILES] = (unsigned long long)tile0[K];
+  sc[SC_NBSRC] = (unsigned long long)pos[nb];
+}
+
+// slot of every non-empty probe (sorted position i -> rank inside its cell)
+__global__ void k_plan_place(const int* __restrict__ key, const int* __restrict__ val, int n, int K, int ma, int qt,
+                             const int* __restrict__ cstart, const int* __restrict__ tile0,
+                             const int* __restrict__ first, int* __restrict__ slot_query,
+                             int* __restrict__ slot_probe, int* __restrict__ live, int* __restrict__ bound_ts) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int c = key[i];
+  if (c >= K) return;
+  const int pi = val[i], q = pi / ma, p = pi % ma;
+  const int ts = tile0[c] * qt + (i - cstart[c]);
+  slot_query[ts] = q;
+  slot_probe[ts] = p;
+  live[i] = ts;
+  if (p == first[q]) bound_ts[q] = ts;
+}
+
+// per cell: padding slots of its last tile, tile rows / samples / unit counts
+__global__ void k_plan_cells(const int* __restrict__ cnt, const int* __restrict__ tile0,
+                             const int64_t* __restrict__ off, int K, int qt, int64_t stride, int64_t per,
+                             int* __restrict__ slot_query, int* __restrict__ slot_probe,
+                             int64_t* __restrict__ tile_row0, int64_t* __restrict__ tile_nsamp,
+                             int64_t* __restrict__ tile_len, int* __restrict__ tile_units) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= K) return;
+  const int t0 = tile0[c], t1 = tile0[c + 1];
+  if (t0 == t1) return;
+  const int64_t len = off[c + 1] - off[c];
+  for (int ts = t0 * qt + cnt[c]; ts < t1 * qt; ++ts) {
+    slot_query[ts] = -1;
+    slot_probe[ts] = 0;
+  }
+  for (int t = t0; t < t1; ++t) {
+    tile_row0[t] = off[c];
+    tile_nsamp[t] = (len + stride - 1) / stride;
+    tile_len[t] = len;
+    tile_units[t] = (int)((len + per - 1) / per);
+  }
+}
+
+__global__ void k_plan_units(const int* __restrict__ ustart, const int* __restrict__ tile_units,
+                             const int64_t* __restrict__ tile_row0, const int64_t* __restrict__ tile_len,
+                             int ntiles, int64_t per, int* __restrict__ unit_tile, int64_t* __restrict__ unit_r0,
+                             int64_t* __restrict__ unit_r1, int* __restrict__ n_units) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ntiles) return;
+  const int u0 = ustart[t], nu = tile_units[t];
+  const int64_t lo = tile_row0[t], hi = lo + tile_len[t];
+  for (int j = 0; j < nu; ++j) {
+    unit_tile[u0 + j] = t;
+    unit_r0[u0 + j] = lo + (int64_t)j * per;
+    unit_r1[u0 + j] = min(hi, lo + (int64_t)(j + 1) * per);
+  }
+  if (t == ntiles - 1) *n_units = u0 + nu;
+}
+
+// bound sources in query order (ivf.py:205-217) and the per-query sampling rate
+__global__ void k_plan_queries(const int64_t* __restrict__ cells, const int64_t* __restrict__ off, int nb, int ma,
+                               int r2, int64_t stride, const int* __restrict__ first, const int* __restrict__ pos,
+                               const int64_t* __restrict__ nr, const int* __restrict__ bound_ts,
+                               int* __restrict__ bsrc, int64_t* __restrict__ pre_off, int64_t* __restrict__ pre_len,
+                               double* __restrict__ lambda) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nb) return;
+  const int f = first[q];
+  if (f >= 0) {
+    const int k = pos[q];
+    const int64_t c = cells[(int64_t)q * ma + f];
+    bsrc[k] = bound_ts[q];
+    pre_off[k] = off[c];
+    pre_len[k] = min((int64_t)r2, off[c + 1] - off[c]);
+  }
+  double lam = -1.0;
+  if (stride > 1 && nr[q] > 0) {
+    int64_t sq = 0;
+    for (int p = 0; p < ma; ++p) {
+      const int64_t c = cells[(int64_t)q * ma + p];
+      const int64_t len = off[c + 1] - off[c];
+      if (len > 0) sq += (len + stride - 1) / stride;
+    }
+    lam = (double)r2 * (double)sq / (double)nr[q];
+  }
+  lambda[q] = lam;
+}
+
+__global__ void k_plan_nsamp(const int64_t* __restrict__ tile_len, int ntiles, int64_t stride,
+                             int64_t* __restrict__ tile_nsamp) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < ntiles) tile_nsamp[t] = (tile_len[t] + stride - 1) / stride;
+}
+
+static int ivf_plan_dev(Index* h, IvfPlan& P, int nb, int ma, int r, int r2) {
+  IvfBuffers& B = ivf_bufs(h);
+  cudaStream_t st = h->stream;
+  const int K = h->n_cells, qt = qt_of(h), n = nb * ma;
+  if (B.max_len < 0) {
+    B.max_len = 0;
+    for (int c = 0; c < K; ++c) B.max_len = std::max(B.max_len, h->h_offsets[c + 1] - h->h_offsets[c]);
+  }
+  // buffers (probe-, cell- and query-indexed)
+  if (n > B.cap_pp || nb + 1 > B.cap_pk) {
+    void* old[] = {B.pl_key, B.pl_val, B.pl_key2, B.pl_val2, B.pl_first, B.pl_flag, B.pl_pos, B.pl_nr};
+    for (void* x : old)
+      if (x) cudaFree(x);
+    B.cap_pp = std::max(n, B.cap_pp);
+    B.cap_pk = std::max(nb + 1, B.cap_pk);
+    DPQ_TRY(dmalloc(&B.pl_key, (size_t)B.cap_pp));
+    DPQ_TRY(dmalloc(&B.pl_val, (size_t)B.cap_pp));
+    DPQ_TRY(dmalloc(&B.pl_key2, (size_t)B.cap_pp));
+    DPQ_TRY(dmalloc(&B.pl_val2, (size_t)B.cap_pp));
+    DPQ_TRY(dmalloc(&B.pl_first, (size_t)B.cap_pk));
+    DPQ_TRY(dmalloc(&B.pl_flag, (size_t)B.cap_pk));
+    DPQ_TRY(dmalloc(&B.pl_pos, (size_t)B.cap_pk));
+    DPQ_TRY(dmalloc(&B.pl_nr, (size_t)B.cap_pk));
+  }
+  if (!B.pl_cnt) {
+    DPQ_TRY(dmalloc(&B.pl_cnt, (size_t)K + 1));
+    DPQ_TRY(dmalloc(&B.pl_cstart, (size_t)K + 1));
+    DPQ_TRY(dmalloc(&B.pl_tpc, (size_t)K + 1));
+    DPQ_TRY(dmalloc(&B.pl_tile0, (size_t)K + 1));
+    DPQ_TRY(dmalloc(&B.pl_sc, (size_t)SC_N));
+    DPQ_TRY(dmalloc(&B.pl_nunits, (size_t)1));
+    DPQ_CUDA(cudaHostAlloc((void**)&B.pl_sc_h, SC_N * sizeof(unsigned long long), cudaHostAllocDefault));
+  }
+  int end_bit = 1;
+  while ((1 << end_bit) <= K) ++end_bit;
+  size_t t_sort = 0, t_scan1 = 0, t_scan2 = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, t_sort, B.pl_key, B.pl_key2, B.pl_val, B.pl_val2, n, 0, end_bit, st);
+  cub::DeviceScan::ExclusiveSum(nullptr, t_scan1, B.pl_cnt, B.pl_cstart, K + 1, st);
+  cub::DeviceScan::ExclusiveSum(nullptr, t_scan2, B.pl_flag, B.pl_pos, nb + 1, st);
+  const size_t need_tmp = std::max(t_sort, std::max(t_scan1, t_scan2)) + 256;
+  if (need_tmp > B.cap_ptmp) {
+    if (B.pl_tmp) cudaFree(B.pl_tmp);
+    B.pl_tmp = nullptr;
+    DPQ_CUDA(cudaMalloc(&B.pl_tmp, need_tmp));
+    B.cap_ptmp = need_tmp;
+  }
+  // phase 1: counts
+  DPQ_CUDA(cudaMemsetAsync(B.pl_cnt, 0, (size_t)(K + 1) * 4, st));
+  DPQ_CUDA(cudaMemsetAsync(B.pl_flag + nb, 0, 4, st));
+  DPQ_CUDA(cudaMemsetAsync(B.pl_sc, 0, SC_N * 8, st));
+  k_plan_probe<<<(nb + 127) / 128, 128, 0, st>>>(B.cells, h->offsets, nb, ma, K, B.pl_key, B.pl_val, B.pl_cnt,
+                                                 B.pl_first, B.pl_nr, B.pl_flag, B.pl_sc);
+  DPQ_LAUNCHED(h);
+  size_t tb = B.cap_ptmp;
+  DPQ_CUDA(cub::DeviceRadixSort::SortPairs(B.pl_tmp, tb, B.pl_key, B.pl_key2, B.pl_val, B.pl_val2, n, 0, end_bit,
+                                           st));
+  k_plan_tpc<<<(K + 256) / 256, 256, 0, st>>>(B.pl_cnt, h->offsets, K, qt, B.pl_tpc, B.pl_sc);
+  DPQ_LAUNCHED(h);
+  tb = B.cap_ptmp;
+  DPQ_CUDA(cub::DeviceScan::ExclusiveSum(B.pl_tmp, tb, B.pl_cnt, B.pl_cstart, K + 1, st));
+  tb = B.cap_ptmp;
+  DPQ_CUDA(cub::DeviceScan::ExclusiveSum(B.pl_tmp, tb, B.pl_tpc, B.pl_tile0, K + 1, st));
+  tb = B.cap_ptmp;
+  DPQ_CUDA(cub::DeviceScan::ExclusiveSum(B.pl_tmp, tb, B.pl_flag, B.pl_pos, nb + 1, st));
+  k_plan_counts<<<1, 1, 0, st>>>(B.pl_cstart, B.pl_tile0, B.pl_pos, K, nb, B.pl_sc);
+  DPQ_LAUNCHED(h);
+  DPQ_CUDA(cudaMemcpyAsync(B.pl_sc_h, B.pl_sc, SC_N * 8, cudaMemcpyDeviceToHost, st));
+  DPQ_CUDA(cudaStreamSynchronize(st));
+  const unsigned long long* sc = B.pl_sc_h;
+  P.nq = nb;
+  P.ma = ma;
+  P.dev = true;
+  P.nph = 0;
+  P.ntiles = (int)sc[SC_NTILES];
+  P.nts = P.ntiles * qt;
+  P.nlive = (int)sc[SC_NNE];
+  P.nbsrc = (int)sc[SC_NBSRC];
+  const int64_t tot_rows = (int64_t)sc[SC_TOT_ROWS];
+  const int64_t avg = nb > 0 ? tot_rows / std::max(1, nb) : 0;
+  P.stride = (avg <= h->exact_limit) ? 1 : std::max<int64_t>(1, avg / std::max<int64_t>(1, h->sample));
+  P.max_nsamp = (B.max_len + P.stride - 1) / P.stride;
+  const int64_t target = std::max<int64_t>(1, (8LL * num_sms(h)));
+  const int64_t per = std::max<int64_t>(4096, ((int64_t)sc[SC_TOT_TILE_ROWS] + target - 1) / target);
+  P.n_units = (int)std::min<int64_t>((int64_t)P.ntiles + target + 1,
+                                     (int64_t)P.ntiles + ((int64_t)sc[SC_TOT_TILE_ROWS] + per - 1) / per);
+  if (h->ws.cap == 0 && h->cap0 == 0) {  // first emit capacity, as the host plan
+    int64_t c = std::max<int64_t>(16384, std::min<int64_t>(tot_rows / std::max(nb, 1) / 256, (int64_t)1 << 20));
+    int64_t p2 = 1;
+    while (p2 < c) p2 <<= 1;
+    h->cap0 = p2;
+  }
+  if (P.nts == 0) return DPQ_OK;
+  // phase 2: placement, tiles, units, bound sources (capacities now exact)
+  DPQ_TRY(ensure_ws(h, P.nts, r, h->d, nb));
+  DPQ_TRY(ivf_ensure(h, nb, ma, P.nts, P.ntiles, std::max(P.n_units, 1)));
+  if (P.ntiles + 1 > B.cap_ptiles) {
+    if (B.pl_tile_len) cudaFree(B.pl_tile_len);
+    if (B.pl_tile_units) cudaFree(B.pl_tile_units);
+    if (B.pl_ustart) cudaFree(B.pl_ustart);
+    B.pl_tile_len = nullptr; B.pl_tile_units = nullptr; B.pl_ustart = nullptr;
+    B.cap_ptiles = P.ntiles + 1;
+    DPQ_TRY(dmalloc(&B.pl_tile_len, (size_t)B.cap_ptiles));
+    DPQ_TRY(dmalloc(&B.pl_tile_units, (size_t)B.cap_ptiles));
+    DPQ_TRY(dmalloc(&B.pl_ustart, (size_t)B.cap_ptiles));
+    size_t t3 = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, t3, B.pl_tile_units, B.pl_ustart, B.cap_ptiles, st);
+    if (t3 + 256 > B.cap_ptmp) {
+      cudaFree(B.pl_tmp);
+      B.pl_tmp = nullptr;
+      DPQ_CUDA(cudaMalloc(&B.pl_tmp, t3 + 256));
+      B.cap_ptmp = t3 + 256;
+    }
+  }
+  Workspace& w = h->ws;
+  DPQ_CUDA(cudaMemsetAsync(B.bound_ts, 0xFF, (size_t)nb * 4, st));
+  k_plan_place<<<(n + 255) / 256, 256, 0, st>>>(B.pl_key2, B.pl_val2, n, K, ma, qt, B.pl_cstart, B.pl_tile0,
+                                                B.pl_first, w.slot_query, w.slot_probe, B.live, B.bound_ts);
+  DPQ_LAUNCHED(h);
+  k_plan_cells<<<(K + 255) / 256, 256, 0, st>>>(B.pl_cnt, B.pl_tile0, h->offsets, K, qt, P.stride, per, w.slot_query,
+                                                w.slot_probe, B.tile_row0, B.tile_nsamp, B.pl_tile_len,
+                                                B.pl_tile_units);
+  DPQ_LAUNCHED(h);
+  DPQ_CUDA(cudaMemsetAsync(B.pl_tile_units + P.ntiles, 0, 4, st));
+  tb = B.cap_ptmp;
+  DPQ_CUDA(cub::DeviceScan::ExclusiveSum(B.pl_tmp, tb, B.pl_tile_units, B.pl_ustart, P.ntiles + 1, st));
+  k_plan_units<<<(P.ntiles + 255) / 256, 256, 0, st>>>(B.pl_ustart, B.pl_tile_units, B.tile_row0, B.pl_tile_len,
+                                                       P.ntiles, per, B.unit_tile, B.unit_r0, B.unit_r1,
+                                                       B.pl_nunits);
+  DPQ_LAUNCHED(h);
+  k_plan_queries<<<(nb + 127) / 128, 128, 0, st>>>(B.cells, h->offsets, nb, ma, r2, P.stride, B.pl_first, B.pl_pos,
+                                                   B.pl_nr, B.bound_ts, B.bsrc, w.slot_pre_off, w.slot_pre_len,
+                                                   B.lambda);
+  DPQ_LAUNCHED(h);
+  return DPQ_OK;
+}
+
+static bool use_dev_plan(const Index* h) { return !h->ivf_shard && h->ivf_dev_plan; }
 
 // Probe (or take the caller's cells) and form the residuals in natural
 // (query, probe) order: B.cells, P.cells (host), B.ynat.
@@ -800,10 +1114,15 @@ static int ivf_probe_residuals(Index* h, int nb, int ma, const float* res_rot, c
     DPQ_TRY(h2d(B.cells, P.cells, h->stream));
   } else {
     DPQ_TRY(ivf_probe_dev(h, nb, ma));
-    DPQ_CUDA(cudaMemcpyAsync(P.cells.data(), B.cells, P.cells.size() * 8, cudaMemcpyDeviceToHost, h->stream));
-    DPQ_CUDA(cudaStreamSynchronize(h->stream));
+    if (!use_dev_plan(h)) {  // the host plan reads the cells
+      DPQ_CUDA(cudaMemcpyAsync(P.cells.data(), B.cells, P.cells.size() * 8, cudaMemcpyDeviceToHost, h->stream));
+      if (!B.ev_cells) DPQ_CUDA(cudaEventCreateWithFlags(&B.ev_cells, cudaEventDisableTiming));
+      DPQ_CUDA(cudaEventRecord(B.ev_cells, h->stream));
+    }
   }
   ev_rec(h, 1);
+  // the residuals are enqueued behind the cell copy, so they run while the
+  // host plans (the caller synchronises on ev_cells before ivf_plan)
   if (res_rot) {
     DPQ_CUDA(cudaMemcpyAsync(B.ynat, res_rot, (size_t)nb * ma * d * 4, cudaMemcpyHostToDevice, h->stream));
   } else {
@@ -811,6 +1130,7 @@ static int ivf_probe_residuals(Index* h, int nb, int ma, const float* res_rot, c
     k_residuals<<<(unsigned)((tot + 255) / 256), 256, 0, h->stream>>>(w.y, h->centers, B.cells, nb, ma, d, B.ynat);
     DPQ_LAUNCHED(h);
   }
+  if (!cells_in && !use_dev_plan(h)) DPQ_CUDA(cudaEventSynchronize(B.ev_cells));
   return DPQ_OK;
 }
 
@@ -827,12 +1147,23 @@ static int ivf_derived_setup(Index* h, int nb, int r, int ma, int r2, bool* empt
   IvfBuffers& B = ivf_bufs(h);
   IvfPlan& P = B.plan;
   const int d = h->d;
+  if (use_dev_plan(h)) {
+    DPQ_TRY(ivf_plan_dev(h, P, nb, ma, r, r2));
+    DPQ_TRY(ensure_ws(h, std::max(P.nts, 1), r, d, nb));
+    DPQ_CUDA(cudaMemsetAsync(w.emit_cnt, 0, (size_t)nb * 4, h->stream));
+    *empty = P.nts == 0;
+    if (*empty) return DPQ_OK;
+  } else {
   try {
     ivf_plan(h, P, nb, ma, r2);
   } catch (const std::bad_alloc&) {
     set_error("ivf plan: pinned host allocation failed");
     return DPQ_ERR_NOMEM;
   }
+  P.dev = false;
+  P.nlive = (int)P.live.size();
+  P.nbsrc = (int)P.bsrc.size();
+  P.n_units = (int)P.unit_tile.size();
   if (h->ws.cap == 0 && h->cap0 == 0) {
     // first emit capacity per query from the probed rows (a query emits ~r2
     // to a few r2 rows; growth covers outliers): avg probed / 256, pow2
@@ -847,9 +1178,9 @@ static int ivf_derived_setup(Index* h, int nb, int r, int ma, int r2, bool* empt
     while (p2 < c) p2 <<= 1;
     h->cap0 = p2;
   }
-  const int nslot = P.nts + P.nph;
-  DPQ_TRY(ensure_ws(h, std::max(nslot, 1), r, d, nb));
-  DPQ_TRY(ivf_ensure(h, nb, ma, std::max(nslot, 1), std::max(P.ntiles, 1), std::max((int)P.unit_tile.size(), 1)));
+  const int nslot0 = P.nts + P.nph;
+  DPQ_TRY(ensure_ws(h, std::max(nslot0, 1), r, d, nb));
+  DPQ_TRY(ivf_ensure(h, nb, ma, std::max(nslot0, 1), std::max(P.ntiles, 1), std::max(P.n_units, 1)));
   DPQ_TRY(h2d(w.slot_query, P.slot_query, h->stream));
   DPQ_TRY(h2d(w.slot_probe, P.slot_probe, h->stream));
   DPQ_TRY(h2d(w.slot_pre_off, P.pre_off, h->stream));
@@ -864,31 +1195,23 @@ static int ivf_derived_setup(Index* h, int nb, int r, int ma, int r2, bool* empt
   DPQ_CUDA(cudaMemsetAsync(w.emit_cnt, 0, (size_t)nb * 4, h->stream));
   *empty = P.nts == 0;
   if (*empty) return DPQ_OK;
-  const int nlive = (int)P.live.size(), nbsrc = (int)P.bsrc.size();
   DPQ_TRY(h2d(B.live, P.live, h->stream));
   DPQ_TRY(h2d(B.bsrc, P.bsrc, h->stream));
-  const int64_t tot = (int64_t)nlive * d;
-  k_gather_slots<<<(unsigned)((tot + 255) / 256), 256, 0, h->stream>>>(B.ynat, w.slot_query, w.slot_probe, ma, d,
-                                                                      nlive, B.live, B.yts);
-  DPQ_LAUNCHED(h);
-  if (P.nph > 0) {  // shard: bound-source slots whose list is empty here
-    DPQ_TRY(h2d(B.phantom, P.phantom, h->stream));
-    const int64_t tp = (int64_t)P.nph * d;
-    k_gather_slots<<<(unsigned)((tp + 255) / 256), 256, 0, h->stream>>>(B.ynat, w.slot_query, w.slot_probe, ma, d,
-                                                                       P.nph, B.phantom, B.yts);
-    DPQ_LAUNCHED(h);
   }
+  const int nslot = P.nts + P.nph;
+  const int nlive = P.nlive, nbsrc = P.nbsrc;
+  // (K1 reads each slot's residual row q * ma + p of ynat directly: no gathered copy)
   const void* prefix = h->ivf_shard ? h->g_prefix : h->codes;
   // K1 pass A: qmin/qmax of the bound-source slots only (their tables are
   // recomputed in pass B; padding slots are never computed)
-  DPQ_TRY(run_small_tables(h, nslot, prefix, 0, w.slot_pre_off, w.slot_pre_len, nullptr, false, B.yts, B.bsrc, nbsrc,
-                           false));
+  DPQ_TRY(run_small_tables(h, nslot, prefix, 0, w.slot_pre_off, w.slot_pre_len, nullptr, false, B.ynat, B.bsrc, nbsrc,
+                           false, nullptr, w.slot_query, w.slot_probe, ma));
   k_slot_bounds<<<(P.nts + 255) / 256, 256, 0, h->stream>>>(w.qmin, w.qmax, B.bound_ts, w.slot_query, P.nts,
                                                             w.bounds);
   DPQ_LAUNCHED(h);
   // K1 pass B: quantize every slot with its query's bounds -> LUT tiles
-  DPQ_TRY(run_small_tables(h, P.nts, prefix, 0, nullptr, nullptr, w.bounds, false, B.yts, B.live, nlive, true,
-                           w.slot_query));
+  DPQ_TRY(run_small_tables(h, P.nts, prefix, 0, nullptr, nullptr, w.bounds, false, B.ynat, B.live, nlive, true,
+                           w.slot_query, w.slot_query, w.slot_probe, ma));
   ev_rec(h, 2);
   return DPQ_OK;
 }
@@ -902,18 +1225,27 @@ static int ivf_sample_hist(Index* h, int nb, int64_t stride) {
   DPQ_CUDA(cudaMemsetAsync(w.hist, 0, (size_t)P.nts * 256 * 4, h->stream));
   DPQ_CUDA(cudaMemsetAsync(B.hist_q, 0, (size_t)nb * 256 * 4, h->stream));
   if (P.nts == 0) return DPQ_OK;
-  std::vector<int64_t> ns(P.ntiles);
   int64_t mx = 0;
-  for (int t = 0; t < P.ntiles; ++t) {
-    const int64_t len = h->h_offsets[P.tile_cell[t] + 1] - h->h_offsets[P.tile_cell[t]];
-    ns[t] = (len + stride - 1) / stride;
-    mx = std::max(mx, ns[t]);
+  if (P.dev) {  // per-tile sample counts on the device (upper bound of the max for the grid)
+    if (stride != P.stride) {
+      k_plan_nsamp<<<(P.ntiles + 255) / 256, 256, 0, h->stream>>>(B.pl_tile_len, P.ntiles, stride, B.tile_nsamp);
+      DPQ_LAUNCHED(h);
+    }
+    mx = (B.max_len + stride - 1) / stride;
+  } else {
+    pinned_vector<int64_t>& ns = P.ns_tmp;
+    ns.resize(P.ntiles);
+    for (int t = 0; t < P.ntiles; ++t) {
+      const int64_t len = h->h_offsets[P.tile_cell[t] + 1] - h->h_offsets[P.tile_cell[t]];
+      ns[t] = (len + stride - 1) / stride;
+      mx = std::max(mx, ns[t]);
+    }
+    DPQ_TRY(h2d(B.tile_nsamp, ns, h->stream));
   }
-  DPQ_TRY(h2d(B.tile_nsamp, ns, h->stream));
   DPQ_TRY(build_lut(h, P.nts, nullptr, nullptr, w.slot_query));  // histograms need unclamped entries
   DPQ_TRY(launch_hist(h, P.ntiles, nullptr, stride, mx, h->plane, B.tile_row0, B.tile_nsamp));
-  k_slot_hist_to_query<<<(unsigned)(((int64_t)P.live.size() * 256 + 255) / 256), 256, 0, h->stream>>>(
-      w.hist, w.slot_query, B.live, (int)P.live.size(), B.hist_q);
+  k_slot_hist_to_query<<<(unsigned)(((int64_t)P.nlive * 256 + 255) / 256), 256, 0, h->stream>>>(
+      w.hist, w.slot_query, B.live, P.nlive, B.hist_q);
   DPQ_LAUNCHED(h);
   return DPQ_OK;
 }
@@ -948,7 +1280,8 @@ static int ivf_scan(Index* h, int nb, int r2, int32_t* hist_out) {
     ea.slot_query = w.slot_query; ea.slot_probe = w.slot_probe;
     ea.emit_cnt = w.emit_cnt; ea.emit = w.emit; ea.cap = w.cap; ea.emit32 = (int)h->emit32;
     ea.unit_tile = B.unit_tile; ea.unit_r0 = B.unit_r0; ea.unit_r1 = B.unit_r1;
-    ea.n_units = (int)P.unit_tile.size(); ea.units_per_tile = 1;
+    ea.n_units = P.n_units; ea.units_per_tile = 1;
+    ea.n_units_dev = P.dev ? B.pl_nunits : nullptr;
     DPQ_TRY(launch_emit(h, ea, P.ntiles, 0));
   }
   k_threshold<256><<<nb, 256, 0, h->stream>>>(w.emit, w.emit_cnt, w.cap, B.guard_q, r2, nullptr, w.bstar, w.ncand,
@@ -1069,7 +1402,7 @@ static int ivf_batch(Index* h, int nb, int r, int ma, int r2, bool derived, cons
   }
   if (trace)
     fprintf(stderr, "[dpq ivf] plan %.1f us | uploads+first pass (host) %.1f us | live %zu of %d slots, %d tiles\n",
-            t_plan1 - t_plan0, now() - t_plan1, P.live.size(), P.nts, P.ntiles);
+            t_plan1 - t_plan0, now() - t_plan1, (size_t)P.nlive, P.nts, P.ntiles);
   RefineArgs ra = make_refine_args(h, r);
   ra.y = B.ynat;
   ra.ystride = ma * d;
@@ -1161,6 +1494,7 @@ int dpq_ivf_create(int device, int m, int k, int kbar, int dsub, const float* co
   if (rc != DPQ_OK) { index_free(h); return rc; }
   h->ivf_state = new IvfBuffers();
   if (const char* e = getenv("DPQ_PROBE_TC")) h->probe_tc = atoi(e);
+  if (const char* e = getenv("DPQ_IVF_DEVPLAN")) h->ivf_dev_plan = atoi(e) != 0;
   // per-cell tiles: 64 queries per tile for m <= 4 (DPQ_IVF_QT=128: the flat geometry)
   if (h->mpad == 4) h->qt = getenv("DPQ_IVF_QT") && atoi(getenv("DPQ_IVF_QT")) == 128 ? 128 : 64;
   h->n = n;

@@ -124,6 +124,9 @@ __host__ __device__ __forceinline__ int64_t lut_index(int j, int i, int qq, int 
 // ============================================================================
 struct TablesArgs {
   const float* y;          // [nslot][d] queries (flat) or residuals (ivf)
+  const int* y_sq = nullptr;  // optional: slot s reads row y_sq[s] * y_ma + y_sp[s] of y (ivf: the
+  const int* y_sp = nullptr;  //   natural (query, probe) residual rows, no gathered copy)
+  int y_ma = 0;
   const float* dcb;        // [m][kbar][dsub] derived codebooks
   int m, kbar, dsub, mask;
   const void* prefix;      // first rows of the scanned list (qmax)
@@ -155,7 +158,8 @@ __global__ void __launch_bounds__(256) k_small_tables(TablesArgs a) {
   float* ys = sm_f;
   float* st = sm_f + d;
   uint8_t* q8 = reinterpret_cast<uint8_t*>(st + ne);
-  for (int i = tid; i < d; i += 256) ys[i] = a.y[(int64_t)s * d + i];
+  const int64_t yrow = a.y_sq ? (int64_t)a.y_sq[s] * a.y_ma + a.y_sp[s] : (int64_t)s;
+  for (int i = tid; i < d; i += 256) ys[i] = a.y[yrow * d + i];
   __syncthreads();
   // compute_tables: row_sq_dists per derived centroid (search.py:24-25,46-47)
   float mn = INFINITY;
@@ -239,14 +243,17 @@ __global__ void __launch_bounds__(256, 2) k_small_tables_ms(TablesArgs a, int n_
   float* ys = sm_ms;            // [SPC][d]
   float* st = sm_ms + SPC * d;  // [SPC][ne]
   __shared__ int sl[SPC];
+  __shared__ int64_t yr[SPC];
   if (tid < SPC) {
     const int b = blockIdx.x * SPC + tid;
-    sl[tid] = b < n_slots ? (a.slot_list ? a.slot_list[b] : b) : -1;
+    const int s = b < n_slots ? (a.slot_list ? a.slot_list[b] : b) : -1;
+    sl[tid] = s;
+    yr[tid] = s < 0 ? 0 : (a.y_sq ? (int64_t)a.y_sq[s] * a.y_ma + a.y_sp[s] : (int64_t)s);
   }
   __syncthreads();
   for (int i = tid; i < SPC * d; i += 256) {
     const int k = i / d, t = i % d;
-    ys[i] = sl[k] >= 0 ? a.y[(int64_t)sl[k] * d + t] : 0.f;
+    ys[i] = sl[k] >= 0 ? a.y[yr[k] * d + t] : 0.f;
   }
   __syncthreads();
   const f32x2_t z2 = a.negzero2;
@@ -789,6 +796,7 @@ struct EmitArgs {
   uint32_t cap;
   unsigned* unit_counter;       // zeroed before launch (persistent scheduling)
   const int* unit_tile;         // optional per-unit tile (ivf); else u / units_per_tile
+  const int* n_units_dev = nullptr;  // optional: the unit count in device memory (device-built ivf plan)
   const int64_t* unit_r0;       // optional per-unit row range (ivf)
   const int64_t* unit_r1;
   uint32_t one;                 // = 1 (opaque to the compiler, see fma_add)
@@ -889,7 +897,7 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
     __syncthreads();
     first_unit = false;
     const int u = s_unit;
-    if (a.chunk_list ? u < 0 : u >= a.n_units) break;
+    if (a.chunk_list ? u < 0 : u >= (a.n_units_dev ? *a.n_units_dev : a.n_units)) break;
     int tile;
     int64_t r0, r1;
     if (a.chunk_list) {

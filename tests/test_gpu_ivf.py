@@ -206,3 +206,33 @@ def test_tc_probe_equals_f64_probe(monkeypatch, K, d, ma):
         exp = np.lexsort((np.arange(K), d2))[:ma]
         assert np.array_equal(got[q], exp)
     assert idx._handle().counters_ex()["probe_exact"] >= ma * Y.shape[0]
+
+
+@pytest.mark.parametrize("sample,exact_limit", [("64", "0"), (None, None)])
+def test_device_plan_equals_host_plan(monkeypatch, sample, exact_limit):
+    """The device-built IVF plan (stable radix sort of probes by cell) and the
+    host plan give the same results, sampled guards and exact ones."""
+    rng = np.random.default_rng(11)
+    K, d, m = 256, 32, 4
+    centers = rng.uniform(0, 64, size=(K, d)).astype(np.float32)
+    cb = rng.normal(size=(m, 256, d // m)).astype(np.float32)
+    der = cb[:, :16].copy()
+    n = 60_000
+    cell_of = rng.integers(0, K, size=n)
+    cell_of[cell_of % 7 == 3] = 5            # a few long lists, several empty cells
+    order = np.argsort(cell_of, kind="stable")
+    offsets = np.concatenate([[0], np.cumsum(np.bincount(cell_of, minlength=K))]).astype(np.int64)
+    codes = rng.integers(0, 256, size=(n, m)).astype(np.uint8)
+    args = (cb, der, centers, offsets, codes[order], order.astype(np.int64))
+    Y = rng.uniform(0, 64, size=(300, d)).astype(np.float32)
+    if sample:
+        monkeypatch.setenv("DPQ_GUARD_SAMPLE", sample)
+        monkeypatch.setenv("DPQ_EXACT_LIMIT", exact_limit)
+    out = {}
+    for dev in ("0", "1"):
+        monkeypatch.setenv("DPQ_IVF_DEVPLAN", dev)
+        idx = IVFIndex.from_arrays(*args, cell_of=cell_of)
+        out[dev] = idx.search(Y, 10, ma=16, mode="derived", r2=200)
+    assert np.array_equal(out["0"][1], out["1"][1]) and _same(out["0"][0], out["1"][0])
+    d0, i0 = O.ivf_search(_oracle_ivf(idx), Y[:3], 10, 16, "derived", 200)
+    assert np.array_equal(i0, out["1"][1][:3]) and _same(d0, out["1"][0][:3])
