@@ -1987,6 +1987,18 @@ __global__ void __launch_bounds__(NT, MODE == MODE_EMIT_APPROX ? 3 : DPQ_REFINE_
   };
   int fb = 0;   // buffer fill before this round (same value in every thread)
   int rnd = 0;  // round index mod 3
+  // Buffer entries may hold a row tagged kDeferId instead of its id (the
+  // piped loop defers the row -> id gather of sorted flat rows until the id
+  // matters): resolved before any sort / select / output.
+  constexpr int64_t kDeferId = (int64_t)1 << 62;
+  auto resolve_ids = [&](int f) {
+    if (!a.row_ids) return;
+    for (int i = threadIdx.x; i < f; i += NT) {
+      const int64_t v = ids[i];
+      if (v & kDeferId) ids[i] = a.row_ids[v & ~kDeferId];
+    }
+    __syncthreads();
+  };
   // one round's survivors into the buffer; sort / select once it fills
   auto commit = [&](const bool* keep, const uint64_t* key, const int64_t* id) {
 #pragma unroll
@@ -2007,6 +2019,7 @@ __global__ void __launch_bounds__(NT, MODE == MODE_EMIT_APPROX ? 3 : DPQ_REFINE_
     // most U * NT <= BUF / 2 entries): early, small sorts tighten the
     // threshold sooner than waiting for a full buffer
     if (f >= BUF - U * NT || (f >= 2 * a.r && f >= (BUF - U * NT) / 2 && thr_k == ~0ull)) {
+      resolve_ids(f);
       if (BUF == NT * 4 && f > a.r) {
         // keep the r smallest (unordered) and set the threshold: radix select
         __shared__ SelShared sel;
@@ -2102,10 +2115,13 @@ __global__ void __launch_bounds__(NT, MODE == MODE_EMIT_APPROX ? 3 : DPQ_REFINE_
               const double dist =
                   __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(0.0, (double)t0), (double)t1), (double)t2), (double)t3);
               key[u] = (uint64_t)__double_as_longlong(dist);
-              keep[u] = key[u] <= thr_k;
-              if (keep[u]) {
+              if (key[u] < thr_k) {  // kept whatever its id: the row -> id gather waits until it matters
+                id[u] = a.row_ids ? (rrow(e0[u]) | kDeferId) : a.id_base + rrow(e0[u]);
+              } else if (key[u] == thr_k) {
                 id[u] = id_of(rrow(e0[u]));
-                keep[u] = pair_less(key[u], id[u], thr_k, thr_i);
+                keep[u] = id[u] < thr_i;
+              } else {
+                keep[u] = false;
               }
             }
           }
@@ -2153,6 +2169,7 @@ __global__ void __launch_bounds__(NT, MODE == MODE_EMIT_APPROX ? 3 : DPQ_REFINE_
   }
   }  // pass
   const int f = fb;
+  resolve_ids(f);
   const int P = pow2_at_least(f);
   for (int i = f + threadIdx.x; i < P; i += NT) { keys[i] = ~0ull; ids[i] = INT64_MAX; }
   __syncthreads();
