@@ -824,13 +824,13 @@ struct EmitArgs {
 // shared memory, ONE global atomicAdd per query present in the buffer to
 // reserve space in that query's emit list, then the stores.  The common path
 // is 4 LDS + ~11 ALU per code and one warp vote per 4 codes.
-constexpr int kWarpBuf = 128;  // staged hits per warp (1 KB)
+constexpr int kWarpBuf = 256;  // staged hits per warp (1 KB of 4-byte entries, flushed at least once per chunk)
 constexpr uint32_t kLutShared = 0x10000;  // LUT at shared address 64 KB
 
 // Shared layout: [stage | hit buffers] below 64 KB, LUT in [64 KB, 192 KB),
 // per-warp hit counters above it.
 template <int MPAD, int NT>
-__host__ __device__ constexpr int emit_low_bytes() { return (NT / 32) * (32 * 16 + kWarpBuf * 8); }
+__host__ __device__ constexpr int emit_low_bytes() { return (NT / 32) * (32 * 16 + kWarpBuf * 4); }
 // (QT-independent)
 constexpr int kLaneQ = 8;  // lane-private hit records per chunk (u16 each)
 template <int MPAD, int NT, int QTX = default_qt(MPAD)>
@@ -852,13 +852,13 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
   if (threadIdx.x == 0) mbar_init(&lut_bar, 1);
   uint8_t* slut = smem + (kLutShared - dyn);
   uint4* stage = reinterpret_cast<uint4*>(smem);
-  uint64_t* hbuf_all = reinterpret_cast<uint64_t*>(smem + NW * 32 * 16);
+  uint32_t* hbuf_all = reinterpret_cast<uint32_t*>(smem + NW * 32 * 16);
   uint32_t* hcnt_all = reinterpret_cast<uint32_t*>(slut + G::LUT_BYTES);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int lic = lane % G::LPC, half = lane / G::LPC;
   const uint32_t lbase = kLutShared | (uint32_t)(lic * 4);
   uint4* wst = stage + warp * 32;
-  uint64_t* hbuf = hbuf_all + warp * kWarpBuf;
+  uint32_t* hbuf = hbuf_all + warp * kWarpBuf;
   uint32_t* hcnt = hcnt_all + warp * G::QT;
   uint16_t* lq = reinterpret_cast<uint16_t*>(hcnt_all + NW * G::QT) + warp * kLaneQ * 32 + lane;
   uint16_t* cq = reinterpret_cast<uint16_t*>(hcnt_all + NW * G::QT) + warp * kLaneQ * 32;  // wide drain (128)
@@ -979,11 +979,13 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
     auto chunk_ptr = [&](int64_t ci) {
       return reinterpret_cast<const uint4*>(a.plane + chunk_row(ci) * MPAD) + lane;
     };
-    // entry: row offset from r0a (32 b) | local slot << 32 | score << 40
+    // entry (4 B): row in the current chunk (7 b) | local slot << 7 | score << 14;
+    // the buffer is flushed before the chunk changes (cur_rb = the chunk's first row)
+    int64_t cur_rb = 0;
     auto flush = [&]() {
       for (int s = lane; s < G::QT; s += 32) hcnt[s] = 0;
       __syncwarp();
-      for (int i = lane; i < wc; i += 32) atomicAdd(hcnt + ((hbuf[i] >> 32) & 0xFF), 1u);
+      for (int i = lane; i < wc; i += 32) atomicAdd(hcnt + ((hbuf[i] >> 7) & 0x7F), 1u);
       __syncwarp();
       for (int s = lane; s < G::QT; s += 32) {
         const uint32_t n = hcnt[s];
@@ -995,8 +997,8 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
       }
       __syncwarp();
       for (int i = lane; i < wc; i += 32) {
-        const uint64_t e = hbuf[i];
-        const int s = (int)((e >> 32) & 0xFF);
+        const uint32_t e = hbuf[i];
+        const int s = (int)((e >> 7) & 0x7F);
         const uint32_t pos = atomicAdd(hcnt + s, 1u);
         const int slot = tile * G::QT + s;
         const int qe = a.slot_query ? a.slot_query[slot] : slot;
@@ -1004,9 +1006,9 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
         if (pos < a.cap) {
           if (a.emit32)
             reinterpret_cast<uint32_t*>(a.emit)[(int64_t)qe * a.cap + pos] =
-                pack_emit32(r0a + (int64_t)(uint32_t)e, (uint32_t)(e >> 40));
+                pack_emit32(cur_rb + (int64_t)(e & 0x7F), e >> 14);
           else
-            a.emit[(int64_t)qe * a.cap + pos] = pack_emit(r0a + (int64_t)(uint32_t)e, probe, (uint32_t)(e >> 40));
+            a.emit[(int64_t)qe * a.cap + pos] = pack_emit(cur_rb + (int64_t)(e & 0x7F), probe, e >> 14);
         }
       }
       __syncwarp();
@@ -1025,8 +1027,7 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
           hm &= hm - 1u;
           const int k = b >> 2, qs = b & 3;
           const Sum4 sk = k == 0 ? sa : (k == 1 ? sb : (k == 2 ? sc2 : sd));
-          hbuf[wc + __popc(bal & lt)] = (uint64_t)(roff0 + k) | ((uint64_t)(4 * lic + qs) << 32) |
-                                        ((uint64_t)sum_of(sk, qs) << 40);
+          hbuf[wc + __popc(bal & lt)] = (roff0 + k) | ((uint32_t)(4 * lic + qs) << 7) | (sum_of(sk, qs) << 14);
         }
         wc += __popc(bal);
       }
@@ -1061,7 +1062,7 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
       const bool edge = rb < r0 || rb + G::CHUNK_ROWS > r1;
       const uint32_t lo = edge ? (uint32_t)max((int64_t)0, r0 - rb) : 0u;
       const uint32_t hi = edge ? (uint32_t)min((int64_t)G::CHUNK_ROWS, r1 - rb) : (uint32_t)G::CHUNK_ROWS;
-      const uint32_t rboff = (uint32_t)(rb - r0a);
+      cur_rb = rb;
       if constexpr (MPAD == 4 && G::QT == 128) {
         if (wide) {
           // Wide loop: quarter qd scans rows 32qd .. 32qd+31 of the chunk,
@@ -1177,7 +1178,7 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
                       const uint32_t ck = k == 0 ? c4[0] : (k == 1 ? c4[1] : (k == 2 ? c4[2] : c4[3]));
                       sc -= (ck >> sh) & 0xFFu;
                     }
-                    hbuf[o++] = (uint64_t)(rboff + r) | ((uint64_t)(16 * sp + b) << 32) | ((uint64_t)sc << 40);
+                    hbuf[o++] = r | ((uint32_t)(16 * sp + b) << 7) | (sc << 14);
                   }
                   wc = lim;
                   // more hits than one buffer holds (<= 512): the rest, one ballot round each
@@ -1196,8 +1197,7 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
                         const uint32_t ck = k == 0 ? c4[0] : (k == 1 ? c4[1] : (k == 2 ? c4[2] : c4[3]));
                         sc -= (ck >> sh) & 0xFFu;
                       }
-                      hbuf[wc + __popc(bal & lt)] =
-                          (uint64_t)(rboff + r) | ((uint64_t)(16 * sp + b) << 32) | ((uint64_t)sc << 40);
+                      hbuf[wc + __popc(bal & lt)] = r | ((uint32_t)(16 * sp + b) << 7) | (sc << 14);
                     }
                     wc += __popc(bal);
                   }
@@ -1213,6 +1213,7 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
             if (tmode == kModeWide5) wide_chunk(std::integral_constant<int, kModeWide5>(), std::false_type());
             else wide_chunk(std::integral_constant<int, kModeWide6>(), std::false_type());
           }
+          if (wc > 0) flush();  // entries are chunk-relative
           continue;
         }
       }
@@ -1301,7 +1302,7 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
               const Sum4 sm = lut_sum_fast<MPAD, QTX>(lbase, w0, w1, one);
               uint32_t hm = bits_x(glo - sm.lo, ghi - sm.hi);
               if (edge && !(r >= lo && r < hi)) hm = 0u;
-              stage_hits(hm, sm, sm, sm, sm, rboff + r);
+              stage_hits(hm, sm, sm, sm, sm, r);
             }
           }
         } else {
@@ -1317,17 +1318,18 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
               const uint32_t r = rowof(i, k);
               has = !edge || (r >= lo && r < hi);
               sc = sum_of(lut_sum_fast<MPAD, QTX>(lbase, w0, w1, one), qs);
-              roff = rboff + r;
+              roff = r;
               slot = 4 * lic + qs;
             }
             const uint32_t bal = __ballot_sync(0xffffffffu, has);
             if (wc + 32 > kWarpBuf) flush();
-            if (has) hbuf[wc + __popc(bal & lt)] = (uint64_t)roff | ((uint64_t)slot << 32) | ((uint64_t)sc << 40);
+            if (has) hbuf[wc + __popc(bal & lt)] = roff | (slot << 7) | (sc << 14);
             wc += __popc(bal);
           }
         }
         lcnt = 0;
       }
+      if (wc > 0) flush();  // entries are chunk-relative
     }
     if (wc > 0) flush();
   }
