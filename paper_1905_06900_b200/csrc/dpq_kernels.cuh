@@ -987,13 +987,22 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
       __syncwarp();
       for (int i = lane; i < wc; i += 32) atomicAdd(hcnt + ((hbuf[i] >> 7) & 0x7F), 1u);
       __syncwarp();
-      for (int s = lane; s < G::QT; s += 32) {
-        const uint32_t n = hcnt[s];
-        if (n) {
-          const int slot = tile * G::QT + s;
-          const int qe = a.slot_query ? a.slot_query[slot] : slot;
-          hcnt[s] = atomicAdd(a.emit_cnt + qe, n);
+      {  // per-query reservations: all of the lane's atomics in flight at once
+        constexpr int SL = G::QT / 32;
+        uint32_t base[SL];
+#pragma unroll
+        for (int k = 0; k < SL; ++k) {
+          const int s = lane + 32 * k;
+          const uint32_t n = hcnt[s];
+          base[k] = 0u;
+          if (n) {
+            const int slot = tile * G::QT + s;
+            const int qe = a.slot_query ? a.slot_query[slot] : slot;
+            base[k] = atomicAdd(a.emit_cnt + qe, n);
+          }
         }
+#pragma unroll
+        for (int k = 0; k < SL; ++k) hcnt[lane + 32 * k] = base[k];
       }
       __syncwarp();
       for (int i = lane; i < wc; i += 32) {
