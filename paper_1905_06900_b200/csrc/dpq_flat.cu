@@ -328,7 +328,11 @@ static int launch_refine_buf(Index* h, const RefineArgs& ra, int nq) {
   // (ivf with a large ma * d)
   const size_t buf_bytes = (size_t)BUF * 16;
   RefineArgs rb = ra;
-  rb.y_in_smem = buf_bytes + (size_t)ra.ystride * 4 <= kRefineSmemMax ? 1 : 0;
+  static const int ysm_env = getenv("DPQ_REFINE_YSMEM") ? atoi(getenv("DPQ_REFINE_YSMEM")) : -1;
+  // stage the block when it fits and is small (a query's full ivf residual block, ma * d floats, is
+  // mostly probes without candidates: read it through L1/L2 instead)
+  const size_t ymax = ysm_env >= 0 ? (ysm_env ? kRefineSmemMax : 0) : (size_t)8192;
+  rb.y_in_smem = buf_bytes + (size_t)ra.ystride * 4 <= kRefineSmemMax && (size_t)ra.ystride * 4 <= ymax ? 1 : 0;
   const size_t smem = buf_bytes + (rb.y_in_smem ? (size_t)ra.ystride * 4 : 0);
   auto go = [&](auto kern) -> int {
     DPQ_TRY(set_smem(h, kern, smem));
