@@ -78,14 +78,20 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// Bounded wait: a copy that never completes traps (a CUDA error) instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
+  uint32_t ok = 0;
+  for (uint32_t spin = 0;; ++spin) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (spin > (1u << 26)) __trap();
+  }
 }
 
 // Tile geometry: MPAD subspaces (4 or 8) x QT queries.  Flat m <= 4 uses
@@ -664,6 +670,46 @@ __device__ __forceinline__ Sum4 lut_sum_fast7(uint32_t base, uint32_t w, uint32_
   return s;
 }
 
+// QT = 64 geometries (CPW = 2): the two half-warps read rows of different
+// codes, and a subspace's 64-B slot sits in the same 16 banks of every row,
+// so unrotated lookups of the two halves always collide (2-way).  Half-warp 1
+// visits the subspaces of each 64-KB table in the order 1, 2, 3, 0 (sums are
+// order-free), which puts the two halves in opposite bank halves: rb[j] /
+// rs[j] = the lane's base (+ offset) and byte selector of its j-th lookup.
+template <int MPAD>
+__device__ __forceinline__ Sum4 lut_sum_rot(const uint32_t* rb, const uint32_t* rs, uint32_t w0, uint32_t w1,
+                                            uint32_t one) {
+  Sum4 s{0u, 0u};
+#pragma unroll
+  for (int j = 0; j < MPAD; ++j) {
+    const uint32_t a = __byte_perm(j < 4 ? w0 : w1, rb[j & 3], rs[j & 3]);
+    uint32_t v;
+    if (j < 4) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    else asm volatile("ld.shared.u32 %0, [%1+65536];" : "=r"(v) : "r"(a));
+    if (j == 0) {
+      s.lo = v & 0x00FF00FFu;
+      s.hi = __byte_perm(v, 0u, 0x4341u);
+    } else {
+      s.lo = fma_add(v & 0x00FF00FFu, one, s.lo);
+      s.hi = fma_add(__byte_perm(v, 0u, 0x4341u), one, s.hi);
+    }
+  }
+  return s;
+}
+__device__ __forceinline__ Sum4 lut_sum_rot7(const uint32_t* rb, const uint32_t* rs, uint32_t w, uint32_t one) {
+  uint32_t v[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t a = __byte_perm(w, rb[j], rs[j]);
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v[j]) : "r"(a));
+  }
+  const uint32_t p01 = fma_add(v[0], one, v[1]), p23 = fma_add(v[2], one, v[3]);
+  Sum4 s;
+  s.lo = fma_add(p01 & 0x00FF00FFu, one, p23 & 0x00FF00FFu);
+  s.hi = fma_add(__byte_perm(p01, 0u, 0x4341u), one, __byte_perm(p23, 0u, 0x4341u));
+  return s;
+}
+
 // 128-bit shared loads of the wide loop (hi: + 64 KB, subspaces 2/3)
 __device__ __forceinline__ uint4 lds128(uint32_t a) {
   uint4 v;
@@ -845,6 +891,7 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
   constexpr int NW = NT / 32;
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ int s_unit;
+  __shared__ int s_next;  // unit mode: the unit's next unclaimed chunk (warps balance within a unit)
   __shared__ __align__(8) uint64_t lut_bar;  // completion of the LUT bulk copy
   uint32_t lut_phase = 0;
   const uint32_t dyn = (uint32_t)__cvta_generic_to_shared(smem);
@@ -857,6 +904,13 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int lic = lane % G::LPC, half = lane / G::LPC;
   const uint32_t lbase = kLutShared | (uint32_t)(lic * 4);
+  uint32_t rot_b[4], rot_s[4];  // CPW = 2: rotated subspace order of this half-warp (lut_sum_rot)
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int jr = (j + (G::CPW == 2 ? half : 0)) & 3;
+    rot_b[j] = lbase + (uint32_t)((jr % G::SPR) * G::ROWB);
+    rot_s[j] = 0x7604u | ((uint32_t)jr << 4);
+  }
   uint4* wst = stage + warp * 32;
   uint32_t* hbuf = hbuf_all + warp * kWarpBuf;
   uint32_t* hcnt = hcnt_all + warp * G::QT;
@@ -864,6 +918,10 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
   uint16_t* cq = reinterpret_cast<uint16_t*>(hcnt_all + NW * G::QT) + warp * kLaneQ * 32;  // wide drain (128)
   const uint32_t lt = (1u << lane) - 1u;
   const uint32_t one = a.one, mone = 0u - a.one;  // opaque 1 / -1 (see fma_add)
+  auto lut_sum_any = [&](uint32_t w0, uint32_t w1) -> Sum4 {  // the lane's sums of one code (any geometry)
+    if constexpr (G::CPW == 2) return lut_sum_rot<MPAD>(rot_b, rot_s, w0, w1, one);
+    else return lut_sum_fast<MPAD, QTX>(lbase, w0, w1, one);
+  };
   int cur_tile = -1;
   bool first_unit = true;
   for (;;) {
@@ -892,6 +950,7 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
         s_unit = pick;
       } else {
         s_unit = (int)atomicAdd(a.unit_counter, 1u);
+        s_next = NW;  // chunks 0 .. NW-1 go to warps 0 .. NW-1
       }
     }
     __syncthreads();
@@ -928,6 +987,10 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
         mbar_expect_tx(&lut_bar, G::LUT_BYTES);
         bulk_g2s(slut, a.lut + (int64_t)tile * G::LUT_BYTES, G::LUT_BYTES, &lut_bar);
       }
+      // warp 0 reconverges before spinning: lanes 1-31 polling the barrier
+      // must not be scheduled ahead of lane 0's copy issue (a layout-dependent
+      // hang otherwise, seen on m = 1 models)
+      __syncwarp();
       mbar_wait(&lut_bar, lut_phase);
       lut_phase ^= 1u;
       cur_tile = tile;
@@ -965,8 +1028,11 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
     // next chunk of this warp: strided, or (list mode) pulled from the
     // tile's global counter so chunks of uneven cost balance across warps/CTAs
     auto next_chunk = [&](int64_t cprev) -> int64_t {
-      if (!clist) return cprev + NW;
       int v = 0;
+      if (!clist) {  // unit mode: claimed from the CTA's shared counter
+        if (lane == 0) v = atomicAdd(&s_next, 1);
+        return (int64_t)__shfl_sync(0xffffffffu, v, 0);
+      }
       if (lane == 0) v = atomicAdd(const_cast<int*>(a.list_next) + tile, 1);
       return (int64_t)__shfl_sync(0xffffffffu, v, 0);
     };
@@ -1262,9 +1328,9 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
         const uint32_t wa = half ? v.z : v.x, wb = half ? v.w : v.y;
         Sum4 s0, s1;
         if constexpr (decltype(fast7)::value) {
-          s0 = lut_sum_fast7<QTX>(lbase, wa, one); s1 = lut_sum_fast7<QTX>(lbase, wb, one);
+          s0 = lut_sum_rot7(rot_b, rot_s, wa, one); s1 = lut_sum_rot7(rot_b, rot_s, wb, one);
         } else {
-          s0 = lut_sum_fast<MPAD, QTX>(lbase, wa, 0, one); s1 = lut_sum_fast<MPAD, QTX>(lbase, wb, 0, one);
+          s0 = lut_sum_rot<MPAD>(rot_b, rot_s, wa, 0, one); s1 = lut_sum_rot<MPAD>(rot_b, rot_s, wb, 0, one);
         }
         const uint32_t xl0 = fma_add(s0.lo, mone, glo), xh0 = fma_add(s0.hi, mone, ghi);
         const uint32_t xl1 = fma_add(s1.lo, mone, glo), xh1 = fma_add(s1.hi, mone, ghi);
@@ -1292,7 +1358,7 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
         for (int i = 0; i < 32; ++i) {
           uint32_t w0, w1;
           wsel(wst[i], 0, w0, w1);
-          const Sum4 s0 = lut_sum_fast<MPAD, QTX>(lbase, w0, w1, one);
+          const Sum4 s0 = lut_sum_any(w0, w1);
           const uint32_t xl0 = fma_add(s0.lo, mone, glo), xh0 = fma_add(s0.hi, mone, ghi);
           if ((xl0 | xh0) & 0x80008000u) record(xl0, xh0, i, 0);
         }
@@ -1308,7 +1374,7 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
               uint32_t w0, w1;
               wsel(v, k, w0, w1);
               const uint32_t r = rowof(i, k);
-              const Sum4 sm = lut_sum_fast<MPAD, QTX>(lbase, w0, w1, one);
+              const Sum4 sm = lut_sum_any(w0, w1);
               uint32_t hm = bits_x(glo - sm.lo, ghi - sm.hi);
               if (edge && !(r >= lo && r < hi)) hm = 0u;
               stage_hits(hm, sm, sm, sm, sm, r);
@@ -1326,7 +1392,7 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
               wsel(wst[i], k, w0, w1);
               const uint32_t r = rowof(i, k);
               has = !edge || (r >= lo && r < hi);
-              sc = sum_of(lut_sum_fast<MPAD, QTX>(lbase, w0, w1, one), qs);
+              sc = sum_of(lut_sum_any(w0, w1), qs);
               roff = r;
               slot = 4 * lic + qs;
             }
