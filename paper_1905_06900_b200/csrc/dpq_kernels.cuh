@@ -243,7 +243,10 @@ __global__ void __launch_bounds__(256) k_small_tables(TablesArgs a) {
 // k_small_tables' — bitwise the same tables, bounds and u8 entries.
 // Requires 8 | dsub <= 128 (16-B rows); one warp per slot after the tables.
 template <int SPC>
-__global__ void __launch_bounds__(256, 2) k_small_tables_ms(TablesArgs a, int n_slots) {
+#ifndef DPQ_K1MS_MINB
+#define DPQ_K1MS_MINB 2
+#endif
+__global__ void __launch_bounds__(256, DPQ_K1MS_MINB) k_small_tables_ms(TablesArgs a, int n_slots) {
   extern __shared__ __align__(16) float sm_ms[];
   const int d = a.m * a.dsub, ne = a.m * a.kbar, tid = threadIdx.x;
   float* ys = sm_ms;            // [SPC][d]
