@@ -229,7 +229,8 @@ static inline float ev_ms(Index* h, int a, int b) {
 template <int MPAD, int QTX>
 static int launch_hist_t(Index* h, int ntiles, const int* tile_list, int64_t stride,
                          int64_t nsamp, const uint8_t* plane, const int64_t* tile_row0 = nullptr,
-                         const int64_t* tile_nsamp = nullptr) {
+                         const int64_t* tile_nsamp = nullptr, const int* slot_query = nullptr,
+                         uint32_t* hist_out = nullptr) {
   using G = ScanGeom<MPAD, QTX>;
   const size_t smem = G::LUT_BYTES + (size_t)G::QT * 128 * 4;
   DPQ_TRY(set_smem(h, k_scan_hist<MPAD, kScanThreads, QTX>, smem));
@@ -242,19 +243,27 @@ static int launch_hist_t(Index* h, int ntiles, const int* tile_list, int64_t str
   if (chunks < 1) chunks = 1;
   dim3 grid(chunks, ntiles);
   k_scan_hist<MPAD, kScanThreads, QTX><<<grid, kScanThreads, smem, h->stream>>>(
-      plane, stride, nsamp, per, h->ws.lut, tile_list, h->ws.hist, tile_row0, tile_nsamp);
+      plane, stride, nsamp, per, h->ws.lut, tile_list, hist_out ? hist_out : h->ws.hist, tile_row0, tile_nsamp,
+      slot_query);
   DPQ_LAUNCHED(h);
   return DPQ_OK;
 }
 
 // nsamp = samples per tile (the max when tile_nsamp is given per tile)
+// slot_query / hist_out (ivf): per-query histograms [nq][256] directly
 static int launch_hist(Index* h, int ntiles, const int* tile_list, int64_t stride, int64_t nsamp,
                        const uint8_t* plane, const int64_t* tile_row0 = nullptr,
-                       const int64_t* tile_nsamp = nullptr) {
+                       const int64_t* tile_nsamp = nullptr, const int* slot_query = nullptr,
+                       uint32_t* hist_out = nullptr) {
   if (ntiles < 1 || nsamp < 1) return DPQ_OK;
-  if (h->mpad == 8) return launch_hist_t<8, 64>(h, ntiles, tile_list, stride, nsamp, plane, tile_row0, tile_nsamp);
-  if (h->qt == 64) return launch_hist_t<4, 64>(h, ntiles, tile_list, stride, nsamp, plane, tile_row0, tile_nsamp);
-  return launch_hist_t<4, 128>(h, ntiles, tile_list, stride, nsamp, plane, tile_row0, tile_nsamp);
+  if (h->mpad == 8)
+    return launch_hist_t<8, 64>(h, ntiles, tile_list, stride, nsamp, plane, tile_row0, tile_nsamp, slot_query,
+                                hist_out);
+  if (h->qt == 64)
+    return launch_hist_t<4, 64>(h, ntiles, tile_list, stride, nsamp, plane, tile_row0, tile_nsamp, slot_query,
+                                hist_out);
+  return launch_hist_t<4, 128>(h, ntiles, tile_list, stride, nsamp, plane, tile_row0, tile_nsamp, slot_query,
+                               hist_out);
 }
 
 static int num_sms(Index* h) {

@@ -310,16 +310,6 @@ __global__ void k_slot_bounds(const double* __restrict__ qmin, const double* __r
 }
 
 // per-query histograms from the live slots' histograms (padding slots skipped)
-__global__ void k_slot_hist_to_query(const uint32_t* __restrict__ hts, const int* __restrict__ slot_query,
-                                     const int* __restrict__ live, int nlive, uint32_t* __restrict__ hq) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= (int64_t)nlive * 256) return;
-  const int ts = live[i >> 8], b = (int)(i & 255);
-  const int q = slot_query[ts];
-  const uint32_t v = hts[(int64_t)ts * 256 + b];
-  if (q >= 0 && v) atomicAdd(hq + (int64_t)q * 256 + b, v);
-}
-
 __global__ void k_expand_gword(const uint16_t* __restrict__ gq, const int* __restrict__ slot_query, int nts,
                                uint16_t* __restrict__ gts) {
   const int ts = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1222,7 +1212,6 @@ static int ivf_sample_hist(Index* h, int nb, int64_t stride) {
   Workspace& w = h->ws;
   IvfBuffers& B = ivf_bufs(h);
   IvfPlan& P = B.plan;
-  DPQ_CUDA(cudaMemsetAsync(w.hist, 0, (size_t)P.nts * 256 * 4, h->stream));
   DPQ_CUDA(cudaMemsetAsync(B.hist_q, 0, (size_t)nb * 256 * 4, h->stream));
   if (P.nts == 0) return DPQ_OK;
   int64_t mx = 0;
@@ -1243,10 +1232,9 @@ static int ivf_sample_hist(Index* h, int nb, int64_t stride) {
     DPQ_TRY(h2d(B.tile_nsamp, ns, h->stream));
   }
   DPQ_TRY(build_lut(h, P.nts, nullptr, nullptr, w.slot_query));  // histograms need unclamped entries
-  DPQ_TRY(launch_hist(h, P.ntiles, nullptr, stride, mx, h->plane, B.tile_row0, B.tile_nsamp));
-  k_slot_hist_to_query<<<(unsigned)(((int64_t)P.nlive * 256 + 255) / 256), 256, 0, h->stream>>>(
-      w.hist, w.slot_query, B.live, P.nlive, B.hist_q);
-  DPQ_LAUNCHED(h);
+  // sampled counts of every slot straight into its query's histogram (B.hist_q)
+  DPQ_TRY(launch_hist(h, P.ntiles, nullptr, stride, mx, h->plane, B.tile_row0, B.tile_nsamp, w.slot_query,
+                      B.hist_q));
   return DPQ_OK;
 }
 

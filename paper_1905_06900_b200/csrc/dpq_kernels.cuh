@@ -762,7 +762,10 @@ __global__ void __launch_bounds__(NT, 1)
     k_scan_hist(const uint8_t* __restrict__ plane, int64_t stride, int64_t n_samp,
                 int64_t samp_per_cta, const uint8_t* __restrict__ lut,
                 const int* __restrict__ tile_list, uint32_t* __restrict__ hist,
-                const int64_t* __restrict__ tile_row0, const int64_t* __restrict__ tile_nsamp) {
+                const int64_t* __restrict__ tile_row0, const int64_t* __restrict__ tile_nsamp,
+                const int* __restrict__ slot_query) {
+  // slot_query (ivf): counts go straight to the histogram row of the slot's
+  // query (hist is then [nq][256]) instead of a per-slot row
   using G = ScanGeom<MPAD, QTX>;
   extern __shared__ __align__(16) uint8_t smem[];
   uint8_t* slut = smem;
@@ -809,12 +812,18 @@ __global__ void __launch_bounds__(NT, 1)
     }
   }
   __syncthreads();
-  uint32_t* gh = hist + (int64_t)tile * G::QT * 256;
   for (int i = threadIdx.x; i < G::QT * 128; i += NT) {
     const uint32_t v = sh[i];
     const int qq = i / 128, b = (i % 128) * 2;
-    if (v & 0xFFFFu) atomicAdd(gh + qq * 256 + b, v & 0xFFFFu);
-    if (v >> 16) atomicAdd(gh + qq * 256 + b + 1, v >> 16);
+    if (!v) continue;
+    int64_t row = (int64_t)tile * G::QT + qq;
+    if (slot_query) {
+      row = slot_query[row];
+      if (row < 0) continue;  // padding slot
+    }
+    uint32_t* gh = hist + row * 256;
+    if (v & 0xFFFFu) atomicAdd(gh + b, v & 0xFFFFu);
+    if (v >> 16) atomicAdd(gh + b + 1, v >> 16);
   }
 }
 
