@@ -591,6 +591,14 @@ def init_dist(local):
     local = local % ngpu  # (functional runs with more ranks than GPUs use gloo)
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
+    if "RANK" not in os.environ:  # a single process without torchrun (--mode shard at N = 1)
+        import socket
+
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        os.environ.update(RANK="0", LOCAL_RANK=str(local), WORLD_SIZE="1", MASTER_ADDR="127.0.0.1",
+                          MASTER_PORT=str(port))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     nccl = world <= ngpu
     if nccl:
