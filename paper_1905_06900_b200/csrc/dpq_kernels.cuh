@@ -699,6 +699,25 @@ __device__ __forceinline__ Sum4 lut_sum_rot(const uint32_t* rb, const uint32_t* 
   }
   return s;
 }
+// MPAD = 8 over 7-bit (clamped, <= 127) tiles: the eight entries added as
+// four byte pair sums (<= 254, no carries), then widened once.
+__device__ __forceinline__ Sum4 lut_sum_rot7_8(const uint32_t* rb, const uint32_t* rs, uint32_t w0, uint32_t w1,
+                                               uint32_t one) {
+  uint32_t v[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint32_t a = __byte_perm(j < 4 ? w0 : w1, rb[j & 3], rs[j & 3]);
+    if (j < 4) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v[j]) : "r"(a));
+    else asm volatile("ld.shared.u32 %0, [%1+65536];" : "=r"(v[j]) : "r"(a));
+  }
+  const uint32_t p0 = fma_add(v[0], one, v[1]), p1 = fma_add(v[2], one, v[3]);
+  const uint32_t p2 = fma_add(v[4], one, v[5]), p3 = fma_add(v[6], one, v[7]);
+  Sum4 s;
+  s.lo = fma_add(p0 & 0x00FF00FFu, one, p1 & 0x00FF00FFu) + fma_add(p2 & 0x00FF00FFu, one, p3 & 0x00FF00FFu);
+  s.hi = fma_add(__byte_perm(p0, 0u, 0x4341u), one, __byte_perm(p1, 0u, 0x4341u)) +
+         fma_add(__byte_perm(p2, 0u, 0x4341u), one, __byte_perm(p3, 0u, 0x4341u));
+  return s;
+}
 __device__ __forceinline__ Sum4 lut_sum_rot7(const uint32_t* rb, const uint32_t* rs, uint32_t w, uint32_t one) {
   uint32_t v[4];
 #pragma unroll
@@ -1366,13 +1385,21 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
           for (int i = 0; i < 32; ++i) group2(wst[i], i, std::integral_constant<bool, false>());
         }
       } else {
-#pragma unroll 2
-        for (int i = 0; i < 32; ++i) {
+        auto group1 = [&](const uint4 v, int i, auto fast7) {  // MPAD = 8: this half-warp's code
           uint32_t w0, w1;
-          wsel(wst[i], 0, w0, w1);
-          const Sum4 s0 = lut_sum_any(w0, w1);
+          wsel(v, 0, w0, w1);
+          Sum4 s0;
+          if constexpr (decltype(fast7)::value) s0 = lut_sum_rot7_8(rot_b, rot_s, w0, w1, one);
+          else s0 = lut_sum_any(w0, w1);
           const uint32_t xl0 = fma_add(s0.lo, mone, glo), xh0 = fma_add(s0.hi, mone, ghi);
           if ((xl0 | xh0) & 0x80008000u) record(xl0, xh0, i, 0);
+        };
+        if (G::CPW == 2 && fast_tile) {
+#pragma unroll 2
+          for (int i = 0; i < 32; ++i) group1(wst[i], i, std::integral_constant<bool, true>());
+        } else {
+#pragma unroll 2
+          for (int i = 0; i < 32; ++i) group1(wst[i], i, std::integral_constant<bool, false>());
         }
       }
       // drain: records -> emit entries (scores recomputed from the staged codes)
