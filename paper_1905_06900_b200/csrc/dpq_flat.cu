@@ -226,6 +226,8 @@ static inline float ev_ms(Index* h, int a, int b) {
 // ---------------------------------------------------------------------------
 // Launch helpers (template dispatch on MPAD)
 // ---------------------------------------------------------------------------
+static int num_sms(Index* h);
+
 template <int MPAD, int QTX>
 static int launch_hist_t(Index* h, int ntiles, const int* tile_list, int64_t stride,
                          int64_t nsamp, const uint8_t* plane, const int64_t* tile_row0 = nullptr,
@@ -234,8 +236,9 @@ static int launch_hist_t(Index* h, int ntiles, const int* tile_list, int64_t str
   using G = ScanGeom<MPAD, QTX>;
   const size_t smem = G::LUT_BYTES + (size_t)G::QT * 128 * 4;
   DPQ_TRY(set_smem(h, k_scan_hist<MPAD, kScanThreads, QTX>, smem));
-  int chunks = (int)std::max<int64_t>(1, std::min<int64_t>((148 * 2 + ntiles - 1) / ntiles,
-                                                          (nsamp + 511) / 512));
+  // one CTA per SM (the 128-KB LUT tile + counters fill its shared memory):
+  // chunks per tile so the grid is a single wave
+  int chunks = (int)std::max<int64_t>(1, std::min<int64_t>(num_sms(h) / ntiles, (nsamp + 511) / 512));
   int64_t per = (nsamp + chunks - 1) / chunks;
   per = (per + 31) / 32 * 32;
   per = std::min<int64_t>(per, kHistRowsPerCta / 32 * 32);  // u16 counters never wrap
@@ -487,10 +490,11 @@ int prepare_flat_scan(Index* h, int nb, const ScanPlan& sp) {
   DPQ_TRY(build_lut(h, nb, sp.gw, sp.slot_q));  // clamped tiles (modes 5/6/7) where the guards allow
   if (sp.list) {  // run filter: per tile, the chunks whose (g0, g1) keys can reach a guard
     DPQ_CUDA(cudaMemsetAsync(w.list_len, 0, (size_t)tiles * 4, h->stream));
-    k_run_potential<<<dim3(64, tiles), 256, (size_t)qt * 64 * 4 + 4 * qt * 4, h->stream>>>(
+    k_run_potential<<<dim3(256 / kRunG0, tiles), 256, (size_t)qt * 64 * 4 + kRunG0 * qt * 4, h->stream>>>(
         w.q8, h->m, h->kbar, sp.slot_q, sp.gw, qt, nb, w.pot);
     DPQ_LAUNCHED(h);
-    k_chunk_list<<<dim3((unsigned)((h->n_chunks + 255) / 256), tiles), 256, 0, h->stream>>>(
+    k_chunk_list<<<dim3((unsigned)((h->n_chunks + 256 * kChunkPerThread - 1) / (256 * kChunkPerThread)), tiles), 256, 0,
+                   h->stream>>>(
         h->chunk_keys, (int)h->n_chunks, 512 / h->mpad, w.pot, w.chunk_list, w.list_len, h->n, nb, qt, h->d_nrows);
     DPQ_LAUNCHED(h);
   }
@@ -518,7 +522,7 @@ static int flat_first_pass(Index* h, int nb, int r2) {
   const int64_t stride = exact ? 1 : n / nsamp;
   DPQ_TRY(launch_hist(h, tiles, nullptr, stride, nsamp, h->plane));
   const double lambda = (double)r2 * (double)nsamp / (double)std::max<int64_t>(n, 1);
-  k_guard<<<(nb + 127) / 128, 128, 0, h->stream>>>(w.hist, nb, r2, lambda, exact ? 1 : 0, nullptr,
+  k_guard<<<(nb + kGuardSlotsPerCta - 1) / kGuardSlotsPerCta, 32 * kGuardSlotsPerCta, 0, h->stream>>>(w.hist, nb, r2, lambda, exact ? 1 : 0, nullptr,
                                                     w.guard_b, w.gword, nullptr);
   DPQ_LAUNCHED(h);
   ScanPlan sp;
@@ -586,7 +590,7 @@ static int flat_first_pass(Index* h, int nb, int r2) {
       DPQ_CUDA(cudaMemsetAsync(w.hist, 0, (size_t)tiles * qt * 256 * 4, h->stream));
       DPQ_TRY(build_lut(h, nb, nullptr));  // exact histogram needs unclamped entries
       DPQ_TRY(launch_hist(h, (int)tl.size(), w.tile_list, 1, n, h->plane));
-      k_guard<<<(nb + 127) / 128, 128, 0, h->stream>>>(w.hist, nb, r2, 0.0, 1, w.only, w.guard_b, w.gword,
+      k_guard<<<(nb + kGuardSlotsPerCta - 1) / kGuardSlotsPerCta, 32 * kGuardSlotsPerCta, 0, h->stream>>>(w.hist, nb, r2, 0.0, 1, w.only, w.guard_b, w.gword,
                                                         nullptr);
       DPQ_LAUNCHED(h);
       DPQ_TRY(sort_and_build());

@@ -1244,7 +1244,7 @@ static int ivf_set_guards(Index* h, int nb, int r2, bool exact, const uint8_t* o
   Workspace& w = h->ws;
   IvfBuffers& B = ivf_bufs(h);
   IvfPlan& P = B.plan;
-  k_guard<<<(nb + 127) / 128, 128, 0, h->stream>>>(B.hist_q, nb, r2, 0.0, exact ? 1 : 0, only, B.guard_q, B.gword_q,
+  k_guard<<<(nb + kGuardSlotsPerCta - 1) / kGuardSlotsPerCta, 32 * kGuardSlotsPerCta, 0, h->stream>>>(B.hist_q, nb, r2, 0.0, exact ? 1 : 0, only, B.guard_q, B.gword_q,
                                                     exact ? nullptr : B.lambda);
   DPQ_LAUNCHED(h);
   if (P.nts == 0) return DPQ_OK;
@@ -1732,7 +1732,7 @@ int dpq_shard_scan(dpq_index_t* index, const int32_t* sample_hist_sum, int64_t n
   DPQ_CUDA(cudaMemcpyAsync(w.hist, sample_hist_sum, (size_t)nb * 256 * 4, cudaMemcpyHostToDevice, h->stream));
   const bool ex = exact || n_global <= h->exact_limit;
   const double lambda = (double)r2 * (double)sample_global / (double)std::max<int64_t>(n_global, 1);
-  k_guard<<<(nb + 127) / 128, 128, 0, h->stream>>>(w.hist, nb, r2, lambda, ex ? 1 : 0, nullptr, w.guard_b, w.gword,
+  k_guard<<<(nb + kGuardSlotsPerCta - 1) / kGuardSlotsPerCta, 32 * kGuardSlotsPerCta, 0, h->stream>>>(w.hist, nb, r2, lambda, ex ? 1 : 0, nullptr, w.guard_b, w.gword,
                                                     nullptr);
   DPQ_LAUNCHED(h);
   // same scan preparation as the single-GPU first pass (slot clustering,
@@ -1857,7 +1857,7 @@ int dpq_shard_scan_dev(dpq_index_t* index, const int32_t* sample_hist_sum, int64
   DPQ_CUDA(cudaMemcpyAsync(w.hist, sample_hist_sum, (size_t)nb * 256 * 4, cudaMemcpyDeviceToDevice, h->stream));
   const bool ex = exact || n_global <= h->exact_limit;
   const double lambda = (double)r2 * (double)sample_global / (double)std::max<int64_t>(n_global, 1);
-  k_guard<<<(nb + 127) / 128, 128, 0, h->stream>>>(w.hist, nb, r2, lambda, ex ? 1 : 0, nullptr, w.guard_b, w.gword,
+  k_guard<<<(nb + kGuardSlotsPerCta - 1) / kGuardSlotsPerCta, 32 * kGuardSlotsPerCta, 0, h->stream>>>(w.hist, nb, r2, lambda, ex ? 1 : 0, nullptr, w.guard_b, w.gword,
                                                     nullptr);
   DPQ_LAUNCHED(h);
   ScanPlan sp;

@@ -289,52 +289,100 @@ __global__ void __launch_bounds__(256, DPQ_K1MS_MINB) k_small_tables_ms(TablesAr
     for (int k = 0; k < SPC; ++k) st[k * ne + e] = pw_combine2(r[k]);
   }
   __syncthreads();
+  // Bounds, quantization and cluster keys: WPS = 8 / SPC warps per slot
+  // (every warp busy), each over an interleaved share of the entries and the
+  // prefix rows; min / max / first-argmin partials combined in shared memory
+  // (order-free, so the results are the per-warp form's bit for bit).
+  constexpr int WPS = SPC >= 8 ? 1 : 8 / SPC;
+  __shared__ float p_min[8];
+  __shared__ double p_max[8];
+  __shared__ uint32_t p_best[8][2];
   const int w = tid >> 5, lane = tid & 31;
-  for (int k = w; k < SPC; k += 8) {
-    const int s = sl[k];
-    if (s < 0) continue;
-    const float* t = st + k * ne;
+  const int k = w / WPS, sub = w % WPS, step = 32 * WPS, e0 = 32 * sub + lane;
+  const int s = k < SPC ? sl[k] : -1;
+  const float* t = st + (k < SPC ? k : 0) * ne;
+  if (s >= 0) {
     float mn = INFINITY;
-    for (int e = lane; e < ne; e += 32) mn = fminf(mn, t[e]);
+    for (int e = e0; e < ne; e += step) mn = fminf(mn, t[e]);
     mn = warp_min_f(mn);
-    double qmin = (double)mn, qmax;
-    if (a.bounds_in) {
-      qmin = a.bounds_in[2 * s];
-      qmax = a.bounds_in[2 * s + 1];
-    } else {
+    double mx = -INFINITY;
+    if (!a.bounds_in) {
       const int pi = a.slot_list ? blockIdx.x * SPC + k : s;
       const int64_t pre_off = a.prefix_off ? a.prefix_off[pi] : 0;
       const int64_t npre = a.prefix_len ? a.prefix_len[pi] : a.npre;
-      double mx = -INFINITY;
-      for (int64_t p = lane; p < npre; p += 32) {
-        double acc = 0.0;
-        for (int j = 0; j < a.m; ++j) {
-          const uint32_t c = code_at(a.prefix, a.code_bytes, (pre_off + p) * a.m + j);
-          acc = __dadd_rn(acc, (double)t[j * a.kbar + (c & a.mask)]);
+      if (a.code_bytes == 2 && a.m == 4) {
+        // one 8-byte code load per row, four rows in flight per lane
+        const uint2* pc = reinterpret_cast<const uint2*>(a.prefix) + pre_off;
+        const uint32_t kb = (uint32_t)a.kbar, msk = (uint32_t)a.mask;
+        for (int64_t p = e0; p < npre; p += 4 * step) {
+          uint2 cv[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int64_t pu = p + (int64_t)u * step;
+            cv[u] = pu < npre ? __ldg(pc + pu) : make_uint2(0u, 0u);
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (p + (int64_t)u * step >= npre) break;
+            double acc = 0.0;
+            acc = __dadd_rn(acc, (double)t[(cv[u].x & 0xFFFFu) & msk]);
+            acc = __dadd_rn(acc, (double)t[kb + ((cv[u].x >> 16) & msk)]);
+            acc = __dadd_rn(acc, (double)t[2 * kb + ((cv[u].y & 0xFFFFu) & msk)]);
+            acc = __dadd_rn(acc, (double)t[3 * kb + ((cv[u].y >> 16) & msk)]);
+            mx = fmax(mx, acc);
+          }
         }
-        mx = fmax(mx, acc);
+      } else {
+#pragma unroll 4
+        for (int64_t p = e0; p < npre; p += step) {
+          double acc = 0.0;
+          for (int j = 0; j < a.m; ++j) {
+            const uint32_t c = code_at(a.prefix, a.code_bytes, (pre_off + p) * a.m + j);
+            acc = __dadd_rn(acc, (double)t[j * a.kbar + (c & a.mask)]);
+          }
+          mx = fmax(mx, acc);
+        }
       }
-      qmax = warp_max_d(mx);
+      mx = warp_max_d(mx);
+    }
+    if (lane == 0) { p_min[w] = mn; p_max[w] = mx; }
+  }
+  __syncthreads();
+  if (s >= 0) {
+    double qmin = (double)p_min[k * WPS], qmax = p_max[k * WPS];
+    for (int i = 1; i < WPS; ++i) {
+      qmin = fmin(qmin, (double)p_min[k * WPS + i]);
+      qmax = fmax(qmax, p_max[k * WPS + i]);
+    }
+    if (a.bounds_in) {
+      qmin = a.bounds_in[2 * s];
+      qmax = a.bounds_in[2 * s + 1];
     }
     const bool degenerate = !(qmax > qmin);
     const double scale = degenerate ? 0.0 : __ddiv_rn(255.0, __dsub_rn(qmax, qmin));
     const float qmaxf = __double2float_rn(qmax);
     uint32_t best0 = 0xFFFFFFFFu, best1 = 0xFFFFFFFFu;
-    for (int e = lane; e < ne; e += 32) {
+    for (int e = e0; e < ne; e += step) {
       const uint8_t q = degenerate ? (uint8_t)0 : quantize_entry(t[e], qmin, scale, qmaxf);
       if (a.small_out) a.small_out[(int64_t)s * ne + e] = t[e];
       if (a.q8_out) a.q8_out[(int64_t)s * ne + e] = q;
       if (e < a.kbar) best0 = min(best0, ((uint32_t)q << 16) | (uint32_t)e);
       else if (e < 2 * a.kbar) best1 = min(best1, ((uint32_t)q << 16) | (uint32_t)(e - a.kbar));
     }
-    if (lane == 0) {
+    if (sub == 0 && lane == 0) {
       a.qmin_out[s] = qmin;
       a.qmax_out[s] = degenerate ? qmin : qmax;
     }
-    if (a.cluster && a.m >= 2) {
-      best0 = __reduce_min_sync(0xffffffffu, best0);
-      best1 = __reduce_min_sync(0xffffffffu, best1);
-      if (lane == 0) a.cluster[s] = (uint16_t)(((best0 & 0xFFu) << 8) | (best1 & 0xFFu));
+    best0 = __reduce_min_sync(0xffffffffu, best0);
+    best1 = __reduce_min_sync(0xffffffffu, best1);
+    if (lane == 0) { p_best[w][0] = best0; p_best[w][1] = best1; }
+  }
+  if (a.cluster && a.m >= 2) {
+    __syncthreads();
+    if (s >= 0 && sub == 0 && lane == 0) {
+      uint32_t b0 = p_best[w][0], b1 = p_best[w][1];
+      for (int i = 1; i < WPS; ++i) { b0 = min(b0, p_best[w + i][0]); b1 = min(b1, p_best[w + i][1]); }
+      a.cluster[s] = (uint16_t)(((b0 & 0xFFu) << 8) | (b1 & 0xFFu));
     }
   }
 }
@@ -467,30 +515,75 @@ __global__ void __launch_bounds__(1024) k_sort_slots(const uint16_t* __restrict_
     return gw >= 0x8000u ? (int)min(gw - 0x8000u, 255u) : 256;
   };
   if (cluster && nq <= kSortMax) {
+    // Bitonic sort of P = pow2 >= nq keys, element i = e * 1024 + tid held in
+    // register x[e]: partner strides >= 1024 are in-thread swaps, 32..512 go
+    // through shared memory, < 32 are warp shuffles (no barrier).
+    constexpr int EMAX = kSortMax / 1024;
     int P = 1;
     while (P < nq) P <<= 1;
-    for (int q = tid; q < P; q += blockDim.x) {
-      if (q >= nq) { kv[q] = ~0ull; continue; }
-      const int B = gkey(q);
-      const uint64_t cls = B == 256 ? 3u : (B <= 30 ? 0u : (B <= 62 ? 1u : 2u));
-      kv[q] = (((cls << 16) | cluster[q]) << 32) | (uint32_t)q;
-    }
-    __syncthreads();
-    for (int size = 2; size <= P; size <<= 1) {
-      for (int stride = size >> 1; stride > 0; stride >>= 1) {
-        for (int t = tid; t < P / 2; t += blockDim.x) {
-          const int i = 2 * t - (t & (stride - 1)), j = i + stride;
-          const bool asc = (i & size) == 0;
-          const uint64_t x = kv[i], y = kv[j];
-          if ((x > y) == asc) { kv[i] = y; kv[j] = x; }
-        }
-        __syncthreads();
+    const int E = P > 1024 ? P / 1024 : 1;
+    uint64_t x[EMAX];
+#pragma unroll
+    for (int e = 0; e < EMAX; ++e) {
+      const int q = e * 1024 + tid;
+      x[e] = ~0ull;
+      if (e < E && q < nq) {
+        const int B = gkey(q);
+        const uint64_t cls = B == 256 ? 3u : (B <= 30 ? 0u : (B <= 62 ? 1u : 2u));
+        x[e] = (((cls << 16) | cluster[q]) << 32) | (uint32_t)q;
       }
     }
-    for (int sl = tid; sl < nq; sl += blockDim.x) {
-      const int q = (int)(kv[sl] & 0xFFFFFFFFu);
-      slot_query[sl] = q;
-      gword_p[sl] = gword[q];
+    // element i keeps the min of (i, i ^ j) iff (i < partner) == ascending
+    auto keep = [](uint64_t mine, uint64_t other, bool take_min) {
+      return take_min ? (other < mine ? other : mine) : (other > mine ? other : mine);
+    };
+    for (int size = 2; size <= P; size <<= 1) {
+      for (int j = size >> 1; j > 0; j >>= 1) {
+        if (j >= 1024) {
+          const int ej = j / 1024;
+#pragma unroll
+          for (int e = 0; e < EMAX; ++e) {
+            if (e >= E || (e & ej)) continue;
+            const int i = e * 1024 + tid;
+            const bool asc = (i & size) == 0;
+            const uint64_t a0 = x[e], a1 = x[e + ej];
+            x[e] = keep(a0, a1, asc);
+            x[e + ej] = keep(a1, a0, !asc);
+          }
+        } else if (j >= 32) {
+#pragma unroll
+          for (int e = 0; e < EMAX; ++e)
+            if (e < E) kv[e * 1024 + tid] = x[e];
+          __syncthreads();
+#pragma unroll
+          for (int e = 0; e < EMAX; ++e) {
+            if (e >= E) continue;
+            const int i = e * 1024 + tid;
+            if (i >= P) continue;
+            const bool asc = (i & size) == 0;
+            x[e] = keep(x[e], kv[i ^ j], ((i & j) == 0) == asc);
+          }
+          __syncthreads();
+        } else {
+#pragma unroll
+          for (int e = 0; e < EMAX; ++e) {
+            if (e >= E) continue;
+            const int i = e * 1024 + tid;
+            const uint64_t o = __shfl_xor_sync(0xffffffffu, x[e], j);
+            const bool asc = (i & size) == 0;
+            x[e] = keep(x[e], o, ((i & j) == 0) == asc);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < EMAX; ++e) {
+      const int sl = e * 1024 + tid;
+      if (e < E && sl < nq) {
+        const int q = (int)(x[e] & 0xFFFFFFFFu);
+        slot_query[sl] = q;
+        gword_p[sl] = gword[q];
+      }
     }
   } else {
     for (int i = tid; i < 258; i += blockDim.x) cnt[i] = 0;
@@ -516,44 +609,66 @@ __global__ void __launch_bounds__(1024) k_sort_slots(const uint16_t* __restrict_
 // bytes of subspaces 0 and 1).  Every entry is >= 0, so a row of key
 // (g0, g1) can only reach a query's guard B if e0[g0] + e1[g1] <= B.
 //   k_run_potential: pot[tile][key] = 1 iff some slot of the tile passes
-//     (grid: 64 x tiles, 4 values of g0 per CTA, 4 of g1 per thread)
+//     (grid: 256 / kRunG0 x tiles, kRunG0 values of g0 per CTA, 4 of g1 per thread)
 //   k_chunk_list: per tile, the scan chunks (512 B of plane) whose key range holds a key
 //     with pot = 1 (unordered list + length); the scan visits only those.
 // Skipped rows have score > B, so they would never be emitted: exact.
+constexpr int kRunG0 = 16;  // values of g0 per k_run_potential CTA
 __global__ void __launch_bounds__(256) k_run_potential(const uint8_t* __restrict__ q8, int m, int kbar,
                                                        const int* __restrict__ slot_query,
                                                        const uint16_t* __restrict__ gword, int qt, int nq,
                                                        uint8_t* __restrict__ pot) {
+  // CTA = (16 values of g0, tile).  The tile's e1 words are staged once per
+  // CTA with eight independent row loads in flight per thread (the load
+  // latency, not the arithmetic, bounds this kernel).
   extern __shared__ __align__(16) uint32_t bw[];  // [qt][64] words: 4 x min(e1, 127)
-  uint32_t* c4 = bw + qt * 64;                    // [4][qt] bias words
+  uint32_t* c4 = bw + qt * 64;                    // [kRunG0][qt] bias words
+  __shared__ int sq[256];                         // slot -> query (qt <= 256)
   const int tile = blockIdx.y, tid = threadIdx.x;
-  for (int i = tid; i < qt * 64; i += 256) {
-    const int sl = i >> 6, g = (i & 63) * 4;
+  for (int sl = tid; sl < qt; sl += 256) {
     const int q = slot_query ? slot_query[tile * qt + sl] : tile * qt + sl;
-    uint32_t w = 0x7F7F7F7Fu;
-    if (q >= 0 && q < nq) {
-      const uint8_t* row = q8 + ((int64_t)q * m + 1) * kbar;
-      if ((kbar & 3) == 0) {
-        if (g < kbar) {
-          const uint32_t v = *reinterpret_cast<const uint32_t*>(row + g);  // min(e1, 127) per byte
-          const uint32_t hi = v & 0x80808080u;                             // bytes >= 128
-          w = (v & ~(hi | (hi >> 1) | (hi >> 2) | (hi >> 3) | (hi >> 4) | (hi >> 5) | (hi >> 6) | (hi >> 7))) |
-              (hi ? (((hi >> 7) * 0x7Fu) & 0x7F7F7F7Fu) : 0u);
+    sq[sl] = (q >= 0 && q < nq) ? q : -1;
+  }
+  __syncthreads();
+  auto clamp127 = [](uint32_t v) {  // min(byte, 127) per byte
+    const uint32_t hi = v & 0x80808080u;
+    return (v & ~(hi | (hi >> 1) | (hi >> 2) | (hi >> 3) | (hi >> 4) | (hi >> 5) | (hi >> 6) | (hi >> 7))) |
+           (hi ? (((hi >> 7) * 0x7Fu) & 0x7F7F7F7Fu) : 0u);
+  };
+  {
+    const int g = (tid & 63) * 4;  // this thread's 4 groups; slots tid/64, +4, +8, ...
+    constexpr int U = 8;
+    for (int sl0 = tid >> 6; sl0 < qt; sl0 += 4 * U) {
+      uint32_t v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int sl = sl0 + 4 * u;
+        const int q = sl < qt ? sq[sl] : -1;
+        v[u] = 0x7F7F7F7Fu;
+        if (q >= 0) {
+          const uint8_t* row = q8 + ((int64_t)q * m + 1) * kbar;
+          if ((kbar & 3) == 0) {
+            if (g < kbar) v[u] = __ldg(reinterpret_cast<const uint32_t*>(row + g));
+          } else {
+            uint32_t w = 0;
+            for (int b = 0; b < 4; ++b) w |= (g + b < kbar ? min((uint32_t)row[g + b], 127u) : 127u) << (8 * b);
+            v[u] = w;
+          }
         }
-      } else {
-        w = 0;
-        for (int b = 0; b < 4; ++b)
-          w |= (g + b < kbar ? min((uint32_t)row[g + b], 127u) : 127u) << (8 * b);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int sl = sl0 + 4 * u;
+        if (sl < qt) bw[sl * 64 + (tid & 63)] = clamp127(v[u]);  // (idempotent on clamped words)
       }
     }
-    bw[i] = w;
   }
-  for (int i = tid; i < 4 * qt; i += 256) {
-    const int gi = i / qt, sl = i % qt, g0 = blockIdx.x * 4 + gi;
-    const int q = slot_query ? slot_query[tile * qt + sl] : tile * qt + sl;
+  for (int i = tid; i < kRunG0 * qt; i += 256) {
+    const int gi = i / qt, sl = i % qt, g0 = blockIdx.x * kRunG0 + gi;
+    const int q = sq[sl];
     const uint32_t gw = gword[tile * qt + sl];
     uint32_t c = 0x80808080u;  // never
-    if (q >= 0 && q < nq && gw >= 0x8000u && g0 < kbar) {
+    if (q >= 0 && gw >= 0x8000u && g0 < kbar) {
       const int D = (int)(gw - 0x8000u) - (int)q8[(int64_t)q * m * kbar + g0];  // e1 must be <= D
       if (D >= 127) c = 0u;  // any (clamped, <= 127) e1 passes
       else if (D >= 0) c = (uint32_t)(127 - D) * 0x01010101u;
@@ -561,41 +676,64 @@ __global__ void __launch_bounds__(256) k_run_potential(const uint8_t* __restrict
     c4[i] = c;
   }
   __syncthreads();
-  const int gi = tid >> 6, t = tid & 63, g0 = blockIdx.x * 4 + gi;
-  uint32_t acc = 0xFFFFFFFFu;
-  for (int sl = 0; sl < qt; ++sl) {
-    const uint32_t b = bw[sl * 64 + t], c = c4[gi * qt + sl];
-    acc &= b | ((b & 0x7F7F7F7Fu) + c);  // bit 7 clear: e1 <= D for this slot
+  const int t = tid & 63;
+  for (int gi = tid >> 6; gi < kRunG0; gi += 4) {
+    const int g0 = blockIdx.x * kRunG0 + gi;
+    uint32_t acc = 0xFFFFFFFFu;
+    for (int sl = 0; sl < qt; ++sl) {
+      const uint32_t b = bw[sl * 64 + t], c = c4[gi * qt + sl];
+      acc &= b | ((b & 0x7F7F7F7Fu) + c);  // bit 7 clear: e1 <= D for this slot
+    }
+    // byte b of the word = key (g0, 4t + b) has potential
+    if (g0 < kbar)
+      reinterpret_cast<uint32_t*>(pot + (int64_t)tile * 65536 + g0 * 256)[t] = (~acc & 0x80808080u) >> 7;
   }
-  // byte b of the word = key (g0, 4t + b) has potential
-  if (g0 < kbar) reinterpret_cast<uint32_t*>(pot + (int64_t)tile * 65536 + g0 * 256)[t] = (~acc & 0x80808080u) >> 7;
 }
 
+constexpr int kChunkPerThread = 4;  // k_chunk_list: chunks per thread, their loads in flight together
 __global__ void __launch_bounds__(256) k_chunk_list(const uint32_t* __restrict__ chunk_keys, int nchunks, int cr,
                                                     const uint8_t* __restrict__ pot, int* __restrict__ list,
                                                     int* __restrict__ list_len, int64_t n, int nb, int qt,
                                                     unsigned long long* __restrict__ n_rows) {
+  // CTA = (256 * kChunkPerThread chunks, tile); chunk c0 + 256 u + tid for u < kChunkPerThread
   const int tile = blockIdx.y, lane = threadIdx.x & 31;
-  const int c = blockIdx.x * 256 + threadIdx.x;
-  bool f = false;
-  if (c < nchunks) {
-    const uint32_t kk = chunk_keys[c];
-    const uint8_t* p = pot + (int64_t)tile * 65536;
-    for (uint32_t k = kk & 0xFFFFu; k <= (kk >> 16) && !f; ++k) f = p[k] != 0;
+  const int c0 = blockIdx.x * 256 * kChunkPerThread + threadIdx.x;
+  const uint8_t* p = pot + (int64_t)tile * 65536;
+  uint32_t kk[kChunkPerThread];
+#pragma unroll
+  for (int u = 0; u < kChunkPerThread; ++u) {
+    const int c = c0 + 256 * u;
+    kk[u] = c < nchunks ? __ldg(chunk_keys + c) : 1u;  // (empty key range lo = 1 > hi = 0)
   }
-  const uint32_t bal = __ballot_sync(0xffffffffu, f);
-  int base = 0;
-  if (lane == 0 && bal) base = atomicAdd(list_len + tile, __popc(bal));
+  bool f[kChunkPerThread];
+#pragma unroll
+  for (int u = 0; u < kChunkPerThread; ++u) {  // first key of each range: loads issued together
+    const uint32_t lo = kk[u] & 0xFFFFu;
+    f[u] = lo <= (kk[u] >> 16) && p[lo] != 0;
+  }
+#pragma unroll
+  for (int u = 0; u < kChunkPerThread; ++u)  // rest of the range (usually empty: ~150 rows per key)
+    for (uint32_t k = (kk[u] & 0xFFFFu) + 1; k <= (kk[u] >> 16) && !f[u]; ++k) f[u] = p[k] != 0;
+  unsigned rows = 0;
+#pragma unroll
+  for (int u = 0; u < kChunkPerThread; ++u) {
+    const int c = c0 + 256 * u;
+    const uint32_t bal = __ballot_sync(0xffffffffu, f[u]);
+    int base = 0;
+    if (lane == 0 && bal) base = atomicAdd(list_len + tile, __popc(bal));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (f[u]) {
+      list[(int64_t)tile * nchunks + base + __popc(bal & ((1u << lane) - 1u))] = c;
+      rows += (unsigned)min((int64_t)cr, n - (int64_t)c * cr);
+    }
+  }
   if (n_rows) {  // query-rows this tile will scan (its real queries x listed rows) and the listed plane rows
-    const unsigned rows = f ? (unsigned)min((int64_t)cr, n - (int64_t)c * cr) : 0u;
     const unsigned wr = __reduce_add_sync(0xffffffffu, rows);
     if (lane == 0 && wr) {
       atomicAdd(n_rows, (unsigned long long)wr * (unsigned long long)min(qt, nb - tile * qt));
       atomicAdd(n_rows + 1, (unsigned long long)wr);
     }
   }
-  base = __shfl_sync(0xffffffffu, base, 0);
-  if (f) list[(int64_t)tile * nchunks + base + __popc(bal & ((1u << lane) - 1u))] = c;
 }
 
 // ============================================================================
@@ -1456,25 +1594,50 @@ __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
 //   b*; B = min{b : cum_s[b] >= lambda + 3 sqrt(lambda) + 4}, else 254.
 // A guard that proves too tight is detected by K3 and redone exactly.
 // ============================================================================
-__global__ void k_guard(const uint32_t* __restrict__ hist, int nslot, int r2,
-                        double lambda, int exact, const uint8_t* __restrict__ only,
-                        uint16_t* __restrict__ guard_b, uint16_t* __restrict__ gword,
-                        const double* __restrict__ lambda_s) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+constexpr int kGuardSlotsPerCta = 4;  // k_guard: one warp per slot
+__global__ void __launch_bounds__(32 * kGuardSlotsPerCta)
+    k_guard(const uint32_t* __restrict__ hist, int nslot, int r2, double lambda, int exact,
+            const uint8_t* __restrict__ only, uint16_t* __restrict__ guard_b, uint16_t* __restrict__ gword,
+            const double* __restrict__ lambda_s) {
+  // lane l holds bins 8l .. 8l+7: lane-local running sums, a warp scan of
+  // the lane totals, then the first bin whose cumulative count reaches the
+  // target (bin 255 never counts: B <= 254)
+  const int s = blockIdx.x * kGuardSlotsPerCta + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (s >= nslot) return;
   if (only && !only[s]) return;
-  const uint32_t* h = hist + (int64_t)s * 256;
+  const uint4* h4 = reinterpret_cast<const uint4*>(hist + (int64_t)s * 256) + 2 * lane;
+  const uint4 a = __ldg(h4), b = __ldg(h4 + 1);
+  const uint32_t v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, lane == 31 ? 0u : b.w};
   const double lam = lambda_s ? lambda_s[s] : lambda;
   const bool ex = exact || lam < 0.0;  // lambda < 0: this slot's histogram is exact
   const double target = ex ? (double)r2 : lam + 3.0 * sqrt(lam) + 4.0;
-  uint64_t cum = 0;
-  int B = 254;
-  for (int b = 0; b < 255; ++b) {
-    cum += h[b];
-    if ((double)cum >= target) { B = b; break; }
+  uint64_t tot = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) tot += v[i];
+  uint64_t incl = tot;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t x = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += x;
   }
-  guard_b[s] = (uint16_t)B;
-  gword[s] = (uint16_t)(0x8000 + B);
+  uint64_t cum = incl - tot;
+  int first = 8;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    cum += v[i];
+    if (first == 8 && (double)cum >= target) first = i;
+  }
+  if (lane == 31 && first == 7) first = 8;  // (bin 255)
+  const uint32_t bal = __ballot_sync(0xffffffffu, first < 8);
+  int B = 254;
+  if (bal) {
+    const int src = __ffs(bal) - 1;
+    B = 8 * src + __shfl_sync(0xffffffffu, first, src);
+  }
+  if (lane == 0) {
+    guard_b[s] = (uint16_t)B;
+    gword[s] = (uint16_t)(0x8000 + B);
+  }
 }
 
 // ============================================================================
@@ -1492,47 +1655,98 @@ __global__ void __launch_bounds__(NT)
                 const uint8_t* __restrict__ only, int32_t* __restrict__ bstar,
                 int64_t* __restrict__ ncand, uint8_t* __restrict__ flags,
                 int32_t* __restrict__ hist_out, unsigned long long* __restrict__ n_emitted, int emit32) {
+  // per-warp sub-histograms (scores cluster in a few bins: 8x less shared
+  // atomic contention), emit lists read with 16-byte loads, two in flight
+  constexpr int NW = NT / 32;
+  __shared__ uint32_t hw[NW][256];
   __shared__ uint32_t h[256];
-  const int q = blockIdx.x;
+  const int q = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
   if (only && !only[q]) return;
   const uint32_t n = emit_cnt[q];
   if (n > cap) {
-    if (threadIdx.x == 0) { flags[q] = 2; bstar[q] = -1; }  // (-1: refine nothing until redone)
+    if (tid == 0) { flags[q] = 2; bstar[q] = -1; }  // (-1: refine nothing until redone)
     if (hist_out)  // sharded: this shard's histogram is unknown, export zeros (the query is redone)
-      for (int i = threadIdx.x; i < 256; i += NT) hist_out[(int64_t)q * 256 + i] = 0;
+      for (int i = tid; i < 256; i += NT) hist_out[(int64_t)q * 256 + i] = 0;
     return;
   }
-  for (int i = threadIdx.x; i < 256; i += NT) h[i] = 0;
-  if (n_emitted && threadIdx.x == 0) atomicAdd(n_emitted, (unsigned long long)n);
+  for (int i = tid; i < NW * 256; i += NT) (&hw[0][0])[i] = 0;
+  if (n_emitted && tid == 0) atomicAdd(n_emitted, (unsigned long long)n);
   __syncthreads();
+  uint32_t* hm = hw[tid >> 5];
   if (emit32) {
     const uint32_t* e = reinterpret_cast<const uint32_t*>(emit) + (int64_t)q * cap;
-    for (uint32_t i = threadIdx.x; i < n; i += NT) atomicAdd(h + (e[i] >> kRow32Bits), 1u);
+    uint32_t done = 0;
+    if ((reinterpret_cast<uintptr_t>(e) & 15) == 0) {
+      const uint4* e4 = reinterpret_cast<const uint4*>(e);
+      const uint32_t n4 = n / 4;
+      auto add4 = [&](uint4 v) {
+        atomicAdd(hm + (v.x >> kRow32Bits), 1u); atomicAdd(hm + (v.y >> kRow32Bits), 1u);
+        atomicAdd(hm + (v.z >> kRow32Bits), 1u); atomicAdd(hm + (v.w >> kRow32Bits), 1u);
+      };
+      for (uint32_t i = tid; i < n4; i += 2 * NT) {
+        const uint4 v0 = __ldg(e4 + i);
+        const bool has1 = i + NT < n4;
+        uint4 v1 = make_uint4(0u, 0u, 0u, 0u);
+        if (has1) v1 = __ldg(e4 + i + NT);
+        add4(v0);
+        if (has1) add4(v1);
+      }
+      done = n4 * 4;
+    }
+    for (uint32_t i = done + tid; i < n; i += NT) atomicAdd(hm + (e[i] >> kRow32Bits), 1u);
   } else {
     const uint64_t* e = emit + (int64_t)q * cap;
-    for (uint32_t i = threadIdx.x; i < n; i += NT) atomicAdd(h + emit_score(e[i]), 1u);
+    for (uint32_t i = tid; i < n; i += NT) atomicAdd(hm + emit_score(e[i]), 1u);
+  }
+  __syncthreads();
+  for (int b = tid; b < 256; b += NT) {
+    uint32_t v = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) v += hw[w][b];
+    h[b] = v;
   }
   __syncthreads();
   if (hist_out) {
-    for (int i = threadIdx.x; i < 256; i += NT) hist_out[(int64_t)q * 256 + i] = (int32_t)h[i];
-    if (threadIdx.x == 0) flags[q] = 0;
+    for (int i = tid; i < 256; i += NT) hist_out[(int64_t)q * 256 + i] = (int32_t)h[i];
+    if (tid == 0) flags[q] = 0;
     return;
   }
-  if (threadIdx.x == 0) {
+  if (tid < 32) {
+    // b* = first b <= B with cum[b] >= r2 (warp scan: lane l holds bins 8l .. 8l+7)
     const int B = guard_b[q];
-    int64_t cum = 0;
-    int bs = -1;
-    for (int b = 0; b <= B; ++b) {
-      cum += h[b];
-      if (cum >= r2) { bs = b; break; }
+    int64_t v[8], tot = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      v[i] = 8 * lane + i <= B ? (int64_t)h[8 * lane + i] : 0;
+      tot += v[i];
     }
-    if (bs >= 0) {
-      bstar[q] = bs; ncand[q] = cum; flags[q] = 0;
-    } else if (B >= 254) {
-      bstar[q] = 254; ncand[q] = cum; flags[q] = 0;
-    } else {
-      flags[q] = 1;
-      bstar[q] = -1;
+    int64_t incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t x = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += x;
+    }
+    int64_t cum = incl - tot, at = 0;
+    int first = 8;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      cum += v[i];
+      if (first == 8 && 8 * lane + i <= B && cum >= r2) { first = i; at = cum; }
+    }
+    const uint32_t bal = __ballot_sync(0xffffffffu, first < 8);
+    const int64_t all = __shfl_sync(0xffffffffu, incl, 31);
+    if (bal) {
+      const int src = __ffs(bal) - 1;
+      const int f = __shfl_sync(0xffffffffu, first, src);
+      const int64_t c = __shfl_sync(0xffffffffu, at, src);
+      if (lane == 0) { bstar[q] = 8 * src + f; ncand[q] = c; flags[q] = 0; }
+    } else if (lane == 0) {
+      if (B >= 254) {
+        bstar[q] = 254; ncand[q] = all; flags[q] = 0;
+      } else {
+        flags[q] = 1;
+        bstar[q] = -1;
+      }
     }
   }
 }
