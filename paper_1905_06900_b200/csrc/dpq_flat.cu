@@ -223,6 +223,20 @@ static inline float ev_ms(Index* h, int a, int b) {
   return ms;
 }
 
+// Fork / join: work enqueued on h->side between fork_side(h, i) and
+// join_side(h, i) runs concurrently with h->stream's (graph capture records
+// the two branches; eager runs overlap them the same way).
+static int fork_side(Index* h, int i) {
+  DPQ_CUDA(cudaEventRecord(h->fk[2 * i], h->stream));
+  DPQ_CUDA(cudaStreamWaitEvent(h->side, h->fk[2 * i], 0));
+  return DPQ_OK;
+}
+static int join_side(Index* h, int i) {
+  DPQ_CUDA(cudaEventRecord(h->fk[2 * i + 1], h->side));
+  DPQ_CUDA(cudaStreamWaitEvent(h->stream, h->fk[2 * i + 1], 0));
+  return DPQ_OK;
+}
+
 // ---------------------------------------------------------------------------
 // Launch helpers (template dispatch on MPAD)
 // ---------------------------------------------------------------------------
@@ -487,7 +501,17 @@ int prepare_flat_scan(Index* h, int nb, const ScanPlan& sp) {
                                             w.slot_query, w.gword_p);
     DPQ_LAUNCHED(h);
   }
-  DPQ_TRY(build_lut(h, nb, sp.gw, sp.slot_q));  // clamped tiles (modes 5/6/7) where the guards allow
+  if (sp.list) {
+    // the LUT tiles (side branch) and the run filter (main) both follow the slot order only
+    DPQ_TRY(fork_side(h, 0));
+    cudaStream_t main_stream = h->stream;
+    h->stream = h->side;
+    const int rc = build_lut(h, nb, sp.gw, sp.slot_q);  // clamped tiles (modes 5/6/7) where the guards allow
+    h->stream = main_stream;
+    DPQ_TRY(rc);
+  } else {
+    DPQ_TRY(build_lut(h, nb, sp.gw, sp.slot_q));
+  }
   if (sp.list) {  // run filter: per tile, the chunks whose (g0, g1) keys can reach a guard
     DPQ_CUDA(cudaMemsetAsync(w.list_len, 0, (size_t)tiles * 4, h->stream));
     k_run_potential<<<dim3(256 / kRunG0, tiles), 256, (size_t)qt * 64 * 4 + kRunG0 * qt * 4, h->stream>>>(
@@ -497,6 +521,7 @@ int prepare_flat_scan(Index* h, int nb, const ScanPlan& sp) {
                    h->stream>>>(
         h->chunk_keys, (int)h->n_chunks, 512 / h->mpad, w.pot, w.chunk_list, w.list_len, h->n, nb, qt, h->d_nrows);
     DPQ_LAUNCHED(h);
+    DPQ_TRY(join_side(h, 0));
   }
   return DPQ_OK;
 }
@@ -510,6 +535,10 @@ void plan_emit_args(Index* h, const ScanPlan& sp, EmitArgs& ea) {
 }
 
 static int flat_first_pass(Index* h, int nb, int r2) {
+  if (h->order_forked) {  // (a previous first pass that did not reach its refine)
+    h->order_forked = false;
+    DPQ_TRY(join_side(h, 1));
+  }
   Workspace& w = h->ws;
   const int qt = qt_of(h);
   const int tiles = tiles_of(nb, h);
@@ -545,6 +574,14 @@ static int flat_first_pass(Index* h, int nb, int r2) {
       h->plane_rows += (int64_t)tiles * n;
     }
     if (first) ev_rec(h, 3);
+    if (!h->no_spec && nb > 1 && attempt == 0) {
+      // the refine order (heaviest emit lists first) needs only the emit
+      // counts: computed on the side branch while K3 runs
+      DPQ_TRY(fork_side(h, 1));
+      k_order_by_count<<<1, 1024, 0, h->side>>>(w.emit_cnt, nb, w.cap, w.order);
+      DPQ_LAUNCHED(h);
+      h->order_forked = true;
+    }
     k_threshold<256><<<nb, 256, 0, h->stream>>>(w.emit, w.emit_cnt, w.cap, w.guard_b, r2, nullptr,
                                                 w.bstar, w.ncand, w.flags, nullptr, h->d_nemit, (int)h->emit32);
     DPQ_LAUNCHED(h);
@@ -752,7 +789,11 @@ static int flat_derived_batch_body(Index* h, int nb, int r, int r2) {
   if (rc != DPQ_OK) return rc;
   ev_rec(h, 5);
   RefineArgs ra = make_refine_args(h, r);
-  if (nb > 1) {  // heaviest emit lists first
+  if (h->order_forked) {  // computed on the side branch during K3
+    h->order_forked = false;
+    DPQ_TRY(join_side(h, 1));
+    ra.order = h->ws.order;
+  } else if (nb > 1) {  // heaviest emit lists first
     k_order_by_count<<<1, 1024, 0, h->stream>>>(h->ws.emit_cnt, nb, h->ws.cap, h->ws.order);
     DPQ_LAUNCHED(h);
     ra.order = h->ws.order;
@@ -1126,6 +1167,8 @@ int index_common_init(Index* h, int device, int m, int k, int kbar, int dsub, co
   DPQ_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   h->own_stream = true;
   for (int i = 0; i < 8; ++i) DPQ_CUDA(cudaEventCreate(&h->ev[i]));
+  DPQ_CUDA(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+  for (int i = 0; i < 4; ++i) DPQ_CUDA(cudaEventCreateWithFlags(&h->fk[i], cudaEventDisableTiming));
   DPQ_TRY(dmalloc(&h->cb, (size_t)m * k * dsub));
   DPQ_TRY(dmalloc(&h->dcb, (size_t)m * kbar * dsub));
   DPQ_TRY(dmalloc(&h->d_nref, 1));
@@ -1165,6 +1208,9 @@ void index_free(Index* h) {
     if (p) cudaFreeHost(p);
   for (int i = 0; i < 8; ++i)
     if (h->ev[i]) cudaEventDestroy(h->ev[i]);
+  for (int i = 0; i < 4; ++i)
+    if (h->fk[i]) cudaEventDestroy(h->fk[i]);
+  if (h->side) cudaStreamDestroy(h->side);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   delete h;
 }

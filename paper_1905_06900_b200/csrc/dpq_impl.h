@@ -122,6 +122,9 @@ struct Index {
   int batch = 1024;
   bool timing = false;
   cudaEvent_t ev[8] = {};
+  cudaStream_t side = nullptr;  // fork/join branch of the batch (independent kernels overlap)
+  cudaEvent_t fk[4] = {};       // fork / join events of the two branch points
+  bool order_forked = false;    // k_order_by_count already enqueued on `side` (speculative first pass)
   float phase_ms[PH_N] = {};
   int64_t counters[8] = {};  // launches, queries, rows scanned, refined, fallbacks, emitted, table entries, wide units
   unsigned long long* d_nref = nullptr;

@@ -507,7 +507,7 @@ constexpr int kSortMax = 4096;
 __global__ void __launch_bounds__(1024) k_sort_slots(const uint16_t* __restrict__ gword,
                                                       const uint16_t* __restrict__ cluster, int nq, int nslot_pad,
                                                       int* __restrict__ slot_query, uint16_t* __restrict__ gword_p) {
-  __shared__ uint64_t kv[kSortMax];
+  __shared__ uint32_t kv32[kSortMax];
   __shared__ int cnt[258];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   auto gkey = [&](int q) {
@@ -522,19 +522,19 @@ __global__ void __launch_bounds__(1024) k_sort_slots(const uint16_t* __restrict_
     int P = 1;
     while (P < nq) P <<= 1;
     const int E = P > 1024 ? P / 1024 : 1;
-    uint64_t x[EMAX];
+    uint32_t x[EMAX];  // key = class << 28 | cluster << 12 | q (q < kSortMax = 2^12)
 #pragma unroll
     for (int e = 0; e < EMAX; ++e) {
       const int q = e * 1024 + tid;
-      x[e] = ~0ull;
+      x[e] = 0xFFFFFFFFu;
       if (e < E && q < nq) {
         const int B = gkey(q);
-        const uint64_t cls = B == 256 ? 3u : (B <= 30 ? 0u : (B <= 62 ? 1u : 2u));
-        x[e] = (((cls << 16) | cluster[q]) << 32) | (uint32_t)q;
+        const uint32_t cls = B == 256 ? 3u : (B <= 30 ? 0u : (B <= 62 ? 1u : 2u));
+        x[e] = (cls << 28) | ((uint32_t)cluster[q] << 12) | (uint32_t)q;
       }
     }
     // element i keeps the min of (i, i ^ j) iff (i < partner) == ascending
-    auto keep = [](uint64_t mine, uint64_t other, bool take_min) {
+    auto keep = [](uint32_t mine, uint32_t other, bool take_min) {
       return take_min ? (other < mine ? other : mine) : (other > mine ? other : mine);
     };
     for (int size = 2; size <= P; size <<= 1) {
@@ -543,17 +543,20 @@ __global__ void __launch_bounds__(1024) k_sort_slots(const uint16_t* __restrict_
           const int ej = j / 1024;
 #pragma unroll
           for (int e = 0; e < EMAX; ++e) {
-            if (e >= E || (e & ej)) continue;
-            const int i = e * 1024 + tid;
-            const bool asc = (i & size) == 0;
-            const uint64_t a0 = x[e], a1 = x[e + ej];
-            x[e] = keep(a0, a1, asc);
-            x[e + ej] = keep(a1, a0, !asc);
+#pragma unroll
+            for (int f = e + 1; f < EMAX; ++f) {  // (compile-time indices: x stays in registers)
+              if (f >= E || f - e != ej || (e & ej)) continue;
+              const int i = e * 1024 + tid;
+              const bool asc = (i & size) == 0;
+              const uint32_t a0 = x[e], a1 = x[f];
+              x[e] = keep(a0, a1, asc);
+              x[f] = keep(a1, a0, !asc);
+            }
           }
         } else if (j >= 32) {
 #pragma unroll
           for (int e = 0; e < EMAX; ++e)
-            if (e < E) kv[e * 1024 + tid] = x[e];
+            if (e < E) kv32[e * 1024 + tid] = x[e];
           __syncthreads();
 #pragma unroll
           for (int e = 0; e < EMAX; ++e) {
@@ -561,7 +564,7 @@ __global__ void __launch_bounds__(1024) k_sort_slots(const uint16_t* __restrict_
             const int i = e * 1024 + tid;
             if (i >= P) continue;
             const bool asc = (i & size) == 0;
-            x[e] = keep(x[e], kv[i ^ j], ((i & j) == 0) == asc);
+            x[e] = keep(x[e], kv32[i ^ j], ((i & j) == 0) == asc);
           }
           __syncthreads();
         } else {
@@ -569,7 +572,7 @@ __global__ void __launch_bounds__(1024) k_sort_slots(const uint16_t* __restrict_
           for (int e = 0; e < EMAX; ++e) {
             if (e >= E) continue;
             const int i = e * 1024 + tid;
-            const uint64_t o = __shfl_xor_sync(0xffffffffu, x[e], j);
+            const uint32_t o = __shfl_xor_sync(0xffffffffu, x[e], j);
             const bool asc = (i & size) == 0;
             x[e] = keep(x[e], o, ((i & j) == 0) == asc);
           }
@@ -580,7 +583,7 @@ __global__ void __launch_bounds__(1024) k_sort_slots(const uint16_t* __restrict_
     for (int e = 0; e < EMAX; ++e) {
       const int sl = e * 1024 + tid;
       if (e < E && sl < nq) {
-        const int q = (int)(x[e] & 0xFFFFFFFFu);
+        const int q = (int)(x[e] & 0xFFFu);
         slot_query[sl] = q;
         gword_p[sl] = gword[q];
       }
@@ -613,7 +616,7 @@ __global__ void __launch_bounds__(1024) k_sort_slots(const uint16_t* __restrict_
 //   k_chunk_list: per tile, the scan chunks (512 B of plane) whose key range holds a key
 //     with pot = 1 (unordered list + length); the scan visits only those.
 // Skipped rows have score > B, so they would never be emitted: exact.
-constexpr int kRunG0 = 16;  // values of g0 per k_run_potential CTA
+constexpr int kRunG0 = 8;  // values of g0 per k_run_potential CTA
 __global__ void __launch_bounds__(256) k_run_potential(const uint8_t* __restrict__ q8, int m, int kbar,
                                                        const int* __restrict__ slot_query,
                                                        const uint16_t* __restrict__ gword, int qt, int nq,
@@ -663,17 +666,31 @@ __global__ void __launch_bounds__(256) k_run_potential(const uint8_t* __restrict
       }
     }
   }
-  for (int i = tid; i < kRunG0 * qt; i += 256) {
-    const int gi = i / qt, sl = i % qt, g0 = blockIdx.x * kRunG0 + gi;
-    const int q = sq[sl];
-    const uint32_t gw = gword[tile * qt + sl];
-    uint32_t c = 0x80808080u;  // never
-    if (q >= 0 && gw >= 0x8000u && g0 < kbar) {
-      const int D = (int)(gw - 0x8000u) - (int)q8[(int64_t)q * m * kbar + g0];  // e1 must be <= D
-      if (D >= 127) c = 0u;  // any (clamped, <= 127) e1 passes
-      else if (D >= 0) c = (uint32_t)(127 - D) * 0x01010101u;
+  {
+    constexpr int U = (kRunG0 * 256 + 255) / 256;  // (gi, slot) pairs per thread (qt <= 256), loads in flight together
+    int ge[U];
+    uint32_t gw[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = tid + 256 * u;
+      const int gi = i / qt, sl = i % qt, g0 = blockIdx.x * kRunG0 + gi;
+      const int q = i < kRunG0 * qt ? sq[sl] : -1;
+      gw[u] = q >= 0 ? (uint32_t)gword[tile * qt + sl] : 0u;
+      ge[u] = (q >= 0 && g0 < kbar) ? (int)__ldg(q8 + (int64_t)q * m * kbar + g0) : 0;
     }
-    c4[i] = c;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = tid + 256 * u;
+      if (i >= kRunG0 * qt) break;
+      const int gi = i / qt, sl = i % qt, g0 = blockIdx.x * kRunG0 + gi;
+      uint32_t c = 0x80808080u;  // never
+      if (sq[sl] >= 0 && gw[u] >= 0x8000u && g0 < kbar) {
+        const int D = (int)(gw[u] - 0x8000u) - ge[u];  // e1 must be <= D
+        if (D >= 127) c = 0u;  // any (clamped, <= 127) e1 passes
+        else if (D >= 0) c = (uint32_t)(127 - D) * 0x01010101u;
+      }
+      c4[i] = c;
+    }
   }
   __syncthreads();
   const int t = tid & 63;
@@ -711,21 +728,49 @@ __global__ void __launch_bounds__(256) k_chunk_list(const uint32_t* __restrict__
     const uint32_t lo = kk[u] & 0xFFFFu;
     f[u] = lo <= (kk[u] >> 16) && p[lo] != 0;
   }
+  // rest of the range, 16 keys per load (pot bytes are 0 / 1; bytes outside [lo, hi] masked)
+  auto any_in = [](uint4 v, uint32_t base, uint32_t lo, uint32_t hi) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    bool r = false;
 #pragma unroll
-  for (int u = 0; u < kChunkPerThread; ++u)  // rest of the range (usually empty: ~150 rows per key)
-    for (uint32_t k = (kk[u] & 0xFFFFu) + 1; k <= (kk[u] >> 16) && !f[u]; ++k) f[u] = p[k] != 0;
+    for (int k = 0; k < 4; ++k) {
+      const int b0 = (int)(base + 4 * k);
+      const int s0 = max((int)lo - b0, 0), s1 = min((int)hi - b0, 3);
+      if (s0 <= s1) r |= (w[k] & ((0xFFFFFFFFu << (8 * s0)) & (0xFFFFFFFFu >> (8 * (3 - s1))))) != 0u;
+    }
+    return r;
+  };
+  const uint4* p4 = reinterpret_cast<const uint4*>(p);
+#pragma unroll
+  for (int u = 0; u < kChunkPerThread; ++u) {
+    const uint32_t lo = (kk[u] & 0xFFFFu) + 1, hi = kk[u] >> 16;
+    for (uint32_t v = lo >> 4; v <= (hi >> 4) && lo <= hi && !f[u]; v += 2) {
+      const uint4 a = __ldg(p4 + v);
+      const bool two = v + 1 <= (hi >> 4);
+      const uint4 b = two ? __ldg(p4 + v + 1) : make_uint4(0u, 0u, 0u, 0u);
+      f[u] = any_in(a, 16 * v, lo, hi) || (two && any_in(b, 16 * (v + 1), lo, hi));
+    }
+  }
+  // one list reservation per warp for all its chunks
+  uint32_t bal[kChunkPerThread];
+  int tot = 0;
+#pragma unroll
+  for (int u = 0; u < kChunkPerThread; ++u) {
+    bal[u] = __ballot_sync(0xffffffffu, f[u]);
+    tot += __popc(bal[u]);
+  }
+  int base = 0;
+  if (lane == 0 && tot) base = atomicAdd(list_len + tile, tot);
+  base = __shfl_sync(0xffffffffu, base, 0);
   unsigned rows = 0;
 #pragma unroll
   for (int u = 0; u < kChunkPerThread; ++u) {
     const int c = c0 + 256 * u;
-    const uint32_t bal = __ballot_sync(0xffffffffu, f[u]);
-    int base = 0;
-    if (lane == 0 && bal) base = atomicAdd(list_len + tile, __popc(bal));
-    base = __shfl_sync(0xffffffffu, base, 0);
     if (f[u]) {
-      list[(int64_t)tile * nchunks + base + __popc(bal & ((1u << lane) - 1u))] = c;
+      list[(int64_t)tile * nchunks + base + __popc(bal[u] & ((1u << lane) - 1u))] = c;
       rows += (unsigned)min((int64_t)cr, n - (int64_t)c * cr);
     }
+    base += __popc(bal[u]);
   }
   if (n_rows) {  // query-rows this tile will scan (its real queries x listed rows) and the listed plane rows
     const unsigned wr = __reduce_add_sync(0xffffffffu, rows);
