@@ -55,6 +55,14 @@ const char* last_error() { return g_last_error.c_str(); }
     (h)->counters[0]++;                                                         \
   } while (0)
 
+// DPQ_DEBUG_ERR=1: report (and clear) a CUDA error left pending by an unchecked call.
+static void dbg_pending(const char* where) {
+  static const bool on = getenv("DPQ_DEBUG_ERR") != nullptr;
+  if (!on) return;
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) fprintf(stderr, "[dpq] pending CUDA error at %s: %s\n", where, cudaGetErrorString(e));
+}
+
 #define DPQ_TRY(expr)            \
   do {                           \
     int rc_ = (expr);            \
@@ -388,7 +396,7 @@ static int launch_refine(Index* h, const RefineArgs& ra, int nq) {
 // K1 for nslot slots whose queries are already in ws.y.
 // ---------------------------------------------------------------------------
 int build_lut(Index* h, int nslot, const uint16_t* gword, const int* slot_query = nullptr,
-              const int* slot_live = nullptr);
+              const int* slot_live = nullptr, const int* live = nullptr);
 // K1 over nslot slots (or only the n_list slots of slot_list) and, with lut,
 // the scan-layout LUT tiles of all nslot slots (slot_live: padding slots < 0).
 int run_small_tables(Index* h, int nslot, const void* prefix, int64_t npre,
@@ -440,20 +448,21 @@ int run_small_tables(Index* h, int nslot, const void* prefix, int64_t npre,
 
 // Scan-layout LUT tiles from ws.q8; with gword (guards known) tiles whose
 // guards are all <= 126 are clamped to 7-bit entries and flagged fast.
-int build_lut(Index* h, int nslot, const uint16_t* gword, const int* slot_query, const int* slot_live) {
+int build_lut(Index* h, int nslot, const uint16_t* gword, const int* slot_query, const int* slot_live,
+              const int* live) {
   Workspace& w = h->ws;
   const int ntiles = tiles_of(nslot, h);
   int* tf = w.tile_fast;  // reset to 0 when gword is null (unclamped LUT)
   const dim3 grid((unsigned)ntiles, (unsigned)h->mpad);
   if (h->mpad == 8)
     k_build_lut<8, 64><<<grid, 256, 0, h->stream>>>(w.q8, nslot, h->m, h->kbar, w.lut, ntiles, gword, tf, h->wide,
-                                                    slot_query, slot_live);
+                                                    slot_query, slot_live, live);
   else if (h->qt == 64)
     k_build_lut<4, 64><<<grid, 256, 0, h->stream>>>(w.q8, nslot, h->m, h->kbar, w.lut, ntiles, gword, tf, h->wide,
-                                                    slot_query, slot_live);
+                                                    slot_query, slot_live, live);
   else
     k_build_lut<4, 128><<<grid, 256, 0, h->stream>>>(w.q8, nslot, h->m, h->kbar, w.lut, ntiles, gword, tf, h->wide,
-                                                     slot_query, slot_live);
+                                                     slot_query, slot_live, live);
   DPQ_LAUNCHED(h);
   return DPQ_OK;
 }
@@ -468,7 +477,8 @@ int build_lut(Index* h, int nslot, const uint16_t* gword, const int* slot_query,
 // with sorted rows the run-filtered chunk lists.  Shared by the single-GPU
 // first pass and the sharded scan (dpq_shard_scan).
 struct ScanPlan {
-  bool sorted = false, list = false;
+  bool sorted = false, list = false, direct = false;
+  int item_cap = 0;
   const uint16_t* gw = nullptr;
   const int* slot_q = nullptr;
 };
@@ -489,6 +499,16 @@ int plan_flat_scan(Index* h, int nb, ScanPlan& sp) {
   }
   sp.gw = sp.sorted ? w.gword_p : w.gword;
   sp.slot_q = sp.sorted ? w.slot_query : nullptr;
+  // queries with few (g0, g1) keys under their guard are scanned one by one (k_scan_direct)
+  sp.direct = sp.list && h->direct && h->key_start && nb <= kDirMaxBatch;
+  if (sp.direct) {
+    sp.item_cap = h->direct_items > 0 ? h->direct_items : std::max(4096, 192 * nb);
+    if (w.dir_items_cap < sp.item_cap) {
+      DPQ_TRY(dmalloc(&w.dir_items, (size_t)sp.item_cap));
+      w.dir_items_cap = sp.item_cap;
+    }
+    if (!w.dir_state) DPQ_TRY(dmalloc(&w.dir_state, 2));
+  }
   return DPQ_OK;
 }
 
@@ -496,9 +516,21 @@ int prepare_flat_scan(Index* h, int nb, const ScanPlan& sp) {
   Workspace& w = h->ws;
   const int qt = qt_of(h);
   const int tiles = tiles_of(nb, h);
+  const int* live = nullptr;  // direct scan: the tile kernels return at once when no query is left to them
+  if (sp.direct) {
+    DPQ_CUDA(cudaMemsetAsync(w.dir_state, 0, 2 * sizeof(int), h->stream));
+    KeySelArgs ka;
+    ka.q8 = w.q8; ka.m = h->m; ka.kbar = h->kbar; ka.guard_b = w.guard_b; ka.gword = w.gword;
+    ka.key_start = h->key_start; ka.items = w.dir_items; ka.state = w.dir_state;
+    ka.item_cap = sp.item_cap; ka.item_qcap = std::max(64, sp.item_cap / 64); ka.pair_cap = 8192;
+    ka.n_rows = h->d_nrows;
+    k_key_select<<<nb, 256, 0, h->stream>>>(ka, nb);
+    DPQ_LAUNCHED(h);
+    live = w.dir_state + 1;
+  }
   if (sp.sorted) {
     k_sort_slots<<<1, 1024, 0, h->stream>>>(w.gword, h->m >= 2 ? w.cluster : nullptr, nb, tiles * qt,
-                                            w.slot_query, w.gword_p);
+                                            w.slot_query, w.gword_p, live);
     DPQ_LAUNCHED(h);
   }
   if (sp.list) {
@@ -506,28 +538,46 @@ int prepare_flat_scan(Index* h, int nb, const ScanPlan& sp) {
     DPQ_TRY(fork_side(h, 0));
     cudaStream_t main_stream = h->stream;
     h->stream = h->side;
-    const int rc = build_lut(h, nb, sp.gw, sp.slot_q);  // clamped tiles (modes 5/6/7) where the guards allow
+    const int rc = build_lut(h, nb, sp.gw, sp.slot_q, nullptr, live);  // clamped tiles (modes 5/6/7) where the guards allow
     h->stream = main_stream;
     DPQ_TRY(rc);
   } else {
-    DPQ_TRY(build_lut(h, nb, sp.gw, sp.slot_q));
+    DPQ_TRY(build_lut(h, nb, sp.gw, sp.slot_q, nullptr, live));
   }
   if (sp.list) {  // run filter: per tile, the chunks whose (g0, g1) keys can reach a guard
     DPQ_CUDA(cudaMemsetAsync(w.list_len, 0, (size_t)tiles * 4, h->stream));
     k_run_potential<<<dim3(256 / kRunG0, tiles), 256, (size_t)qt * 64 * 4 + kRunG0 * qt * 4, h->stream>>>(
-        w.q8, h->m, h->kbar, sp.slot_q, sp.gw, qt, nb, w.pot);
+        w.q8, h->m, h->kbar, sp.slot_q, sp.gw, qt, nb, w.pot, live);
     DPQ_LAUNCHED(h);
     k_chunk_list<<<dim3((unsigned)((h->n_chunks + 256 * kChunkPerThread - 1) / (256 * kChunkPerThread)), tiles), 256, 0,
                    h->stream>>>(
-        h->chunk_keys, (int)h->n_chunks, 512 / h->mpad, w.pot, w.chunk_list, w.list_len, h->n, nb, qt, h->d_nrows);
+        h->chunk_keys, (int)h->n_chunks, 512 / h->mpad, w.pot, w.chunk_list, w.list_len, h->n, nb, qt, h->d_nrows,
+        live);
     DPQ_LAUNCHED(h);
     DPQ_TRY(join_side(h, 0));
   }
   return DPQ_OK;
 }
 
+// The direct scan of the queries k_key_select took (after launch_emit: both
+// append to the emit lists with atomics, in any order).
+int launch_direct(Index* h, const ScanPlan& sp) {
+  if (!sp.direct) return DPQ_OK;
+  Workspace& w = h->ws;
+  DirectArgs da;
+  da.plane = h->plane; da.q8 = w.q8; da.m = h->m; da.kbar = h->kbar; da.guard_b = w.guard_b;
+  da.items = w.dir_items; da.state = w.dir_state; da.item_cap = sp.item_cap;
+  da.emit_cnt = w.emit_cnt; da.emit = w.emit; da.cap = w.cap; da.emit32 = (int)h->emit32;
+  const int grid = 8 * num_sms(h);  // 8 x 256 threads per SM, items strided over the warps
+  if (h->mpad == 8) k_scan_direct<8><<<grid, 256, 0, h->stream>>>(da);
+  else k_scan_direct<4><<<grid, 256, 0, h->stream>>>(da);
+  DPQ_LAUNCHED(h);
+  return DPQ_OK;
+}
+
 void plan_emit_args(Index* h, const ScanPlan& sp, EmitArgs& ea) {
   ea.gword = sp.gw;
+  ea.live = sp.direct ? h->ws.dir_state + 1 : nullptr;
   ea.slot_query = sp.slot_q;
   ea.chunk_list = sp.list ? h->ws.chunk_list : nullptr;
   ea.list_len = h->ws.list_len;
@@ -569,6 +619,7 @@ static int flat_first_pass(Index* h, int nb, int r2) {
     ea.unit_tile = nullptr; ea.unit_r0 = nullptr; ea.unit_r1 = nullptr;
     ea.emit_cnt = w.emit_cnt; ea.emit = w.emit; ea.cap = w.cap; ea.emit32 = (int)h->emit32;
     DPQ_TRY(launch_emit(h, ea, tiles, n));
+    DPQ_TRY(launch_direct(h, sp));
     if (!sp.list) {  // (list mode: counted on the device)
       h->counters[2] += (int64_t)nb * n;
       h->plane_rows += (int64_t)tiles * n;
@@ -1093,11 +1144,28 @@ static int sort_rows(Index* h) {
   if ((rc = dmalloc(&k0, (size_t)n)) || (rc = dmalloc(&k1, (size_t)n)) || (rc = dmalloc(&r0, (size_t)n)) ||
       (rc = dmalloc(&r1, (size_t)n))) { cleanup(); return rc; }
   const unsigned blocks = (unsigned)((n + 255) / 256);
-  k_row_keys<<<blocks, 256, 0, h->stream>>>(h->codes, h->code_bytes, n, h->m, h->mask, k0, r0);
-  cub::DeviceRadixSort::SortPairs(nullptr, tbytes, k0, k1, r0, r1, (int)n, 0, 16, h->stream);
+  {
+    dbg_pending("sort_rows entry");
+    cudaGetLastError();  // an error left pending by someone else's unchecked call is not this sort's (cub returns it)
+    k_row_keys<<<blocks, 256, 0, h->stream>>>(h->codes, h->code_bytes, n, h->m, h->mask, k0, r0);
+    const cudaError_t e1 = cudaGetLastError();
+    const cudaError_t e2 = cub::DeviceRadixSort::SortPairs(nullptr, tbytes, k0, k1, r0, r1, (int)n, 0, 16, h->stream);
+    if (e1 != cudaSuccess || e2 != cudaSuccess) {
+      cleanup();
+      set_error(std::string("row sort setup failed: keys '") + cudaGetErrorString(e1) + "', sort size '" +
+                cudaGetErrorString(e2) + "', n = " + std::to_string(n));
+      return DPQ_ERR_CUDA;
+    }
+  }
   if ((rc = dmalloc(&tmp, tbytes))) { cleanup(); return rc; }
-  if (cub::DeviceRadixSort::SortPairs(tmp, tbytes, k0, k1, r0, r1, (int)n, 0, 16, h->stream) != cudaSuccess) {
-    cleanup(); set_error("row sort failed"); return DPQ_ERR_CUDA;
+  {
+    const cudaError_t e = cub::DeviceRadixSort::SortPairs(tmp, tbytes, k0, k1, r0, r1, (int)n, 0, 16, h->stream);
+    if (e != cudaSuccess) {
+      cleanup();
+      set_error(std::string("row sort failed: ") + cudaGetErrorString(e) + " (n = " + std::to_string(n) +
+                ", temp bytes " + std::to_string(tbytes) + ")");
+      return DPQ_ERR_CUDA;
+    }
   }
   const int row_bytes = h->m * h->code_bytes;
   if ((rc = dmalloc(&sorted, (size_t)n * row_bytes + 16)) || (rc = dmalloc(&h->sorted_ids, (size_t)n))) {
@@ -1109,7 +1177,17 @@ static int sort_rows(Index* h) {
   h->n_chunks = (n + cr - 1) / cr;
   if ((rc = dmalloc(&h->chunk_keys, (size_t)h->n_chunks))) { cudaFree(sorted); cleanup(); return rc; }
   k_chunk_keys<<<(unsigned)((h->n_chunks + 255) / 256), 256, 0, h->stream>>>(k1, n, h->n_chunks, cr, h->chunk_keys);
-  if (cudaStreamSynchronize(h->stream) != cudaSuccess) { cleanup(); set_error("row sort failed"); return DPQ_ERR_CUDA; }
+  if (n < ((int64_t)1 << 32) - 2 * kDirSeg) {  // (direct scan items hold 32-bit rows)
+    if ((rc = dmalloc(&h->key_start, (size_t)65537))) { cudaFree(sorted); cleanup(); return rc; }
+    k_key_starts<<<(unsigned)((n + 1 + 255) / 256), 256, 0, h->stream>>>(k1, n, h->key_start);
+  }
+  {
+    cudaError_t e = cudaStreamSynchronize(h->stream);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      cleanup(); set_error(std::string("row sort failed (sync): ") + cudaGetErrorString(e)); return DPQ_ERR_CUDA;
+    }
+  }
   cleanup();
   if (h->prefix == h->codes) {  // original order stays as the qmax prefix
     h->own_prefix = true;
@@ -1159,6 +1237,8 @@ int index_common_init(Index* h, int device, int m, int k, int kbar, int dsub, co
   if (const char* e = getenv("DPQ_SORT_SLOTS")) h->sort_slots = atoi(e) != 0;
   if (const char* e = getenv("DPQ_SORT_ROWS")) h->sort_rows = atoi(e) != 0;
   if (const char* e = getenv("DPQ_RUN_FILTER")) h->run_filter = atoi(e) != 0;
+  if (const char* e = getenv("DPQ_DIRECT")) h->direct = atoi(e) != 0;
+  if (const char* e = getenv("DPQ_DIRECT_ITEMS")) h->direct_items = std::max(0, atoi(e));
   if (const char* e = getenv("DPQ_DIRECT_COPY")) h->direct_copy = atoi(e) != 0;
   if (const char* e = getenv("DPQ_SPECULATE")) h->no_spec = atoi(e) == 0;
   if (const char* e = getenv("DPQ_GRAPH")) h->use_graph = atoi(e) != 0;
@@ -1188,8 +1268,10 @@ int index_common_init(Index* h, int device, int m, int k, int kbar, int dsub, co
 
 void index_free(Index* h) {
   if (!h) return;
+  dbg_pending("index_free entry");
   cudaSetDevice(h->device);
   ivf_free(h);
+  dbg_pending("after ivf_free");
   if (h->stream) cudaStreamSynchronize(h->stream);
   tct_free(h->tct);
   if (h->tct_eps) cudaFree(h->tct_eps);
@@ -1197,12 +1279,16 @@ void index_free(Index* h) {
   if (h->graph.exec) cudaGraphExecDestroy(h->graph.exec);
   Workspace& w = h->ws;
   void* dev[] = {h->cb, h->dcb, h->codes, h->plane, h->own_prefix ? h->prefix : nullptr, h->centers,
-                 h->offsets, h->sorted_ids, h->d_nref, h->d_nemit, h->d_nent, h->d_nwide, h->d_nrows, h->chunk_keys, w.pot, w.chunk_list, w.list_len, w.y, w.small, w.q8, w.qmin, w.qmax, w.bounds,
+                 h->offsets, h->sorted_ids, h->d_nref, h->d_nemit, h->d_nent, h->d_nwide, h->d_nrows, h->chunk_keys, h->key_start, w.dir_items, w.dir_state, w.pot, w.chunk_list, w.list_len, w.y, w.small, w.q8, w.qmin, w.qmax, w.bounds,
                  w.lut, w.hist, w.hist_i, w.guard_b, w.gword, w.gword_p, w.emit_cnt, w.emit, w.bstar, w.ncand,
                  w.flags, w.only, w.tile_list, w.order, w.cluster, w.out_d, w.out_i, w.tables, w.slot_query, w.slot_probe,
                  w.slot_pre_off, w.slot_pre_len, w.counter, w.tile_fast};
+  dbg_pending("index_free before frees");
   for (void* p : dev)
-    if (p) cudaFree(p);
+    if (p) {
+      cudaFree(p);
+      dbg_pending("index_free cudaFree");
+    }
   void* host[] = {w.h_y, w.h_d, w.h_i, w.h_flags, w.h_cnt};
   for (void* p : host)
     if (p) cudaFreeHost(p);
@@ -1212,6 +1298,7 @@ void index_free(Index* h) {
     if (h->fk[i]) cudaEventDestroy(h->fk[i]);
   if (h->side) cudaStreamDestroy(h->side);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+  dbg_pending("index_free exit");
   delete h;
 }
 
@@ -1292,6 +1379,7 @@ int dpq_flat_create(int device, int m, int k, int kbar, int dsub, const float* c
     return DPQ_ERR_ARG;
   }
   if (n >= ((int64_t)1 << kRowBits)) { set_error("too many rows for one index shard"); return DPQ_ERR_ARG; }
+  dbg_pending("flat_create entry");
   Index* h = new Index();
   h->kind = KIND_FLAT;
   int rc = index_common_init(h, device, m, k, kbar, dsub, codebooks, derived_codebooks, code_bytes);

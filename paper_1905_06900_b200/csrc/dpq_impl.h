@@ -53,6 +53,9 @@ struct Workspace {
   uint8_t* pot = nullptr;       // run filter: [tiles][65536] key has potential
   int* chunk_list = nullptr;    // [tiles][n_chunks] chunks to scan
   int* list_len = nullptr;      // [tiles]
+  uint2* dir_items = nullptr;   // direct scan work items (k_key_select)
+  int dir_items_cap = 0;
+  int* dir_state = nullptr;     // [0] items reserved, [1] queries left to the tile scan
   int list_tiles = 0;
   int64_t list_chunks = 0;
   uint32_t* emit_cnt = nullptr;
@@ -152,6 +155,9 @@ struct Index {
   int direct_copy = 0;  // host API: copy straight from/to the caller's (pageable) buffers (env DPQ_DIRECT_COPY)
   int run_filter = 1;  // flat sorted rows: scan only chunks whose keys can reach a guard (env DPQ_RUN_FILTER=0)
   uint32_t* chunk_keys = nullptr;  // [n_chunks] first | last key << 16 of each 128-row chunk
+  uint32_t* key_start = nullptr;   // [65537] first row of every (g0, g1) key (sorted flat rows)
+  int direct = 1;          // per-query direct scan of the few (g0, g1) runs a query can hit (env DPQ_DIRECT=0 disables)
+  int direct_items = 0;    // work-item budget per batch (env DPQ_DIRECT_ITEMS; 0: 192 per query)
   int64_t n_chunks = 0;
   // tensor-core full tables (dpq_tctab.cu): prepared operand, per-batch
   // entry error bounds, mode (-1 auto: dsub >= 64; env DPQ_TC_TABLES=0/1)

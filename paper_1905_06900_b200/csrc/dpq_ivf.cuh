@@ -962,9 +962,8 @@ static int ivf_plan_dev(Index* h, IvfPlan& P, int nb, int ma, int r, int r2) {
   }
   // buffers (probe-, cell- and query-indexed)
   if (n > B.cap_pp || nb + 1 > B.cap_pk) {
-    void* old[] = {B.pl_key, B.pl_val, B.pl_key2, B.pl_val2, B.pl_first, B.pl_flag, B.pl_pos, B.pl_nr};
-    for (void* x : old)
-      if (x) cudaFree(x);
+    // (dmalloc releases the previous buffer itself: freeing it here as well
+    // would free it twice, and the second free could hit a buffer just handed out again)
     B.cap_pp = std::max(n, B.cap_pp);
     B.cap_pk = std::max(nb + 1, B.cap_pk);
     DPQ_TRY(dmalloc(&B.pl_key, (size_t)B.cap_pp));
@@ -1540,7 +1539,10 @@ int dpq_ivf_search_derived(dpq_index_t* index, const float* y, int64_t nq, int r
   if (nq < 0 || r < 1 || r2 < 1 || r > r2) { set_error("need 1 <= r <= r2"); return DPQ_ERR_ARG; }
   if (ma < 1 || ma > h->n_cells) { set_error("ma out of range"); return DPQ_ERR_ARG; }
   cudaSetDevice(h->device);
-  return ivf_driver(h, y, nq, r, ma, r2, true, res_rot, cells, dists, ids, phase_us);
+  dbg_pending("ivf_search_derived entry");
+  const int rc_ = ivf_driver(h, y, nq, r, ma, r2, true, res_rot, cells, dists, ids, phase_us);
+  dbg_pending("ivf_search_derived exit");
+  return rc_;
 }
 
 int dpq_ivf_search_conventional(dpq_index_t* index, const float* y, int64_t nq, int r, int ma,
@@ -1551,7 +1553,10 @@ int dpq_ivf_search_conventional(dpq_index_t* index, const float* y, int64_t nq, 
   if (nq < 0 || r < 1) { set_error("need r >= 1"); return DPQ_ERR_ARG; }
   if (ma < 1 || ma > h->n_cells) { set_error("ma out of range"); return DPQ_ERR_ARG; }
   cudaSetDevice(h->device);
-  return ivf_driver(h, y, nq, r, ma, 1, false, res_rot, cells, dists, ids, phase_us);
+  dbg_pending("ivf_search_conventional entry");
+  const int rc_ = ivf_driver(h, y, nq, r, ma, 1, false, res_rot, cells, dists, ids, phase_us);
+  dbg_pending("ivf_search_conventional exit");
+  return rc_;
 }
 
 // ------------------------------------------------- ivf list-split shards --
@@ -1750,6 +1755,7 @@ int dpq_shard_scan(dpq_index_t* index, const int32_t* sample_hist_sum, int64_t n
       ea.unit_tile = nullptr; ea.unit_r0 = nullptr; ea.unit_r1 = nullptr;
       ea.emit_cnt = w.emit_cnt; ea.emit = w.emit; ea.cap = w.cap; ea.emit32 = (int)h->emit32;
       DPQ_TRY(launch_emit(h, ea, tiles, h->n));
+      DPQ_TRY(launch_direct(h, sp));
       if (!sp.list) h->counters[2] += (int64_t)nb * h->n;
     }
     k_threshold<256><<<nb, 256, 0, h->stream>>>(w.emit, w.emit_cnt, w.cap, w.guard_b, r2, nullptr, w.bstar,
@@ -1872,6 +1878,7 @@ int dpq_shard_scan_dev(dpq_index_t* index, const int32_t* sample_hist_sum, int64
     ea.unit_tile = nullptr; ea.unit_r0 = nullptr; ea.unit_r1 = nullptr;
     ea.emit_cnt = w.emit_cnt; ea.emit = w.emit; ea.cap = w.cap; ea.emit32 = (int)h->emit32;
     DPQ_TRY(launch_emit(h, ea, tiles, h->n));
+    DPQ_TRY(launch_direct(h, sp));
     if (!sp.list) h->counters[2] += (int64_t)nb * h->n;
   }
   k_threshold<256><<<nb, 256, 0, h->stream>>>(w.emit, w.emit_cnt, w.cap, w.guard_b, r2, nullptr, w.bstar, w.ncand,

@@ -419,7 +419,9 @@ __global__ void __launch_bounds__(256) k_build_lut(const uint8_t* __restrict__ q
                                                    uint8_t* __restrict__ lut, int ntiles,
                                                    const uint16_t* __restrict__ gword, int* __restrict__ tile_fast,
                                                    int allow_wide, const int* __restrict__ slot_query,
-                                                   const int* __restrict__ slot_live) {
+                                                   const int* __restrict__ slot_live,
+                                                   const int* __restrict__ live = nullptr) {
+  if (live && *live == 0) return;  // every query took the direct scan
   // One CTA per (tile, subspace j): the QT slots' u8 rows of subspace j are
   // staged in shared memory ([slot][group], rows padded to 65 words so the
   // transposed reads below are conflict-free), then written as the tile's
@@ -506,7 +508,9 @@ __global__ void __launch_bounds__(256) k_build_lut(const uint8_t* __restrict__ q
 constexpr int kSortMax = 4096;
 __global__ void __launch_bounds__(1024) k_sort_slots(const uint16_t* __restrict__ gword,
                                                       const uint16_t* __restrict__ cluster, int nq, int nslot_pad,
-                                                      int* __restrict__ slot_query, uint16_t* __restrict__ gword_p) {
+                                                      int* __restrict__ slot_query, uint16_t* __restrict__ gword_p,
+                                                      const int* __restrict__ live = nullptr) {
+  if (live && *live == 0) return;  // every query took the direct scan
   __shared__ uint32_t kv32[kSortMax];
   __shared__ int cnt[258];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -620,7 +624,9 @@ constexpr int kRunG0 = 8;  // values of g0 per k_run_potential CTA
 __global__ void __launch_bounds__(256) k_run_potential(const uint8_t* __restrict__ q8, int m, int kbar,
                                                        const int* __restrict__ slot_query,
                                                        const uint16_t* __restrict__ gword, int qt, int nq,
-                                                       uint8_t* __restrict__ pot) {
+                                                       uint8_t* __restrict__ pot,
+                                                       const int* __restrict__ live = nullptr) {
+  if (live && *live == 0) return;  // every query took the direct scan
   // CTA = (16 values of g0, tile).  The tile's e1 words are staged once per
   // CTA with eight independent row loads in flight per thread (the load
   // latency, not the arithmetic, bounds this kernel).
@@ -711,7 +717,9 @@ constexpr int kChunkPerThread = 4;  // k_chunk_list: chunks per thread, their lo
 __global__ void __launch_bounds__(256) k_chunk_list(const uint32_t* __restrict__ chunk_keys, int nchunks, int cr,
                                                     const uint8_t* __restrict__ pot, int* __restrict__ list,
                                                     int* __restrict__ list_len, int64_t n, int nb, int qt,
-                                                    unsigned long long* __restrict__ n_rows) {
+                                                    unsigned long long* __restrict__ n_rows,
+                                                    const int* __restrict__ live = nullptr) {
+  if (live && *live == 0) return;  // every query took the direct scan (list lengths stay 0)
   // CTA = (256 * kChunkPerThread chunks, tile); chunk c0 + 256 u + tid for u < kChunkPerThread
   const int tile = blockIdx.y, lane = threadIdx.x & 31;
   const int c0 = blockIdx.x * 256 * kChunkPerThread + threadIdx.x;
@@ -777,6 +785,239 @@ __global__ void __launch_bounds__(256) k_chunk_list(const uint32_t* __restrict__
     if (lane == 0 && wr) {
       atomicAdd(n_rows, (unsigned long long)wr * (unsigned long long)min(qt, nb - tile * qt));
       atomicAdd(n_rows + 1, (unsigned long long)wr);
+    }
+  }
+}
+
+// ============================================================================
+// Direct first pass (flat indexes whose rows are sorted by key = g0 << 8 | g1).
+//
+// A row can reach a query's guard B only if e0[g0] + e1[g1] <= B, and on
+// clustered data a query has very few such keys (BASELINE configs[1]: a
+// median of ONE key, 0.3% of the rows, of which 60% are hits).  So instead of
+// testing 128 queries against the union of their rows (k_scan_emit), a query
+// whose keys are few is scanned on its own: k_key_select enumerates its keys,
+// cuts their row runs (key_start, built with the index) into work items of
+// <= kDirSeg rows, and k_scan_direct tests each row with two byte lookups in
+// the query's own 8-bit tables; hits are warp-compacted straight into the
+// query's emit list (one reservation per 128 rows, no staging, no per-hit
+// atomics).  The emitted set is exactly {rows : score <= B}, the same set
+// k_scan_emit emits, so K3 / K6 and the results are unchanged.  Queries with
+// too many keys or rows (large guards) stay on the tile path: k_key_select
+// leaves their guard word in place and replaces a direct query's by "no
+// guard" so the tile kernels see it as padding; with no query left they
+// return at once (`live`).
+// ============================================================================
+constexpr int kDirSeg = 1024;         // rows per work item
+constexpr uint32_t kDirNullQ = 0x3FFFu;
+constexpr int kDirMaxBatch = 0x3FFE;  // queries per batch the item format holds
+// item: x = first row, y = e01 | (rows - 1) << 8 | query << 18
+
+__global__ void k_key_starts(const uint32_t* __restrict__ skeys, int64_t n, uint32_t* __restrict__ key_start) {
+  // key_start[k] = first row whose key is >= k (k = 0 .. 65536); thread i owns the keys that start at row i
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > n) return;
+  const uint32_t k = i < n ? skeys[i] : 65536u;
+  const uint32_t kp = i > 0 ? skeys[i - 1] + 1u : 0u;
+  for (uint32_t key = kp; key <= k; ++key) key_start[key] = (uint32_t)i;
+}
+
+struct KeySelArgs {
+  const uint8_t* q8;           // [nq][m][kbar]
+  int m, kbar;
+  const uint16_t* guard_b;     // [nq] guard B
+  uint16_t* gword;             // [nq] guard words: rewritten (direct: 0x7F7F, tile path: 0x8000 + B)
+  const uint32_t* key_start;   // [65537]
+  uint2* items;
+  int* state;                  // [0] items reserved, [1] queries left to the tile path (zeroed before)
+  int item_cap, item_qcap, pair_cap;
+  unsigned long long* n_rows;  // optional counters: [0] query-rows, [1] plane rows
+};
+
+__device__ __forceinline__ int block_scan_256(int v, int* s_warp, int& total) {  // inclusive; blockDim = 256
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  __syncthreads();  // (s_warp reuse)
+  if (lane == 31) s_warp[warp] = x;
+  __syncthreads();
+  int add = 0, tot = 0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) {
+    const int sw = s_warp[w];
+    if (w < warp) add += sw;
+    tot += sw;
+  }
+  total = tot;
+  return x + add;
+}
+
+__global__ void __launch_bounds__(256) k_key_select(KeySelArgs a, int nq) {
+  __shared__ uint8_t s_e1[256];
+  __shared__ int s_cum[256];
+  __shared__ int s_warp[8];
+  __shared__ int s_base;
+  const int q = blockIdx.x, t = threadIdx.x;
+  if (q >= nq) return;
+  const int B = a.guard_b[q];
+  const uint8_t* e = a.q8 + (int64_t)q * a.m * a.kbar;
+  const int e0 = t < a.kbar ? (int)e[t] : 255;
+  const int e1 = t < a.kbar ? (int)e[a.kbar + t] : 255;
+  s_e1[t] = (uint8_t)e1;
+  s_cum[t] = 0;
+  __syncthreads();
+  if (t < a.kbar) atomicAdd(&s_cum[e1], 1);
+  __syncthreads();
+  int tot = 0;
+  const int c = block_scan_256(s_cum[t], s_warp, tot);  // c = #g1 with e1 <= t
+  __syncthreads();
+  s_cum[t] = c;
+  __syncthreads();
+  const int lim = t < a.kbar ? B - e0 : -1;  // e1 must be <= lim
+  int pairs = 0;
+  block_scan_256(lim >= 0 ? s_cum[min(lim, 255)] : 0, s_warp, pairs);
+  bool direct = pairs <= a.pair_cap;
+  int my_items = 0, items = 0, excl = 0;
+  long long my_rows = 0;
+  if (direct) {
+    if (lim >= 0)
+      for (int g1 = 0; g1 < a.kbar; ++g1)
+        if ((int)s_e1[g1] <= lim) {
+          const uint32_t key = ((uint32_t)t << 8) | (uint32_t)g1;
+          const uint32_t len = __ldg(a.key_start + key + 1) - __ldg(a.key_start + key);
+          my_items += (int)((len + kDirSeg - 1) / kDirSeg);
+          my_rows += len;
+        }
+    excl = block_scan_256(my_items, s_warp, items) - my_items;
+    direct = items <= a.item_qcap;
+  }
+  if (direct && items > 0) {
+    if (t == 0) s_base = atomicAdd(a.state, items);
+    __syncthreads();
+    const int base = s_base;
+    if (base + items > a.item_cap) {  // list full: null items over the reserved part, query stays on the tile path
+      direct = false;
+      for (int i = base + t; i < min(base + items, a.item_cap); i += 256) a.items[i] = make_uint2(0u, kDirNullQ << 18);
+    } else if (lim >= 0) {
+      int o = base + excl;
+      for (int g1 = 0; g1 < a.kbar; ++g1)
+        if ((int)s_e1[g1] <= lim) {
+          const uint32_t key = ((uint32_t)t << 8) | (uint32_t)g1;
+          uint32_t r0 = __ldg(a.key_start + key);
+          const uint32_t r1 = __ldg(a.key_start + key + 1);
+          const uint32_t e01 = (uint32_t)(e0 + (int)s_e1[g1]);
+          for (; r0 < r1; r0 += kDirSeg)
+            a.items[o++] = make_uint2(r0, e01 | ((min(r1 - r0, (uint32_t)kDirSeg) - 1u) << 8) | ((uint32_t)q << 18));
+        }
+    }
+  }
+  if (direct && a.n_rows) {  // rows this query tests (reported with the scan counters)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) my_rows += __shfl_xor_sync(0xffffffffu, my_rows, o);
+    if ((t & 31) == 0 && my_rows) {
+      atomicAdd(a.n_rows, (unsigned long long)my_rows);
+      atomicAdd(a.n_rows + 1, (unsigned long long)my_rows);
+    }
+  }
+  if (t == 0) {
+    a.gword[q] = direct ? (uint16_t)0x7F7Fu : (uint16_t)(0x8000 + B);
+    if (!direct) atomicAdd(a.state + 1, 1);
+  }
+}
+
+struct DirectArgs {
+  const uint8_t* plane;
+  const uint8_t* q8;
+  int m, kbar;
+  const uint16_t* guard_b;
+  const uint2* items;
+  const int* state;
+  int item_cap;
+  uint32_t* emit_cnt;
+  uint64_t* emit;
+  uint32_t cap;
+  int emit32;
+};
+
+template <int MPAD>
+__global__ void __launch_bounds__(256) k_scan_direct(DirectArgs a) {
+  constexpr int TB = (MPAD - 2) * 256;  // table bytes per warp: subspaces 2 .. MPAD-1
+  __shared__ __align__(16) uint8_t s_tab[8 * TB];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint8_t* tab = s_tab + warp * TB;
+  const uint32_t lt = (1u << lane) - 1u;
+  const int n_items = min(*a.state, a.item_cap);
+  const int nw = gridDim.x * 8;
+  int curq = -1;
+  for (int i = blockIdx.x * 8 + warp; i < n_items; i += nw) {
+    const uint2 it = __ldg(a.items + i);
+    const int q = (int)(it.y >> 18);
+    if (q == (int)kDirNullQ) continue;
+    const int len = (int)((it.y >> 8) & 0x3FFu) + 1;
+    const int e01 = (int)(it.y & 0xFFu);
+    if (q != curq) {
+      __syncwarp();
+      const uint8_t* src = a.q8 + ((int64_t)q * a.m + 2) * a.kbar;
+      const int nb = (a.m - 2) * a.kbar;
+      if (a.kbar == 256) {
+        for (int v = lane; v * 16 < nb; v += 32)
+          reinterpret_cast<uint4*>(tab)[v] = __ldg(reinterpret_cast<const uint4*>(src) + v);
+      } else {
+        for (int b = lane; b < nb; b += 32) tab[(b / a.kbar) * 256 + (b % a.kbar)] = src[b];
+      }
+      __syncwarp();
+      curq = q;
+    }
+    const int Bp = (int)a.guard_b[q] - e01;
+    const int64_t row0 = (int64_t)it.x;
+    uint32_t* cnt = a.emit_cnt + q;
+    for (int r0 = 0; r0 < len; r0 += 128) {
+      int tsum[4];
+      uint32_t bal[4];
+      int tot = 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int r = r0 + 32 * u + lane;
+        const bool in = r < len;
+        int tt = 0;
+        if constexpr (MPAD == 4) {
+          const uint32_t w = in ? __ldg(reinterpret_cast<const uint32_t*>(a.plane) + row0 + r) : 0u;
+          if (a.m > 2) tt += (int)tab[(w >> 16) & 0xFFu];
+          if (a.m > 3) tt += (int)tab[256 + (w >> 24)];
+        } else {
+          const uint2 w = in ? __ldg(reinterpret_cast<const uint2*>(a.plane) + row0 + r) : make_uint2(0u, 0u);
+          if (a.m > 2) tt += (int)tab[(w.x >> 16) & 0xFFu];
+          if (a.m > 3) tt += (int)tab[256 + (w.x >> 24)];
+          if (a.m > 4) tt += (int)tab[512 + (w.y & 0xFFu)];
+          if (a.m > 5) tt += (int)tab[768 + ((w.y >> 8) & 0xFFu)];
+          if (a.m > 6) tt += (int)tab[1024 + ((w.y >> 16) & 0xFFu)];
+          if (a.m > 7) tt += (int)tab[1280 + (w.y >> 24)];
+        }
+        tsum[u] = tt;
+        bal[u] = __ballot_sync(0xffffffffu, in && tt <= Bp);
+        tot += __popc(bal[u]);
+      }
+      if (tot == 0) continue;
+      uint32_t pos = 0;
+      if (lane == 0) pos = atomicAdd(cnt, (uint32_t)tot);
+      pos = __shfl_sync(0xffffffffu, pos, 0);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if ((bal[u] >> lane) & 1u) {
+          const uint32_t p = pos + (uint32_t)__popc(bal[u] & lt);
+          if (p < a.cap) {
+            const int64_t row = row0 + r0 + 32 * u + lane;
+            const uint32_t sc = (uint32_t)(e01 + tsum[u]);
+            if (a.emit32) reinterpret_cast<uint32_t*>(a.emit)[(int64_t)q * a.cap + p] = pack_emit32(row, sc);
+            else a.emit[(int64_t)q * a.cap + p] = pack_emit(row, 0u, sc);
+          }
+        }
+        pos += (uint32_t)__popc(bal[u]);
+      }
     }
   }
 }
@@ -1071,6 +1312,7 @@ struct EmitArgs {
   int units_per_tile;
   int emit32 = 0;               // 4-byte records (pack_emit32) instead of pack_emit
   unsigned long long* n_lut = nullptr;  // optional: LUT tile loads (bulk copies of G::LUT_BYTES)
+  const int* live = nullptr;    // optional: queries left to this scan (0: every query took the direct scan)
 };
 
 // Persistent scan.  Work unit = (query tile, contiguous row range); CTAs
@@ -1103,6 +1345,7 @@ template <int MPAD, int NT, int QTX = default_qt(MPAD)>
 __global__ void __launch_bounds__(NT, 1) k_scan_emit(EmitArgs a) {
   using G = ScanGeom<MPAD, QTX>;
   constexpr int NW = NT / 32;
+  if (a.live && *a.live == 0) return;
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ int s_unit;
   __shared__ int s_next;  // unit mode: the unit's next unclaimed chunk (warps balance within a unit)
