@@ -522,7 +522,7 @@ int prepare_flat_scan(Index* h, int nb, const ScanPlan& sp) {
     KeySelArgs ka;
     ka.q8 = w.q8; ka.m = h->m; ka.kbar = h->kbar; ka.guard_b = w.guard_b; ka.gword = w.gword;
     ka.key_start = h->key_start; ka.items = w.dir_items; ka.state = w.dir_state;
-    ka.item_cap = sp.item_cap; ka.item_qcap = std::max(64, sp.item_cap / 64); ka.pair_cap = 8192;
+    ka.item_cap = sp.item_cap; ka.item_qcap = std::max(64, sp.item_cap / 8); ka.pair_cap = 16384;
     ka.n_rows = h->d_nrows;
     k_key_select<<<nb, 256, 0, h->stream>>>(ka, nb);
     DPQ_LAUNCHED(h);
@@ -567,10 +567,25 @@ int launch_direct(Index* h, const ScanPlan& sp) {
   DirectArgs da;
   da.plane = h->plane; da.q8 = w.q8; da.m = h->m; da.kbar = h->kbar; da.guard_b = w.guard_b;
   da.items = w.dir_items; da.state = w.dir_state; da.item_cap = sp.item_cap;
-  da.emit_cnt = w.emit_cnt; da.emit = w.emit; da.cap = w.cap; da.emit32 = (int)h->emit32;
-  const int grid = 8 * num_sms(h);  // 8 x 256 threads per SM, items strided over the warps
-  if (h->mpad == 8) k_scan_direct<8><<<grid, 256, 0, h->stream>>>(da);
-  else k_scan_direct<4><<<grid, 256, 0, h->stream>>>(da);
+  da.emit_cnt = w.emit_cnt; da.emit = w.emit; da.cap = w.cap;
+  // one wave of resident CTAs, items strided over their warps
+  auto go = [&](auto kern, int slot) -> int {
+    static int per_sm[4] = {0, 0, 0, 0};
+    if (!per_sm[slot]) {
+      int nb = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 256, 0) != cudaSuccess || nb < 1) nb = 4;
+      per_sm[slot] = nb;
+    }
+    kern<<<per_sm[slot] * num_sms(h), 256, 0, h->stream>>>(da);
+    return DPQ_OK;
+  };
+  if (h->mpad == 8) {
+    if (h->emit32) go(k_scan_direct<8, true>, 0);
+    else go(k_scan_direct<8, false>, 1);
+  } else {
+    if (h->emit32) go(k_scan_direct<4, true>, 2);
+    else go(k_scan_direct<4, false>, 3);
+  }
   DPQ_LAUNCHED(h);
   return DPQ_OK;
 }

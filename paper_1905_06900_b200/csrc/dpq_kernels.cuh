@@ -857,18 +857,24 @@ __device__ __forceinline__ int block_scan_256(int v, int* s_warp, int& total) { 
 }
 
 __global__ void __launch_bounds__(256) k_key_select(KeySelArgs a, int nq) {
-  __shared__ uint8_t s_e1[256];
+  // One CTA per query.  Thread t plays g0 = t while the (g0, g1) pairs are
+  // counted, then g1 = t: for every g0 whose e0 leaves room under the guard
+  // the CTA tests its 256 keys (g0, t) together, reading the adjacent
+  // key_start words with coalesced loads.
   __shared__ int s_cum[256];
   __shared__ int s_warp[8];
-  __shared__ int s_base;
+  __shared__ int s_act[256];  // g0 values with e0 + min(e1) <= B
+  __shared__ uint8_t s_e0[256];
+  __shared__ int s_nact, s_base;
   const int q = blockIdx.x, t = threadIdx.x;
   if (q >= nq) return;
   const int B = a.guard_b[q];
   const uint8_t* e = a.q8 + (int64_t)q * a.m * a.kbar;
   const int e0 = t < a.kbar ? (int)e[t] : 255;
   const int e1 = t < a.kbar ? (int)e[a.kbar + t] : 255;
-  s_e1[t] = (uint8_t)e1;
   s_cum[t] = 0;
+  s_e0[t] = (uint8_t)e0;
+  if (t == 0) s_nact = 0;
   __syncthreads();
   if (t < a.kbar) atomicAdd(&s_cum[e1], 1);
   __syncthreads();
@@ -877,21 +883,36 @@ __global__ void __launch_bounds__(256) k_key_select(KeySelArgs a, int nq) {
   __syncthreads();
   s_cum[t] = c;
   __syncthreads();
-  const int lim = t < a.kbar ? B - e0 : -1;  // e1 must be <= lim
+  const int lim0 = t < a.kbar ? B - e0 : -1;  // (as g0) e1 must be <= lim0
+  const int np = lim0 >= 0 ? s_cum[min(lim0, 255)] : 0;
   int pairs = 0;
-  block_scan_256(lim >= 0 ? s_cum[min(lim, 255)] : 0, s_warp, pairs);
+  block_scan_256(np, s_warp, pairs);
   bool direct = pairs <= a.pair_cap;
   int my_items = 0, items = 0, excl = 0;
   long long my_rows = 0;
   if (direct) {
-    if (lim >= 0)
-      for (int g1 = 0; g1 < a.kbar; ++g1)
-        if ((int)s_e1[g1] <= lim) {
-          const uint32_t key = ((uint32_t)t << 8) | (uint32_t)g1;
-          const uint32_t len = __ldg(a.key_start + key + 1) - __ldg(a.key_start + key);
+    if (np > 0) s_act[atomicAdd(&s_nact, 1)] = t;
+    __syncthreads();
+    const int nact = s_nact;
+    // key_start words of 8 values of g0 in flight together (unconditional, coalesced loads)
+    for (int i0 = 0; i0 < nact; i0 += 8) {
+      uint32_t ks[8], ke[8];
+      int lim[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int g0 = s_act[min(i0 + u, nact - 1)];
+        lim[u] = i0 + u < nact ? B - (int)s_e0[g0] : -1;
+        ks[u] = __ldg(a.key_start + ((g0 << 8) | t));
+        ke[u] = __ldg(a.key_start + ((g0 << 8) | t) + 1);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (e1 <= lim[u]) {  // (t >= kbar: e1 = 255 never passes)
+          const uint32_t len = ke[u] - ks[u];
           my_items += (int)((len + kDirSeg - 1) / kDirSeg);
           my_rows += len;
         }
+    }
     excl = block_scan_256(my_items, s_warp, items) - my_items;
     direct = items <= a.item_qcap;
   }
@@ -902,17 +923,28 @@ __global__ void __launch_bounds__(256) k_key_select(KeySelArgs a, int nq) {
     if (base + items > a.item_cap) {  // list full: null items over the reserved part, query stays on the tile path
       direct = false;
       for (int i = base + t; i < min(base + items, a.item_cap); i += 256) a.items[i] = make_uint2(0u, kDirNullQ << 18);
-    } else if (lim >= 0) {
+    } else if (my_items > 0) {
       int o = base + excl;
-      for (int g1 = 0; g1 < a.kbar; ++g1)
-        if ((int)s_e1[g1] <= lim) {
-          const uint32_t key = ((uint32_t)t << 8) | (uint32_t)g1;
-          uint32_t r0 = __ldg(a.key_start + key);
-          const uint32_t r1 = __ldg(a.key_start + key + 1);
-          const uint32_t e01 = (uint32_t)(e0 + (int)s_e1[g1]);
-          for (; r0 < r1; r0 += kDirSeg)
-            a.items[o++] = make_uint2(r0, e01 | ((min(r1 - r0, (uint32_t)kDirSeg) - 1u) << 8) | ((uint32_t)q << 18));
+      const int nact = s_nact;
+      for (int i0 = 0; i0 < nact; i0 += 8) {
+        uint32_t ks[8], ke[8];
+        int e0g[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int g0 = s_act[min(i0 + u, nact - 1)];
+          e0g[u] = i0 + u < nact ? (int)s_e0[g0] : 1024;
+          ks[u] = __ldg(a.key_start + ((g0 << 8) | t));
+          ke[u] = __ldg(a.key_start + ((g0 << 8) | t) + 1);
         }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (e1 <= B - e0g[u]) {
+            const uint32_t e01 = (uint32_t)(e0g[u] + e1);
+            for (uint32_t r0 = ks[u]; r0 < ke[u]; r0 += kDirSeg)
+              a.items[o++] =
+                  make_uint2(r0, e01 | ((min(ke[u] - r0, (uint32_t)kDirSeg) - 1u) << 8) | ((uint32_t)q << 18));
+          }
+      }
     }
   }
   if (direct && a.n_rows) {  // rows this query tests (reported with the scan counters)
@@ -940,10 +972,9 @@ struct DirectArgs {
   uint32_t* emit_cnt;
   uint64_t* emit;
   uint32_t cap;
-  int emit32;
 };
 
-template <int MPAD>
+template <int MPAD, bool E32>
 __global__ void __launch_bounds__(256) k_scan_direct(DirectArgs a) {
   constexpr int TB = (MPAD - 2) * 256;  // table bytes per warp: subspaces 2 .. MPAD-1
   __shared__ __align__(16) uint8_t s_tab[8 * TB];
@@ -953,12 +984,27 @@ __global__ void __launch_bounds__(256) k_scan_direct(DirectArgs a) {
   const int n_items = min(*a.state, a.item_cap);
   const int nw = gridDim.x * 8;
   int curq = -1;
-  for (int i = blockIdx.x * 8 + warp; i < n_items; i += nw) {
-    const uint2 it = __ldg(a.items + i);
-    const int q = (int)(it.y >> 18);
+  int i = blockIdx.x * 8 + warp;
+  uint2 it = i < n_items ? __ldg(a.items + i) : make_uint2(0u, 0u);
+  for (; i < n_items; i += nw) {
+    const uint2 cur = it;
+    if (i + nw < n_items) it = __ldg(a.items + i + nw);  // next item in flight
+    const int q = (int)(cur.y >> 18);
     if (q == (int)kDirNullQ) continue;
-    const int len = (int)((it.y >> 8) & 0x3FFu) + 1;
-    const int e01 = (int)(it.y & 0xFFu);
+    const int len = (int)((cur.y >> 8) & 0x3FFu) + 1;
+    const uint32_t e01 = cur.y & 0xFFu;
+    // first rows of the item in flight before the tables are (re)loaded
+    const int64_t row0 = (int64_t)cur.x;
+    auto load_row = [&](int r, uint32_t& w0, uint32_t& w1) {
+      if constexpr (MPAD == 4) {
+        w0 = __ldg(reinterpret_cast<const uint32_t*>(a.plane) + row0 + r);
+        w1 = 0u;
+      } else {
+        const uint2 v = __ldg(reinterpret_cast<const uint2*>(a.plane) + row0 + r);
+        w0 = v.x; w1 = v.y;
+      }
+    };
+    const int Bp = (int)__ldg(a.guard_b + q) - (int)e01;
     if (q != curq) {
       __syncwarp();
       const uint8_t* src = a.q8 + ((int64_t)q * a.m + 2) * a.kbar;
@@ -972,49 +1018,71 @@ __global__ void __launch_bounds__(256) k_scan_direct(DirectArgs a) {
       __syncwarp();
       curq = q;
     }
-    const int Bp = (int)a.guard_b[q] - e01;
-    const int64_t row0 = (int64_t)it.x;
-    uint32_t* cnt = a.emit_cnt + q;
-    for (int r0 = 0; r0 < len; r0 += 128) {
-      int tsum[4];
-      uint32_t bal[4];
-      int tot = 0;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int r = r0 + 32 * u + lane;
-        const bool in = r < len;
-        int tt = 0;
-        if constexpr (MPAD == 4) {
-          const uint32_t w = in ? __ldg(reinterpret_cast<const uint32_t*>(a.plane) + row0 + r) : 0u;
-          if (a.m > 2) tt += (int)tab[(w >> 16) & 0xFFu];
-          if (a.m > 3) tt += (int)tab[256 + (w >> 24)];
-        } else {
-          const uint2 w = in ? __ldg(reinterpret_cast<const uint2*>(a.plane) + row0 + r) : make_uint2(0u, 0u);
-          if (a.m > 2) tt += (int)tab[(w.x >> 16) & 0xFFu];
-          if (a.m > 3) tt += (int)tab[256 + (w.x >> 24)];
-          if (a.m > 4) tt += (int)tab[512 + (w.y & 0xFFu)];
-          if (a.m > 5) tt += (int)tab[768 + ((w.y >> 8) & 0xFFu)];
-          if (a.m > 6) tt += (int)tab[1024 + ((w.y >> 16) & 0xFFu)];
-          if (a.m > 7) tt += (int)tab[1280 + (w.y >> 24)];
-        }
-        tsum[u] = tt;
-        bal[u] = __ballot_sync(0xffffffffu, in && tt <= Bp);
-        tot += __popc(bal[u]);
+    auto tsum_of = [&](uint32_t w0, uint32_t w1) -> int {
+      int tt = 0;
+      if (a.m > 2) tt += (int)tab[(w0 >> 16) & 0xFFu];
+      if (a.m > 3) tt += (int)tab[256 + (w0 >> 24)];
+      if constexpr (MPAD == 8) {
+        if (a.m > 4) tt += (int)tab[512 + (w1 & 0xFFu)];
+        if (a.m > 5) tt += (int)tab[768 + ((w1 >> 8) & 0xFFu)];
+        if (a.m > 6) tt += (int)tab[1024 + ((w1 >> 16) & 0xFFu)];
+        if (a.m > 7) tt += (int)tab[1280 + (w1 >> 24)];
       }
+      return tt;
+    };
+    uint32_t* cnt = a.emit_cnt + q;
+    uint32_t* e32 = reinterpret_cast<uint32_t*>(a.emit) + (int64_t)q * a.cap;
+    uint64_t* e64 = a.emit + (int64_t)q * a.cap;
+    // record of row (row0 + r) with score e01 + t:  E32: row | score << 24
+    const uint32_t rec0 = (uint32_t)row0 + (uint32_t)lane + (e01 << kRow32Bits);
+    for (int r0 = 0; r0 < len; r0 += 128) {
+      int ts[4];
+      uint32_t bal[4];
+      if (r0 + 128 <= len) {  // full group: no bounds tests
+        uint32_t w0[4], w1[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) load_row(r0 + 32 * u + lane, w0[u], w1[u]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          ts[u] = tsum_of(w0[u], w1[u]);
+          bal[u] = __ballot_sync(0xffffffffu, ts[u] <= Bp);
+        }
+      } else {
+        uint32_t w0[4], w1[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          w0[u] = 0u; w1[u] = 0u;
+          if (r0 + 32 * u + lane < len) load_row(r0 + 32 * u + lane, w0[u], w1[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          ts[u] = tsum_of(w0[u], w1[u]);
+          bal[u] = __ballot_sync(0xffffffffu, r0 + 32 * u + lane < len && ts[u] <= Bp);
+        }
+      }
+      const int tot = __popc(bal[0]) + __popc(bal[1]) + __popc(bal[2]) + __popc(bal[3]);
       if (tot == 0) continue;
       uint32_t pos = 0;
       if (lane == 0) pos = atomicAdd(cnt, (uint32_t)tot);
       pos = __shfl_sync(0xffffffffu, pos, 0);
+      if (pos + (uint32_t)tot > a.cap) {  // list overflow (K3 flags the query): store what fits
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t p = pos + (uint32_t)__popc(bal[u] & lt);
+          if (((bal[u] >> lane) & 1u) && p < a.cap) {
+            if constexpr (E32) e32[p] = rec0 + (uint32_t)(r0 + 32 * u) + ((uint32_t)ts[u] << kRow32Bits);
+            else e64[p] = pack_emit(row0 + r0 + 32 * u + lane, 0u, e01 + (uint32_t)ts[u]);
+          }
+          pos += (uint32_t)__popc(bal[u]);
+        }
+        continue;
+      }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         if ((bal[u] >> lane) & 1u) {
           const uint32_t p = pos + (uint32_t)__popc(bal[u] & lt);
-          if (p < a.cap) {
-            const int64_t row = row0 + r0 + 32 * u + lane;
-            const uint32_t sc = (uint32_t)(e01 + tsum[u]);
-            if (a.emit32) reinterpret_cast<uint32_t*>(a.emit)[(int64_t)q * a.cap + p] = pack_emit32(row, sc);
-            else a.emit[(int64_t)q * a.cap + p] = pack_emit(row, 0u, sc);
-          }
+          if constexpr (E32) e32[p] = rec0 + (uint32_t)(r0 + 32 * u) + ((uint32_t)ts[u] << kRow32Bits);
+          else e64[p] = pack_emit(row0 + r0 + 32 * u + lane, 0u, e01 + (uint32_t)ts[u]);
         }
         pos += (uint32_t)__popc(bal[u]);
       }
