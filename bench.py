@@ -363,16 +363,19 @@ def cpu_baseline(wl, cfg, args, gpu_ids):
 
 # ----------------------------------------------------------------- ours --
 
-def roofline(cfg, nb, ms_scan, dc, peak):
-    """The first-pass scan (k_scan_emit) against HBM, from counters read in
-    this run: plane rows the run-filtered scan read per query tile (MPAD B
-    each), LUT tiles bulk-copied into shared memory (128 KB each) and the
-    emitted (row, score) entries written (8 B each), per launch."""
+def roofline(cfg, nb, ms_scan, dc, peak, ms_refine=None):
+    """The first-pass scan against HBM, from counters read in this run: plane
+    rows the scan read (MPAD B each: the rows of the (g0, g1) runs a query can
+    hit for k_scan_direct, the listed chunks per query tile for k_scan_emit),
+    LUT tiles bulk-copied into shared memory (k_scan_emit, 128 KB each) and
+    the emitted (row, score) records written, per launch, over the CUDA-event
+    time of the scan launches."""
     mpad = 4 if cfg["m"] <= 4 else 8
+    rec = 4 if (cfg["n"] < (1 << 24) and cfg["m"] == 4) else 8  # emit record width (dpq_flat_create)
     steps = max(1, dc["launch_batches"])
     plane_b = dc["plane_rows"] * mpad / steps
     lut_b = dc["lut_loads"] * 128 * 1024 / steps
-    emit_b = dc["emitted"] * 8 / steps
+    emit_b = dc["emitted"] * rec / steps
     moved = plane_b + lut_b + emit_b
     achieved = moved / (ms_scan * 1e-3) / 1e9
     alg = float(cfg["n"]) * cfg["m"] * 2 * nb  # SURVEY §8d: N * m * 2 B of codes per query
@@ -383,18 +386,32 @@ def roofline(cfg, nb, ms_scan, dc, peak):
             traffic = int(prof["traffic_bytes"])
     except (OSError, ValueError, KeyError):
         pass
-    return {"bound": "hbm", "kernel": "k_scan_emit (first-pass scan, K2)", "achieved": round(achieved, 1),
-            "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-            "bytes_per_launch": {"plane": int(plane_b), "lut": int(lut_b), "emit": int(emit_b)},
-            "per_launch_ms": round(ms_scan, 4),
-            "counters": "dpq_counters_ex: plane rows read per query tile, LUT tile loads, emitted entries",
-            "traffic_source": "profiles/ncu_scan_traffic.json (ncu --set full of this config), else null",
-            "algorithmic": {"bytes_per_launch": alg, "gbs": round(alg / (ms_scan * 1e-3) / 1e9, 1),
-                            "frac": round(alg / (ms_scan * 1e-3) / 1e9 / peak, 3),
-                            "note": "SURVEY 8d: N*m*2 B of codes per query x the batch; > 1 because one pass "
-                                    "over the 4 B/row low-byte plane serves a 128-query tile and the (g0, g1) "
-                                    "run filter skips most rows"},
-            "limiter": "shared-memory LUT gathers + hit emission (issue-bound), not DRAM"}
+    out = {"bound": "hbm", "kernel": "first-pass scan, K2 (k_scan_direct per query over its (g0, g1) runs; "
+                                     "k_scan_emit for query tiles left to it)",
+           "achieved": round(achieved, 1),
+           "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+           "bytes_per_launch": {"plane": int(plane_b), "lut": int(lut_b), "emit": int(emit_b)},
+           "per_launch_ms": round(ms_scan, 4),
+           "counters": "dpq_counters_ex: plane rows read, LUT tile loads, emitted records",
+           "traffic_source": "profiles/ncu_scan_traffic.json (ncu --set full of this config), else null",
+           "algorithmic": {"bytes_per_launch": alg, "gbs": round(alg / (ms_scan * 1e-3) / 1e9, 1),
+                           "frac": round(alg / (ms_scan * 1e-3) / 1e9 / peak, 3),
+                           "note": "SURVEY 8d: N*m*2 B of codes per query x the batch; far above 1 because the "
+                                   "rows are sorted by (g0, g1) and a query only reads the runs whose two "
+                                   "entries fit under its guard (0.3% of the rows on this data)"},
+           "limiter": "instruction issue and load/atomic latency of the per-query compaction (plane rows are "
+                      "re-read from L2 by the queries that share a run), not DRAM"}
+    if ms_refine:
+        # second pass (K5 + K6, the largest share of the step): per candidate a code row (m x code bytes),
+        # its emit record and m exact table entries (4 B each) gathered, over the refine phase time
+        cand = dc["refined"] / steps
+        rb = cand * (cfg["m"] * 2 + rec + cfg["m"] * 4)
+        out["second_pass"] = {"kernel": "k_group_tables_reg + k_refine_topk (K5 + K6)",
+                              "bytes_per_launch": int(rb), "per_launch_ms": round(ms_refine, 4),
+                              "achieved": round(rb / (ms_refine * 1e-3) / 1e9, 1), "unit": "GB/s",
+                              "frac": round(rb / (ms_refine * 1e-3) / 1e9 / peak, 4),
+                              "limiter": "gather latency, exact (dist, id) selection barriers (issue ~59%)"}
+    return out
 
 
 def peaks():
@@ -487,7 +504,7 @@ def run_single(args, cfg):
     peak, peak_src = peaks()
     phases = {k: round(float(np.mean(phase[:, i])), 4) for i, k in
               enumerate(["tables", "guard", "scan", "threshold", "refine", "fallback", "batch"])}
-    rl = roofline(cfg, Bq, float(np.mean(phase[:, 2])), dc, peak)
+    rl = roofline(cfg, Bq, float(np.mean(phase[:, 2])), dc, peak, float(np.mean(phase[:, 4])))
     rl["peak_source"] = peak_src
     # e2e through the public API with host buffers
     e2e = None

@@ -507,7 +507,7 @@ int plan_flat_scan(Index* h, int nb, ScanPlan& sp) {
       DPQ_TRY(dmalloc(&w.dir_items, (size_t)sp.item_cap));
       w.dir_items_cap = sp.item_cap;
     }
-    if (!w.dir_state) DPQ_TRY(dmalloc(&w.dir_state, 2));
+    if (!w.dir_state) DPQ_TRY(dmalloc(&w.dir_state, 4));
   }
   return DPQ_OK;
 }
@@ -518,7 +518,7 @@ int prepare_flat_scan(Index* h, int nb, const ScanPlan& sp) {
   const int tiles = tiles_of(nb, h);
   const int* live = nullptr;  // direct scan: the tile kernels return at once when no query is left to them
   if (sp.direct) {
-    DPQ_CUDA(cudaMemsetAsync(w.dir_state, 0, 2 * sizeof(int), h->stream));
+    DPQ_CUDA(cudaMemsetAsync(w.dir_state, 0, 4 * sizeof(int), h->stream));
     KeySelArgs ka;
     ka.q8 = w.q8; ka.m = h->m; ka.kbar = h->kbar; ka.guard_b = w.guard_b; ka.gword = w.gword;
     ka.key_start = h->key_start; ka.items = w.dir_items; ka.state = w.dir_state;

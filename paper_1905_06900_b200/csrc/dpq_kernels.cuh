@@ -967,7 +967,7 @@ struct DirectArgs {
   int m, kbar;
   const uint16_t* guard_b;
   const uint2* items;
-  const int* state;
+  const int* state;  // [0] items listed
   int item_cap;
   uint32_t* emit_cnt;
   uint64_t* emit;
@@ -984,6 +984,8 @@ __global__ void __launch_bounds__(256) k_scan_direct(DirectArgs a) {
   const int n_items = min(*a.state, a.item_cap);
   const int nw = gridDim.x * 8;
   int curq = -1;
+  // (items strided over the warps: claiming them from a global counter
+  // instead, two ahead, measured slower — 88 -> 98 us — for ~50k claims)
   int i = blockIdx.x * 8 + warp;
   uint2 it = i < n_items ? __ldg(a.items + i) : make_uint2(0u, 0u);
   for (; i < n_items; i += nw) {
@@ -1077,14 +1079,17 @@ __global__ void __launch_bounds__(256) k_scan_direct(DirectArgs a) {
         }
         continue;
       }
+      uint32_t* g32 = e32 + pos;  // (one 64-bit base per group, 32-bit offsets below)
+      uint64_t* g64 = e64 + pos;
+      uint32_t off = 0;
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         if ((bal[u] >> lane) & 1u) {
-          const uint32_t p = pos + (uint32_t)__popc(bal[u] & lt);
-          if constexpr (E32) e32[p] = rec0 + (uint32_t)(r0 + 32 * u) + ((uint32_t)ts[u] << kRow32Bits);
-          else e64[p] = pack_emit(row0 + r0 + 32 * u + lane, 0u, e01 + (uint32_t)ts[u]);
+          const uint32_t p = off + (uint32_t)__popc(bal[u] & lt);
+          if constexpr (E32) g32[p] = rec0 + (uint32_t)(r0 + 32 * u) + ((uint32_t)ts[u] << kRow32Bits);
+          else g64[p] = pack_emit(row0 + r0 + 32 * u + lane, 0u, e01 + (uint32_t)ts[u]);
         }
-        pos += (uint32_t)__popc(bal[u]);
+        off += (uint32_t)__popc(bal[u]);
       }
     }
   }
