@@ -744,6 +744,15 @@ int run_group_tables(Index* h, int nq, int ystride) {
   ga.cb = h->cb; ga.y = w.y; ga.ystride = ystride; ga.q8 = w.q8; ga.bstar = w.bstar;
   ga.nq = nq; ga.m = h->m; ga.k = h->k; ga.kbar = h->kbar; ga.bbar = h->bbar; ga.dsub = h->dsub;
   ga.tables = w.tables; ga.n_entries = h->d_nent;
+  if (h->m <= 8 && h->gt_slack) {  // tighter activity test: the other subspaces' smallest entries count too
+    if (w.slack_cap < nq * h->m) {
+      DPQ_TRY(dmalloc(&w.slack, (size_t)nq * h->m));
+      w.slack_cap = nq * h->m;
+    }
+    k_entry_slack<<<(nq + 3) / 4, 128, 0, h->stream>>>(w.q8, nq, h->m, h->kbar, w.slack);
+    DPQ_LAUNCHED(h);
+    ga.slack = w.slack;
+  }
   const int gsize = h->k / h->kbar;
   const int ld = ((h->dsub & 7) == 0 && h->dsub <= 128) ? h->dsub + 4 : h->dsub + 1;  // k_group_tables rows
   const size_t smem = (size_t)gsize * ld * 4 + (size_t)nq * 4;
@@ -1253,6 +1262,7 @@ int index_common_init(Index* h, int device, int m, int k, int kbar, int dsub, co
   if (const char* e = getenv("DPQ_SORT_ROWS")) h->sort_rows = atoi(e) != 0;
   if (const char* e = getenv("DPQ_RUN_FILTER")) h->run_filter = atoi(e) != 0;
   if (const char* e = getenv("DPQ_DIRECT")) h->direct = atoi(e) != 0;
+  if (const char* e = getenv("DPQ_GT_SLACK")) h->gt_slack = atoi(e) != 0;
   if (const char* e = getenv("DPQ_DIRECT_ITEMS")) h->direct_items = std::max(0, atoi(e));
   if (const char* e = getenv("DPQ_DIRECT_COPY")) h->direct_copy = atoi(e) != 0;
   if (const char* e = getenv("DPQ_SPECULATE")) h->no_spec = atoi(e) == 0;
@@ -1294,7 +1304,7 @@ void index_free(Index* h) {
   if (h->graph.exec) cudaGraphExecDestroy(h->graph.exec);
   Workspace& w = h->ws;
   void* dev[] = {h->cb, h->dcb, h->codes, h->plane, h->own_prefix ? h->prefix : nullptr, h->centers,
-                 h->offsets, h->sorted_ids, h->d_nref, h->d_nemit, h->d_nent, h->d_nwide, h->d_nrows, h->chunk_keys, h->key_start, w.dir_items, w.dir_state, w.pot, w.chunk_list, w.list_len, w.y, w.small, w.q8, w.qmin, w.qmax, w.bounds,
+                 h->offsets, h->sorted_ids, h->d_nref, h->d_nemit, h->d_nent, h->d_nwide, h->d_nrows, h->chunk_keys, h->key_start, w.dir_items, w.dir_state, w.slack, w.pot, w.chunk_list, w.list_len, w.y, w.small, w.q8, w.qmin, w.qmax, w.bounds,
                  w.lut, w.hist, w.hist_i, w.guard_b, w.gword, w.gword_p, w.emit_cnt, w.emit, w.bstar, w.ncand,
                  w.flags, w.only, w.tile_list, w.order, w.cluster, w.out_d, w.out_i, w.tables, w.slot_query, w.slot_probe,
                  w.slot_pre_off, w.slot_pre_len, w.counter, w.tile_fast};

@@ -53,6 +53,8 @@ struct Workspace {
   uint8_t* pot = nullptr;       // run filter: [tiles][65536] key has potential
   int* chunk_list = nullptr;    // [tiles][n_chunks] chunks to scan
   int* list_len = nullptr;      // [tiles]
+  int32_t* slack = nullptr;     // [qb][m] group-table activity slack (k_entry_slack)
+  int slack_cap = 0;
   uint2* dir_items = nullptr;   // direct scan work items (k_key_select)
   int dir_items_cap = 0;
   int* dir_state = nullptr;     // [0] items reserved, [1] queries left to the tile scan
@@ -157,6 +159,7 @@ struct Index {
   uint32_t* chunk_keys = nullptr;  // [n_chunks] first | last key << 16 of each 128-row chunk
   uint32_t* key_start = nullptr;   // [65537] first row of every (g0, g1) key (sorted flat rows)
   int direct = 1;          // per-query direct scan of the few (g0, g1) runs a query can hit (env DPQ_DIRECT=0 disables)
+  int gt_slack = 1;        // group-table activity test tightened by the other subspaces' minima (env DPQ_GT_SLACK=0)
   int direct_items = 0;    // work-item budget per batch (env DPQ_DIRECT_ITEMS; 0: 192 per query)
   int64_t n_chunks = 0;
   // tensor-core full tables (dpq_tctab.cu): prepared operand, per-batch

@@ -866,15 +866,32 @@ __global__ void __launch_bounds__(256) k_key_select(KeySelArgs a, int nq) {
   __shared__ int s_act[256];  // g0 values with e0 + min(e1) <= B
   __shared__ uint8_t s_e0[256];
   __shared__ int s_nact, s_base;
+  __shared__ int s_rest;  // sum over subspaces j >= 2 of min_g e_j[g]
   const int q = blockIdx.x, t = threadIdx.x;
   if (q >= nq) return;
-  const int B = a.guard_b[q];
+  const int Bg = a.guard_b[q];
   const uint8_t* e = a.q8 + (int64_t)q * a.m * a.kbar;
   const int e0 = t < a.kbar ? (int)e[t] : 255;
   const int e1 = t < a.kbar ? (int)e[a.kbar + t] : 255;
   s_cum[t] = 0;
   s_e0[t] = (uint8_t)e0;
-  if (t == 0) s_nact = 0;
+  if (t == 0) { s_nact = 0; s_rest = 0; }
+  __syncthreads();
+  // a row of key (g0, g1) scores at least e0 + e1 + sum_{j >= 2} min e_j: only keys with
+  // e0 + e1 <= B = guard - that sum can hold a hit (the items still carry the full guard)
+  for (int j = 2; j < a.m; ++j) {
+    const unsigned v = __reduce_min_sync(0xffffffffu, t < a.kbar ? (unsigned)e[j * a.kbar + t] : 255u);
+    if ((t & 31) == 0) s_cum[(j - 2) * 8 + (t >> 5)] = (int)v;  // (s_cum reused: cleared below)
+  }
+  __syncthreads();
+  if (t < a.m - 2) {
+    int mn = 255;
+    for (int w = 0; w < 8; ++w) mn = min(mn, s_cum[t * 8 + w]);
+    atomicAdd(&s_rest, mn);
+  }
+  __syncthreads();
+  const int B = Bg - s_rest;
+  s_cum[t] = 0;
   __syncthreads();
   if (t < a.kbar) atomicAdd(&s_cum[e1], 1);
   __syncthreads();
@@ -956,7 +973,7 @@ __global__ void __launch_bounds__(256) k_key_select(KeySelArgs a, int nq) {
     }
   }
   if (t == 0) {
-    a.gword[q] = direct ? (uint16_t)0x7F7Fu : (uint16_t)(0x8000 + B);
+    a.gword[q] = direct ? (uint16_t)0x7F7Fu : (uint16_t)(0x8000 + Bg);
     if (!direct) atomicAdd(a.state + 1, 1);
   }
 }
@@ -2203,11 +2220,32 @@ __host__ __device__ __forceinline__ int64_t table_index(int q, int j, uint32_t c
 struct GroupTablesArgs {
   const float* cb; const float* y; int ystride;
   const uint8_t* q8; const int32_t* bstar;
+  const int32_t* slack = nullptr;  // [nq][m] sum over the other subspaces of their smallest entry (k_entry_slack)
   int nq, m, k, kbar, bbar, dsub;
   float* tables;
   unsigned long long* n_entries;
   unsigned long long negzero2 = kNegZero2;  // runtime (-0, -0) pair for sqdiff2 (see dpq_device.cuh)
 };
+
+// slack[q][j] = sum over subspaces i != j of min_g q8[q][i][g].  A candidate
+// (score <= b*) whose sub-code of subspace j lies in group g has
+// q8[q][j][g] <= b* - slack[q][j], so only those groups need exact entries.
+// One warp per query.
+__global__ void __launch_bounds__(128) k_entry_slack(const uint8_t* __restrict__ q8, int nq, int m, int kbar,
+                                                     int32_t* __restrict__ slack) {
+  const int q = blockIdx.x * 4 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (q >= nq) return;
+  const uint8_t* e = q8 + (int64_t)q * m * kbar;
+  int mn[8], sum = 0;
+  for (int j = 0; j < m && j < 8; ++j) {
+    unsigned v = 255u;
+    for (int g = lane; g < kbar; g += 32) v = min(v, (unsigned)e[j * kbar + g]);
+    mn[j] = (int)__reduce_min_sync(0xffffffffu, v);
+    sum += mn[j];
+  }
+  if (lane == 0)
+    for (int j = 0; j < m && j < 8; ++j) slack[q * m + j] = sum - mn[j];
+}
 
 // Register-row variant (DSUB = 32): thread ib holds codebook row ib of the
 // group in registers and loops over the group's active queries, whose
@@ -2225,7 +2263,8 @@ __global__ void __launch_bounds__(256) k_group_tables_reg(GroupTablesArgs a) {
   __syncthreads();
   // blockIdx.z of gridDim.z CTAs per group: queries q = z (mod gridDim.z)
   for (int q = blockIdx.z + tid * gridDim.z; q < a.nq; q += 256 * gridDim.z)
-    if ((int)a.q8[((int64_t)q * a.m + j) * a.kbar + g] <= a.bstar[q]) act[atomicAdd(&nact, 1)] = q;
+    if ((int)a.q8[((int64_t)q * a.m + j) * a.kbar + g] <= a.bstar[q] - (a.slack ? a.slack[q * a.m + j] : 0))
+      act[atomicAdd(&nact, 1)] = q;
   __syncthreads();
   const int n = nact;
   for (int ib0 = 0; ib0 < gsize; ib0 += 256) {
@@ -2291,7 +2330,8 @@ __global__ void __launch_bounds__(256) k_group_tables(GroupTablesArgs a) {
   }
   __syncthreads();
   for (int q = threadIdx.x; q < a.nq; q += 256)
-    if ((int)a.q8[((int64_t)q * a.m + j) * a.kbar + g] <= a.bstar[q]) act[atomicAdd(&nact, 1)] = q;
+    if ((int)a.q8[((int64_t)q * a.m + j) * a.kbar + g] <= a.bstar[q] - (a.slack ? a.slack[q * a.m + j] : 0))
+      act[atomicAdd(&nact, 1)] = q;
   __syncthreads();
   const int n = nact;
   for (int p = threadIdx.x; p < n * gsize; p += 256) {
