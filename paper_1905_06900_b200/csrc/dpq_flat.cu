@@ -502,7 +502,11 @@ int plan_flat_scan(Index* h, int nb, ScanPlan& sp) {
   // queries with few (g0, g1) keys under their guard are scanned one by one (k_scan_direct)
   sp.direct = sp.list && h->direct && h->key_start && nb <= kDirMaxBatch;
   if (sp.direct) {
-    sp.item_cap = h->direct_items > 0 ? h->direct_items : std::max(4096, 192 * nb);
+    // budget: on average n / 64 rows per query (beyond that the tile scan, which shares one pass over the
+    // rows between 128 queries, is cheaper), never less than 192 items per query
+    const int64_t per_q = std::max<int64_t>(192, h->n / ((int64_t)kDirSeg * 64) + 64);
+    sp.item_cap = h->direct_items > 0 ? h->direct_items
+                                      : (int)std::min<int64_t>((int64_t)1 << 26, std::max<int64_t>(4096, per_q * nb));
     if (w.dir_items_cap < sp.item_cap) {
       DPQ_TRY(dmalloc(&w.dir_items, (size_t)sp.item_cap));
       w.dir_items_cap = sp.item_cap;
