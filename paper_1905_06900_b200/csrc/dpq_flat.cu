@@ -779,8 +779,12 @@ int run_group_tables(Index* h, int nq, int ystride) {
 // Tensor-core full tables (dpq_tctab.cu) instead of the lazy exact group
 // tables: used where the lazy builder's CUDA-core work is large (dsub >= 64,
 // e.g. BASELINE configs[4]: 8 x 65536 x 120), or forced by DPQ_TC_TABLES.
-static bool use_tc_tables(Index* h) {
-  const int mode = h->use_tc >= 0 ? h->use_tc : (h->dsub >= 64 ? 1 : 0);
+// Auto: large sub-vectors, unless the candidate fraction is small (r2 / n <=
+// 1 / 4096): then the slack-tightened lazy tables touch so few groups (configs[4]:
+// 7.6k of 524k entries per query) that they beat the full GEMM by far.
+static bool use_tc_tables(Index* h, int r2) {
+  const bool few = h->gt_slack && r2 > 0 && (int64_t)r2 * 4096 <= h->n;
+  const int mode = h->use_tc >= 0 ? h->use_tc : ((h->dsub >= 64 && !few) ? 1 : 0);
   return mode != 0 && tct_supported(h->m, h->k, h->kbar, h->dsub);
 }
 
@@ -814,7 +818,7 @@ static int flat_derived_batch_body(Index* h, int nb, int r, int r2);
 // of ~20 kernel launches and memsets per batch.  The first call with a new
 // configuration runs eagerly (it sizes every buffer), the second captures.
 static int flat_derived_batch(Index* h, int nb, int r, int r2) {
-  if (use_tc_tables(h)) DPQ_TRY(ensure_tct(h));  // (synchronous, never inside a graph capture)
+  if (use_tc_tables(h, r2)) DPQ_TRY(ensure_tct(h));  // (synchronous, never inside a graph capture)
   const bool graphable = h->use_graph && !h->timing && !h->no_spec;
   if (!graphable) return flat_derived_batch_body(h, nb, r, r2);
   BatchGraph& G = h->graph;
@@ -877,7 +881,7 @@ static int flat_derived_batch_body(Index* h, int nb, int r, int r2) {
     DPQ_LAUNCHED(h);
     ra.order = h->ws.order;
   }
-  if (use_tc_tables(h)) {  // tensor-core full tables + exact re-rank of the margin set
+  if (use_tc_tables(h, r2)) {  // tensor-core full tables + exact re-rank of the margin set
     DPQ_TRY(run_tc_tables(h, nb, h->ws.y, h->d));
     ra.tables = h->ws.tables;
     ra.ny = h->tct_ny;

@@ -382,3 +382,42 @@ def test_graph_replay_and_speculation_match_eager(monkeypatch):
         d3, i3 = idx3.search(Y, 12, mode="derived", r2=200)
         assert np.array_equal(i3, outs[0][1]) and _same(d3, outs[0][0])
     assert idx3._handle().counters()["fallbacks"] > 0
+
+
+@pytest.mark.parametrize("m,bits", [(4, 12), (8, 11), (3, 10), (2, 9)])
+def test_direct_scan_vs_tile_scan_and_oracle(monkeypatch, m, bits):
+    """The per-query direct first pass (k_key_select + k_scan_direct over the
+    (g0, g1) key runs under the guard) emits exactly the tile scan's set:
+    identical results with DPQ_DIRECT=0, with an item budget so small that
+    part of the batch stays on the tile path (mixed batch, null-filled
+    reservations), with the slack-tightened group tables off, and against
+    the oracle; MPAD 4 and 8, m = 2 (no table lookups) and m = 3."""
+    import torch
+    from paper_1905_06900_b200 import train
+
+    st = datagen.seed_streams(33 + m)
+    centres = datagen.sift_centres(st["centres"])
+    X = datagen.sift_like(st["database"], centres, 90_000)
+    Y = datagen.sift_like(st["queries"], centres, 140)
+    d = X.shape[1] // m * m
+    X, Y = np.ascontiguousarray(X[:, :d]), np.ascontiguousarray(Y[:, :d])
+    xt = torch.as_tensor(X, device="cuda")
+    cb, der = train.train_pq(xt, m, bits, 4, iters=6, seed=33)  # kbar = 16
+    codes = train.encode(xt, cb).cpu().numpy().astype(np.uint16)
+    idx = FlatIndex.from_arrays(cb, der, codes)
+    d1, i1 = idx.search(Y, 20, mode="derived", r2=150)
+    b1, n1 = idx.candidate_counts(Y, 150)
+    for env in ({"DPQ_DIRECT": "0"}, {"DPQ_DIRECT_ITEMS": "96"}, {"DPQ_GT_SLACK": "0"},
+                {"DPQ_GRAPH": "0", "DPQ_SPECULATE": "0"}):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        idx2 = FlatIndex.from_arrays(cb, der, codes)
+        for _ in range(2):  # (second call: graph replay)
+            d2, i2 = idx2.search(Y, 20, mode="derived", r2=150)
+            assert np.array_equal(i1, i2) and _same(d1, d2), env
+        b2, n2 = idx2.candidate_counts(Y, 150)
+        assert np.array_equal(b1, b2) and np.array_equal(n1, n2), env
+        for k in env:
+            monkeypatch.delenv(k)
+    d0, i0 = _oracle(cb, der, codes, Y[:24], 20, 150)
+    assert np.array_equal(i0, i1[:24]) and _same(d0, d1[:24])
