@@ -74,7 +74,10 @@ static constexpr int kScanThreads = 1024;
 #define DPQ_EMIT_THREADS 1024
 #endif
 static constexpr int kEmitThreads = DPQ_EMIT_THREADS;  // (512 x 128 registers measured slower)
-static constexpr int kTopThreads = 256;
+#ifndef DPQ_TOP_THREADS
+#define DPQ_TOP_THREADS 256  // threads of a refine CTA (A/B: 512 with DPQ_REFINE_MINB=2)
+#endif
+static constexpr int kTopThreads = DPQ_TOP_THREADS;
 
 static uint64_t g_alloc_epoch = 0;  // bumped by every device (re)allocation (invalidates captured graphs)
 
