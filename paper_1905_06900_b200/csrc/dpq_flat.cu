@@ -481,6 +481,10 @@ int build_lut(Index* h, int nslot, const uint16_t* gword, const int* slot_query,
 // first pass and the sharded scan (dpq_shard_scan).
 struct ScanPlan {
   bool sorted = false, list = false, direct = false;
+  bool skip_tiles = false;      // (single-GPU speculative first pass only) tile kernels not launched
+  const uint32_t* hist = nullptr;  // when set, k_key_select computes the guard itself (k_guard's rule)
+  int r2 = 0, exact = 0;
+  double lambda = 0.0;
   int item_cap = 0;
   const uint16_t* gw = nullptr;
   const int* slot_q = nullptr;
@@ -515,6 +519,11 @@ int plan_flat_scan(Index* h, int nb, ScanPlan& sp) {
       w.dir_items_cap = sp.item_cap;
     }
     if (!w.dir_state) DPQ_TRY(dmalloc(&w.dir_state, 4));
+    if (!w.h_tileq) DPQ_TRY(hmalloc(&w.h_tileq, 1));
+    if (h->gt_slack && h->m <= 8 && w.slack_cap < nb * h->m) {
+      DPQ_TRY(dmalloc(&w.slack, (size_t)nb * h->m));
+      w.slack_cap = nb * h->m;
+    }
   }
   return DPQ_OK;
 }
@@ -531,9 +540,16 @@ int prepare_flat_scan(Index* h, int nb, const ScanPlan& sp) {
     ka.key_start = h->key_start; ka.items = w.dir_items; ka.state = w.dir_state;
     ka.item_cap = sp.item_cap; ka.item_qcap = std::max(64, sp.item_cap / 8); ka.pair_cap = 16384;
     ka.n_rows = h->d_nrows;
+    ka.hist = sp.hist; ka.r2 = sp.r2; ka.exact = sp.exact; ka.lambda = sp.lambda;
+    ka.skip_tiles = sp.skip_tiles ? 1 : 0;
+    if (h->gt_slack && h->m <= 8) ka.slack = w.slack;
     k_key_select<<<nb, 256, 0, h->stream>>>(ka, nb);
     DPQ_LAUNCHED(h);
+    w.slack_ready = ka.slack != nullptr;
     live = w.dir_state + 1;
+    if (sp.skip_tiles) return DPQ_OK;  // no tile kernels at all (see Index::tile_skip)
+  } else {
+    w.slack_ready = false;
   }
   if (sp.sorted) {
     k_sort_slots<<<1, 1024, 0, h->stream>>>(w.gword, h->m >= 2 ? w.cluster : nullptr, nb, tiles * qt,
@@ -623,13 +639,20 @@ static int flat_first_pass(Index* h, int nb, int r2) {
   const int64_t stride = exact ? 1 : n / nsamp;
   DPQ_TRY(launch_hist(h, tiles, nullptr, stride, nsamp, h->plane));
   const double lambda = (double)r2 * (double)nsamp / (double)std::max<int64_t>(n, 1);
-  k_guard<<<(nb + kGuardSlotsPerCta - 1) / kGuardSlotsPerCta, 32 * kGuardSlotsPerCta, 0, h->stream>>>(w.hist, nb, r2, lambda, exact ? 1 : 0, nullptr,
-                                                    w.guard_b, w.gword, nullptr);
-  DPQ_LAUNCHED(h);
   ScanPlan sp;
   DPQ_TRY(plan_flat_scan(h, nb, sp));
+  h->dir_batch = sp.direct;
+  if (sp.direct) {  // k_key_select computes the guard itself
+    sp.hist = w.hist; sp.r2 = r2; sp.exact = exact ? 1 : 0; sp.lambda = lambda;
+    sp.skip_tiles = h->tile_skip && h->tile_skip_ok && !h->no_spec && nb > 1;
+  } else {
+    k_guard<<<(nb + kGuardSlotsPerCta - 1) / kGuardSlotsPerCta, 32 * kGuardSlotsPerCta, 0, h->stream>>>(w.hist, nb, r2, lambda, exact ? 1 : 0, nullptr,
+                                                      w.guard_b, w.gword, nullptr);
+    DPQ_LAUNCHED(h);
+  }
   auto sort_and_build = [&]() -> int { return prepare_flat_scan(h, nb, sp); };
   DPQ_TRY(sort_and_build());
+  sp.hist = nullptr;  // (an exact redo below sets its guards with k_guard)
   ev_rec(h, 2);
   bool first = true;
   for (int attempt = 0; attempt < 8; ++attempt) {
@@ -640,7 +663,7 @@ static int flat_first_pass(Index* h, int nb, int r2) {
     plan_emit_args(h, sp, ea);
     ea.unit_tile = nullptr; ea.unit_r0 = nullptr; ea.unit_r1 = nullptr;
     ea.emit_cnt = w.emit_cnt; ea.emit = w.emit; ea.cap = w.cap; ea.emit32 = (int)h->emit32;
-    DPQ_TRY(launch_emit(h, ea, tiles, n));
+    if (!sp.skip_tiles) DPQ_TRY(launch_emit(h, ea, tiles, n));
     DPQ_TRY(launch_direct(h, sp));
     if (!sp.list) {  // (list mode: counted on the device)
       h->counters[2] += (int64_t)nb * n;
@@ -661,6 +684,8 @@ static int flat_first_pass(Index* h, int nb, int r2) {
     if (first) ev_rec(h, 4);
     first = false;
     DPQ_CUDA(cudaMemcpyAsync(w.h_flags, w.flags, nb, cudaMemcpyDeviceToHost, h->stream));
+    if (sp.direct && attempt == 0)
+      DPQ_CUDA(cudaMemcpyAsync(w.h_tileq, w.dir_state + 1, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
     if (!h->no_spec) {
       // speculative: the batch goes on (flagged queries have b* = -1 and
       // refine nothing); the caller checks h_flags after its final sync and
@@ -756,8 +781,11 @@ int run_group_tables(Index* h, int nq, int ystride) {
       DPQ_TRY(dmalloc(&w.slack, (size_t)nq * h->m));
       w.slack_cap = nq * h->m;
     }
-    k_entry_slack<<<(nq + 3) / 4, 128, 0, h->stream>>>(w.q8, nq, h->m, h->kbar, w.slack);
-    DPQ_LAUNCHED(h);
+    if (!w.slack_ready) {  // (else k_key_select wrote this batch's slack)
+      k_entry_slack<<<(nq + 3) / 4, 128, 0, h->stream>>>(w.q8, nq, h->m, h->kbar, w.slack);
+      DPQ_LAUNCHED(h);
+    }
+    w.slack_ready = false;
     ga.slack = w.slack;
   }
   const int gsize = h->k / h->kbar;
@@ -826,7 +854,7 @@ static int flat_derived_batch(Index* h, int nb, int r, int r2) {
   if (!graphable) return flat_derived_batch_body(h, nb, r, r2);
   BatchGraph& G = h->graph;
   const bool same = G.nb == nb && G.r == r && G.r2 == r2 && G.host_out == (int)h->host_out &&
-                    G.epoch == g_alloc_epoch;
+                    G.tile_skip == h->tile_skip && G.epoch == g_alloc_epoch;
   if (G.exec && same) {
     DPQ_CUDA(cudaGraphLaunch(G.exec, h->stream));
     for (int i = 0; i < 8; ++i) h->counters[i] += G.counters[i];
@@ -836,7 +864,7 @@ static int flat_derived_batch(Index* h, int nb, int r, int r2) {
   if (!same || !G.warm) {  // eager run; capture on the next call with this configuration
     if (G.exec) { cudaGraphExecDestroy(G.exec); G.exec = nullptr; }
     const int rc = flat_derived_batch_body(h, nb, r, r2);
-    G.nb = nb; G.r = r; G.r2 = r2; G.host_out = (int)h->host_out; G.epoch = g_alloc_epoch; G.warm = rc == DPQ_OK;
+    G.nb = nb; G.r = r; G.r2 = r2; G.host_out = (int)h->host_out; G.tile_skip = h->tile_skip; G.epoch = g_alloc_epoch; G.warm = rc == DPQ_OK;
     return rc;
   }
   int64_t c0[8];
@@ -999,9 +1027,18 @@ static cudaError_t sync_copy_out(cudaStream_t st, void* d0, const void* s0, size
 static bool spec_failed(Index* h) {
   const int nb = h->spec_nb;
   h->spec_nb = 0;
-  for (int q = 0; q < nb; ++q)
-    if (h->ws.h_flags[q]) return true;
-  return false;
+  bool failed = false;
+  for (int q = 0; q < nb && !failed; ++q) failed = h->ws.h_flags[q] != 0;
+  if (nb > 0 && h->dir_batch && h->ws.h_tileq) {  // adaptive tile-kernel skipping (Index::tile_skip)
+    if (h->tile_skip) {
+      if (failed) { h->tile_skip = 0; h->skip_streak = 0; }
+    } else if (!failed && *h->ws.h_tileq == 0) {
+      if (++h->skip_streak >= 2) h->tile_skip = 1;
+    } else {
+      h->skip_streak = 0;
+    }
+  }
+  return failed;
 }
 
 template <class F>
@@ -1274,6 +1311,7 @@ int index_common_init(Index* h, int device, int m, int k, int kbar, int dsub, co
   if (const char* e = getenv("DPQ_RUN_FILTER")) h->run_filter = atoi(e) != 0;
   if (const char* e = getenv("DPQ_DIRECT")) h->direct = atoi(e) != 0;
   if (const char* e = getenv("DPQ_GT_SLACK")) h->gt_slack = atoi(e) != 0;
+  if (const char* e = getenv("DPQ_TILE_SKIP")) h->tile_skip_ok = atoi(e) != 0;
   if (const char* e = getenv("DPQ_DIRECT_ITEMS")) h->direct_items = std::max(0, atoi(e));
   if (const char* e = getenv("DPQ_DIRECT_COPY")) h->direct_copy = atoi(e) != 0;
   if (const char* e = getenv("DPQ_SPECULATE")) h->no_spec = atoi(e) == 0;
@@ -1325,7 +1363,7 @@ void index_free(Index* h) {
       cudaFree(p);
       dbg_pending("index_free cudaFree");
     }
-  void* host[] = {w.h_y, w.h_d, w.h_i, w.h_flags, w.h_cnt};
+  void* host[] = {w.h_y, w.h_d, w.h_i, w.h_flags, w.h_cnt, w.h_tileq};
   for (void* p : host)
     if (p) cudaFreeHost(p);
   for (int i = 0; i < 8; ++i)

@@ -53,8 +53,10 @@ struct Workspace {
   uint8_t* pot = nullptr;       // run filter: [tiles][65536] key has potential
   int* chunk_list = nullptr;    // [tiles][n_chunks] chunks to scan
   int* list_len = nullptr;      // [tiles]
-  int32_t* slack = nullptr;     // [qb][m] group-table activity slack (k_entry_slack)
+  int32_t* slack = nullptr;     // [qb][m] group-table activity slack (k_entry_slack / k_key_select)
   int slack_cap = 0;
+  bool slack_ready = false;     // this batch's slack was written by k_key_select
+  int* h_tileq = nullptr;       // pinned: queries the last first pass left to the tile scan (dir_state[1])
   uint2* dir_items = nullptr;   // direct scan work items (k_key_select)
   int dir_items_cap = 0;
   int* dir_state = nullptr;     // [0] items reserved, [1] queries left to the tile scan
@@ -89,7 +91,7 @@ struct Workspace {
 
 struct BatchGraph {
   cudaGraphExec_t exec = nullptr;
-  int nb = -1, r = -1, r2 = -1, host_out = -1;
+  int nb = -1, r = -1, r2 = -1, host_out = -1, tile_skip = -1;
   uint64_t epoch = 0;
   bool warm = false;
   int64_t counters[8] = {};  // host counter increments of one captured batch
@@ -159,6 +161,12 @@ struct Index {
   uint32_t* chunk_keys = nullptr;  // [n_chunks] first | last key << 16 of each 128-row chunk
   uint32_t* key_start = nullptr;   // [65537] first row of every (g0, g1) key (sorted flat rows)
   int direct = 1;          // per-query direct scan of the few (g0, g1) runs a query can hit (env DPQ_DIRECT=0 disables)
+  // Adaptive: after batches in which every query took the direct scan the tile kernels are not even
+  // launched (a query that needs them makes K3 flag the batch, which is redone with them).
+  int tile_skip = 0;       // current mode
+  int skip_streak = 0;     // consecutive all-direct speculative batches
+  int tile_skip_ok = 1;    // env DPQ_TILE_SKIP=0 disables
+  bool dir_batch = false;  // the last first pass ran k_key_select (h_tileq is valid after its sync)
   int gt_slack = 1;        // group-table activity test tightened by the other subspaces' minima (env DPQ_GT_SLACK=0)
   int direct_items = 0;    // work-item budget per batch (env DPQ_DIRECT_ITEMS; 0: 192 per query)
   int64_t n_chunks = 0;

@@ -822,10 +822,50 @@ __global__ void k_key_starts(const uint32_t* __restrict__ skeys, int64_t n, uint
   for (uint32_t key = kp; key <= k; ++key) key_start[key] = (uint32_t)i;
 }
 
+// Guard B of one slot from its (sample or exact) score histogram, computed by
+// one warp (see k_guard below for the rule): lane l holds bins 8l .. 8l+7.
+__device__ __forceinline__ int guard_of_hist(const uint32_t* __restrict__ hist_row, int lane, int r2, double lam,
+                                             bool ex) {
+  const uint4* h4 = reinterpret_cast<const uint4*>(hist_row) + 2 * lane;
+  const uint4 a = __ldg(h4), b = __ldg(h4 + 1);
+  const uint32_t v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, lane == 31 ? 0u : b.w};
+  const double target = ex ? (double)r2 : lam + 3.0 * sqrt(lam) + 4.0;
+  uint64_t tot = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) tot += v[i];
+  uint64_t incl = tot;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t x = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += x;
+  }
+  uint64_t cum = incl - tot;
+  int first = 8;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    cum += v[i];
+    if (first == 8 && (double)cum >= target) first = i;
+  }
+  if (lane == 31 && first == 7) first = 8;  // (bin 255)
+  const uint32_t bal = __ballot_sync(0xffffffffu, first < 8);
+  int B = 254;
+  if (bal) {
+    const int src = __ffs(bal) - 1;
+    B = 8 * src + __shfl_sync(0xffffffffu, first, src);
+  }
+  return B;
+}
+
 struct KeySelArgs {
   const uint8_t* q8;           // [nq][m][kbar]
   int m, kbar;
-  const uint16_t* guard_b;     // [nq] guard B
+  uint16_t* guard_b;           // [nq] guard B (read; written when hist is given or a query is handed back, see skip_tiles)
+  const uint32_t* hist = nullptr;  // optional [nq][256] score histograms: the guard is computed here (k_guard's rule)
+  int r2 = 0, exact = 0;
+  double lambda = 0.0;
+  int32_t* slack = nullptr;    // optional [nq][m]: k_entry_slack's output, computed here
+  int skip_tiles = 0;          // the tile kernels are not launched: a query that needs them gets guard 0, which
+                               // K3 flags as too tight (the batch is then redone with the tile path)
   uint16_t* gword;             // [nq] guard words: rewritten (direct: 0x7F7F, tile path: 0x8000 + B)
   const uint32_t* key_start;   // [65537]
   uint2* items;
@@ -867,9 +907,18 @@ __global__ void __launch_bounds__(256) k_key_select(KeySelArgs a, int nq) {
   __shared__ uint8_t s_e0[256];
   __shared__ int s_nact, s_base;
   __shared__ int s_rest;  // sum over subspaces j >= 2 of min_g e_j[g]
+  __shared__ int s_guard;
+  __shared__ int s_min[8];
   const int q = blockIdx.x, t = threadIdx.x;
   if (q >= nq) return;
-  const int Bg = a.guard_b[q];
+  if (a.hist) {
+    if (t < 32) {
+      const int Bh = guard_of_hist(a.hist + (int64_t)q * 256, t, a.r2, a.lambda, a.exact != 0 || a.lambda < 0.0);
+      if (t == 0) s_guard = Bh;
+    }
+    __syncthreads();
+  }
+  const int Bg = a.hist ? s_guard : (int)a.guard_b[q];
   const uint8_t* e = a.q8 + (int64_t)q * a.m * a.kbar;
   const int e0 = t < a.kbar ? (int)e[t] : 255;
   const int e1 = t < a.kbar ? (int)e[a.kbar + t] : 255;
@@ -879,17 +928,23 @@ __global__ void __launch_bounds__(256) k_key_select(KeySelArgs a, int nq) {
   __syncthreads();
   // a row of key (g0, g1) scores at least e0 + e1 + sum_{j >= 2} min e_j: only keys with
   // e0 + e1 <= B = guard - that sum can hold a hit (the items still carry the full guard)
-  for (int j = 2; j < a.m; ++j) {
+  for (int j = 0; j < a.m && j < 8; ++j) {
     const unsigned v = __reduce_min_sync(0xffffffffu, t < a.kbar ? (unsigned)e[j * a.kbar + t] : 255u);
-    if ((t & 31) == 0) s_cum[(j - 2) * 8 + (t >> 5)] = (int)v;  // (s_cum reused: cleared below)
+    if ((t & 31) == 0) s_cum[j * 8 + (t >> 5)] = (int)v;  // (s_cum reused: cleared below)
   }
   __syncthreads();
-  if (t < a.m - 2) {
+  if (t < a.m && t < 8) {
     int mn = 255;
     for (int w = 0; w < 8; ++w) mn = min(mn, s_cum[t * 8 + w]);
-    atomicAdd(&s_rest, mn);
+    s_min[t] = mn;
+    if (t >= 2) atomicAdd(&s_rest, mn);
   }
   __syncthreads();
+  if (a.slack && t < a.m && t < 8) {  // slack[q][j] = sum of the other subspaces' smallest entries (k_entry_slack)
+    int sum = 0;
+    for (int j = 0; j < a.m && j < 8; ++j) sum += s_min[j];
+    a.slack[q * a.m + t] = sum - s_min[t];
+  }
   const int B = Bg - s_rest;
   s_cum[t] = 0;
   __syncthreads();
@@ -974,6 +1029,7 @@ __global__ void __launch_bounds__(256) k_key_select(KeySelArgs a, int nq) {
   }
   if (t == 0) {
     a.gword[q] = direct ? (uint16_t)0x7F7Fu : (uint16_t)(0x8000 + Bg);
+    if (a.hist || (a.skip_tiles && !direct)) a.guard_b[q] = (uint16_t)((a.skip_tiles && !direct) ? 0 : Bg);
     if (!direct) atomicAdd(a.state + 1, 1);
   }
 }
@@ -1979,39 +2035,12 @@ __global__ void __launch_bounds__(32 * kGuardSlotsPerCta)
             const double* __restrict__ lambda_s) {
   // lane l holds bins 8l .. 8l+7: lane-local running sums, a warp scan of
   // the lane totals, then the first bin whose cumulative count reaches the
-  // target (bin 255 never counts: B <= 254)
+  // target (bin 255 never counts: B <= 254) — guard_of_hist
   const int s = blockIdx.x * kGuardSlotsPerCta + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (s >= nslot) return;
   if (only && !only[s]) return;
-  const uint4* h4 = reinterpret_cast<const uint4*>(hist + (int64_t)s * 256) + 2 * lane;
-  const uint4 a = __ldg(h4), b = __ldg(h4 + 1);
-  const uint32_t v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, lane == 31 ? 0u : b.w};
   const double lam = lambda_s ? lambda_s[s] : lambda;
-  const bool ex = exact || lam < 0.0;  // lambda < 0: this slot's histogram is exact
-  const double target = ex ? (double)r2 : lam + 3.0 * sqrt(lam) + 4.0;
-  uint64_t tot = 0;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) tot += v[i];
-  uint64_t incl = tot;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint64_t x = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += x;
-  }
-  uint64_t cum = incl - tot;
-  int first = 8;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    cum += v[i];
-    if (first == 8 && (double)cum >= target) first = i;
-  }
-  if (lane == 31 && first == 7) first = 8;  // (bin 255)
-  const uint32_t bal = __ballot_sync(0xffffffffu, first < 8);
-  int B = 254;
-  if (bal) {
-    const int src = __ffs(bal) - 1;
-    B = 8 * src + __shfl_sync(0xffffffffu, first, src);
-  }
+  const int B = guard_of_hist(hist + (int64_t)s * 256, lane, r2, lam, exact || lam < 0.0);  // lambda < 0: exact histogram
   if (lane == 0) {
     guard_b[s] = (uint16_t)B;
     gword[s] = (uint16_t)(0x8000 + B);

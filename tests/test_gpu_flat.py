@@ -421,3 +421,43 @@ def test_direct_scan_vs_tile_scan_and_oracle(monkeypatch, m, bits):
             monkeypatch.delenv(k)
     d0, i0 = _oracle(cb, der, codes, Y[:24], 20, 150)
     assert np.array_equal(i0, i1[:24]) and _same(d0, d1[:24])
+
+
+def test_tile_skip_mode_and_fallback(monkeypatch):
+    """After batches in which every query took the direct scan the tile
+    kernels are not launched at all (no LUT tile loads); a later batch that
+    needs them (large r2: every key admissible) is flagged by K3 and redone
+    with the tile path.  Results equal the tile-only pipeline throughout."""
+    import torch
+    from paper_1905_06900_b200 import train
+
+    st = datagen.seed_streams(41)
+    centres = datagen.sift_centres(st["centres"])
+    X = datagen.sift_like(st["database"], centres, 120_000)
+    Y = datagen.sift_like(st["queries"], centres, 96)
+    xt = torch.as_tensor(X, device="cuda")
+    cb, der = train.train_pq(xt, 4, 12, 4, iters=6, seed=41)
+    codes = train.encode(xt, cb).cpu().numpy().astype(np.uint16)
+    idx = FlatIndex.from_arrays(cb, der, codes)
+    monkeypatch.setenv("DPQ_DIRECT", "0")
+    ref = FlatIndex.from_arrays(cb, der, codes)
+    monkeypatch.delenv("DPQ_DIRECT")
+    d_small, i_small = ref.search(Y, 10, mode="derived", r2=100)
+    d_big, i_big = ref.search(Y, 10, mode="derived", r2=60_000)
+    luts = lambda: idx._handle().counters_ex()["lut_loads"]
+    deltas = []
+    for _ in range(6):  # eager, capture, replay; then the skip mode (recapture, replay)
+        l0 = luts()
+        d, i = idx.search(Y, 10, mode="derived", r2=100)
+        deltas.append(luts() - l0)
+        assert np.array_equal(i, i_small) and _same(d, d_small)
+    # (the sample-histogram tiles are loaded by k_scan_hist, not counted; the scan's are)
+    assert deltas[-1] == 0, deltas
+    l0 = luts()
+    for _ in range(2):
+        d, i = idx.search(Y, 10, mode="derived", r2=60_000)
+        assert np.array_equal(i, i_big) and _same(d, d_big)
+    assert luts() > l0  # the redo ran the tile scan
+    for _ in range(4):
+        d, i = idx.search(Y, 10, mode="derived", r2=100)
+        assert np.array_equal(i, i_small) and _same(d, d_small)
