@@ -98,6 +98,13 @@ int dpq_set_stream(dpq_index_t* index, void* stream);
 int dpq_set_batch(dpq_index_t* index, int batch);
 /* Enable per-phase CUDA-event timing (dpq_last_phase_ms). */
 int dpq_set_timing(dpq_index_t* index, int enabled);
+/* Validate host query buffers inside the flat searches (the finiteness part of
+ * sklearn check_array that flat.py:71 runs first): the scan rides on the
+ * staging copy of each batch.  A NaN or +-inf makes the search return
+ * DPQ_ERR_ARG with a dpq_last_error() that starts with "non-finite query"
+ * before any result is written; the caller then raises the reference's error
+ * (paper_1905_06900_b200/flat.py re-runs check_array for its message). */
+int dpq_set_check_finite(dpq_index_t* index, int enabled);
 
 /* ------------------------------------------------------ flat searches --
  * dpq_flat_search_derived: FlatIndex.search(..., mode="derived", r2)

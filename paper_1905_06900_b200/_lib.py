@@ -35,6 +35,7 @@ SIGNATURES = {
     "dpq_destroy": (None, [c_void_p]),
     "dpq_set_stream": (c_int, [c_void_p, c_void_p]),
     "dpq_set_batch": (c_int, [c_void_p, c_int]),
+    "dpq_set_check_finite": (c_int, [c_void_p, c_int]),
     "dpq_set_timing": (c_int, [c_void_p, c_int]),
     "dpq_flat_search_derived": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_int, c_int, c_void_p,
                                         c_void_p, c_void_p]),
@@ -176,6 +177,9 @@ class Handle:
     def set_timing(self, on: bool) -> None:
         check(lib().dpq_set_timing(self.raw, int(bool(on))))
 
+    def set_check_finite(self, on: bool) -> None:
+        check(lib().dpq_set_check_finite(self.raw, int(bool(on))))
+
     def set_batch(self, batch: int) -> None:
         check(lib().dpq_set_batch(self.raw, int(batch)))
 
@@ -234,15 +238,17 @@ def ivf_create(codebooks, derived, centers, offsets, sorted_codes, sorted_ids, d
     return Handle(out, device)
 
 
-def query_array(Y):
+def query_array(Y, defer_finite: bool = False):
     """Y as the reference's check_array(Y, dtype=float32, order="C") would
     return it (flat.py:71, ivf.py:125), with the common case (a 2-D,
     C-contiguous float32 ndarray) validated by one native finiteness scan
     instead of sklearn's; anything else, and every failure, goes through
-    check_array itself so types and messages are the reference's."""
+    check_array itself so types and messages are the reference's.
+    defer_finite: the caller's C search scans the values while it stages them
+    (dpq_set_check_finite) and calls check_array itself on a failure."""
     if (isinstance(Y, np.ndarray) and type(Y) is np.ndarray and Y.ndim == 2 and Y.dtype == np.float32
             and Y.flags.c_contiguous and Y.shape[0] > 0 and Y.shape[1] > 0
-            and lib().dpq_all_finite(Y.ctypes.data, Y.size) == 0):
+            and (defer_finite or lib().dpq_all_finite(Y.ctypes.data, Y.size) == 0)):
         return Y
     from sklearn.utils.validation import check_array
 

@@ -986,6 +986,25 @@ static void par_memcpy2(void* d0, const void* s0, size_t b0, void* d1, const voi
 }
 static void par_memcpy(void* dst, const void* src, size_t bytes) { par_memcpy2(dst, src, bytes, nullptr, nullptr, 0); }
 
+// The staging copy of a float32 query batch with the finiteness scan of
+// check_array riding on it (each thread scans the slice it just copied, still
+// in its cache): returns true when a NaN or +-inf was seen.
+static bool par_memcpy_check_f32(float* dst, const float* src, size_t n) {
+  constexpr size_t kMin = 64 << 10;  // floats (256 KB)
+  const int nt = n < kMin ? 1 : (int)std::min<size_t>(8, n / (kMin / 2));
+  uint32_t special = 0;
+#pragma omp parallel for num_threads(nt) schedule(static) reduction(| : special)
+  for (int t = 0; t < nt; ++t) {
+    const size_t a = n * t / nt, b = n * (t + 1) / nt;
+    memcpy(dst + a, src + a, (b - a) * 4);
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(dst + a);
+    uint32_t s = 0;
+    for (size_t i = 0; i < b - a; ++i) s |= (uint32_t)((w[i] & 0x7F800000u) == 0x7F800000u);
+    special |= s;
+  }
+  return special != 0;
+}
+
 // Wait for the stream, then copy the staged results to the caller's buffers.
 // The threads touch their slice of the destination pages while the GPU still
 // works (first-touch faults of freshly allocated numpy results cost ~70 us
@@ -1059,9 +1078,22 @@ static int host_driver(Index* h, const float* y, int64_t nq, int r, int batch_li
     DPQ_TRY(ensure_ws(h, nb, r, h->d, -1));
     Workspace& w = h->ws;
     if (h->direct_copy) {
+      if (h->check_finite && dpq_all_finite(y + q0 * h->d, (int64_t)nb * h->d) != 0) {
+        set_error("non-finite query value");
+        return DPQ_ERR_ARG;
+      }
       DPQ_CUDA(cudaMemcpyAsync(w.y, y + q0 * h->d, (size_t)nb * h->d * 4, cudaMemcpyHostToDevice, h->stream));
     } else {
-      par_memcpy(w.h_y, y + q0 * h->d, (size_t)nb * h->d * 4);
+      if (h->check_finite) {
+        if (par_memcpy_check_f32(w.h_y, y + q0 * h->d, (size_t)nb * h->d)) {
+          // (earlier batches' results may already be in the caller's buffers: the caller raises)
+          cudaStreamSynchronize(h->stream);
+          set_error("non-finite query value");
+          return DPQ_ERR_ARG;
+        }
+      } else {
+        par_memcpy(w.h_y, y + q0 * h->d, (size_t)nb * h->d * 4);
+      }
       DPQ_CUDA(cudaMemcpyAsync(w.y, w.h_y, (size_t)nb * h->d * 4, cudaMemcpyHostToDevice, h->stream));
     }
     const bool want_t = phase_us != nullptr;
@@ -1483,6 +1515,9 @@ int dpq_flat_create(int device, int m, int k, int kbar, int dsub, const float* c
               !(getenv("DPQ_EMIT32") && atoi(getenv("DPQ_EMIT32")) == 0);
   if (h->sort_rows && m >= 2 && n > 1 && n < ((int64_t)1 << 31) &&
       (rc = sort_rows(h)) != DPQ_OK) { index_free(h); return rc; }
+  // optimistic start: the first batch already runs without the tile kernels (a query that needs them
+  // gets the batch redone with them and switches the mode off)
+  h->tile_skip = (h->direct && h->key_start && h->tile_skip_ok) ? 1 : 0;
   if ((rc = make_plane(h)) != DPQ_OK) { index_free(h); return rc; }
   if (cudaStreamSynchronize(h->stream) != cudaSuccess) {
     set_error("index build failed"); index_free(h); return DPQ_ERR_CUDA;
@@ -1512,6 +1547,13 @@ int dpq_set_batch(dpq_index_t* index, int batch) {
   Index* h = reinterpret_cast<Index*>(index);
   if (!h || batch < 1) { set_error("bad batch"); return DPQ_ERR_ARG; }
   h->batch = batch;
+  return DPQ_OK;
+}
+
+int dpq_set_check_finite(dpq_index_t* index, int enabled) {
+  Index* h = reinterpret_cast<Index*>(index);
+  if (!h) { set_error("null index"); return DPQ_ERR_ARG; }
+  h->check_finite = enabled != 0;
   return DPQ_OK;
 }
 

@@ -128,6 +128,7 @@ struct Index {
   bool own_stream = false;
   int batch = 1024;
   bool timing = false;
+  bool check_finite = false;  // dpq_set_check_finite: host query batches scanned while they are staged
   cudaEvent_t ev[8] = {};
   cudaStream_t side = nullptr;  // fork/join branch of the batch (independent kernels overlap)
   cudaEvent_t fk[4] = {};       // fork / join events of the two branch points
@@ -163,7 +164,7 @@ struct Index {
   int direct = 1;          // per-query direct scan of the few (g0, g1) runs a query can hit (env DPQ_DIRECT=0 disables)
   // Adaptive: after batches in which every query took the direct scan the tile kernels are not even
   // launched (a query that needs them makes K3 flag the batch, which is redone with them).
-  int tile_skip = 0;       // current mode
+  int tile_skip = 0;       // current mode (starts on for indexes with a direct scan, dpq_flat_create)
   int skip_streak = 0;     // consecutive all-direct speculative batches
   int tile_skip_ok = 1;    // env DPQ_TILE_SKIP=0 disables
   bool dir_batch = false;  // the last first pass ran k_key_select (h_tileq is valid after its sync)

@@ -152,6 +152,7 @@ class FlatIndex(BaseEstimator):
         if dev is None or dev[0] != key:
             h = _lib.flat_create(self.quantizer.codebooks_, self.quantizer.derived_codebooks_, codes,
                                  device=self.device)
+            h.set_check_finite(True)  # host queries are validated while libdpq stages them (search below)
             self._dev = (key, h)
         return self._dev[1]
 
@@ -165,26 +166,39 @@ class FlatIndex(BaseEstimator):
                return_timings: bool = False):
         """Top-r neighbours for each query row (see derivedpq.FlatIndex.search)."""
         check_is_fitted(self, "codes_")
-        Y = _lib.query_array(Y)
+        # check_array's finiteness scan (flat.py:71) rides on libdpq's staging copy of the queries
+        # (dpq_set_check_finite) unless they are rotated first; it still comes before every other
+        # error, as in the reference: _invalid re-runs it before raising
+        # (only once the device handle exists: without a device the check must still come first)
+        defer = getattr(self.quantizer, "rotation_", None) is None and getattr(self, "_dev", None) is not None
+        Y = _lib.query_array(Y, defer_finite=defer)
+
+        def _invalid(msg):
+            if defer:
+                from sklearn.utils.validation import check_array
+
+                check_array(Y, dtype=np.float32, order="C")
+            return ValueError(msg)
+
         if mode not in ("conventional", "derived"):
-            raise ValueError(f"unknown mode {mode!r}")
+            raise _invalid(f"unknown mode {mode!r}")
         nq = Y.shape[0]
         if mode == "derived" and r2 is None:
-            raise ValueError("derived mode requires r2")
+            raise _invalid("derived mode requires r2")
         if nq == 0:
             dists = np.full((0, r), np.inf)
             ids = np.full((0, r), -1, dtype=np.int64)
             return (dists, ids, _timings(0, None)) if return_timings else (dists, ids)
         if mode == "derived":
             if r > r2:  # twopass.py:330-331
-                raise ValueError(f"r={r} must not exceed r2={r2}")
+                raise _invalid(f"r={r} must not exceed r2={r2}")
             if self.codes_.shape[0] == 0 or r2 < 1:  # twopass.py:76-77
-                raise ValueError("need at least one code to estimate qmax")
+                raise _invalid("need at least one code to estimate qmax")
         m, _, dsub = self.quantizer.codebooks_.shape
         if Y.shape[1] != m * dsub:  # search.py:42-43
-            raise ValueError(f"query dimension {Y.shape[1]} != {m}*{dsub}")
+            raise _invalid(f"query dimension {Y.shape[1]} != {m}*{dsub}")
         if r < 1:  # search.py:99-101 (ResultSet)
-            raise ValueError(f"result size must be >= 1, got {r}")
+            raise _invalid(f"result size must be >= 1, got {r}")
         yr = rotated_queries(self.quantizer, Y)
         h = self._handle()
         dists = np.empty((nq, r), dtype=np.float64)
@@ -197,6 +211,10 @@ class FlatIndex(BaseEstimator):
         else:
             rc = L.dpq_flat_search_conventional(h.raw, _lib.ptr(yr), nq, int(r), _lib.ptr(dists),
                                                 _lib.ptr(ids), _lib.ptr(phase))
+        if rc == _lib.DPQ_ERR_ARG and _lib.last_error().startswith("non-finite"):
+            from sklearn.utils.validation import check_array
+
+            check_array(Y, dtype=np.float32, order="C")  # raises the reference's ValueError
         _lib.check(rc, f"FlatIndex.search(mode={mode!r})")
         if return_timings:
             t = _timings(nq, phase)

@@ -461,3 +461,32 @@ def test_tile_skip_mode_and_fallback(monkeypatch):
     for _ in range(4):
         d, i = idx.search(Y, 10, mode="derived", r2=100)
         assert np.array_equal(i, i_small) and _same(d, d_small)
+
+
+def test_deferred_finiteness_check_raises_like_check_array():
+    """Once the device handle exists the finiteness scan of check_array rides
+    on libdpq's staging copy (dpq_set_check_finite): NaN / infinity still
+    raise sklearn's ValueError, before any other argument error, in every
+    batch of a multi-batch call, and valid calls keep working afterwards."""
+    cb, der, codes, Y = _sift_setup(20_000, 40, seed=23)
+    idx = FlatIndex.from_arrays(cb, der, codes)
+    d0, i0 = idx.search(Y, 5, mode="derived", r2=100)  # creates the handle (eager check on this call)
+    bad = Y.copy()
+    bad[7, 3] = np.inf
+    with pytest.raises(ValueError, match="infinity"):
+        idx.search(bad, 5, mode="derived", r2=100)
+    with pytest.raises(ValueError, match="infinity"):
+        idx.search(bad, 5)  # conventional
+    bad[30, 0] = np.nan
+    with pytest.raises(ValueError, match="NaN"):
+        idx.search(bad, 5, mode="derived", r2=100)
+    with pytest.raises(ValueError, match="NaN"):  # the reference checks the array before its other arguments
+        idx.search(bad, 5, mode="blended")
+    with pytest.raises(ValueError, match="unknown mode"):
+        idx.search(Y, 5, mode="blended")
+    idx._handle().set_batch(16)  # the bad row sits in the third batch
+    with pytest.raises(ValueError, match="NaN"):
+        idx.search(bad, 5, mode="derived", r2=100)
+    idx._handle().set_batch(1024)
+    d1, i1 = idx.search(Y, 5, mode="derived", r2=100)
+    assert np.array_equal(i0, i1) and _same(d0, d1)
