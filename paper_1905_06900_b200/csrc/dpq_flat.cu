@@ -749,6 +749,9 @@ static RefineArgs make_refine_args(Index* h, int r) {
   if (h->host_out) {  // pinned host memory is device-addressable (UVA): results cross PCIe as CTAs finish
     ra.out_d = w.h_d;
     ra.out_i = w.h_i;
+  } else if (h->dev_out_d) {
+    ra.out_d = h->dev_out_d;
+    ra.out_i = h->dev_out_i;
   }
   return ra;
 }
@@ -854,7 +857,8 @@ static int flat_derived_batch(Index* h, int nb, int r, int r2) {
   if (!graphable) return flat_derived_batch_body(h, nb, r, r2);
   BatchGraph& G = h->graph;
   const bool same = G.nb == nb && G.r == r && G.r2 == r2 && G.host_out == (int)h->host_out &&
-                    G.tile_skip == h->tile_skip && G.epoch == g_alloc_epoch;
+                    G.tile_skip == h->tile_skip && G.dev_out == (const void*)h->dev_out_d &&
+                    G.epoch == g_alloc_epoch;
   if (G.exec && same) {
     DPQ_CUDA(cudaGraphLaunch(G.exec, h->stream));
     for (int i = 0; i < 8; ++i) h->counters[i] += G.counters[i];
@@ -864,7 +868,7 @@ static int flat_derived_batch(Index* h, int nb, int r, int r2) {
   if (!same || !G.warm) {  // eager run; capture on the next call with this configuration
     if (G.exec) { cudaGraphExecDestroy(G.exec); G.exec = nullptr; }
     const int rc = flat_derived_batch_body(h, nb, r, r2);
-    G.nb = nb; G.r = r; G.r2 = r2; G.host_out = (int)h->host_out; G.tile_skip = h->tile_skip; G.epoch = g_alloc_epoch; G.warm = rc == DPQ_OK;
+    G.nb = nb; G.r = r; G.r2 = r2; G.host_out = (int)h->host_out; G.tile_skip = h->tile_skip; G.dev_out = h->dev_out_d; G.epoch = g_alloc_epoch; G.warm = rc == DPQ_OK;
     return rc;
   }
   int64_t c0[8];
@@ -1592,11 +1596,19 @@ int dpq_flat_search_derived_dev(dpq_index_t* index, const float* yr, int64_t nq,
   if (h->kind != KIND_FLAT) { set_error("not a flat index"); return DPQ_ERR_STATE; }
   int bsz = h->batch;
   int64_t q0 = 0;
+  struct DevOutReset {  // (cleared on every exit)
+    Index* h;
+    ~DevOutReset() { h->dev_out_d = nullptr; h->dev_out_i = nullptr; }
+  } dev_out_reset{h};
   while (q0 < nq) {
     const int nb = (int)std::min<int64_t>(bsz, nq - q0);
     DPQ_TRY(ensure_ws(h, nb, r, h->d, -1));
     Workspace& w = h->ws;
     DPQ_CUDA(cudaMemcpyAsync(w.y, yr + q0 * h->d, (size_t)nb * h->d * 4, cudaMemcpyDeviceToDevice, h->stream));
+    // a call that is one batch: the refine writes into the caller's buffers (the graph is keyed on them)
+    const bool direct_out = q0 == 0 && nb == nq;
+    h->dev_out_d = direct_out ? dists : nullptr;
+    h->dev_out_i = direct_out ? ids : nullptr;
     int rc = flat_derived_batch(h, nb, r, r2);
     if (rc == 100) { bsz = std::max(1, nb / 2); continue; }
     if (rc != DPQ_OK) return rc;
@@ -1610,8 +1622,10 @@ int dpq_flat_search_derived_dev(dpq_index_t* index, const float* yr, int64_t nq,
         if (rc != DPQ_OK) return rc;
       }
     }
-    DPQ_CUDA(cudaMemcpyAsync(dists + q0 * r, w.out_d, (size_t)nb * r * 8, cudaMemcpyDeviceToDevice, h->stream));
-    DPQ_CUDA(cudaMemcpyAsync(ids + q0 * r, w.out_i, (size_t)nb * r * 8, cudaMemcpyDeviceToDevice, h->stream));
+    if (!direct_out) {
+      DPQ_CUDA(cudaMemcpyAsync(dists + q0 * r, w.out_d, (size_t)nb * r * 8, cudaMemcpyDeviceToDevice, h->stream));
+      DPQ_CUDA(cudaMemcpyAsync(ids + q0 * r, w.out_i, (size_t)nb * r * 8, cudaMemcpyDeviceToDevice, h->stream));
+    }
     q0 += nb;
   }
   DPQ_CUDA(cudaStreamSynchronize(h->stream));

@@ -92,6 +92,7 @@ struct Workspace {
 struct BatchGraph {
   cudaGraphExec_t exec = nullptr;
   int nb = -1, r = -1, r2 = -1, host_out = -1, tile_skip = -1;
+  const void* dev_out = nullptr;  // device-API calls: the caller's result buffer the refine writes into
   uint64_t epoch = 0;
   bool warm = false;
   int64_t counters[8] = {};  // host counter increments of one captured batch
@@ -148,6 +149,8 @@ struct Index {
   int64_t exact_limit = 65536;
   int64_t cap0 = 0;
   bool host_out = false;  // host API: the refine writes results straight into the pinned staging buffers
+  double* dev_out_d = nullptr;  // device API, single-batch call: the refine writes straight into the caller's
+  int64_t* dev_out_i = nullptr; //   device buffers (no copy after the batch)
   int wide = 1;       // wide scan tiles (env DPQ_SCAN_WIDE=0 disables)
   int sort_slots = 1; // flat: order query tiles by guard (env DPQ_SORT_SLOTS=0)
   int sort_rows = 1;  // flat: rows sorted by (g0, g1) at build (env DPQ_SORT_ROWS=0)

@@ -490,3 +490,28 @@ def test_deferred_finiteness_check_raises_like_check_array():
     idx._handle().set_batch(1024)
     d1, i1 = idx.search(Y, 5, mode="derived", r2=100)
     assert np.array_equal(i0, i1) and _same(d0, d1)
+
+
+def test_device_buffer_api_single_and_multi_batch():
+    """dpq_flat_search_derived_dev (queries and results in device memory): a
+    call that is one batch has the refine write straight into the caller's
+    buffers (graph keyed on them), a longer call goes through the workspace;
+    both equal the host API, also when the output buffers change between
+    calls."""
+    import torch
+    from paper_1905_06900_b200 import _lib
+
+    cb, der, codes, Y = _sift_setup(60_000, 100, seed=29)
+    idx = FlatIndex.from_arrays(cb, der, codes)
+    d0, i0 = idx.search(Y, 7, mode="derived", r2=120)
+    h, L = idx._handle(), _lib.lib()
+    q = torch.as_tensor(Y, device="cuda")
+    for batch in (1024, 32):  # one batch / four batches
+        h.set_batch(batch)
+        for rep in range(4):  # eager, capture, replay, new output buffers
+            od = torch.full((100, 7), -1.0, dtype=torch.float64, device="cuda")
+            oi = torch.full((100, 7), -7, dtype=torch.int64, device="cuda")
+            _lib.check(L.dpq_flat_search_derived_dev(h.raw, _lib.ptr(q), 100, 7, 120, _lib.ptr(od), _lib.ptr(oi)))
+            torch.cuda.synchronize()
+            assert np.array_equal(oi.cpu().numpy(), i0) and _same(od.cpu().numpy(), d0), (batch, rep)
+    h.set_batch(1024)
