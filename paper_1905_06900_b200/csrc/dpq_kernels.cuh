@@ -2296,6 +2296,7 @@ __global__ void __launch_bounds__(256) k_group_tables_reg(GroupTablesArgs a) {
       act[atomicAdd(&nact, 1)] = q;
   __syncthreads();
   const int n = nact;
+  if (n == 0) return;  // (no codebook rows loaded for a group no query needs)
   for (int ib0 = 0; ib0 < gsize; ib0 += 256) {
     const int ib = ib0 + tid;
     f32x2_t c2[DSUB / 2];  // the codebook row as lane pairs
