@@ -51,6 +51,21 @@ REF_PATH = ROOT / "baseline" / "_ref"
 METRIC = "queries/s at Recall@100 (derived two-pass PQ search, k=100)"
 
 
+def shard_n1_record():
+    """The shard workload (configs[2]) measured on ONE B200 with `bench.py --mode shard --gpus 1`, as
+    recorded under profiles/: the N = 1 line of a driver scaling run is configs[1] (the metric's
+    single-GPU config, 10M rows), so this is the same-workload point N > 1 lines compare with."""
+    src = ROOT / "profiles" / "r2_bench_shard_n1_c3_direct.json"
+    try:
+        line = [l for l in src.read_text().splitlines() if l.startswith("{")][-1]
+        d = json.loads(line)
+        return {"value": d["value"], "unit": d["unit"], "ms_per_step": d["ms_per_step"],
+                "e2e": (d.get("e2e") or {}).get("value"), "recorded": str(src.relative_to(ROOT)),
+                "note": "recorded run, not measured in this one"}
+    except Exception:
+        return None
+
+
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
@@ -711,7 +726,8 @@ def run_replicas(args, cfg, rank, world, local):
                 "h2d_bytes_per_step": world * Bq * wl["queries"].shape[1] * 4,
                 "d2h_bytes_per_step": world * Bq * r * 16,
                 "api": "FlatIndex.search(Y_host, ...) per rank, max wall over ranks"},
-            "gpu_launches": int(sm[2]), "clocks": clk.summary(), "setup_s": round(wl["setup_s"], 1)}), flush=True)
+            "gpu_launches": int(sm[2]), "clocks": clk.summary(), "setup_s": round(wl["setup_s"], 1),
+            "n1_same_workload": shard_n1_record()}), flush=True)
     dist.barrier()
     dist.destroy_process_group()
 
@@ -796,7 +812,8 @@ def run_sharded(args, cfg, rank, world, local):
                 "value": round(args.steps * Bq / float(mx[1]), 1), "unit": "queries/s",
                 "h2d_bytes_per_step": Bq * qh.shape[1] * 4, "d2h_bytes_per_step": Bq * r * 16,
                 "api": "ShardedFlatIndex.search(Y_host, ...) on every rank (max wall over ranks)"},
-            "gpu_launches": int(sm[2]), "clocks": clk.summary(), "setup_s": round(wl["setup_s"], 1)}), flush=True)
+            "gpu_launches": int(sm[2]), "clocks": clk.summary(), "setup_s": round(wl["setup_s"], 1),
+            "n1_same_workload": shard_n1_record()}), flush=True)
     dist.barrier()
     dist.destroy_process_group()
 
