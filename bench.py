@@ -55,7 +55,7 @@ def shard_n1_record():
     """The shard workload (configs[2]) measured on ONE B200 with `bench.py --mode shard --gpus 1`, as
     recorded under profiles/: the N = 1 line of a driver scaling run is configs[1] (the metric's
     single-GPU config, 10M rows), so this is the same-workload point N > 1 lines compare with."""
-    src = ROOT / "profiles" / "r2_bench_shard_n1_c3_direct.json"
+    src = ROOT / "profiles" / "r2_bench_shard_n1_c3_final.json"
     try:
         line = [l for l in src.read_text().splitlines() if l.startswith("{")][-1]
         d = json.loads(line)

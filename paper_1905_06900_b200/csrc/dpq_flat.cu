@@ -482,6 +482,7 @@ int build_lut(Index* h, int nslot, const uint16_t* gword, const int* slot_query,
 struct ScanPlan {
   bool sorted = false, list = false, direct = false;
   bool skip_tiles = false;      // (single-GPU speculative first pass only) tile kernels not launched
+  bool scan_hist = false;       // (with skip_tiles) the direct scan counts its hits by score into ws.hist for K3
   const uint32_t* hist = nullptr;  // when set, k_key_select computes the guard itself (k_guard's rule)
   int r2 = 0, exact = 0;
   double lambda = 0.0;
@@ -528,6 +529,8 @@ int plan_flat_scan(Index* h, int nb, ScanPlan& sp) {
   return DPQ_OK;
 }
 
+static bool scan_hist_on(const Index* h) { return h->scan_hist >= 0 ? h->scan_hist != 0 : !h->emit32; }
+
 int prepare_flat_scan(Index* h, int nb, const ScanPlan& sp) {
   Workspace& w = h->ws;
   const int qt = qt_of(h);
@@ -542,6 +545,7 @@ int prepare_flat_scan(Index* h, int nb, const ScanPlan& sp) {
     ka.n_rows = h->d_nrows;
     ka.hist = sp.hist; ka.r2 = sp.r2; ka.exact = sp.exact; ka.lambda = sp.lambda;
     ka.skip_tiles = sp.skip_tiles ? 1 : 0;
+    ka.zero_hist = (sp.scan_hist && sp.hist) ? 1 : 0;
     if (h->gt_slack && h->m <= 8) ka.slack = w.slack;
     k_key_select<<<nb, 256, 0, h->stream>>>(ka, nb);
     DPQ_LAUNCHED(h);
@@ -591,9 +595,10 @@ int launch_direct(Index* h, const ScanPlan& sp) {
   da.plane = h->plane; da.q8 = w.q8; da.m = h->m; da.kbar = h->kbar; da.guard_b = w.guard_b;
   da.items = w.dir_items; da.state = w.dir_state; da.item_cap = sp.item_cap;
   da.emit_cnt = w.emit_cnt; da.emit = w.emit; da.cap = w.cap;
+  da.hist = sp.scan_hist ? w.hist : nullptr;
   // one wave of resident CTAs, items strided over their warps
   auto go = [&](auto kern, int slot) -> int {
-    static int per_sm[4] = {0, 0, 0, 0};
+    static int per_sm[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (!per_sm[slot]) {
       int nb = 0;
       if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 256, 0) != cudaSuccess || nb < 1) nb = 4;
@@ -602,7 +607,15 @@ int launch_direct(Index* h, const ScanPlan& sp) {
     kern<<<per_sm[slot] * num_sms(h), 256, 0, h->stream>>>(da);
     return DPQ_OK;
   };
-  if (h->mpad == 8) {
+  if (da.hist) {
+    if (h->mpad == 8) {
+      if (h->emit32) go(k_scan_direct<8, true, true>, 4);
+      else go(k_scan_direct<8, false, true>, 5);
+    } else {
+      if (h->emit32) go(k_scan_direct<4, true, true>, 6);
+      else go(k_scan_direct<4, false, true>, 7);
+    }
+  } else if (h->mpad == 8) {
     if (h->emit32) go(k_scan_direct<8, true>, 0);
     else go(k_scan_direct<8, false>, 1);
   } else {
@@ -645,6 +658,7 @@ static int flat_first_pass(Index* h, int nb, int r2) {
   if (sp.direct) {  // k_key_select computes the guard itself
     sp.hist = w.hist; sp.r2 = r2; sp.exact = exact ? 1 : 0; sp.lambda = lambda;
     sp.skip_tiles = h->tile_skip && h->tile_skip_ok && !h->no_spec && nb > 1;
+    sp.scan_hist = sp.skip_tiles && scan_hist_on(h);  // every emitted record then comes from k_scan_direct
   } else {
     k_guard<<<(nb + kGuardSlotsPerCta - 1) / kGuardSlotsPerCta, 32 * kGuardSlotsPerCta, 0, h->stream>>>(w.hist, nb, r2, lambda, exact ? 1 : 0, nullptr,
                                                       w.guard_b, w.gword, nullptr);
@@ -679,7 +693,8 @@ static int flat_first_pass(Index* h, int nb, int r2) {
       h->order_forked = true;
     }
     k_threshold<256><<<nb, 256, 0, h->stream>>>(w.emit, w.emit_cnt, w.cap, w.guard_b, r2, nullptr,
-                                                w.bstar, w.ncand, w.flags, nullptr, h->d_nemit, (int)h->emit32);
+                                                w.bstar, w.ncand, w.flags, nullptr, h->d_nemit, (int)h->emit32,
+                                                (sp.scan_hist && attempt == 0) ? w.hist : nullptr);
     DPQ_LAUNCHED(h);
     if (first) ev_rec(h, 4);
     first = false;
@@ -1348,6 +1363,7 @@ int index_common_init(Index* h, int device, int m, int k, int kbar, int dsub, co
   if (const char* e = getenv("DPQ_DIRECT")) h->direct = atoi(e) != 0;
   if (const char* e = getenv("DPQ_GT_SLACK")) h->gt_slack = atoi(e) != 0;
   if (const char* e = getenv("DPQ_TILE_SKIP")) h->tile_skip_ok = atoi(e) != 0;
+  if (const char* e = getenv("DPQ_SCAN_HIST")) h->scan_hist = atoi(e) != 0;
   if (const char* e = getenv("DPQ_DIRECT_ITEMS")) h->direct_items = std::max(0, atoi(e));
   if (const char* e = getenv("DPQ_DIRECT_COPY")) h->direct_copy = atoi(e) != 0;
   if (const char* e = getenv("DPQ_SPECULATE")) h->no_spec = atoi(e) == 0;

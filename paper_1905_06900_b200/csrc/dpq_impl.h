@@ -133,6 +133,11 @@ struct Index {
   cudaEvent_t ev[8] = {};
   cudaStream_t side = nullptr;  // fork/join branch of the batch (independent kernels overlap)
   cudaEvent_t fk[4] = {};       // fork / join events of the two branch points
+  // The direct scan counts its hits by score for K3, which then skips its pass over those queries'
+  // emit lists.  -1 = auto: on for 8-byte emit records (shards of 2^24 rows or more, where the lists
+  // outgrow L2: configs[2] K3 0.31 -> 0.01 ms, scan 0.75 -> 0.90), off for 4-byte records (configs[1]:
+  // K3 24 -> 10 us, scan 80 -> 100 us).  env DPQ_SCAN_HIST=0/1 forces it.
+  int scan_hist = -1;
   bool order_forked = false;    // k_order_by_count already enqueued on `side` (speculative first pass)
   float phase_ms[PH_N] = {};
   int64_t counters[8] = {};  // launches, queries, rows scanned, refined, fallbacks, emitted, table entries, wide units

@@ -1745,8 +1745,10 @@ int dpq_shard_scan(dpq_index_t* index, const int32_t* sample_hist_sum, int64_t n
   ScanPlan sp;
   DPQ_TRY(plan_flat_scan(h, nb, sp));
   DPQ_TRY(prepare_flat_scan(h, nb, sp));
+  sp.scan_hist = sp.direct && scan_hist_on(h);  // (ws.hist is free once k_guard has read it)
   for (int attempt = 0; attempt < 4; ++attempt) {
     DPQ_CUDA(cudaMemsetAsync(w.emit_cnt, 0, (size_t)nb * 4, h->stream));
+    if (sp.scan_hist) DPQ_CUDA(cudaMemsetAsync(w.hist, 0, (size_t)nb * 256 * 4, h->stream));
     if (h->n > 0) {
       EmitArgs ea;
       ea.plane = h->plane; ea.row_begin = 0; ea.row_end = h->n; ea.rows_per_cta = 0;
@@ -1759,7 +1761,8 @@ int dpq_shard_scan(dpq_index_t* index, const int32_t* sample_hist_sum, int64_t n
       if (!sp.list) h->counters[2] += (int64_t)nb * h->n;
     }
     k_threshold<256><<<nb, 256, 0, h->stream>>>(w.emit, w.emit_cnt, w.cap, w.guard_b, r2, nullptr, w.bstar,
-                                                w.ncand, w.flags, w.hist_i, h->d_nemit, (int)h->emit32);
+                                                w.ncand, w.flags, w.hist_i, h->d_nemit, (int)h->emit32,
+                                                sp.scan_hist ? w.hist : nullptr, w.gword);
     DPQ_LAUNCHED(h);
     DPQ_CUDA(cudaMemcpyAsync(w.h_flags, w.flags, nb, cudaMemcpyDeviceToHost, h->stream));
     DPQ_CUDA(cudaMemcpyAsync(w.h_cnt, w.emit_cnt, (size_t)nb * 4, cudaMemcpyDeviceToHost, h->stream));
@@ -1869,7 +1872,9 @@ int dpq_shard_scan_dev(dpq_index_t* index, const int32_t* sample_hist_sum, int64
   ScanPlan sp;
   DPQ_TRY(plan_flat_scan(h, nb, sp));
   DPQ_TRY(prepare_flat_scan(h, nb, sp));
+  sp.scan_hist = sp.direct && scan_hist_on(h);  // (ws.hist is free once k_guard has read it)
   DPQ_CUDA(cudaMemsetAsync(w.emit_cnt, 0, (size_t)nb * 4, h->stream));
+  if (sp.scan_hist) DPQ_CUDA(cudaMemsetAsync(w.hist, 0, (size_t)nb * 256 * 4, h->stream));
   if (h->n > 0) {
     EmitArgs ea;
     ea.plane = h->plane; ea.row_begin = 0; ea.row_end = h->n; ea.rows_per_cta = 0;
@@ -1882,7 +1887,8 @@ int dpq_shard_scan_dev(dpq_index_t* index, const int32_t* sample_hist_sum, int64
     if (!sp.list) h->counters[2] += (int64_t)nb * h->n;
   }
   k_threshold<256><<<nb, 256, 0, h->stream>>>(w.emit, w.emit_cnt, w.cap, w.guard_b, r2, nullptr, w.bstar, w.ncand,
-                                              w.flags, cand_hist, h->d_nemit, (int)h->emit32);
+                                              w.flags, cand_hist, h->d_nemit, (int)h->emit32,
+                                              sp.scan_hist ? w.hist : nullptr, w.gword);
   DPQ_LAUNCHED(h);
   return DPQ_OK;
 }

@@ -864,6 +864,8 @@ struct KeySelArgs {
   int r2 = 0, exact = 0;
   double lambda = 0.0;
   int32_t* slack = nullptr;    // optional [nq][m]: k_entry_slack's output, computed here
+  int zero_hist = 0;           // (with hist) clear the query's histogram row once the guard is read: the direct
+                               // scan then counts its hits by score into it (DirectArgs::hist)
   int skip_tiles = 0;          // the tile kernels are not launched: a query that needs them gets guard 0, which
                                // K3 flags as too tight (the batch is then redone with the tile path)
   uint16_t* gword;             // [nq] guard words: rewritten (direct: 0x7F7F, tile path: 0x8000 + B)
@@ -917,6 +919,7 @@ __global__ void __launch_bounds__(256) k_key_select(KeySelArgs a, int nq) {
       if (t == 0) s_guard = Bh;
     }
     __syncthreads();
+    if (a.zero_hist) const_cast<uint32_t*>(a.hist)[(int64_t)q * 256 + t] = 0u;
   }
   const int Bg = a.hist ? s_guard : (int)a.guard_b[q];
   const uint8_t* e = a.q8 + (int64_t)q * a.m * a.kbar;
@@ -1045,10 +1048,13 @@ struct DirectArgs {
   uint32_t* emit_cnt;
   uint64_t* emit;
   uint32_t cap;
+  // optional [nq][256], zeroed: hits counted by score (one atomic per distinct score of 32 rows), so K3
+  // takes b* from it without reading the emit lists back
+  uint32_t* hist = nullptr;
 };
 
-template <int MPAD, bool E32>
-__global__ void __launch_bounds__(256) k_scan_direct(DirectArgs a) {
+template <int MPAD, bool E32, bool HIST = false>  // HIST: count the hits into a.hist (its own build: 48 vs 40 registers)
+__global__ void __launch_bounds__(256, HIST ? 6 : 0) k_scan_direct(DirectArgs a) {  // (HIST: 41 -> 40 registers, 6 CTAs / SM like the plain build)
   constexpr int TB = (MPAD - 2) * 256;  // table bytes per warp: subspaces 2 .. MPAD-1
   __shared__ __align__(16) uint8_t s_tab[8 * TB];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1137,6 +1143,16 @@ __global__ void __launch_bounds__(256) k_scan_direct(DirectArgs a) {
       }
       const int tot = __popc(bal[0]) + __popc(bal[1]) + __popc(bal[2]) + __popc(bal[3]);
       if (tot == 0) continue;
+      if constexpr (HIST) {
+        uint32_t* hq = a.hist + (int64_t)q * 256 + e01;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if ((bal[u] >> lane) & 1u) {
+            const unsigned same = __match_any_sync(bal[u], ts[u]);
+            if (lane == __ffs(same) - 1) atomicAdd(hq + ts[u], (uint32_t)__popc(same));
+          }
+        }
+      }
       uint32_t pos = 0;
       if (lane == 0) pos = atomicAdd(cnt, (uint32_t)tot);
       pos = __shfl_sync(0xffffffffu, pos, 0);
@@ -2061,7 +2077,9 @@ __global__ void __launch_bounds__(NT)
                 uint32_t cap, const uint16_t* __restrict__ guard_b, int r2,
                 const uint8_t* __restrict__ only, int32_t* __restrict__ bstar,
                 int64_t* __restrict__ ncand, uint8_t* __restrict__ flags,
-                int32_t* __restrict__ hist_out, unsigned long long* __restrict__ n_emitted, int emit32) {
+                int32_t* __restrict__ hist_out, unsigned long long* __restrict__ n_emitted, int emit32,
+                const uint32_t* __restrict__ scan_hist = nullptr,
+                const uint16_t* __restrict__ direct_gword = nullptr) {
   // per-warp sub-histograms (scores cluster in a few bins: 8x less shared
   // atomic contention), emit lists read with 16-byte loads, two in flight
   constexpr int NW = NT / 32;
@@ -2076,8 +2094,13 @@ __global__ void __launch_bounds__(NT)
       for (int i = tid; i < 256; i += NT) hist_out[(int64_t)q * 256 + i] = 0;
     return;
   }
-  for (int i = tid; i < NW * 256; i += NT) (&hw[0][0])[i] = 0;
   if (n_emitted && tid == 0) atomicAdd(n_emitted, (unsigned long long)n);
+  // the direct scan counted its hits by score (DirectArgs::hist): no pass over the emit list of a
+  // query it scanned (all of them, or with direct_gword those k_key_select marked 0x7F7F)
+  if (scan_hist && (!direct_gword || direct_gword[q] == (uint16_t)0x7F7Fu)) {
+    for (int b = tid; b < 256; b += NT) h[b] = scan_hist[(int64_t)q * 256 + b];
+  } else {
+  for (int i = tid; i < NW * 256; i += NT) (&hw[0][0])[i] = 0;
   __syncthreads();
   uint32_t* hm = hw[tid >> 5];
   if (emit32) {
@@ -2112,6 +2135,7 @@ __global__ void __launch_bounds__(NT)
     for (int w = 0; w < NW; ++w) v += hw[w][b];
     h[b] = v;
   }
+  }  // !scan_hist
   __syncthreads();
   if (hist_out) {
     for (int i = tid; i < 256; i += NT) hist_out[(int64_t)q * 256 + i] = (int32_t)h[i];

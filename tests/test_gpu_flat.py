@@ -463,6 +463,40 @@ def test_tile_skip_mode_and_fallback(monkeypatch):
         assert np.array_equal(i, i_small) and _same(d, d_small)
 
 
+@pytest.mark.parametrize("r2", [100, 2000])
+def test_scan_side_histogram_equals_emit_list_histogram(monkeypatch, r2):
+    """DPQ_SCAN_HIST=1: the direct scan counts its hits by score and K3 takes b*
+    from those counts instead of reading the emit lists back (the default for
+    shards of 2^24 rows or more).  Same ids, distances and refined-candidate
+    counts as with DPQ_SCAN_HIST=0, batch after batch (eager, captured graph,
+    tile-skip mode), and as the oracle."""
+    import torch
+    from paper_1905_06900_b200 import train
+
+    st = datagen.seed_streams(43)
+    centres = datagen.sift_centres(st["centres"])
+    X = datagen.sift_like(st["database"], centres, 150_000)
+    Y = datagen.sift_like(st["queries"], centres, 64)
+    xt = torch.as_tensor(X, device="cuda")
+    cb, der = train.train_pq(xt, 4, 12, 4, iters=6, seed=43)
+    codes = train.encode(xt, cb).cpu().numpy().astype(np.uint16)
+    monkeypatch.setenv("DPQ_SCAN_HIST", "0")
+    off = FlatIndex.from_arrays(cb, der, codes)
+    monkeypatch.setenv("DPQ_SCAN_HIST", "1")
+    on = FlatIndex.from_arrays(cb, der, codes)
+    d0, i0 = O.flat_search(cb, der, codes, Y[:8], 10, "derived", r2)
+    for _ in range(5):
+        refined = []
+        res = []
+        for idx in (off, on):
+            c0 = idx._handle().counters_ex()["refined"]
+            res.append(idx.search(Y, 10, mode="derived", r2=r2))
+            refined.append(idx._handle().counters_ex()["refined"] - c0)
+        assert np.array_equal(res[0][1], res[1][1]) and _same(res[0][0], res[1][0])
+        assert refined[0] == refined[1], refined
+        assert np.array_equal(res[1][1][:8], i0) and _same(res[1][0][:8], d0)
+
+
 def test_deferred_finiteness_check_raises_like_check_array():
     """Once the device handle exists the finiteness scan of check_array rides
     on libdpq's staging copy (dpq_set_check_finite): NaN / infinity still

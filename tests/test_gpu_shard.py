@@ -42,7 +42,9 @@ def _run_shards(cb, der, codes, Y, r, r2, world):
     return out
 
 
-@pytest.mark.parametrize("world,env", [(3, {}), (2, {"DPQ_EXACT_LIMIT": "0", "DPQ_GUARD_SAMPLE": "16"})])
+@pytest.mark.parametrize("world,env", [(3, {}), (2, {"DPQ_EXACT_LIMIT": "0", "DPQ_GUARD_SAMPLE": "16"}),
+                                       (2, {"DPQ_SCAN_HIST": "1"}),
+                                       (2, {"DPQ_SCAN_HIST": "1", "DPQ_EXACT_LIMIT": "0", "DPQ_EMIT_CAP": "64"})])
 def test_sharded_gpu_equals_unsharded(world, env, monkeypatch):
     for k, v in env.items():
         monkeypatch.setenv(k, v)
@@ -110,7 +112,10 @@ def _model(seed, m=4, k=1024, kbar=256, dsub=8, n=40000, nq=20):
 
 
 @pytest.mark.parametrize("world,env", [(3, {}), (2, {"DPQ_EXACT_LIMIT": "0", "DPQ_GUARD_SAMPLE": "16"}),
-                                       (2, {"DPQ_EXACT_LIMIT": "0", "DPQ_EMIT_CAP": "64"})])
+                                       (2, {"DPQ_EXACT_LIMIT": "0", "DPQ_EMIT_CAP": "64"}),
+                                       (3, {"DPQ_SCAN_HIST": "1"}),
+                                       (2, {"DPQ_SCAN_HIST": "1", "DPQ_EXACT_LIMIT": "0", "DPQ_EMIT_CAP": "64"}),
+                                       (2, {"DPQ_SCAN_HIST": "1", "DPQ_EXACT_LIMIT": "0", "DPQ_GUARD_SAMPLE": "16"})])
 def test_sharded_device_protocol_equals_unsharded(world, env, monkeypatch):
     """dpq_shard_*_dev + in-place exchange + dpq_merge_topr_dev, including the
     flagged-redo path (tight guards from a 16-row sample; emit overflow)."""
